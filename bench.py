@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native Cool-chic RD forward (BASELINE.json metric:
+"decoded pixels/sec (RD forward incl. ARM rate) and fraction of B200 roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one full RD forward (ARM rate over every latent, upsampling,
+synthesis, MSE, RD cost) of the BASELINE.json configs[3] batch -- 64 images of
+1365x2048 at the ~2000 MAC/pixel architecture -- per GPU (weak scaling: each
+rank owns 64 independent images; the per-image results are all-reduced).  Rank
+0 prints one JSON line.  ``--impl reference`` times the fp64 CPU oracle on the
+host cores (the tier's reference arm; rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import faulthandler
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workload  # noqa: E402
+
+METRIC = "decoded pixels/sec (RD forward incl. ARM rate) and fraction of B200 roofline"
+UNIT = "pixels/s"
+# FP32 FMA roofline: 148 SMs x 128 FP32 lanes x 2 FLOP x
+# 1.965 GHz (B200_PROFILING.md SM count, clocks.max.sm).  The FFMA2 probe
+# (tools/microbench/ffma_probe.cu) measured 126.9 FMA/clk/SM = 99.2 % of it.
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+REASONS = [(0x1, "gpu_idle"), (0x2, "applications_clocks_setting"), (0x4, "sw_power_cap"),
+           (0x8, "hw_slowdown"), (0x10, "sync_boost"), (0x20, "sw_thermal_slowdown"),
+           (0x40, "hw_thermal_slowdown"), (0x80, "hw_power_brake_slowdown")]
+
+
+class ClockSampler(threading.Thread):
+    """Samples the SM clock and clock-event reasons through NVML while the
+    timed region runs (B200_PROFILING.md clocks rule)."""
+
+    def __init__(self, cuda_index: int, period: float = 0.01):
+        super().__init__(daemon=True)
+        self.period = period
+        self.samples = []
+        self.max_mhz = None
+        self._halt = threading.Event()
+        self.ok = False
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            h = None
+            try:  # match the CUDA device to its NVML handle by UUID
+                import torch
+                want = str(torch.cuda.get_device_properties(cuda_index).uuid)
+                for i in range(N.nvmlDeviceGetCount()):
+                    hi = N.nvmlDeviceGetHandleByIndex(i)
+                    u = N.nvmlDeviceGetUUID(hi)
+                    u = u.decode() if isinstance(u, bytes) else u
+                    if u.replace("GPU-", "") == want.replace("GPU-", ""):
+                        h = hi
+                        break
+            except Exception:
+                h = None
+            if h is None:
+                vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+                idx = int(vis.split(",")[cuda_index]) if vis and vis.split(",")[0].isdigit() else cuda_index
+                h = N.nvmlDeviceGetHandleByIndex(idx)
+            self.h = h
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - reported in the JSON
+            self.err = repr(e)
+
+    def run(self):
+        if not self.ok:
+            return
+        N = self.N
+        while not self._halt.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+                try:
+                    rs = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:
+                    rs = N.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.samples.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def stop(self):
+        self._halt.set()
+        self.join(timeout=2)
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "nvml")}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        mask = 0
+        for _, r in self.samples:
+            mask |= r
+        return {"sm_mhz": float(statistics.median(s for s, _ in self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": [n for b, n in REASONS if mask & b and n != "gpu_idle"], "samples": len(self.samples)}
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def load_traffic(kernel: str):
+    """Per-launch DRAM bytes of `kernel` from the committed ncu --set full
+    summary (profiles/), or None."""
+    for name in sorted(os.listdir(os.path.join(ROOT, "profiles")), reverse=True) if os.path.isdir(
+            os.path.join(ROOT, "profiles")) else []:
+        if name.startswith("ncu_full_") and name.endswith(".json"):
+            try:
+                with open(os.path.join(ROOT, "profiles", name)) as f:
+                    d = json.load(f)
+                k = d.get("kernels", {}).get(kernel)
+                if k and k.get("dram_bytes_per_launch"):
+                    return float(k["dram_bytes_per_launch"])
+            except Exception:
+                pass
+    return None
+
+
+# --------------------------------------------------------------------------- ours
+def run_ours(args, rk):
+    import torch
+
+    import paper_2403_11651_b200 as P
+    from paper_2403_11651_b200 import dist
+
+    cfg = workload.CONFIGS[args.config]
+    n_img = args.images or cfg.n_img
+    dev = torch.device("cuda", rk.local_rank)
+    torch.cuda.set_device(dev)
+    P.load()
+    seeds = [workload.image_seed(args.seed, g) for g in dist.owned_images(rk.rank, n_img)]
+    t0 = time.perf_counter()
+    images = workload.make_batch(cfg, seeds, threads=min(16, host_cores()))
+    gen_s = time.perf_counter() - t0
+    log(f"generated {len(images)} images in {gen_s:.1f}s")
+    batch = P.DeviceBatch(cfg, images, device=dev, with_xhat=True)
+    desc = batch.desc
+    macs = P.cc_mac_per_pixel(desc)
+    log("device batch ready")
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+
+    def step():
+        res = batch.forward(sptr)
+        if rk.world > 1:
+            dist.allreduce_results(dist.scatter_results(res, rk.rank, rk.world, n_img))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    log("warm-up done")
+    sampler = ClockSampler(rk.local_rank)
+    log(f"sampler ok={sampler.ok}")
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    P.ccrd.cc_profile_begin()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    launches = 0
+    for _ in range(args.steps):
+        step()
+        launches += P.ccrd.cc_last_launch_count()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    sampler.stop()
+    prof = P.ccrd.cc_profile_end()
+    log("timed region done")
+    ms = ev0.elapsed_time(ev1)
+    ms_max = dist.max_over_ranks(ms, device=dev)
+    P_img = cfg.H * cfg.W
+    px_total = rk.world * n_img * P_img * args.steps
+    value = px_total / (ms_max / 1e3)
+
+    # roofline of the dominant kernel (arm_rate: ~69 % of the MACs)
+    arm_avg_s = prof.arm_ms / max(1, prof.arm_launches) / 1e3
+    syn_avg_s = prof.syn_ms / max(1, prof.syn_launches) / 1e3
+    arm_tflops = 2.0 * macs.arm_macs / arm_avg_s / 1e12
+    syn_tflops = 2.0 * (macs.up_macs + macs.syn_macs) / syn_avg_s / 1e12
+    path_tflops = 2.0 * macs.total * value / rk.world / 1e12
+    traffic = load_traffic("arm_rate_kernel")
+
+    # end to end: host (pinned) buffers through cc_rd_forward_host
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, cfg, images, desc, dev, stream, rk, n_img)
+
+    # sanity: results finite, rate positive
+    res = batch.results.cpu().numpy()
+    assert np.isfinite(res).all() and (res[:, 0] > 0).all(), "non-finite or empty results"
+
+    log("e2e done")
+    clocks = sampler.summary()
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": rk.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {
+            "workload": f"{args.config}: {n_img} x {cfg.H}x{cfg.W} RGB images per GPU, L={cfg.L}, "
+                        f"ARM {list(cfg.arm_widths)} C={cfg.n_ctx}, synthesis {list(cfg.syn_widths)}+{cfg.syn_n_res}x"
+                        f"res3x3, {cfg.up_taps}-tap separable upsampling (BASELINE.json configs[3])",
+            "images_per_gpu": n_img, "H": cfg.H, "W": cfg.W, "mac_per_pixel": round(macs.total, 3),
+            "l2": f"inputs larger than L2: {(sum(im.latents.nbytes + im.image.nbytes for im in images)) / 1e9:.2f} GB "
+                  "read per step per GPU (126 MB L2)",
+            "parallelism": f"image-sharded x{rk.world}",
+        },
+        "roofline": {
+            "bound": "alu", "kernel": "arm_rate_kernel", "achieved": arm_tflops, "peak": FP32_PEAK_TFLOPS,
+            "unit": "TFLOP/s", "frac": arm_tflops / FP32_PEAK_TFLOPS, "traffic": traffic,
+            "algorithmic": f"{macs.arm_macs} FP32 FMA (2 FLOP) per launch = 1 image's latents x "
+                           f"{sum(cfg.arm_widths[k] * cfg.arm_widths[k + 1] for k in range(len(cfg.arm_widths) - 1))} MAC",
+            "avg_launch_ms": arm_avg_s * 1e3,
+            "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (B200_PROFILING.md); "
+                           "FFMA2 probe measured 99.2 % of it",
+        },
+        "kernels": {
+            "arm_rate_kernel": {"avg_ms": arm_avg_s * 1e3, "launches": prof.arm_launches, "tflops": arm_tflops,
+                                "frac": arm_tflops / FP32_PEAK_TFLOPS, "share": prof.arm_ms / ms},
+            "synth_kernel": {"avg_ms": syn_avg_s * 1e3, "launches": prof.syn_launches, "tflops": syn_tflops,
+                             "frac": syn_tflops / FP32_PEAK_TFLOPS, "share": prof.syn_ms / ms},
+            "reduce_batch_kernel": {"ms_total": prof.reduce_ms, "launches": prof.reduce_launches},
+        },
+        "path_roofline": {"achieved_tflops_per_gpu": path_tflops, "frac": path_tflops / FP32_PEAK_TFLOPS,
+                          "note": "whole step: pixels/s x closed-form MAC/px x 2 / FP32 peak"},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "input_gen_s": round(gen_s, 2),
+    }
+    if rk.rank == 0 and rk.world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = run_cpu_baseline(cfg, images)
+    if rk.rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def run_e2e(args, cfg, images, desc, dev, stream, rk, n_img):
+    import torch
+
+    import paper_2403_11651_b200 as P
+    from paper_2403_11651_b200 import dist
+    lat = [torch.from_numpy(im.latents).pin_memory() for im in images]
+    img = [torch.from_numpy(im.image).pin_memory() for im in images]
+    xh = [torch.empty_like(t).pin_memory() for t in img]
+    io = [P.CcImageIO(lat[i].data_ptr(), images[i].arm_w.ctypes.data, images[i].up_w.ctypes.data,
+                      images[i].syn_w.ctypes.data, img[i].data_ptr(), xh[i].data_ptr()) for i in range(n_img)]
+    ws_b = P.cc_workspace_bytes_host(desc, n_img)
+    ws = torch.empty(ws_b, dtype=torch.uint8, device=dev)
+    res = np.zeros((n_img, 4))
+    steps = max(2, min(args.steps, args.e2e_steps))
+    P.cc_rd_forward_host(desc, io, res, ws.data_ptr(), ws_b, stream.cuda_stream)   # warm-up
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        P.cc_rd_forward_host(desc, io, res, ws.data_ptr(), ws_b, stream.cuda_stream)
+    torch.cuda.synchronize(dev)
+    wall = time.perf_counter() - t0
+    wall = dist.max_over_ranks(wall, device=dev)
+    h2d = sum(im.latents.nbytes + im.image.nbytes for im in images)
+    d2h = sum(im.image.nbytes for im in images) + 32 * n_img
+    return {"value": rk.world * n_img * cfg.H * cfg.W * steps / wall, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": steps,
+            "api": "cc_rd_forward_host (pinned host latents+image in, x_hat+results out, synchronous)"}
+
+
+def run_cpu_baseline(cfg, images):
+    import oracle
+    cores = host_cores()
+    oracle.set_threads(cores)
+    done, wall = 0, 0.0
+    for im in images:
+        t, _ = oracle.time_rd_forward(cfg, im, cores)
+        wall += t
+        done += 1
+        if wall * cores >= 10.0 or done >= 4:
+            break
+    return {"value": done * cfg.H * cfg.W / wall, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{done} full {cfg.H}x{cfg.W} image(s) of the same workload, fp64 C oracle "
+                      f"(OpenMP over rows, {cores} threads), {wall:.2f} s wall"}
+
+
+# ---------------------------------------------------------------------- reference
+def run_reference(args, rk):
+    """The tier's reference arm: the fp64 CPU oracle, as it stands, on the host
+    cores; each step = one image of the same workload (bounded sample)."""
+    if rk.rank != 0:
+        return
+    import oracle
+    cfg = workload.CONFIGS[args.config]
+    cores = host_cores()
+    oracle.set_threads(cores)
+    n = args.steps + args.warmup
+    ims = workload.make_batch(cfg, [workload.image_seed(args.seed, g) for g in range(min(n, 4))],
+                              threads=min(16, cores))
+    for i in range(args.warmup):
+        oracle.rd_forward_image(cfg, ims[i % len(ims)])
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        oracle.rd_forward_image(cfg, ims[(args.warmup + i) % len(ims)])
+    wall = time.perf_counter() - t0
+    value = args.steps * cfg.H * cfg.W / wall
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": rk.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{args.config}: one {cfg.H}x{cfg.W} image of the same workload per step "
+                               f"(bounded sample of the {cfg.n_img}-image batch)", "H": cfg.H, "W": cfg.W},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{args.steps} timed steps x 1 image, fp64 C oracle, {cores} OpenMP threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def log(msg):
+    if os.environ.get("CCRD_BENCH_VERBOSE"):
+        print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
+def main():
+    faulthandler.enable()
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="batched2k", choices=list(workload.CONFIGS))
+    ap.add_argument("--images", type=int, default=0, help="images per GPU (default: the config's)")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 breaks the timing rules", file=sys.stderr)
+    from paper_2403_11651_b200 import dist
+    if args.impl == "reference":
+        rk = dist.rank_from_env()
+        run_reference(args, rk)
+        return
+    rk = dist.init("nccl")
+    run_ours(args, rk)
+    import torch.distributed as tdist
+    if tdist.is_initialized():
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,191 @@
+/*
+ * ccrd.h -- C ABI of the B200-native Cool-chic rate-distortion forward.
+ *
+ * Computes, for each image, Eq. 1 (lines 117-124):
+ *
+ *     cost = D(x, x_hat) + lambda * R(y_hat) / (H W)
+ *     R(y_hat) = sum over every latent of every grid of -log2 p_psi(y_hat)
+ *     x_hat    = f_theta(f_upsilon(y_hat))       (Table 1)
+ *     D        = mean-squared error over the 3 H W values ("here the
+ *                mean-squared error")
+ *
+ * with the readings of DESIGN.md ("Readings of the paper"): Laplace(mu, b)
+ * integrated over the unit bin, b = exp(clamp(out1, logscale_min,
+ * logscale_max)), probability floored at p_floor before -log2, shared separable
+ * stride-2 transposed-conv upsampling with replicate padding, synthesis 1x1
+ * layers then residual 3x3 layers with replicate padding, ReLU after every layer
+ * except the last of each module (Table 1 caption).
+ *
+ * Every step runs in CUDA kernels compiled for sm_100a.  There is no CPU
+ * fallback: if no CUDA device is present every compute entry returns CC_ECUDA.
+ *
+ * Conventions
+ *   - All functions return 0 (CC_OK) or a negative CC_E* code; nothing aborts,
+ *     prints or throws across the ABI.  cc_last_error() gives a thread-local
+ *     human-readable detail of the last failure on the calling thread.
+ *   - The caller owns every buffer.  The library allocates nothing on the
+ *     device, keeps no pointer after return, and is reentrant.  Device buffers
+ *     must stay alive until the work queued on `stream` completes (CUDA stream
+ *     semantics).  `stream` is a cudaStream_t passed as void* (NULL = legacy
+ *     default stream).
+ *   - Weight blobs are HOST pointers (<= 8 KB per image); they are packed into
+ *     kernel parameters at call time, so no device->host synchronisation is
+ *     needed and the host memory may be reused as soon as the call returns.
+ *   - Latents: int16, device, levels 0..L-1 packed one after the other, each
+ *     row-major with h_l = ceil(H / 2^l) rows and w_l = ceil(W / 2^l) columns
+ *     (PAPER.md:103-105 writes H/2^l; SPEC.md:135 gives the ceiling).
+ *   - Images and x_hat: fp32, device, planar [3][H][W].
+ */
+#ifndef CCRD_H
+#define CCRD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CC_OK 0
+#define CC_EINVAL (-1)      /* null pointer, bad size, inconsistent widths, non-causal offset */
+#define CC_ENOTSUP (-2)     /* valid per the paper but not compiled in (see cc_model_desc)     */
+#define CC_EWORKSPACE (-3)  /* workspace missing or smaller than cc_workspace_bytes()         */
+#define CC_ECUDA (-4)       /* CUDA launch / runtime error (detail in cc_last_error)          */
+#define CC_ENONFINITE (-5)  /* non-finite result (opt-in check)                                */
+
+#define CC_MAX_LEVELS 12
+#define CC_MAX_CTX 32
+#define CC_MAX_LAYERS 8
+
+/* Model descriptor (by value; validated on every call).
+ *
+ * ARM f_psi (Table 1 ARM column): arm_widths = [n_ctx,
+ *   hidden..., 2]; layer k is "LinR" (u = W z + b + z) when bit k of
+ *   arm_residual_mask is set (requires in == out and k not last); ReLU after
+ *   every layer except the last; outputs (mu, log-scale).
+ *   Compiled: n_ctx in {8, 16, 24}, 1..3 hidden layers of equal width in
+ *   {8, 16, 24, 32}.
+ * Context: n_ctx strictly causal offsets (dy < 0, or dy == 0 and dx < 0) with
+ *   -3 <= dy <= 0 and |dx| <= 4; neighbours outside the grid read 0.
+ * Upsampling f_upsilon (Table 1 "1-1-TConv-K"): shared
+ *   separable k (x) k, K = up_taps in {4, 8}; no bias.
+ * Synthesis f_theta (Table 1 synthesis column): syn_widths = [L, C_h, 3]
+ *   (syn_n_1x1 = 2) then syn_n_res residual 3x3 3->3 layers.
+ *   Compiled: L in 1..8 with C_h in {8, 16, 24, 32, 40, 48}; syn_n_res in 0..3.
+ */
+typedef struct {
+  int32_t H, W, L;                     /* image size; 1 <= L <= 12                     */
+  int32_t n_ctx;                       /* context size C                               */
+  int8_t ctx_dy[CC_MAX_CTX];           /* offsets, in the order they feed layer 0      */
+  int8_t ctx_dx[CC_MAX_CTX];
+  int32_t arm_n_layers;                /* number of ARM linear layers                  */
+  int32_t arm_widths[CC_MAX_LAYERS + 1];
+  uint32_t arm_residual_mask;
+  int32_t up_taps;                     /* K                                            */
+  int32_t syn_n_1x1;                   /* number of 1x1 layers (2 supported)           */
+  int32_t syn_widths[CC_MAX_LAYERS + 1];
+  int32_t syn_n_res;                   /* residual 3x3 layers                          */
+  float logscale_min, logscale_max;    /* clamp of the ARM log-scale output            */
+  float p_floor;                       /* probability floor before -log2               */
+  double lambda;                       /* Lagrange multiplier of Eq. 1                 */
+} cc_model_desc;
+
+/* Per-image result, written to DEVICE memory (so it can be all-reduced
+ * without a host synchronisation). */
+typedef struct {
+  double rate_bits;  /* R, bits                          */
+  double sse;        /* sum over 3HW of (x - x_hat)^2    */
+  double mse;        /* sse / (3 H W)                    */
+  double cost;       /* mse + lambda * rate_bits / (H W) */
+} cc_rd_result;
+
+/* One image.  Blob layouts (fp32, row-major):
+ *   arm_w: per layer k: W_k[out][in], then b_k[out].
+ *   up_w : k[K].
+ *   syn_w: per 1x1 layer: A_m[out][in], a_m[out]; then per residual 3x3 layer
+ *          G_r[co][ci][ky][kx] (cross-correlation, replicate padding), g_r[3]. */
+typedef struct {
+  const int16_t* latents;  /* device, packed pyramid                     */
+  const float* arm_w;      /* HOST                                        */
+  const float* up_w;       /* HOST                                        */
+  const float* syn_w;      /* HOST                                        */
+  const float* image;      /* device [3][H][W] (may be NULL: sse = 0)     */
+  float* x_hat;            /* device [3][H][W] or NULL (not written)      */
+} cc_image_io;
+
+/* Workspace (device) needed by cc_rd_forward for n_img images; 0 on error. */
+size_t cc_workspace_bytes(const cc_model_desc* desc, int32_t n_img);
+
+/* The full RD forward for n_img images that share one descriptor (each image
+ * has its own latents, weights and image).  results: DEVICE array [n_img].
+ * Work is queued on `stream`; the call does not synchronise. */
+int cc_rd_forward(const cc_model_desc* desc, const cc_image_io* io, int32_t n_img,
+                  cc_rd_result* results, void* workspace, size_t workspace_bytes,
+                  void* stream);
+
+/* Same computation from HOST buffers (end-to-end path): io[i].latents,
+ * io[i].image and io[i].x_hat (optional) are host pointers (pinned memory
+ * recommended); results is a HOST array [n_img].  The call copies inputs to
+ * the device workspace (double-buffered, overlapped with compute), runs the
+ * forward, copies the results (and x_hat if requested) back and synchronises
+ * `stream` before returning.  Workspace: cc_workspace_bytes_host(). */
+size_t cc_workspace_bytes_host(const cc_model_desc* desc, int32_t n_img);
+int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t n_img,
+                       cc_rd_result* results, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
+/* Stage entry: ARM rate only (PAPER.md:120 R term).  rate: DEVICE double [1].
+ * Optional DEVICE float arrays (packed like the latents, NULL to skip):
+ * mu, scale (= b), bits (per latent -log2 P).  Workspace as cc_rd_forward(1). */
+int cc_arm_rate(const cc_model_desc* desc, const int16_t* latents, const float* arm_w,
+                double* rate, float* mu, float* scale, float* bits,
+                void* workspace, size_t workspace_bytes, void* stream);
+
+/* Stage entry: upsampling only -- DEVICE dense [L][H][W] fp32 (PAPER.md:109-111,
+ * "upsample the latents to a dense representation").  Runs the same fused
+ * kernel as cc_rd_forward with its dense output enabled. */
+int cc_upsample(const cc_model_desc* desc, const int16_t* latents, const float* up_w,
+                float* dense, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Stage entry: synthesis from a DEVICE dense [L][H][W] fp32 tensor to x_hat
+ * [3][H][W] (device) and sse (device double [1], needs image; NULL to skip).
+ * h_1x1 (optional, device [3][H][W]): output of the 1x1 stack. */
+int cc_synthesize(const cc_model_desc* desc, const float* dense, const float* syn_w,
+                  const float* image, float* x_hat, double* sse, float* h_1x1,
+                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* Closed-form multiply-accumulates per output pixel (host only, no device). */
+typedef struct {
+  double arm, up, syn, total;  /* per pixel                         */
+  int64_t arm_macs, up_macs, syn_macs;  /* per image (exact integers)  */
+  int64_t n_latents;
+} cc_mac_breakdown;
+double cc_mac_per_pixel(const cc_model_desc* desc, cc_mac_breakdown* out);
+
+/* Validates a descriptor (host only).  0 or a negative code. */
+int cc_validate(const cc_model_desc* desc);
+
+const char* cc_strerror(int code);
+const char* cc_last_error(void);
+const char* cc_version(void);
+
+/* Number of kernels the last cc_rd_forward / cc_rd_forward_host call on this
+ * thread launched (bench bookkeeping). */
+int64_t cc_last_launch_count(void);
+
+/* Per-kernel timing (bench.py roofline): between cc_profile_begin() and
+ * cc_profile_end(), every kernel the calling thread launches through this
+ * library is bracketed by CUDA events recorded on its own stream.
+ * cc_profile_end() synchronises those events and returns the summed device
+ * time per kernel kind.  Events only; no extra synchronisation in between. */
+typedef struct {
+  double arm_ms, syn_ms, reduce_ms;           /* summed event time per kind */
+  int64_t arm_launches, syn_launches, reduce_launches;
+} cc_profile_summary;
+int cc_profile_begin(void);
+int cc_profile_end(cc_profile_summary* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CCRD_H */

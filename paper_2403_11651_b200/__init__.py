@@ -1,0 +1,14 @@
+"""B200-native Cool-chic rate-distortion forward (arXiv 2403.11651).
+
+The product is the C-ABI library libccrd.so (include/ccrd.h) built from
+csrc/*.cu for sm_100a; ``ccrd`` is its thin ctypes binding and ``dist`` the
+one-process-per-GPU sharding.  There is no CPU fallback.
+"""
+from . import ccrd  # noqa: F401
+from .ccrd import (  # noqa: F401
+    CcError, CcImageIO, CcModelDesc, CcRdResult, DeviceBatch, cc_arm_rate, cc_mac_per_pixel,
+    cc_rd_forward, cc_rd_forward_host, cc_synthesize, cc_upsample, cc_validate, cc_workspace_bytes,
+    cc_workspace_bytes_host, desc_from_config, load,
+)
+
+__version__ = "0.1.0"

@@ -1,0 +1,266 @@
+"""Thin ctypes binding of libccrd.so (include/ccrd.h) -- argument marshalling
+only.  Every step of the RD forward runs in the library's CUDA kernels; there
+is no Python or CPU fallback: if the library cannot be loaded, or no CUDA
+device is present, calls raise.
+
+Functions keep the C names (cc_rd_forward, cc_arm_rate, ...).  Device buffers
+are passed as raw pointers (ints); ``torch`` is only used by the convenience
+helpers at the bottom for device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import build as _build
+
+CC_MAX_LEVELS = 12
+CC_MAX_CTX = 32
+CC_MAX_LAYERS = 8
+
+CC_OK, CC_EINVAL, CC_ENOTSUP, CC_EWORKSPACE, CC_ECUDA, CC_ENONFINITE = 0, -1, -2, -3, -4, -5
+
+
+class CcModelDesc(C.Structure):
+    _fields_ = [
+        ("H", C.c_int32), ("W", C.c_int32), ("L", C.c_int32),
+        ("n_ctx", C.c_int32),
+        ("ctx_dy", C.c_int8 * CC_MAX_CTX), ("ctx_dx", C.c_int8 * CC_MAX_CTX),
+        ("arm_n_layers", C.c_int32), ("arm_widths", C.c_int32 * (CC_MAX_LAYERS + 1)),
+        ("arm_residual_mask", C.c_uint32),
+        ("up_taps", C.c_int32),
+        ("syn_n_1x1", C.c_int32), ("syn_widths", C.c_int32 * (CC_MAX_LAYERS + 1)),
+        ("syn_n_res", C.c_int32),
+        ("logscale_min", C.c_float), ("logscale_max", C.c_float),
+        ("p_floor", C.c_float),
+        ("lam", C.c_double),
+    ]
+
+
+class CcRdResult(C.Structure):
+    _fields_ = [("rate_bits", C.c_double), ("sse", C.c_double), ("mse", C.c_double), ("cost", C.c_double)]
+
+
+class CcImageIO(C.Structure):
+    _fields_ = [("latents", C.c_void_p), ("arm_w", C.c_void_p), ("up_w", C.c_void_p),
+                ("syn_w", C.c_void_p), ("image", C.c_void_p), ("x_hat", C.c_void_p)]
+
+
+class CcMacBreakdown(C.Structure):
+    _fields_ = [("arm", C.c_double), ("up", C.c_double), ("syn", C.c_double), ("total", C.c_double),
+                ("arm_macs", C.c_int64), ("up_macs", C.c_int64), ("syn_macs", C.c_int64),
+                ("n_latents", C.c_int64)]
+
+
+class CcProfileSummary(C.Structure):
+    _fields_ = [("arm_ms", C.c_double), ("syn_ms", C.c_double), ("reduce_ms", C.c_double),
+                ("arm_launches", C.c_int64), ("syn_launches", C.c_int64), ("reduce_launches", C.c_int64)]
+
+
+# Symbols include/ccrd.h declares (checked by tests/test_abi.py).
+EXPORTS = ["cc_workspace_bytes", "cc_rd_forward", "cc_workspace_bytes_host", "cc_rd_forward_host",
+           "cc_arm_rate", "cc_upsample", "cc_synthesize", "cc_mac_per_pixel", "cc_validate",
+           "cc_strerror", "cc_last_error", "cc_version", "cc_last_launch_count",
+           "cc_profile_begin", "cc_profile_end"]
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load(rebuild_if_stale: bool = True) -> C.CDLL:
+    """Load libccrd.so (building it in-tree with nvcc if missing or stale)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if rebuild_if_stale:
+        try:
+            _build.build()
+        except FileNotFoundError:
+            pass  # no nvcc: fall through to loading what exists
+    if not os.path.exists(_build.LIB):
+        raise ImportError(f"libccrd.so not built ({_build.LIB}); run paper_2403_11651_b200/build.py")
+    L = C.CDLL(_build.LIB)
+    P, V, S = C.POINTER, C.c_void_p, C.c_size_t
+    D = P(CcModelDesc)
+    L.cc_workspace_bytes.restype = S
+    L.cc_workspace_bytes.argtypes = [D, C.c_int32]
+    L.cc_workspace_bytes_host.restype = S
+    L.cc_workspace_bytes_host.argtypes = [D, C.c_int32]
+    L.cc_rd_forward.restype = C.c_int
+    L.cc_rd_forward.argtypes = [D, P(CcImageIO), C.c_int32, V, V, S, V]
+    L.cc_rd_forward_host.restype = C.c_int
+    L.cc_rd_forward_host.argtypes = [D, P(CcImageIO), C.c_int32, V, V, S, V]
+    L.cc_arm_rate.restype = C.c_int
+    L.cc_arm_rate.argtypes = [D, V, V, V, V, V, V, V, S, V]
+    L.cc_upsample.restype = C.c_int
+    L.cc_upsample.argtypes = [D, V, V, V, V, S, V]
+    L.cc_synthesize.restype = C.c_int
+    L.cc_synthesize.argtypes = [D, V, V, V, V, V, V, V, S, V]
+    L.cc_mac_per_pixel.restype = C.c_double
+    L.cc_mac_per_pixel.argtypes = [D, P(CcMacBreakdown)]
+    L.cc_validate.restype = C.c_int
+    L.cc_validate.argtypes = [D]
+    L.cc_strerror.restype = C.c_char_p
+    L.cc_strerror.argtypes = [C.c_int]
+    L.cc_last_error.restype = C.c_char_p
+    L.cc_version.restype = C.c_char_p
+    L.cc_last_launch_count.restype = C.c_int64
+    L.cc_profile_begin.restype = C.c_int
+    L.cc_profile_end.restype = C.c_int
+    L.cc_profile_end.argtypes = [P(CcProfileSummary)]
+    _lib = L
+    return L
+
+
+class CcError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        L = load()
+        super().__init__(f"{where}: {L.cc_strerror(code).decode()} ({code}): {L.cc_last_error().decode()}")
+        self.code = code
+
+
+def _check(rc: int, where: str):
+    if rc != CC_OK:
+        raise CcError(rc, where)
+
+
+# ------------------------------------------------------------------ descriptor
+def make_desc(H, W, L, ctx, arm_widths, arm_residual, up_taps, syn_widths, syn_n_res,
+              logscale_min, logscale_max, p_floor, lam) -> CcModelDesc:
+    d = CcModelDesc()
+    d.H, d.W, d.L = H, W, L
+    d.n_ctx = len(ctx)
+    for c, (dy, dx) in enumerate(ctx):
+        d.ctx_dy[c] = dy
+        d.ctx_dx[c] = dx
+    d.arm_n_layers = len(arm_widths) - 1
+    for k, v in enumerate(arm_widths):
+        d.arm_widths[k] = v
+    d.arm_residual_mask = sum(1 << k for k, r in enumerate(arm_residual) if r)
+    d.up_taps = up_taps
+    d.syn_n_1x1 = len(syn_widths) - 1
+    for k, v in enumerate(syn_widths):
+        d.syn_widths[k] = v
+    d.syn_n_res = syn_n_res
+    d.logscale_min, d.logscale_max, d.p_floor = logscale_min, logscale_max, p_floor
+    d.lam = lam
+    return d
+
+
+def desc_from_config(cfg, H: Optional[int] = None, W: Optional[int] = None) -> CcModelDesc:
+    """Descriptor from a workload.Config (the shared, arithmetic-free config)."""
+    return make_desc(cfg.H if H is None else H, cfg.W if W is None else W, cfg.L, cfg.ctx,
+                     cfg.arm_widths, cfg.arm_residual, cfg.up_taps, cfg.syn_widths, cfg.syn_n_res,
+                     cfg.logscale_min, cfg.logscale_max, cfg.p_floor, cfg.lam)
+
+
+# ------------------------------------------------------------------ raw calls
+def cc_workspace_bytes(desc: CcModelDesc, n_img: int) -> int:
+    return load().cc_workspace_bytes(C.byref(desc), n_img)
+
+
+def cc_workspace_bytes_host(desc: CcModelDesc, n_img: int) -> int:
+    return load().cc_workspace_bytes_host(C.byref(desc), n_img)
+
+
+def cc_validate(desc: CcModelDesc) -> int:
+    return load().cc_validate(C.byref(desc))
+
+
+def cc_mac_per_pixel(desc: CcModelDesc) -> CcMacBreakdown:
+    out = CcMacBreakdown()
+    v = load().cc_mac_per_pixel(C.byref(desc), C.byref(out))
+    if v < 0:
+        raise CcError(cc_validate(desc), "cc_mac_per_pixel")
+    return out
+
+
+def cc_rd_forward(desc, io: Sequence[CcImageIO], results_ptr: int, ws_ptr: int, ws_bytes: int,
+                  stream_ptr: int = 0) -> None:
+    arr = (CcImageIO * len(io))(*io)
+    _check(load().cc_rd_forward(C.byref(desc), arr, len(io), results_ptr, ws_ptr, ws_bytes, stream_ptr),
+           "cc_rd_forward")
+
+
+def cc_rd_forward_host(desc, io: Sequence[CcImageIO], results: np.ndarray, ws_ptr: int, ws_bytes: int,
+                       stream_ptr: int = 0) -> None:
+    assert results.dtype == np.float64 and results.size >= 4 * len(io) and results.flags.c_contiguous
+    arr = (CcImageIO * len(io))(*io)
+    _check(load().cc_rd_forward_host(C.byref(desc), arr, len(io), results.ctypes.data, ws_ptr, ws_bytes,
+                                     stream_ptr), "cc_rd_forward_host")
+
+
+def cc_arm_rate(desc, latents_ptr, arm_w: np.ndarray, rate_ptr, mu_ptr, scale_ptr, bits_ptr, ws_ptr, ws_bytes,
+                stream_ptr=0) -> None:
+    aw = np.ascontiguousarray(arm_w, np.float32)
+    _check(load().cc_arm_rate(C.byref(desc), latents_ptr, aw.ctypes.data, rate_ptr, mu_ptr, scale_ptr, bits_ptr,
+                              ws_ptr, ws_bytes, stream_ptr), "cc_arm_rate")
+
+
+def cc_upsample(desc, latents_ptr, up_w: np.ndarray, dense_ptr, ws_ptr=0, ws_bytes=0, stream_ptr=0) -> None:
+    uw = np.ascontiguousarray(up_w, np.float32)
+    _check(load().cc_upsample(C.byref(desc), latents_ptr, uw.ctypes.data, dense_ptr, ws_ptr, ws_bytes, stream_ptr),
+           "cc_upsample")
+
+
+def cc_synthesize(desc, dense_ptr, syn_w: np.ndarray, image_ptr, x_hat_ptr, sse_ptr, h1_ptr, ws_ptr, ws_bytes,
+                  stream_ptr=0) -> None:
+    sw = np.ascontiguousarray(syn_w, np.float32)
+    _check(load().cc_synthesize(C.byref(desc), dense_ptr, sw.ctypes.data, image_ptr, x_hat_ptr, sse_ptr, h1_ptr,
+                                ws_ptr, ws_bytes, stream_ptr), "cc_synthesize")
+
+
+def cc_last_launch_count() -> int:
+    return load().cc_last_launch_count()
+
+
+def cc_profile_begin() -> None:
+    _check(load().cc_profile_begin(), "cc_profile_begin")
+
+
+def cc_profile_end() -> CcProfileSummary:
+    out = CcProfileSummary()
+    _check(load().cc_profile_end(C.byref(out)), "cc_profile_end")
+    return out
+
+
+def cc_version() -> str:
+    return load().cc_version().decode()
+
+
+# ------------------------------------------------------------- torch helpers
+class DeviceBatch:
+    """Device-resident inputs of n images (torch tensors for memory only) and
+    the host weight blobs, laid out for cc_rd_forward."""
+
+    def __init__(self, cfg, images: List, device="cuda", with_xhat=True):
+        import torch
+        self.cfg = cfg
+        self.desc = desc_from_config(cfg)
+        self.n = len(images)
+        self.lat = [torch.from_numpy(im.latents).to(device) for im in images]
+        self.img = [torch.from_numpy(im.image).to(device) for im in images]
+        self.xhat = [torch.empty_like(t) for t in self.img] if with_xhat else None
+        self.arm_w = [np.ascontiguousarray(im.arm_w, np.float32) for im in images]
+        self.up_w = [np.ascontiguousarray(im.up_w, np.float32) for im in images]
+        self.syn_w = [np.ascontiguousarray(im.syn_w, np.float32) for im in images]
+        self.ws_bytes = cc_workspace_bytes(self.desc, self.n)
+        if self.ws_bytes == 0:
+            raise CcError(cc_validate(self.desc), "cc_workspace_bytes")
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=device)
+        self.results = torch.zeros((self.n, 4), dtype=torch.float64, device=device)
+        self.io = [CcImageIO(self.lat[i].data_ptr(), self.arm_w[i].ctypes.data, self.up_w[i].ctypes.data,
+                             self.syn_w[i].ctypes.data, self.img[i].data_ptr(),
+                             self.xhat[i].data_ptr() if with_xhat else None) for i in range(self.n)]
+
+    def forward(self, stream_ptr: Optional[int] = None):
+        import torch
+        s = torch.cuda.current_stream().cuda_stream if stream_ptr is None else stream_ptr
+        cc_rd_forward(self.desc, self.io, self.results.data_ptr(), self.ws.data_ptr(), self.ws_bytes, s)
+        return self.results

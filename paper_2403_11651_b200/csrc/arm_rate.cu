@@ -1,0 +1,195 @@
+// arm_rate.cu -- ARM rate kernel: causal context gather, ARM MLP f_psi, Laplace
+// bin probability and -log2, summed over every latent of every grid in ONE
+// launch (PAPER.md:106-109 ARM, :120 R term of Eq. 1; Table 1 ARM column).
+//
+// Design (B200, FP32-FMA bound):
+//   * one CTA = 8 rows x 32 latents of one grid; CTAs of all L grids form one
+//     grid, mapped to (level, tile) through a prefix table in the parameters;
+//   * the causal window (3 rows above, 4 columns each side) is staged from the
+//     int16 pyramid into shared memory as fp32, zero outside the grid;
+//   * one latent per thread; the MLP weights live in the kernel-parameter bank
+//     (uniform operands, no LSU traffic) and every multiply-accumulate is a
+//     packed FFMA2 producing two output neurons;
+//   * stable Laplace -log2 P in fp32; per-thread bits -> warp shuffle ->
+//     fp64 per-CTA partial (deterministic; final sum in ccrd_api.cu).
+#include "ccrd_common.cuh"
+
+namespace ccrd {
+
+// -log2 of the Laplace(mu, b) mass of the bin [y - 1/2, y + 1/2], floored at
+// p_floor (readings #1-#3).  With a = |y - mu| and
+// ib = 1/b:
+//   a <  1/2 : P = 1 - (exp(-(1/2 - a) ib) + exp(-(1/2 + a) ib)) / 2
+//   a >= 1/2 : -log2 P = 1 + (a - 1/2) ib log2(e) - log2(1 - exp(-ib))
+// (the second form is log-domain, so far tails do not underflow).
+__device__ __forceinline__ float laplace_bits(float y, float mu, float s, const ArmGeom& g) {
+  s = fminf(fmaxf(s, g.lsmin), g.lsmax);
+  const float ib = __expf(-s);
+  const float a = fabsf(y - mu);
+  const float am = fminf(a, 0.5f);
+  const float e1 = __expf((am - 0.5f) * ib);
+  const float e2 = __expf(-(am + 0.5f) * ib);
+  const float p_in = 1.0f - 0.5f * (e1 + e2);
+  const float bits_in = -__log2f(fmaxf(p_in, g.p_floor));
+  const float bits_out = 1.0f + (a - 0.5f) * ib * 1.4426950408889634f - __log2f(-expm1f(-ib));
+  return fminf(a < 0.5f ? bits_in : bits_out, g.bits_cap);
+}
+
+// One dense layer NIN -> 2*NO2 with FFMA2 (two outputs per instruction).
+template <int NIN, int NO2, bool RELU>
+__device__ __forceinline__ void dense_ffma2(const float (&in)[NIN], float (&out)[2 * NO2],
+                                            const float2 (&W)[NIN][NO2], const float2 (&B)[NO2]) {
+  uint64_t acc[NO2];
+#pragma unroll
+  for (int n = 0; n < NO2; n++) acc[n] = ldp2(B[n]);
+#pragma unroll
+  for (int i = 0; i < NIN; i++) {
+    const uint64_t x = f2pack(in[i], in[i]);
+#pragma unroll
+    for (int n = 0; n < NO2; n++) acc[n] = ffma2(x, ldp2(W[i][n]), acc[n]);
+  }
+#pragma unroll
+  for (int n = 0; n < NO2; n++) {
+    float2 v = f2unpack(acc[n]);
+    out[2 * n] = RELU ? fmaxf(v.x, 0.0f) : v.x;
+    out[2 * n + 1] = RELU ? fmaxf(v.y, 0.0f) : v.y;
+  }
+}
+
+template <int C, int NH, int NHL>
+__global__ void __launch_bounds__(ARM_THREADS, 2)
+    arm_rate_kernel(const __grid_constant__ ArmParams<C, NH, NHL> p) {
+  __shared__ float tile[ARM_SH * ARM_SW];
+  __shared__ double warp_buf[ARM_THREADS / 32];
+
+  // (level, tile) of this CTA
+  const int b = blockIdx.x;
+  int l = 0;
+#pragma unroll 1
+  while (l + 1 < p.g.L && b >= p.g.tile_begin[l + 1]) l++;
+  const int h = p.g.lv.h[l], w = p.g.lv.w[l];
+  const int t = b - p.g.tile_begin[l];
+  const int ty = t / p.g.tiles_x[l];
+  const int tx = t - ty * p.g.tiles_x[l];
+  const int i0 = ty * ARM_TY, j0 = tx * ARM_TX;
+  const int16_t* __restrict__ grid = p.lat + p.g.lv.off[l];
+
+  // stage the causal window, fp32, zero outside the grid (reading #5)
+#pragma unroll 1
+  for (int s = threadIdx.x; s < ARM_SH * ARM_SW; s += ARM_THREADS) {
+    const int r = s / ARM_SW, c = s - r * ARM_SW;
+    const int gi = i0 - ARM_HALO_TOP + r, gj = j0 - ARM_HALO_X + c;
+    float v = 0.0f;
+    if (gi >= 0 && gi < h && gj >= 0 && gj < w) v = (float)__ldg(grid + (int64_t)gi * w + gj);
+    tile[s] = v;
+  }
+  __syncthreads();
+
+  const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
+  const int i = i0 + ly, j = j0 + lx;
+  const bool valid = (i < h) && (j < w);
+  const float* center = tile + (ly + ARM_HALO_TOP) * ARM_SW + (lx + ARM_HALO_X);
+
+  // context gather (reading #4: offsets in template order)
+  float z0[C];
+#pragma unroll
+  for (int c = 0; c < C; c++) z0[c] = center[p.g.ctx_off[c]];
+  const float y = center[0];
+
+  // ARM MLP: C -> NH (ReLU) -> [NH -> NH (ReLU)] x (NHL-1) -> 2
+  float z[NH];
+  dense_ffma2<C, NH / 2, true>(z0, z, p.w.w0, p.w.b0);
+#pragma unroll
+  for (int k = 0; k < NHL - 1; k++) {
+    float zn[NH];
+    dense_ffma2<NH, NH / 2, true>(z, zn, p.w.wh[k], p.w.bh[k]);
+#pragma unroll
+    for (int n = 0; n < NH; n++) z[n] = zn[n];
+  }
+  uint64_t o = ldp2(p.w.bo);
+#pragma unroll
+  for (int n = 0; n < NH; n++) o = ffma2(f2pack(z[n], z[n]), ldp2(p.w.wo[n]), o);
+  const float2 ms = f2unpack(o);
+
+  float bits = 0.0f;
+  if (valid) {
+    bits = laplace_bits(y, ms.x, ms.y, p.g);
+    if (p.bits != nullptr) {
+      const int64_t q = p.g.lv.off[l] + (int64_t)i * w + j;
+      p.bits[q] = bits;
+      if (p.mu) p.mu[q] = ms.x;
+      if (p.scale) p.scale[q] = __expf(fminf(fmaxf(ms.y, p.g.lsmin), p.g.lsmax));
+    }
+  }
+  const double s = block_sum<ARM_THREADS>(bits, warp_buf);
+  if (threadIdx.x == 0) p.partial[b] = s;
+}
+
+// ---------------------------------------------------------------- host launcher
+template <int C, int NH, int NHL>
+static int launch_arm(const ArmGeom& g, const cc_model_desc& d, const float* arm_w,
+                      const int16_t* lat, double* partial, float* mu, float* scale, float* bits,
+                      cudaStream_t stream) {
+  ArmParams<C, NH, NHL> p;
+  p.g = g;
+  p.lat = lat;
+  p.partial = partial;
+  p.mu = mu;
+  p.scale = scale;
+  p.bits = bits;
+  // pack weights (blob: per layer W[out][in] then b[out]); fold residuals
+  const float* q = arm_w;
+  auto res = [&](int k) { return (d.arm_residual_mask >> k) & 1u; };
+  for (int i = 0; i < C; i++)
+    for (int n = 0; n < NH / 2; n++) {
+      float a = q[(2 * n) * C + i], b = q[(2 * n + 1) * C + i];
+      if (res(0)) {  // only legal when C == NH (validated)
+        a += (i == 2 * n) ? 1.0f : 0.0f;
+        b += (i == 2 * n + 1) ? 1.0f : 0.0f;
+      }
+      p.w.w0[i][n] = make_float2(a, b);
+    }
+  for (int n = 0; n < NH / 2; n++) p.w.b0[n] = make_float2(q[C * NH + 2 * n], q[C * NH + 2 * n + 1]);
+  q += C * NH + NH;
+  for (int k = 0; k < NHL - 1; k++) {
+    for (int i = 0; i < NH; i++)
+      for (int n = 0; n < NH / 2; n++) {
+        float a = q[(2 * n) * NH + i], b = q[(2 * n + 1) * NH + i];
+        if (res(k + 1)) {
+          a += (i == 2 * n) ? 1.0f : 0.0f;
+          b += (i == 2 * n + 1) ? 1.0f : 0.0f;
+        }
+        p.w.wh[k][i][n] = make_float2(a, b);
+      }
+    for (int n = 0; n < NH / 2; n++) p.w.bh[k][n] = make_float2(q[NH * NH + 2 * n], q[NH * NH + 2 * n + 1]);
+    q += NH * NH + NH;
+  }
+  for (int i = 0; i < NH; i++) p.w.wo[i] = make_float2(q[i], q[NH + i]);
+  p.w.bo = make_float2(q[2 * NH], q[2 * NH + 1]);
+
+  const int grid = g.tile_begin[g.L];
+  arm_rate_kernel<C, NH, NHL><<<grid, ARM_THREADS, 0, stream>>>(p);
+  return 0;
+}
+
+struct ArmEntry {
+  int C, NH, NHL;
+  ArmLaunchFn fn;
+};
+
+// Compiled architectures: BASELINE.json configs ([8,8,8,2], [16,24,24,2]) and
+// the Table 1 ARMs (A300 [8,8,2], A545 [8,8,8,2], A1079 [16,16,16,2],
+// A2300 [24,24,24,2]).
+static const ArmEntry kArm[] = {
+    {8, 8, 1, launch_arm<8, 8, 1>},     {8, 8, 2, launch_arm<8, 8, 2>},
+    {16, 16, 2, launch_arm<16, 16, 2>}, {16, 24, 2, launch_arm<16, 24, 2>},
+    {24, 24, 2, launch_arm<24, 24, 2>},
+};
+
+ArmLaunchFn find_arm_launcher(int C, int NH, int NHL) {
+  for (const auto& e : kArm)
+    if (e.C == C && e.NH == NH && e.NHL == NHL) return e.fn;
+  return nullptr;
+}
+
+}  // namespace ccrd

@@ -1,0 +1,589 @@
+// ccrd_api.cu -- the C ABI (include/ccrd.h): validation, geometry, dispatch to
+// the compiled kernel shapes, the deterministic fp64 reduction kernel, the
+// host-buffer (end-to-end) path and the MAC closed form.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "ccrd_common.cuh"
+
+namespace ccrd {
+
+static thread_local char g_err[512] = "";
+static thread_local int64_t g_launches = 0;
+
+// ---- optional per-kernel event timing (cc_profile_begin / cc_profile_end)
+enum { PK_ARM = 0, PK_SYN = 1, PK_RED = 2 };
+struct ProfRec {
+  int kind;
+  cudaEvent_t a, b;
+};
+struct ProfState {
+  bool on = false;
+  ProfRec* recs = nullptr;
+  int n = 0, cap = 0;
+  cudaEvent_t* pool = nullptr;  // reusable events
+  int pool_n = 0, pool_used = 0;
+};
+static thread_local ProfState g_prof;
+
+static cudaEvent_t prof_event() {
+  ProfState& P = g_prof;
+  if (P.pool_used == P.pool_n) {
+    int nn = P.pool_n ? 2 * P.pool_n : 256;
+    cudaEvent_t* np = new cudaEvent_t[nn];
+    for (int i = 0; i < P.pool_n; i++) np[i] = P.pool[i];
+    for (int i = P.pool_n; i < nn; i++) cudaEventCreate(&np[i]);
+    delete[] P.pool;
+    P.pool = np;
+    P.pool_n = nn;
+  }
+  return P.pool[P.pool_used++];
+}
+
+// RAII bracket around one launch
+struct ProfScope {
+  int kind;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  ProfScope(int k, cudaStream_t st) : kind(k), s(st) {
+    if (g_prof.on) {
+      a = prof_event();
+      cudaEventRecord(a, s);
+    }
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEvent_t b = prof_event();
+    cudaEventRecord(b, s);
+    ProfState& P = g_prof;
+    if (P.n == P.cap) {
+      int nc = P.cap ? 2 * P.cap : 256;
+      ProfRec* nr = new ProfRec[nc];
+      for (int i = 0; i < P.n; i++) nr[i] = P.recs[i];
+      delete[] P.recs;
+      P.recs = nr;
+      P.cap = nc;
+    }
+    P.recs[P.n++] = ProfRec{kind, a, b};
+  }
+};
+
+static int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+static int cuda_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(CC_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return CC_OK;
+}
+
+// ------------------------------------------------------------- descriptor
+static void level_dims(const cc_model_desc& d, LevelGeom& g, int64_t* n_lat) {
+  int64_t off = 0;
+  for (int l = 0; l < CC_MAX_LEVELS; l++) {
+    if (l < d.L) {
+      const int64_t s = (int64_t)1 << l;
+      g.h[l] = (int32_t)((d.H + s - 1) / s);
+      g.w[l] = (int32_t)((d.W + s - 1) / s);
+      g.off[l] = off;
+      off += (int64_t)g.h[l] * g.w[l];
+    } else {
+      g.h[l] = g.w[l] = 0;
+      g.off[l] = off;
+    }
+  }
+  if (n_lat) *n_lat = off;
+}
+
+static int validate(const cc_model_desc* dp) {
+  if (!dp) return fail(CC_EINVAL, "null descriptor");
+  const cc_model_desc& d = *dp;
+  if (d.H < 1 || d.W < 1) return fail(CC_EINVAL, "H, W must be >= 1 (got %d x %d)", d.H, d.W);
+  if ((int64_t)d.H * d.W > ((int64_t)1 << 31)) return fail(CC_ENOTSUP, "image larger than 2^31 pixels");
+  if (d.L < 1 || d.L > CC_MAX_LEVELS) return fail(CC_EINVAL, "L must be in 1..%d (got %d)", CC_MAX_LEVELS, d.L);
+  if (d.n_ctx < 1 || d.n_ctx > CC_MAX_CTX) return fail(CC_EINVAL, "n_ctx must be in 1..%d", CC_MAX_CTX);
+  for (int c = 0; c < d.n_ctx; c++) {
+    const int dy = d.ctx_dy[c], dx = d.ctx_dx[c];
+    if (!(dy < 0 || (dy == 0 && dx < 0)))
+      return fail(CC_EINVAL, "context offset %d (%d,%d) is not strictly causal", c, dy, dx);
+    if (dy < -ARM_HALO_TOP || dx < -ARM_HALO_X || dx > ARM_HALO_X)
+      return fail(CC_ENOTSUP, "context offset %d (%d,%d) outside the staged window (dy>=-3, |dx|<=4)", c, dy, dx);
+    for (int e = 0; e < c; e++)
+      if (d.ctx_dy[e] == dy && d.ctx_dx[e] == dx) return fail(CC_EINVAL, "duplicate context offset %d", c);
+  }
+  if (d.arm_n_layers < 2 || d.arm_n_layers > CC_MAX_LAYERS)
+    return fail(CC_ENOTSUP, "arm_n_layers must be in 2..%d", CC_MAX_LAYERS);
+  if (d.arm_widths[0] != d.n_ctx) return fail(CC_EINVAL, "arm_widths[0] (%d) != n_ctx (%d)", d.arm_widths[0], d.n_ctx);
+  if (d.arm_widths[d.arm_n_layers] != 2) return fail(CC_EINVAL, "ARM must output 2 values (mu, log-scale)");
+  for (int k = 0; k < d.arm_n_layers; k++) {
+    if (d.arm_widths[k] < 1) return fail(CC_EINVAL, "ARM width %d < 1", k);
+    if ((d.arm_residual_mask >> k) & 1u) {
+      if (k == d.arm_n_layers - 1) return fail(CC_EINVAL, "residual on the last ARM layer");
+      if (d.arm_widths[k] != d.arm_widths[k + 1]) return fail(CC_EINVAL, "residual ARM layer %d is not square", k);
+    }
+  }
+  if (d.arm_residual_mask >> d.arm_n_layers) return fail(CC_EINVAL, "residual mask has bits past the last layer");
+  for (int k = 2; k < d.arm_n_layers; k++)
+    if (d.arm_widths[k] != d.arm_widths[1]) return fail(CC_ENOTSUP, "ARM hidden layers must share one width");
+  if (d.up_taps != 4 && d.up_taps != 8) return fail(CC_ENOTSUP, "up_taps must be 4 or 8");
+  if (d.syn_n_1x1 != 2) return fail(CC_ENOTSUP, "synthesis must have exactly two 1x1 layers");
+  if (d.syn_widths[0] != d.L) return fail(CC_EINVAL, "syn_widths[0] (%d) != L (%d)", d.syn_widths[0], d.L);
+  if (d.syn_widths[2] != 3) return fail(CC_EINVAL, "synthesis must output 3 channels");
+  if (d.syn_widths[1] < 1) return fail(CC_EINVAL, "synthesis hidden width < 1");
+  if (d.syn_n_res < 0 || d.syn_n_res > 3) return fail(CC_ENOTSUP, "syn_n_res must be in 0..3");
+  if (!(d.logscale_min <= d.logscale_max)) return fail(CC_EINVAL, "logscale_min > logscale_max");
+  if (!(d.p_floor > 0.0f && d.p_floor < 1.0f)) return fail(CC_EINVAL, "p_floor must be in (0, 1)");
+  for (int l = 0; l < d.L; l++) {
+    const int64_t s = (int64_t)1 << l;
+    if ((d.H + s - 1) / s < 1 || (d.W + s - 1) / s < 1) return fail(CC_EINVAL, "level %d has zero size", l);
+  }
+  if (!find_arm_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1))
+    return fail(CC_ENOTSUP, "ARM shape (C=%d, hidden=%d x %d) not compiled", d.n_ctx, d.arm_widths[1],
+                d.arm_n_layers - 1);
+  if (!find_syn_launcher(d.L, d.syn_widths[1], d.syn_n_res, d.up_taps))
+    return fail(CC_ENOTSUP, "synthesis shape (L=%d, C_h=%d, R=%d, K=%d) not compiled", d.L, d.syn_widths[1],
+                d.syn_n_res, d.up_taps);
+  return CC_OK;
+}
+
+static void arm_geom(const cc_model_desc& d, ArmGeom& g) {
+  memset(&g, 0, sizeof(g));
+  level_dims(d, g.lv, nullptr);
+  g.L = d.L;
+  int acc = 0;
+  for (int l = 0; l < CC_MAX_LEVELS; l++) {
+    g.tile_begin[l] = acc;
+    if (l < d.L) {
+      g.tiles_x[l] = (g.lv.w[l] + ARM_TX - 1) / ARM_TX;
+      acc += g.tiles_x[l] * ((g.lv.h[l] + ARM_TY - 1) / ARM_TY);
+    }
+  }
+  g.tile_begin[CC_MAX_LEVELS] = acc;
+  g.tile_begin[d.L] = acc;
+  for (int c = 0; c < d.n_ctx; c++) g.ctx_off[c] = d.ctx_dy[c] * ARM_SW + d.ctx_dx[c];
+  g.lsmin = d.logscale_min;
+  g.lsmax = d.logscale_max;
+  g.p_floor = d.p_floor;
+  g.bits_cap = (float)(-log2((double)d.p_floor));
+}
+
+static void syn_geom(const cc_model_desc& d, SynGeom& g) {
+  memset(&g, 0, sizeof(g));
+  level_dims(d, g.lv, nullptr);
+  g.H = d.H;
+  g.W = d.W;
+  g.tiles_x = (d.W + SYN_TW - 1) / SYN_TW;
+  g.n_tiles = g.tiles_x * ((d.H + SYN_TH - 1) / SYN_TH);
+}
+
+static int n_arm_ctas(const cc_model_desc& d) {
+  ArmGeom g;
+  arm_geom(d, g);
+  return g.tile_begin[d.L];
+}
+static int n_syn_ctas(const cc_model_desc& d) {
+  SynGeom g;
+  syn_geom(d, g);
+  return g.n_tiles;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// per image: ARM partials + synthesis partials (fp64) + a result scratch slot
+// used by the stage entries
+static size_t partial_bytes(const cc_model_desc& d) {
+  return align256(sizeof(double) * (size_t)(n_arm_ctas(d) + n_syn_ctas(d))) + align256(sizeof(cc_rd_result));
+}
+
+// ------------------------------------------------------------- reduction
+// One CTA per image, fixed-order tree => bitwise deterministic.
+// Kernel-parameter batch of reduction jobs (avoids a host->device copy).
+constexpr int MAX_JOBS_PER_LAUNCH = 64;
+struct ReduceBatch {
+  ReduceJob j[MAX_JOBS_PER_LAUNCH];
+};
+__global__ void __launch_bounds__(256) reduce_batch_kernel(const __grid_constant__ ReduceBatch b,
+                                                           cc_rd_result* __restrict__ out) {
+  __shared__ double sa[256], ss[256];
+  const ReduceJob& j = b.j[blockIdx.x];
+  double a = 0.0, s = 0.0;
+  for (int i = threadIdx.x; i < j.n_arm; i += 256) a += j.arm_partial[i];
+  for (int i = threadIdx.x; i < j.n_syn; i += 256) s += j.syn_partial[i];
+  sa[threadIdx.x] = a;
+  ss[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      sa[threadIdx.x] += sa[threadIdx.x + o];
+      ss[threadIdx.x] += ss[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    cc_rd_result r;
+    r.rate_bits = sa[0];
+    r.sse = ss[0];
+    r.mse = ss[0] * j.inv_3p;
+    r.cost = r.mse + j.lambda_over_p * sa[0];
+    out[blockIdx.x] = r;
+  }
+}
+
+static ReduceJob make_job(const cc_model_desc& d, double* part) {
+  ReduceJob j;
+  j.n_arm = n_arm_ctas(d);
+  j.n_syn = n_syn_ctas(d);
+  j.arm_partial = part;
+  j.syn_partial = part + j.n_arm;
+  const double P = (double)d.H * (double)d.W;
+  j.inv_3p = 1.0 / (3.0 * P);
+  j.lambda_over_p = d.lambda / P;
+  return j;
+}
+
+static int launch_reduce(const ReduceJob* jobs, int n, cc_rd_result* out, cudaStream_t s) {
+  for (int b = 0; b < n; b += MAX_JOBS_PER_LAUNCH) {
+    ReduceBatch rb;
+    const int m = (n - b < MAX_JOBS_PER_LAUNCH) ? n - b : MAX_JOBS_PER_LAUNCH;
+    for (int i = 0; i < m; i++) rb.j[i] = jobs[b + i];
+    ProfScope ps(PK_RED, s);
+    reduce_batch_kernel<<<m, 256, 0, s>>>(rb, out + b);
+    g_launches++;
+  }
+  return cuda_check("reduce_batch_kernel");
+}
+
+static bool have_device(void) {
+  int n = 0;
+  return cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
+}
+
+// one image: ARM + fused upsample/synthesis
+static int forward_one(const cc_model_desc& d, const int16_t* lat, const float* arm_w, const float* up_w,
+                       const float* syn_w, const float* image, float* x_hat, double* part, cudaStream_t s) {
+  ArmGeom ag;
+  arm_geom(d, ag);
+  SynGeom sg;
+  syn_geom(d, sg);
+  ArmLaunchFn arm = find_arm_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1);
+  SynLaunchFn syn = find_syn_launcher(d.L, d.syn_widths[1], d.syn_n_res, d.up_taps);
+  {
+    ProfScope ps(PK_ARM, s);
+    arm(ag, d, arm_w, lat, part, nullptr, nullptr, nullptr, s);
+  }
+  g_launches++;
+  int rc = cuda_check("arm_rate_kernel");
+  if (rc) return rc;
+  {
+    ProfScope ps(PK_SYN, s);
+    syn(sg, d, up_w, syn_w, lat, nullptr, image, x_hat, nullptr, nullptr, part + ag.tile_begin[d.L], s);
+  }
+  g_launches++;
+  return cuda_check("synth_kernel");
+}
+
+}  // namespace ccrd
+
+using namespace ccrd;
+
+extern "C" {
+
+const char* cc_version(void) { return "ccrd 0.1 (sm_100a)"; }
+
+const char* cc_strerror(int code) {
+  switch (code) {
+    case CC_OK: return "ok";
+    case CC_EINVAL: return "invalid argument";
+    case CC_ENOTSUP: return "not supported by the compiled kernels";
+    case CC_EWORKSPACE: return "workspace missing or too small";
+    case CC_ECUDA: return "CUDA error";
+    case CC_ENONFINITE: return "non-finite value";
+    default: return "unknown error";
+  }
+}
+
+const char* cc_last_error(void) { return g_err; }
+
+int cc_profile_begin(void) {
+  g_prof.on = true;
+  g_prof.n = 0;
+  g_prof.pool_used = 0;
+  return CC_OK;
+}
+
+int cc_profile_end(cc_profile_summary* out) {
+  ProfState& P = g_prof;
+  P.on = false;
+  if (!out) return fail(CC_EINVAL, "null summary");
+  memset(out, 0, sizeof(*out));
+  for (int i = 0; i < P.n; i++) {
+    if (cudaEventSynchronize(P.recs[i].b) != cudaSuccess) return cuda_check("cc_profile_end");
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, P.recs[i].a, P.recs[i].b);
+    switch (P.recs[i].kind) {
+      case PK_ARM: out->arm_ms += ms; out->arm_launches++; break;
+      case PK_SYN: out->syn_ms += ms; out->syn_launches++; break;
+      default: out->reduce_ms += ms; out->reduce_launches++; break;
+    }
+  }
+  P.n = 0;
+  P.pool_used = 0;
+  return cuda_check("cc_profile_end");
+}
+int64_t cc_last_launch_count(void) { return g_launches; }
+
+int cc_validate(const cc_model_desc* desc) { return validate(desc); }
+
+size_t cc_workspace_bytes(const cc_model_desc* desc, int32_t n_img) {
+  if (validate(desc) != CC_OK || n_img < 1) return 0;
+  return partial_bytes(*desc) * (size_t)n_img;
+}
+
+int cc_rd_forward(const cc_model_desc* desc, const cc_image_io* io, int32_t n_img, cc_rd_result* results,
+                  void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  int rc = validate(desc);
+  if (rc) return rc;
+  if (!io || n_img < 1 || !results) return fail(CC_EINVAL, "io/results null or n_img < 1");
+  const size_t per = partial_bytes(*desc);
+  if (!workspace || workspace_bytes < per * (size_t)n_img)
+    return fail(CC_EWORKSPACE, "need %zu workspace bytes, got %zu", per * (size_t)n_img, workspace_bytes);
+  for (int i = 0; i < n_img; i++)
+    if (!io[i].latents || !io[i].arm_w || !io[i].up_w || !io[i].syn_w)
+      return fail(CC_EINVAL, "image %d: null latents or weights", i);
+  if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
+  cudaStream_t s = (cudaStream_t)stream;
+  ReduceJob jobs[MAX_JOBS_PER_LAUNCH];
+  for (int b = 0; b < n_img; b += MAX_JOBS_PER_LAUNCH) {
+    const int m = (n_img - b < MAX_JOBS_PER_LAUNCH) ? n_img - b : MAX_JOBS_PER_LAUNCH;
+    for (int i = 0; i < m; i++) {
+      const cc_image_io& x = io[b + i];
+      double* part = (double*)((char*)workspace + per * (size_t)(b + i));
+      rc = forward_one(*desc, x.latents, x.arm_w, x.up_w, x.syn_w, x.image, x.x_hat, part, s);
+      if (rc) return rc;
+      jobs[i] = make_job(*desc, part);
+    }
+    rc = launch_reduce(jobs, m, results + b, s);
+    if (rc) return rc;
+  }
+  return CC_OK;
+}
+
+// ---------------------------------------------------------------- host path
+// Device workspace layout: [partials x n_img][results x n_img][2 staging slots:
+// latents | image | x_hat].
+static size_t stage_slot_bytes(const cc_model_desc& d) {
+  int64_t n_lat = 0;
+  LevelGeom g;
+  level_dims(d, g, &n_lat);
+  const size_t P = (size_t)d.H * d.W;
+  return align256(sizeof(int16_t) * (size_t)n_lat) + 2 * align256(sizeof(float) * 3 * P);
+}
+
+size_t cc_workspace_bytes_host(const cc_model_desc* desc, int32_t n_img) {
+  if (validate(desc) != CC_OK || n_img < 1) return 0;
+  return partial_bytes(*desc) * (size_t)n_img + align256(sizeof(cc_rd_result) * (size_t)n_img) +
+         2 * stage_slot_bytes(*desc);
+}
+
+int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t n_img, cc_rd_result* results,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  int rc = validate(desc);
+  if (rc) return rc;
+  if (!io || n_img < 1 || !results) return fail(CC_EINVAL, "io/results null or n_img < 1");
+  const cc_model_desc& d = *desc;
+  const size_t need = cc_workspace_bytes_host(desc, n_img);
+  if (!workspace || workspace_bytes < need)
+    return fail(CC_EWORKSPACE, "need %zu workspace bytes, got %zu", need, workspace_bytes);
+  if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
+  const size_t per = partial_bytes(d);
+  char* ws = (char*)workspace;
+  cc_rd_result* dres = (cc_rd_result*)(ws + per * (size_t)n_img);
+  char* stage = ws + per * (size_t)n_img + align256(sizeof(cc_rd_result) * (size_t)n_img);
+  const size_t slot = stage_slot_bytes(d);
+  int64_t n_lat = 0;
+  LevelGeom lg;
+  level_dims(d, lg, &n_lat);
+  const size_t P = (size_t)d.H * d.W;
+  const size_t lat_b = sizeof(int16_t) * (size_t)n_lat, img_b = sizeof(float) * 3 * P;
+
+  cudaStream_t s = (cudaStream_t)stream;
+  // copy stream + per-slot events: copies of image i+1 overlap compute of image i
+  cudaStream_t cs;
+  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return cuda_check("stream create");
+  cudaEvent_t copied[2], consumed[2];
+  for (int k = 0; k < 2; k++) {
+    cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&consumed[k], cudaEventDisableTiming);
+  }
+  // start the copy stream after whatever is already queued on s
+  cudaEventRecord(consumed[0], s);
+  cudaStreamWaitEvent(cs, consumed[0], 0);
+  cudaEventRecord(consumed[1], s);
+  ReduceJob* jobs = new ReduceJob[n_img];
+  for (int i = 0; i < n_img && rc == CC_OK; i++) {
+    const int k = i & 1;
+    char* base = stage + slot * (size_t)k;
+    int16_t* dlat = (int16_t*)base;
+    float* dimg = (float*)(base + align256(lat_b));
+    float* dxh = (float*)(base + align256(lat_b) + align256(img_b));
+    const cc_image_io& x = io[i];
+    if (!x.latents || !x.arm_w || !x.up_w || !x.syn_w) {
+      rc = fail(CC_EINVAL, "image %d: null latents or weights", i);
+      break;
+    }
+    cudaStreamWaitEvent(cs, consumed[k], 0);
+    cudaMemcpyAsync(dlat, x.latents, lat_b, cudaMemcpyHostToDevice, cs);
+    if (x.image) cudaMemcpyAsync(dimg, x.image, img_b, cudaMemcpyHostToDevice, cs);
+    cudaEventRecord(copied[k], cs);
+    cudaStreamWaitEvent(s, copied[k], 0);
+    double* part = (double*)(ws + per * (size_t)i);
+    rc = forward_one(d, dlat, x.arm_w, x.up_w, x.syn_w, x.image ? dimg : nullptr, x.x_hat ? dxh : nullptr, part,
+                     s);
+    if (rc) break;
+    if (x.x_hat) cudaMemcpyAsync(x.x_hat, dxh, img_b, cudaMemcpyDeviceToHost, s);
+    cudaEventRecord(consumed[k], s);
+    jobs[i] = make_job(d, part);
+  }
+  if (rc == CC_OK) rc = launch_reduce(jobs, n_img, dres, s);
+  if (rc == CC_OK) {
+    cudaMemcpyAsync(results, dres, sizeof(cc_rd_result) * (size_t)n_img, cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) rc = cuda_check("cc_rd_forward_host sync");
+  } else {
+    cudaStreamSynchronize(s);
+  }
+  cudaStreamSynchronize(cs);
+  delete[] jobs;
+  for (int k = 0; k < 2; k++) {
+    cudaEventDestroy(copied[k]);
+    cudaEventDestroy(consumed[k]);
+  }
+  cudaStreamDestroy(cs);
+  if (rc == CC_OK) rc = cuda_check("cc_rd_forward_host");
+  return rc;
+}
+
+// ---------------------------------------------------------------- stages
+int cc_arm_rate(const cc_model_desc* desc, const int16_t* latents, const float* arm_w, double* rate, float* mu,
+                float* scale, float* bits, void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  int rc = validate(desc);
+  if (rc) return rc;
+  if (!latents || !arm_w || !rate) return fail(CC_EINVAL, "null latents / arm_w / rate");
+  const size_t per = partial_bytes(*desc);
+  if (!workspace || workspace_bytes < per) return fail(CC_EWORKSPACE, "need %zu workspace bytes", per);
+  if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
+  if ((mu || scale) && !bits) return fail(CC_EINVAL, "mu/scale debug outputs need bits != NULL");
+  const cc_model_desc& d = *desc;
+  cudaStream_t s = (cudaStream_t)stream;
+  ArmGeom ag;
+  arm_geom(d, ag);
+  double* part = (double*)workspace;
+  find_arm_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1)(ag, d, arm_w, latents, part, mu, scale, bits, s);
+  g_launches++;
+  if ((rc = cuda_check("arm_rate_kernel"))) return rc;
+  // rate only: reduce with an empty synthesis partial set
+  ReduceJob j = make_job(d, part);
+  j.n_syn = 0;
+  cc_rd_result* tmp = (cc_rd_result*)((char*)workspace + per - align256(sizeof(cc_rd_result)));
+  if ((rc = launch_reduce(&j, 1, tmp, s))) return rc;
+  cudaMemcpyAsync(rate, &tmp->rate_bits, sizeof(double), cudaMemcpyDeviceToDevice, s);
+  return cuda_check("cc_arm_rate");
+}
+
+int cc_upsample(const cc_model_desc* desc, const int16_t* latents, const float* up_w, float* dense,
+                void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  int rc = validate(desc);
+  if (rc) return rc;
+  if (!latents || !up_w || !dense) return fail(CC_EINVAL, "null latents / up_w / dense");
+  (void)workspace;
+  (void)workspace_bytes;
+  if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
+  const cc_model_desc& d = *desc;
+  SynGeom sg;
+  syn_geom(d, sg);
+  // synthesis weights are irrelevant here: zero blob of the right size
+  const int CH = d.syn_widths[1];
+  const int nsyn = d.L * CH + CH + CH * 3 + 3 + 84 * d.syn_n_res;
+  float* zeros = new float[nsyn]();
+  find_syn_launcher(d.L, CH, d.syn_n_res, d.up_taps)(sg, d, up_w, zeros, latents, nullptr, nullptr, nullptr,
+                                                      dense, nullptr, nullptr, (cudaStream_t)stream);
+  delete[] zeros;
+  g_launches++;
+  return cuda_check("synth_kernel(dense_out)");
+}
+
+int cc_synthesize(const cc_model_desc* desc, const float* dense, const float* syn_w, const float* image,
+                  float* x_hat, double* sse, float* h_1x1, void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  int rc = validate(desc);
+  if (rc) return rc;
+  if (!dense || !syn_w) return fail(CC_EINVAL, "null dense / syn_w");
+  if (sse && !image) return fail(CC_EINVAL, "sse requested without image");
+  const cc_model_desc& d = *desc;
+  SynGeom sg;
+  syn_geom(d, sg);
+  const size_t need = align256(sizeof(double) * (size_t)sg.n_tiles) + sizeof(cc_rd_result);
+  if (sse && (!workspace || workspace_bytes < need)) return fail(CC_EWORKSPACE, "need %zu workspace bytes", need);
+  if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
+  cudaStream_t s = (cudaStream_t)stream;
+  double* part = sse ? (double*)workspace : nullptr;
+  find_syn_launcher(d.L, d.syn_widths[1], d.syn_n_res, d.up_taps)(sg, d, nullptr, syn_w, nullptr, dense, image,
+                                                                   x_hat, nullptr, h_1x1, part, s);
+  g_launches++;
+  if ((rc = cuda_check("synth_kernel(dense_in)"))) return rc;
+  if (sse) {
+    ReduceJob j = make_job(d, part);
+    j.n_arm = 0;
+    j.syn_partial = part;
+    cc_rd_result* tmp = (cc_rd_result*)((char*)workspace + align256(sizeof(double) * (size_t)sg.n_tiles));
+    if ((rc = launch_reduce(&j, 1, tmp, s))) return rc;
+    cudaMemcpyAsync(sse, &tmp->sse, sizeof(double), cudaMemcpyDeviceToDevice, s);
+  }
+  return cuda_check("cc_synthesize");
+}
+
+// ---------------------------------------------------------------- MAC count
+// Closed form: ARM sum_k in_k out_k per latent;
+// upsampling (K/2) MAC per produced sample of every separable pass; synthesis
+// sum in out + 81 R per pixel.  Biases and residual adds are free.
+double cc_mac_per_pixel(const cc_model_desc* desc, cc_mac_breakdown* out) {
+  if (validate(desc) != CC_OK) return -1.0;
+  const cc_model_desc& d = *desc;
+  LevelGeom g;
+  int64_t n_lat = 0;
+  level_dims(d, g, &n_lat);
+  int64_t arm_pl = 0;
+  for (int k = 0; k < d.arm_n_layers; k++) arm_pl += (int64_t)d.arm_widths[k] * d.arm_widths[k + 1];
+  const int64_t arm = arm_pl * n_lat;
+  int64_t up = 0;
+  for (int l = 1; l < d.L; l++)
+    for (int j = 0; j < l; j++)
+      up += (int64_t)(d.up_taps / 2) * ((int64_t)g.h[j + 1] * g.w[j] + (int64_t)g.h[j] * g.w[j]);
+  int64_t syn_pp = 81 * (int64_t)d.syn_n_res;
+  for (int k = 0; k < d.syn_n_1x1; k++) syn_pp += (int64_t)d.syn_widths[k] * d.syn_widths[k + 1];
+  const int64_t P = (int64_t)d.H * d.W;
+  const int64_t syn = syn_pp * P;
+  const double tot = (double)(arm + up + syn) / (double)P;
+  if (out) {
+    out->arm = (double)arm / P;
+    out->up = (double)up / P;
+    out->syn = (double)syn / P;
+    out->total = tot;
+    out->arm_macs = arm;
+    out->up_macs = up;
+    out->syn_macs = syn;
+    out->n_latents = n_lat;
+  }
+  return tot;
+}
+
+}  // extern "C"

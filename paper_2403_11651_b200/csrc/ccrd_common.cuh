@@ -1,0 +1,165 @@
+// ccrd_common.cuh -- shared device helpers and launch-parameter records of the
+// CUDA product path.  Nothing here is shared with oracle/ (independent code).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/ccrd.h"
+
+namespace ccrd {
+
+// ---------------------------------------------------------------- FFMA2 helpers
+// sm_100a has a packed fp32 FMA (PTX fma.rn.f32x2, SASS FFMA2): one warp
+// instruction performs 64 FMAs and occupies the FMA pipe for two cycles, so the
+// issue slot it frees carries the loads, ReLUs and index math.  Measured on the
+// B200 (tools/microbench/ffma_probe.cu): 126.9 FMA/clk/SM with FFMA2 vs 111-124
+// with scalar FFMA.  Rounding is identical to fmaf (round-to-nearest, fused).
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2unpack(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+// 64-bit view of a float2 stored in the kernel parameter bank
+__device__ __forceinline__ uint64_t ldp2(const float2& v) {
+  return *reinterpret_cast<const uint64_t*>(&v);
+}
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
+
+// Block-wide deterministic sum of one fp32 value per thread -> fp64 (thread 0).
+template <int NT>
+__device__ __forceinline__ double block_sum(float v, double* warp_buf) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) warp_buf[wid] = (double)v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 0; w < NT / 32; w++) s += warp_buf[w];
+  }
+  return s;
+}
+
+// ------------------------------------------------------------------ geometry
+struct LevelGeom {
+  int32_t h[CC_MAX_LEVELS];
+  int32_t w[CC_MAX_LEVELS];
+  int64_t off[CC_MAX_LEVELS];  // element offset of level l in the packed pyramid
+};
+
+// ARM tiling: one CTA = 8 rows x 32 latents of one grid (one warp per row).
+constexpr int ARM_TX = 32;
+constexpr int ARM_TY = 8;
+constexpr int ARM_THREADS = ARM_TX * ARM_TY;
+constexpr int ARM_HALO_TOP = 3;  // dy >= -3
+constexpr int ARM_HALO_X = 4;    // |dx| <= 4
+constexpr int ARM_SW = ARM_TX + 2 * ARM_HALO_X;
+constexpr int ARM_SH = ARM_TY + ARM_HALO_TOP;
+
+struct ArmGeom {
+  LevelGeom lv;
+  int32_t L;
+  int32_t tiles_x[CC_MAX_LEVELS];
+  int32_t tile_begin[CC_MAX_LEVELS + 1];  // prefix over levels; [L] = total CTAs
+  int32_t ctx_off[CC_MAX_CTX];            // dy * ARM_SW + dx (shared-memory offsets)
+  float lsmin, lsmax;                     // log-scale clamp
+  float p_floor;                          // probability floor
+  float bits_cap;                         // -log2(p_floor)
+};
+
+// ARM weights packed for FFMA2: for input i, the pair (out 2n, out 2n+1).
+// Residual layers are folded on the host (W' = W + I: LinR computes
+// ReLU(W z + b + z) = ReLU(W' z + b)).
+template <int C, int NH, int NHL>
+struct ArmWeights {
+  float2 w0[C][NH / 2];
+  float2 b0[NH / 2];
+  float2 wh[(NHL > 1) ? (NHL - 1) : 1][NH][NH / 2];
+  float2 bh[(NHL > 1) ? (NHL - 1) : 1][NH / 2];
+  float2 wo[NH];  // (mu, log-scale) pair per input
+  float2 bo;
+};
+
+template <int C, int NH, int NHL>
+struct ArmParams {
+  ArmGeom g;
+  const int16_t* lat;
+  double* partial;  // [n CTAs] per-CTA rate partial sums
+  float* mu;        // optional per-latent debug outputs
+  float* scale;
+  float* bits;
+  ArmWeights<C, NH, NHL> w;
+};
+
+// Synthesis tiling: one CTA = 32 x 64 output pixels, 256 threads.
+constexpr int SYN_TH = 32;
+constexpr int SYN_TW = 64;
+constexpr int SYN_THREADS = 256;
+
+template <int L, int CH, int R, int K>
+struct SynWeights {
+  float k[K];                 // upsampling taps
+  float2 A0[L][CH / 2];       // 1x1 layer 0, pairs of outputs per input
+  float2 a0[CH / 2];
+  float2 A1p[CH];             // 1x1 layer 1 outputs (0, 1) per input
+  float A1s[CH];              // 1x1 layer 1 output 2 per input
+  float a1[3];
+  float2 Gp[(R > 0) ? R : 1][3][3][3];  // residual 3x3: (co 0, co 1) per [ci][ky][kx]
+  float Gs[(R > 0) ? R : 1][3][3][3];   // co 2
+  float g[(R > 0) ? R : 1][3];
+};
+
+struct SynGeom {
+  LevelGeom lv;
+  int32_t H, W;
+  int32_t tiles_x, n_tiles;
+};
+
+template <int L, int CH, int R, int K>
+struct SynParams {
+  SynGeom g;
+  const int16_t* lat;      // latents (chain mode)
+  const float* dense_in;   // [L][H][W] (synthesize-from-dense mode) or null
+  const float* image;      // [3][H][W] or null
+  float* x_hat;            // [3][H][W] or null
+  float* dense_out;        // debug [L][H][W] or null
+  float* h1_out;           // debug [3][H][W] or null
+  double* partial;         // [n tiles] per-CTA SSE partial sums
+  SynWeights<L, CH, R, K> w;
+};
+
+// Reduction of per-CTA partials into per-image results (deterministic, fp64).
+struct ReduceJob {
+  const double* arm_partial;
+  int32_t n_arm;
+  const double* syn_partial;
+  int32_t n_syn;
+  double inv_3p, lambda_over_p;
+};
+
+// Host-side launchers (defined in arm_rate.cu / synth.cu).
+typedef int (*ArmLaunchFn)(const ArmGeom& g, const cc_model_desc& d, const float* arm_w,
+                           const int16_t* lat, double* partial, float* mu, float* scale,
+                           float* bits, cudaStream_t s);
+typedef int (*SynLaunchFn)(const SynGeom& g, const cc_model_desc& d, const float* up_w,
+                           const float* syn_w, const int16_t* lat, const float* dense_in,
+                           const float* image, float* x_hat, float* dense_out, float* h1_out,
+                           double* partial, cudaStream_t s);
+
+ArmLaunchFn find_arm_launcher(int C, int NH, int NHL);
+SynLaunchFn find_syn_launcher(int L, int CH, int R, int K);
+
+}  // namespace ccrd

@@ -1,0 +1,245 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle, element by
+element on the same seeded inputs.
+
+Tolerances (north_star):
+  * x_hat: 1e-5 absolute per pixel;
+  * total rate bits and MSE: 1e-4 relative (expected ~1e-7);
+  * per-latent bits: 1e-3 absolute (fast-intrinsic Laplace; expected ~1e-5);
+    mu: 1e-5 absolute + 1e-5 relative;
+  * dense upsampled tensor: per level 1e-5 relative to the level's max |value|.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle
+import workload
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _P():
+    import paper_2403_11651_b200 as P
+    return P
+
+
+def run_forward(cfg, images, with_xhat=True):
+    P = _P()
+    b = P.DeviceBatch(cfg, images, with_xhat=with_xhat)
+    res = b.forward()
+    torch.cuda.synchronize()
+    out = res.cpu().numpy()
+    xh = [t.cpu().numpy() for t in b.xhat] if with_xhat else None
+    return out, xh
+
+
+def check_image(cfg, im, res_row, xh, tol_px=1e-5):
+    ref = oracle.rd_forward_image(cfg, im, want_xhat=True)
+    assert abs(res_row[0] - ref["rate_bits"]) <= 1e-4 * ref["rate_bits"], (res_row[0], ref["rate_bits"])
+    assert abs(res_row[2] - ref["mse"]) <= 1e-4 * ref["mse"], (res_row[2], ref["mse"])
+    assert abs(res_row[1] - ref["sse"]) <= 1e-4 * ref["sse"]
+    assert abs(res_row[3] - ref["cost"]) <= 1e-4 * ref["cost"]
+    if xh is not None:
+        err = np.abs(xh.astype(np.float64) - ref["x_hat"]).max()
+        assert err <= tol_px, f"max |x_hat - oracle| = {err}"
+    return ref
+
+
+@pytest.mark.parametrize("name", ["tiny", "low", "ref"])
+@pytest.mark.parametrize("filt", ["random", "lanczos2"])
+def test_rd_forward_configs(name, filt):
+    cfg = workload.CONFIGS[name]
+    im = workload.make_image(cfg, 100, filter_kind=filt)
+    out, xh = run_forward(cfg, [im])
+    check_image(cfg, im, out[0], xh[0])
+
+
+@pytest.mark.parametrize("H,W,L,res,taps", [
+    (37, 53, 5, 1, 8), (37, 53, 5, 1, 4), (33, 97, 4, 1, 8), (65, 129, 4, 3, 8), (64, 64, 4, 0, 8),
+    (1, 1, 1, 1, 8), (3, 300, 2, 1, 8), (300, 3, 2, 1, 8), (5, 5, 2, 1, 8), (31, 63, 3, 1, 8),
+])
+def test_rd_forward_odd_shapes(H, W, L, res, taps):
+    cfg = workload.CONFIGS["tiny"].replace(H=H, W=W, L=L, syn_widths=(L, 8, 3), syn_n_res=res, up_taps=taps)
+    im = workload.make_image(cfg, 7, filter_kind="lanczos2" if taps == 8 else "random")
+    out, xh = run_forward(cfg, [im])
+    check_image(cfg, im, out[0], xh[0])
+
+
+def test_table1_shapes():
+    """Table 1 ARM / synthesis widths (separable TConv reading) on a ragged size."""
+    base = workload.CONFIGS["ref"]
+    for key, a in workload.TABLE1.items():
+        aw = a["arm"]
+        cfg = base.replace(H=71, W=133, n_ctx=aw[0], arm_widths=aw, syn_widths=a["syn"],
+                           syn_n_res=a["syn_n_res"], up_taps=a["up_kernel"])
+        im = workload.make_image(cfg, key)
+        out, xh = run_forward(cfg, [im])
+        check_image(cfg, im, out[0], xh[0])
+
+
+def test_batch_has_per_image_weights():
+    cfg = workload.CONFIGS["ref"].replace(H=96, W=160)
+    ims = workload.make_batch(cfg, [11, 12, 13])
+    out, xh = run_forward(cfg, ims)
+    for i, im in enumerate(ims):
+        check_image(cfg, im, out[i], xh[i])
+    assert len({round(r, 6) for r in out[:, 0]}) == 3
+
+
+def test_arm_stage_per_latent():
+    P = _P()
+    for name, H, W in [("tiny", 64, 64), ("ref", 70, 101), ("low", 53, 37)]:
+        cfg = workload.CONFIGS[name].replace(H=H, W=W)
+        im = workload.make_image(cfg, 5)
+        d = P.desc_from_config(cfg)
+        lat = torch.from_numpy(im.latents).cuda()
+        n = im.latents.size
+        mu, sc, bits = (torch.zeros(n, device="cuda") for _ in range(3))
+        rate = torch.zeros(1, dtype=torch.float64, device="cuda")
+        ws_b = P.cc_workspace_bytes(d, 1)
+        ws = torch.empty(ws_b, dtype=torch.uint8, device="cuda")
+        P.cc_arm_rate(d, lat.data_ptr(), im.arm_w, rate.data_ptr(), mu.data_ptr(), sc.data_ptr(),
+                      bits.data_ptr(), ws.data_ptr(), ws_b, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        R, mu_o, b_o, bits_o, _ = oracle.rate(oracle.model(cfg), im.latents, im.arm_w, per_latent=True)
+        np.testing.assert_allclose(mu.cpu().numpy(), mu_o, rtol=1e-5, atol=1e-5)
+        np.testing.assert_allclose(sc.cpu().numpy(), b_o, rtol=1e-5, atol=0)
+        np.testing.assert_allclose(bits.cpu().numpy(), bits_o, rtol=0, atol=1e-3)
+        assert abs(rate.item() - R) <= 1e-5 * R
+
+
+def test_arm_stage_logscale_clamps_and_floor():
+    """Push the log-scale output past both clamps and latents far into the
+    tails (probability floor): per-latent bits still match."""
+    P = _P()
+    cfg = workload.CONFIGS["tiny"].replace(lat_scale=6.0, lat_clip=60)
+    im = workload.make_image(cfg, 9)
+    for bias_s in (12.0, -12.0, 3.0):
+        aw = im.arm_w.copy()
+        aw[-1] = bias_s
+        d = P.desc_from_config(cfg)
+        lat = torch.from_numpy(im.latents).cuda()
+        n = im.latents.size
+        bits = torch.zeros(n, device="cuda")
+        rate = torch.zeros(1, dtype=torch.float64, device="cuda")
+        ws_b = P.cc_workspace_bytes(d, 1)
+        ws = torch.empty(ws_b, dtype=torch.uint8, device="cuda")
+        P.cc_arm_rate(d, lat.data_ptr(), aw, rate.data_ptr(), 0, 0, bits.data_ptr(), ws.data_ptr(), ws_b, 0)
+        torch.cuda.synchronize()
+        R, _, _, bits_o, _ = oracle.rate(oracle.model(cfg), im.latents, aw, per_latent=True)
+        np.testing.assert_allclose(bits.cpu().numpy(), bits_o, rtol=0, atol=1e-3)
+        assert abs(rate.item() - R) <= 1e-5 * R
+
+
+@pytest.mark.parametrize("filt", ["random", "lanczos2"])
+def test_upsample_stage_per_level(filt):
+    P = _P()
+    for name, H, W in [("tiny", 64, 64), ("ref", 75, 141), ("ref", 128, 64)]:
+        cfg = workload.CONFIGS[name].replace(H=H, W=W)
+        im = workload.make_image(cfg, 21, filter_kind=filt)
+        d = P.desc_from_config(cfg)
+        lat = torch.from_numpy(im.latents).cuda()
+        dense = torch.zeros((cfg.L, H, W), device="cuda")
+        P.cc_upsample(d, lat.data_ptr(), im.up_w, dense.data_ptr())
+        torch.cuda.synchronize()
+        ref, _ = oracle.upsample(oracle.model(cfg), im.latents, im.up_w)
+        got = dense.cpu().numpy().astype(np.float64)
+        for l in range(cfg.L):
+            scale = max(np.abs(ref[l]).max(), 1e-30)
+            err = np.abs(got[l] - ref[l]).max() / scale
+            assert err <= 1e-5, f"level {l}: rel err {err}"
+
+
+def test_synthesize_stage_from_dense():
+    P = _P()
+    cfg = workload.CONFIGS["ref"].replace(H=77, W=130)
+    im = workload.make_image(cfg, 31)
+    m = oracle.model(cfg)
+    dense_o, _ = oracle.upsample(m, im.latents, im.up_w)
+    dense32 = dense_o.astype(np.float32)
+    xh_o, h1_o, _ = oracle.synthesis(m, dense32.astype(np.float64), im.syn_w)
+    d = P.desc_from_config(cfg)
+    dense = torch.from_numpy(dense32).cuda()
+    img = torch.from_numpy(im.image).cuda()
+    xh = torch.zeros((3, 77, 130), device="cuda")
+    h1 = torch.zeros((3, 77, 130), device="cuda")
+    sse = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ws_b = P.cc_workspace_bytes(d, 1)
+    ws = torch.empty(ws_b, dtype=torch.uint8, device="cuda")
+    P.cc_synthesize(d, dense.data_ptr(), im.syn_w, img.data_ptr(), xh.data_ptr(), sse.data_ptr(), h1.data_ptr(),
+                    ws.data_ptr(), ws_b)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(h1.cpu().numpy(), h1_o, rtol=0, atol=1e-5)
+    np.testing.assert_allclose(xh.cpu().numpy(), xh_o, rtol=0, atol=1e-5)
+    sse_o = ((im.image.astype(np.float64) - xh_o) ** 2).sum()
+    assert abs(sse.item() - sse_o) <= 1e-5 * sse_o
+
+
+def test_deterministic_and_host_path_match():
+    P = _P()
+    cfg = workload.CONFIGS["ref"].replace(H=200, W=300)
+    ims = workload.make_batch(cfg, [41, 42])
+    a, xa = run_forward(cfg, ims)
+    b, xb = run_forward(cfg, ims)
+    np.testing.assert_array_equal(a, b)
+    for u, v in zip(xa, xb):
+        np.testing.assert_array_equal(u, v)
+    # end-to-end host-buffer path: identical numbers
+    d = P.desc_from_config(cfg)
+    lat = [torch.from_numpy(im.latents).pin_memory() for im in ims]
+    img = [torch.from_numpy(im.image).pin_memory() for im in ims]
+    xh = [torch.empty_like(t).pin_memory() for t in img]
+    io = [P.CcImageIO(lat[i].data_ptr(), ims[i].arm_w.ctypes.data, ims[i].up_w.ctypes.data,
+                      ims[i].syn_w.ctypes.data, img[i].data_ptr(), xh[i].data_ptr()) for i in range(2)]
+    ws_b = P.cc_workspace_bytes_host(d, 2)
+    ws = torch.empty(ws_b, dtype=torch.uint8, device="cuda")
+    res = np.zeros((2, 4))
+    P.cc_rd_forward_host(d, io, res, ws.data_ptr(), ws_b, torch.cuda.current_stream().cuda_stream)
+    np.testing.assert_array_equal(res, a)
+    for i in range(2):
+        np.testing.assert_array_equal(xh[i].numpy(), xa[i])
+
+
+@pytest.mark.slow
+def test_full_size_2k_batch():
+    """BASELINE.json configs[3] image size, two images through the same
+    cc_rd_forward call bench.py times (all outputs vs the oracle)."""
+    cfg = workload.CONFIGS["batched2k"]
+    ims = workload.make_batch(cfg, [workload.image_seed(0, 0), workload.image_seed(0, 1)])
+    oracle.set_threads(max(1, min(32, __import__("os").cpu_count() or 1)))
+    out, xh = run_forward(cfg, ims)
+    for i, im in enumerate(ims):
+        check_image(cfg, im, out[i], xh[i])
+
+
+@pytest.mark.slow
+def test_full_size_8k_sampled_rows():
+    """BASELINE.json configs[4] size: per-latent bits on sampled rows of every
+    level (oracle evaluated row by row) and the total rate / MSE invariants."""
+    P = _P()
+    cfg = workload.CONFIGS["8k"]
+    im = workload.make_image(cfg, 8)
+    d = P.desc_from_config(cfg)
+    lat = torch.from_numpy(im.latents).cuda()
+    n = im.latents.size
+    bits = torch.zeros(n, device="cuda")
+    rate = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ws_b = P.cc_workspace_bytes(d, 1)
+    ws = torch.empty(ws_b, dtype=torch.uint8, device="cuda")
+    P.cc_arm_rate(d, lat.data_ptr(), im.arm_w, rate.data_ptr(), 0, 0, bits.data_ptr(), ws.data_ptr(), ws_b, 0)
+    torch.cuda.synchronize()
+    bits_np = bits.cpu().numpy()
+    m = oracle.model(cfg)
+    dims = cfg.level_dims()
+    off = 0
+    rng = np.random.default_rng(0)
+    for l, (h, w) in enumerate(dims):
+        for r in sorted(set([0, 1, 2, h - 1] + list(rng.integers(0, h, 3)))):
+            _, ob = oracle.rate_rows(m, im.latents, im.arm_w, l, r, r + 1)
+            np.testing.assert_allclose(bits_np[off + r * w: off + (r + 1) * w], ob[0], rtol=0, atol=1e-3)
+        off += h * w
+    # total rate = fp64 sum of the per-latent bits the kernel produced
+    assert abs(rate.item() - bits_np.astype(np.float64).sum()) <= 1e-6 * rate.item()
