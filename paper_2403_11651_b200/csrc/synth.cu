@@ -3,285 +3,492 @@
 // One CTA produces a 32 x 64 tile of x_hat ("upsample the
 // latents to a dense representation and synthesize the decoded image";
 // Table 1 upsampling / synthesis columns; Eq. 1 distortion):
-//   1. upsampling chain in shared memory, coarse to fine: the stack of grids
-//      l >= j is carried at resolution j over the window the tile needs, each
-//      x2 step a separable stride-2 transposed conv (horizontal pass, then
-//      vertical pass; replicate padding = index clamping, crop = never
-//      computing past the next level's size);
-//   2. per pixel of the tile + R-pixel halo: the last vertical step and the
-//      L -> C_h -> 3 1x1 MLP in registers (packed FFMA2, two neurons per
-//      instruction), result to shared memory;
-//   3. R residual 3x3 layers on shared memory (replicate padding at the image
-//      border; the halo is recomputed, never exchanged);
-//   4. x_hat store (optional) and (x - x_hat)^2 partial sums -> fp64 per CTA.
+//   1. upsampling chain in shared memory, coarse to fine.  The stack of grids
+//      l >= j is carried at resolution j over the window the tile needs; each
+//      x2 step is a separable stride-2 transposed conv (horizontal pass, then
+//      vertical pass).  Windows are NOT clipped to the grid: entries outside
+//      it hold the replicated edge value (replicate padding), so the taps
+//      never clamp; crop = never producing past the next level's size.
+//   2. per PAIR of rows (2q, 2q+1) of the tile + halo: the last vertical step
+//      (both phases share the K/2 + 1 source rows) and the L -> C_h -> 3 1x1
+//      MLP for both pixels in registers (packed FFMA2, two neurons per
+//      instruction, each uniform weight load feeding two pixels).
+//   3. residual 3x3 layers: each thread slides a 3-row register window down a
+//      column segment (9 shared loads per output); the halo ring of the
+//      non-last layers is recomputed, never exchanged; replicate padding at
+//      the image border is index clamping.
+//   4. the last layer's output goes straight from registers to x_hat
+//      (optional) and the (x - x_hat)^2 partial sum -> fp64 per CTA.
 // The dense L x H x W tensor is never materialised in HBM.
 #include "ccrd_common.cuh"
 
 namespace ccrd {
 
+// Window sizes of the upsampling chain (compile time).  Level 0's window is the
+// tile + an even halo RE; level j+1's window starts at ((lo_j >> 1) - K/4)
+// rounded down to even and holds n_j/2 + K/2 + 1 entries rounded up to even --
+// every source index the x2 step from level j+1 to level j touches.
+template <int K>
+__host__ __device__ constexpr int wnext(int n) {
+  return ((n / 2 + K / 2 + 1) + 1) & ~1;
+}
+template <int K>
+__host__ __device__ constexpr int wsize(int n0, int j) {
+  return j == 0 ? n0 : wnext<K>(wsize<K>(n0, j - 1));
+}
+
 template <int L, int CH, int R, int K>
 struct SynShape {
-  static constexpr int RH0 = SYN_TH + 2 * R;  // rows of the level-0 region (tile + halo)
-  static constexpr int RW0 = SYN_TW + 2 * R;
-  static constexpr int MR1 = RH0 / 2 + 6;     // bound on window rows at levels >= 1
-  static constexpr int MC1 = RW0 / 2 + 6;
+  static constexpr int RE = 2 * ((R + 1) / 2);   // even halo of the level-0 region
+  static constexpr int RH0 = SYN_TH + 2 * RE;    // level-0 region rows
+  static constexpr int RW0 = SYN_TW + 2 * RE;    // level-0 region cols
+  static constexpr int NR1 = wsize<K>(RH0, 1);   // level-1 window (largest of levels >= 1)
+  static constexpr int NC1 = wsize<K>(RW0, 1);
   static constexpr int NS = (L > 1) ? (L - 1) : 1;  // stack slots (levels 1..L-1)
-  static constexpr int STACK = NS * MR1 * MC1;
+  static constexpr int SLOT = NR1 * NC1;            // stack slot (floats)
+  static constexpr int TSLOT = NR1 * RW0;           // tmph slot (floats)
+  static constexpr int STACK = NS * SLOT;
   static constexpr int HBUF = 3 * RH0 * RW0;
-  static constexpr int BUF_A = (STACK > HBUF) ? STACK : HBUF;          // stack | h (ping)
-  static constexpr int TMPH = NS * MR1 * RW0;
-  static constexpr int BUF_B = (TMPH > HBUF) ? TMPH : HBUF;            // tmpH | h (pong)
-  static constexpr size_t SMEM = sizeof(float) * (size_t)(BUF_A + BUF_B);
+  static constexpr int BUF_A = (STACK > HBUF) ? STACK : HBUF;  // stack | h (ping)
+  static constexpr int TMPH = NS * TSLOT;
+  static constexpr int BUF_B = (TMPH > HBUF) ? TMPH : HBUF;    // tmph  | h (pong)
+  static constexpr int LAT0 = ((RH0 * RW0 + 1) / 2);           // int16 level-0 region, in floats
+  static constexpr size_t SMEM = sizeof(float) * (size_t)(BUF_A + BUF_B + LAT0);
+  static constexpr int NWARPS = SYN_THREADS / 32;
+  static constexpr int SEGS = SYN_THREADS / SYN_TW;            // column segments per tile column
+  static constexpr int RS = SYN_TH / SEGS;                      // rows per segment
+  static_assert(SYN_THREADS % SYN_TW == 0 && SYN_TH % SEGS == 0, "conv mapping");
+  static_assert(SYN_TH % 2 == 0 && SYN_TW % 2 == 0, "even tiles");
 };
 
-struct Win {
-  int r_lo, r_hi, c_lo, c_hi;  // inclusive window of a level
+struct SynCtx {
+  float* stack;   // [slot][NR_j][NC_j]      (slot = level - 1)
+  float* tmph;    // [slot][NR_{j+1}][NC_j]
+  int* wlo_r;     // window origins (shared), per level
+  int* wlo_c;
 };
 
-// out[2q + r] = sum_t k[2t + 1 - r] * g[clamp(q + r + K/4 - 1 - t)]
-// (stride-2 transposed conv on the replicate-extended input, DESIGN.md
-//  readings #12-#13; the oracle evaluates the same definition as a scatter).
-template <int K>
-__device__ __forceinline__ float up_tap(const float* __restrict__ kk, const float* src, int stride,
-                                        int o, int n_src, int lo_src) {
-  const int q = o >> 1, par = o & 1;
-  float acc = 0.0f;
-#pragma unroll
-  for (int t = 0; t < K / 2; t++) {
-    const int idx = clampi(q + par + K / 4 - 1 - t, 0, n_src - 1) - lo_src;
-    acc = fmaf(kk[2 * t + 1 - par], src[idx * stride], acc);
+// replicate-extended window of grid LEV into stack slot LEV - 1
+template <int L, int CH, int R, int K, int LEV>
+__device__ __forceinline__ void load_window(const SynParams<L, CH, R, K>& p, const SynCtx& c) {
+  using S = SynShape<L, CH, R, K>;
+  constexpr int NR = wsize<K>(S::RH0, LEV), NC = wsize<K>(S::RW0, LEV);
+  const int16_t* g = p.lat + p.g.lv.off[LEV];
+  const int gh = p.g.lv.h[LEV], gw = p.g.lv.w[LEV];
+  const int lr = c.wlo_r[LEV], lc = c.wlo_c[LEV];
+  float* dst = c.stack + (LEV - 1) * S::SLOT;
+#pragma unroll 1
+  for (int it = threadIdx.x; it < NR * NC; it += SYN_THREADS) {
+    const int rr = it / NC, cc = it - rr * NC;
+    dst[it] = (float)__ldg(g + (int64_t)clampi(lr + rr, 0, gh - 1) * gw + clampi(lc + cc, 0, gw - 1));
   }
-  return acc;
 }
+
+// One x2 step of the chain, from level J+1 to level J, for every grid l > J
+// (stack slots J .. L-2).  out[2q + r] = sum_t k[2t + 1 - r] g[q + r + K/4 - 1 - t]
+// (stride-2 transposed conv on the replicate-extended input, DESIGN.md readings
+// #12-#13): the even and odd outputs share the K/2 + 1 sources
+// g[q - K/4 .. q + K/4]; replicate padding = clamping the SOURCE index.
+template <int L, int CH, int R, int K, int J>
+struct ChainStep {
+  using S = SynShape<L, CH, R, K>;
+  static constexpr int NRs = wsize<K>(S::RH0, J + 1), NCs = wsize<K>(S::RW0, J + 1);  // source window
+  static constexpr int NRd = wsize<K>(S::RH0, J), NCd = wsize<K>(S::RW0, J);          // dest window
+  static constexpr int NSL = L - 1 - J;
+
+  static __device__ __forceinline__ void run(const SynParams<L, CH, R, K>& p, const SynCtx& c) {
+    const float* kk = p.w.k;
+    // ---- horizontal: (rows of window J+1) x (cols of window J), column pairs
+    {
+      constexpr int NCP = NCd / 2;
+      constexpr int NRG = SYN_THREADS / NCP;
+      const int cp = threadIdx.x % NCP, rg = threadIdx.x / NCP;
+      if (rg < NRG) {
+        const int q = (c.wlo_c[J] >> 1) + cp;  // (lo_c[J] + 2 cp) / 2; lo_c[J] even
+        const int ws = p.g.lv.w[J + 1], lo_s = c.wlo_c[J + 1];
+        int off[K / 2 + 1];
+#pragma unroll
+        for (int u = 0; u <= K / 2; u++) off[u] = clampi(q - K / 4 + u, 0, ws - 1) - lo_s;
+#pragma unroll 2
+        for (int k = rg; k < NSL * NRs; k += NRG) {
+          const int sl = k / NRs, row = k - sl * NRs;
+          const float* src = c.stack + (J + sl) * S::SLOT + row * NCs;
+          float sv[K / 2 + 1];
+#pragma unroll
+          for (int u = 0; u <= K / 2; u++) sv[u] = src[off[u]];
+          float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+          for (int t = 0; t < K / 2; t++) {
+            a0 = fmaf(kk[2 * t + 1], sv[K / 2 - 1 - t], a0);
+            a1 = fmaf(kk[2 * t], sv[K / 2 - t], a1);
+          }
+          *reinterpret_cast<float2*>(c.tmph + (J + sl) * S::TSLOT + row * NCd + 2 * cp) = make_float2(a0, a1);
+        }
+      }
+    }
+    __syncthreads();
+    if constexpr (J > 0) {
+      // ---- vertical: (rows of window J) x (cols of window J); each thread
+      //      slides a (K/2 + 1)-row register window down one column
+      const int hs = p.g.lv.h[J + 1], lo_s = c.wlo_r[J + 1];
+      const int q0 = c.wlo_r[J] >> 1;
+#pragma unroll 1
+      for (int it = threadIdx.x; it < NSL * NCd; it += SYN_THREADS) {
+        const int sl = it / NCd, col = it - sl * NCd;
+        const float* src = c.tmph + (J + sl) * S::TSLOT + col;
+        float* dst = c.stack + (J + sl) * S::SLOT + col;
+        float sv[K / 2 + 1];
+#pragma unroll
+        for (int u = 0; u < K / 2; u++) sv[u] = src[(clampi(q0 - K / 4 + u, 0, hs - 1) - lo_s) * NCd];
+#pragma unroll 2
+        for (int rp = 0; rp < NRd / 2; rp++) {
+          const int q = q0 + rp;
+          sv[K / 2] = src[(clampi(q + K / 4, 0, hs - 1) - lo_s) * NCd];
+          float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+          for (int t = 0; t < K / 2; t++) {
+            a0 = fmaf(kk[2 * t + 1], sv[K / 2 - 1 - t], a0);
+            a1 = fmaf(kk[2 * t], sv[K / 2 - t], a1);
+          }
+          dst[(2 * rp) * NCd] = a0;
+          dst[(2 * rp + 1) * NCd] = a1;
+#pragma unroll
+          for (int u = 0; u < K / 2; u++) sv[u] = sv[u + 1];
+        }
+      }
+      // grid J joins the stack (slot J - 1) at its own resolution
+      load_window<L, CH, R, K, J>(p, c);
+      __syncthreads();
+      ChainStep<L, CH, R, K, J - 1>::run(p, c);
+    }
+  }
+
+};
 
 template <int L, int CH, int R, int K, bool DENSE_IN>
 __global__ void __launch_bounds__(SYN_THREADS, 2)
     synth_kernel(const __grid_constant__ SynParams<L, CH, R, K> p) {
   using S = SynShape<L, CH, R, K>;
+  constexpr int RE = S::RE, RH0 = S::RH0, RW0 = S::RW0;
+  constexpr int HP = RH0 * RW0;
   extern __shared__ float smem[];
   float* bufA = smem;
   float* bufB = smem + S::BUF_A;
-  __shared__ Win win[CC_MAX_LEVELS];
+  int16_t* lat0 = reinterpret_cast<int16_t*>(smem + S::BUF_A + S::BUF_B);  // [RH0][RW0]
+  __shared__ int wlo_r[CC_MAX_LEVELS], wlo_c[CC_MAX_LEVELS];
   __shared__ double warp_buf[SYN_THREADS / 32];
 
   const int H = p.g.H, W = p.g.W;
   const int ty = blockIdx.x / p.g.tiles_x;
   const int tx = blockIdx.x - ty * p.g.tiles_x;
   const int Y0 = ty * SYN_TH, X0 = tx * SYN_TW;
-  const int Y1 = min(H, Y0 + SYN_TH), X1 = min(W, X0 + SYN_TW);
-  // level-0 region: tile + R halo, clamped to the image
-  const int r0 = max(0, Y0 - R), r1 = min(H, Y1 + R);
-  const int c0 = max(0, X0 - R), c1 = min(W, X1 + R);
-  const int nr0 = r1 - r0, nc0 = c1 - c0;
+  const int RY = Y0 - RE, RX = X0 - RE;  // origin of the level-0 region (even)
 
-  if (threadIdx.x == 0) {
-    Win v{r0, r1 - 1, c0, c1 - 1};
-    win[0] = v;
-    for (int j = 1; j < L; j++) {
-      v.r_lo = max(0, (v.r_lo >> 1) - K / 4);
-      v.r_hi = min(p.g.lv.h[j] - 1, (v.r_hi >> 1) + K / 4);
-      v.c_lo = max(0, (v.c_lo >> 1) - K / 4);
-      v.c_hi = min(p.g.lv.w[j] - 1, (v.c_hi >> 1) + K / 4);
-      win[j] = v;
+  if (threadIdx.x < 32) {
+    int r = RY, cl = RX;
+    for (int j = 0; j < L; j++) {
+      if (threadIdx.x == j) {
+        wlo_r[j] = r;
+        wlo_c[j] = cl;
+      }
+      r = ((r >> 1) - K / 4) & ~1;  // arithmetic shift = floor division
+      cl = ((cl >> 1) - K / 4) & ~1;
     }
   }
   __syncthreads();
 
   // ---------------------------------------------------------------- 1. chain
-  if constexpr (!DENSE_IN && L > 1) {
-    constexpr int MR1 = S::MR1, MC1 = S::MC1, RW0 = S::RW0;
-    float* stack = bufA;  // [slot][MR1][MC1], slot = level - 1
-    float* tmph = bufB;   // [slot][MR1][RW0]
-    auto load_level = [&](int lev) {
-      const Win v = win[lev];
-      const int nr = v.r_hi - v.r_lo + 1, nc = v.c_hi - v.c_lo + 1;
-      const int16_t* g = p.lat + p.g.lv.off[lev];
-      const int gw = p.g.lv.w[lev];
-      float* dst = stack + (lev - 1) * MR1 * MC1;
+  if constexpr (!DENSE_IN) {
+    // level-0 latents of the region (clamped reads; only in-image entries are used)
 #pragma unroll 1
-      for (int s = threadIdx.x; s < nr * nc; s += SYN_THREADS) {
-        const int rr = s / nc, cc = s - rr * nc;
-        dst[rr * MC1 + cc] = (float)__ldg(g + (int64_t)(v.r_lo + rr) * gw + v.c_lo + cc);
-      }
-    };
-    load_level(L - 1);
-    __syncthreads();
-#pragma unroll 1
-    for (int j = L - 1; j >= 1; j--) {
-      // horizontal pass: level j (window j) -> columns of window j-1, for grids j..L-1
-      const Win vs = win[j], vd = win[j - 1];
-      const int nrs = vs.r_hi - vs.r_lo + 1;
-      const int ncd = vd.c_hi - vd.c_lo + 1;
-      const int nslots = L - j;  // slots j-1 .. L-2
-      const int per = nrs * ncd;
-      const int tstride = (j == 1) ? RW0 : MC1;
-#pragma unroll 1
-      for (int s = threadIdx.x; s < nslots * per; s += SYN_THREADS) {
-        const int sl = s / per, rem = s - sl * per;
-        const int rr = rem / ncd, cc = rem - rr * ncd;
-        const int slot = j - 1 + sl;
-        const float* src = stack + slot * MR1 * MC1 + rr * MC1;
-        tmph[slot * MR1 * RW0 + rr * tstride + cc] =
-            up_tap<K>(p.w.k, src, 1, vd.c_lo + cc, p.g.lv.w[j], vs.c_lo);
-      }
+    for (int it = threadIdx.x; it < RH0 * RW0; it += SYN_THREADS) {
+      const int rr = it / RW0, cc = it - rr * RW0;
+      lat0[it] = __ldg(p.lat + (int64_t)clampi(RY + rr, 0, H - 1) * W + clampi(RX + cc, 0, W - 1));
+    }
+    if constexpr (L > 1) {
+      SynCtx c{bufA, bufB, wlo_r, wlo_c};
+      load_window<L, CH, R, K, L - 1>(p, c);
       __syncthreads();
-      if (j == 1) break;  // the last vertical step is done per pixel in phase 2
-      // vertical pass: rows of window j-1
-      const int nrd = vd.r_hi - vd.r_lo + 1;
-      const int per2 = nrd * ncd;
-#pragma unroll 1
-      for (int s = threadIdx.x; s < nslots * per2; s += SYN_THREADS) {
-        const int sl = s / per2, rem = s - sl * per2;
-        const int rr = rem / ncd, cc = rem - rr * ncd;
-        const int slot = j - 1 + sl;
-        const float* src = tmph + slot * MR1 * RW0 + cc;
-        stack[slot * MR1 * MC1 + rr * MC1 + cc] =
-            up_tap<K>(p.w.k, src, MC1, vd.r_lo + rr, p.g.lv.h[j], vs.r_lo);
-      }
-      // grid j-1 joins the stack (slot j-2) at its own resolution
-      if (j - 1 >= 1) load_level(j - 1);
+      ChainStep<L, CH, R, K, L - 2>::run(p, c);
+    } else {
       __syncthreads();
     }
   }
 
-  // ------------------------------------------------- 2. last step + 1x1 MLP
-  float* hA = bufA;  // [3][RH0][RW0], indexed relative to (r0, c0)
+  // ------------------------------------- 2. last vertical step + 1x1 MLP
+  // Items: pairs of rows (2q, 2q+1) x columns of the level-0 region.
+  float* hA = bufA;  // [3][RH0][RW0] relative to (RY, RX)
   float* hB = bufB;
-  constexpr int RH0 = S::RH0, RW0 = S::RW0;
-  constexpr int HP = RH0 * RW0;
   {
-    const Win v1 = win[(L > 1) ? 1 : 0];
-    const int16_t* g0 = p.lat;
     const int64_t P = (int64_t)H * W;
+    const int h1 = (L > 1) ? p.g.lv.h[1] : 1;
+    const int lo1 = wlo_r[(L > 1) ? 1 : 0];
+    constexpr int NPAIR = (RH0 / 2) * RW0;
 #pragma unroll 1
-    for (int s = threadIdx.x; s < nr0 * nc0; s += SYN_THREADS) {
-      const int rr = s / nc0, cc = s - rr * nc0;
-      const int y = r0 + rr, x = c0 + cc;
-      float v[L];
+    for (int item = threadIdx.x; item < NPAIR; item += SYN_THREADS) {
+      const int rp = item / RW0;  // compile-time divisor
+      const int cc = item - rp * RW0;
+      const int y0 = RY + 2 * rp, x = RX + cc;
+      if (x < 0 || x >= W || y0 + 1 < 0 || y0 >= H) continue;  // never read by the convs
+      const bool has1 = (y0 + 1 < H);
+      float v0[L], v1[L];
       if constexpr (DENSE_IN) {
 #pragma unroll
-        for (int l = 0; l < L; l++) v[l] = __ldg(p.dense_in + l * P + (int64_t)y * W + x);
+        for (int l = 0; l < L; l++) {
+          v0[l] = __ldg(p.dense_in + l * P + (int64_t)y0 * W + x);
+          v1[l] = has1 ? __ldg(p.dense_in + l * P + (int64_t)(y0 + 1) * W + x) : 0.0f;
+        }
       } else {
-        v[0] = (float)__ldg(g0 + (int64_t)y * W + x);
+        v0[0] = (float)lat0[2 * rp * RW0 + cc];
+        v1[0] = (float)lat0[(2 * rp + 1) * RW0 + cc];
+        if constexpr (L > 1) {
+          // sources: rows q - K/4 .. q + K/4 of window 1 (q = y0 / 2), clamped
+          const int q = y0 >> 1;
+          int ro[K / 2 + 1];
 #pragma unroll
-        for (int l = 1; l < L; l++) {
-          const float* src = bufB + (l - 1) * S::MR1 * RW0 + cc;
-          v[l] = up_tap<K>(p.w.k, src, RW0, y, p.g.lv.h[1], v1.r_lo);
+          for (int u = 0; u <= K / 2; u++) ro[u] = (clampi(q - K / 4 + u, 0, h1 - 1) - lo1) * RW0 + cc;
+#pragma unroll
+          for (int l = 1; l < L; l++) {
+            const float* src = bufB + (l - 1) * S::TSLOT;
+            float sv[K / 2 + 1];
+#pragma unroll
+            for (int u = 0; u <= K / 2; u++) sv[u] = src[ro[u]];
+            float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+            for (int t = 0; t < K / 2; t++) {
+              a0 = fmaf(p.w.k[2 * t + 1], sv[K / 2 - 1 - t], a0);
+              a1 = fmaf(p.w.k[2 * t], sv[K / 2 - t], a1);
+            }
+            v0[l] = a0;
+            v1[l] = a1;
+          }
         }
       }
-      const bool inner = (y >= Y0 && y < Y1 && x >= X0 && x < X1);
-      if (p.dense_out != nullptr && inner) {
+      const bool inx = (x >= X0 && x < X0 + SYN_TW);
+      const bool in0 = inx && y0 >= Y0 && y0 < Y0 + SYN_TH;
+      const bool in1 = inx && has1 && y0 + 1 >= Y0 && y0 + 1 < Y0 + SYN_TH;
+      if (p.dense_out != nullptr) {
 #pragma unroll
-        for (int l = 0; l < L; l++) p.dense_out[l * P + (int64_t)y * W + x] = v[l];
+        for (int l = 0; l < L; l++) {
+          if (in0) p.dense_out[l * P + (int64_t)y0 * W + x] = v0[l];
+          if (in1) p.dense_out[l * P + (int64_t)(y0 + 1) * W + x] = v1[l];
+        }
       }
-      // layer 0: L -> CH, ReLU
-      uint64_t acc[CH / 2];
+      // layer 0: L -> CH (ReLU), two pixels share every weight load
+      uint64_t acc0[CH / 2], acc1[CH / 2];
 #pragma unroll
-      for (int n = 0; n < CH / 2; n++) acc[n] = ldp2(p.w.a0[n]);
+      for (int n = 0; n < CH / 2; n++) acc0[n] = acc1[n] = ldp2(p.w.a0[n]);
 #pragma unroll
       for (int i = 0; i < L; i++) {
-        const uint64_t xi = f2pack(v[i], v[i]);
+        const uint64_t x0 = f2pack(v0[i], v0[i]), x1 = f2pack(v1[i], v1[i]);
 #pragma unroll
-        for (int n = 0; n < CH / 2; n++) acc[n] = ffma2(xi, ldp2(p.w.A0[i][n]), acc[n]);
+        for (int n = 0; n < CH / 2; n++) {
+          const uint64_t wgt = ldp2(p.w.A0[i][n]);
+          acc0[n] = ffma2(x0, wgt, acc0[n]);
+          acc1[n] = ffma2(x1, wgt, acc1[n]);
+        }
       }
-      // layer 1: CH -> 3 (ReLU unless it is the module's last layer, i.e. R == 0)
-      uint64_t o01a = f2pack(p.w.a1[0], p.w.a1[1]), o01b = f2pack(0.0f, 0.0f);
-      float o2a = p.w.a1[2], o2b = 0.0f;
+      // layer 1: CH -> 3 (ReLU unless it is the module's last layer, R == 0)
+      uint64_t o0 = f2pack(p.w.a1[0], p.w.a1[1]), o1 = o0;
+      float o0s = p.w.a1[2], o1s = p.w.a1[2];
 #pragma unroll
       for (int n = 0; n < CH / 2; n++) {
-        const float2 hv = f2unpack(acc[n]);
-        const float h0 = fmaxf(hv.x, 0.0f), h1 = fmaxf(hv.y, 0.0f);
-        o01a = ffma2(f2pack(h0, h0), ldp2(p.w.A1p[2 * n]), o01a);
-        o2a = fmaf(h0, p.w.A1s[2 * n], o2a);
-        o01b = ffma2(f2pack(h1, h1), ldp2(p.w.A1p[2 * n + 1]), o01b);
-        o2b = fmaf(h1, p.w.A1s[2 * n + 1], o2b);
+        const float2 h0 = f2unpack(acc0[n]), h1v = f2unpack(acc1[n]);
+        const float h0a = fmaxf(h0.x, 0.0f), h0b = fmaxf(h0.y, 0.0f);
+        const float h1a = fmaxf(h1v.x, 0.0f), h1b = fmaxf(h1v.y, 0.0f);
+        const uint64_t wa = ldp2(p.w.A1p[2 * n]), wb = ldp2(p.w.A1p[2 * n + 1]);
+        o0 = ffma2(f2pack(h0a, h0a), wa, o0);
+        o1 = ffma2(f2pack(h1a, h1a), wa, o1);
+        o0s = fmaf(h0a, p.w.A1s[2 * n], o0s);
+        o1s = fmaf(h1a, p.w.A1s[2 * n], o1s);
+        o0 = ffma2(f2pack(h0b, h0b), wb, o0);
+        o1 = ffma2(f2pack(h1b, h1b), wb, o1);
+        o0s = fmaf(h0b, p.w.A1s[2 * n + 1], o0s);
+        o1s = fmaf(h1b, p.w.A1s[2 * n + 1], o1s);
       }
-      const float2 oa = f2unpack(o01a), ob = f2unpack(o01b);
-      float o[3] = {oa.x + ob.x, oa.y + ob.y, o2a + o2b};
+      const float2 r0 = f2unpack(o0), r1 = f2unpack(o1);
+      float out0[3] = {r0.x, r0.y, o0s}, out1[3] = {r1.x, r1.y, o1s};
       if (R > 0) {
 #pragma unroll
-        for (int c = 0; c < 3; c++) o[c] = fmaxf(o[c], 0.0f);
+        for (int c = 0; c < 3; c++) {
+          out0[c] = fmaxf(out0[c], 0.0f);
+          out1[c] = fmaxf(out1[c], 0.0f);
+        }
       }
-      if (p.h1_out != nullptr && inner) {
+      if (p.h1_out != nullptr) {
 #pragma unroll
-        for (int c = 0; c < 3; c++) p.h1_out[c * P + (int64_t)y * W + x] = o[c];
+        for (int c = 0; c < 3; c++) {
+          if (in0) p.h1_out[c * P + (int64_t)y0 * W + x] = out0[c];
+          if (in1) p.h1_out[c * P + (int64_t)(y0 + 1) * W + x] = out1[c];
+        }
       }
+      const int o = 2 * rp * RW0 + cc;
 #pragma unroll
-      for (int c = 0; c < 3; c++) hA[c * HP + rr * RW0 + cc] = o[c];
+      for (int c = 0; c < 3; c++) {
+        hA[c * HP + o] = out0[c];
+        hA[c * HP + o + RW0] = out1[c];
+      }
     }
   }
   __syncthreads();
 
   // ------------------------------------------------- 3. residual 3x3 layers
+  const int64_t Pimg = (int64_t)H * W;
+  float sse = 0.0f;
   float* hin = hA;
   float* hout = hB;
+  // conv output at (y, x) from hin (replicate padding = clamped reads)
+  auto conv_px = [&](int r, int y, int x, float (&o)[3]) {
+    int ro[3], co[3];
+#pragma unroll
+    for (int d = 0; d < 3; d++) {
+      ro[d] = (clampi(y + d - 1, 0, H - 1) - RY) * RW0;
+      co[d] = clampi(x + d - 1, 0, W - 1) - RX;
+    }
+    const int ctr = (y - RY) * RW0 + (x - RX);
+    uint64_t a01 = f2pack(hin[ctr] + p.w.g[r][0], hin[HP + ctr] + p.w.g[r][1]);
+    float a2 = hin[2 * HP + ctr] + p.w.g[r][2];
+#pragma unroll
+    for (int ci = 0; ci < 3; ci++)
+#pragma unroll
+      for (int ky = 0; ky < 3; ky++)
+#pragma unroll
+        for (int kx = 0; kx < 3; kx++) {
+          const float hv = hin[ci * HP + ro[ky] + co[kx]];
+          a01 = ffma2(f2pack(hv, hv), ldp2(p.w.Gp[r][ci][ky][kx]), a01);
+          a2 = fmaf(hv, p.w.Gs[r][ci][ky][kx], a2);
+        }
+    const float2 a = f2unpack(a01);
+    o[0] = a.x;
+    o[1] = a.y;
+    o[2] = a2;
+  };
 #pragma unroll
   for (int r = 0; r < R; r++) {
-    const int e = R - 1 - r;  // remaining halo after this layer
-    const int yr0 = max(0, Y0 - e), yr1 = min(H, Y1 + e);
-    const int xr0 = max(0, X0 - e), xr1 = min(W, X1 + e);
-    const int nr = yr1 - yr0, nc = xr1 - xr0;
+    const int e = R - 1 - r;  // halo this layer's output still needs
     const bool last = (r == R - 1);
-#pragma unroll 1
-    for (int s = threadIdx.x; s < nr * nc; s += SYN_THREADS) {
-      const int rr = s / nc, cc = s - rr * nc;
-      const int y = yr0 + rr, x = xr0 + cc;
-      int ro[3], co[3];
+    // interior (the tile): column segments with a sliding 3-row register window
+    {
+      const int cc = threadIdx.x % SYN_TW, seg = threadIdx.x / SYN_TW;
+      const int x = X0 + cc;
+      const int yb = Y0 + seg * S::RS;
+      if (x < W && yb < H) {
+        int co[3];
 #pragma unroll
-      for (int d = 0; d < 3; d++) {
-        ro[d] = (clampi(y + d - 1, 0, H - 1) - r0) * RW0;
-        co[d] = clampi(x + d - 1, 0, W - 1) - c0;
-      }
-      const int ctr = (y - r0) * RW0 + (x - c0);
-      uint64_t a01 = f2pack(hin[ctr] + p.w.g[r][0], hin[HP + ctr] + p.w.g[r][1]);
-      float a2 = hin[2 * HP + ctr] + p.w.g[r][2];
+        for (int d = 0; d < 3; d++) co[d] = clampi(x + d - 1, 0, W - 1) - RX;
+        float img[S::RS][3];  // x for this thread's output rows, loaded ahead of the math
+        if (last && p.image != nullptr) {
 #pragma unroll
-      for (int ci = 0; ci < 3; ci++)
+          for (int i = 0; i < S::RS; i++)
 #pragma unroll
-        for (int ky = 0; ky < 3; ky++)
+            for (int c = 0; c < 3; c++)
+              img[i][c] = (yb + i < H) ? __ldg(p.image + c * Pimg + (int64_t)(yb + i) * W + x) : 0.0f;
+        }
+        float wv[3][3][3];  // [row: y-1, y, y+1][ci][col]
 #pragma unroll
-          for (int kx = 0; kx < 3; kx++) {
-            const float hv = hin[ci * HP + ro[ky] + co[kx]];
-            a01 = ffma2(f2pack(hv, hv), ldp2(p.w.Gp[r][ci][ky][kx]), a01);
-            a2 = fmaf(hv, p.w.Gs[r][ci][ky][kx], a2);
+        for (int d = 0; d < 2; d++) {
+          const int rof = (clampi(yb + d - 1, 0, H - 1) - RY) * RW0;
+#pragma unroll
+          for (int ci = 0; ci < 3; ci++)
+#pragma unroll
+            for (int kx = 0; kx < 3; kx++) wv[d][ci][kx] = hin[ci * HP + rof + co[kx]];
+        }
+#pragma unroll
+        for (int i = 0; i < S::RS; i++) {
+          const int y = yb + i;
+          if (y >= H) break;
+          const int rof = (clampi(y + 1, 0, H - 1) - RY) * RW0;
+#pragma unroll
+          for (int ci = 0; ci < 3; ci++)
+#pragma unroll
+            for (int kx = 0; kx < 3; kx++) wv[2][ci][kx] = hin[ci * HP + rof + co[kx]];
+          uint64_t a01 = f2pack(wv[1][0][1] + p.w.g[r][0], wv[1][1][1] + p.w.g[r][1]);
+          float a2 = wv[1][2][1] + p.w.g[r][2];
+#pragma unroll
+          for (int ci = 0; ci < 3; ci++)
+#pragma unroll
+            for (int ky = 0; ky < 3; ky++)
+#pragma unroll
+              for (int kx = 0; kx < 3; kx++) {
+                const float hv = wv[ky][ci][kx];
+                a01 = ffma2(f2pack(hv, hv), ldp2(p.w.Gp[r][ci][ky][kx]), a01);
+                a2 = fmaf(hv, p.w.Gs[r][ci][ky][kx], a2);
+              }
+          const float2 a = f2unpack(a01);
+          float o[3] = {a.x, a.y, a2};
+          if (!last) {
+            const int ctr = (y - RY) * RW0 + (x - RX);
+#pragma unroll
+            for (int c = 0; c < 3; c++) hout[c * HP + ctr] = fmaxf(o[c], 0.0f);
+          } else {
+            const int64_t gi = (int64_t)y * W + x;
+#pragma unroll
+            for (int c = 0; c < 3; c++) {
+              if (p.x_hat != nullptr) p.x_hat[c * Pimg + gi] = o[c];
+              if (p.image != nullptr) {
+                const float ev = img[i][c] - o[c];
+                sse = fmaf(ev, ev, sse);
+              }
+            }
           }
-      const float2 a = f2unpack(a01);
-      float o[3] = {a.x, a.y, a2};
-      if (!last) {
 #pragma unroll
-        for (int c = 0; c < 3; c++) o[c] = fmaxf(o[c], 0.0f);
+          for (int ci = 0; ci < 3; ci++)
+#pragma unroll
+            for (int kx = 0; kx < 3; kx++) {
+              wv[0][ci][kx] = wv[1][ci][kx];
+              wv[1][ci][kx] = wv[2][ci][kx];
+            }
+        }
       }
-#pragma unroll
-      for (int c = 0; c < 3; c++) hout[c * HP + ctr] = o[c];
     }
-    __syncthreads();
-    float* t = hin;
-    hin = hout;
-    hout = t;
+    // halo ring of width e around the tile (non-last layers only)
+    if (e > 0) {
+      constexpr int EXT_MAX = 2 * ((R > 1) ? (R - 1) : 0);
+      const int nr = SYN_TH + 2 * e, nc = SYN_TW + 2 * e;
+      (void)EXT_MAX;
+#pragma unroll 1
+      for (int item = threadIdx.x; item < nr * nc; item += SYN_THREADS) {
+        const int rr = item / nc, cc = item - rr * nc;
+        if (rr >= e && rr < e + SYN_TH && cc >= e && cc < e + SYN_TW) continue;  // interior
+        const int y = Y0 - e + rr, x = X0 - e + cc;
+        if (y < 0 || y >= H || x < 0 || x >= W) continue;
+        float o[3];
+        conv_px(r, y, x, o);
+        const int ctr = (y - RY) * RW0 + (x - RX);
+#pragma unroll
+        for (int c = 0; c < 3; c++) hout[c * HP + ctr] = fmaxf(o[c], 0.0f);
+      }
+    }
+    if (!last) {
+      __syncthreads();
+      float* t = hin;
+      hin = hout;
+      hout = t;
+    }
   }
 
-  // --------------------------------------------- 4. x_hat + distortion (Eq. 1)
-  float sse = 0.0f;
-  {
-    const int64_t P = (int64_t)H * W;
-    const int nr = Y1 - Y0, nc = X1 - X0;
+  // R == 0: the 1x1 stack's output is x_hat
+  if constexpr (R == 0) {
 #pragma unroll 1
-    for (int s = threadIdx.x; s < nr * nc; s += SYN_THREADS) {
-      const int rr = s / nc, cc = s - rr * nc;
+    for (int item = threadIdx.x; item < SYN_TH * SYN_TW; item += SYN_THREADS) {
+      const int rr = item / SYN_TW, cc = item - rr * SYN_TW;
       const int y = Y0 + rr, x = X0 + cc;
-      const int ctr = (y - r0) * RW0 + (x - c0);
-      const int64_t gidx = (int64_t)y * W + x;
+      if (y >= H || x >= W) continue;
+      const int ctr = (y - RY) * RW0 + (x - RX);
+      const int64_t gi = (int64_t)y * W + x;
 #pragma unroll
       for (int c = 0; c < 3; c++) {
         const float xh = hin[c * HP + ctr];
-        if (p.x_hat != nullptr) p.x_hat[c * P + gidx] = xh;
+        if (p.x_hat != nullptr) p.x_hat[c * Pimg + gi] = xh;
         if (p.image != nullptr) {
-          const float e = __ldg(p.image + c * P + gidx) - xh;
-          sse = fmaf(e, e, sse);
+          const float ev = __ldg(p.image + c * Pimg + gi) - xh;
+          sse = fmaf(ev, ev, sse);
         }
       }
     }
   }
+
+  // ------------------------------------------------------ 4. distortion
   const double s = block_sum<SYN_THREADS>(sse, warp_buf);
   if (threadIdx.x == 0 && p.partial != nullptr) p.partial[blockIdx.x] = s;
 }
@@ -353,7 +560,8 @@ struct SynEntry {
 
 // Compiled synthesis shapes: BASELINE.json configs (tiny [4,8,3]+1, low
 // [7,16,3]+2, ref [7,40,3]+2; 8 taps), Table 1 (A300 [7,8,3]+1, A545/A1079
-// [7,16,3]+2 with 4 taps, A2300 [7,40,3]+2 with 8 taps) and small L for tests.
+// [7,16,3]+2 with 4 taps, A2300 [7,40,3]+2 with 8 taps) and small L / other R
+// for the edge-case tests.
 static const SynEntry kSyn[] = {
     {4, 8, 1, 8, launch_syn<4, 8, 1, 8>},     {7, 16, 2, 8, launch_syn<7, 16, 2, 8>},
     {7, 40, 2, 8, launch_syn<7, 40, 2, 8>},   {7, 8, 1, 4, launch_syn<7, 8, 1, 4>},
