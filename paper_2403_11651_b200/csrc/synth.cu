@@ -68,21 +68,56 @@ struct SynCtx {
   int* wlo_c;
 };
 
-// replicate-extended window of grid LEV into stack slot LEV - 1
+// Latent staging: every thread first issues all of its loads, then stores
+// (compile-time trip counts, so the loads of every level are in flight
+// together).  Clamped reads = replicate-extended windows.
 template <int L, int CH, int R, int K, int LEV>
-__device__ __forceinline__ void load_window(const SynParams<L, CH, R, K>& p, const SynCtx& c) {
+struct LoadWindows {
   using S = SynShape<L, CH, R, K>;
-  constexpr int NR = wsize<K>(S::RH0, LEV), NC = wsize<K>(S::RW0, LEV);
-  const int16_t* g = p.lat + p.g.lv.off[LEV];
-  const int gh = p.g.lv.h[LEV], gw = p.g.lv.w[LEV];
-  const int lr = c.wlo_r[LEV], lc = c.wlo_c[LEV];
-  float* dst = c.stack + (LEV - 1) * S::SLOT;
-#pragma unroll 1
-  for (int it = threadIdx.x; it < NR * NC; it += SYN_THREADS) {
-    const int rr = it / NC, cc = it - rr * NC;
-    dst[it] = (float)__ldg(g + (int64_t)clampi(lr + rr, 0, gh - 1) * gw + clampi(lc + cc, 0, gw - 1));
+  static constexpr int NR = wsize<K>(S::RH0, LEV), NC = wsize<K>(S::RW0, LEV);
+  static constexpr int IT = (NR * NC + SYN_THREADS - 1) / SYN_THREADS;
+  static __device__ __forceinline__ void run(const SynParams<L, CH, R, K>& p, const SynCtx& c) {
+    const int16_t* g = p.lat + p.g.lv.off[LEV];
+    const int gh = p.g.lv.h[LEV], gw = p.g.lv.w[LEV];
+    const int lr = c.wlo_r[LEV], lc = c.wlo_c[LEV];
+    int16_t v[IT];
+#pragma unroll
+    for (int k = 0; k < IT; k++) {
+      const int it = threadIdx.x + k * SYN_THREADS;
+      const int rr = it / NC, cc = it - rr * NC;
+      v[k] = (it < NR * NC) ? __ldg(g + (int64_t)clampi(lr + rr, 0, gh - 1) * gw + clampi(lc + cc, 0, gw - 1)) : 0;
+    }
+    if constexpr (LEV > 1) LoadWindows<L, CH, R, K, LEV - 1>::run(p, c);
+    float* dst = c.stack + (LEV - 1) * S::SLOT;
+#pragma unroll
+    for (int k = 0; k < IT; k++) {
+      const int it = threadIdx.x + k * SYN_THREADS;
+      if (it < NR * NC) dst[it] = (float)v[k];
+    }
   }
-}
+};
+
+template <int L, int CH, int R, int K>
+struct LoadLat0 {
+  using S = SynShape<L, CH, R, K>;
+  static constexpr int N = S::RH0 * S::RW0;
+  static constexpr int IT = (N + SYN_THREADS - 1) / SYN_THREADS;
+  static __device__ __forceinline__ void run(const SynParams<L, CH, R, K>& p, int16_t* lat0, int RY, int RX) {
+    const int H = p.g.H, W = p.g.W;
+    int16_t v[IT];
+#pragma unroll
+    for (int k = 0; k < IT; k++) {
+      const int it = threadIdx.x + k * SYN_THREADS;
+      const int rr = it / S::RW0, cc = it - rr * S::RW0;
+      v[k] = (it < N) ? __ldg(p.lat + (int64_t)clampi(RY + rr, 0, H - 1) * W + clampi(RX + cc, 0, W - 1)) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < IT; k++) {
+      const int it = threadIdx.x + k * SYN_THREADS;
+      if (it < N) lat0[it] = v[k];
+    }
+  }
+};
 
 // One x2 step of the chain, from level J+1 to level J, for every grid l > J
 // (stack slots J .. L-2).  out[2q + r] = sum_t k[2t + 1 - r] g[q + r + K/4 - 1 - t]
@@ -156,9 +191,7 @@ struct ChainStep {
           for (int u = 0; u < K / 2; u++) sv[u] = sv[u + 1];
         }
       }
-      // grid J joins the stack (slot J - 1) at its own resolution
-      load_window<L, CH, R, K, J>(p, c);
-      __syncthreads();
+      __syncthreads();  // grid J was staged into slot J - 1 up front
       ChainStep<L, CH, R, K, J - 1>::run(p, c);
     }
   }
@@ -199,15 +232,13 @@ __global__ void __launch_bounds__(SYN_THREADS, 2)
 
   // ---------------------------------------------------------------- 1. chain
   if constexpr (!DENSE_IN) {
-    // level-0 latents of the region (clamped reads; only in-image entries are used)
-#pragma unroll 1
-    for (int it = threadIdx.x; it < RH0 * RW0; it += SYN_THREADS) {
-      const int rr = it / RW0, cc = it - rr * RW0;
-      lat0[it] = __ldg(p.lat + (int64_t)clampi(RY + rr, 0, H - 1) * W + clampi(RX + cc, 0, W - 1));
-    }
+    // all latent windows up front (many loads in flight): level 0's region
+    // (int16) and every grid l >= 1 into its stack slot, which no chain step
+    // touches before grid l is needed (clamped reads = replicate padding).
+    LoadLat0<L, CH, R, K>::run(p, lat0, RY, RX);
     if constexpr (L > 1) {
       SynCtx c{bufA, bufB, wlo_r, wlo_c};
-      load_window<L, CH, R, K, L - 1>(p, c);
+      LoadWindows<L, CH, R, K, L - 1>::run(p, c);
       __syncthreads();
       ChainStep<L, CH, R, K, L - 2>::run(p, c);
     } else {
@@ -384,60 +415,73 @@ __global__ void __launch_bounds__(SYN_THREADS, 2)
             for (int c = 0; c < 3; c++)
               img[i][c] = (yb + i < H) ? __ldg(p.image + c * Pimg + (int64_t)(yb + i) * W + x) : 0.0f;
         }
-        float wv[3][3][3];  // [row: y-1, y, y+1][ci][col]
+        // 4 output rows per pass: every uniform weight load feeds 4 outputs;
+        // the 6 input rows slide (2 reused) between the two passes.
+        constexpr int G = 4;
+        static_assert(S::RS % G == 0, "row groups");
+        float in[G + 2][3][3];  // [row y0-1 .. y0+G][ci][col]
 #pragma unroll
-        for (int d = 0; d < 2; d++) {
-          const int rof = (clampi(yb + d - 1, 0, H - 1) - RY) * RW0;
+        for (int g = 0; g < S::RS / G; g++) {
+          const int y0 = yb + g * G;
 #pragma unroll
-          for (int ci = 0; ci < 3; ci++)
+          for (int d = 0; d < G + 2; d++) {
+            if (g > 0 && d < 2) {
 #pragma unroll
-            for (int kx = 0; kx < 3; kx++) wv[d][ci][kx] = hin[ci * HP + rof + co[kx]];
-        }
+              for (int ci = 0; ci < 3; ci++)
 #pragma unroll
-        for (int i = 0; i < S::RS; i++) {
-          const int y = yb + i;
-          if (y >= H) break;
-          const int rof = (clampi(y + 1, 0, H - 1) - RY) * RW0;
+                for (int kx = 0; kx < 3; kx++) in[d][ci][kx] = in[d + G][ci][kx];
+            } else {
+              const int rof = (clampi(y0 + d - 1, 0, H - 1) - RY) * RW0;
 #pragma unroll
-          for (int ci = 0; ci < 3; ci++)
+              for (int ci = 0; ci < 3; ci++)
 #pragma unroll
-            for (int kx = 0; kx < 3; kx++) wv[2][ci][kx] = hin[ci * HP + rof + co[kx]];
-          uint64_t a01 = f2pack(wv[1][0][1] + p.w.g[r][0], wv[1][1][1] + p.w.g[r][1]);
-          float a2 = wv[1][2][1] + p.w.g[r][2];
+                for (int kx = 0; kx < 3; kx++) in[d][ci][kx] = hin[ci * HP + rof + co[kx]];
+            }
+          }
+          uint64_t a01[G];
+          float a2[G];
+#pragma unroll
+          for (int i = 0; i < G; i++) {
+            a01[i] = f2pack(in[i + 1][0][1] + p.w.g[r][0], in[i + 1][1][1] + p.w.g[r][1]);
+            a2[i] = in[i + 1][2][1] + p.w.g[r][2];
+          }
 #pragma unroll
           for (int ci = 0; ci < 3; ci++)
 #pragma unroll
             for (int ky = 0; ky < 3; ky++)
 #pragma unroll
               for (int kx = 0; kx < 3; kx++) {
-                const float hv = wv[ky][ci][kx];
-                a01 = ffma2(f2pack(hv, hv), ldp2(p.w.Gp[r][ci][ky][kx]), a01);
-                a2 = fmaf(hv, p.w.Gs[r][ci][ky][kx], a2);
+                const uint64_t w01 = ldp2(p.w.Gp[r][ci][ky][kx]);
+                const float w2 = p.w.Gs[r][ci][ky][kx];
+#pragma unroll
+                for (int i = 0; i < G; i++) {
+                  const float hv = in[i + ky][ci][kx];
+                  a01[i] = ffma2(f2pack(hv, hv), w01, a01[i]);
+                  a2[i] = fmaf(hv, w2, a2[i]);
+                }
               }
-          const float2 a = f2unpack(a01);
-          float o[3] = {a.x, a.y, a2};
-          if (!last) {
-            const int ctr = (y - RY) * RW0 + (x - RX);
 #pragma unroll
-            for (int c = 0; c < 3; c++) hout[c * HP + ctr] = fmaxf(o[c], 0.0f);
-          } else {
-            const int64_t gi = (int64_t)y * W + x;
+          for (int i = 0; i < G; i++) {
+            const int y = y0 + i;
+            if (y >= H) break;
+            const float2 a = f2unpack(a01[i]);
+            const float o[3] = {a.x, a.y, a2[i]};
+            if (!last) {
+              const int ctr = (y - RY) * RW0 + (x - RX);
 #pragma unroll
-            for (int c = 0; c < 3; c++) {
-              if (p.x_hat != nullptr) p.x_hat[c * Pimg + gi] = o[c];
-              if (p.image != nullptr) {
-                const float ev = img[i][c] - o[c];
-                sse = fmaf(ev, ev, sse);
+              for (int c = 0; c < 3; c++) hout[c * HP + ctr] = fmaxf(o[c], 0.0f);
+            } else {
+              const int64_t gi = (int64_t)y * W + x;
+#pragma unroll
+              for (int c = 0; c < 3; c++) {
+                if (p.x_hat != nullptr) p.x_hat[c * Pimg + gi] = o[c];
+                if (p.image != nullptr) {
+                  const float ev = img[g * G + i][c] - o[c];
+                  sse = fmaf(ev, ev, sse);
+                }
               }
             }
           }
-#pragma unroll
-          for (int ci = 0; ci < 3; ci++)
-#pragma unroll
-            for (int kx = 0; kx < 3; kx++) {
-              wv[0][ci][kx] = wv[1][ci][kx];
-              wv[1][ci][kx] = wv[2][ci][kx];
-            }
         }
       }
     }
