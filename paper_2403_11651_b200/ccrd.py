@@ -78,14 +78,16 @@ def load(rebuild_if_stale: bool = True) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if rebuild_if_stale:
+    alt = os.environ.get("CCRD_LIB")  # experiment variant built by tools/ (same ABI)
+    if alt:
+        rebuild_if_stale = False
         try:
             _build.build()
         except FileNotFoundError:
             pass  # no nvcc: fall through to loading what exists
-    if not os.path.exists(_build.LIB):
+    if not os.path.exists(alt or _build.LIB):
         raise ImportError(f"libccrd.so not built ({_build.LIB}); run paper_2403_11651_b200/build.py")
-    L = C.CDLL(_build.LIB)
+    L = C.CDLL(alt or _build.LIB)
     P, V, S = C.POINTER, C.c_void_p, C.c_size_t
     D = P(CcModelDesc)
     L.cc_workspace_bytes.restype = S

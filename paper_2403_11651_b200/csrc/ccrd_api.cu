@@ -182,10 +182,10 @@ static void syn_geom(const cc_model_desc& d, SynGeom& g) {
   g.n_tiles = g.tiles_x * ((d.H + SYN_TH - 1) / SYN_TH);
 }
 
-static int n_arm_ctas(const cc_model_desc& d) {
+static int n_arm_partials(const cc_model_desc& d) {  // one per ARM warp
   ArmGeom g;
   arm_geom(d, g);
-  return g.tile_begin[d.L];
+  return g.tile_begin[d.L] * (ARM_THREADS / 32);
 }
 static int n_syn_ctas(const cc_model_desc& d) {
   SynGeom g;
@@ -195,10 +195,10 @@ static int n_syn_ctas(const cc_model_desc& d) {
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// per image: ARM partials + synthesis partials (fp64) + a result scratch slot
-// used by the stage entries
+// Workspace per image: ARM partials + synthesis partials (fp64) + a result
+// scratch slot used by the stage entries
 static size_t partial_bytes(const cc_model_desc& d) {
-  return align256(sizeof(double) * (size_t)(n_arm_ctas(d) + n_syn_ctas(d))) + align256(sizeof(cc_rd_result));
+  return align256(sizeof(double) * (size_t)(n_arm_partials(d) + n_syn_ctas(d))) + align256(sizeof(cc_rd_result));
 }
 
 // ------------------------------------------------------------- reduction
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(256) reduce_batch_kernel(const __grid_constant
 
 static ReduceJob make_job(const cc_model_desc& d, double* part) {
   ReduceJob j;
-  j.n_arm = n_arm_ctas(d);
+  j.n_arm = n_arm_partials(d);
   j.n_syn = n_syn_ctas(d);
   j.arm_partial = part;
   j.syn_partial = part + j.n_arm;
@@ -282,7 +282,7 @@ static int forward_one(const cc_model_desc& d, const int16_t* lat, const float* 
   if (rc) return rc;
   {
     ProfScope ps(PK_SYN, s);
-    syn(sg, d, up_w, syn_w, lat, nullptr, image, x_hat, nullptr, nullptr, part + ag.tile_begin[d.L], s);
+    syn(sg, d, up_w, syn_w, lat, nullptr, image, x_hat, nullptr, nullptr, part + n_arm_partials(d), s);
   }
   g_launches++;
   return cuda_check("synth_kernel");
@@ -352,19 +352,21 @@ int cc_rd_forward(const cc_model_desc* desc, const cc_image_io* io, int32_t n_im
   if (rc) return rc;
   if (!io || n_img < 1 || !results) return fail(CC_EINVAL, "io/results null or n_img < 1");
   const size_t per = partial_bytes(*desc);
-  if (!workspace || workspace_bytes < per * (size_t)n_img)
-    return fail(CC_EWORKSPACE, "need %zu workspace bytes, got %zu", per * (size_t)n_img, workspace_bytes);
+  const size_t need = per * (size_t)n_img;
+  if (!workspace || workspace_bytes < need)
+    return fail(CC_EWORKSPACE, "need %zu workspace bytes, got %zu", need, workspace_bytes);
   for (int i = 0; i < n_img; i++)
     if (!io[i].latents || !io[i].arm_w || !io[i].up_w || !io[i].syn_w)
       return fail(CC_EINVAL, "image %d: null latents or weights", i);
   if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
   cudaStream_t s = (cudaStream_t)stream;
+  char* slices = (char*)workspace;
   ReduceJob jobs[MAX_JOBS_PER_LAUNCH];
   for (int b = 0; b < n_img; b += MAX_JOBS_PER_LAUNCH) {
     const int m = (n_img - b < MAX_JOBS_PER_LAUNCH) ? n_img - b : MAX_JOBS_PER_LAUNCH;
     for (int i = 0; i < m; i++) {
       const cc_image_io& x = io[b + i];
-      double* part = (double*)((char*)workspace + per * (size_t)(b + i));
+      double* part = (double*)(slices + per * (size_t)(b + i));
       rc = forward_one(*desc, x.latents, x.arm_w, x.up_w, x.syn_w, x.image, x.x_hat, part, s);
       if (rc) return rc;
       jobs[i] = make_job(*desc, part);
@@ -388,8 +390,8 @@ static size_t stage_slot_bytes(const cc_model_desc& d) {
 
 size_t cc_workspace_bytes_host(const cc_model_desc* desc, int32_t n_img) {
   if (validate(desc) != CC_OK || n_img < 1) return 0;
-  return partial_bytes(*desc) * (size_t)n_img + align256(sizeof(cc_rd_result) * (size_t)n_img) +
-         2 * stage_slot_bytes(*desc);
+  return partial_bytes(*desc) * (size_t)n_img +
+         align256(sizeof(cc_rd_result) * (size_t)n_img) + 2 * stage_slot_bytes(*desc);
 }
 
 int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t n_img, cc_rd_result* results,
@@ -478,7 +480,8 @@ int cc_arm_rate(const cc_model_desc* desc, const int16_t* latents, const float* 
   if (rc) return rc;
   if (!latents || !arm_w || !rate) return fail(CC_EINVAL, "null latents / arm_w / rate");
   const size_t per = partial_bytes(*desc);
-  if (!workspace || workspace_bytes < per) return fail(CC_EWORKSPACE, "need %zu workspace bytes", per);
+  if (!workspace || workspace_bytes < per)
+    return fail(CC_EWORKSPACE, "need %zu workspace bytes", per);
   if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
   if ((mu || scale) && !bits) return fail(CC_EINVAL, "mu/scale debug outputs need bits != NULL");
   const cc_model_desc& d = *desc;

@@ -37,6 +37,18 @@ __device__ __forceinline__ uint64_t ldp2(const float2& v) {
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
 
+// Single-MUFU base-2 exponential / logarithm (PTX ex2.approx / lg2.approx).
+__device__ __forceinline__ float exp2f_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float log2f_approx(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // Block-wide deterministic sum of one fp32 value per thread -> fp64 (thread 0).
 template <int NT>
 __device__ __forceinline__ double block_sum(float v, double* warp_buf) {
@@ -60,10 +72,14 @@ struct LevelGeom {
   int64_t off[CC_MAX_LEVELS];  // element offset of level l in the packed pyramid
 };
 
-// ARM tiling: one CTA = 8 rows x 32 latents of one grid (one warp per row).
-constexpr int ARM_TX = 32;
+// ARM tiling: one CTA = 8 rows x 64 latents of one grid; warp w owns row w,
+// lane t the latents at columns t and t + 32 (two latents per thread, so every
+// uniform weight load feeds two FFMA2).
+constexpr int ARM_LPT = 2;                 // latents per thread
+constexpr int ARM_TX = 32 * ARM_LPT;
 constexpr int ARM_TY = 8;
-constexpr int ARM_THREADS = ARM_TX * ARM_TY;
+constexpr int ARM_THREADS = 32 * ARM_TY;
+constexpr int ARM_CTAS_PER_SM = 2;
 constexpr int ARM_HALO_TOP = 3;  // dy >= -3
 constexpr int ARM_HALO_X = 4;    // |dx| <= 4
 constexpr int ARM_SW = ARM_TX + 2 * ARM_HALO_X;
@@ -97,7 +113,7 @@ template <int C, int NH, int NHL>
 struct ArmParams {
   ArmGeom g;
   const int16_t* lat;
-  double* partial;  // [n CTAs] per-CTA rate partial sums
+  double* partial;  // [CTAs x warps] per-warp rate partial sums
   float* mu;        // optional per-latent debug outputs
   float* scale;
   float* bits;
