@@ -121,9 +121,16 @@ struct ArmParams {
 };
 
 // Synthesis tiling: one CTA = 32 x 64 output pixels, 256 threads.
+#ifndef CCRD_SYN_THREADS
+#define CCRD_SYN_THREADS 256
+#endif
+#ifndef CCRD_SYN_CPS
+#define CCRD_SYN_CPS 2
+#endif
 constexpr int SYN_TH = 32;
 constexpr int SYN_TW = 64;
-constexpr int SYN_THREADS = 256;
+constexpr int SYN_THREADS = CCRD_SYN_THREADS;
+constexpr int SYN_CTAS_PER_SM = CCRD_SYN_CPS;
 
 template <int L, int CH, int R, int K>
 struct SynWeights {

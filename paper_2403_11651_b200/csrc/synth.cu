@@ -13,16 +13,31 @@
 //      (both phases share the K/2 + 1 source rows) and the L -> C_h -> 3 1x1
 //      MLP for both pixels in registers (packed FFMA2, two neurons per
 //      instruction, each uniform weight load feeding two pixels).
-//   3. residual 3x3 layers: each thread slides a 3-row register window down a
-//      column segment (9 shared loads per output); the halo ring of the
-//      non-last layers is recomputed, never exchanged; replicate padding at
-//      the image border is index clamping.
+//   3. residual 3x3 layers: each thread owns a column segment of 8 rows and,
+//      per input channel, loads its 10 x 3 window once; every uniform weight
+//      feeds 8 outputs.  The halo ring of the non-last layers is recomputed,
+//      never exchanged; replicate padding at the image border is index
+//      clamping.
 //   4. the last layer's output goes straight from registers to x_hat
 //      (optional) and the (x - x_hat)^2 partial sum -> fp64 per CTA.
 // The dense L x H x W tensor is never materialised in HBM.
 #include "ccrd_common.cuh"
 
 namespace ccrd {
+
+#ifdef CCRD_SYN_TIMING
+// experiment build: per-CTA phase timestamps [cta][8] (clock64), read back by
+// cc_debug_syn_timing (tools/ only)
+__device__ unsigned long long g_syn_timing[1 << 16][8];
+#define SYN_MARK(k)                                                               \
+  if (threadIdx.x == 0 && blockIdx.x < (1 << 16)) {                                \
+    unsigned long long t;                                                          \
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));                              \
+    g_syn_timing[blockIdx.x][k] = t;                                               \
+  }
+#else
+#define SYN_MARK(k)
+#endif
 
 // Window sizes of the upsampling chain (compile time).  Level 0's window is the
 // tile + an even halo RE; level j+1's window starts at ((lo_j >> 1) - K/4)
@@ -199,7 +214,7 @@ struct ChainStep {
 };
 
 template <int L, int CH, int R, int K, bool DENSE_IN>
-__global__ void __launch_bounds__(SYN_THREADS, 2)
+__global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
     synth_kernel(const __grid_constant__ SynParams<L, CH, R, K> p) {
   using S = SynShape<L, CH, R, K>;
   constexpr int RE = S::RE, RH0 = S::RH0, RW0 = S::RW0;
@@ -235,12 +250,15 @@ __global__ void __launch_bounds__(SYN_THREADS, 2)
     // all latent windows up front (many loads in flight): level 0's region
     // (int16) and every grid l >= 1 into its stack slot, which no chain step
     // touches before grid l is needed (clamped reads = replicate padding).
+    SYN_MARK(0);
     LoadLat0<L, CH, R, K>::run(p, lat0, RY, RX);
     if constexpr (L > 1) {
       SynCtx c{bufA, bufB, wlo_r, wlo_c};
       LoadWindows<L, CH, R, K, L - 1>::run(p, c);
       __syncthreads();
+      SYN_MARK(1);
       ChainStep<L, CH, R, K, L - 2>::run(p, c);
+      SYN_MARK(2);
     } else {
       __syncthreads();
     }
@@ -363,12 +381,14 @@ __global__ void __launch_bounds__(SYN_THREADS, 2)
   }
   __syncthreads();
 
+  SYN_MARK(3);
   // ------------------------------------------------- 3. residual 3x3 layers
   const int64_t Pimg = (int64_t)H * W;
   float sse = 0.0f;
   float* hin = hA;
   float* hout = hB;
-  // conv output at (y, x) from hin (replicate padding = clamped reads)
+  // conv output at (y, x) from hin (replicate padding = clamped reads); used
+  // for the halo ring only
   auto conv_px = [&](int r, int y, int x, float (&o)[3]) {
     int ro[3], co[3];
 #pragma unroll
@@ -398,103 +418,112 @@ __global__ void __launch_bounds__(SYN_THREADS, 2)
   for (int r = 0; r < R; r++) {
     const int e = R - 1 - r;  // halo this layer's output still needs
     const bool last = (r == R - 1);
-    // interior (the tile): column segments with a sliding 3-row register window
+    // interior (the tile): each thread owns a column segment of RS rows; per
+    // input channel it loads the (RS + 2) x 3 window once and every uniform
+    // weight (pair) feeds RS outputs
     {
+      constexpr int RS = S::RS;
       const int cc = threadIdx.x % SYN_TW, seg = threadIdx.x / SYN_TW;
       const int x = X0 + cc;
-      const int yb = Y0 + seg * S::RS;
+      const int yb = Y0 + seg * RS;
       if (x < W && yb < H) {
         int co[3];
 #pragma unroll
         for (int d = 0; d < 3; d++) co[d] = clampi(x + d - 1, 0, W - 1) - RX;
-        float img[S::RS][3];  // x for this thread's output rows, loaded ahead of the math
+        float img[RS][3];  // x for the output rows, in flight during the math
         if (last && p.image != nullptr) {
 #pragma unroll
-          for (int i = 0; i < S::RS; i++)
+          for (int i = 0; i < RS; i++)
 #pragma unroll
             for (int c = 0; c < 3; c++)
               img[i][c] = (yb + i < H) ? __ldg(p.image + c * Pimg + (int64_t)(yb + i) * W + x) : 0.0f;
         }
-        // 4 output rows per pass: every uniform weight load feeds 4 outputs;
-        // the 6 input rows slide (2 reused) between the two passes.
-        constexpr int G = 4;
-        static_assert(S::RS % G == 0, "row groups");
-        float in[G + 2][3][3];  // [row y0-1 .. y0+G][ci][col]
+        uint64_t a01[RS];
+        float a2[RS];
 #pragma unroll
-        for (int g = 0; g < S::RS / G; g++) {
-          const int y0 = yb + g * G;
+        for (int i = 0; i < RS; i++) {
+          a01[i] = f2pack(p.w.g[r][0], p.w.g[r][1]);
+          a2[i] = p.w.g[r][2];
+        }
 #pragma unroll
-          for (int d = 0; d < G + 2; d++) {
-            if (g > 0 && d < 2) {
+        for (int ci = 0; ci < 3; ci++) {
+          float in[RS + 2][3];  // rows yb-1 .. yb+RS (clamped) x cols x-1 .. x+1
 #pragma unroll
-              for (int ci = 0; ci < 3; ci++)
+          for (int d = 0; d < RS + 2; d++) {
+            const int rof = ci * HP + (clampi(yb + d - 1, 0, H - 1) - RY) * RW0;
 #pragma unroll
-                for (int kx = 0; kx < 3; kx++) in[d][ci][kx] = in[d + G][ci][kx];
+            for (int kx = 0; kx < 3; kx++) in[d][kx] = hin[rof + co[kx]];
+          }
+          // residual: output channel co = ci adds its own input
+#pragma unroll
+          for (int i = 0; i < RS; i++) {
+            if (ci == 2) {
+              a2[i] += in[i + 1][1];
             } else {
-              const int rof = (clampi(y0 + d - 1, 0, H - 1) - RY) * RW0;
-#pragma unroll
-              for (int ci = 0; ci < 3; ci++)
-#pragma unroll
-                for (int kx = 0; kx < 3; kx++) in[d][ci][kx] = hin[ci * HP + rof + co[kx]];
+              float2 t = f2unpack(a01[i]);
+              if (ci == 0) t.x += in[i + 1][1];
+              else t.y += in[i + 1][1];
+              a01[i] = f2pack(t.x, t.y);
             }
           }
-          uint64_t a01[G];
-          float a2[G];
 #pragma unroll
-          for (int i = 0; i < G; i++) {
-            a01[i] = f2pack(in[i + 1][0][1] + p.w.g[r][0], in[i + 1][1][1] + p.w.g[r][1]);
-            a2[i] = in[i + 1][2][1] + p.w.g[r][2];
-          }
+          for (int ky = 0; ky < 3; ky++)
 #pragma unroll
-          for (int ci = 0; ci < 3; ci++)
+            for (int kx = 0; kx < 3; kx++) {
+              const uint64_t w01 = ldp2(p.w.Gp[r][ci][ky][kx]);
+              const float w2 = p.w.Gs[r][ci][ky][kx];
 #pragma unroll
-            for (int ky = 0; ky < 3; ky++)
-#pragma unroll
-              for (int kx = 0; kx < 3; kx++) {
-                const uint64_t w01 = ldp2(p.w.Gp[r][ci][ky][kx]);
-                const float w2 = p.w.Gs[r][ci][ky][kx];
-#pragma unroll
-                for (int i = 0; i < G; i++) {
-                  const float hv = in[i + ky][ci][kx];
-                  a01[i] = ffma2(f2pack(hv, hv), w01, a01[i]);
-                  a2[i] = fmaf(hv, w2, a2[i]);
-                }
+              for (int i = 0; i < RS; i++) {
+                const float hv = in[i + ky][kx];
+                a01[i] = ffma2(f2pack(hv, hv), w01, a01[i]);
+                a2[i] = fmaf(hv, w2, a2[i]);
               }
+            }
+        }
 #pragma unroll
-          for (int i = 0; i < G; i++) {
-            const int y = y0 + i;
-            if (y >= H) break;
-            const float2 a = f2unpack(a01[i]);
-            const float o[3] = {a.x, a.y, a2[i]};
-            if (!last) {
-              const int ctr = (y - RY) * RW0 + (x - RX);
+        for (int i = 0; i < RS; i++) {
+          const int y = yb + i;
+          if (y >= H) break;
+          const float2 a = f2unpack(a01[i]);
+          const float o[3] = {a.x, a.y, a2[i]};
+          if (!last) {
+            const int ctr = (y - RY) * RW0 + (x - RX);
 #pragma unroll
-              for (int c = 0; c < 3; c++) hout[c * HP + ctr] = fmaxf(o[c], 0.0f);
-            } else {
-              const int64_t gi = (int64_t)y * W + x;
+            for (int c = 0; c < 3; c++) hout[c * HP + ctr] = fmaxf(o[c], 0.0f);
+          } else {
+            const int64_t gi = (int64_t)y * W + x;
 #pragma unroll
-              for (int c = 0; c < 3; c++) {
-                if (p.x_hat != nullptr) p.x_hat[c * Pimg + gi] = o[c];
-                if (p.image != nullptr) {
-                  const float ev = img[g * G + i][c] - o[c];
-                  sse = fmaf(ev, ev, sse);
-                }
+            for (int c = 0; c < 3; c++) {
+              if (p.x_hat != nullptr) p.x_hat[c * Pimg + gi] = o[c];
+              if (p.image != nullptr) {
+                const float ev = img[i][c] - o[c];
+                sse = fmaf(ev, ev, sse);
               }
             }
           }
         }
       }
     }
-    // halo ring of width e around the tile (non-last layers only)
+    // halo ring of width e around the tile (non-last layers only), enumerated
+    // directly: top / bottom rows, then left / right columns
     if (e > 0) {
-      constexpr int EXT_MAX = 2 * ((R > 1) ? (R - 1) : 0);
-      const int nr = SYN_TH + 2 * e, nc = SYN_TW + 2 * e;
-      (void)EXT_MAX;
+      const int NWr = SYN_TW + 2 * e;
+      const int n_top = e * NWr, n_side = e * SYN_TH;
 #pragma unroll 1
-      for (int item = threadIdx.x; item < nr * nc; item += SYN_THREADS) {
-        const int rr = item / nc, cc = item - rr * nc;
-        if (rr >= e && rr < e + SYN_TH && cc >= e && cc < e + SYN_TW) continue;  // interior
-        const int y = Y0 - e + rr, x = X0 - e + cc;
+      for (int idx = threadIdx.x; idx < 2 * n_top + 2 * n_side; idx += SYN_THREADS) {
+        int y, x;
+        if (idx < 2 * n_top) {
+          const int j = idx < n_top ? idx : idx - n_top;
+          const int rr = j / NWr;
+          y = (idx < n_top) ? Y0 - e + rr : Y0 + SYN_TH + rr;
+          x = X0 - e + (j - rr * NWr);
+        } else {
+          const int j0 = idx - 2 * n_top;
+          const int j = j0 < n_side ? j0 : j0 - n_side;
+          const int rr = j / e;
+          y = Y0 + rr;
+          x = (j0 < n_side) ? X0 - e + (j - rr * e) : X0 + SYN_TW + (j - rr * e);
+        }
         if (y < 0 || y >= H || x < 0 || x >= W) continue;
         float o[3];
         conv_px(r, y, x, o);
@@ -505,6 +534,7 @@ __global__ void __launch_bounds__(SYN_THREADS, 2)
     }
     if (!last) {
       __syncthreads();
+      SYN_MARK(4);
       float* t = hin;
       hin = hout;
       hout = t;
@@ -535,7 +565,23 @@ __global__ void __launch_bounds__(SYN_THREADS, 2)
   // ------------------------------------------------------ 4. distortion
   const double s = block_sum<SYN_THREADS>(sse, warp_buf);
   if (threadIdx.x == 0 && p.partial != nullptr) p.partial[blockIdx.x] = s;
+  SYN_MARK(5);
+#ifdef CCRD_SYN_TIMING
+  if (threadIdx.x == 0 && blockIdx.x < (1 << 16)) {
+    unsigned int sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    g_syn_timing[blockIdx.x][6] = sm;
+  }
+#endif
 }
+
+#ifdef CCRD_SYN_TIMING
+}  // namespace ccrd
+extern "C" int cc_debug_syn_timing(unsigned long long* host, int n_cta) {
+  return (int)cudaMemcpyFromSymbol(host, ccrd::g_syn_timing, sizeof(unsigned long long) * 8 * (size_t)n_cta);
+}
+namespace ccrd {
+#endif
 
 // ---------------------------------------------------------------- host launcher
 template <int L, int CH, int R, int K>
