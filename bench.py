@@ -239,6 +239,7 @@ def run_ours(args, rk):
                                 "frac": arm_tflops / FP32_PEAK_TFLOPS, "share": prof.arm_ms / ms},
             "synth_kernel": {"avg_ms": syn_avg_s * 1e3, "launches": prof.syn_launches, "tflops": syn_tflops,
                              "frac": syn_tflops / FP32_PEAK_TFLOPS, "share": prof.syn_ms / ms},
+            "pyramid_kernel": {"ms_total": prof.pyr_ms, "launches": prof.pyr_launches, "share": prof.pyr_ms / ms},
             "reduce_batch_kernel": {"ms_total": prof.reduce_ms, "launches": prof.reduce_launches},
         },
         "path_roofline": {"achieved_tflops_per_gpu": path_tflops, "frac": path_tflops / FP32_PEAK_TFLOPS,

@@ -142,8 +142,9 @@ int cc_arm_rate(const cc_model_desc* desc, const int16_t* latents, const float* 
                 void* workspace, size_t workspace_bytes, void* stream);
 
 /* Stage entry: upsampling only -- DEVICE dense [L][H][W] fp32 (PAPER.md:109-111,
- * "upsample the latents to a dense representation").  Runs the same fused
- * kernel as cc_rd_forward with its dense output enabled. */
+ * "upsample the latents to a dense representation").  Runs the same kernels as
+ * cc_rd_forward (coarse pyramid + fused last step) with the dense output of
+ * the synthesis kernel enabled.  Workspace: cc_workspace_bytes(desc, 1). */
 int cc_upsample(const cc_model_desc* desc, const int16_t* latents, const float* up_w,
                 float* dense, void* workspace, size_t workspace_bytes, void* stream);
 
@@ -179,8 +180,8 @@ int64_t cc_last_launch_count(void);
  * cc_profile_end() synchronises those events and returns the summed device
  * time per kernel kind.  Events only; no extra synchronisation in between. */
 typedef struct {
-  double arm_ms, syn_ms, reduce_ms;           /* summed event time per kind */
-  int64_t arm_launches, syn_launches, reduce_launches;
+  double arm_ms, syn_ms, reduce_ms, pyr_ms;   /* summed event time per kind */
+  int64_t arm_launches, syn_launches, reduce_launches, pyr_launches;
 } cc_profile_summary;
 int cc_profile_begin(void);
 int cc_profile_end(cc_profile_summary* out);

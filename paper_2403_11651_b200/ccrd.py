@@ -56,8 +56,9 @@ class CcMacBreakdown(C.Structure):
 
 
 class CcProfileSummary(C.Structure):
-    _fields_ = [("arm_ms", C.c_double), ("syn_ms", C.c_double), ("reduce_ms", C.c_double),
-                ("arm_launches", C.c_int64), ("syn_launches", C.c_int64), ("reduce_launches", C.c_int64)]
+    _fields_ = [("arm_ms", C.c_double), ("syn_ms", C.c_double), ("reduce_ms", C.c_double), ("pyr_ms", C.c_double),
+                ("arm_launches", C.c_int64), ("syn_launches", C.c_int64), ("reduce_launches", C.c_int64),
+                ("pyr_launches", C.c_int64)]
 
 
 # Symbols include/ccrd.h declares (checked by tests/test_abi.py).

@@ -13,7 +13,7 @@ static thread_local char g_err[512] = "";
 static thread_local int64_t g_launches = 0;
 
 // ---- optional per-kernel event timing (cc_profile_begin / cc_profile_end)
-enum { PK_ARM = 0, PK_SYN = 1, PK_RED = 2 };
+enum { PK_ARM = 0, PK_SYN = 1, PK_RED = 2, PK_PYR = 3 };
 struct ProfRec {
   int kind;
   cudaEvent_t a, b;
@@ -195,11 +195,30 @@ static int n_syn_ctas(const cc_model_desc& d) {
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+static void pyr_geom(const cc_model_desc& d, PyrGeom& g) {
+  memset(&g, 0, sizeof(g));
+  level_dims(d, g.lv, nullptr);
+  g.L = d.L;
+  int64_t off = 0;
+  for (int j = 1; j + 1 < d.L; j++) {  // S_j: grids j+1 .. L-1 at level j
+    g.s_off[j] = off;
+    off += (int64_t)(d.L - 1 - j) * g.lv.h[j] * g.lv.w[j];
+    off = (off + 63) & ~(int64_t)63;
+  }
+  g.s_floats = off;
+}
+
 // Workspace per image: ARM partials + synthesis partials (fp64) + a result
-// scratch slot used by the stage entries
+// scratch slot used by the stage entries + the upsampling pyramid S_1..S_{L-2}
 static size_t partial_bytes(const cc_model_desc& d) {
   return align256(sizeof(double) * (size_t)(n_arm_partials(d) + n_syn_ctas(d))) + align256(sizeof(cc_rd_result));
 }
+static size_t slice_bytes(const cc_model_desc& d) {
+  PyrGeom pg;
+  pyr_geom(d, pg);
+  return partial_bytes(d) + align256(sizeof(float) * (size_t)pg.s_floats);
+}
+static float* slice_pyr(const cc_model_desc& d, void* slice) { return (float*)((char*)slice + partial_bytes(d)); }
 
 // ------------------------------------------------------------- reduction
 // One CTA per image, fixed-order tree => bitwise deterministic.
@@ -264,28 +283,83 @@ static bool have_device(void) {
   return cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
 }
 
-// one image: ARM + fused upsample/synthesis
-static int forward_one(const cc_model_desc& d, const int16_t* lat, const float* arm_w, const float* up_w,
-                       const float* syn_w, const float* image, float* x_hat, double* part, cudaStream_t s) {
+// ARM rate of one image (per-warp partials at the start of `part`)
+static int arm_one(const cc_model_desc& d, const int16_t* lat, const float* arm_w, double* part, cudaStream_t s) {
   ArmGeom ag;
   arm_geom(d, ag);
-  SynGeom sg;
-  syn_geom(d, sg);
-  ArmLaunchFn arm = find_arm_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1);
-  SynLaunchFn syn = find_syn_launcher(d.L, d.syn_widths[1], d.syn_n_res, d.up_taps);
   {
     ProfScope ps(PK_ARM, s);
-    arm(ag, d, arm_w, lat, part, nullptr, nullptr, nullptr, s);
+    find_arm_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1)(ag, d, arm_w, lat, part, nullptr, nullptr,
+                                                                    nullptr, s);
   }
   g_launches++;
-  int rc = cuda_check("arm_rate_kernel");
-  if (rc) return rc;
+  return cuda_check("arm_rate_kernel");
+}
+
+// coarse upsampling pyramid of n images (batched launches)
+static int pyr_many(const cc_model_desc& d, const PyrImage* imgs, int n, cudaStream_t s) {
+  PyrGeom pg;
+  pyr_geom(d, pg);
+  {
+    ProfScope ps(PK_PYR, s);
+    launch_pyramid(pg, d.up_taps, imgs, n, s);
+  }
+  g_launches += pyramid_launch_count(pg, n);
+  return cuda_check("pyramid_kernel");
+}
+
+// fused last upsampling step + synthesis + distortion of one image
+static int syn_one(const cc_model_desc& d, const int16_t* lat, const float* s1, const float* up_w,
+                   const float* syn_w, const float* image, float* x_hat, float* dense_out, double* syn_part,
+                   cudaStream_t s) {
+  SynGeom sg;
+  syn_geom(d, sg);
   {
     ProfScope ps(PK_SYN, s);
-    syn(sg, d, up_w, syn_w, lat, nullptr, image, x_hat, nullptr, nullptr, part + n_arm_partials(d), s);
+    find_syn_launcher(d.L, d.syn_widths[1], d.syn_n_res, d.up_taps)(sg, d, up_w, syn_w, lat, s1, nullptr, image,
+                                                                    x_hat, dense_out, nullptr, syn_part, s);
   }
   g_launches++;
   return cuda_check("synth_kernel");
+}
+
+static PyrImage pyr_image(const cc_model_desc& d, const int16_t* lat, const float* up_w, float* S) {
+  PyrImage im;
+  im.lat = lat;
+  im.S = S;
+  for (int t = 0; t < 8; t++) im.k[t] = t < d.up_taps ? up_w[t] : 0.0f;
+  return im;
+}
+
+// whole path for images [0, n): ARM, pyramid, synthesis; slices of `per` bytes
+static int forward_batch(const cc_model_desc& d, const int16_t* const* lat, const float* const* arm_w,
+                         const float* const* up_w, const float* const* syn_w, const float* const* image,
+                         float* const* x_hat, char* slices, size_t per, int n, cudaStream_t s) {
+  PyrGeom pg;
+  pyr_geom(d, pg);
+  const int n_arm = n_arm_partials(d);
+  int rc;
+  // chunks of PYR_CHUNK images keep each chunk's pyramid resident in L2
+  // between the pyramid and the synthesis launches
+  constexpr int PYR_CHUNK = 8;
+  for (int b = 0; b < n; b += PYR_CHUNK) {
+    const int m = (n - b < PYR_CHUNK) ? n - b : PYR_CHUNK;
+    PyrImage imgs[PYR_CHUNK];
+    for (int i = 0; i < m; i++) {
+      char* sl = slices + per * (size_t)(b + i);
+      if ((rc = arm_one(d, lat[b + i], arm_w[b + i], (double*)sl, s))) return rc;
+      imgs[i] = pyr_image(d, lat[b + i], up_w[b + i], slice_pyr(d, sl));
+    }
+    if ((rc = pyr_many(d, imgs, m, s))) return rc;
+    for (int i = 0; i < m; i++) {
+      char* sl = slices + per * (size_t)(b + i);
+      const float* s1 = slice_pyr(d, sl) + pg.s_off[1];
+      if ((rc = syn_one(d, lat[b + i], s1, up_w[b + i], syn_w[b + i], image[b + i], x_hat[b + i], nullptr,
+                        (double*)sl + n_arm, s)))
+        return rc;
+    }
+  }
+  return CC_OK;
 }
 
 }  // namespace ccrd
@@ -329,6 +403,7 @@ int cc_profile_end(cc_profile_summary* out) {
     switch (P.recs[i].kind) {
       case PK_ARM: out->arm_ms += ms; out->arm_launches++; break;
       case PK_SYN: out->syn_ms += ms; out->syn_launches++; break;
+      case PK_PYR: out->pyr_ms += ms; out->pyr_launches++; break;
       default: out->reduce_ms += ms; out->reduce_launches++; break;
     }
   }
@@ -342,7 +417,7 @@ int cc_validate(const cc_model_desc* desc) { return validate(desc); }
 
 size_t cc_workspace_bytes(const cc_model_desc* desc, int32_t n_img) {
   if (validate(desc) != CC_OK || n_img < 1) return 0;
-  return partial_bytes(*desc) * (size_t)n_img;
+  return slice_bytes(*desc) * (size_t)n_img;
 }
 
 int cc_rd_forward(const cc_model_desc* desc, const cc_image_io* io, int32_t n_img, cc_rd_result* results,
@@ -351,7 +426,7 @@ int cc_rd_forward(const cc_model_desc* desc, const cc_image_io* io, int32_t n_im
   int rc = validate(desc);
   if (rc) return rc;
   if (!io || n_img < 1 || !results) return fail(CC_EINVAL, "io/results null or n_img < 1");
-  const size_t per = partial_bytes(*desc);
+  const size_t per = slice_bytes(*desc);
   const size_t need = per * (size_t)n_img;
   if (!workspace || workspace_bytes < need)
     return fail(CC_EWORKSPACE, "need %zu workspace bytes, got %zu", need, workspace_bytes);
@@ -361,16 +436,25 @@ int cc_rd_forward(const cc_model_desc* desc, const cc_image_io* io, int32_t n_im
   if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
   cudaStream_t s = (cudaStream_t)stream;
   char* slices = (char*)workspace;
-  ReduceJob jobs[MAX_JOBS_PER_LAUNCH];
   for (int b = 0; b < n_img; b += MAX_JOBS_PER_LAUNCH) {
     const int m = (n_img - b < MAX_JOBS_PER_LAUNCH) ? n_img - b : MAX_JOBS_PER_LAUNCH;
+    const int16_t* lat[MAX_JOBS_PER_LAUNCH];
+    const float *aw[MAX_JOBS_PER_LAUNCH], *uw[MAX_JOBS_PER_LAUNCH], *sw[MAX_JOBS_PER_LAUNCH],
+        *img[MAX_JOBS_PER_LAUNCH];
+    float* xh[MAX_JOBS_PER_LAUNCH];
+    ReduceJob jobs[MAX_JOBS_PER_LAUNCH];
     for (int i = 0; i < m; i++) {
       const cc_image_io& x = io[b + i];
-      double* part = (double*)(slices + per * (size_t)(b + i));
-      rc = forward_one(*desc, x.latents, x.arm_w, x.up_w, x.syn_w, x.image, x.x_hat, part, s);
-      if (rc) return rc;
-      jobs[i] = make_job(*desc, part);
+      lat[i] = x.latents;
+      aw[i] = x.arm_w;
+      uw[i] = x.up_w;
+      sw[i] = x.syn_w;
+      img[i] = x.image;
+      xh[i] = x.x_hat;
+      jobs[i] = make_job(*desc, (double*)(slices + per * (size_t)(b + i)));
     }
+    rc = forward_batch(*desc, lat, aw, uw, sw, img, xh, slices + per * (size_t)b, per, m, s);
+    if (rc) return rc;
     rc = launch_reduce(jobs, m, results + b, s);
     if (rc) return rc;
   }
@@ -390,7 +474,7 @@ static size_t stage_slot_bytes(const cc_model_desc& d) {
 
 size_t cc_workspace_bytes_host(const cc_model_desc* desc, int32_t n_img) {
   if (validate(desc) != CC_OK || n_img < 1) return 0;
-  return partial_bytes(*desc) * (size_t)n_img +
+  return slice_bytes(*desc) * (size_t)n_img +
          align256(sizeof(cc_rd_result) * (size_t)n_img) + 2 * stage_slot_bytes(*desc);
 }
 
@@ -405,7 +489,7 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
   if (!workspace || workspace_bytes < need)
     return fail(CC_EWORKSPACE, "need %zu workspace bytes, got %zu", need, workspace_bytes);
   if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
-  const size_t per = partial_bytes(d);
+  const size_t per = slice_bytes(d);
   char* ws = (char*)workspace;
   cc_rd_result* dres = (cc_rd_result*)(ws + per * (size_t)n_img);
   char* stage = ws + per * (size_t)n_img + align256(sizeof(cc_rd_result) * (size_t)n_img);
@@ -447,8 +531,10 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
     cudaEventRecord(copied[k], cs);
     cudaStreamWaitEvent(s, copied[k], 0);
     double* part = (double*)(ws + per * (size_t)i);
-    rc = forward_one(d, dlat, x.arm_w, x.up_w, x.syn_w, x.image ? dimg : nullptr, x.x_hat ? dxh : nullptr, part,
-                     s);
+    const int16_t* l1[1] = {dlat};
+    const float *a1[1] = {x.arm_w}, *u1[1] = {x.up_w}, *s1[1] = {x.syn_w}, *i1[1] = {x.image ? dimg : nullptr};
+    float* x1[1] = {x.x_hat ? dxh : nullptr};
+    rc = forward_batch(d, l1, a1, u1, s1, i1, x1, (char*)part, per, 1, s);
     if (rc) break;
     if (x.x_hat) cudaMemcpyAsync(x.x_hat, dxh, img_b, cudaMemcpyDeviceToHost, s);
     cudaEventRecord(consumed[k], s);
@@ -481,7 +567,7 @@ int cc_arm_rate(const cc_model_desc* desc, const int16_t* latents, const float* 
   if (!latents || !arm_w || !rate) return fail(CC_EINVAL, "null latents / arm_w / rate");
   const size_t per = partial_bytes(*desc);
   if (!workspace || workspace_bytes < per)
-    return fail(CC_EWORKSPACE, "need %zu workspace bytes", per);
+    return fail(CC_EWORKSPACE, "need %zu workspace bytes", per);  // <= cc_workspace_bytes(desc, 1)
   if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
   if ((mu || scale) && !bits) return fail(CC_EINVAL, "mu/scale debug outputs need bits != NULL");
   const cc_model_desc& d = *desc;
@@ -507,21 +593,24 @@ int cc_upsample(const cc_model_desc* desc, const int16_t* latents, const float* 
   int rc = validate(desc);
   if (rc) return rc;
   if (!latents || !up_w || !dense) return fail(CC_EINVAL, "null latents / up_w / dense");
-  (void)workspace;
-  (void)workspace_bytes;
-  if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
   const cc_model_desc& d = *desc;
-  SynGeom sg;
-  syn_geom(d, sg);
+  const size_t per = slice_bytes(d);
+  if (!workspace || workspace_bytes < per) return fail(CC_EWORKSPACE, "need %zu workspace bytes", per);
+  if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
+  cudaStream_t s = (cudaStream_t)stream;
+  // the production path (pyramid + fused last step) with its dense output on;
   // synthesis weights are irrelevant here: zero blob of the right size
+  PyrGeom pg;
+  pyr_geom(d, pg);
+  float* S = slice_pyr(d, workspace);
+  PyrImage im = pyr_image(d, latents, up_w, S);
+  if ((rc = pyr_many(d, &im, 1, s))) return rc;
   const int CH = d.syn_widths[1];
   const int nsyn = d.L * CH + CH + CH * 3 + 3 + 84 * d.syn_n_res;
   float* zeros = new float[nsyn]();
-  find_syn_launcher(d.L, CH, d.syn_n_res, d.up_taps)(sg, d, up_w, zeros, latents, nullptr, nullptr, nullptr,
-                                                      dense, nullptr, nullptr, (cudaStream_t)stream);
+  rc = syn_one(d, latents, S + pg.s_off[1], up_w, zeros, nullptr, nullptr, dense, nullptr, s);
   delete[] zeros;
-  g_launches++;
-  return cuda_check("synth_kernel(dense_out)");
+  return rc;
 }
 
 int cc_synthesize(const cc_model_desc* desc, const float* dense, const float* syn_w, const float* image,
@@ -539,8 +628,8 @@ int cc_synthesize(const cc_model_desc* desc, const float* dense, const float* sy
   if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
   cudaStream_t s = (cudaStream_t)stream;
   double* part = sse ? (double*)workspace : nullptr;
-  find_syn_launcher(d.L, d.syn_widths[1], d.syn_n_res, d.up_taps)(sg, d, nullptr, syn_w, nullptr, dense, image,
-                                                                   x_hat, nullptr, h_1x1, part, s);
+  find_syn_launcher(d.L, d.syn_widths[1], d.syn_n_res, d.up_taps)(sg, d, nullptr, syn_w, nullptr, nullptr, dense,
+                                                                   image, x_hat, nullptr, h_1x1, part, s);
   g_launches++;
   if ((rc = cuda_check("synth_kernel(dense_in)"))) return rc;
   if (sse) {

@@ -155,6 +155,7 @@ template <int L, int CH, int R, int K>
 struct SynParams {
   SynGeom g;
   const int16_t* lat;      // latents (chain mode)
+  const float* s1;         // S_1 = grids 2..L-1 upsampled to level 1, [L-2][h1][w1] (pyramid.cu)
   const float* dense_in;   // [L][H][W] (synthesize-from-dense mode) or null
   const float* image;      // [3][H][W] or null
   float* x_hat;            // [3][H][W] or null
@@ -163,6 +164,36 @@ struct SynParams {
   double* partial;         // [n tiles] per-CTA SSE partial sums
   SynWeights<L, CH, R, K> w;
 };
+
+// Coarse upsampling pyramid (pyramid.cu): S_j = grids j+1 .. L-1 at level j.
+constexpr int PYR_TH = 32;
+constexpr int PYR_TW = 64;
+constexpr int PYR_THREADS = 256;
+constexpr int PYR_MAX_IMG = 64;  // images per launch (kernel-parameter batch)
+
+struct PyrImage {
+  const int16_t* lat;  // packed latents of this image
+  float* S;            // this image's pyramid buffer (S_j at S + s_off[j])
+  float k[8];          // upsampling taps
+};
+
+struct PyrGeom {
+  LevelGeom lv;
+  int32_t L;
+  int64_t s_off[CC_MAX_LEVELS];  // float offset of S_j; S_j = [L-1-j][h_j][w_j]
+  int64_t s_floats;              // total floats per image
+};
+
+template <int K>
+struct PyrParams {
+  LevelGeom lv;
+  int32_t L, j, tiles_x;
+  int64_t s_off[CC_MAX_LEVELS];
+  PyrImage img[PYR_MAX_IMG];
+};
+
+int launch_pyramid(const PyrGeom& g, int K, const PyrImage* imgs, int n_img, cudaStream_t s);
+int pyramid_launch_count(const PyrGeom& g, int n_img);
 
 // Reduction of per-CTA partials into per-image results (deterministic, fp64).
 struct ReduceJob {
@@ -178,7 +209,7 @@ typedef int (*ArmLaunchFn)(const ArmGeom& g, const cc_model_desc& d, const float
                            const int16_t* lat, double* partial, float* mu, float* scale,
                            float* bits, cudaStream_t s);
 typedef int (*SynLaunchFn)(const SynGeom& g, const cc_model_desc& d, const float* up_w,
-                           const float* syn_w, const int16_t* lat, const float* dense_in,
+                           const float* syn_w, const int16_t* lat, const float* s1, const float* dense_in,
                            const float* image, float* x_hat, float* dense_out, float* h1_out,
                            double* partial, cudaStream_t s);
 

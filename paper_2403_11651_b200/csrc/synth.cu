@@ -3,12 +3,10 @@
 // One CTA produces a 32 x 64 tile of x_hat ("upsample the
 // latents to a dense representation and synthesize the decoded image";
 // Table 1 upsampling / synthesis columns; Eq. 1 distortion):
-//   1. upsampling chain in shared memory, coarse to fine.  The stack of grids
-//      l >= j is carried at resolution j over the window the tile needs; each
-//      x2 step is a separable stride-2 transposed conv (horizontal pass, then
-//      vertical pass).  Windows are NOT clipped to the grid: entries outside
-//      it hold the replicated edge value (replicate padding), so the taps
-//      never clamp; crop = never producing past the next level's size.
+//   1. last x2 upsampling step.  pyramid.cu has already carried grids 2..L-1
+//      to level 1 (S_1); the tile stages grid 1 + S_1 over its level-1 window
+//      (replicate padding = clamped reads) and runs the horizontal pass of the
+//      separable stride-2 transposed conv into shared memory.
 //   2. per PAIR of rows (2q, 2q+1) of the tile + halo: the last vertical step
 //      (both phases share the K/2 + 1 source rows) and the L -> C_h -> 3 1x1
 //      MLP for both pixels in registers (packed FFMA2, two neurons per
@@ -83,32 +81,37 @@ struct SynCtx {
   int* wlo_c;
 };
 
-// Latent staging: every thread first issues all of its loads, then stores
-// (compile-time trip counts, so the loads of every level are in flight
-// together).  Clamped reads = replicate-extended windows.
-template <int L, int CH, int R, int K, int LEV>
-struct LoadWindows {
+// Level-1 staging: slot 0 = grid 1 (int16 latents), slots 1 .. L-2 = S_1
+// (grids 2 .. L-1 already upsampled to level 1 by pyramid.cu), each over the
+// level-1 window, replicate-extended (clamped reads).  Every thread issues all
+// of its loads before the first store.
+template <int L, int CH, int R, int K>
+struct LoadLevel1 {
   using S = SynShape<L, CH, R, K>;
-  static constexpr int NR = wsize<K>(S::RH0, LEV), NC = wsize<K>(S::RW0, LEV);
+  static constexpr int NR = S::NR1, NC = S::NC1;
   static constexpr int IT = (NR * NC + SYN_THREADS - 1) / SYN_THREADS;
   static __device__ __forceinline__ void run(const SynParams<L, CH, R, K>& p, const SynCtx& c) {
-    const int16_t* g = p.lat + p.g.lv.off[LEV];
-    const int gh = p.g.lv.h[LEV], gw = p.g.lv.w[LEV];
-    const int lr = c.wlo_r[LEV], lc = c.wlo_c[LEV];
-    int16_t v[IT];
+    const int gh = p.g.lv.h[1], gw = p.g.lv.w[1];
+    const int lr = c.wlo_r[1], lc = c.wlo_c[1];
+    const int16_t* g1 = p.lat + p.g.lv.off[1];
+    float v[L - 1][IT];
 #pragma unroll
     for (int k = 0; k < IT; k++) {
       const int it = threadIdx.x + k * SYN_THREADS;
       const int rr = it / NC, cc = it - rr * NC;
-      v[k] = (it < NR * NC) ? __ldg(g + (int64_t)clampi(lr + rr, 0, gh - 1) * gw + clampi(lc + cc, 0, gw - 1)) : 0;
-    }
-    if constexpr (LEV > 1) LoadWindows<L, CH, R, K, LEV - 1>::run(p, c);
-    float* dst = c.stack + (LEV - 1) * S::SLOT;
+      const int64_t gi = (int64_t)clampi(lr + rr, 0, gh - 1) * gw + clampi(lc + cc, 0, gw - 1);
+      const bool ok = it < NR * NC;
+      v[0][k] = ok ? (float)__ldg(g1 + gi) : 0.0f;
 #pragma unroll
-    for (int k = 0; k < IT; k++) {
-      const int it = threadIdx.x + k * SYN_THREADS;
-      if (it < NR * NC) dst[it] = (float)v[k];
+      for (int sl = 1; sl < L - 1; sl++) v[sl][k] = ok ? __ldg(p.s1 + (int64_t)(sl - 1) * gh * gw + gi) : 0.0f;
     }
+#pragma unroll
+    for (int sl = 0; sl < L - 1; sl++)
+#pragma unroll
+      for (int k = 0; k < IT; k++) {
+        const int it = threadIdx.x + k * SYN_THREADS;
+        if (it < NR * NC) c.stack[sl * S::SLOT + it] = v[sl][k];
+      }
   }
 };
 
@@ -134,8 +137,9 @@ struct LoadLat0 {
   }
 };
 
-// One x2 step of the chain, from level J+1 to level J, for every grid l > J
-// (stack slots J .. L-2).  out[2q + r] = sum_t k[2t + 1 - r] g[q + r + K/4 - 1 - t]
+// Horizontal pass of the x2 step from level J+1 to level J (J = 0 here) for
+// every grid l > J (stack slots J .. L-2); the vertical pass of the last step is
+// done per pixel pair in phase 2.  out[2q + r] = sum_t k[2t + 1 - r] g[q + r + K/4 - 1 - t]
 // (stride-2 transposed conv on the replicate-extended input, DESIGN.md readings
 // #12-#13): the even and odd outputs share the K/2 + 1 sources
 // g[q - K/4 .. q + K/4]; replicate padding = clamping the SOURCE index.
@@ -177,40 +181,7 @@ struct ChainStep {
       }
     }
     __syncthreads();
-    if constexpr (J > 0) {
-      // ---- vertical: (rows of window J) x (cols of window J); each thread
-      //      slides a (K/2 + 1)-row register window down one column
-      const int hs = p.g.lv.h[J + 1], lo_s = c.wlo_r[J + 1];
-      const int q0 = c.wlo_r[J] >> 1;
-#pragma unroll 1
-      for (int it = threadIdx.x; it < NSL * NCd; it += SYN_THREADS) {
-        const int sl = it / NCd, col = it - sl * NCd;
-        const float* src = c.tmph + (J + sl) * S::TSLOT + col;
-        float* dst = c.stack + (J + sl) * S::SLOT + col;
-        float sv[K / 2 + 1];
-#pragma unroll
-        for (int u = 0; u < K / 2; u++) sv[u] = src[(clampi(q0 - K / 4 + u, 0, hs - 1) - lo_s) * NCd];
-#pragma unroll 2
-        for (int rp = 0; rp < NRd / 2; rp++) {
-          const int q = q0 + rp;
-          sv[K / 2] = src[(clampi(q + K / 4, 0, hs - 1) - lo_s) * NCd];
-          float a0 = 0.0f, a1 = 0.0f;
-#pragma unroll
-          for (int t = 0; t < K / 2; t++) {
-            a0 = fmaf(kk[2 * t + 1], sv[K / 2 - 1 - t], a0);
-            a1 = fmaf(kk[2 * t], sv[K / 2 - t], a1);
-          }
-          dst[(2 * rp) * NCd] = a0;
-          dst[(2 * rp + 1) * NCd] = a1;
-#pragma unroll
-          for (int u = 0; u < K / 2; u++) sv[u] = sv[u + 1];
-        }
-      }
-      __syncthreads();  // grid J was staged into slot J - 1 up front
-      ChainStep<L, CH, R, K, J - 1>::run(p, c);
-    }
   }
-
 };
 
 template <int L, int CH, int R, int K, bool DENSE_IN>
@@ -247,17 +218,16 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
 
   // ---------------------------------------------------------------- 1. chain
   if constexpr (!DENSE_IN) {
-    // all latent windows up front (many loads in flight): level 0's region
-    // (int16) and every grid l >= 1 into its stack slot, which no chain step
-    // touches before grid l is needed (clamped reads = replicate padding).
+    // level 0's region (int16) and the level-1 stack (grid 1 + S_1), all
+    // loads in flight together (clamped reads = replicate padding)
     SYN_MARK(0);
     LoadLat0<L, CH, R, K>::run(p, lat0, RY, RX);
     if constexpr (L > 1) {
       SynCtx c{bufA, bufB, wlo_r, wlo_c};
-      LoadWindows<L, CH, R, K, L - 1>::run(p, c);
+      LoadLevel1<L, CH, R, K>::run(p, c);
       __syncthreads();
       SYN_MARK(1);
-      ChainStep<L, CH, R, K, L - 2>::run(p, c);
+      ChainStep<L, CH, R, K, 0>::run(p, c);  // last step's horizontal pass
       SYN_MARK(2);
     } else {
       __syncthreads();
@@ -586,13 +556,14 @@ namespace ccrd {
 // ---------------------------------------------------------------- host launcher
 template <int L, int CH, int R, int K>
 static int launch_syn(const SynGeom& g, const cc_model_desc& d, const float* up_w,
-                      const float* syn_w, const int16_t* lat, const float* dense_in,
+                      const float* syn_w, const int16_t* lat, const float* s1, const float* dense_in,
                       const float* image, float* x_hat, float* dense_out, float* h1_out,
                       double* partial, cudaStream_t stream) {
   (void)d;
   SynParams<L, CH, R, K> p;
   p.g = g;
   p.lat = lat;
+  p.s1 = s1;
   p.dense_in = dense_in;
   p.image = image;
   p.x_hat = x_hat;

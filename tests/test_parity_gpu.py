@@ -143,7 +143,9 @@ def test_upsample_stage_per_level(filt):
         d = P.desc_from_config(cfg)
         lat = torch.from_numpy(im.latents).cuda()
         dense = torch.zeros((cfg.L, H, W), device="cuda")
-        P.cc_upsample(d, lat.data_ptr(), im.up_w, dense.data_ptr())
+        ws_b = P.cc_workspace_bytes(d, 1)
+        ws = torch.empty(ws_b, dtype=torch.uint8, device="cuda")
+        P.cc_upsample(d, lat.data_ptr(), im.up_w, dense.data_ptr(), ws.data_ptr(), ws_b)
         torch.cuda.synchronize()
         ref, _ = oracle.upsample(oracle.model(cfg), im.latents, im.up_w)
         got = dense.cpu().numpy().astype(np.float64)
