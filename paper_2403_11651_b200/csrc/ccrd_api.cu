@@ -331,33 +331,59 @@ static PyrImage pyr_image(const cc_model_desc& d, const int16_t* lat, const floa
   return im;
 }
 
-// whole path for images [0, n): ARM, pyramid, synthesis; slices of `per` bytes
+// Side stream for the upsampling pyramid (lazily created, one per host
+// thread): the pyramid is latency-bound and independent of the ARM, so it runs
+// concurrently with the ARM launches and is joined before the synthesis.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  int device = -1;
+};
+static thread_local SideStream g_side;
+
+static int side_stream(SideStream** out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cuda_check("cudaGetDevice");
+  if (g_side.s == nullptr || g_side.device != dev) {
+    if (cudaStreamCreateWithFlags(&g_side.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_side.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_side.join, cudaEventDisableTiming) != cudaSuccess)
+      return cuda_check("side stream");
+    g_side.device = dev;
+  }
+  *out = &g_side;
+  return CC_OK;
+}
+
+// whole path for images [0, n): pyramid (side stream) || ARM, then synthesis;
+// per-image workspace slices of `per` bytes
 static int forward_batch(const cc_model_desc& d, const int16_t* const* lat, const float* const* arm_w,
                          const float* const* up_w, const float* const* syn_w, const float* const* image,
-                         float* const* x_hat, char* slices, size_t per, int n, cudaStream_t s) {
+                         float* const* x_hat, char* slices, size_t per, int n, cudaStream_t s, bool overlap) {
   PyrGeom pg;
   pyr_geom(d, pg);
   const int n_arm = n_arm_partials(d);
   int rc;
-  // chunks of PYR_CHUNK images keep each chunk's pyramid resident in L2
-  // between the pyramid and the synthesis launches
-  constexpr int PYR_CHUNK = 8;
-  for (int b = 0; b < n; b += PYR_CHUNK) {
-    const int m = (n - b < PYR_CHUNK) ? n - b : PYR_CHUNK;
-    PyrImage imgs[PYR_CHUNK];
-    for (int i = 0; i < m; i++) {
-      char* sl = slices + per * (size_t)(b + i);
-      if ((rc = arm_one(d, lat[b + i], arm_w[b + i], (double*)sl, s))) return rc;
-      imgs[i] = pyr_image(d, lat[b + i], up_w[b + i], slice_pyr(d, sl));
-    }
-    if ((rc = pyr_many(d, imgs, m, s))) return rc;
-    for (int i = 0; i < m; i++) {
-      char* sl = slices + per * (size_t)(b + i);
-      const float* s1 = slice_pyr(d, sl) + pg.s_off[1];
-      if ((rc = syn_one(d, lat[b + i], s1, up_w[b + i], syn_w[b + i], image[b + i], x_hat[b + i], nullptr,
-                        (double*)sl + n_arm, s)))
-        return rc;
-    }
+  PyrImage imgs[MAX_JOBS_PER_LAUNCH];
+  for (int i = 0; i < n; i++) imgs[i] = pyr_image(d, lat[i], up_w[i], slice_pyr(d, slices + per * (size_t)i));
+  SideStream* side = nullptr;
+  if (overlap && pg.L >= 3) {
+    if ((rc = side_stream(&side))) return rc;
+    cudaEventRecord(side->fork, s);
+    cudaStreamWaitEvent(side->s, side->fork, 0);
+    if ((rc = pyr_many(d, imgs, n, side->s))) return rc;
+    cudaEventRecord(side->join, side->s);
+  } else if ((rc = pyr_many(d, imgs, n, s))) {
+    return rc;
+  }
+  for (int i = 0; i < n; i++)
+    if ((rc = arm_one(d, lat[i], arm_w[i], (double*)(slices + per * (size_t)i), s))) return rc;
+  if (side) cudaStreamWaitEvent(s, side->join, 0);
+  for (int i = 0; i < n; i++) {
+    char* sl = slices + per * (size_t)i;
+    const float* s1 = slice_pyr(d, sl) + pg.s_off[1];
+    if ((rc = syn_one(d, lat[i], s1, up_w[i], syn_w[i], image[i], x_hat[i], nullptr, (double*)sl + n_arm, s)))
+      return rc;
   }
   return CC_OK;
 }
@@ -453,7 +479,7 @@ int cc_rd_forward(const cc_model_desc* desc, const cc_image_io* io, int32_t n_im
       xh[i] = x.x_hat;
       jobs[i] = make_job(*desc, (double*)(slices + per * (size_t)(b + i)));
     }
-    rc = forward_batch(*desc, lat, aw, uw, sw, img, xh, slices + per * (size_t)b, per, m, s);
+    rc = forward_batch(*desc, lat, aw, uw, sw, img, xh, slices + per * (size_t)b, per, m, s, false);
     if (rc) return rc;
     rc = launch_reduce(jobs, m, results + b, s);
     if (rc) return rc;
@@ -534,7 +560,7 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
     const int16_t* l1[1] = {dlat};
     const float *a1[1] = {x.arm_w}, *u1[1] = {x.up_w}, *s1[1] = {x.syn_w}, *i1[1] = {x.image ? dimg : nullptr};
     float* x1[1] = {x.x_hat ? dxh : nullptr};
-    rc = forward_batch(d, l1, a1, u1, s1, i1, x1, (char*)part, per, 1, s);
+    rc = forward_batch(d, l1, a1, u1, s1, i1, x1, (char*)part, per, 1, s, false);
     if (rc) break;
     if (x.x_hat) cudaMemcpyAsync(x.x_hat, dxh, img_b, cudaMemcpyDeviceToHost, s);
     cudaEventRecord(consumed[k], s);

@@ -168,7 +168,10 @@ struct SynParams {
 // Coarse upsampling pyramid (pyramid.cu): S_j = grids j+1 .. L-1 at level j.
 constexpr int PYR_TH = 32;
 constexpr int PYR_TW = 64;
-constexpr int PYR_THREADS = 256;
+#ifndef CCRD_PYR_THREADS
+#define CCRD_PYR_THREADS 256
+#endif
+constexpr int PYR_THREADS = CCRD_PYR_THREADS;
 constexpr int PYR_MAX_IMG = 64;  // images per launch (kernel-parameter batch)
 
 struct PyrImage {

@@ -20,77 +20,68 @@ __global__ void __launch_bounds__(PYR_THREADS)
     pyramid_kernel(const __grid_constant__ PyrParams<K> p) {
   constexpr int SR = PYR_TH / 2 + K / 2;  // source rows of a tile
   constexpr int SC = PYR_TW / 2 + K / 2;  // source cols
-  __shared__ float sw[SR][SC];
-  __shared__ float tmp[SR][PYR_TW];
+  extern __shared__ float psm[];
   const PyrImage& im = p.img[blockIdx.y];
   const int j = p.j;
+  const int nch = p.L - 1 - j;
+  float* sw = psm;                       // [nch][SR][SC]
+  float* tmp = psm + nch * SR * SC;      // [nch][SR][PYR_TW]
   const int hj = p.lv.h[j], wj = p.lv.w[j];
   const int hs = p.lv.h[j + 1], ws = p.lv.w[j + 1];
   const int ty = blockIdx.x / p.tiles_x;
   const int Y0 = ty * PYR_TH, X0 = (blockIdx.x - ty * p.tiles_x) * PYR_TW;
   const int r0 = (Y0 >> 1) - K / 4, c0 = (X0 >> 1) - K / 4;  // source window origin
-  const int nch = p.L - 1 - j;
   float* Sj = im.S + p.s_off[j];
   const float* Sn = im.S + p.s_off[j + 1];  // S_{j+1}, nch - 1 channels
   const int16_t* lat = im.lat + p.lv.off[j + 1];
 
-#pragma unroll 1
-  for (int k = 0; k < nch; k++) {
-    // source window, replicate-extended (clamped) ---------------------------
-    constexpr int N = SR * SC;
-    constexpr int IT = (N + PYR_THREADS - 1) / PYR_THREADS;
-    float v[IT];
-#pragma unroll
-    for (int u = 0; u < IT; u++) {
-      const int it = threadIdx.x + u * PYR_THREADS;
-      const int rr = it / SC, cc = it - rr * SC;
-      const int64_t gi = (int64_t)clampi(r0 + rr, 0, hs - 1) * ws + clampi(c0 + cc, 0, ws - 1);
-      v[u] = 0.0f;
-      if (it < N) v[u] = (k == 0) ? (float)__ldg(lat + gi) : __ldg(Sn + (int64_t)(k - 1) * hs * ws + gi);
-    }
-#pragma unroll
-    for (int u = 0; u < IT; u++) {
-      const int it = threadIdx.x + u * PYR_THREADS;
-      if (it < N) (&sw[0][0])[it] = v[u];
-    }
-    __syncthreads();
-    // horizontal: column pairs (2q, 2q+1) share sources q - K/4 .. q + K/4 --
+  // source windows of every channel, replicate-extended (clamped) ------------
+#pragma unroll 4
+  for (int it = threadIdx.x; it < nch * SR * SC; it += PYR_THREADS) {
+    const int k = it / (SR * SC), rem = it - k * (SR * SC);
+    const int rr = rem / SC, cc = rem - rr * SC;
+    const int64_t gi = (int64_t)clampi(r0 + rr, 0, hs - 1) * ws + clampi(c0 + cc, 0, ws - 1);
+    sw[it] = (k == 0) ? (float)__ldg(lat + gi) : __ldg(Sn + (int64_t)(k - 1) * hs * ws + gi);
+  }
+  __syncthreads();
+  // horizontal: column pairs (2q, 2q+1) share sources q - K/4 .. q + K/4 ----
 #pragma unroll 2
-    for (int it = threadIdx.x; it < SR * (PYR_TW / 2); it += PYR_THREADS) {
-      const int rr = it / (PYR_TW / 2), cp = it - rr * (PYR_TW / 2);
-      float s[K / 2 + 1];
+  for (int it = threadIdx.x; it < nch * SR * (PYR_TW / 2); it += PYR_THREADS) {
+    const int row = it / (PYR_TW / 2), cp = it - row * (PYR_TW / 2);  // row = k * SR + rr
+    const float* src = sw + row * SC + cp;
+    float s[K / 2 + 1];
 #pragma unroll
-      for (int u = 0; u <= K / 2; u++) s[u] = sw[rr][cp + u];
-      float a0 = 0.0f, a1 = 0.0f;
+    for (int u = 0; u <= K / 2; u++) s[u] = src[u];
+    float a0 = 0.0f, a1 = 0.0f;
 #pragma unroll
-      for (int t = 0; t < K / 2; t++) {
-        a0 = fmaf(im.k[2 * t + 1], s[K / 2 - 1 - t], a0);
-        a1 = fmaf(im.k[2 * t], s[K / 2 - t], a1);
-      }
-      *reinterpret_cast<float2*>(&tmp[rr][2 * cp]) = make_float2(a0, a1);
+    for (int t = 0; t < K / 2; t++) {
+      a0 = fmaf(im.k[2 * t + 1], s[K / 2 - 1 - t], a0);
+      a1 = fmaf(im.k[2 * t], s[K / 2 - t], a1);
     }
-    __syncthreads();
-    // vertical: row pairs, stored (cropped) to S_j[k] ------------------------
+    *reinterpret_cast<float2*>(tmp + row * PYR_TW + 2 * cp) = make_float2(a0, a1);
+  }
+  __syncthreads();
+  // vertical: row pairs, stored (cropped) to S_j[k] ----------------------------
 #pragma unroll 2
-    for (int it = threadIdx.x; it < (PYR_TH / 2) * PYR_TW; it += PYR_THREADS) {
-      const int rp = it / PYR_TW, cc = it - rp * PYR_TW;
-      float s[K / 2 + 1];
+  for (int it = threadIdx.x; it < nch * (PYR_TH / 2) * PYR_TW; it += PYR_THREADS) {
+    const int kr = it / PYR_TW, cc = it - kr * PYR_TW;
+    const int k = kr / (PYR_TH / 2), rp = kr - k * (PYR_TH / 2);
+    const float* src = tmp + (k * SR + rp) * PYR_TW + cc;
+    float s[K / 2 + 1];
 #pragma unroll
-      for (int u = 0; u <= K / 2; u++) s[u] = tmp[rp + u][cc];
-      float a0 = 0.0f, a1 = 0.0f;
+    for (int u = 0; u <= K / 2; u++) s[u] = src[u * PYR_TW];
+    float a0 = 0.0f, a1 = 0.0f;
 #pragma unroll
-      for (int t = 0; t < K / 2; t++) {
-        a0 = fmaf(im.k[2 * t + 1], s[K / 2 - 1 - t], a0);
-        a1 = fmaf(im.k[2 * t], s[K / 2 - t], a1);
-      }
-      const int y = Y0 + 2 * rp, x = X0 + cc;
-      if (x < wj) {
-        float* dst = Sj + (int64_t)k * hj * wj + (int64_t)y * wj + x;
-        if (y < hj) dst[0] = a0;
-        if (y + 1 < hj) dst[wj] = a1;
-      }
+    for (int t = 0; t < K / 2; t++) {
+      a0 = fmaf(im.k[2 * t + 1], s[K / 2 - 1 - t], a0);
+      a1 = fmaf(im.k[2 * t], s[K / 2 - t], a1);
     }
-    __syncthreads();
+    const int y = Y0 + 2 * rp, x = X0 + cc;
+    if (x < wj) {
+      float* dst = Sj + (int64_t)k * hj * wj + (int64_t)y * wj + x;
+      if (y < hj) dst[0] = a0;
+      if (y + 1 < hj) dst[wj] = a1;
+    }
   }
 }
 
@@ -107,7 +98,11 @@ static int launch_pyr(const PyrGeom& g, const PyrImage* imgs, int n_img, cudaStr
     for (int b = 0; b < n_img; b += PYR_MAX_IMG) {
       const int m = (n_img - b < PYR_MAX_IMG) ? n_img - b : PYR_MAX_IMG;
       for (int i = 0; i < m; i++) p.img[i] = imgs[b + i];
-      pyramid_kernel<K><<<dim3(tiles, m), PYR_THREADS, 0, s>>>(p);
+      constexpr int SR = PYR_TH / 2 + K / 2, SC = PYR_TW / 2 + K / 2;
+      const size_t smem = sizeof(float) * (size_t)(g.L - 1 - j) * SR * (SC + PYR_TW);
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(pyramid_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      pyramid_kernel<K><<<dim3(tiles, m), PYR_THREADS, smem, s>>>(p);
     }
   }
   return 0;

@@ -184,6 +184,84 @@ struct ChainStep {
   }
 };
 
+// 1x1 synthesis layers L -> CH (ReLU) -> 3 (ReLU unless R == 0: the module's
+// last layer) for two pixels; every uniform weight (pair) feeds both.
+template <int L, int CH, int R, int K>
+__device__ __forceinline__ void mlp_2px(const SynParams<L, CH, R, K>& p, const float (&v0)[L], const float (&v1)[L],
+                                        float (&out0)[3], float (&out1)[3]) {
+  uint64_t acc0[CH / 2], acc1[CH / 2];
+#pragma unroll
+  for (int n = 0; n < CH / 2; n++) acc0[n] = acc1[n] = ldp2(p.w.a0[n]);
+#pragma unroll
+  for (int i = 0; i < L; i++) {
+    const uint64_t x0 = f2pack(v0[i], v0[i]), x1 = f2pack(v1[i], v1[i]);
+#pragma unroll
+    for (int n = 0; n < CH / 2; n++) {
+      const uint64_t wgt = ldp2(p.w.A0[i][n]);
+      acc0[n] = ffma2(x0, wgt, acc0[n]);
+      acc1[n] = ffma2(x1, wgt, acc1[n]);
+    }
+  }
+  uint64_t o0 = f2pack(p.w.a1[0], p.w.a1[1]), o1 = o0;
+  float o0s = p.w.a1[2], o1s = p.w.a1[2];
+#pragma unroll
+  for (int n = 0; n < CH / 2; n++) {
+    const float2 h0 = f2unpack(acc0[n]), h1v = f2unpack(acc1[n]);
+    const float h0a = fmaxf(h0.x, 0.0f), h0b = fmaxf(h0.y, 0.0f);
+    const float h1a = fmaxf(h1v.x, 0.0f), h1b = fmaxf(h1v.y, 0.0f);
+    const uint64_t wa = ldp2(p.w.A1p[2 * n]), wb = ldp2(p.w.A1p[2 * n + 1]);
+    o0 = ffma2(f2pack(h0a, h0a), wa, o0);
+    o1 = ffma2(f2pack(h1a, h1a), wa, o1);
+    o0s = fmaf(h0a, p.w.A1s[2 * n], o0s);
+    o1s = fmaf(h1a, p.w.A1s[2 * n], o1s);
+    o0 = ffma2(f2pack(h0b, h0b), wb, o0);
+    o1 = ffma2(f2pack(h1b, h1b), wb, o1);
+    o0s = fmaf(h0b, p.w.A1s[2 * n + 1], o0s);
+    o1s = fmaf(h1b, p.w.A1s[2 * n + 1], o1s);
+  }
+  const float2 r0 = f2unpack(o0), r1 = f2unpack(o1);
+  out0[0] = r0.x; out0[1] = r0.y; out0[2] = o0s;
+  out1[0] = r1.x; out1[1] = r1.y; out1[2] = o1s;
+  if (R > 0) {
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      out0[c] = fmaxf(out0[c], 0.0f);
+      out1[c] = fmaxf(out1[c], 0.0f);
+    }
+  }
+}
+
+// the same for one pixel (same FMA order, fewer live registers)
+template <int L, int CH, int R, int K>
+__device__ __forceinline__ void mlp_1px(const SynParams<L, CH, R, K>& p, const float (&v)[L], float (&out)[3]) {
+  uint64_t acc[CH / 2];
+#pragma unroll
+  for (int n = 0; n < CH / 2; n++) acc[n] = ldp2(p.w.a0[n]);
+#pragma unroll
+  for (int i = 0; i < L; i++) {
+    const uint64_t x = f2pack(v[i], v[i]);
+#pragma unroll
+    for (int n = 0; n < CH / 2; n++) acc[n] = ffma2(x, ldp2(p.w.A0[i][n]), acc[n]);
+  }
+  uint64_t o = f2pack(p.w.a1[0], p.w.a1[1]);
+  float os = p.w.a1[2];
+#pragma unroll
+  for (int n = 0; n < CH / 2; n++) {
+    const float2 h = f2unpack(acc[n]);
+    const float ha = fmaxf(h.x, 0.0f), hb = fmaxf(h.y, 0.0f);
+    o = ffma2(f2pack(ha, ha), ldp2(p.w.A1p[2 * n]), o);
+    os = fmaf(ha, p.w.A1s[2 * n], os);
+    o = ffma2(f2pack(hb, hb), ldp2(p.w.A1p[2 * n + 1]), o);
+    os = fmaf(hb, p.w.A1s[2 * n + 1], os);
+  }
+  const float2 r = f2unpack(o);
+  out[0] = r.x; out[1] = r.y; out[2] = os;
+  if (R > 0) {
+#pragma unroll
+    for (int c = 0; c < 3; c++) out[c] = fmaxf(out[c], 0.0f);
+  }
+}
+
 template <int L, int CH, int R, int K, bool DENSE_IN>
 __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
     synth_kernel(const __grid_constant__ SynParams<L, CH, R, K> p) {
@@ -293,47 +371,13 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
           if (in1) p.dense_out[l * P + (int64_t)(y0 + 1) * W + x] = v1[l];
         }
       }
-      // layer 0: L -> CH (ReLU), two pixels share every weight load
-      uint64_t acc0[CH / 2], acc1[CH / 2];
-#pragma unroll
-      for (int n = 0; n < CH / 2; n++) acc0[n] = acc1[n] = ldp2(p.w.a0[n]);
-#pragma unroll
-      for (int i = 0; i < L; i++) {
-        const uint64_t x0 = f2pack(v0[i], v0[i]), x1 = f2pack(v1[i], v1[i]);
-#pragma unroll
-        for (int n = 0; n < CH / 2; n++) {
-          const uint64_t wgt = ldp2(p.w.A0[i][n]);
-          acc0[n] = ffma2(x0, wgt, acc0[n]);
-          acc1[n] = ffma2(x1, wgt, acc1[n]);
-        }
-      }
-      // layer 1: CH -> 3 (ReLU unless it is the module's last layer, R == 0)
-      uint64_t o0 = f2pack(p.w.a1[0], p.w.a1[1]), o1 = o0;
-      float o0s = p.w.a1[2], o1s = p.w.a1[2];
-#pragma unroll
-      for (int n = 0; n < CH / 2; n++) {
-        const float2 h0 = f2unpack(acc0[n]), h1v = f2unpack(acc1[n]);
-        const float h0a = fmaxf(h0.x, 0.0f), h0b = fmaxf(h0.y, 0.0f);
-        const float h1a = fmaxf(h1v.x, 0.0f), h1b = fmaxf(h1v.y, 0.0f);
-        const uint64_t wa = ldp2(p.w.A1p[2 * n]), wb = ldp2(p.w.A1p[2 * n + 1]);
-        o0 = ffma2(f2pack(h0a, h0a), wa, o0);
-        o1 = ffma2(f2pack(h1a, h1a), wa, o1);
-        o0s = fmaf(h0a, p.w.A1s[2 * n], o0s);
-        o1s = fmaf(h1a, p.w.A1s[2 * n], o1s);
-        o0 = ffma2(f2pack(h0b, h0b), wb, o0);
-        o1 = ffma2(f2pack(h1b, h1b), wb, o1);
-        o0s = fmaf(h0b, p.w.A1s[2 * n + 1], o0s);
-        o1s = fmaf(h1b, p.w.A1s[2 * n + 1], o1s);
-      }
-      const float2 r0 = f2unpack(o0), r1 = f2unpack(o1);
-      float out0[3] = {r0.x, r0.y, o0s}, out1[3] = {r1.x, r1.y, o1s};
-      if (R > 0) {
-#pragma unroll
-        for (int c = 0; c < 3; c++) {
-          out0[c] = fmaxf(out0[c], 0.0f);
-          out1[c] = fmaxf(out1[c], 0.0f);
-        }
-      }
+      float out0[3], out1[3];
+#ifdef CCRD_SYN_MLP1
+      mlp_1px<L, CH, R, K>(p, v0, out0);
+      mlp_1px<L, CH, R, K>(p, v1, out1);
+#else
+      mlp_2px<L, CH, R, K>(p, v0, v1, out0, out1);
+#endif
       if (p.h1_out != nullptr) {
 #pragma unroll
         for (int c = 0; c < 3; c++) {
