@@ -255,6 +255,95 @@ def run_ours(args, rk):
         print(json.dumps(out), flush=True)
 
 
+def run_strip(args, rk):
+    """BASELINE.json configs[4]: ONE 4320x7680 image split into horizontal
+    strips, one per rank (strong scaling).  A step = the halo exchange of
+    latent rows (grouped NCCL send/recv into the window buffers; none at N=1),
+    cc_rd_forward_strip on every rank, and the all-reduce of the additive
+    (rate, sse, mse, cost) shares."""
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2403_11651_b200 as P
+    from paper_2403_11651_b200 import dist
+
+    cfg = workload.CONFIGS[args.config]
+    dev = torch.device("cuda", rk.local_rank)
+    torch.cuda.set_device(dev)
+    P.load()
+    desc = P.desc_from_config(cfg)
+    strips, lays = dist.strip_layouts(desc, rk.world)
+    st, lay = strips[rk.rank], lays[rk.rank]
+    t0 = time.perf_counter()
+    im = workload.make_image(cfg, workload.image_seed(args.seed, 0))
+    gen_s = time.perf_counter() - t0
+    dims = cfg.level_dims()
+    off = [sum(h * w for h, w in dims[:l]) for l in range(cfg.L)]
+    ds = P.ccrd.DeviceStrip(cfg, st, im.arm_w, im.up_w, im.syn_w, image_rows=im.image[:, st.r0:st.r1], device=dev)
+    # this rank's bitstream share: its owned latent rows only; halos arrive by exchange
+    ds.lat.copy_(dist.pack_window(torch.from_numpy(im.latents), off, lay, owned_only=True).to(dev))
+    macs = P.cc_mac_per_pixel(desc)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    halo_bytes = [0]
+
+    def step():
+        halo_bytes[0] = dist.exchange_halos(ds.lat, lays, rk.rank)
+        r = ds.forward(sptr)
+        if rk.world > 1:
+            tdist.all_reduce(r, op=tdist.ReduceOp.SUM)
+        return r
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(rk.local_rank)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    P.ccrd.cc_profile_begin()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    launches = 0
+    for _ in range(args.steps):
+        res = step()
+        launches += P.ccrd.cc_last_launch_count()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    sampler.stop()
+    prof = P.ccrd.cc_profile_end()
+    ms = ev0.elapsed_time(ev1)
+    ms_max = dist.max_over_ranks(ms, device=dev)
+    value = cfg.H * cfg.W * args.steps / (ms_max / 1e3)
+    resn = res.cpu().numpy()
+    assert np.isfinite(resn).all() and resn[0] > 0
+    arm_avg_s = prof.arm_ms / max(1, prof.arm_launches) / 1e3
+    own_lat = sum((st.own_hi[l] - st.own_lo[l]) * dims[l][1] for l in range(cfg.L))
+    arm_pl = sum(cfg.arm_widths[k] * cfg.arm_widths[k + 1] for k in range(len(cfg.arm_widths) - 1))
+    arm_tflops = 2.0 * own_lat * arm_pl / arm_avg_s / 1e12
+    path_tflops = 2.0 * macs.total * value / rk.world / 1e12
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": rk.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"8k: one {cfg.H}x{cfg.W} RGB image in {rk.world} horizontal strip(s), L={cfg.L}, "
+                               f"ARM {list(cfg.arm_widths)} C={cfg.n_ctx}, synthesis {list(cfg.syn_widths)}+"
+                               f"{cfg.syn_n_res}xres3x3 (BASELINE.json configs[4])",
+                   "H": cfg.H, "W": cfg.W, "mac_per_pixel": round(macs.total, 3),
+                   "strip_rows": [st.r0, st.r1], "halo_bytes_recv_per_step_rank0": halo_bytes[0],
+                   "l2": "inputs larger than L2 (0.4 GB of image + latents per step)",
+                   "parallelism": f"strips x{rk.world}, NCCL halo exchange + all-reduce"},
+        "roofline": {"bound": "alu", "kernel": "arm_rate_kernel", "achieved": arm_tflops, "peak": FP32_PEAK_TFLOPS,
+                     "unit": "TFLOP/s", "frac": arm_tflops / FP32_PEAK_TFLOPS, "traffic": None,
+                     "avg_launch_ms": arm_avg_s * 1e3},
+        "path_roofline": {"achieved_tflops_per_gpu": path_tflops, "frac": path_tflops / FP32_PEAK_TFLOPS},
+        "e2e": None, "gpu_launches": launches, "clocks": sampler.summary(), "input_gen_s": round(gen_s, 2),
+    }
+    if rk.rank == 0:
+        print(json.dumps(out), flush=True)
+
+
 def run_e2e(args, cfg, images, desc, dev, stream, rk, n_img):
     import torch
 
@@ -361,7 +450,10 @@ def main():
         run_reference(args, rk)
         return
     rk = dist.init("nccl")
-    run_ours(args, rk)
+    if args.config == "8k":
+        run_strip(args, rk)
+    else:
+        run_ours(args, rk)
     import torch.distributed as tdist
     if tdist.is_initialized():
         tdist.destroy_process_group()

@@ -134,6 +134,55 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
                        cc_rd_result* results, void* workspace, size_t workspace_bytes,
                        void* stream);
 
+/* ------------------------------------------------------------------ strips
+ * One image split into horizontal strips of pixel rows (the
+ * BASELINE.json configs[4] single 4320x7680 image across 1/2/4/8 GPUs).  A
+ * strip owns pixel rows [r0, r1) and, at every level l, latent rows
+ * own_lo[l] = ceil(r0 / 2^l) .. own_hi[l] = ceil(r1 / 2^l) (so the strips of a
+ * partition own every latent exactly once).  Its latent BUFFER holds global rows
+ * [lo[l], hi[l]) of each grid: the owned rows plus a halo copied from the
+ * neighbouring strips (the halo exchange).  cc_strip_window() computes the
+ * smallest window from the receptive field of the forward:
+ *   level 0: rows r0 - R .. r1 + R (R residual 3x3 layers);
+ *   level j+1: rows floor(a/2) - K/4 .. floor(b/2) + K/4 for level j's rows a..b
+ *              (one x2 stride-2 transposed-conv step, reading #12);
+ *   and, for the ARM, the context rows above the owned rows
+ *   (max -dy of the template);
+ * clipped to the grid.  Inside it the kernels compute exactly what the full
+ * image computes for the owned rows (replicate padding only at true image
+ * borders), so the strips' x_hat are bit-identical to the full image's rows.
+ */
+typedef struct {
+  int32_t r0, r1;                      /* owned pixel rows; 0 <= r0 < r1 <= H, r0 even */
+  int32_t own_lo[CC_MAX_LEVELS];       /* owned latent rows of grid l                   */
+  int32_t own_hi[CC_MAX_LEVELS];
+  int32_t lo[CC_MAX_LEVELS];           /* rows present in the latent buffer (window)    */
+  int32_t hi[CC_MAX_LEVELS];
+} cc_strip;
+
+/* Fills *out with the owned rows and the minimal window of pixel rows
+ * [r0, r1) (host only; no device).  CC_EINVAL on a bad descriptor or range
+ * (r0 odd, r0 >= r1, r1 > H). */
+int cc_strip_window(const cc_model_desc* desc, int32_t r0, int32_t r1, cc_strip* out);
+
+/* Number of int16 latents in a strip's window buffer: sum_l (hi_l - lo_l) w_l;
+ * grid l starts at sum_{m<l} (hi_m - lo_m) w_m.  -1 on error. */
+int64_t cc_strip_latent_count(const cc_model_desc* desc, const cc_strip* strip);
+
+/* Workspace (device) of cc_rd_forward_strip; 0 on error. */
+size_t cc_workspace_bytes_strip(const cc_model_desc* desc, const cc_strip* strip);
+
+/* The RD forward of one strip.  io->latents: DEVICE window buffer (above);
+ * io->image / io->x_hat: DEVICE [3][r1 - r0][W] (strip rows only; image may be
+ * NULL, x_hat may be NULL).  *result (DEVICE) receives the strip's ADDITIVE
+ * share: rate_bits over the owned latents, sse over the owned pixels,
+ * mse = sse / (3 H W) and cost = mse + lambda rate_bits / (H W) with the FULL
+ * image's H W -- summing the four fields over the strips of a partition (one
+ * all-reduce) gives the full image's result.  The window must contain the one
+ * cc_strip_window() returns for (r0, r1) (CC_EINVAL otherwise). */
+int cc_rd_forward_strip(const cc_model_desc* desc, const cc_strip* strip, const cc_image_io* io,
+                        cc_rd_result* result, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Stage entry: ARM rate only (PAPER.md:120 R term).  rate: DEVICE double [1].
  * Optional DEVICE float arrays (packed like the latents, NULL to skip):
  * mu, scale (= b), bits (per latent -log2 P).  Workspace as cc_rd_forward(1). */

@@ -55,6 +55,14 @@ class CcMacBreakdown(C.Structure):
                 ("n_latents", C.c_int64)]
 
 
+class CcStrip(C.Structure):
+    """include/ccrd.h cc_strip: owned pixel rows [r0, r1), owned latent rows
+    [own_lo[l], own_hi[l]) and the latent-buffer window [lo[l], hi[l])."""
+    _fields_ = [("r0", C.c_int32), ("r1", C.c_int32),
+                ("own_lo", C.c_int32 * CC_MAX_LEVELS), ("own_hi", C.c_int32 * CC_MAX_LEVELS),
+                ("lo", C.c_int32 * CC_MAX_LEVELS), ("hi", C.c_int32 * CC_MAX_LEVELS)]
+
+
 class CcProfileSummary(C.Structure):
     _fields_ = [("arm_ms", C.c_double), ("syn_ms", C.c_double), ("reduce_ms", C.c_double), ("pyr_ms", C.c_double),
                 ("arm_launches", C.c_int64), ("syn_launches", C.c_int64), ("reduce_launches", C.c_int64),
@@ -65,7 +73,8 @@ class CcProfileSummary(C.Structure):
 EXPORTS = ["cc_workspace_bytes", "cc_rd_forward", "cc_workspace_bytes_host", "cc_rd_forward_host",
            "cc_arm_rate", "cc_upsample", "cc_synthesize", "cc_mac_per_pixel", "cc_validate",
            "cc_strerror", "cc_last_error", "cc_version", "cc_last_launch_count",
-           "cc_profile_begin", "cc_profile_end"]
+           "cc_profile_begin", "cc_profile_end", "cc_strip_window", "cc_strip_latent_count",
+           "cc_workspace_bytes_strip", "cc_rd_forward_strip"]
 
 _lib = None
 
@@ -117,6 +126,14 @@ def load(rebuild_if_stale: bool = True) -> C.CDLL:
     L.cc_profile_begin.restype = C.c_int
     L.cc_profile_end.restype = C.c_int
     L.cc_profile_end.argtypes = [P(CcProfileSummary)]
+    L.cc_strip_window.restype = C.c_int
+    L.cc_strip_window.argtypes = [D, C.c_int32, C.c_int32, P(CcStrip)]
+    L.cc_strip_latent_count.restype = C.c_int64
+    L.cc_strip_latent_count.argtypes = [D, P(CcStrip)]
+    L.cc_workspace_bytes_strip.restype = S
+    L.cc_workspace_bytes_strip.argtypes = [D, P(CcStrip)]
+    L.cc_rd_forward_strip.restype = C.c_int
+    L.cc_rd_forward_strip.argtypes = [D, P(CcStrip), P(CcImageIO), V, V, S, V]
     _lib = L
     return L
 
@@ -219,6 +236,29 @@ def cc_synthesize(desc, dense_ptr, syn_w: np.ndarray, image_ptr, x_hat_ptr, sse_
                                 ws_ptr, ws_bytes, stream_ptr), "cc_synthesize")
 
 
+def cc_strip_window(desc, r0: int, r1: int) -> CcStrip:
+    st = CcStrip()
+    _check(load().cc_strip_window(C.byref(desc), r0, r1, C.byref(st)), "cc_strip_window")
+    return st
+
+
+def cc_strip_latent_count(desc, strip: CcStrip) -> int:
+    n = load().cc_strip_latent_count(C.byref(desc), C.byref(strip))
+    if n < 0:
+        raise CcError(CC_EINVAL, "cc_strip_latent_count")
+    return n
+
+
+def cc_workspace_bytes_strip(desc, strip: CcStrip) -> int:
+    return load().cc_workspace_bytes_strip(C.byref(desc), C.byref(strip))
+
+
+def cc_rd_forward_strip(desc, strip: CcStrip, io: CcImageIO, result_ptr: int, ws_ptr: int, ws_bytes: int,
+                        stream_ptr: int = 0) -> None:
+    _check(load().cc_rd_forward_strip(C.byref(desc), C.byref(strip), C.byref(io), result_ptr, ws_ptr, ws_bytes,
+                                      stream_ptr), "cc_rd_forward_strip")
+
+
 def cc_last_launch_count() -> int:
     return load().cc_last_launch_count()
 
@@ -267,3 +307,42 @@ class DeviceBatch:
         s = torch.cuda.current_stream().cuda_stream if stream_ptr is None else stream_ptr
         cc_rd_forward(self.desc, self.io, self.results.data_ptr(), self.ws.data_ptr(), self.ws_bytes, s)
         return self.results
+
+
+class DeviceStrip:
+    """One strip of one image on the device (include/ccrd.h "strips"): the
+    latent window buffer, the strip's image rows, its x_hat rows, workspace and
+    the device result slot.  ``lat`` is filled by the caller (owned rows from
+    the bitstream, halo rows by dist.exchange_halos)."""
+
+    def __init__(self, cfg, strip: "CcStrip", arm_w, up_w, syn_w, image_rows=None, device="cuda",
+                 with_xhat=True):
+        import torch
+        self.cfg = cfg
+        self.desc = desc_from_config(cfg)
+        self.strip = strip
+        n = cc_strip_latent_count(self.desc, strip)
+        self.lat = torch.zeros(n, dtype=torch.int16, device=device)
+        rows = strip.r1 - strip.r0
+        self.img = None if image_rows is None else torch.as_tensor(image_rows).to(device).contiguous()
+        if self.img is not None:
+            assert tuple(self.img.shape) == (3, rows, cfg.W), self.img.shape
+        self.xhat = torch.empty((3, rows, cfg.W), dtype=torch.float32, device=device) if with_xhat else None
+        self.arm_w = np.ascontiguousarray(arm_w, np.float32)
+        self.up_w = np.ascontiguousarray(up_w, np.float32)
+        self.syn_w = np.ascontiguousarray(syn_w, np.float32)
+        self.ws_bytes = cc_workspace_bytes_strip(self.desc, strip)
+        if self.ws_bytes == 0:
+            raise CcError(CC_EINVAL, "cc_workspace_bytes_strip")
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=device)
+        self.result = torch.zeros(4, dtype=torch.float64, device=device)
+        self.io = CcImageIO(self.lat.data_ptr(), self.arm_w.ctypes.data, self.up_w.ctypes.data,
+                            self.syn_w.ctypes.data, self.img.data_ptr() if self.img is not None else None,
+                            self.xhat.data_ptr() if with_xhat else None)
+
+    def forward(self, stream_ptr: Optional[int] = None):
+        import torch
+        s = torch.cuda.current_stream().cuda_stream if stream_ptr is None else stream_ptr
+        cc_rd_forward_strip(self.desc, self.strip, self.io, self.result.data_ptr(), self.ws.data_ptr(),
+                            self.ws_bytes, s)
+        return self.result

@@ -86,13 +86,16 @@ __global__ void __launch_bounds__(ARM_THREADS, ARM_CTAS_PER_SM)
   int l = 0;
 #pragma unroll 1
   while (l + 1 < p.g.L && b >= p.g.tile_begin[l + 1]) l++;
-  const int h = p.g.lv.h[l], w = p.g.lv.w[l];
+  const int w = p.g.lv.w[l];
+  const int rlo = p.g.lv.lo[l], rhi = p.g.lv.hi[l];  // buffer window (full image: 0 .. h)
+  const int own_hi = p.g.own_hi[l];
   const int t = b - p.g.tile_begin[l];
   const int ty = t / p.g.tiles_x[l];
-  const int i0 = ty * ARM_TY, j0 = (t - ty * p.g.tiles_x[l]) * ARM_TX;
+  const int i0 = p.g.own_lo[l] + ty * ARM_TY, j0 = (t - ty * p.g.tiles_x[l]) * ARM_TX;
   const int16_t* __restrict__ grid = p.lat + p.g.lv.off[l];
 
-  // stage the causal window, fp32, zero outside the grid (reading #5); every
+  // stage the causal window, fp32, zero outside the grid (reading #5; the
+  // buffer window contains every row an owned latent's context reaches); every
   // load is issued before the first store
   {
     int16_t v[IT];
@@ -101,7 +104,8 @@ __global__ void __launch_bounds__(ARM_THREADS, ARM_CTAS_PER_SM)
       const int s = threadIdx.x + k * ARM_THREADS;
       const int r = s / ARM_SW, c = s - r * ARM_SW;
       const int gi = i0 - ARM_HALO_TOP + r, gj = j0 - ARM_HALO_X + c;
-      v[k] = (s < N && gi >= 0 && gi < h && gj >= 0 && gj < w) ? __ldg(grid + (int64_t)gi * w + gj) : (int16_t)0;
+      v[k] = (s < N && gi >= rlo && gi < rhi && gj >= 0 && gj < w) ? __ldg(grid + (int64_t)(gi - rlo) * w + gj)
+                                                                  : (int16_t)0;
     }
 #pragma unroll
     for (int k = 0; k < IT; k++) {
@@ -150,12 +154,12 @@ __global__ void __launch_bounds__(ARM_THREADS, ARM_CTAS_PER_SM)
 #pragma unroll
   for (int m = 0; m < M; m++) {
     const int j = j0 + lane + 32 * m;
-    if (i < h && j < w) {
+    if (i < own_hi && j < w) {
       const float2 ms = f2unpack(o[m]);
       const float bm = laplace_bits(y[m], ms.x, ms.y, p.g);
       bits += bm;
       if (p.bits != nullptr) {
-        const int64_t q = p.g.lv.off[l] + (int64_t)i * w + j;
+        const int64_t q = p.g.lv.off[l] + (int64_t)(i - rlo) * w + j;
         p.bits[q] = bm;
         if (p.mu) p.mu[q] = ms.x;
         if (p.scale) p.scale[q] = __expf(fminf(fmaxf(ms.y, p.g.lsmin), p.g.lsmax));

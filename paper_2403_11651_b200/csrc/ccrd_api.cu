@@ -84,21 +84,69 @@ static int cuda_check(const char* what) {
 }
 
 // ------------------------------------------------------------- descriptor
-static void level_dims(const cc_model_desc& d, LevelGeom& g, int64_t* n_lat) {
+static int32_t ceil_shift(int64_t v, int l) { return (int32_t)((v + ((int64_t)1 << l) - 1) >> l); }
+
+// Level dimensions; `win` (a strip) sets the buffer window of every grid
+// (nullptr: the full image, window = the whole grid).
+static void level_dims(const cc_model_desc& d, const cc_strip* win, LevelGeom& g, int64_t* n_lat) {
   int64_t off = 0;
   for (int l = 0; l < CC_MAX_LEVELS; l++) {
     if (l < d.L) {
-      const int64_t s = (int64_t)1 << l;
-      g.h[l] = (int32_t)((d.H + s - 1) / s);
-      g.w[l] = (int32_t)((d.W + s - 1) / s);
+      g.h[l] = ceil_shift(d.H, l);
+      g.w[l] = ceil_shift(d.W, l);
+      g.lo[l] = win ? win->lo[l] : 0;
+      g.hi[l] = win ? win->hi[l] : g.h[l];
       g.off[l] = off;
-      off += (int64_t)g.h[l] * g.w[l];
+      off += (int64_t)(g.hi[l] - g.lo[l]) * g.w[l];
     } else {
-      g.h[l] = g.w[l] = 0;
+      g.h[l] = g.w[l] = g.lo[l] = g.hi[l] = 0;
       g.off[l] = off;
     }
   }
   if (n_lat) *n_lat = off;
+}
+static void level_dims(const cc_model_desc& d, LevelGeom& g, int64_t* n_lat) { level_dims(d, nullptr, g, n_lat); }
+
+// The strip of pixel rows [r0, r1): owned latent rows and the minimal buffer
+// window (include/ccrd.h "strips").  Assumes a valid descriptor.
+static void strip_window(const cc_model_desc& d, int r0, int r1, cc_strip& st) {
+  memset(&st, 0, sizeof(st));
+  st.r0 = r0;
+  st.r1 = r1;
+  int maxdy = 0;
+  for (int c = 0; c < d.n_ctx; c++) maxdy = (-d.ctx_dy[c] > maxdy) ? -d.ctx_dy[c] : maxdy;
+  // synthesis receptive field: R residual 3x3 layers at level 0, then one x2
+  // step per level (sources floor(y/2) - K/4 .. floor(y/2) + K/4)
+  int a = r0 - d.syn_n_res, b = r1 - 1 + d.syn_n_res;  // inclusive rows
+  for (int l = 0; l < d.L; l++) {
+    const int h = ceil_shift(d.H, l);
+    if (l > 0) {
+      a = (a >> 1) - d.up_taps / 4;  // arithmetic shift = floor
+      b = (b >> 1) + d.up_taps / 4;
+    }
+    a = a < 0 ? 0 : a;
+    b = b > h - 1 ? h - 1 : b;
+    st.own_lo[l] = ceil_shift(r0, l);
+    st.own_hi[l] = ceil_shift(r1, l);
+    int lo = a, hi = b + 1;
+    if (st.own_hi[l] > st.own_lo[l]) {  // ARM: the context rows above the owned rows
+      const int alo = st.own_lo[l] - maxdy < 0 ? 0 : st.own_lo[l] - maxdy;
+      lo = alo < lo ? alo : lo;
+      hi = st.own_hi[l] > hi ? st.own_hi[l] : hi;
+    }
+    st.lo[l] = lo;
+    st.hi[l] = hi;
+  }
+}
+
+static void full_strip(const cc_model_desc& d, cc_strip& st) {
+  memset(&st, 0, sizeof(st));
+  st.r0 = 0;
+  st.r1 = d.H;
+  for (int l = 0; l < d.L; l++) {
+    st.own_lo[l] = st.lo[l] = 0;
+    st.own_hi[l] = st.hi[l] = ceil_shift(d.H, l);
+  }
 }
 
 static int validate(const cc_model_desc* dp) {
@@ -152,16 +200,18 @@ static int validate(const cc_model_desc* dp) {
   return CC_OK;
 }
 
-static void arm_geom(const cc_model_desc& d, ArmGeom& g) {
+static void arm_geom(const cc_model_desc& d, const cc_strip* win, ArmGeom& g) {
   memset(&g, 0, sizeof(g));
-  level_dims(d, g.lv, nullptr);
+  level_dims(d, win, g.lv, nullptr);
   g.L = d.L;
   int acc = 0;
   for (int l = 0; l < CC_MAX_LEVELS; l++) {
     g.tile_begin[l] = acc;
     if (l < d.L) {
+      g.own_lo[l] = win ? win->own_lo[l] : 0;
+      g.own_hi[l] = win ? win->own_hi[l] : g.lv.h[l];
       g.tiles_x[l] = (g.lv.w[l] + ARM_TX - 1) / ARM_TX;
-      acc += g.tiles_x[l] * ((g.lv.h[l] + ARM_TY - 1) / ARM_TY);
+      acc += g.tiles_x[l] * ((g.own_hi[l] - g.own_lo[l] + ARM_TY - 1) / ARM_TY);
     }
   }
   g.tile_begin[CC_MAX_LEVELS] = acc;
@@ -173,36 +223,38 @@ static void arm_geom(const cc_model_desc& d, ArmGeom& g) {
   g.bits_cap = (float)(-log2((double)d.p_floor));
 }
 
-static void syn_geom(const cc_model_desc& d, SynGeom& g) {
+static void syn_geom(const cc_model_desc& d, const cc_strip* win, SynGeom& g) {
   memset(&g, 0, sizeof(g));
-  level_dims(d, g.lv, nullptr);
+  level_dims(d, win, g.lv, nullptr);
   g.H = d.H;
   g.W = d.W;
+  g.y0 = win ? win->r0 : 0;
+  g.y1 = win ? win->r1 : d.H;
   g.tiles_x = (d.W + SYN_TW - 1) / SYN_TW;
-  g.n_tiles = g.tiles_x * ((d.H + SYN_TH - 1) / SYN_TH);
+  g.n_tiles = g.tiles_x * ((g.y1 - g.y0 + SYN_TH - 1) / SYN_TH);
 }
 
-static int n_arm_partials(const cc_model_desc& d) {  // one per ARM warp
+static int n_arm_partials(const cc_model_desc& d, const cc_strip* win) {  // one per ARM warp
   ArmGeom g;
-  arm_geom(d, g);
+  arm_geom(d, win, g);
   return g.tile_begin[d.L] * (ARM_THREADS / 32);
 }
-static int n_syn_ctas(const cc_model_desc& d) {
+static int n_syn_ctas(const cc_model_desc& d, const cc_strip* win) {
   SynGeom g;
-  syn_geom(d, g);
+  syn_geom(d, win, g);
   return g.n_tiles;
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-static void pyr_geom(const cc_model_desc& d, PyrGeom& g) {
+static void pyr_geom(const cc_model_desc& d, const cc_strip* win, PyrGeom& g) {
   memset(&g, 0, sizeof(g));
-  level_dims(d, g.lv, nullptr);
+  level_dims(d, win, g.lv, nullptr);
   g.L = d.L;
   int64_t off = 0;
-  for (int j = 1; j + 1 < d.L; j++) {  // S_j: grids j+1 .. L-1 at level j
+  for (int j = 1; j + 1 < d.L; j++) {  // S_j: grids j+1 .. L-1 at level j, over the window rows
     g.s_off[j] = off;
-    off += (int64_t)(d.L - 1 - j) * g.lv.h[j] * g.lv.w[j];
+    off += (int64_t)(d.L - 1 - j) * (g.lv.hi[j] - g.lv.lo[j]) * g.lv.w[j];
     off = (off + 63) & ~(int64_t)63;
   }
   g.s_floats = off;
@@ -210,15 +262,18 @@ static void pyr_geom(const cc_model_desc& d, PyrGeom& g) {
 
 // Workspace per image: ARM partials + synthesis partials (fp64) + a result
 // scratch slot used by the stage entries + the upsampling pyramid S_1..S_{L-2}
-static size_t partial_bytes(const cc_model_desc& d) {
-  return align256(sizeof(double) * (size_t)(n_arm_partials(d) + n_syn_ctas(d))) + align256(sizeof(cc_rd_result));
+static size_t partial_bytes(const cc_model_desc& d, const cc_strip* win) {
+  return align256(sizeof(double) * (size_t)(n_arm_partials(d, win) + n_syn_ctas(d, win))) +
+         align256(sizeof(cc_rd_result));
 }
-static size_t slice_bytes(const cc_model_desc& d) {
+static size_t slice_bytes(const cc_model_desc& d, const cc_strip* win) {
   PyrGeom pg;
-  pyr_geom(d, pg);
-  return partial_bytes(d) + align256(sizeof(float) * (size_t)pg.s_floats);
+  pyr_geom(d, win, pg);
+  return partial_bytes(d, win) + align256(sizeof(float) * (size_t)pg.s_floats);
 }
-static float* slice_pyr(const cc_model_desc& d, void* slice) { return (float*)((char*)slice + partial_bytes(d)); }
+static float* slice_pyr(const cc_model_desc& d, const cc_strip* win, void* slice) {
+  return (float*)((char*)slice + partial_bytes(d, win));
+}
 
 // ------------------------------------------------------------- reduction
 // One CTA per image, fixed-order tree => bitwise deterministic.
@@ -254,10 +309,10 @@ __global__ void __launch_bounds__(256) reduce_batch_kernel(const __grid_constant
   }
 }
 
-static ReduceJob make_job(const cc_model_desc& d, double* part) {
+static ReduceJob make_job(const cc_model_desc& d, const cc_strip* win, double* part) {
   ReduceJob j;
-  j.n_arm = n_arm_partials(d);
-  j.n_syn = n_syn_ctas(d);
+  j.n_arm = n_arm_partials(d, win);
+  j.n_syn = n_syn_ctas(d, win);
   j.arm_partial = part;
   j.syn_partial = part + j.n_arm;
   const double P = (double)d.H * (double)d.W;
@@ -284,9 +339,11 @@ static bool have_device(void) {
 }
 
 // ARM rate of one image (per-warp partials at the start of `part`)
-static int arm_one(const cc_model_desc& d, const int16_t* lat, const float* arm_w, double* part, cudaStream_t s) {
+static int arm_one(const cc_model_desc& d, const cc_strip* win, const int16_t* lat, const float* arm_w, double* part,
+                   cudaStream_t s) {
   ArmGeom ag;
-  arm_geom(d, ag);
+  arm_geom(d, win, ag);
+  if (ag.tile_begin[d.L] == 0) return CC_OK;  // a strip owning no latent rows
   {
     ProfScope ps(PK_ARM, s);
     find_arm_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1)(ag, d, arm_w, lat, part, nullptr, nullptr,
@@ -297,9 +354,9 @@ static int arm_one(const cc_model_desc& d, const int16_t* lat, const float* arm_
 }
 
 // coarse upsampling pyramid of n images (batched launches)
-static int pyr_many(const cc_model_desc& d, const PyrImage* imgs, int n, cudaStream_t s) {
+static int pyr_many(const cc_model_desc& d, const cc_strip* win, const PyrImage* imgs, int n, cudaStream_t s) {
   PyrGeom pg;
-  pyr_geom(d, pg);
+  pyr_geom(d, win, pg);
   {
     ProfScope ps(PK_PYR, s);
     launch_pyramid(pg, d.up_taps, imgs, n, s);
@@ -309,11 +366,11 @@ static int pyr_many(const cc_model_desc& d, const PyrImage* imgs, int n, cudaStr
 }
 
 // fused last upsampling step + synthesis + distortion of one image
-static int syn_one(const cc_model_desc& d, const int16_t* lat, const float* s1, const float* up_w,
-                   const float* syn_w, const float* image, float* x_hat, float* dense_out, double* syn_part,
-                   cudaStream_t s) {
+static int syn_one(const cc_model_desc& d, const cc_strip* win, const int16_t* lat, const float* s1,
+                   const float* up_w, const float* syn_w, const float* image, float* x_hat, float* dense_out,
+                   double* syn_part, cudaStream_t s) {
   SynGeom sg;
-  syn_geom(d, sg);
+  syn_geom(d, win, sg);
   {
     ProfScope ps(PK_SYN, s);
     find_syn_launcher(d.L, d.syn_widths[1], d.syn_n_res, d.up_taps)(sg, d, up_w, syn_w, lat, s1, nullptr, image,
@@ -357,32 +414,34 @@ static int side_stream(SideStream** out) {
 
 // whole path for images [0, n): pyramid (side stream) || ARM, then synthesis;
 // per-image workspace slices of `per` bytes
-static int forward_batch(const cc_model_desc& d, const int16_t* const* lat, const float* const* arm_w,
-                         const float* const* up_w, const float* const* syn_w, const float* const* image,
-                         float* const* x_hat, char* slices, size_t per, int n, cudaStream_t s, bool overlap) {
+static int forward_batch(const cc_model_desc& d, const cc_strip* win, const int16_t* const* lat,
+                         const float* const* arm_w, const float* const* up_w, const float* const* syn_w,
+                         const float* const* image, float* const* x_hat, char* slices, size_t per, int n,
+                         cudaStream_t s, bool overlap) {
   PyrGeom pg;
-  pyr_geom(d, pg);
-  const int n_arm = n_arm_partials(d);
+  pyr_geom(d, win, pg);
+  const int n_arm = n_arm_partials(d, win);
   int rc;
   PyrImage imgs[MAX_JOBS_PER_LAUNCH];
-  for (int i = 0; i < n; i++) imgs[i] = pyr_image(d, lat[i], up_w[i], slice_pyr(d, slices + per * (size_t)i));
+  for (int i = 0; i < n; i++)
+    imgs[i] = pyr_image(d, lat[i], up_w[i], slice_pyr(d, win, slices + per * (size_t)i));
   SideStream* side = nullptr;
   if (overlap && pg.L >= 3) {
     if ((rc = side_stream(&side))) return rc;
     cudaEventRecord(side->fork, s);
     cudaStreamWaitEvent(side->s, side->fork, 0);
-    if ((rc = pyr_many(d, imgs, n, side->s))) return rc;
+    if ((rc = pyr_many(d, win, imgs, n, side->s))) return rc;
     cudaEventRecord(side->join, side->s);
-  } else if ((rc = pyr_many(d, imgs, n, s))) {
+  } else if ((rc = pyr_many(d, win, imgs, n, s))) {
     return rc;
   }
   for (int i = 0; i < n; i++)
-    if ((rc = arm_one(d, lat[i], arm_w[i], (double*)(slices + per * (size_t)i), s))) return rc;
+    if ((rc = arm_one(d, win, lat[i], arm_w[i], (double*)(slices + per * (size_t)i), s))) return rc;
   if (side) cudaStreamWaitEvent(s, side->join, 0);
   for (int i = 0; i < n; i++) {
     char* sl = slices + per * (size_t)i;
-    const float* s1 = slice_pyr(d, sl) + pg.s_off[1];
-    if ((rc = syn_one(d, lat[i], s1, up_w[i], syn_w[i], image[i], x_hat[i], nullptr, (double*)sl + n_arm, s)))
+    const float* s1 = slice_pyr(d, win, sl) + pg.s_off[1];
+    if ((rc = syn_one(d, win, lat[i], s1, up_w[i], syn_w[i], image[i], x_hat[i], nullptr, (double*)sl + n_arm, s)))
       return rc;
   }
   return CC_OK;
@@ -443,7 +502,7 @@ int cc_validate(const cc_model_desc* desc) { return validate(desc); }
 
 size_t cc_workspace_bytes(const cc_model_desc* desc, int32_t n_img) {
   if (validate(desc) != CC_OK || n_img < 1) return 0;
-  return slice_bytes(*desc) * (size_t)n_img;
+  return slice_bytes(*desc, nullptr) * (size_t)n_img;
 }
 
 int cc_rd_forward(const cc_model_desc* desc, const cc_image_io* io, int32_t n_img, cc_rd_result* results,
@@ -452,7 +511,7 @@ int cc_rd_forward(const cc_model_desc* desc, const cc_image_io* io, int32_t n_im
   int rc = validate(desc);
   if (rc) return rc;
   if (!io || n_img < 1 || !results) return fail(CC_EINVAL, "io/results null or n_img < 1");
-  const size_t per = slice_bytes(*desc);
+  const size_t per = slice_bytes(*desc, nullptr);
   const size_t need = per * (size_t)n_img;
   if (!workspace || workspace_bytes < need)
     return fail(CC_EWORKSPACE, "need %zu workspace bytes, got %zu", need, workspace_bytes);
@@ -477,9 +536,9 @@ int cc_rd_forward(const cc_model_desc* desc, const cc_image_io* io, int32_t n_im
       sw[i] = x.syn_w;
       img[i] = x.image;
       xh[i] = x.x_hat;
-      jobs[i] = make_job(*desc, (double*)(slices + per * (size_t)(b + i)));
+      jobs[i] = make_job(*desc, nullptr, (double*)(slices + per * (size_t)(b + i)));
     }
-    rc = forward_batch(*desc, lat, aw, uw, sw, img, xh, slices + per * (size_t)b, per, m, s, false);
+    rc = forward_batch(*desc, nullptr, lat, aw, uw, sw, img, xh, slices + per * (size_t)b, per, m, s, false);
     if (rc) return rc;
     rc = launch_reduce(jobs, m, results + b, s);
     if (rc) return rc;
@@ -500,7 +559,7 @@ static size_t stage_slot_bytes(const cc_model_desc& d) {
 
 size_t cc_workspace_bytes_host(const cc_model_desc* desc, int32_t n_img) {
   if (validate(desc) != CC_OK || n_img < 1) return 0;
-  return slice_bytes(*desc) * (size_t)n_img +
+  return slice_bytes(*desc, nullptr) * (size_t)n_img +
          align256(sizeof(cc_rd_result) * (size_t)n_img) + 2 * stage_slot_bytes(*desc);
 }
 
@@ -515,7 +574,7 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
   if (!workspace || workspace_bytes < need)
     return fail(CC_EWORKSPACE, "need %zu workspace bytes, got %zu", need, workspace_bytes);
   if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
-  const size_t per = slice_bytes(d);
+  const size_t per = slice_bytes(d, nullptr);
   char* ws = (char*)workspace;
   cc_rd_result* dres = (cc_rd_result*)(ws + per * (size_t)n_img);
   char* stage = ws + per * (size_t)n_img + align256(sizeof(cc_rd_result) * (size_t)n_img);
@@ -560,11 +619,11 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
     const int16_t* l1[1] = {dlat};
     const float *a1[1] = {x.arm_w}, *u1[1] = {x.up_w}, *s1[1] = {x.syn_w}, *i1[1] = {x.image ? dimg : nullptr};
     float* x1[1] = {x.x_hat ? dxh : nullptr};
-    rc = forward_batch(d, l1, a1, u1, s1, i1, x1, (char*)part, per, 1, s, false);
+    rc = forward_batch(d, nullptr, l1, a1, u1, s1, i1, x1, (char*)part, per, 1, s, false);
     if (rc) break;
     if (x.x_hat) cudaMemcpyAsync(x.x_hat, dxh, img_b, cudaMemcpyDeviceToHost, s);
     cudaEventRecord(consumed[k], s);
-    jobs[i] = make_job(d, part);
+    jobs[i] = make_job(d, nullptr, part);
   }
   if (rc == CC_OK) rc = launch_reduce(jobs, n_img, dres, s);
   if (rc == CC_OK) {
@@ -584,6 +643,70 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
   return rc;
 }
 
+// ---------------------------------------------------------------- strips
+static int validate_strip(const cc_model_desc& d, const cc_strip* st) {
+  if (!st) return fail(CC_EINVAL, "null strip");
+  if (st->r0 < 0 || st->r1 > d.H || st->r0 >= st->r1 || (st->r0 & 1))
+    return fail(CC_EINVAL, "strip rows [%d, %d) must satisfy 0 <= r0 < r1 <= H (%d) with r0 even", st->r0, st->r1,
+                d.H);
+  cc_strip need;
+  strip_window(d, st->r0, st->r1, need);
+  for (int l = 0; l < d.L; l++) {
+    if (st->own_lo[l] != need.own_lo[l] || st->own_hi[l] != need.own_hi[l])
+      return fail(CC_EINVAL, "strip level %d: owned rows [%d, %d) != ceil(r/2^l) = [%d, %d)", l, st->own_lo[l],
+                  st->own_hi[l], need.own_lo[l], need.own_hi[l]);
+    if (st->lo[l] < 0 || st->hi[l] > ceil_shift(d.H, l) || st->lo[l] > need.lo[l] || st->hi[l] < need.hi[l])
+      return fail(CC_EINVAL, "strip level %d: window [%d, %d) does not contain the receptive field [%d, %d)", l,
+                  st->lo[l], st->hi[l], need.lo[l], need.hi[l]);
+  }
+  return CC_OK;
+}
+
+int cc_strip_window(const cc_model_desc* desc, int32_t r0, int32_t r1, cc_strip* out) {
+  int rc = validate(desc);
+  if (rc) return rc;
+  if (!out) return fail(CC_EINVAL, "null strip");
+  if (r0 < 0 || r1 > desc->H || r0 >= r1 || (r0 & 1))
+    return fail(CC_EINVAL, "strip rows [%d, %d) must satisfy 0 <= r0 < r1 <= H (%d) with r0 even", r0, r1, desc->H);
+  strip_window(*desc, r0, r1, *out);
+  return CC_OK;
+}
+
+int64_t cc_strip_latent_count(const cc_model_desc* desc, const cc_strip* strip) {
+  if (validate(desc) != CC_OK || validate_strip(*desc, strip) != CC_OK) return -1;
+  LevelGeom g;
+  int64_t n = 0;
+  level_dims(*desc, strip, g, &n);
+  return n;
+}
+
+size_t cc_workspace_bytes_strip(const cc_model_desc* desc, const cc_strip* strip) {
+  if (validate(desc) != CC_OK || validate_strip(*desc, strip) != CC_OK) return 0;
+  return slice_bytes(*desc, strip);
+}
+
+int cc_rd_forward_strip(const cc_model_desc* desc, const cc_strip* strip, const cc_image_io* io,
+                        cc_rd_result* result, void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  int rc = validate(desc);
+  if (rc) return rc;
+  const cc_model_desc& d = *desc;
+  if ((rc = validate_strip(d, strip))) return rc;
+  if (!io || !result) return fail(CC_EINVAL, "io/result null");
+  if (!io->latents || !io->arm_w || !io->up_w || !io->syn_w) return fail(CC_EINVAL, "null latents or weights");
+  const size_t per = slice_bytes(d, strip);
+  if (!workspace || workspace_bytes < per)
+    return fail(CC_EWORKSPACE, "need %zu workspace bytes, got %zu", per, workspace_bytes);
+  if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int16_t* l1[1] = {io->latents};
+  const float *a1[1] = {io->arm_w}, *u1[1] = {io->up_w}, *s1[1] = {io->syn_w}, *i1[1] = {io->image};
+  float* x1[1] = {io->x_hat};
+  if ((rc = forward_batch(d, strip, l1, a1, u1, s1, i1, x1, (char*)workspace, per, 1, s, false))) return rc;
+  ReduceJob j = make_job(d, strip, (double*)workspace);
+  return launch_reduce(&j, 1, result, s);
+}
+
 // ---------------------------------------------------------------- stages
 int cc_arm_rate(const cc_model_desc* desc, const int16_t* latents, const float* arm_w, double* rate, float* mu,
                 float* scale, float* bits, void* workspace, size_t workspace_bytes, void* stream) {
@@ -591,7 +714,7 @@ int cc_arm_rate(const cc_model_desc* desc, const int16_t* latents, const float* 
   int rc = validate(desc);
   if (rc) return rc;
   if (!latents || !arm_w || !rate) return fail(CC_EINVAL, "null latents / arm_w / rate");
-  const size_t per = partial_bytes(*desc);
+  const size_t per = partial_bytes(*desc, nullptr);
   if (!workspace || workspace_bytes < per)
     return fail(CC_EWORKSPACE, "need %zu workspace bytes", per);  // <= cc_workspace_bytes(desc, 1)
   if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
@@ -599,13 +722,13 @@ int cc_arm_rate(const cc_model_desc* desc, const int16_t* latents, const float* 
   const cc_model_desc& d = *desc;
   cudaStream_t s = (cudaStream_t)stream;
   ArmGeom ag;
-  arm_geom(d, ag);
+  arm_geom(d, nullptr, ag);
   double* part = (double*)workspace;
   find_arm_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1)(ag, d, arm_w, latents, part, mu, scale, bits, s);
   g_launches++;
   if ((rc = cuda_check("arm_rate_kernel"))) return rc;
   // rate only: reduce with an empty synthesis partial set
-  ReduceJob j = make_job(d, part);
+  ReduceJob j = make_job(d, nullptr, part);
   j.n_syn = 0;
   cc_rd_result* tmp = (cc_rd_result*)((char*)workspace + per - align256(sizeof(cc_rd_result)));
   if ((rc = launch_reduce(&j, 1, tmp, s))) return rc;
@@ -620,21 +743,21 @@ int cc_upsample(const cc_model_desc* desc, const int16_t* latents, const float* 
   if (rc) return rc;
   if (!latents || !up_w || !dense) return fail(CC_EINVAL, "null latents / up_w / dense");
   const cc_model_desc& d = *desc;
-  const size_t per = slice_bytes(d);
+  const size_t per = slice_bytes(d, nullptr);
   if (!workspace || workspace_bytes < per) return fail(CC_EWORKSPACE, "need %zu workspace bytes", per);
   if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
   cudaStream_t s = (cudaStream_t)stream;
   // the production path (pyramid + fused last step) with its dense output on;
   // synthesis weights are irrelevant here: zero blob of the right size
   PyrGeom pg;
-  pyr_geom(d, pg);
-  float* S = slice_pyr(d, workspace);
+  pyr_geom(d, nullptr, pg);
+  float* S = slice_pyr(d, nullptr, workspace);
   PyrImage im = pyr_image(d, latents, up_w, S);
-  if ((rc = pyr_many(d, &im, 1, s))) return rc;
+  if ((rc = pyr_many(d, nullptr, &im, 1, s))) return rc;
   const int CH = d.syn_widths[1];
   const int nsyn = d.L * CH + CH + CH * 3 + 3 + 84 * d.syn_n_res;
   float* zeros = new float[nsyn]();
-  rc = syn_one(d, latents, S + pg.s_off[1], up_w, zeros, nullptr, nullptr, dense, nullptr, s);
+  rc = syn_one(d, nullptr, latents, S + pg.s_off[1], up_w, zeros, nullptr, nullptr, dense, nullptr, s);
   delete[] zeros;
   return rc;
 }
@@ -648,7 +771,7 @@ int cc_synthesize(const cc_model_desc* desc, const float* dense, const float* sy
   if (sse && !image) return fail(CC_EINVAL, "sse requested without image");
   const cc_model_desc& d = *desc;
   SynGeom sg;
-  syn_geom(d, sg);
+  syn_geom(d, nullptr, sg);
   const size_t need = align256(sizeof(double) * (size_t)sg.n_tiles) + sizeof(cc_rd_result);
   if (sse && (!workspace || workspace_bytes < need)) return fail(CC_EWORKSPACE, "need %zu workspace bytes", need);
   if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
@@ -659,7 +782,7 @@ int cc_synthesize(const cc_model_desc* desc, const float* dense, const float* sy
   g_launches++;
   if ((rc = cuda_check("synth_kernel(dense_in)"))) return rc;
   if (sse) {
-    ReduceJob j = make_job(d, part);
+    ReduceJob j = make_job(d, nullptr, part);
     j.n_arm = 0;
     j.syn_partial = part;
     cc_rd_result* tmp = (cc_rd_result*)((char*)workspace + align256(sizeof(double) * (size_t)sg.n_tiles));

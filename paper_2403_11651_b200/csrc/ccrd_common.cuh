@@ -66,10 +66,17 @@ __device__ __forceinline__ double block_sum(float v, double* warp_buf) {
 }
 
 // ------------------------------------------------------------------ geometry
+// Level dimensions and the latent-buffer window.  Full image: lo = 0, hi = h.
+// Strip (cc_rd_forward_strip): the buffer holds only global rows
+// [lo_l, hi_l) of grid l; every latent read clamps its row to that window (at
+// a true image border the window edge IS the border, so this is the replicate
+// padding; at an interior window edge it only feeds rows that are discarded).
 struct LevelGeom {
-  int32_t h[CC_MAX_LEVELS];
+  int32_t h[CC_MAX_LEVELS];    // global grid height ceil(H / 2^l)
   int32_t w[CC_MAX_LEVELS];
-  int64_t off[CC_MAX_LEVELS];  // element offset of level l in the packed pyramid
+  int32_t lo[CC_MAX_LEVELS];   // first global row present in the buffer
+  int32_t hi[CC_MAX_LEVELS];   // one past the last row present
+  int64_t off[CC_MAX_LEVELS];  // element offset of level l in the packed (windowed) buffer
 };
 
 // ARM tiling: one CTA = 8 rows x 64 latents of one grid; warp w owns row w,
@@ -90,6 +97,8 @@ struct ArmGeom {
   int32_t L;
   int32_t tiles_x[CC_MAX_LEVELS];
   int32_t tile_begin[CC_MAX_LEVELS + 1];  // prefix over levels; [L] = total CTAs
+  int32_t own_lo[CC_MAX_LEVELS];          // latent rows whose rate this launch counts
+  int32_t own_hi[CC_MAX_LEVELS];          //   (full image: 0 .. h)
   int32_t ctx_off[CC_MAX_CTX];            // dy * ARM_SW + dx (shared-memory offsets)
   float lsmin, lsmax;                     // log-scale clamp
   float p_floor;                          // probability floor
@@ -148,6 +157,7 @@ struct SynWeights {
 struct SynGeom {
   LevelGeom lv;
   int32_t H, W;
+  int32_t y0, y1;  // output pixel rows [y0, y1) (full image: 0 .. H); y0 even
   int32_t tiles_x, n_tiles;
 };
 
@@ -183,14 +193,14 @@ struct PyrImage {
 struct PyrGeom {
   LevelGeom lv;
   int32_t L;
-  int64_t s_off[CC_MAX_LEVELS];  // float offset of S_j; S_j = [L-1-j][h_j][w_j]
+  int64_t s_off[CC_MAX_LEVELS];  // float offset of S_j; S_j = [L-1-j][hi_j - lo_j][w_j]
   int64_t s_floats;              // total floats per image
 };
 
 template <int K>
 struct PyrParams {
   LevelGeom lv;
-  int32_t L, j, tiles_x;
+  int32_t L, j, tiles_x, y_base;  // tiles cover rows y_base + PYR_TH * ty (y_base = lo_j rounded down to even)
   int64_t s_off[CC_MAX_LEVELS];
   PyrImage img[PYR_MAX_IMG];
 };

@@ -26,10 +26,12 @@ __global__ void __launch_bounds__(PYR_THREADS)
   const int nch = p.L - 1 - j;
   float* sw = psm;                       // [nch][SR][SC]
   float* tmp = psm + nch * SR * SC;      // [nch][SR][PYR_TW]
-  const int hj = p.lv.h[j], wj = p.lv.w[j];
-  const int hs = p.lv.h[j + 1], ws = p.lv.w[j + 1];
+  // level j rows [lo_j, hi_j) are produced (buffer row = global row - lo_j);
+  // level j+1 sources are read clamped to ITS window [lo_{j+1}, hi_{j+1})
+  const int wj = p.lv.w[j], loj = p.lv.lo[j], hij = p.lv.hi[j], nj = hij - loj;
+  const int ws = p.lv.w[j + 1], los = p.lv.lo[j + 1], his = p.lv.hi[j + 1], ns = his - los;
   const int ty = blockIdx.x / p.tiles_x;
-  const int Y0 = ty * PYR_TH, X0 = (blockIdx.x - ty * p.tiles_x) * PYR_TW;
+  const int Y0 = p.y_base + ty * PYR_TH, X0 = (blockIdx.x - ty * p.tiles_x) * PYR_TW;
   const int r0 = (Y0 >> 1) - K / 4, c0 = (X0 >> 1) - K / 4;  // source window origin
   float* Sj = im.S + p.s_off[j];
   const float* Sn = im.S + p.s_off[j + 1];  // S_{j+1}, nch - 1 channels
@@ -40,8 +42,8 @@ __global__ void __launch_bounds__(PYR_THREADS)
   for (int it = threadIdx.x; it < nch * SR * SC; it += PYR_THREADS) {
     const int k = it / (SR * SC), rem = it - k * (SR * SC);
     const int rr = rem / SC, cc = rem - rr * SC;
-    const int64_t gi = (int64_t)clampi(r0 + rr, 0, hs - 1) * ws + clampi(c0 + cc, 0, ws - 1);
-    sw[it] = (k == 0) ? (float)__ldg(lat + gi) : __ldg(Sn + (int64_t)(k - 1) * hs * ws + gi);
+    const int64_t gi = (int64_t)(clampi(r0 + rr, los, his - 1) - los) * ws + clampi(c0 + cc, 0, ws - 1);
+    sw[it] = (k == 0) ? (float)__ldg(lat + gi) : __ldg(Sn + (int64_t)(k - 1) * ns * ws + gi);
   }
   __syncthreads();
   // horizontal: column pairs (2q, 2q+1) share sources q - K/4 .. q + K/4 ----
@@ -78,9 +80,9 @@ __global__ void __launch_bounds__(PYR_THREADS)
     }
     const int y = Y0 + 2 * rp, x = X0 + cc;
     if (x < wj) {
-      float* dst = Sj + (int64_t)k * hj * wj + (int64_t)y * wj + x;
-      if (y < hj) dst[0] = a0;
-      if (y + 1 < hj) dst[wj] = a1;
+      float* dst = Sj + (int64_t)k * nj * wj + (int64_t)(y - loj) * wj + x;
+      if (y >= loj && y < hij) dst[0] = a0;
+      if (y + 1 >= loj && y + 1 < hij) dst[wj] = a1;
     }
   }
 }
@@ -94,7 +96,9 @@ static int launch_pyr(const PyrGeom& g, const PyrImage* imgs, int n_img, cudaStr
   for (int j = g.L - 2; j >= 1; j--) {
     p.j = j;
     p.tiles_x = (g.lv.w[j] + PYR_TW - 1) / PYR_TW;
-    const int tiles = p.tiles_x * ((g.lv.h[j] + PYR_TH - 1) / PYR_TH);
+    p.y_base = g.lv.lo[j] & ~1;
+    const int tiles = p.tiles_x * ((g.lv.hi[j] - p.y_base + PYR_TH - 1) / PYR_TH);
+    if (tiles == 0) continue;
     for (int b = 0; b < n_img; b += PYR_MAX_IMG) {
       const int m = (n_img - b < PYR_MAX_IMG) ? n_img - b : PYR_MAX_IMG;
       for (int i = 0; i < m; i++) p.img[i] = imgs[b + i];
@@ -115,7 +119,9 @@ int launch_pyramid(const PyrGeom& g, int K, const PyrImage* imgs, int n_img, cud
 
 int pyramid_launch_count(const PyrGeom& g, int n_img) {
   if (g.L < 3) return 0;
-  return (g.L - 2) * ((n_img + PYR_MAX_IMG - 1) / PYR_MAX_IMG);
+  int lv = 0;
+  for (int j = g.L - 2; j >= 1; j--) lv += (g.lv.hi[j] > g.lv.lo[j]) ? 1 : 0;
+  return lv * ((n_img + PYR_MAX_IMG - 1) / PYR_MAX_IMG);
 }
 
 }  // namespace ccrd

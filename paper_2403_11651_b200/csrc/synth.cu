@@ -91,19 +91,20 @@ struct LoadLevel1 {
   static constexpr int NR = S::NR1, NC = S::NC1;
   static constexpr int IT = (NR * NC + SYN_THREADS - 1) / SYN_THREADS;
   static __device__ __forceinline__ void run(const SynParams<L, CH, R, K>& p, const SynCtx& c) {
-    const int gh = p.g.lv.h[1], gw = p.g.lv.w[1];
+    const int gw = p.g.lv.w[1], blo = p.g.lv.lo[1], bhi = p.g.lv.hi[1];  // buffer window of level 1
     const int lr = c.wlo_r[1], lc = c.wlo_c[1];
     const int16_t* g1 = p.lat + p.g.lv.off[1];
+    const int64_t plane = (int64_t)(bhi - blo) * gw;
     float v[L - 1][IT];
 #pragma unroll
     for (int k = 0; k < IT; k++) {
       const int it = threadIdx.x + k * SYN_THREADS;
       const int rr = it / NC, cc = it - rr * NC;
-      const int64_t gi = (int64_t)clampi(lr + rr, 0, gh - 1) * gw + clampi(lc + cc, 0, gw - 1);
+      const int64_t gi = (int64_t)(clampi(lr + rr, blo, bhi - 1) - blo) * gw + clampi(lc + cc, 0, gw - 1);
       const bool ok = it < NR * NC;
       v[0][k] = ok ? (float)__ldg(g1 + gi) : 0.0f;
 #pragma unroll
-      for (int sl = 1; sl < L - 1; sl++) v[sl][k] = ok ? __ldg(p.s1 + (int64_t)(sl - 1) * gh * gw + gi) : 0.0f;
+      for (int sl = 1; sl < L - 1; sl++) v[sl][k] = ok ? __ldg(p.s1 + (int64_t)(sl - 1) * plane + gi) : 0.0f;
     }
 #pragma unroll
     for (int sl = 0; sl < L - 1; sl++)
@@ -121,13 +122,14 @@ struct LoadLat0 {
   static constexpr int N = S::RH0 * S::RW0;
   static constexpr int IT = (N + SYN_THREADS - 1) / SYN_THREADS;
   static __device__ __forceinline__ void run(const SynParams<L, CH, R, K>& p, int16_t* lat0, int RY, int RX) {
-    const int H = p.g.H, W = p.g.W;
+    const int W = p.g.W, blo = p.g.lv.lo[0], bhi = p.g.lv.hi[0];  // buffer window of level 0
     int16_t v[IT];
 #pragma unroll
     for (int k = 0; k < IT; k++) {
       const int it = threadIdx.x + k * SYN_THREADS;
       const int rr = it / S::RW0, cc = it - rr * S::RW0;
-      v[k] = (it < N) ? __ldg(p.lat + (int64_t)clampi(RY + rr, 0, H - 1) * W + clampi(RX + cc, 0, W - 1)) : 0;
+      v[k] = (it < N) ? __ldg(p.lat + (int64_t)(clampi(RY + rr, blo, bhi - 1) - blo) * W + clampi(RX + cc, 0, W - 1))
+                      : 0;
     }
 #pragma unroll
     for (int k = 0; k < IT; k++) {
@@ -276,9 +278,10 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
   __shared__ double warp_buf[SYN_THREADS / 32];
 
   const int H = p.g.H, W = p.g.W;
+  const int Ys = p.g.y0, Ye = p.g.y1;  // output rows (full image: 0 .. H); x_hat / image rows are Ys-relative
   const int ty = blockIdx.x / p.g.tiles_x;
   const int tx = blockIdx.x - ty * p.g.tiles_x;
-  const int Y0 = ty * SYN_TH, X0 = tx * SYN_TW;
+  const int Y0 = Ys + ty * SYN_TH, X0 = tx * SYN_TW;
   const int RY = Y0 - RE, RX = X0 - RE;  // origin of the level-0 region (even)
 
   if (threadIdx.x < 32) {
@@ -318,7 +321,9 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
   float* hB = bufB;
   {
     const int64_t P = (int64_t)H * W;
-    const int h1 = (L > 1) ? p.g.lv.h[1] : 1;
+    const int64_t Pst = (int64_t)(Ye - Ys) * W;
+    // level-1 rows are clamped to the buffer window (= [0, h_1) for a full image)
+    const int b1lo = (L > 1) ? p.g.lv.lo[1] : 0, b1hi = (L > 1) ? p.g.lv.hi[1] : 1;
     const int lo1 = wlo_r[(L > 1) ? 1 : 0];
     constexpr int NPAIR = (RH0 / 2) * RW0;
 #pragma unroll 1
@@ -343,7 +348,7 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
           const int q = y0 >> 1;
           int ro[K / 2 + 1];
 #pragma unroll
-          for (int u = 0; u <= K / 2; u++) ro[u] = (clampi(q - K / 4 + u, 0, h1 - 1) - lo1) * RW0 + cc;
+          for (int u = 0; u <= K / 2; u++) ro[u] = (clampi(q - K / 4 + u, b1lo, b1hi - 1) - lo1) * RW0 + cc;
 #pragma unroll
           for (int l = 1; l < L; l++) {
             const float* src = bufB + (l - 1) * S::TSLOT;
@@ -381,8 +386,8 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
       if (p.h1_out != nullptr) {
 #pragma unroll
         for (int c = 0; c < 3; c++) {
-          if (in0) p.h1_out[c * P + (int64_t)y0 * W + x] = out0[c];
-          if (in1) p.h1_out[c * P + (int64_t)(y0 + 1) * W + x] = out1[c];
+          if (in0 && y0 < Ye) p.h1_out[c * Pst + (int64_t)(y0 - Ys) * W + x] = out0[c];
+          if (in1 && y0 + 1 < Ye) p.h1_out[c * Pst + (int64_t)(y0 + 1 - Ys) * W + x] = out1[c];
         }
       }
       const int o = 2 * rp * RW0 + cc;
@@ -397,7 +402,7 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
 
   SYN_MARK(3);
   // ------------------------------------------------- 3. residual 3x3 layers
-  const int64_t Pimg = (int64_t)H * W;
+  const int64_t Pimg = (int64_t)(Ye - Ys) * W;  // plane of image / x_hat (strip rows only)
   float sse = 0.0f;
   float* hin = hA;
   float* hout = hB;
@@ -411,10 +416,23 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
       co[d] = clampi(x + d - 1, 0, W - 1) - RX;
     }
     const int ctr = (y - RY) * RW0 + (x - RX);
-    uint64_t a01 = f2pack(hin[ctr] + p.w.g[r][0], hin[HP + ctr] + p.w.g[r][1]);
-    float a2 = hin[2 * HP + ctr] + p.w.g[r][2];
+    // same operation order as the interior path (bias, then per input channel
+    // its residual term and its 9 taps), so a pixel's value does not depend on
+    // whether it falls in a tile's interior or its halo ring: strips and the
+    // full image agree bit for bit
+    uint64_t a01 = f2pack(p.w.g[r][0], p.w.g[r][1]);
+    float a2 = p.w.g[r][2];
 #pragma unroll
-    for (int ci = 0; ci < 3; ci++)
+    for (int ci = 0; ci < 3; ci++) {
+      const float c = hin[ci * HP + ctr];
+      if (ci == 2) {
+        a2 += c;
+      } else {
+        float2 t = f2unpack(a01);
+        if (ci == 0) t.x += c;
+        else t.y += c;
+        a01 = f2pack(t.x, t.y);
+      }
 #pragma unroll
       for (int ky = 0; ky < 3; ky++)
 #pragma unroll
@@ -423,6 +441,7 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
           a01 = ffma2(f2pack(hv, hv), ldp2(p.w.Gp[r][ci][ky][kx]), a01);
           a2 = fmaf(hv, p.w.Gs[r][ci][ky][kx], a2);
         }
+    }
     const float2 a = f2unpack(a01);
     o[0] = a.x;
     o[1] = a.y;
@@ -432,6 +451,7 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
   for (int r = 0; r < R; r++) {
     const int e = R - 1 - r;  // halo this layer's output still needs
     const bool last = (r == R - 1);
+    const int ylim = last ? Ye : H;  // non-last layers also feed the rows just past the strip
     // interior (the tile): each thread owns a column segment of RS rows; per
     // input channel it loads the (RS + 2) x 3 window once and every uniform
     // weight (pair) feeds RS outputs
@@ -440,7 +460,7 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
       const int cc = threadIdx.x % SYN_TW, seg = threadIdx.x / SYN_TW;
       const int x = X0 + cc;
       const int yb = Y0 + seg * RS;
-      if (x < W && yb < H) {
+      if (x < W && yb < ylim) {
         int co[3];
 #pragma unroll
         for (int d = 0; d < 3; d++) co[d] = clampi(x + d - 1, 0, W - 1) - RX;
@@ -450,7 +470,7 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
           for (int i = 0; i < RS; i++)
 #pragma unroll
             for (int c = 0; c < 3; c++)
-              img[i][c] = (yb + i < H) ? __ldg(p.image + c * Pimg + (int64_t)(yb + i) * W + x) : 0.0f;
+              img[i][c] = (yb + i < Ye) ? __ldg(p.image + c * Pimg + (int64_t)(yb + i - Ys) * W + x) : 0.0f;
         }
         uint64_t a01[RS];
         float a2[RS];
@@ -497,7 +517,7 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
 #pragma unroll
         for (int i = 0; i < RS; i++) {
           const int y = yb + i;
-          if (y >= H) break;
+          if (y >= ylim) break;
           const float2 a = f2unpack(a01[i]);
           const float o[3] = {a.x, a.y, a2[i]};
           if (!last) {
@@ -505,7 +525,7 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
 #pragma unroll
             for (int c = 0; c < 3; c++) hout[c * HP + ctr] = fmaxf(o[c], 0.0f);
           } else {
-            const int64_t gi = (int64_t)y * W + x;
+            const int64_t gi = (int64_t)(y - Ys) * W + x;
 #pragma unroll
             for (int c = 0; c < 3; c++) {
               if (p.x_hat != nullptr) p.x_hat[c * Pimg + gi] = o[c];
@@ -561,9 +581,9 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
     for (int item = threadIdx.x; item < SYN_TH * SYN_TW; item += SYN_THREADS) {
       const int rr = item / SYN_TW, cc = item - rr * SYN_TW;
       const int y = Y0 + rr, x = X0 + cc;
-      if (y >= H || x >= W) continue;
+      if (y >= Ye || x >= W) continue;
       const int ctr = (y - RY) * RW0 + (x - RX);
-      const int64_t gi = (int64_t)y * W + x;
+      const int64_t gi = (int64_t)(y - Ys) * W + x;
 #pragma unroll
       for (int c = 0; c < 3; c++) {
         const float xh = hin[c * HP + ctr];
