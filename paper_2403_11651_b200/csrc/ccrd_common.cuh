@@ -136,18 +136,24 @@ struct ArmParams {
 #ifndef CCRD_SYN_CPS
 #define CCRD_SYN_CPS 2
 #endif
-constexpr int SYN_TH = 32;
-constexpr int SYN_TW = 64;
+#ifndef CCRD_SYN_TH
+#define CCRD_SYN_TH 32
+#endif
+#ifndef CCRD_SYN_TW
+#define CCRD_SYN_TW 64
+#endif
+constexpr int SYN_TH = CCRD_SYN_TH;
+constexpr int SYN_TW = CCRD_SYN_TW;
 constexpr int SYN_THREADS = CCRD_SYN_THREADS;
 constexpr int SYN_CTAS_PER_SM = CCRD_SYN_CPS;
 
 template <int L, int CH, int R, int K>
 struct SynWeights {
   float k[K];                 // upsampling taps
-  float2 A0[L][CH / 2];       // 1x1 layer 0, pairs of outputs per input
-  float2 a0[CH / 2];
-  float2 A1p[CH];             // 1x1 layer 1 outputs (0, 1) per input
-  float A1s[CH];              // 1x1 layer 1 output 2 per input
+  float2 kv[K / 2 + 1];       // last vertical step, both phases: (a0, a1) += sv[u] x kv[u]
+  float A0t[L][CH];           // 1x1 layer 0, input-major (4 consecutive outputs per uniform load)
+  float a0[CH];
+  float A1[3][CH];            // 1x1 layer 1
   float a1[3];
   float2 Gp[(R > 0) ? R : 1][3][3][3];  // residual 3x3: (co 0, co 1) per [ci][ky][kx]
   float Gs[(R > 0) ? R : 1][3][3][3];   // co 2

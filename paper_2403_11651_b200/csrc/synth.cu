@@ -187,80 +187,36 @@ struct ChainStep {
 };
 
 // 1x1 synthesis layers L -> CH (ReLU) -> 3 (ReLU unless R == 0: the module's
-// last layer) for two pixels; every uniform weight (pair) feeds both.
+// last layer) for a PAIR of pixels (rows 2q, 2q+1) held in the two lanes of
+// every FFMA2: v[i] = (pixel 0, pixel 1) of input channel i, and each weight
+// is a broadcast uniform operand (UR.F32), so one instruction does one MAC of
+// both pixels and 4 weights come per uniform load.  Per neuron: bias first,
+// then the inputs in order (the oracle's summation order).
 template <int L, int CH, int R, int K>
-__device__ __forceinline__ void mlp_2px(const SynParams<L, CH, R, K>& p, const float (&v0)[L], const float (&v1)[L],
-                                        float (&out0)[3], float (&out1)[3]) {
-  uint64_t acc0[CH / 2], acc1[CH / 2];
+__device__ __forceinline__ void mlp_pair(const SynParams<L, CH, R, K>& p, const uint64_t (&v)[L], uint64_t (&out)[3]) {
+  const uint64_t one = f2pack(1.0f, 1.0f);
+  uint64_t acc[CH];
 #pragma unroll
-  for (int n = 0; n < CH / 2; n++) acc0[n] = acc1[n] = ldp2(p.w.a0[n]);
+  for (int n = 0; n < CH; n++) acc[n] = ffma2(one, f2pack(p.w.a0[n], p.w.a0[n]), 0ull);
 #pragma unroll
-  for (int i = 0; i < L; i++) {
-    const uint64_t x0 = f2pack(v0[i], v0[i]), x1 = f2pack(v1[i], v1[i]);
+  for (int i = 0; i < L; i++)
 #pragma unroll
-    for (int n = 0; n < CH / 2; n++) {
-      const uint64_t wgt = ldp2(p.w.A0[i][n]);
-      acc0[n] = ffma2(x0, wgt, acc0[n]);
-      acc1[n] = ffma2(x1, wgt, acc1[n]);
-    }
-  }
-  uint64_t o0 = f2pack(p.w.a1[0], p.w.a1[1]), o1 = o0;
-  float o0s = p.w.a1[2], o1s = p.w.a1[2];
+    for (int n = 0; n < CH; n++) acc[n] = ffma2(v[i], f2pack(p.w.A0t[i][n], p.w.A0t[i][n]), acc[n]);
 #pragma unroll
-  for (int n = 0; n < CH / 2; n++) {
-    const float2 h0 = f2unpack(acc0[n]), h1v = f2unpack(acc1[n]);
-    const float h0a = fmaxf(h0.x, 0.0f), h0b = fmaxf(h0.y, 0.0f);
-    const float h1a = fmaxf(h1v.x, 0.0f), h1b = fmaxf(h1v.y, 0.0f);
-    const uint64_t wa = ldp2(p.w.A1p[2 * n]), wb = ldp2(p.w.A1p[2 * n + 1]);
-    o0 = ffma2(f2pack(h0a, h0a), wa, o0);
-    o1 = ffma2(f2pack(h1a, h1a), wa, o1);
-    o0s = fmaf(h0a, p.w.A1s[2 * n], o0s);
-    o1s = fmaf(h1a, p.w.A1s[2 * n], o1s);
-    o0 = ffma2(f2pack(h0b, h0b), wb, o0);
-    o1 = ffma2(f2pack(h1b, h1b), wb, o1);
-    o0s = fmaf(h0b, p.w.A1s[2 * n + 1], o0s);
-    o1s = fmaf(h1b, p.w.A1s[2 * n + 1], o1s);
-  }
-  const float2 r0 = f2unpack(o0), r1 = f2unpack(o1);
-  out0[0] = r0.x; out0[1] = r0.y; out0[2] = o0s;
-  out1[0] = r1.x; out1[1] = r1.y; out1[2] = o1s;
-  if (R > 0) {
-#pragma unroll
-    for (int c = 0; c < 3; c++) {
-      out0[c] = fmaxf(out0[c], 0.0f);
-      out1[c] = fmaxf(out1[c], 0.0f);
-    }
-  }
-}
-
-// the same for one pixel (same FMA order, fewer live registers)
-template <int L, int CH, int R, int K>
-__device__ __forceinline__ void mlp_1px(const SynParams<L, CH, R, K>& p, const float (&v)[L], float (&out)[3]) {
-  uint64_t acc[CH / 2];
-#pragma unroll
-  for (int n = 0; n < CH / 2; n++) acc[n] = ldp2(p.w.a0[n]);
-#pragma unroll
-  for (int i = 0; i < L; i++) {
-    const uint64_t x = f2pack(v[i], v[i]);
-#pragma unroll
-    for (int n = 0; n < CH / 2; n++) acc[n] = ffma2(x, ldp2(p.w.A0[i][n]), acc[n]);
-  }
-  uint64_t o = f2pack(p.w.a1[0], p.w.a1[1]);
-  float os = p.w.a1[2];
-#pragma unroll
-  for (int n = 0; n < CH / 2; n++) {
+  for (int n = 0; n < CH; n++) {
     const float2 h = f2unpack(acc[n]);
-    const float ha = fmaxf(h.x, 0.0f), hb = fmaxf(h.y, 0.0f);
-    o = ffma2(f2pack(ha, ha), ldp2(p.w.A1p[2 * n]), o);
-    os = fmaf(ha, p.w.A1s[2 * n], os);
-    o = ffma2(f2pack(hb, hb), ldp2(p.w.A1p[2 * n + 1]), o);
-    os = fmaf(hb, p.w.A1s[2 * n + 1], os);
+    acc[n] = f2pack(fmaxf(h.x, 0.0f), fmaxf(h.y, 0.0f));
   }
-  const float2 r = f2unpack(o);
-  out[0] = r.x; out[1] = r.y; out[2] = os;
-  if (R > 0) {
 #pragma unroll
-    for (int c = 0; c < 3; c++) out[c] = fmaxf(out[c], 0.0f);
+  for (int c = 0; c < 3; c++) {
+    uint64_t o = ffma2(one, f2pack(p.w.a1[c], p.w.a1[c]), 0ull);
+#pragma unroll
+    for (int n = 0; n < CH; n++) o = ffma2(acc[n], f2pack(p.w.A1[c][n], p.w.A1[c][n]), o);
+    if (R > 0) {
+      const float2 h = f2unpack(o);
+      o = f2pack(fmaxf(h.x, 0.0f), fmaxf(h.y, 0.0f));
+    }
+    out[c] = o;
   }
 }
 
@@ -333,18 +289,18 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
       const int y0 = RY + 2 * rp, x = RX + cc;
       if (x < 0 || x >= W || y0 + 1 < 0 || y0 >= H) continue;  // never read by the convs
       const bool has1 = (y0 + 1 < H);
-      float v0[L], v1[L];
+      uint64_t v[L];  // (row y0, row y0 + 1) of every dense channel
       if constexpr (DENSE_IN) {
 #pragma unroll
-        for (int l = 0; l < L; l++) {
-          v0[l] = __ldg(p.dense_in + l * P + (int64_t)y0 * W + x);
-          v1[l] = has1 ? __ldg(p.dense_in + l * P + (int64_t)(y0 + 1) * W + x) : 0.0f;
-        }
+        for (int l = 0; l < L; l++)
+          v[l] = f2pack(__ldg(p.dense_in + l * P + (int64_t)y0 * W + x),
+                        has1 ? __ldg(p.dense_in + l * P + (int64_t)(y0 + 1) * W + x) : 0.0f);
       } else {
-        v0[0] = (float)lat0[2 * rp * RW0 + cc];
-        v1[0] = (float)lat0[(2 * rp + 1) * RW0 + cc];
+        v[0] = f2pack((float)lat0[2 * rp * RW0 + cc], (float)lat0[(2 * rp + 1) * RW0 + cc]);
         if constexpr (L > 1) {
-          // sources: rows q - K/4 .. q + K/4 of window 1 (q = y0 / 2), clamped
+          // last vertical x2 step, both phases in one FFMA2 lane pair:
+          // (out[2q], out[2q+1]) = sum_u sv[u] (k[K-1-2u], k[K-2u]) over the
+          // sources sv[u] = rows q - K/4 + u of window 1 (clamped)
           const int q = y0 >> 1;
           int ro[K / 2 + 1];
 #pragma unroll
@@ -352,17 +308,13 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
 #pragma unroll
           for (int l = 1; l < L; l++) {
             const float* src = bufB + (l - 1) * S::TSLOT;
-            float sv[K / 2 + 1];
+            uint64_t a = 0ull;
 #pragma unroll
-            for (int u = 0; u <= K / 2; u++) sv[u] = src[ro[u]];
-            float a0 = 0.0f, a1 = 0.0f;
-#pragma unroll
-            for (int t = 0; t < K / 2; t++) {
-              a0 = fmaf(p.w.k[2 * t + 1], sv[K / 2 - 1 - t], a0);
-              a1 = fmaf(p.w.k[2 * t], sv[K / 2 - t], a1);
+            for (int u = K / 2; u >= 0; u--) {
+              const float sv = src[ro[u]];
+              a = ffma2(f2pack(sv, sv), ldp2(p.w.kv[u]), a);
             }
-            v0[l] = a0;
-            v1[l] = a1;
+            v[l] = a;
           }
         }
       }
@@ -372,17 +324,20 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
       if (p.dense_out != nullptr) {
 #pragma unroll
         for (int l = 0; l < L; l++) {
-          if (in0) p.dense_out[l * P + (int64_t)y0 * W + x] = v0[l];
-          if (in1) p.dense_out[l * P + (int64_t)(y0 + 1) * W + x] = v1[l];
+          const float2 d = f2unpack(v[l]);
+          if (in0) p.dense_out[l * P + (int64_t)y0 * W + x] = d.x;
+          if (in1) p.dense_out[l * P + (int64_t)(y0 + 1) * W + x] = d.y;
         }
       }
+      uint64_t op[3];
+      mlp_pair<L, CH, R, K>(p, v, op);
       float out0[3], out1[3];
-#ifdef CCRD_SYN_MLP1
-      mlp_1px<L, CH, R, K>(p, v0, out0);
-      mlp_1px<L, CH, R, K>(p, v1, out1);
-#else
-      mlp_2px<L, CH, R, K>(p, v0, v1, out0, out1);
-#endif
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        const float2 t = f2unpack(op[c]);
+        out0[c] = t.x;
+        out1[c] = t.y;
+      }
       if (p.h1_out != nullptr) {
 #pragma unroll
         for (int c = 0; c < 3; c++) {
@@ -635,15 +590,17 @@ static int launch_syn(const SynGeom& g, const cc_model_desc& d, const float* up_
   p.h1_out = h1_out;
   p.partial = partial;
   for (int t = 0; t < K; t++) p.w.k[t] = up_w ? up_w[t] : 0.0f;
+  // last vertical step: (a0, a1) += sv[u] (k[K-1-2u], k[K-2u]), zero where a
+  // phase has no tap (u = K/2 for a0, u = 0 for a1)
+  for (int u = 0; u <= K / 2; u++)
+    p.w.kv[u] = make_float2(u < K / 2 && up_w ? up_w[K - 1 - 2 * u] : 0.0f, u > 0 && up_w ? up_w[K - 2 * u] : 0.0f);
   const float* q = syn_w;
   for (int i = 0; i < L; i++)
-    for (int n = 0; n < CH / 2; n++) p.w.A0[i][n] = make_float2(q[(2 * n) * L + i], q[(2 * n + 1) * L + i]);
-  for (int n = 0; n < CH / 2; n++) p.w.a0[n] = make_float2(q[L * CH + 2 * n], q[L * CH + 2 * n + 1]);
+    for (int n = 0; n < CH; n++) p.w.A0t[i][n] = q[n * L + i];
+  for (int n = 0; n < CH; n++) p.w.a0[n] = q[L * CH + n];
   q += L * CH + CH;
-  for (int i = 0; i < CH; i++) {
-    p.w.A1p[i] = make_float2(q[i], q[CH + i]);
-    p.w.A1s[i] = q[2 * CH + i];
-  }
+  for (int c = 0; c < 3; c++)
+    for (int n = 0; n < CH; n++) p.w.A1[c][n] = q[c * CH + n];
   for (int c = 0; c < 3; c++) p.w.a1[c] = q[3 * CH + c];
   q += 3 * CH + 3;
   for (int r = 0; r < R; r++) {
