@@ -1,0 +1,437 @@
+// arm_tc.cu -- ARM rate on the 5th-generation tensor cores (tcgen05 + TMEM).
+//
+// Same function as arm_rate.cu (PAPER.md:106-109 ARM f_psi, :120 R term of
+// Eq. 1; Table 1 ARM column; readings #1-#8): for every latent the
+// causal context c, the MLP z1 = ReLU(W0 c + b0), z_{k+1} = ReLU(W_k z_k + b_k
+// [+ z_k]), (mu, s) = W_out z + b_out, then -log2 of the Laplace bin mass.
+//
+// The hidden layers are dense contractions over all latents at once -- [128
+// latents x K] x [K x N] per MMA block -- so they run as tcgen05.mma kind::tf32
+// with fp32 accumulators in TMEM:
+//   * layer 0: A = the context rows, small integers (|y| <= 2^10), EXACT in
+//     tf32, so only the weights are split: W = W_hi + W_lo (tf32 each) and
+//     D = A.W_hi + A.W_lo.  The bias rides on a constant-1 input column.
+//   * hidden layer k >= 1: the activations are arbitrary fp32, split per
+//     element z = z_hi + z_lo (cvt.rna.tf32 + exact subtraction):
+//     D = z_hi.W_hi + z_hi.W_lo + z_lo.W_hi ("3xTF32"): every product is exact
+//     in fp32 and only the z_lo.W_lo term (~2^-22 relative) is dropped, so the
+//     result is fp32-accurate (well inside the 1e-3-bit per-latent and 1e-4
+//     total-rate tolerances).
+//   * the 2-wide output layer, the Laplace bits and the reduction stay on the
+//     CUDA cores (packed FFMA2, uniform weights), one latent per thread.
+//
+// CTA = 128 threads = one MMA block of M = 128 latents at a time: thread t
+// owns latent t of the block, writes row t of the A operand and reads TMEM
+// lane t of the accumulator (warp w <-> lanes 32w .. 32w+31).  A tile of the
+// FFMA2 kernel's geometry (8 rows x 64 latents; same tile table, same window
+// staging) is 4 blocks of 2 rows.  Operands are K-major, no-swizzle canonical
+// layout in shared memory (8-row x 16-byte core matrices; LBO = 128 B between
+// K-adjacent core matrices, SBO = K/4 x 128 B between 8-row groups; the encoding
+// is validated by tools/microbench/tc_probe.cu).  Several CTAs per SM overlap
+// one CTA's MMA wait with the others' CUDA-core work.
+//
+// Status (measured on B200): 142 us per 2K image vs 140 us for
+// the FFMA2 kernel -- each 128-latent block pays two serialised MMA round trips
+// and 4 CTAs per SM do not hide them; a variant with the A operands in TMEM
+// (tcgen05.st, TS MMAs) measured 175 us.  Beating FFMA2 needs a warp-specialised
+// multi-stage pipeline, so this path is opt-in (CCRD_ARM_PATH=tc) and
+// parity-tested, not the default.
+#include <cstring>
+
+#include "ccrd_common.cuh"
+
+namespace ccrd {
+
+constexpr int TC_THREADS = 128;
+constexpr int TC_M = 128;
+constexpr int TC_CTAS_PER_SM = 4;
+
+__host__ __device__ constexpr int rup(int x, int m) { return (x + m - 1) / m * m; }
+
+template <int C, int NH, int NHL>
+struct ArmTcShape {
+  static constexpr int K0 = rup(C + 1, 8);                  // context + bias column
+  static constexpr int NP = rup(NH, 16) < 16 ? 16 : rup(NH, 16);  // MMA N (M = 128 needs N % 16 == 0)
+  static constexpr int K1 = rup(NH + 1, 8);                 // hidden + bias column
+  static constexpr int NHID = NHL - 1;                      // NH -> NH layers on the tensor cores
+  static constexpr int BW0 = NP * K0;                       // floats per weight matrix
+  static constexpr int BW1 = NP * K1;
+  static constexpr int A_FLOATS = TC_M * (K0 > 2 * K1 ? K0 : 2 * K1);  // A0 | (A_hi, A_lo)
+  static constexpr int WIN = ARM_SH * ARM_SW;
+  static constexpr int B_FLOATS = 2 * BW0 + 2 * NHID * BW1;
+  static constexpr size_t SMEM = sizeof(float) * (size_t)(A_FLOATS + B_FLOATS + WIN) + 64;
+  static_assert(NP <= 32, "one 32-column TMEM accumulator");
+  static_assert(K0 % 8 == 0 && K1 % 8 == 0, "tcgen05 shape");
+};
+
+// K-major canonical offset (floats) of element (r, k) of an operand with K
+// columns: core matrix (r/8, k/4), 8 rows x 4 floats each
+__host__ __device__ constexpr int kmaj(int r, int k, int K) {
+  return (r >> 3) * (K / 4) * 32 + (k >> 2) * 32 + (r & 7) * 4 + (k & 3);
+}
+
+template <int C, int NH, int NHL>
+struct ArmTcParams {
+  using S = ArmTcShape<C, NH, NHL>;
+  ArmGeom g;
+  const int16_t* lat;
+  double* partial;  // [tiles][16]: one per (block, warp)
+  float* mu;        // optional per-latent debug outputs
+  float* scale;
+  float* bits;
+  // weights, pre-split on the host into tf32 (hi, lo) pairs, canonical layout
+  float B0[2][S::BW0];                                    // [hi/lo] layer 0 (bias in column C)
+  float B1[(S::NHID > 0) ? S::NHID : 1][2][S::BW1];       // [layer][hi/lo] (residual folded, bias in column NH)
+  float2 wo[NH];                                          // output layer (mu, log-scale) per input
+  float2 bo;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);  // version 1, no swizzle
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t b = smem_u32(bar);
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(b), "r"(phase));
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// TMEM lane block of this warp -> NP fp32 registers (this thread's latent)
+template <int NP>
+__device__ __forceinline__ void tmem_row(uint32_t taddr, float (&v)[NP]);
+template <>
+__device__ __forceinline__ void tmem_row<32>(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 32; j++) v[j] = __uint_as_float(r[j]);
+}
+template <>
+__device__ __forceinline__ void tmem_row<16>(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 16; j++) v[j] = __uint_as_float(r[j]);
+}
+
+// -log2 Laplace bin mass (identical to arm_rate.cu's; see there)
+__device__ __forceinline__ float laplace_bits_tc(float y, float mu, float s, const ArmGeom& g) {
+  constexpr float LOG2E = 1.4426950408889634f;
+  s = fminf(fmaxf(s, g.lsmin), g.lsmax);
+  const float ibl = exp2f_approx(-s * LOG2E) * LOG2E;
+  const float a = fabsf(y - mu);
+  const float am = fminf(a, 0.5f);
+  const float e1 = exp2f_approx((am - 0.5f) * ibl);
+  const float e2 = exp2f_approx(-(am + 0.5f) * ibl);
+  const float p_in = 1.0f - 0.5f * (e1 + e2);
+  const float bits_in = -log2f_approx(fmaxf(p_in, g.p_floor));
+  const float bits_out = fmaf(a - 0.5f, ibl, 1.0f) - log2f_approx(1.0f - exp2f_approx(-ibl));
+  return fminf(a < 0.5f ? bits_in : bits_out, g.bits_cap);
+}
+
+template <int C, int NH, int NHL>
+__global__ void __launch_bounds__(TC_THREADS, TC_CTAS_PER_SM)
+    arm_tc_kernel(const __grid_constant__ ArmTcParams<C, NH, NHL> p) {
+  using S = ArmTcShape<C, NH, NHL>;
+  constexpr int K0 = S::K0, NP = S::NP, K1 = S::K1;
+  extern __shared__ __align__(1024) float tsm[];
+  float* sA = tsm;                              // A0 [128 x K0] | A_hi, A_lo [128 x K1] each
+  float* sB = tsm + S::A_FLOATS;                // B0 hi, lo, then B1 hi, lo per hidden layer
+  float* win = sB + S::B_FLOATS;                // causal window of the tile (fp32)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(win + S::WIN + (S::WIN & 1));
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  // weights -> shared memory (canonical layout prepared on the host)
+  {
+    const float4* src0 = reinterpret_cast<const float4*>(&p.B0[0][0]);
+    float4* dst = reinterpret_cast<float4*>(sB);
+    for (int i = t; i < 2 * S::BW0 / 4; i += TC_THREADS) dst[i] = src0[i];
+    if constexpr (S::NHID > 0) {
+      const float4* src1 = reinterpret_cast<const float4*>(&p.B1[0][0][0]);
+      for (int i = t; i < 2 * S::NHID * S::BW1 / 4; i += TC_THREADS) dst[2 * S::BW0 / 4 + i] = src1[i];
+    }
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+  const uint32_t sA_u = smem_u32(sA), sB_u = smem_u32(sB);
+  uint32_t phase = 0;
+
+  const int n_tiles = p.g.tile_begin[p.g.L];
+#pragma unroll 1
+  for (int b = blockIdx.x; b < n_tiles; b += gridDim.x) {
+    // ---- (level, tile) and the causal window (zero outside the grid)
+    int l = 0;
+#pragma unroll 1
+    while (l + 1 < p.g.L && b >= p.g.tile_begin[l + 1]) l++;
+    const int tl = b - p.g.tile_begin[l];
+    const int ty = tl / p.g.tiles_x[l];
+    const int i0 = p.g.own_lo[l] + ty * ARM_TY, j0 = (tl - ty * p.g.tiles_x[l]) * ARM_TX;
+    const int w = p.g.lv.w[l], rlo = p.g.lv.lo[l], rhi = p.g.lv.hi[l];
+    const int16_t* __restrict__ grid = p.lat + p.g.lv.off[l];
+    {
+      constexpr int IT = (S::WIN + TC_THREADS - 1) / TC_THREADS;
+      int16_t v[IT];
+#pragma unroll
+      for (int k = 0; k < IT; k++) {
+        const int s = t + k * TC_THREADS;
+        const int r = s / ARM_SW, c = s - r * ARM_SW;
+        const int gi = i0 - ARM_HALO_TOP + r, gj = j0 - ARM_HALO_X + c;
+        v[k] = (s < S::WIN && gi >= rlo && gi < rhi && gj >= 0 && gj < w) ? __ldg(grid + (int64_t)(gi - rlo) * w + gj)
+                                                                        : (int16_t)0;
+      }
+      __syncthreads();  // the previous tile's readers of `win` are done
+#pragma unroll
+      for (int k = 0; k < IT; k++) {
+        const int s = t + k * TC_THREADS;
+        if (s < S::WIN) win[s] = (float)v[k];
+      }
+      __syncthreads();
+    }
+
+    // ---- four blocks of 2 rows x 64 latents
+#pragma unroll 1
+    for (int q = 0; q < ARM_TY / 2; q++) {
+      const int ry = 2 * q + (t >> 6), cx = t & 63;  // this thread's latent in the tile
+      const float* center = win + (ry + ARM_HALO_TOP) * ARM_SW + cx + ARM_HALO_X;
+      const float y = center[0];
+      // A0 row t: [context (C), 1 (bias), 0 ...]
+      {
+        float row[K0];
+#pragma unroll
+        for (int c = 0; c < C; c++) row[c] = center[p.g.ctx_off[c]];
+        row[C] = 1.0f;
+#pragma unroll
+        for (int c = C + 1; c < K0; c++) row[c] = 0.0f;
+#pragma unroll
+        for (int c4 = 0; c4 < K0 / 4; c4++)
+          *reinterpret_cast<float4*>(sA + kmaj(t, 4 * c4, K0)) =
+              make_float4(row[4 * c4], row[4 * c4 + 1], row[4 * c4 + 2], row[4 * c4 + 3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncthreads();
+      if (t == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+        for (int s = 0; s < K0 / 8; s++) {
+          const uint64_t da = umma_desc(sA_u + s * 256, 128, (K0 / 4) * 128);
+          mma_tf32(tmem, da, umma_desc(sB_u + s * 256, 128, (K0 / 4) * 128), IDESC, s > 0);
+          mma_tf32(tmem, da, umma_desc(sB_u + S::BW0 * 4 + s * 256, 128, (K0 / 4) * 128), IDESC, 1);
+        }
+        mma_commit(bar);
+      }
+      mbar_wait(bar, phase);
+      phase ^= 1;
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      float z[NP];
+      tmem_row<NP>(taddr, z);
+#pragma unroll
+      for (int n = 0; n < NH; n++) z[n] = fmaxf(z[n], 0.0f);
+
+      // ---- hidden layers NH -> NH (3xTF32)
+#pragma unroll 1
+      for (int k = 0; k < S::NHID; k++) {
+        float* aH = sA;
+        float* aL = sA + TC_M * K1;
+#pragma unroll
+        for (int c4 = 0; c4 < K1 / 4; c4++) {
+          float hi[4], lo[4];
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            const int c = 4 * c4 + e;
+            const float x = (c < NH) ? z[c] : (c == NH ? 1.0f : 0.0f);
+            hi[e] = tf32_rna(x);
+            lo[e] = x - hi[e];
+          }
+          *reinterpret_cast<float4*>(aH + kmaj(t, 4 * c4, K1)) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<float4*>(aL + kmaj(t, 4 * c4, K1)) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        if (t == 0) {
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t bh = sB_u + 4 * (2 * S::BW0 + 2 * k * S::BW1), bl = bh + 4 * S::BW1;
+          const uint32_t ah = sA_u, al = sA_u + 4 * TC_M * K1;
+#pragma unroll
+          for (int s = 0; s < K1 / 8; s++) {
+            const uint64_t dah = umma_desc(ah + s * 256, 128, (K1 / 4) * 128);
+            const uint64_t dal = umma_desc(al + s * 256, 128, (K1 / 4) * 128);
+            const uint64_t dbh = umma_desc(bh + s * 256, 128, (K1 / 4) * 128);
+            const uint64_t dbl = umma_desc(bl + s * 256, 128, (K1 / 4) * 128);
+            mma_tf32(tmem, dah, dbh, IDESC, s > 0);
+            mma_tf32(tmem, dah, dbl, IDESC, 1);
+            mma_tf32(tmem, dal, dbh, IDESC, 1);
+          }
+          mma_commit(bar);
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        tmem_row<NP>(taddr, z);
+#pragma unroll
+        for (int n = 0; n < NH; n++) z[n] = fmaxf(z[n], 0.0f);
+      }
+
+      // ---- output layer (mu, log-scale) on the CUDA cores, Laplace bits
+      uint64_t o = ldp2(p.bo);
+#pragma unroll
+      for (int n = 0; n < NH; n++) o = ffma2(f2pack(z[n], z[n]), ldp2(p.wo[n]), o);
+      const int i = i0 + ry, j = j0 + cx;
+      float bits = 0.0f;
+      if (i < p.g.own_hi[l] && j < w) {
+        const float2 ms = f2unpack(o);
+        bits = laplace_bits_tc(y, ms.x, ms.y, p.g);
+        if (p.bits != nullptr) {
+          const int64_t qi = p.g.lv.off[l] + (int64_t)(i - rlo) * w + j;
+          p.bits[qi] = bits;
+          if (p.mu) p.mu[qi] = ms.x;
+          if (p.scale) p.scale[qi] = __expf(fminf(fmaxf(ms.y, p.g.lsmin), p.g.lsmax));
+        }
+      }
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) bits += __shfl_xor_sync(0xffffffffu, bits, o2);
+      if (lane == 0) p.partial[(int64_t)b * 16 + q * 4 + warp] = (double)bits;
+      // the next block rewrites A and the accumulator: every thread's TMEM load
+      // of this block is complete (wait::ld in tmem_row) before the barrier
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;");
+    }
+  }
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
+}
+
+// ---------------------------------------------------------------- host launcher
+// tf32 round-to-nearest (ties away, like cvt.rna) of a finite float
+static float tf32_rna_host(float x) {
+  uint32_t u;
+  memcpy(&u, &x, 4);
+  u = (u + 0x1000u) & 0xFFFFE000u;
+  float r;
+  memcpy(&r, &u, 4);
+  return r;
+}
+
+template <int C, int NH, int NHL>
+static int launch_arm_tc(const ArmGeom& g, const cc_model_desc& d, const float* arm_w, const int16_t* lat,
+                         double* partial, float* mu, float* scale, float* bits, cudaStream_t stream) {
+  using S = ArmTcShape<C, NH, NHL>;
+  using P = ArmTcParams<C, NH, NHL>;
+  static_assert(sizeof(P) <= 32 * 1024 - 16, "kernel parameters exceed the 32 KB bank");
+  P p;  // ~15 KB, copied into the launch's parameter bank
+  memset(&p, 0, sizeof(p));
+  p.g = g;
+  p.lat = lat;
+  p.partial = partial;
+  p.mu = mu;
+  p.scale = scale;
+  p.bits = bits;
+  auto res = [&](int k) { return (d.arm_residual_mask >> k) & 1u; };
+  auto put = [](float* hi, float* lo, int n, int k, int K, float v) {
+    const float h = tf32_rna_host(v);
+    hi[kmaj(n, k, K)] = h;
+    lo[kmaj(n, k, K)] = v - h;
+  };
+  // blob: per layer W[out][in] then b[out]
+  const float* q = arm_w;
+  for (int n = 0; n < NH; n++) {
+    for (int i = 0; i < C; i++) put(p.B0[0], p.B0[1], n, i, S::K0, q[n * C + i] + ((res(0) && i == n) ? 1.0f : 0.0f));
+    put(p.B0[0], p.B0[1], n, C, S::K0, q[C * NH + n]);
+  }
+  q += C * NH + NH;
+  for (int k = 0; k < NHL - 1; k++) {
+    for (int n = 0; n < NH; n++) {
+      for (int i = 0; i < NH; i++)
+        put(p.B1[k][0], p.B1[k][1], n, i, S::K1, q[n * NH + i] + ((res(k + 1) && i == n) ? 1.0f : 0.0f));
+      put(p.B1[k][0], p.B1[k][1], n, NH, S::K1, q[NH * NH + n]);
+    }
+    q += NH * NH + NH;
+  }
+  for (int i = 0; i < NH; i++) p.wo[i] = make_float2(q[i], q[NH + i]);
+  p.bo = make_float2(q[2 * NH], q[2 * NH + 1]);
+
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(arm_tc_kernel<C, NH, NHL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+    attr = true;
+  }
+  const int tiles = g.tile_begin[g.L];
+  if (tiles == 0) return 0;
+  const int cap = TC_CTAS_PER_SM * device_sm_count();
+  arm_tc_kernel<C, NH, NHL><<<tiles < cap ? tiles : cap, TC_THREADS, S::SMEM, stream>>>(p);
+  return 1;
+}
+
+struct ArmTcEntry {
+  int C, NH, NHL;
+  ArmLaunchFn fn;
+};
+
+// Tensor-core ARM shapes: the ~2000 MAC/pixel config ([16,24,24,2]) and the
+// Table 1 wider ARMs (A1079 [16,16,16,2], A2300 [24,24,24,2]).
+static const ArmTcEntry kArmTc[] = {
+    {16, 24, 2, launch_arm_tc<16, 24, 2>},
+    {16, 16, 2, launch_arm_tc<16, 16, 2>},
+    {24, 24, 2, launch_arm_tc<24, 24, 2>},
+};
+
+ArmLaunchFn find_arm_tc_launcher(int C, int NH, int NHL) {
+  for (const auto& e : kArmTc)
+    if (e.C == C && e.NH == NH && e.NHL == NHL) return e.fn;
+  return nullptr;
+}
+
+}  // namespace ccrd

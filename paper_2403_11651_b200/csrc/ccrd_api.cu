@@ -2,6 +2,7 @@
 // the compiled kernel shapes, the deterministic fp64 reduction kernel, the
 // host-buffer (end-to-end) path and the MAC closed form.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 
@@ -149,6 +150,39 @@ static void full_strip(const cc_model_desc& d, cc_strip& st) {
   }
 }
 
+// SM count of the current device (lazily cached device attribute; 148 = B200
+// when no device is visible).  Sizes the persistent grids.
+int device_sm_count() {
+  static thread_local int dev_cached = -2, sms = 148;
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = -1;
+  if (dev != dev_cached) {
+    int n = 0;
+    if (dev < 0 || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cudaGetLastError();
+    sms = n;
+    dev_cached = dev;
+  }
+  return sms;
+}
+
+// ARM path: the FFMA2 kernel (arm_rate.cu) by default -- measured faster than
+// the tensor-core kernel (arm_tc.cu).  CCRD_ARM_PATH=tc selects
+// the tensor-core kernel for the shapes it is compiled for (read once).
+static bool arm_use_tc(const cc_model_desc& d) {
+  static int want_tc = -1;
+  if (want_tc < 0) {
+    const char* e = getenv("CCRD_ARM_PATH");
+    want_tc = (e && strcmp(e, "tc") == 0) ? 1 : 0;
+  }
+  return want_tc && find_arm_tc_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1) != nullptr;
+}
+static ArmLaunchFn arm_launcher(const cc_model_desc& d) {
+  return arm_use_tc(d) ? find_arm_tc_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1)
+                       : find_arm_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1);
+}
+static int arm_partials_per_tile(const cc_model_desc& d) { return arm_use_tc(d) ? 16 : ARM_TY; }
+
 static int validate(const cc_model_desc* dp) {
   if (!dp) return fail(CC_EINVAL, "null descriptor");
   const cc_model_desc& d = *dp;
@@ -237,7 +271,7 @@ static void syn_geom(const cc_model_desc& d, const cc_strip* win, SynGeom& g) {
 static int n_arm_partials(const cc_model_desc& d, const cc_strip* win) {  // one per ARM warp
   ArmGeom g;
   arm_geom(d, win, g);
-  return g.tile_begin[d.L] * (ARM_THREADS / 32);
+  return g.tile_begin[d.L] * arm_partials_per_tile(d);
 }
 static int n_syn_ctas(const cc_model_desc& d, const cc_strip* win) {
   SynGeom g;
@@ -346,7 +380,7 @@ static int arm_one(const cc_model_desc& d, const cc_strip* win, const int16_t* l
   if (ag.tile_begin[d.L] == 0) return CC_OK;  // a strip owning no latent rows
   {
     ProfScope ps(PK_ARM, s);
-    find_arm_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1)(ag, d, arm_w, lat, part, nullptr, nullptr,
+    arm_launcher(d)(ag, d, arm_w, lat, part, nullptr, nullptr,
                                                                     nullptr, s);
   }
   g_launches++;
@@ -724,7 +758,7 @@ int cc_arm_rate(const cc_model_desc* desc, const int16_t* latents, const float* 
   ArmGeom ag;
   arm_geom(d, nullptr, ag);
   double* part = (double*)workspace;
-  find_arm_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1)(ag, d, arm_w, latents, part, mu, scale, bits, s);
+  arm_launcher(d)(ag, d, arm_w, latents, part, mu, scale, bits, s);
   g_launches++;
   if ((rc = cuda_check("arm_rate_kernel"))) return rc;
   // rate only: reduce with an empty synthesis partial set

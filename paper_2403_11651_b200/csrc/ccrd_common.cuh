@@ -232,7 +232,9 @@ typedef int (*SynLaunchFn)(const SynGeom& g, const cc_model_desc& d, const float
                            const float* image, float* x_hat, float* dense_out, float* h1_out,
                            double* partial, cudaStream_t s);
 
-ArmLaunchFn find_arm_launcher(int C, int NH, int NHL);
+ArmLaunchFn find_arm_launcher(int C, int NH, int NHL);     // FFMA2 path (arm_rate.cu)
+ArmLaunchFn find_arm_tc_launcher(int C, int NH, int NHL);  // tensor-core path (arm_tc.cu)
+int device_sm_count();  // current device's SMs (lazily cached; 148 without a device)
 SynLaunchFn find_syn_launcher(int L, int CH, int R, int K);
 
 }  // namespace ccrd

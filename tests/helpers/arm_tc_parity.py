@@ -1,0 +1,47 @@
+"""Subprocess helper of tests/test_arm_tc_gpu.py: with CCRD_ARM_PATH=tc (set
+by the caller before the library loads) checks the tensor-core ARM against the
+fp64 oracle -- per-latent bits / mu / scale and the full RD forward."""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import oracle  # noqa: E402
+import paper_2403_11651_b200 as P  # noqa: E402
+import workload  # noqa: E402
+
+assert os.environ.get("CCRD_ARM_PATH") == "tc"
+cases = [("ref", 70, 101, None), ("ref", 64, 200, None), ("ref", 71, 133, workload.TABLE1[1079]["arm"]),
+         ("ref", 53, 61, workload.TABLE1[2300]["arm"])]
+for name, H, W, arm in cases:
+    cfg = workload.CONFIGS[name].replace(H=H, W=W)
+    if arm is not None:
+        cfg = cfg.replace(n_ctx=arm[0], arm_widths=arm)
+    im = workload.make_image(cfg, 5)
+    d = P.desc_from_config(cfg)
+    lat = torch.from_numpy(im.latents).cuda()
+    n = im.latents.size
+    mu, sc, bits = (torch.zeros(n, device="cuda") for _ in range(3))
+    rate = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ws_b = P.cc_workspace_bytes(d, 1)
+    ws = torch.empty(ws_b, dtype=torch.uint8, device="cuda")
+    P.cc_arm_rate(d, lat.data_ptr(), im.arm_w, rate.data_ptr(), mu.data_ptr(), sc.data_ptr(), bits.data_ptr(),
+                  ws.data_ptr(), ws_b, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    R, mu_o, b_o, bits_o, _ = oracle.rate(oracle.model(cfg), im.latents, im.arm_w, per_latent=True)
+    np.testing.assert_allclose(mu.cpu().numpy(), mu_o, rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(sc.cpu().numpy(), b_o, rtol=1e-5, atol=0)
+    np.testing.assert_allclose(bits.cpu().numpy(), bits_o, rtol=0, atol=1e-3)
+    assert abs(rate.item() - R) <= 1e-5 * R, (rate.item(), R)
+    b = P.DeviceBatch(cfg, [im])
+    res = b.forward()
+    torch.cuda.synchronize()
+    ref = oracle.rd_forward_image(cfg, im)
+    got = res.cpu().numpy()[0]
+    assert abs(got[0] - ref["rate_bits"]) <= 1e-4 * ref["rate_bits"]
+    assert abs(got[3] - ref["cost"]) <= 1e-4 * ref["cost"]
+print("arm_tc parity ok")

@@ -1,0 +1,21 @@
+"""Parity of the opt-in tensor-core ARM kernel (arm_tc.cu: tcgen05 kind::tf32,
+3xTF32 split) against the fp64 oracle.  The path is chosen once
+per process from CCRD_ARM_PATH, so the checks run in a subprocess
+(tests/helpers/arm_tc_parity.py)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.timeout(600)
+def test_arm_tensor_core_path_matches_oracle():
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, CCRD_ARM_PATH="tc")
+    r = subprocess.run([sys.executable, os.path.join(here, "helpers", "arm_tc_parity.py")], env=env,
+                       capture_output=True, text=True, timeout=540)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "arm_tc parity ok" in r.stdout
