@@ -621,17 +621,26 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
 
   cudaStream_t s = (cudaStream_t)stream;
   // copy stream + per-slot events: copies of image i+1 overlap compute of image i
-  cudaStream_t cs;
-  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return cuda_check("stream create");
-  cudaEvent_t copied[2], consumed[2];
+  // three streams: uploads (cs), compute (s), readbacks (ds); PCIe is full
+  // duplex, so image i+1's upload, image i's compute and image i-1's x_hat
+  // readback overlap.  Two staging slots; events guard their reuse.
+  cudaStream_t cs, ds;
+  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking) != cudaSuccess)
+    return cuda_check("stream create");
+  cudaEvent_t copied[2], computed[2], read_back[2];
   for (int k = 0; k < 2; k++) {
     cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&consumed[k], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&computed[k], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&read_back[k], cudaEventDisableTiming);
   }
-  // start the copy stream after whatever is already queued on s
-  cudaEventRecord(consumed[0], s);
-  cudaStreamWaitEvent(cs, consumed[0], 0);
-  cudaEventRecord(consumed[1], s);
+  // start the side streams after whatever is already queued on s
+  cudaEventRecord(computed[0], s);
+  cudaStreamWaitEvent(cs, computed[0], 0);
+  cudaStreamWaitEvent(ds, computed[0], 0);
+  cudaEventRecord(computed[1], s);
+  cudaEventRecord(read_back[0], s);
+  cudaEventRecord(read_back[1], s);
   ReduceJob* jobs = new ReduceJob[n_img];
   for (int i = 0; i < n_img && rc == CC_OK; i++) {
     const int k = i & 1;
@@ -644,19 +653,24 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
       rc = fail(CC_EINVAL, "image %d: null latents or weights", i);
       break;
     }
-    cudaStreamWaitEvent(cs, consumed[k], 0);
+    cudaStreamWaitEvent(cs, computed[k], 0);  // slot k's inputs were consumed by image i-2
     cudaMemcpyAsync(dlat, x.latents, lat_b, cudaMemcpyHostToDevice, cs);
     if (x.image) cudaMemcpyAsync(dimg, x.image, img_b, cudaMemcpyHostToDevice, cs);
     cudaEventRecord(copied[k], cs);
     cudaStreamWaitEvent(s, copied[k], 0);
+    cudaStreamWaitEvent(s, read_back[k], 0);  // slot k's x_hat of image i-2 is read back
     double* part = (double*)(ws + per * (size_t)i);
     const int16_t* l1[1] = {dlat};
     const float *a1[1] = {x.arm_w}, *u1[1] = {x.up_w}, *s1[1] = {x.syn_w}, *i1[1] = {x.image ? dimg : nullptr};
     float* x1[1] = {x.x_hat ? dxh : nullptr};
     rc = forward_batch(d, nullptr, l1, a1, u1, s1, i1, x1, (char*)part, per, 1, s, false);
     if (rc) break;
-    if (x.x_hat) cudaMemcpyAsync(x.x_hat, dxh, img_b, cudaMemcpyDeviceToHost, s);
-    cudaEventRecord(consumed[k], s);
+    cudaEventRecord(computed[k], s);
+    if (x.x_hat) {
+      cudaStreamWaitEvent(ds, computed[k], 0);
+      cudaMemcpyAsync(x.x_hat, dxh, img_b, cudaMemcpyDeviceToHost, ds);
+    }
+    cudaEventRecord(read_back[k], ds);
     jobs[i] = make_job(d, nullptr, part);
   }
   if (rc == CC_OK) rc = launch_reduce(jobs, n_img, dres, s);
@@ -667,12 +681,15 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
     cudaStreamSynchronize(s);
   }
   cudaStreamSynchronize(cs);
+  if (cudaStreamSynchronize(ds) != cudaSuccess && rc == CC_OK) rc = cuda_check("cc_rd_forward_host readback");
   delete[] jobs;
   for (int k = 0; k < 2; k++) {
     cudaEventDestroy(copied[k]);
-    cudaEventDestroy(consumed[k]);
+    cudaEventDestroy(computed[k]);
+    cudaEventDestroy(read_back[k]);
   }
   cudaStreamDestroy(cs);
+  cudaStreamDestroy(ds);
   if (rc == CC_OK) rc = cuda_check("cc_rd_forward_host");
   return rc;
 }
