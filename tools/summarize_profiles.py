@@ -54,7 +54,8 @@ if os.path.exists(lp):
     open(os.path.join(PROF, f"ncu_launches_{R}.md"), "w").write("\n".join(launch_md) + "\n")
 
 # ---- full capture
-fp = os.path.join(OUT, f"full_{R}.ncu-rep")
+import glob
+fps = sorted(glob.glob(os.path.join(OUT, f"full_{R}*.ncu-rep")))
 want = {
     "gpu__time_duration.sum": "duration",
     "dram__bytes_read.sum": "dram_read",
@@ -69,9 +70,11 @@ want = {
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum": "smem_bank_conflicts",
 }
 kern = {}
-if os.path.exists(fp):
+for fp in fps:
     raw = subprocess.run(["ncu", "-i", fp, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
+    if len(rows) < 3:
+        continue
     hdr, units = rows[0], rows[1]
     for r in rows[2:]:
         name = short(r[hdr.index("Kernel Name")])
@@ -96,7 +99,8 @@ if os.path.exists(fp):
                 d[key] = val
         d["dram_bytes_per_launch"] = d.get("dram_read", 0) + d.get("dram_write", 0)
         kern.setdefault(name, d)
-    json.dump({"round": R, "source": f"ncu --set full --clock-control none capture full_{R}.ncu-rep "
+if kern:
+    json.dump({"round": R, "source": f"ncu --set full --clock-control none captures full_{R}_<kernel>.ncu-rep "
                                      "(one launch per kernel, 2K image of the bench workload)",
                "kernels": kern}, open(os.path.join(PROF, f"ncu_full_{R}.json"), "w"), indent=1)
 
