@@ -27,7 +27,7 @@ class OrcModel(C.Structure):
         ("n_ctx", C.c_int32), ("ctx_dy", C.c_int32 * 32), ("ctx_dx", C.c_int32 * 32),
         ("arm_n_layers", C.c_int32), ("arm_widths", C.c_int32 * (MAX_LAYERS + 1)),
         ("arm_residual", C.c_int32 * MAX_LAYERS),
-        ("up_taps", C.c_int32),
+        ("up_taps", C.c_int32), ("up_2d", C.c_int32),
         ("syn_n_1x1", C.c_int32), ("syn_widths", C.c_int32 * (MAX_LAYERS + 1)),
         ("syn_n_res", C.c_int32),
         ("logscale_min", C.c_double), ("logscale_max", C.c_double),
@@ -115,6 +115,7 @@ def model(cfg, H=None, W=None, arm_residual=None) -> OrcModel:
     for k, v in enumerate(res):
         m.arm_residual[k] = v
     m.up_taps = cfg.up_taps
+    m.up_2d = int(getattr(cfg, "up_2d", False))
     sw = cfg.syn_widths
     m.syn_n_1x1 = len(sw) - 1
     for k, v in enumerate(sw):

@@ -186,6 +186,37 @@ static void tconv_1d(const double* g, int n, int64_t gs, const float* k, int K,
   }
 }
 
+/* ---- step 7 (Table 1 exact architectures, NEXT-1): one stride-2 transposed
+ *      convolution with a non-separable K x K kernel (Table 1 "1-1-TConv-4" /
+ *      "TConv-8": 16 / 64 parameters), the 2-D form of
+ *      tconv_1d's definition on the input replicate-extended along both axes
+ *      (x_ext[i][i'] = g[clamp(i - E)][clamp(i' - E)]):
+ *          out[o][o'] = sum over (i, a, i', b) with 2 i + a - P == o and
+ *                       2 i' + b - P == o' of x_ext[i][i'] k2[a][b],
+ *      cropped to (mh x mw).  Scatter of each extended input sample. ------ */
+static void tconv_2d(const double* g, int n, int nw, const float* k2, int K, double* out, int mh, int mw,
+                     int64_t* macs) {
+  int E = K / 4, P = K / 2 - 1 + 2 * E;
+  for (int64_t t = 0; t < (int64_t)mh * mw; t++) out[t] = 0.0;
+  int64_t mc = 0;
+  for (int i = 0; i < n + 2 * E; i++)
+    for (int i2 = 0; i2 < nw + 2 * E; i2++) {
+      double xi = g[(int64_t)clampi(i - E, 0, n - 1) * nw + clampi(i2 - E, 0, nw - 1)];
+      for (int a = 0; a < K; a++) {
+        int o = 2 * i + a - P;
+        if (o < 0 || o >= mh) continue;
+        for (int b = 0; b < K; b++) {
+          int o2 = 2 * i2 + b - P;
+          if (o2 >= 0 && o2 < mw) {
+            out[(int64_t)o * mw + o2] += xi * (double)k2[a * K + b];
+            mc++;
+          }
+        }
+      }
+    }
+  *macs += mc;
+}
+
 /* ---- step 7: upsampling f_upsilon ("The linear upsampling
  *      ... upsample the latents to a dense representation").  Channel 0 is
  *      y_0; grid l >= 1 goes through l successive x2 steps with the shared
@@ -204,6 +235,15 @@ void orc_upsample(const orc_model* m, const int16_t* latents, const float* up_w,
     for (int64_t t = 0; t < (int64_t)h[l] * w[l]; t++) g[t] = (double)latents[off + t];
     int gh = h[l], gw = w[l];
     for (int j = l - 1; j >= 0; j--) {
+      if (m->up_2d) { /* Table 1 2-D TConv-K: (gh x gw) -> (h_j x w_j) in one step */
+        double* t2 = (double*)malloc(sizeof(double) * (size_t)h[j] * w[j]);
+        tconv_2d(g, gh, gw, up_w, m->up_taps, t2, h[j], w[j], &up_macs);
+        free(g);
+        g = t2;
+        gh = h[j];
+        gw = w[j];
+        continue;
+      }
       /* along x: (gh x gw) -> (gh x w_j) */
       double* t1 = (double*)malloc(sizeof(double) * (size_t)gh * w[j]);
       int64_t mx = 0;

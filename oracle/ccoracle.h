@@ -35,6 +35,9 @@ typedef struct {
   int32_t arm_widths[ORC_MAX_LAYERS + 1];/* [n_ctx, hidden..., 2]                       */
   int32_t arm_residual[ORC_MAX_LAYERS];  /* 1 = "LinR" layer (u += z)                   */
   int32_t up_taps;                       /* K: 4 or 8                                   */
+  int32_t up_2d;                         /* 0: separable k (x) k, up_w = k[K] (BASELINE)  */
+                                         /* 1: 2-D K x K kernel, up_w = k2[K][K] row-major */
+                                         /*    (Table 1 "TConv-K", 16 / 64 params; NEXT-1) */
   int32_t syn_n_1x1;                     /* number of 1x1 layers                        */
   int32_t syn_widths[ORC_MAX_LAYERS + 1];/* [L, C_h..., 3]                              */
   int32_t syn_n_res;                     /* residual 3x3 3->3 layers                    */
@@ -66,7 +69,8 @@ void orc_context(const orc_model* m, const int16_t* grid, int32_t h, int32_t w,
 double orc_rate(const orc_model* m, const int16_t* latents, const float* arm_w,
                 double* mu, double* b, double* bits, orc_macs* macs);
 
-/* Upsampling f_upsilon: dense [L][H][W] (reading #11-#14). */
+/* Upsampling f_upsilon: dense [L][H][W] (reading #11-#14;
+ * up_2d: Table 1's non-separable 2-D TConv-K). */
 void orc_upsample(const orc_model* m, const int16_t* latents, const float* up_w,
                   double* dense, orc_macs* macs);
 

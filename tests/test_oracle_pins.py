@@ -448,3 +448,76 @@ def test_table1_params_and_macs():
         tot = arm_m + up_m + syn_m
         assert abs(tot - row["mac_per_pixel"]) / row["mac_per_pixel"] < 0.01
         assert arm_m / tot <= g["arm_share_max"]["value"]
+
+
+# -------------------------------------------- Table 1 2-D TConv (NEXT-1)
+def _torch_upsample_chain_2d(lat_grid, k2, dims_chain, K):
+    """Reference: per x2 step, replicate pad E = K/4 then F.conv_transpose2d with
+    the (non-separable) K x K kernel, stride 2, padding K/2 - 1 + 2E, crop."""
+    x = torch.from_numpy(lat_grid.astype(np.float64))[None, None]
+    kk = torch.from_numpy(k2.astype(np.float64))[None, None]
+    E = K // 4
+    for (h, w) in dims_chain:
+        xp = F.pad(x, (E, E, E, E), mode="replicate")
+        y = F.conv_transpose2d(xp, kk, stride=2, padding=K // 2 - 1 + 2 * E)
+        x = y[:, :, :h, :w]
+    return x[0, 0].numpy()
+
+
+@pytest.mark.parametrize("K,H,W,L", [(8, 37, 53, 5), (4, 37, 53, 5), (8, 33, 17, 4), (4, 64, 64, 3)])
+def test_upsample_2d_vs_torch_conv_transpose(K, H, W, L):
+    """Table 1 TConv-K as a true 2-D kernel: random, asymmetric and
+    non-separable (rank K), so orientation and indexing on both axes are pinned."""
+    cfg = workload.CONFIGS["tiny"].replace(H=H, W=W, L=L, up_taps=K, up_2d=True, syn_widths=(L, 8, 3))
+    im = workload.make_image(cfg, 13)
+    k2 = np.random.default_rng(4).normal(0, 0.5, (K, K)).astype(np.float32)
+    assert np.linalg.matrix_rank(k2.astype(np.float64)) == K
+    dense, _ = oracle.upsample(oracle.model(cfg), im.latents, k2.ravel())
+    dims = cfg.level_dims()
+    np.testing.assert_array_equal(dense[0], im.level(cfg, 0))
+    for l in range(1, L):
+        ref = _torch_upsample_chain_2d(im.level(cfg, l), k2, dims[l - 1::-1], K)
+        np.testing.assert_allclose(dense[l], ref, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("K", [8, 4])
+def test_upsample_2d_separable_kernel_equals_separable_path(K):
+    """k2 = k (x) k through the 2-D scatter == the separable two-pass path (two
+    independent code paths of the oracle; fp64 rounding only)."""
+    base = workload.CONFIGS["tiny"].replace(H=41, W=58, L=5, up_taps=K, syn_widths=(5, 8, 3))
+    im = workload.make_image(base, 14)
+    # taps in multiples of 1/8: k (x) k is exact in fp32, so only the fp64
+    # summation order differs between the two paths
+    k = (np.random.default_rng(5).integers(-8, 9, K) / 8.0).astype(np.float32)
+    d1, m1 = oracle.upsample(oracle.model(base), im.latents, k)
+    k2 = np.outer(k, k).astype(np.float32)
+    d2, m2 = oracle.upsample(oracle.model(base.replace(up_2d=True)), im.latents, k2.ravel())
+    np.testing.assert_allclose(d2, d1, rtol=1e-12, atol=1e-9)
+
+
+def test_upsample_2d_normalised_preserves_constants():
+    cfg = workload.CONFIGS["t2300"].replace(H=45, W=71, L=6, syn_widths=(6, 40, 3))
+    im = workload.make_image(cfg, 15, filter_kind="normalised2d")
+    for ra in (0, 1):
+        for sb in (0, 1):
+            assert abs(im.up_w.reshape(8, 8)[ra::2, sb::2].sum() - 1.0) < 1e-6
+    lat = np.full(cfg.n_latents, -5, np.int16)
+    dense, _ = oracle.upsample(oracle.model(cfg), lat, im.up_w)
+    np.testing.assert_allclose(dense, -5.0, rtol=0, atol=1e-4)
+
+
+@pytest.mark.parametrize("name", ["t300", "t545", "t1079", "t2300"])
+def test_table1_configs_oracle_macs_match_table(name):
+    """The instrumented oracle on the Table 1 architectures (2-D TConv) counts
+    (K/2)^2 MAC per produced sample and lands within 1 % of the paper's printed
+    MAC/pixel (PAPER.md:307-310: 300 / 545 / 1079 / 2300)."""
+    cfg = workload.CONFIGS[name]
+    g = gold("table1.json")["rows"][name[1:]]
+    im = workload.make_image(cfg, 16)
+    r = oracle.rd_forward_image(cfg, im)
+    dims = cfg.level_dims()
+    K = cfg.up_taps
+    up = sum((K // 2) ** 2 * dims[j][0] * dims[j][1] for l in range(1, cfg.L) for j in range(l))
+    assert r["macs"]["up"] == up
+    tot = sum(r["macs"].values()) / (cfg.H * cfg.W)
+    assert abs(tot - g["mac_per_pixel"]) / g["mac_per_pixel"] < 0.01

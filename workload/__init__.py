@@ -62,6 +62,7 @@ class Config:
     syn_widths: tuple          # (L, C_h..., 3)             Table 1 synthesis 1x1 layers
     syn_n_res: int             # residual 3x3 3->3 layers   Table 1 "3-3-ConvR-3"
     up_taps: int = 8           # shared separable k (x) k   BASELINE.json configs[0]
+    up_2d: bool = False        # Table 1 non-separable K x K TConv (NEXT-1): up_w has K*K taps
     lat_scale: float = 1.0
     lat_clip: int = 16
     lam: float = 1e-3
@@ -97,6 +98,10 @@ class Config:
         return sum(w[k] * w[k + 1] + w[k + 1] for k in range(len(w) - 1))
 
     @property
+    def n_up_w(self):
+        return self.up_taps * self.up_taps if self.up_2d else self.up_taps
+
+    @property
     def n_syn_w(self):
         w = self.syn_widths
         return (sum(w[k] * w[k + 1] + w[k + 1] for k in range(len(w) - 1))
@@ -122,14 +127,20 @@ CONFIGS = {
     "8k": Config("8k", 4320, 7680, 7, 16, (16, 24, 24, 2), (7, 40, 3), 2),
 }
 
-# Table 1 exact architectures: NEXT-1 (2-D TConv).  Kept as
-# data for the parameter-count pin (281/525/941/1925) and the MAC closed form.
+# Table 1 exact architectures (NEXT-1): ARM with C = width
+# of its first layer, 2-D non-separable TConv-K upsampling, synthesis widths.
 TABLE1 = {
     300: dict(arm=(8, 8, 2), up_kernel=4, syn=(7, 8, 3), syn_n_res=1),
     545: dict(arm=(8, 8, 8, 2), up_kernel=4, syn=(7, 16, 3), syn_n_res=2),
     1079: dict(arm=(16, 16, 16, 2), up_kernel=4, syn=(7, 16, 3), syn_n_res=2),
     2300: dict(arm=(24, 24, 24, 2), up_kernel=8, syn=(7, 40, 3), syn_n_res=2),
 }
+
+# ... as workload configs on Kodak-sized synthetic images (512 x 768, L = 7;
+# PAPER.md:347 "768 x 512"), the value distributions of configs[1]/[2].
+for _k, _a in TABLE1.items():
+    CONFIGS[f"t{_k}"] = Config(f"t{_k}", 512, 768, 7, _a["arm"][0], _a["arm"], _a["syn"], _a["syn_n_res"],
+                               up_taps=_a["up_kernel"], up_2d=True)
 
 
 @dataclasses.dataclass
@@ -192,7 +203,7 @@ def gen_latents(rng: np.random.Generator, cfg: Config) -> np.ndarray:
 def gen_weights(rng: np.random.Generator, cfg: Config, filter_kind: str = "random"):
     """fp32 blobs drawn N(0, 0.1) in blob order: ARM, upsampling taps, synthesis."""
     arm_w = rng.normal(0.0, 0.1, cfg.n_arm_w).astype(np.float32)
-    up_w = rng.normal(0.0, 0.1, cfg.up_taps).astype(np.float32)
+    up_w = rng.normal(0.0, 0.1, cfg.n_up_w).astype(np.float32)
     syn_w = rng.normal(0.0, 0.1, cfg.n_syn_w).astype(np.float32)
     if filter_kind == "lanczos2":
         if cfg.up_taps != 8:
@@ -201,8 +212,23 @@ def gen_weights(rng: np.random.Generator, cfg: Config, filter_kind: str = "rando
     elif filter_kind == "bilinear":
         up_w = (np.array([0, 0, .25, .75, .75, .25, 0, 0], np.float32) if cfg.up_taps == 8
                 else np.array([.25, .75, .75, .25], np.float32))
+    elif filter_kind == "normalised2d":
+        # a NON-separable K x K kernel whose four polyphase components
+        # (rows a = 2t+1-r, columns b = 2u+1-s) each sum to 1, so every level
+        # carries O(1) signal: bilinear (x) bilinear plus seeded noise,
+        # renormalised per phase
+        k1 = (np.array([0, 0, .25, .75, .75, .25, 0, 0]) if cfg.up_taps == 8 else np.array([.25, .75, .75, .25]))
+        k2 = np.outer(k1, k1) + rng.normal(0.0, 0.05, (cfg.up_taps, cfg.up_taps))
+        for ra in (0, 1):
+            for sb in (0, 1):
+                k2[ra::2, sb::2] /= k2[ra::2, sb::2].sum()
+        up_w = k2.astype(np.float32).ravel()
     elif filter_kind != "random":
         raise ValueError(filter_kind)
+    if cfg.up_2d and filter_kind in ("lanczos2", "bilinear"):
+        up_w = np.outer(up_w, up_w).astype(np.float32).ravel()  # separable special case k (x) k
+    if filter_kind == "normalised2d" and not cfg.up_2d:
+        raise ValueError("normalised2d needs up_2d")
     return arm_w, up_w, syn_w
 
 
