@@ -67,8 +67,10 @@ extern "C" {
  *   {8, 16, 24, 32}.
  * Context: n_ctx strictly causal offsets (dy < 0, or dy == 0 and dx < 0) with
  *   -3 <= dy <= 0 and |dx| <= 4; neighbours outside the grid read 0.
- * Upsampling f_upsilon (Table 1 "1-1-TConv-K"): shared
- *   separable k (x) k, K = up_taps in {4, 8}; no bias.
+ * Upsampling f_upsilon (Table 1 "1-1-TConv-K"): one shared
+ *   stride-2 transposed conv, K = up_taps in {4, 8}, no bias: separable
+ *   k (x) k (up_2d = 0, BASELINE.json) or a non-separable K x K kernel
+ *   (up_2d = 1, Table 1's exact architectures; not available for strips).
  * Synthesis f_theta (Table 1 synthesis column): syn_widths = [L, C_h, 3]
  *   (syn_n_1x1 = 2) then syn_n_res residual 3x3 3->3 layers.
  *   Compiled: L in 1..8 with C_h in {8, 16, 24, 32, 40, 48}; syn_n_res in 0..3.
@@ -82,6 +84,9 @@ typedef struct {
   int32_t arm_widths[CC_MAX_LAYERS + 1];
   uint32_t arm_residual_mask;
   int32_t up_taps;                     /* K                                            */
+  int32_t up_2d;                       /* 0: separable k (x) k, up_w = k[K] (BASELINE)   */
+                                       /* 1: 2-D K x K kernel, up_w = k2[K][K] row-major */
+                                       /*    (Table 1 "TConv-K", 16 / 64 params)          */
   int32_t syn_n_1x1;                   /* number of 1x1 layers (2 supported)           */
   int32_t syn_widths[CC_MAX_LAYERS + 1];
   int32_t syn_n_res;                   /* residual 3x3 layers                          */
@@ -101,7 +106,9 @@ typedef struct {
 
 /* One image.  Blob layouts (fp32, row-major):
  *   arm_w: per layer k: W_k[out][in], then b_k[out].
- *   up_w : k[K].
+ *   up_w : k[K] (separable), or k2[a][b] row-major (up_2d; a = vertical tap,
+ *          b = horizontal): out[2q+r][2p+s] = sum_{t,u} k2[2t+1-r][2u+1-s]
+ *          g[q+r+K/4-1-t][p+s+K/4-1-u] on the replicate-extended grid.
  *   syn_w: per 1x1 layer: A_m[out][in], a_m[out]; then per residual 3x3 layer
  *          G_r[co][ci][ky][kx] (cross-correlation, replicate padding), g_r[3]. */
 typedef struct {

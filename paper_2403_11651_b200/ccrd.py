@@ -31,7 +31,7 @@ class CcModelDesc(C.Structure):
         ("ctx_dy", C.c_int8 * CC_MAX_CTX), ("ctx_dx", C.c_int8 * CC_MAX_CTX),
         ("arm_n_layers", C.c_int32), ("arm_widths", C.c_int32 * (CC_MAX_LAYERS + 1)),
         ("arm_residual_mask", C.c_uint32),
-        ("up_taps", C.c_int32),
+        ("up_taps", C.c_int32), ("up_2d", C.c_int32),
         ("syn_n_1x1", C.c_int32), ("syn_widths", C.c_int32 * (CC_MAX_LAYERS + 1)),
         ("syn_n_res", C.c_int32),
         ("logscale_min", C.c_float), ("logscale_max", C.c_float),
@@ -152,7 +152,7 @@ def _check(rc: int, where: str):
 
 # ------------------------------------------------------------------ descriptor
 def make_desc(H, W, L, ctx, arm_widths, arm_residual, up_taps, syn_widths, syn_n_res,
-              logscale_min, logscale_max, p_floor, lam) -> CcModelDesc:
+              logscale_min, logscale_max, p_floor, lam, up_2d=False) -> CcModelDesc:
     d = CcModelDesc()
     d.H, d.W, d.L = H, W, L
     d.n_ctx = len(ctx)
@@ -164,6 +164,7 @@ def make_desc(H, W, L, ctx, arm_widths, arm_residual, up_taps, syn_widths, syn_n
         d.arm_widths[k] = v
     d.arm_residual_mask = sum(1 << k for k, r in enumerate(arm_residual) if r)
     d.up_taps = up_taps
+    d.up_2d = int(bool(up_2d))
     d.syn_n_1x1 = len(syn_widths) - 1
     for k, v in enumerate(syn_widths):
         d.syn_widths[k] = v
@@ -177,7 +178,8 @@ def desc_from_config(cfg, H: Optional[int] = None, W: Optional[int] = None) -> C
     """Descriptor from a workload.Config (the shared, arithmetic-free config)."""
     return make_desc(cfg.H if H is None else H, cfg.W if W is None else W, cfg.L, cfg.ctx,
                      cfg.arm_widths, cfg.arm_residual, cfg.up_taps, cfg.syn_widths, cfg.syn_n_res,
-                     cfg.logscale_min, cfg.logscale_max, cfg.p_floor, cfg.lam)
+                     cfg.logscale_min, cfg.logscale_max, cfg.p_floor, cfg.lam,
+                     up_2d=getattr(cfg, "up_2d", False))
 
 
 # ------------------------------------------------------------------ raw calls

@@ -214,6 +214,7 @@ static int validate(const cc_model_desc* dp) {
   for (int k = 2; k < d.arm_n_layers; k++)
     if (d.arm_widths[k] != d.arm_widths[1]) return fail(CC_ENOTSUP, "ARM hidden layers must share one width");
   if (d.up_taps != 4 && d.up_taps != 8) return fail(CC_ENOTSUP, "up_taps must be 4 or 8");
+  if (d.up_2d != 0 && d.up_2d != 1) return fail(CC_EINVAL, "up_2d must be 0 or 1");
   if (d.syn_n_1x1 != 2) return fail(CC_ENOTSUP, "synthesis must have exactly two 1x1 layers");
   if (d.syn_widths[0] != d.L) return fail(CC_EINVAL, "syn_widths[0] (%d) != L (%d)", d.syn_widths[0], d.L);
   if (d.syn_widths[2] != 3) return fail(CC_EINVAL, "synthesis must output 3 channels");
@@ -300,10 +301,19 @@ static size_t partial_bytes(const cc_model_desc& d, const cc_strip* win) {
   return align256(sizeof(double) * (size_t)(n_arm_partials(d, win) + n_syn_ctas(d, win))) +
          align256(sizeof(cc_rd_result));
 }
+// 2-D TConv (up_2d): the dense [L][H][W] level-0 tensor after the pyramid
+static size_t dense_bytes(const cc_model_desc& d) {
+  return d.up_2d ? align256(sizeof(float) * (size_t)d.L * d.H * d.W) : 0;
+}
 static size_t slice_bytes(const cc_model_desc& d, const cc_strip* win) {
   PyrGeom pg;
   pyr_geom(d, win, pg);
-  return partial_bytes(d, win) + align256(sizeof(float) * (size_t)pg.s_floats);
+  return partial_bytes(d, win) + align256(sizeof(float) * (size_t)pg.s_floats) + dense_bytes(d);
+}
+static float* slice_dense(const cc_model_desc& d, const cc_strip* win, void* slice) {
+  PyrGeom pg;
+  pyr_geom(d, win, pg);
+  return (float*)((char*)slice + partial_bytes(d, win) + align256(sizeof(float) * (size_t)pg.s_floats));
 }
 static float* slice_pyr(const cc_model_desc& d, const cc_strip* win, void* slice) {
   return (float*)((char*)slice + partial_bytes(d, win));
@@ -456,6 +466,37 @@ static int forward_batch(const cc_model_desc& d, const cc_strip* win, const int1
   pyr_geom(d, win, pg);
   const int n_arm = n_arm_partials(d, win);
   int rc;
+  if (d.up_2d) {  // Table 1 2-D TConv: full pyramid -> dense, then synthesis from it
+    static thread_local Pyr2dImage im2[MAX_JOBS_PER_LAUNCH];
+    for (int i = 0; i < n; i++) {
+      im2[i].lat = lat[i];
+      im2[i].S = slice_pyr(d, win, slices + per * (size_t)i);
+      im2[i].dense = slice_dense(d, win, slices + per * (size_t)i);
+      for (int t = 0; t < 64; t++) im2[i].k2[t] = t < d.up_taps * d.up_taps ? up_w[i][t] : 0.0f;
+    }
+    {
+      ProfScope ps(PK_PYR, s);
+      launch_pyramid2d(pg, d.up_taps, im2, n, s);
+    }
+    g_launches += pyramid2d_launch_count(pg, n);
+    if ((rc = cuda_check("pyramid2d_kernel"))) return rc;
+    for (int i = 0; i < n; i++)
+      if ((rc = arm_one(d, win, lat[i], arm_w[i], (double*)(slices + per * (size_t)i), s))) return rc;
+    for (int i = 0; i < n; i++) {
+      char* sl = slices + per * (size_t)i;
+      SynGeom sg;
+      syn_geom(d, win, sg);
+      {
+        ProfScope ps(PK_SYN, s);
+        find_syn_launcher(d.L, d.syn_widths[1], d.syn_n_res, d.up_taps)(
+            sg, d, nullptr, syn_w[i], lat[i], nullptr, slice_dense(d, win, sl), image[i], x_hat[i], nullptr, nullptr,
+            (double*)sl + n_arm, s);
+      }
+      g_launches++;
+      if ((rc = cuda_check("synth_kernel(dense_in)"))) return rc;
+    }
+    return CC_OK;
+  }
   PyrImage imgs[MAX_JOBS_PER_LAUNCH];
   for (int i = 0; i < n; i++)
     imgs[i] = pyr_image(d, lat[i], up_w[i], slice_pyr(d, win, slices + per * (size_t)i));
@@ -697,6 +738,7 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
 // ---------------------------------------------------------------- strips
 static int validate_strip(const cc_model_desc& d, const cc_strip* st) {
   if (!st) return fail(CC_EINVAL, "null strip");
+  if (d.up_2d) return fail(CC_ENOTSUP, "strips are implemented for the separable upsampling only");
   if (st->r0 < 0 || st->r1 > d.H || st->r0 >= st->r1 || (st->r0 & 1))
     return fail(CC_EINVAL, "strip rows [%d, %d) must satisfy 0 <= r0 < r1 <= H (%d) with r0 even", st->r0, st->r1,
                 d.H);
@@ -798,6 +840,19 @@ int cc_upsample(const cc_model_desc* desc, const int16_t* latents, const float* 
   if (!workspace || workspace_bytes < per) return fail(CC_EWORKSPACE, "need %zu workspace bytes", per);
   if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
   cudaStream_t s = (cudaStream_t)stream;
+  if (d.up_2d) {  // the production 2-D path: pyramid2d writes channels 1..L-1
+    PyrGeom pg;
+    pyr_geom(d, nullptr, pg);
+    Pyr2dImage im2;
+    im2.lat = latents;
+    im2.S = slice_pyr(d, nullptr, workspace);
+    im2.dense = dense;
+    for (int t = 0; t < 64; t++) im2.k2[t] = t < d.up_taps * d.up_taps ? up_w[t] : 0.0f;
+    launch_pyramid2d(pg, d.up_taps, &im2, 1, s);
+    launch_lat0_to_dense(latents, dense, (int64_t)d.H * d.W, s);
+    g_launches += pyramid2d_launch_count(pg, 1) + 1;
+    return cuda_check("cc_upsample(2d)");
+  }
   // the production path (pyramid + fused last step) with its dense output on;
   // synthesis weights are irrelevant here: zero blob of the right size
   PyrGeom pg;
@@ -859,7 +914,8 @@ double cc_mac_per_pixel(const cc_model_desc* desc, cc_mac_breakdown* out) {
   int64_t up = 0;
   for (int l = 1; l < d.L; l++)
     for (int j = 0; j < l; j++)
-      up += (int64_t)(d.up_taps / 2) * ((int64_t)g.h[j + 1] * g.w[j] + (int64_t)g.h[j] * g.w[j]);
+      up += d.up_2d ? (int64_t)(d.up_taps / 2) * (d.up_taps / 2) * g.h[j] * g.w[j]  // (K/2)^2 per output
+                    : (int64_t)(d.up_taps / 2) * ((int64_t)g.h[j + 1] * g.w[j] + (int64_t)g.h[j] * g.w[j]);
   int64_t syn_pp = 81 * (int64_t)d.syn_n_res;
   for (int k = 0; k < d.syn_n_1x1; k++) syn_pp += (int64_t)d.syn_widths[k] * d.syn_widths[k + 1];
   const int64_t P = (int64_t)d.H * d.W;

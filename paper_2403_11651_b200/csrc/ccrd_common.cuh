@@ -214,6 +214,19 @@ struct PyrParams {
 int launch_pyramid(const PyrGeom& g, int K, const PyrImage* imgs, int n_img, cudaStream_t s);
 int pyramid_launch_count(const PyrGeom& g, int n_img);
 
+// Table 1 2-D TConv-K (up_2d): the pyramid runs every level down to level 0,
+// whose L-1 upsampled grids go to a dense [L][H][W] buffer (channels 1..L-1)
+// that the synthesis kernel reads in its dense-input mode.
+struct Pyr2dImage {
+  const int16_t* lat;  // packed latents
+  float* S;            // S_j for j >= 1 (workspace, PyrGeom offsets)
+  float* dense;        // [L][H][W]: S_0 = channels 1 .. L-1
+  float k2[64];        // K x K taps, row-major (a = vertical, b = horizontal)
+};
+int launch_pyramid2d(const PyrGeom& g, int K, const Pyr2dImage* imgs, int n_img, cudaStream_t s);
+int pyramid2d_launch_count(const PyrGeom& g, int n_img);
+int launch_lat0_to_dense(const int16_t* lat, float* dense, int64_t n, cudaStream_t s);
+
 // Reduction of per-CTA partials into per-image results (deterministic, fp64).
 struct ReduceJob {
   const double* arm_partial;

@@ -11,6 +11,8 @@
 // The last step (S_1 and y_1 -> level 0) is fused into synth_kernel, so the
 // full-resolution dense tensor never exists in memory.  The FMA order per
 // output matches synth_kernel's ChainStep exactly.
+#include <cstring>
+
 #include "ccrd_common.cuh"
 
 namespace ccrd {
@@ -122,6 +124,132 @@ int pyramid_launch_count(const PyrGeom& g, int n_img) {
   int lv = 0;
   for (int j = g.L - 2; j >= 1; j--) lv += (g.lv.hi[j] > g.lv.lo[j]) ? 1 : 0;
   return lv * ((n_img + PYR_MAX_IMG - 1) / PYR_MAX_IMG);
+}
+
+// ------------------------------------------------------------------ 2-D TConv
+// Table 1 "1-1-TConv-K" as a non-separable K x K kernel (
+// NEXT-1): out[2q+r][2p+s] = sum_{t,u} k2[2t+1-r][2u+1-s] g[q+r+K/4-1-t][p+s+K/4-1-u]
+// on the replicate-extended input (clamped source rows / columns), cropped.
+// One launch per level j = L-2 .. 0 for all images; a thread produces a 2x2
+// output block from the (K/2+1)^2 shared sources around (q, p).
+constexpr int PYR2D_MAX_IMG = 32;  // images per launch (k2 in the parameter bank)
+
+template <int K>
+struct Pyr2dParams {
+  LevelGeom lv;
+  int32_t L, j, tiles_x;
+  int64_t s_off[CC_MAX_LEVELS];
+  int64_t plane0;  // H * W (level-0 channel stride of the dense buffer)
+  Pyr2dImage img[PYR2D_MAX_IMG];
+};
+
+template <int K>
+__global__ void __launch_bounds__(PYR_THREADS)
+    pyramid2d_kernel(const __grid_constant__ Pyr2dParams<K> p) {
+  constexpr int SR = PYR_TH / 2 + K / 2;  // source rows of a tile
+  constexpr int SC = PYR_TW / 2 + K / 2;  // source cols
+  constexpr int H2 = K / 2;
+  extern __shared__ float psm[];
+  const Pyr2dImage& im = p.img[blockIdx.y];
+  const int j = p.j;
+  const int nch = p.L - 1 - j;
+  float* sw = psm;  // [nch][SR][SC]
+  const int hj = p.lv.h[j], wj = p.lv.w[j];
+  const int hs = p.lv.h[j + 1], ws = p.lv.w[j + 1];
+  const int ty = blockIdx.x / p.tiles_x;
+  const int Y0 = ty * PYR_TH, X0 = (blockIdx.x - ty * p.tiles_x) * PYR_TW;
+  const int r0 = (Y0 >> 1) - K / 4, c0 = (X0 >> 1) - K / 4;  // source window origin
+  const float* Sn = im.S + p.s_off[j + 1];                    // S_{j+1}, nch - 1 channels
+  const int16_t* lat = im.lat + p.lv.off[j + 1];
+  float* Sj = (j == 0) ? im.dense + p.plane0 : im.S + p.s_off[j];
+  const int64_t plane_j = (int64_t)hj * wj;
+
+#pragma unroll 4
+  for (int it = threadIdx.x; it < nch * SR * SC; it += PYR_THREADS) {
+    const int k = it / (SR * SC), rem = it - k * (SR * SC);
+    const int rr = rem / SC, cc = rem - rr * SC;
+    const int64_t gi = (int64_t)clampi(r0 + rr, 0, hs - 1) * ws + clampi(c0 + cc, 0, ws - 1);
+    sw[it] = (k == 0) ? (float)__ldg(lat + gi) : __ldg(Sn + (int64_t)(k - 1) * hs * ws + gi);
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int it = threadIdx.x; it < nch * (PYR_TH / 2) * (PYR_TW / 2); it += PYR_THREADS) {
+    const int k = it / ((PYR_TH / 2) * (PYR_TW / 2)), rem = it - k * ((PYR_TH / 2) * (PYR_TW / 2));
+    const int qq = rem / (PYR_TW / 2), pp = rem - qq * (PYR_TW / 2);
+    // sources rho, sigma = 0 .. K/2 <-> rows q - K/4 + rho, columns p - K/4 + sigma
+    const float* src = sw + (k * SR + qq) * SC + pp;
+    float g[H2 + 1][H2 + 1];
+#pragma unroll
+    for (int a = 0; a <= H2; a++)
+#pragma unroll
+      for (int b = 0; b <= H2; b++) g[a][b] = src[a * SC + b];
+    float o[2][2];
+#pragma unroll
+    for (int r = 0; r < 2; r++)
+#pragma unroll
+      for (int s = 0; s < 2; s++) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int t = 0; t < H2; t++)
+#pragma unroll
+          for (int u = 0; u < H2; u++)
+            acc = fmaf(im.k2[(2 * t + 1 - r) * K + (2 * u + 1 - s)], g[r + H2 - 1 - t][s + H2 - 1 - u], acc);
+        o[r][s] = acc;
+      }
+    const int y = Y0 + 2 * qq, x = X0 + 2 * pp;
+    float* dst = Sj + (int64_t)k * plane_j;
+#pragma unroll
+    for (int r = 0; r < 2; r++)
+#pragma unroll
+      for (int s = 0; s < 2; s++)
+        if (y + r < hj && x + s < wj) dst[(int64_t)(y + r) * wj + x + s] = o[r][s];
+  }
+}
+
+template <int K>
+static int launch_pyr2d(const PyrGeom& g, const Pyr2dImage* imgs, int n_img, cudaStream_t s) {
+  Pyr2dParams<K> p;  // ~9 KB, copied into the launch's parameter bank
+  memset(&p, 0, sizeof(p));
+  p.lv = g.lv;
+  p.L = g.L;
+  p.plane0 = (int64_t)g.lv.h[0] * g.lv.w[0];
+  for (int l = 0; l < CC_MAX_LEVELS; l++) p.s_off[l] = g.s_off[l];
+  for (int j = g.L - 2; j >= 0; j--) {
+    p.j = j;
+    p.tiles_x = (g.lv.w[j] + PYR_TW - 1) / PYR_TW;
+    const int tiles = p.tiles_x * ((g.lv.h[j] + PYR_TH - 1) / PYR_TH);
+    constexpr int SR = PYR_TH / 2 + K / 2, SC = PYR_TW / 2 + K / 2;
+    const size_t smem = sizeof(float) * (size_t)(g.L - 1 - j) * SR * SC;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(pyramid2d_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    for (int b = 0; b < n_img; b += PYR2D_MAX_IMG) {
+      const int m = (n_img - b < PYR2D_MAX_IMG) ? n_img - b : PYR2D_MAX_IMG;
+      for (int i = 0; i < m; i++) p.img[i] = imgs[b + i];
+      pyramid2d_kernel<K><<<dim3(tiles, m), PYR_THREADS, smem, s>>>(p);
+    }
+  }
+  return 0;
+}
+
+int launch_pyramid2d(const PyrGeom& g, int K, const Pyr2dImage* imgs, int n_img, cudaStream_t s) {
+  if (g.L < 2) return 0;
+  return K == 4 ? launch_pyr2d<4>(g, imgs, n_img, s) : launch_pyr2d<8>(g, imgs, n_img, s);
+}
+
+int pyramid2d_launch_count(const PyrGeom& g, int n_img) {
+  if (g.L < 2) return 0;
+  return (g.L - 1) * ((n_img + PYR2D_MAX_IMG - 1) / PYR2D_MAX_IMG);
+}
+
+__global__ void lat0_to_dense_kernel(const int16_t* __restrict__ lat, float* __restrict__ dense, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dense[i] = (float)lat[i];
+}
+
+int launch_lat0_to_dense(const int16_t* lat, float* dense, int64_t n, cudaStream_t s) {
+  const int blocks = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+  lat0_to_dense_kernel<<<blocks, 256, 0, s>>>(lat, dense, n);
+  return 0;
 }
 
 }  // namespace ccrd

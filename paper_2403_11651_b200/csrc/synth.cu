@@ -291,10 +291,17 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
       const bool has1 = (y0 + 1 < H);
       uint64_t v[L];  // (row y0, row y0 + 1) of every dense channel
       if constexpr (DENSE_IN) {
+        // channel 0 straight from the int16 latents when given (the 2-D TConv
+        // path: the pyramid fills channels 1 .. L-1), else from the dense tensor
 #pragma unroll
-        for (int l = 0; l < L; l++)
-          v[l] = f2pack(__ldg(p.dense_in + l * P + (int64_t)y0 * W + x),
-                        has1 ? __ldg(p.dense_in + l * P + (int64_t)(y0 + 1) * W + x) : 0.0f);
+        for (int l = 0; l < L; l++) {
+          if (l == 0 && p.lat != nullptr)
+            v[0] = f2pack((float)__ldg(p.lat + (int64_t)y0 * W + x),
+                          has1 ? (float)__ldg(p.lat + (int64_t)(y0 + 1) * W + x) : 0.0f);
+          else
+            v[l] = f2pack(__ldg(p.dense_in + l * P + (int64_t)y0 * W + x),
+                          has1 ? __ldg(p.dense_in + l * P + (int64_t)(y0 + 1) * W + x) : 0.0f);
+        }
       } else {
         v[0] = f2pack((float)lat0[2 * rp * RW0 + cc], (float)lat0[(2 * rp + 1) * RW0 + cc]);
         if constexpr (L > 1) {
