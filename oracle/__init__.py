@@ -16,6 +16,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "ccoracle.c")
+_SRC_TRAIN = os.path.join(_HERE, "cctrain.c")  # NEXT-2: one training iteration
 _LIB = os.path.join(_HERE, "libccoracle.so")
 
 MAX_LAYERS = 8
@@ -35,6 +36,11 @@ class OrcModel(C.Structure):
     ]
 
 
+class OrcAdam(C.Structure):
+    _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("t", C.c_int32)]
+
+
 class OrcMacs(C.Structure):
     _fields_ = [("arm", C.c_int64), ("up", C.c_int64), ("syn", C.c_int64)]
 
@@ -42,10 +48,10 @@ class OrcMacs(C.Structure):
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc (plain C99 + OpenMP)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
-            os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "ccoracle.h"))):
+            os.path.getmtime(_SRC), os.path.getmtime(_SRC_TRAIN), os.path.getmtime(os.path.join(_HERE, "ccoracle.h"))):
         tmp = _LIB + f".{os.getpid()}.tmp"
         subprocess.check_call(["gcc", "-O2", "-std=c99", "-fopenmp", "-fPIC", "-shared",
-                               "-o", tmp, _SRC, "-lm"])
+                               "-o", tmp, _SRC, _SRC_TRAIN, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -83,6 +89,12 @@ def lib():
         L.orc_synthesis.argtypes = [P(OrcModel), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, P(OrcMacs)]
         L.orc_rd_forward.restype = C.c_int
         L.orc_rd_forward.argtypes = [P(OrcModel)] + [C.c_void_p] * 8 + [P(OrcMacs)]
+        L.orc_train_param_count.restype = C.c_int64
+        L.orc_train_param_count.argtypes = [P(OrcModel)]
+        L.orc_train_grad.restype = C.c_int
+        L.orc_train_grad.argtypes = [P(OrcModel)] + [C.c_void_p] * 5
+        L.orc_adam_step.restype = None
+        L.orc_adam_step.argtypes = [C.c_int64] + [C.c_void_p] * 4 + [P(OrcAdam)]
         L.orc_set_threads.argtypes = [C.c_int]
         L.orc_get_threads.restype = C.c_int
         _lib = L
@@ -242,3 +254,35 @@ def time_rd_forward(cfg, im, threads: int):
     t0 = time.perf_counter()
     r = rd_forward_image(cfg, im)
     return time.perf_counter() - t0, r
+
+
+# ------------------------------------------------------------ training (NEXT-2)
+def train_param_count(m: OrcModel) -> int:
+    return lib().orc_train_param_count(C.byref(m))
+
+
+def pack_params(latents_float, arm_w, up_w, syn_w) -> np.ndarray:
+    """[y | arm_w | up_w | syn_w] fp32 (the documented parameter layout)."""
+    return np.concatenate([np.asarray(latents_float, np.float32).ravel(), np.asarray(arm_w, np.float32).ravel(),
+                           np.asarray(up_w, np.float32).ravel(), np.asarray(syn_w, np.float32).ravel()])
+
+
+def train_grad(m: OrcModel, params, noise, image):
+    """(out[4] = rate_bits, sse, mse, cost), gradient (fp64, parameter layout)."""
+    par = _c(params, np.float32)
+    nz = _c(noise, np.float32)
+    img = _c(image, np.float32)
+    out = np.zeros(4)
+    grad = np.zeros(train_param_count(m))
+    rc = lib().orc_train_grad(C.byref(m), _p(par), _p(nz), _p(img), _p(out), _p(grad))
+    if rc != 0:
+        raise ValueError(f"orc_train_grad rc={rc}")
+    return out, grad
+
+
+def adam_step(params: np.ndarray, grad, mom1: np.ndarray, mom2: np.ndarray, lr, beta1, beta2, eps, t):
+    """In place on params (fp32), mom1 / mom2 (fp64)."""
+    assert params.dtype == np.float32 and mom1.dtype == np.float64 and mom2.dtype == np.float64
+    g = _c(grad, np.float64)
+    lib().orc_adam_step(params.size, _p(params), _p(g), _p(mom1), _p(mom2),
+                        C.byref(OrcAdam(lr, beta1, beta2, eps, t)))

@@ -232,6 +232,18 @@ def gen_weights(rng: np.random.Generator, cfg: Config, filter_kind: str = "rando
     return arm_w, up_w, syn_w
 
 
+def gen_noise(rng: np.random.Generator, n: int) -> np.ndarray:
+    """Training-proxy noise u ~ U(-1/2, 1/2) (reading T1),
+    fp32: the random numbers of the training iteration are INPUT data."""
+    return rng.uniform(-0.5, 0.5, n).astype(np.float32)
+
+
+def gen_continuous_latents(rng: np.random.Generator, latents_int: np.ndarray) -> np.ndarray:
+    """A training state's continuous latents y: the integer draw plus a seeded
+    offset in (-1/2, 1/2) (fp32)."""
+    return (latents_int.astype(np.float64) + rng.uniform(-0.49, 0.49, latents_int.size)).astype(np.float32)
+
+
 def make_image(cfg: Config, seed: int, filter_kind: str = "random") -> Image:
     r_img, r_lat, r_w = _streams(seed)
     img = gen_image(r_img, cfg.H, cfg.W)
