@@ -344,6 +344,78 @@ def run_strip(args, rk):
         print(json.dumps(out), flush=True)
 
 
+def run_train(args, rk):
+    """NEXT-2: the encoder training iteration (forward on the noise proxy,
+    backward, Adam) of ONE image per GPU (BASELINE.json configs[2] by default:
+    the 512x768 ~2000 MAC/px model, the size the paper's encoding times are
+    for).  value = training iterations/s x pixels (forward+backward pixels/s,
+    whole job); also iterations/s and the encoding MAC/s with the paper's
+    kappa_enc = 3 kappa_dec accounting."""
+    import torch
+
+    import paper_2403_11651_b200 as P
+    from paper_2403_11651_b200 import dist
+
+    cfg = workload.CONFIGS[args.config if args.config != "batched2k" else "ref"]
+    dev = torch.device("cuda", rk.local_rank)
+    torch.cuda.set_device(dev)
+    P.load()
+    im = workload.make_image(cfg, workload.image_seed(args.seed, rk.rank))
+    rng = np.random.default_rng(args.seed + 77 + rk.rank)
+    y = workload.gen_continuous_latents(rng, im.latents)
+    tr = P.DeviceTrainer(cfg, y, im.arm_w, im.up_w, im.syn_w, im.image, device=dev)
+    noises = [torch.from_numpy(workload.gen_noise(rng, y.size)).to(dev) for _ in range(4)]
+    macs = P.cc_mac_per_pixel(tr.desc)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(k):
+        tr.noise.copy_(noises[k % len(noises)])   # on-device copy: the noise is an input of the iteration
+        return tr.step(lr=1e-3)
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(rk.local_rank)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    launches = 0
+    for k in range(args.steps):
+        res = step(k)
+        launches += P.ccrd.cc_last_launch_count()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    sampler.stop()
+    ms = dist.max_over_ranks(ev0.elapsed_time(ev1), device=dev)
+    its = rk.world * args.steps / (ms / 1e3)
+    r = res.cpu().numpy()
+    assert np.isfinite(r).all()
+    px = cfg.H * cfg.W
+    enc_flops = 3.0 * macs.total * px * its * 2
+    out = {
+        "metric": "encoder training iterations (forward + backward + Adam) as pixels/s", "value": its * px,
+        "unit": "pixels/s", "n_gpus": rk.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"train_{cfg.name}: one {cfg.H}x{cfg.W} image per GPU, ARM {list(cfg.arm_widths)}, "
+                               f"synthesis {list(cfg.syn_widths)}+{cfg.syn_n_res}xres3x3, noise proxy, Adam",
+                   "H": cfg.H, "W": cfg.W, "mac_per_pixel_dec": round(macs.total, 3),
+                   "l2": "per-step working set ~200 MB > 126 MB L2", "parallelism": f"image per GPU x{rk.world}"},
+        "iterations_per_s": its,
+        "path_roofline": {"achieved_tflops_per_gpu": enc_flops / rk.world / 1e12,
+                          "frac": enc_flops / rk.world / 1e12 / FP32_PEAK_TFLOPS,
+                          "note": "kappa_enc = 3 kappa_dec MAC per pixel per iteration (PAPER.md:389-394)"},
+        "context": "paper: ~30 min for ~102950 iterations on a 512x768 image (~57 it/s), hardware not stated "
+                   "(BASELINE.md section 1)",
+        "e2e": None, "gpu_launches": launches, "clocks": sampler.summary(),
+    }
+    if rk.rank == 0:
+        print(json.dumps(out), flush=True)
+
+
 def run_e2e(args, cfg, images, desc, dev, stream, rk, n_img):
     import torch
 
@@ -441,6 +513,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--train", action="store_true", help="time the encoder training iteration (NEXT-2)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 breaks the timing rules", file=sys.stderr)
@@ -450,7 +523,9 @@ def main():
         run_reference(args, rk)
         return
     rk = dist.init("nccl")
-    if args.config == "8k":
+    if args.train:
+        run_train(args, rk)
+    elif args.config == "8k":
         run_strip(args, rk)
     else:
         run_ours(args, rk)

@@ -190,6 +190,35 @@ size_t cc_workspace_bytes_strip(const cc_model_desc* desc, const cc_strip* strip
 int cc_rd_forward_strip(const cc_model_desc* desc, const cc_strip* strip, const cc_image_io* io,
                         cc_rd_result* result, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---------------------------------------------------------- training (NEXT-2)
+ * ONE encoder training iteration (Eq. 1 "simultaneously
+ * learning the latent and the different neural networks"
+ * "one forward pass and one backward pass"; SPEC.md:476-479 Adam on every
+ * parameter): forward on the proxy latents y_hat = y + u, the exact gradient
+ * of J = MSE + lambda R / (H W) wrt every parameter, then one Adam step.
+ * Readings (T1-T3): u ~ U(-1/2, 1/2) is an INPUT (`noise`, packed
+ * like the latents), its gradient passes unchanged to y; ReLU'(0) = 0; no
+ * gradient through the log-scale clamp outside (logscale_min, logscale_max) or
+ * through the probability floor.  Separable upsampling only (up_2d = 0).
+ *
+ * params: DEVICE fp32 [cc_train_param_count()] = [ y (N_lat, packed like the
+ * latents) | arm_w | up_w | syn_w ] (blob layouts as in cc_image_io), updated
+ * in place.  adam_m, adam_v: DEVICE fp32, same length (zero before step t = 1).
+ * grad: DEVICE fp32, same length: receives the gradient at the input point.
+ * opt: HOST; NULL = gradient only (no update).  result: DEVICE, the cost of
+ * this forward (rate_bits, sse, mse, cost).  image: DEVICE [3][H][W].
+ * Weights are staged into a __constant__ bank per call: one training call in
+ * flight per process (CUDA stream order). */
+typedef struct {
+  float lr, beta1, beta2, eps;
+  int32_t t;  /* Adam step number, >= 1 */
+} cc_adam;
+int64_t cc_train_param_count(const cc_model_desc* desc);   /* -1 on error */
+size_t cc_train_workspace_bytes(const cc_model_desc* desc);
+int cc_train_step(const cc_model_desc* desc, float* params, const float* noise, const float* image,
+                  float* adam_m, float* adam_v, const cc_adam* opt, cc_rd_result* result, float* grad,
+                  void* workspace, size_t workspace_bytes, void* stream);
+
 /* Stage entry: ARM rate only (PAPER.md:120 R term).  rate: DEVICE double [1].
  * Optional DEVICE float arrays (packed like the latents, NULL to skip):
  * mu, scale (= b), bits (per latent -log2 P).  Workspace as cc_rd_forward(1). */

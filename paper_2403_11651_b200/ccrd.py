@@ -63,6 +63,11 @@ class CcStrip(C.Structure):
                 ("lo", C.c_int32 * CC_MAX_LEVELS), ("hi", C.c_int32 * CC_MAX_LEVELS)]
 
 
+class CcAdam(C.Structure):
+    _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
+                ("t", C.c_int32)]
+
+
 class CcProfileSummary(C.Structure):
     _fields_ = [("arm_ms", C.c_double), ("syn_ms", C.c_double), ("reduce_ms", C.c_double), ("pyr_ms", C.c_double),
                 ("arm_launches", C.c_int64), ("syn_launches", C.c_int64), ("reduce_launches", C.c_int64),
@@ -74,7 +79,8 @@ EXPORTS = ["cc_workspace_bytes", "cc_rd_forward", "cc_workspace_bytes_host", "cc
            "cc_arm_rate", "cc_upsample", "cc_synthesize", "cc_mac_per_pixel", "cc_validate",
            "cc_strerror", "cc_last_error", "cc_version", "cc_last_launch_count",
            "cc_profile_begin", "cc_profile_end", "cc_strip_window", "cc_strip_latent_count",
-           "cc_workspace_bytes_strip", "cc_rd_forward_strip"]
+           "cc_workspace_bytes_strip", "cc_rd_forward_strip", "cc_train_param_count",
+           "cc_train_workspace_bytes", "cc_train_step"]
 
 _lib = None
 
@@ -134,6 +140,12 @@ def load(rebuild_if_stale: bool = True) -> C.CDLL:
     L.cc_workspace_bytes_strip.argtypes = [D, P(CcStrip)]
     L.cc_rd_forward_strip.restype = C.c_int
     L.cc_rd_forward_strip.argtypes = [D, P(CcStrip), P(CcImageIO), V, V, S, V]
+    L.cc_train_param_count.restype = C.c_int64
+    L.cc_train_param_count.argtypes = [D]
+    L.cc_train_workspace_bytes.restype = S
+    L.cc_train_workspace_bytes.argtypes = [D]
+    L.cc_train_step.restype = C.c_int
+    L.cc_train_step.argtypes = [D, V, V, V, V, V, P(CcAdam), V, V, V, S, V]
     _lib = L
     return L
 
@@ -261,6 +273,24 @@ def cc_rd_forward_strip(desc, strip: CcStrip, io: CcImageIO, result_ptr: int, ws
                                       stream_ptr), "cc_rd_forward_strip")
 
 
+def cc_train_param_count(desc) -> int:
+    n = load().cc_train_param_count(C.byref(desc))
+    if n < 0:
+        raise CcError(cc_validate(desc), "cc_train_param_count")
+    return n
+
+
+def cc_train_workspace_bytes(desc) -> int:
+    return load().cc_train_workspace_bytes(C.byref(desc))
+
+
+def cc_train_step(desc, params_ptr, noise_ptr, image_ptr, m_ptr, v_ptr, opt: Optional[CcAdam], result_ptr, grad_ptr,
+                  ws_ptr, ws_bytes, stream_ptr=0) -> None:
+    _check(load().cc_train_step(C.byref(desc), params_ptr, noise_ptr, image_ptr, m_ptr, v_ptr,
+                                C.byref(opt) if opt is not None else None, result_ptr, grad_ptr, ws_ptr, ws_bytes,
+                                stream_ptr), "cc_train_step")
+
+
 def cc_last_launch_count() -> int:
     return load().cc_last_launch_count()
 
@@ -347,4 +377,44 @@ class DeviceStrip:
         s = torch.cuda.current_stream().cuda_stream if stream_ptr is None else stream_ptr
         cc_rd_forward_strip(self.desc, self.strip, self.io, self.result.data_ptr(), self.ws.data_ptr(),
                             self.ws_bytes, s)
+        return self.result
+
+
+class DeviceTrainer:
+    """Device state of one image's encoder training (NEXT-2): the parameter
+    vector [y | arm_w | up_w | syn_w], Adam moments, gradient, image, workspace."""
+
+    def __init__(self, cfg, y, arm_w, up_w, syn_w, image, device="cuda"):
+        import torch
+        self.cfg = cfg
+        self.desc = desc_from_config(cfg)
+        self.n = cc_train_param_count(self.desc)
+        par = np.concatenate([np.asarray(y, np.float32).ravel(), np.asarray(arm_w, np.float32).ravel(),
+                              np.asarray(up_w, np.float32).ravel(), np.asarray(syn_w, np.float32).ravel()])
+        assert par.size == self.n, (par.size, self.n)
+        self.params = torch.from_numpy(par).to(device)
+        self.m = torch.zeros_like(self.params)
+        self.v = torch.zeros_like(self.params)
+        self.grad = torch.zeros_like(self.params)
+        self.image = torch.as_tensor(np.ascontiguousarray(image, np.float32)).to(device)
+        self.noise = torch.zeros(int(np.asarray(y).size), dtype=torch.float32, device=device)
+        self.result = torch.zeros(4, dtype=torch.float64, device=device)
+        self.ws_bytes = cc_train_workspace_bytes(self.desc)
+        if self.ws_bytes == 0:
+            raise CcError(CC_ENOTSUP, "cc_train_workspace_bytes")
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=device)
+        self.t = 0
+
+    def step(self, noise=None, lr=1e-2, betas=(0.9, 0.999), eps=1e-8, update=True, stream_ptr=None):
+        import torch
+        if noise is not None:
+            self.noise.copy_(torch.as_tensor(noise))
+        s = torch.cuda.current_stream().cuda_stream if stream_ptr is None else stream_ptr
+        opt = None
+        if update:
+            self.t += 1
+            opt = CcAdam(lr, betas[0], betas[1], eps, self.t)
+        cc_train_step(self.desc, self.params.data_ptr(), self.noise.data_ptr(), self.image.data_ptr(),
+                      self.m.data_ptr(), self.v.data_ptr(), opt, self.result.data_ptr(), self.grad.data_ptr(),
+                      self.ws.data_ptr(), self.ws_bytes, s)
         return self.result

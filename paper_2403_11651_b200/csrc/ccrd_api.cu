@@ -800,6 +800,38 @@ int cc_rd_forward_strip(const cc_model_desc* desc, const cc_strip* strip, const 
   return launch_reduce(&j, 1, result, s);
 }
 
+// ---------------------------------------------------------------- training
+int64_t cc_train_param_count(const cc_model_desc* desc) {
+  if (validate(desc) != CC_OK) return -1;
+  return train_param_count(*desc);
+}
+
+size_t cc_train_workspace_bytes(const cc_model_desc* desc) {
+  if (validate(desc) != CC_OK || !train_supported(*desc)) return 0;
+  return train_workspace_bytes(*desc);
+}
+
+int cc_train_step(const cc_model_desc* desc, float* params, const float* noise, const float* image, float* adam_m,
+                  float* adam_v, const cc_adam* opt, cc_rd_result* result, float* grad, void* workspace,
+                  size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  int rc = validate(desc);
+  if (rc) return rc;
+  const cc_model_desc& d = *desc;
+  if (!train_supported(d)) return fail(CC_ENOTSUP, "training step not compiled for this shape (or up_2d)");
+  if (!params || !noise || !image || !result || !grad) return fail(CC_EINVAL, "null params / noise / image / result / grad");
+  if (opt && (!adam_m || !adam_v || opt->t < 1)) return fail(CC_EINVAL, "Adam needs m, v and t >= 1");
+  const size_t need = train_workspace_bytes(d);
+  if (!workspace || workspace_bytes < need)
+    return fail(CC_EWORKSPACE, "need %zu workspace bytes, got %zu", need, workspace_bytes);
+  if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
+  const int n = train_step_impl(d, params, noise, image, adam_m, adam_v, opt, result, grad, workspace,
+                                (cudaStream_t)stream);
+  if (n < 0) return fail(CC_ENOTSUP, "training step: unsupported shape (%d)", n);
+  g_launches = n;
+  return cuda_check("cc_train_step");
+}
+
 // ---------------------------------------------------------------- stages
 int cc_arm_rate(const cc_model_desc* desc, const int16_t* latents, const float* arm_w, double* rate, float* mu,
                 float* scale, float* bits, void* workspace, size_t workspace_bytes, void* stream) {

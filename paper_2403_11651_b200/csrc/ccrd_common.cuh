@@ -248,6 +248,13 @@ typedef int (*SynLaunchFn)(const SynGeom& g, const cc_model_desc& d, const float
 ArmLaunchFn find_arm_launcher(int C, int NH, int NHL);     // FFMA2 path (arm_rate.cu)
 ArmLaunchFn find_arm_tc_launcher(int C, int NH, int NHL);  // tensor-core path (arm_tc.cu)
 int device_sm_count();  // current device's SMs (lazily cached; 148 without a device)
+
+// training iteration (train.cu, NEXT-2)
+int64_t train_param_count(const cc_model_desc& d);
+size_t train_workspace_bytes(const cc_model_desc& d);
+int train_supported(const cc_model_desc& d);
+int train_step_impl(const cc_model_desc& d, float* par, const float* noise, const float* image, float* am, float* av,
+                    const cc_adam* opt, cc_rd_result* result, float* grad, void* ws, cudaStream_t s);
 SynLaunchFn find_syn_launcher(int L, int CH, int R, int K);
 
 }  // namespace ccrd

@@ -1,0 +1,897 @@
+// train.cu -- ONE Cool-chic encoder training iteration on the GPU (NEXT-2).
+//
+// PAPER.md:113-126 (Eq. 1): the encoder minimises J = D(x, x_hat) +
+// lambda R(y_hat) / (H W) over the latents and psi, upsilon, theta through the
+// continuous latents y and a differentiable proxy of Q; "One
+// training iteration consists in one forward pass and one backward pass";
+// Adam on every parameter.  Readings (T1-T3):
+// noise proxy y_hat = y + u with u given as input (the random numbers are
+// data), gradient passed unchanged to y; ReLU'(0) = 0, no gradient through the
+// log-scale clamp outside its range or through the probability floor.
+//
+// Parameter vector (device fp32, the layout of include/ccrd.h):
+//   [ y (N_lat, packed like the latents) | arm_w | up_w | syn_w ].
+// The weights (arm | up | syn, <= 8 KB) are copied device-to-device into a
+// __constant__ bank at the start of the step, so every kernel reads them as
+// uniform operands with compile-time offsets.
+//
+// First version (correctness first): simple kernels, intermediates materialised
+// in HBM, one output element / latent / pixel per thread.
+//   1. proxy       y_hat = y + u
+//   2. ARM         forward + backward per latent: rate, d/dy_hat (own + context,
+//                  the latter gathered in a second kernel: deterministic),
+//                  per-CTA partial weight gradients (shared-memory outer products)
+//   3. upsampling  separable stride-2 transposed-conv steps level by level,
+//                  every step's input kept (dense [L][H][W] at the end)
+//   4. synthesis   1x1 layers, residual 3x3 layers, distortion; then their
+//                  adjoints (3x3 adjoint in gather form over the clamped
+//                  neighbourhood = replicate padding's adjoint), per-block
+//                  partial weight gradients
+//   5. upsampling adjoint, in gather form, tap-gradient partials
+//   6. fp64 reduction of every partial into the gradient, Adam, cost.
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "ccrd_common.cuh"
+
+namespace ccrd {
+
+constexpr int TR_MAX_W = 2048;  // arm + up + syn weights (floats)
+__constant__ float c_tw[TR_MAX_W];
+
+constexpr int TA_THREADS = 128;  // ARM: latents per CTA
+constexpr int TS_THREADS = 128;  // synthesis 1x1 backward: pixels per CTA
+constexpr int TB = 256;          // generic elementwise / stencil kernels
+
+struct TrainLevels {
+  int32_t L, H, W;
+  int32_t h[CC_MAX_LEVELS], w[CC_MAX_LEVELS];
+  int64_t off[CC_MAX_LEVELS];
+  int64_t n_lat;
+};
+
+// --------------------------------------------------------------- 1. proxy
+__global__ void tr_proxy_kernel(const float* __restrict__ y, const float* __restrict__ u, float* __restrict__ yq,
+                                int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    yq[i] = y[i] + u[i];
+}
+
+// --------------------------------------------------------------- 2. ARM
+struct TrainArmParams {
+  TrainLevels lv;
+  int32_t n_ctx;
+  int32_t dy[CC_MAX_CTX], dx[CC_MAX_CTX];
+  uint32_t res_mask;
+  float lsmin, lsmax, bits_cap, w_r;  // w_r = lambda / (H W)
+  const float* yq;
+  float* gown;     // [N_lat]      w_r d bits / d y_hat (own position)
+  float* dctx;     // [N_lat][C]   d J / d context value c of this latent
+  double* rate;    // [CTAs][4]    per-warp bits
+  float* wpart;    // [CTAs][n_arm] partial weight gradients
+  int32_t n_arm;
+};
+
+// bits and d bits / d (y, mu, s) -- fp32, IEEE exp / log (the hybrid stable
+// form of the forward kernel and its derivative)
+__device__ __forceinline__ float tr_bits(float y, float mu, float s, const TrainArmParams& p, float& gy,
+                                         float& gmu, float& gs) {
+  constexpr float LN2 = 0.6931471805599453f;
+  const bool inside = s > p.lsmin && s < p.lsmax;
+  const float sc = fminf(fmaxf(s, p.lsmin), p.lsmax);
+  const float b = expf(sc), ib = 1.0f / b;
+  const float d = y - mu, a = fabsf(d), sg = d >= 0.0f ? 1.0f : -1.0f;
+  float bits, dbda, dbdb;
+  if (a >= 0.5f) {  // log domain: bits = 1 + (a - 1/2) / (b ln2) - log2(1 - e^{-1/b})
+    const float em = expm1f(ib);  // e^{1/b} - 1
+    bits = 1.0f + (a - 0.5f) * ib / LN2 - log2f(-expm1f(-ib));
+    dbda = ib / LN2;
+    dbdb = (ib * ib / LN2) * (1.0f / em - (a - 0.5f));
+  } else {
+    const float e1 = expf(-(0.5f - a) * ib), e2 = expf(-(0.5f + a) * ib);
+    const float P = 1.0f - 0.5f * (e1 + e2);
+    bits = -log2f(P);
+    const float dPda = -(e1 - e2) * 0.5f * ib;
+    const float dPdb = -0.5f * ib * ib * (e1 * (0.5f - a) + e2 * (0.5f + a));
+    dbda = -dPda / (P * LN2);
+    dbdb = -dPdb / (P * LN2);
+  }
+  if (bits >= p.bits_cap) {  // probability floor: constant
+    gy = gmu = gs = 0.0f;
+    return p.bits_cap;
+  }
+  gy = sg * dbda;
+  gmu = -sg * dbda;
+  gs = inside ? dbdb * b : 0.0f;
+  return bits;
+}
+
+template <int C, int NH, int NHL>
+__global__ void __launch_bounds__(TA_THREADS) tr_arm_kernel(const __grid_constant__ TrainArmParams p) {
+  // per latent, in shared memory for the weight-gradient outer products:
+  //   layer k input z_k (C or NH) and output gradient du_k (NH, or 2 for the last)
+  constexpr int NL = NHL + 1;  // linear layers
+  constexpr int VEC = C + (NL - 1) * NH /* inputs of layers 1.. */ + (NL - 1) * NH /* du of hidden layers */ + 2;
+  extern __shared__ float tsm[];
+  float* vec = tsm + threadIdx.x * (VEC + 1);  // +1: bank spread
+  const int64_t q = blockIdx.x * (int64_t)TA_THREADS + threadIdx.x;
+  const bool valid = q < p.lv.n_lat;
+  float bits = 0.0f;
+  if (valid) {
+    int l = 0;
+    while (l + 1 < p.lv.L && q >= p.lv.off[l + 1]) l++;
+    const int h = p.lv.h[l], w = p.lv.w[l];
+    const int64_t t = q - p.lv.off[l];
+    const int i = (int)(t / w), j = (int)(t - (int64_t)i * w);
+    const float* g = p.yq + p.lv.off[l];
+    float z[NL][NH > C ? NH : C];  // z[k] = input of layer k
+    float u[NL][NH];               // pre-activations of the hidden layers
+#pragma unroll
+    for (int c = 0; c < C; c++) {
+      const int ii = i + p.dy[c], jj = j + p.dx[c];
+      z[0][c] = (ii >= 0 && ii < h && jj >= 0 && jj < w) ? g[(int64_t)ii * w + jj] : 0.0f;
+    }
+    // forward (weights: per layer W[out][in] then b[out], offset in c_tw)
+    int off = 0;
+    float mu = 0.0f, s = 0.0f;
+#pragma unroll
+    for (int k = 0; k < NL; k++) {
+      const int nin = (k == 0) ? C : NH, nout = (k == NL - 1) ? 2 : NH;
+      const bool res = (p.res_mask >> k) & 1u;
+#pragma unroll
+      for (int o = 0; o < nout; o++) {
+        float a = c_tw[off + nin * nout + o];
+#pragma unroll
+        for (int t2 = 0; t2 < nin; t2++) a = fmaf(c_tw[off + o * nin + t2], z[k][t2], a);
+        if (res) a += z[k][o];
+        if (k < NL - 1) {
+          u[k][o] = a;
+          z[k + 1][o] = fmaxf(a, 0.0f);
+        } else if (o == 0) {
+          mu = a;
+        } else {
+          s = a;
+        }
+      }
+      off += nin * nout + nout;
+    }
+    float gy, gmu, gs;
+    bits = tr_bits(g[t], mu, s, p, gy, gmu, gs);
+    p.gown[q] = p.w_r * gy;
+    // backward
+    float du[NH > 2 ? NH : 2];
+    du[0] = p.w_r * gmu;
+    du[1] = p.w_r * gs;
+    // stash the layer inputs and output gradients
+    int vo = 0;
+#pragma unroll
+    for (int c = 0; c < C; c++) vec[vo + c] = z[0][c];
+    vo += C;
+#pragma unroll
+    for (int k = 1; k < NL; k++)
+#pragma unroll
+      for (int n = 0; n < NH; n++) vec[vo + (k - 1) * NH + n] = z[k][n];
+    vo += (NL - 1) * NH;
+    const int du_base = vo;  // du of layer k (k < NL-1) at du_base + k*NH; last layer at du_base + (NL-1)*NH
+    vec[du_base + (NL - 1) * NH + 0] = du[0];
+    vec[du_base + (NL - 1) * NH + 1] = du[1];
+    int offk[NL];
+    {
+      int o2 = 0;
+#pragma unroll
+      for (int k = 0; k < NL; k++) {
+        const int nin = (k == 0) ? C : NH, nout = (k == NL - 1) ? 2 : NH;
+        offk[k] = o2;
+        o2 += nin * nout + nout;
+      }
+    }
+#pragma unroll
+    for (int k = NL - 1; k >= 0; k--) {
+      const int nin = (k == 0) ? C : NH, nout = (k == NL - 1) ? 2 : NH;
+      const bool res = (p.res_mask >> k) & 1u;
+      float dz[NH > C ? NH : C];
+#pragma unroll
+      for (int t2 = 0; t2 < nin; t2++) {
+        float a = res ? du[t2] : 0.0f;
+#pragma unroll
+        for (int o = 0; o < nout; o++) a = fmaf(c_tw[offk[k] + o * nin + t2], du[o], a);
+        dz[t2] = a;
+      }
+      if (k > 0) {
+#pragma unroll
+        for (int n = 0; n < NH; n++) {
+          du[n] = u[k - 1][n] > 0.0f ? dz[n] : 0.0f;
+          vec[du_base + (k - 1) * NH + n] = du[n];
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < C; c++) p.dctx[q * C + c] = dz[c];
+      }
+    }
+  } else {
+    for (int v = 0; v < VEC; v++) vec[v] = 0.0f;
+  }
+  // rate: one fp64 partial per warp
+#pragma unroll
+  for (int o2 = 16; o2 > 0; o2 >>= 1) bits += __shfl_xor_sync(0xffffffffu, bits, o2);
+  if ((threadIdx.x & 31) == 0) p.rate[blockIdx.x * (TA_THREADS / 32) + (threadIdx.x >> 5)] = (double)bits;
+  __syncthreads();
+  // per-CTA weight gradients: entry e of layer k = sum over the CTA's latents of
+  // du_k[o] z_k[i] (weights) or du_k[o] (biases)
+  for (int e = threadIdx.x; e < p.n_arm; e += TA_THREADS) {
+    int k = 0, base = 0, rem = e;
+    int nin = C, nout = (NL == 1) ? 2 : NH;
+    while (true) {
+      nin = (k == 0) ? C : NH;
+      nout = (k == NL - 1) ? 2 : NH;
+      if (rem < nin * nout + nout) break;
+      rem -= nin * nout + nout;
+      base += nin * nout + nout;
+      k++;
+    }
+    (void)base;
+    const int zoff = (k == 0) ? 0 : C + (k - 1) * NH;
+    const int duoff = C + (NL - 1) * NH + k * NH;
+    float acc = 0.0f;
+    if (rem < nin * nout) {
+      const int o = rem / nin, i2 = rem - o * nin;
+      for (int m = 0; m < TA_THREADS; m++) {
+        const float* v = tsm + m * (VEC + 1);
+        acc = fmaf(v[duoff + o], v[zoff + i2], acc);
+      }
+    } else {
+      const int o = rem - nin * nout;
+      for (int m = 0; m < TA_THREADS; m++) acc += tsm[m * (VEC + 1) + duoff + o];
+    }
+    p.wpart[(int64_t)blockIdx.x * p.n_arm + e] = acc;
+  }
+}
+
+// gradient of J wrt y_hat from the rate: own term + the context terms of the
+// latents that use this one (gather: deterministic)
+struct TrainCtx {
+  int32_t C;
+  int32_t dy[CC_MAX_CTX], dx[CC_MAX_CTX];
+};
+__global__ void tr_arm_gather_kernel(TrainLevels lv, const __grid_constant__ TrainCtx cx, const float* __restrict__ gown,
+                                     const float* __restrict__ dctx, float* __restrict__ gy) {
+  const int C = cx.C;
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= lv.n_lat) return;
+  int l = 0;
+  while (l + 1 < lv.L && q >= lv.off[l + 1]) l++;
+  const int h = lv.h[l], w = lv.w[l];
+  const int64_t t = q - lv.off[l];
+  const int i = (int)(t / w), j = (int)(t - (int64_t)i * w);
+  float g = gown[q];
+  for (int c = 0; c < C; c++) {
+    const int pi = i - cx.dy[c], pj = j - cx.dx[c];  // latent whose context c is (i, j)
+    if (pi >= 0 && pi < h && pj >= 0 && pj < w) g += dctx[(lv.off[l] + (int64_t)pi * w + pj) * C + c];
+  }
+  gy[q] = g;
+}
+
+// ------------------------------------------------ 3 / 5. one upsampling step
+// Along one axis of `lines` lines: out[o] = sum_t k[2t+1-r] g[clamp(q+r+K/4-1-t)],
+// o = 2q + r < m (the gather form of the stride-2 transposed conv on the
+// replicate-extended input, reading #12).
+__global__ void tr_tconv_fwd_kernel(const float* __restrict__ g, float* __restrict__ out, int lines, int n, int m,
+                                    int64_t g_ls, int64_t g_es, int64_t o_ls, int64_t o_es, int K, int koff) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)lines * m) return;
+  const int line = (int)(idx / m), o = (int)(idx - (int64_t)line * m);
+  const int q = o >> 1, r = o & 1;
+  float acc = 0.0f;
+  for (int t = 0; t < K / 2; t++)
+    acc = fmaf(c_tw[koff + 2 * t + 1 - r], g[line * g_ls + (int64_t)clampi(q + r + K / 4 - 1 - t, 0, n - 1) * g_es], acc);
+  out[line * o_ls + (int64_t)o * o_es] = acc;
+}
+
+// Adjoint: gg[s] = sum over extended positions i with clamp(i - E) = s of
+// sum_j k[j] gout[2i + j - P]; tap gradient dk[j] = sum x_ext[i] gout[2i + j - P]
+// (per-block partials [blocks][K]).
+__global__ void tr_tconv_bwd_kernel(const float* __restrict__ g, const float* __restrict__ gout, float* __restrict__ gg,
+                                    int lines, int n, int m, int64_t g_ls, int64_t g_es, int64_t o_ls, int64_t o_es,
+                                    int K, int koff, float* __restrict__ kpart) {
+  __shared__ float red[8][TB / 32];
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  float dk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (idx < (int64_t)lines * n) {
+    const int line = (int)(idx / n), s = (int)(idx - (int64_t)line * n);
+    const int E = K / 4, P = K / 2 - 1 + 2 * E;
+    const float xs = g[line * g_ls + (int64_t)s * g_es];
+    const int i_lo = (s == 0) ? 0 : s + E, i_hi = (s == n - 1) ? n - 1 + 2 * E : s + E;  // extended positions
+    float acc = 0.0f;
+    for (int i = i_lo; i <= i_hi; i++)
+      for (int j = 0; j < K; j++) {
+        const int o = 2 * i + j - P;
+        if (o >= 0 && o < m) {
+          const float go = gout[line * o_ls + (int64_t)o * o_es];
+          acc = fmaf(c_tw[koff + j], go, acc);
+          dk[j] = fmaf(xs, go, dk[j]);
+        }
+      }
+    gg[line * g_ls + (int64_t)s * g_es] = acc;
+  }
+  // block partial of the tap gradient
+  for (int j = 0; j < K; j++) {
+    float v = dk[j];
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o2);
+    if ((threadIdx.x & 31) == 0) red[j][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    float v = 0.0f;
+    for (int w2 = 0; w2 < TB / 32; w2++) v += red[threadIdx.x][w2];
+    kpart[(int64_t)blockIdx.x * K + threadIdx.x] = v;
+  }
+}
+
+// ------------------------------------------------------------ 4. synthesis
+struct TrainSynDims {
+  int32_t H, W, L, CH, R;
+  int64_t P;
+  int32_t oA0, oa0, oA1, oa1, oG;  // offsets of the synthesis blocks in c_tw
+};
+
+// 1x1 layers: u1 = A0 v + a0 (kept), h = A1 ReLU(u1) + a1 (pre kept), ReLU if R > 0
+__global__ void tr_syn1x1_fwd_kernel(TrainSynDims d, const float* __restrict__ dense, float* __restrict__ u1,
+                                     float* __restrict__ us0, float* __restrict__ hs0) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= d.P) return;
+  float v[16], o[3];
+  for (int i = 0; i < d.L; i++) v[i] = dense[(int64_t)i * d.P + p];
+  for (int c = 0; c < 3; c++) o[c] = c_tw[d.oa1 + c];
+  for (int n = 0; n < d.CH; n++) {
+    float a = c_tw[d.oa0 + n];
+    for (int i = 0; i < d.L; i++) a = fmaf(c_tw[d.oA0 + n * d.L + i], v[i], a);
+    u1[(int64_t)n * d.P + p] = a;
+    const float r = fmaxf(a, 0.0f);
+    for (int c = 0; c < 3; c++) o[c] = fmaf(c_tw[d.oA1 + c * d.CH + n], r, o[c]);
+  }
+  for (int c = 0; c < 3; c++) {
+    us0[c * d.P + p] = o[c];
+    hs0[c * d.P + p] = d.R > 0 ? fmaxf(o[c], 0.0f) : o[c];
+  }
+}
+
+// residual 3x3 layer r: us = hin + g + G * hin (replicate padding), hout = ReLU unless last
+__global__ void tr_conv_fwd_kernel(TrainSynDims d, int r, const float* __restrict__ hin, float* __restrict__ us,
+                                   float* __restrict__ hout) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= d.P) return;
+  const int y = (int)(p / d.W), x = (int)(p - (int64_t)y * d.W);
+  const int oG = d.oG + 84 * r;
+  for (int co = 0; co < 3; co++) {
+    float a = hin[co * d.P + p] + c_tw[oG + 81 + co];
+    for (int ci = 0; ci < 3; ci++)
+      for (int ky = 0; ky < 3; ky++)
+        for (int kx = 0; kx < 3; kx++)
+          a = fmaf(c_tw[oG + ((co * 3 + ci) * 3 + ky) * 3 + kx],
+                   hin[ci * d.P + (int64_t)clampi(y + ky - 1, 0, d.H - 1) * d.W + clampi(x + kx - 1, 0, d.W - 1)], a);
+    us[co * d.P + p] = a;
+    hout[co * d.P + p] = (r < d.R - 1) ? fmaxf(a, 0.0f) : a;
+  }
+}
+
+// distortion: dJ/dx_hat = -2 (x - x_hat) / (3 P); SSE per block (fp64)
+__global__ void tr_loss_kernel(TrainSynDims d, const float* __restrict__ xh, const float* __restrict__ img,
+                               float* __restrict__ gh, double* __restrict__ sse_part) {
+  __shared__ double red[TB / 32];
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  float e2 = 0.0f;
+  if (t < 3 * d.P) {
+    const float e = img[t] - xh[t];
+    gh[t] = -2.0f * e / (3.0f * (float)d.P);
+    e2 = e * e;
+  }
+#pragma unroll
+  for (int o2 = 16; o2 > 0; o2 >>= 1) e2 += __shfl_xor_sync(0xffffffffu, e2, o2);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = (double)e2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < TB / 32; w++) s += red[w];
+    sse_part[blockIdx.x] = s;
+  }
+}
+
+// adjoint of residual layer r: gpre = gh (x) ReLU'(us) (not on the last layer);
+// gin = gpre (residual) + G^T-gather over the clamped neighbourhood;
+// dG[co][ci][ky][kx] = sum gpre[co](p) hin[ci](clamp(p + tap)), dg[co] = sum gpre[co]
+__global__ void tr_conv_bwd_kernel(TrainSynDims d, int r, const float* __restrict__ hin, const float* __restrict__ us,
+                                   const float* __restrict__ gh, float* __restrict__ gin, float* __restrict__ gpart) {
+  __shared__ float red[84][TB / 32];
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int oG = d.oG + 84 * r;
+  const bool relu = r < d.R - 1;
+  float dG[84];
+#pragma unroll
+  for (int e = 0; e < 84; e++) dG[e] = 0.0f;
+  if (p < d.P) {
+    const int y = (int)(p / d.W), x = (int)(p - (int64_t)y * d.W);
+    auto gpre = [&](int c, int64_t q) {
+      const float v = gh[c * d.P + q];
+      return (!relu || us[c * d.P + q] > 0.0f) ? v : 0.0f;
+    };
+    float gp[3];
+    for (int co = 0; co < 3; co++) gp[co] = gpre(co, p);
+    // weight / bias gradients from this output position
+    for (int co = 0; co < 3; co++) {
+      dG[81 + co] = gp[co];
+      for (int ci = 0; ci < 3; ci++)
+        for (int ky = 0; ky < 3; ky++)
+          for (int kx = 0; kx < 3; kx++)
+            dG[((co * 3 + ci) * 3 + ky) * 3 + kx] =
+                gp[co] * hin[ci * d.P + (int64_t)clampi(y + ky - 1, 0, d.H - 1) * d.W + clampi(x + kx - 1, 0, d.W - 1)];
+    }
+    // input gradient: every output q and tap whose clamped source is p
+    const bool interior = y >= 1 && y <= d.H - 2 && x >= 1 && x <= d.W - 2;
+    for (int ci = 0; ci < 3; ci++) {
+      float a = gp[ci];  // residual
+      for (int ky = 0; ky < 3; ky++)
+        for (int kx = 0; kx < 3; kx++) {
+          if (interior) {
+            const int64_t q = (int64_t)(y - ky + 1) * d.W + (x - kx + 1);
+            for (int co = 0; co < 3; co++) a = fmaf(c_tw[oG + ((co * 3 + ci) * 3 + ky) * 3 + kx], gpre(co, q), a);
+          } else {
+            for (int qy = max(y - 1, 0); qy <= min(y + 1, d.H - 1); qy++)
+              for (int qx = max(x - 1, 0); qx <= min(x + 1, d.W - 1); qx++)
+                if (clampi(qy + ky - 1, 0, d.H - 1) == y && clampi(qx + kx - 1, 0, d.W - 1) == x)
+                  for (int co = 0; co < 3; co++)
+                    a = fmaf(c_tw[oG + ((co * 3 + ci) * 3 + ky) * 3 + kx], gpre(co, (int64_t)qy * d.W + qx), a);
+          }
+        }
+      gin[ci * d.P + p] = a;
+    }
+  }
+  for (int e = 0; e < 84; e++) {
+    float v = dG[e];
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o2);
+    if ((threadIdx.x & 31) == 0) red[e][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 84; e += TB) {
+    float v = 0.0f;
+    for (int w2 = 0; w2 < TB / 32; w2++) v += red[e][w2];
+    gpart[(int64_t)blockIdx.x * 84 + e] = v;
+  }
+}
+
+// adjoint of the 1x1 layers per pixel, dense gradient, per-CTA weight-gradient
+// partials (shared-memory outer products over the CTA's pixels)
+__global__ void __launch_bounds__(TS_THREADS)
+    tr_syn1x1_bwd_kernel(TrainSynDims d, const float* __restrict__ dense, const float* __restrict__ u1,
+                         const float* __restrict__ us0, const float* __restrict__ gh, float* __restrict__ gdense,
+                         float* __restrict__ wpart, int n_w) {
+  extern __shared__ float ssm[];
+  const int VEC = 3 + 2 * d.CH + d.L;  // d2 (3), v1 (CH), d1 (CH), dense (L)
+  float* vec = ssm + threadIdx.x * (VEC + 1);
+  const int64_t p = blockIdx.x * (int64_t)TS_THREADS + threadIdx.x;
+  if (p < d.P) {
+    float d2[3];
+    for (int c = 0; c < 3; c++) {
+      float g = gh[c * d.P + p];
+      if (d.R > 0 && !(us0[c * d.P + p] > 0.0f)) g = 0.0f;
+      d2[c] = g;
+      vec[c] = g;
+    }
+    for (int i = 0; i < d.L; i++) vec[3 + 2 * d.CH + i] = dense[(int64_t)i * d.P + p];
+    float gd[16];
+    for (int i = 0; i < d.L; i++) gd[i] = 0.0f;
+    for (int n = 0; n < d.CH; n++) {
+      const float a = u1[(int64_t)n * d.P + p];
+      vec[3 + n] = fmaxf(a, 0.0f);
+      float g = 0.0f;
+      for (int c = 0; c < 3; c++) g = fmaf(c_tw[d.oA1 + c * d.CH + n], d2[c], g);
+      g = a > 0.0f ? g : 0.0f;
+      vec[3 + d.CH + n] = g;
+      for (int i = 0; i < d.L; i++) gd[i] = fmaf(c_tw[d.oA0 + n * d.L + i], g, gd[i]);
+    }
+    for (int i = 0; i < d.L; i++) gdense[(int64_t)i * d.P + p] = gd[i];
+  } else {
+    for (int v = 0; v < VEC; v++) vec[v] = 0.0f;
+  }
+  __syncthreads();
+  // entries in the synthesis blob order: A0[n][i], a0[n], A1[c][n], a1[c]
+  for (int e = threadIdx.x; e < n_w; e += TS_THREADS) {
+    float acc = 0.0f;
+    if (e < d.CH * d.L) {
+      const int n = e / d.L, i = e - n * d.L;
+      for (int m = 0; m < TS_THREADS; m++) acc = fmaf(ssm[m * (VEC + 1) + 3 + d.CH + n], ssm[m * (VEC + 1) + 3 + 2 * d.CH + i], acc);
+    } else if (e < d.CH * d.L + d.CH) {
+      const int n = e - d.CH * d.L;
+      for (int m = 0; m < TS_THREADS; m++) acc += ssm[m * (VEC + 1) + 3 + d.CH + n];
+    } else if (e < d.CH * d.L + d.CH + 3 * d.CH) {
+      const int t = e - d.CH * d.L - d.CH, c = t / d.CH, n = t - c * d.CH;
+      for (int m = 0; m < TS_THREADS; m++) acc = fmaf(ssm[m * (VEC + 1) + c], ssm[m * (VEC + 1) + 3 + n], acc);
+    } else {
+      const int c = e - d.CH * d.L - d.CH - 3 * d.CH;
+      for (int m = 0; m < TS_THREADS; m++) acc += ssm[m * (VEC + 1) + c];
+    }
+    wpart[(int64_t)blockIdx.x * n_w + e] = acc;
+  }
+}
+
+// ------------------------------------------------------------ 6. reduction
+// grad[dst + e] (=|+=) sum over `blocks` partial rows of part[b * stride + e] (fp64)
+__global__ void tr_reduce_kernel(const float* __restrict__ part, int64_t blocks, int64_t stride, int n,
+                                 float* __restrict__ grad, int accumulate) {
+  __shared__ double red[TB];
+  for (int e = blockIdx.x; e < n; e += gridDim.x) {
+    double s = 0.0;
+    for (int64_t b = threadIdx.x; b < blocks; b += TB) s += (double)part[b * stride + e];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = TB / 2; o > 0; o >>= 1) {
+      if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) grad[e] = (float)(accumulate ? (double)grad[e] + red[0] : red[0]);
+    __syncthreads();
+  }
+}
+
+__global__ void tr_result_kernel(const double* __restrict__ rate_part, int64_t n_rate, const double* __restrict__ sse_part,
+                                 int64_t n_sse, double inv_3p, double lambda_over_p, cc_rd_result* out) {
+  __shared__ double ra[TB], sa[TB];
+  double r = 0.0, s = 0.0;
+  for (int64_t i = threadIdx.x; i < n_rate; i += TB) r += rate_part[i];
+  for (int64_t i = threadIdx.x; i < n_sse; i += TB) s += sse_part[i];
+  ra[threadIdx.x] = r;
+  sa[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = TB / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      ra[threadIdx.x] += ra[threadIdx.x + o];
+      sa[threadIdx.x] += sa[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    cc_rd_result res;
+    res.rate_bits = ra[0];
+    res.sse = sa[0];
+    res.mse = sa[0] * inv_3p;
+    res.cost = res.mse + lambda_over_p * ra[0];
+    *out = res;
+  }
+}
+
+// Adam (Kingma & Ba): m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2;
+// p -= lr (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps)
+__global__ void tr_adam_kernel(float* __restrict__ par, const float* __restrict__ g, float* __restrict__ m,
+                               float* __restrict__ v, int64_t n, float lr, float b1, float b2, float eps, float c1,
+                               float c2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.0f - b1) * gi;
+    const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    par[i] -= lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+  }
+}
+
+// ============================================================== host side
+struct TrainPlan {
+  TrainLevels lv;
+  int64_t n_arm, n_up, n_syn, n_par;
+  // workspace offsets (bytes)
+  size_t o_yq, o_gown, o_dctx, o_rate, o_wpart_arm, o_chain, o_dense, o_u1, o_us, o_hs, o_gh0, o_gh1, o_gdense,
+      o_g0, o_g1, o_kpart, o_cpart, o_spart, o_sse, o_grad_tmp, total;
+  int64_t arm_ctas, p_blocks, s_blocks, kpart_rows;
+  std::vector<int64_t> chain_off;  // per (l, j): output of step j for grid l; mid after the x pass
+  std::vector<int64_t> mid_off;
+};
+
+static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static void make_plan(const cc_model_desc& d, TrainPlan& pl) {
+  TrainLevels& lv = pl.lv;
+  memset(&lv, 0, sizeof(lv));
+  lv.L = d.L;
+  lv.H = d.H;
+  lv.W = d.W;
+  int64_t off = 0;
+  for (int l = 0; l < d.L; l++) {
+    lv.h[l] = (int32_t)((d.H + (1 << l) - 1) >> l);
+    lv.w[l] = (int32_t)((d.W + (1 << l) - 1) >> l);
+    lv.off[l] = off;
+    off += (int64_t)lv.h[l] * lv.w[l];
+  }
+  lv.n_lat = off;
+  pl.n_arm = 0;
+  for (int k = 0; k < d.arm_n_layers; k++) pl.n_arm += (int64_t)d.arm_widths[k] * d.arm_widths[k + 1] + d.arm_widths[k + 1];
+  pl.n_up = d.up_taps;
+  const int CH = d.syn_widths[1];
+  pl.n_syn = (int64_t)d.L * CH + CH + 3 * CH + 3 + 84 * (int64_t)d.syn_n_res;
+  pl.n_par = lv.n_lat + pl.n_arm + pl.n_up + pl.n_syn;
+  const int64_t P = (int64_t)d.H * d.W;
+  pl.arm_ctas = (lv.n_lat + TA_THREADS - 1) / TA_THREADS;
+  pl.p_blocks = (P + TB - 1) / TB;
+  pl.s_blocks = (P + TS_THREADS - 1) / TS_THREADS;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t r = o;
+    o += a256(bytes);
+    return r;
+  };
+  pl.o_yq = take(4 * lv.n_lat);
+  pl.o_gown = take(4 * lv.n_lat);
+  pl.o_dctx = take(4 * lv.n_lat * d.n_ctx);
+  pl.o_rate = take(8 * pl.arm_ctas * (TA_THREADS / 32));
+  pl.o_wpart_arm = take(4 * pl.arm_ctas * pl.n_arm);
+  // upsampling chains: grid l (l >= 1) at level j, j = l-1 .. 0, and the x-pass intermediates
+  pl.chain_off.assign(CC_MAX_LEVELS * CC_MAX_LEVELS, -1);
+  pl.mid_off.assign(CC_MAX_LEVELS * CC_MAX_LEVELS, -1);
+  int64_t c = 0, kp = 0;
+  for (int l = 1; l < d.L; l++)
+    for (int j = l - 1; j >= 0; j--) {
+      pl.mid_off[l * CC_MAX_LEVELS + j] = c;
+      c += (int64_t)lv.h[j + 1] * lv.w[j];
+      pl.chain_off[l * CC_MAX_LEVELS + j] = c;
+      c += (int64_t)lv.h[j] * lv.w[j];
+      // adjoint launches: y pass over h_{j+1} x w_j inputs, x pass over h_{j+1} x w_{j+1}
+      kp += ((int64_t)lv.h[j + 1] * lv.w[j] + TB - 1) / TB + ((int64_t)lv.h[j + 1] * lv.w[j + 1] + TB - 1) / TB;
+    }
+  pl.kpart_rows = kp > 0 ? kp : 1;
+  pl.o_chain = take(4 * (c > 0 ? c : 1));
+  pl.o_dense = take(4 * (size_t)d.L * P);
+  pl.o_u1 = take(4 * (size_t)CH * P);
+  pl.o_us = take(4 * (size_t)(d.syn_n_res + 1) * 3 * P);
+  pl.o_hs = take(4 * (size_t)(d.syn_n_res + 1) * 3 * P);
+  pl.o_gh0 = take(4 * 3 * (size_t)P);
+  pl.o_gh1 = take(4 * 3 * (size_t)P);
+  pl.o_gdense = take(4 * (size_t)d.L * P);
+  pl.o_g0 = take(4 * (size_t)P);
+  pl.o_g1 = take(4 * (size_t)P);
+  pl.o_kpart = take(4 * (size_t)pl.kpart_rows * d.up_taps);
+  pl.o_cpart = take(4 * (size_t)(d.syn_n_res > 0 ? d.syn_n_res : 1) * pl.p_blocks * 84);
+  pl.o_spart = take(4 * (size_t)pl.s_blocks * (d.L * CH + CH + 3 * CH + 3));
+  pl.o_sse = take(8 * (size_t)((3 * P + TB - 1) / TB));
+  pl.o_grad_tmp = take(4 * (size_t)(pl.n_up + 84));
+  pl.total = o;
+}
+
+int64_t train_param_count(const cc_model_desc& d) {
+  TrainPlan pl;
+  make_plan(d, pl);
+  return pl.n_par;
+}
+size_t train_workspace_bytes(const cc_model_desc& d) {
+  TrainPlan pl;
+  make_plan(d, pl);
+  return pl.total;
+}
+
+typedef void (*TrArmFn)(dim3, int, size_t, cudaStream_t, const TrainArmParams&);
+template <int C, int NH, int NHL>
+static void tr_arm_launch(dim3 g, int t, size_t smem, cudaStream_t s, const TrainArmParams& p) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tr_arm_kernel<C, NH, NHL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr = true;
+  }
+  tr_arm_kernel<C, NH, NHL><<<g, t, smem, s>>>(p);
+}
+struct TrArmEntry {
+  int C, NH, NHL;
+  TrArmFn fn;
+};
+static const TrArmEntry kTrArm[] = {
+    {16, 24, 2, tr_arm_launch<16, 24, 2>}, {8, 8, 2, tr_arm_launch<8, 8, 2>}, {8, 8, 1, tr_arm_launch<8, 8, 1>},
+    {16, 16, 2, tr_arm_launch<16, 16, 2>}, {24, 24, 2, tr_arm_launch<24, 24, 2>},
+};
+
+int train_supported(const cc_model_desc& d) {
+  if (d.up_2d) return 0;
+  if (d.syn_widths[1] > 64 || d.L > 16) return 0;
+  for (const auto& e : kTrArm)
+    if (e.C == d.n_ctx && e.NH == d.arm_widths[1] && e.NHL == d.arm_n_layers - 1) return 1;
+  return 0;
+}
+
+static int blocks_for(int64_t n) { return (int)((n + TB - 1) / TB); }
+
+// The iteration.  Returns the number of kernel launches (>= 0) or -1 if a
+// CUDA call failed (the caller checks cudaGetLastError).
+int train_step_impl(const cc_model_desc& d, float* par, const float* noise, const float* image, float* am, float* av,
+                    const cc_adam* opt, cc_rd_result* result, float* grad, void* ws, cudaStream_t s) {
+  TrainPlan pl;
+  make_plan(d, pl);
+  char* W = (char*)ws;
+  auto F = [&](size_t o) { return (float*)(W + o); };
+  const TrainLevels& lv = pl.lv;
+  const int64_t P = (int64_t)d.H * d.W;
+  const int L = d.L, K = d.up_taps, CH = d.syn_widths[1], R = d.syn_n_res;
+  int launches = 0;
+  // weights -> constant bank (arm | up | syn), device to device
+  const int64_t nw = pl.n_arm + pl.n_up + pl.n_syn;
+  if (nw > TR_MAX_W) return -2;
+  cudaMemcpyToSymbolAsync(c_tw, par + lv.n_lat, sizeof(float) * (size_t)nw, 0, cudaMemcpyDeviceToDevice, s);
+  const int koff = (int)pl.n_arm;  // taps in c_tw
+  TrainSynDims sd;
+  sd.H = d.H;
+  sd.W = d.W;
+  sd.L = L;
+  sd.CH = CH;
+  sd.R = R;
+  sd.P = P;
+  sd.oA0 = (int)(pl.n_arm + pl.n_up);
+  sd.oa0 = sd.oA0 + L * CH;
+  sd.oA1 = sd.oa0 + CH;
+  sd.oa1 = sd.oA1 + 3 * CH;
+  sd.oG = sd.oa1 + 3;
+  float* g_lat = grad;                     // gradient layout = parameter layout
+  float* g_arm = grad + lv.n_lat;
+  float* g_up = g_arm + pl.n_arm;
+  float* g_syn = g_up + pl.n_up;
+
+  // 1. proxy
+  tr_proxy_kernel<<<blocks_for(lv.n_lat), TB, 0, s>>>(par, noise, F(pl.o_yq), lv.n_lat);
+  launches++;
+  // 2. ARM forward + backward, gather, weight-gradient reduction
+  {
+    TrainArmParams ap;
+    memset(&ap, 0, sizeof(ap));
+    ap.lv = lv;
+    ap.n_ctx = d.n_ctx;
+    for (int c = 0; c < d.n_ctx; c++) {
+      ap.dy[c] = d.ctx_dy[c];
+      ap.dx[c] = d.ctx_dx[c];
+    }
+    ap.res_mask = d.arm_residual_mask;
+    ap.lsmin = d.logscale_min;
+    ap.lsmax = d.logscale_max;
+    ap.bits_cap = (float)(-log2((double)d.p_floor));
+    ap.w_r = (float)(d.lambda / (double)P);
+    ap.yq = F(pl.o_yq);
+    ap.gown = F(pl.o_gown);
+    ap.dctx = F(pl.o_dctx);
+    ap.rate = (double*)(W + pl.o_rate);
+    ap.wpart = F(pl.o_wpart_arm);
+    ap.n_arm = (int)pl.n_arm;
+    const int C = d.n_ctx, NH = d.arm_widths[1], NL = d.arm_n_layers;
+    const int vec = C + (NL - 1) * NH * 2 + 2;
+    const size_t smem = sizeof(float) * (size_t)TA_THREADS * (vec + 1);
+    TrArmFn fn = nullptr;
+    for (const auto& e : kTrArm)
+      if (e.C == C && e.NH == NH && e.NHL == NL - 1) fn = e.fn;
+    if (!fn) return -3;
+    fn(dim3((unsigned)pl.arm_ctas), TA_THREADS, smem, s, ap);
+    launches++;
+  }
+  {
+    TrainCtx cx;
+    memset(&cx, 0, sizeof(cx));
+    cx.C = d.n_ctx;
+    for (int c = 0; c < d.n_ctx; c++) {
+      cx.dy[c] = d.ctx_dy[c];
+      cx.dx[c] = d.ctx_dx[c];
+    }
+    tr_arm_gather_kernel<<<blocks_for(lv.n_lat), TB, 0, s>>>(lv, cx, F(pl.o_gown), F(pl.o_dctx), g_lat);
+    launches++;
+    tr_reduce_kernel<<<(int)(pl.n_arm < 1024 ? pl.n_arm : 1024), TB, 0, s>>>(F(pl.o_wpart_arm), pl.arm_ctas, pl.n_arm,
+                                                                          (int)pl.n_arm, g_arm, 0);
+    launches++;
+  }
+  // 3. upsampling forward: dense[0] = y_hat_0; grid l >= 1 through l steps
+  float* dense = F(pl.o_dense);
+  float* chain = F(pl.o_chain);
+  cudaMemcpyAsync(dense, F(pl.o_yq), sizeof(float) * (size_t)P, cudaMemcpyDeviceToDevice, s);
+  for (int l = 1; l < L; l++) {
+    const float* g = F(pl.o_yq) + lv.off[l];
+    for (int j = l - 1; j >= 0; j--) {
+      float* mid = chain + pl.mid_off[l * CC_MAX_LEVELS + j];
+      float* out = (j == 0) ? dense + (int64_t)l * P : chain + pl.chain_off[l * CC_MAX_LEVELS + j];
+      const int hs = lv.h[j + 1], ws2 = lv.w[j + 1], wd = lv.w[j], hd = lv.h[j];
+      // x pass: lines = rows (hs), n = ws2 -> m = wd
+      tr_tconv_fwd_kernel<<<blocks_for((int64_t)hs * wd), TB, 0, s>>>(g, mid, hs, ws2, wd, ws2, 1, wd, 1, K, koff);
+      // y pass: lines = columns (wd), n = hs -> m = hd
+      tr_tconv_fwd_kernel<<<blocks_for((int64_t)wd * hd), TB, 0, s>>>(mid, out, wd, hs, hd, 1, wd, 1, wd, K, koff);
+      launches += 2;
+      g = out;
+    }
+  }
+  // 4. synthesis forward, distortion, synthesis adjoint
+  float* u1 = F(pl.o_u1);
+  float* us = F(pl.o_us);
+  float* hsb = F(pl.o_hs);
+  tr_syn1x1_fwd_kernel<<<blocks_for(P), TB, 0, s>>>(sd, dense, u1, us, hsb);
+  launches++;
+  for (int r = 0; r < R; r++) {
+    tr_conv_fwd_kernel<<<blocks_for(P), TB, 0, s>>>(sd, r, hsb + (int64_t)r * 3 * P, us + (int64_t)(r + 1) * 3 * P,
+                                                  hsb + (int64_t)(r + 1) * 3 * P);
+    launches++;
+  }
+  float* gh = F(pl.o_gh0);
+  float* gh2 = F(pl.o_gh1);
+  const int64_t n_sse = (3 * P + TB - 1) / TB;
+  tr_loss_kernel<<<(int)n_sse, TB, 0, s>>>(sd, hsb + (int64_t)R * 3 * P, image, gh, (double*)(W + pl.o_sse));
+  launches++;
+  for (int r = R - 1; r >= 0; r--) {
+    float* cpart = F(pl.o_cpart) + (int64_t)r * pl.p_blocks * 84;
+    tr_conv_bwd_kernel<<<(int)pl.p_blocks, TB, 0, s>>>(sd, r, hsb + (int64_t)r * 3 * P, us + (int64_t)(r + 1) * 3 * P,
+                                                     gh, gh2, cpart);
+    launches++;
+    tr_reduce_kernel<<<84, TB, 0, s>>>(cpart, pl.p_blocks, 84, 84, g_syn + (sd.oG - sd.oA0) + 84 * r, 0);
+    launches++;
+    float* t = gh;
+    gh = gh2;
+    gh2 = t;
+  }
+  {
+    const int n_w = L * CH + CH + 3 * CH + 3;
+    const int vec = 3 + 2 * CH + L;
+    const size_t smem = sizeof(float) * (size_t)TS_THREADS * (vec + 1);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(tr_syn1x1_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      attr = true;
+    }
+    tr_syn1x1_bwd_kernel<<<(int)pl.s_blocks, TS_THREADS, smem, s>>>(sd, dense, u1, us, gh, F(pl.o_gdense),
+                                                                    F(pl.o_spart), n_w);
+    launches++;
+    tr_reduce_kernel<<<n_w < 1024 ? n_w : 1024, TB, 0, s>>>(F(pl.o_spart), pl.s_blocks, n_w, n_w, g_syn, 0);
+    launches++;
+  }
+  // 5. upsampling adjoint: grad of y_hat_l (l >= 1) += T^T ... T^T gdense[l]; taps
+  float* gdense = F(pl.o_gdense);
+  // channel 0 goes straight to the level-0 latents
+  {
+    // g_lat[0 .. P) += gdense[0]: reuse the proxy kernel as an axpy-free add
+    // (y + u form: out = a + b)
+    tr_proxy_kernel<<<blocks_for(P), TB, 0, s>>>(g_lat, gdense, g_lat, P);
+    launches++;
+  }
+  float* kpart = F(pl.o_kpart);
+  int64_t krow = 0;
+  for (int l = 1; l < L; l++) {
+    const float* gcur = gdense + (int64_t)l * P;
+    for (int j = 0; j < l; j++) {
+      const int hs = lv.h[j + 1], ws2 = lv.w[j + 1], wd = lv.w[j], hd = lv.h[j];
+      const float* mid = chain + pl.mid_off[l * CC_MAX_LEVELS + j];
+      const float* gin = (j == l - 1) ? F(pl.o_yq) + lv.off[l] : chain + pl.chain_off[l * CC_MAX_LEVELS + (j + 1)];
+      float* gmid = F(pl.o_g1);   // gcur (gdense or o_g0) -> gmid -> gprev (o_g0: gcur is consumed)
+      float* gprev = F(pl.o_g0);
+      // the y pass's adjoint: lines = columns (wd), inputs mid (n = hs), outputs gcur (m = hd)
+      const int64_t b1 = blocks_for((int64_t)wd * hs);
+      tr_tconv_bwd_kernel<<<(int)b1, TB, 0, s>>>(mid, gcur, gmid, wd, hs, hd, 1, wd, 1, wd, K, koff,
+                                                 kpart + krow * K);
+      krow += b1;
+      // the x pass's adjoint: lines = rows (hs), inputs gin (n = ws2), outputs gmid (m = wd)
+      const int64_t b2 = blocks_for((int64_t)hs * ws2);
+      tr_tconv_bwd_kernel<<<(int)b2, TB, 0, s>>>(gin, gmid, gprev, hs, ws2, wd, ws2, 1, wd, 1, K, koff,
+                                                 kpart + krow * K);
+      krow += b2;
+      launches += 2;
+      gcur = gprev;
+    }
+    tr_proxy_kernel<<<blocks_for((int64_t)lv.h[l] * lv.w[l]), TB, 0, s>>>(g_lat + lv.off[l], gcur, g_lat + lv.off[l],
+                                                                        (int64_t)lv.h[l] * lv.w[l]);
+    launches++;
+  }
+  if (krow > 0) {
+    tr_reduce_kernel<<<K, TB, 0, s>>>(kpart, krow, K, K, g_up, 0);
+    launches++;
+  } else {
+    cudaMemsetAsync(g_up, 0, sizeof(float) * (size_t)K, s);
+  }
+  // 6. cost of this forward, then Adam on every parameter
+  tr_result_kernel<<<1, TB, 0, s>>>((double*)(W + pl.o_rate), pl.arm_ctas * (TA_THREADS / 32), (double*)(W + pl.o_sse),
+                                    n_sse, 1.0 / (3.0 * (double)P), d.lambda / (double)P, result);
+  launches++;
+  if (opt) {
+    const float c1 = (float)(1.0 - pow((double)opt->beta1, opt->t)), c2 = (float)(1.0 - pow((double)opt->beta2, opt->t));
+    tr_adam_kernel<<<blocks_for(pl.n_par) < 4096 ? blocks_for(pl.n_par) : 4096, TB, 0, s>>>(
+        par, grad, am, av, pl.n_par, opt->lr, opt->beta1, opt->beta2, opt->eps, c1, c2);
+    launches++;
+  }
+  return launches;
+}
+
+}  // namespace ccrd
