@@ -277,9 +277,12 @@ __global__ void tr_arm_gather_kernel(TrainLevels lv, const __grid_constant__ Tra
 // o = 2q + r < m (the gather form of the stride-2 transposed conv on the
 // replicate-extended input, reading #12).
 __global__ void tr_tconv_fwd_kernel(const float* __restrict__ g, float* __restrict__ out, int lines, int n, int m,
-                                    int64_t g_ls, int64_t g_es, int64_t o_ls, int64_t o_es, int K, int koff) {
+                                    int64_t g_ls, int64_t g_es, int64_t o_ls, int64_t o_es, int K, int koff,
+                                    int64_t g_cs, int64_t o_cs) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= (int64_t)lines * m) return;
+  g += blockIdx.y * g_cs;  // channel
+  out += blockIdx.y * o_cs;
   const int line = (int)(idx / m), o = (int)(idx - (int64_t)line * m);
   const int q = o >> 1, r = o & 1;
   float acc = 0.0f;
@@ -293,9 +296,13 @@ __global__ void tr_tconv_fwd_kernel(const float* __restrict__ g, float* __restri
 // (per-block partials [blocks][K]).
 __global__ void tr_tconv_bwd_kernel(const float* __restrict__ g, const float* __restrict__ gout, float* __restrict__ gg,
                                     int lines, int n, int m, int64_t g_ls, int64_t g_es, int64_t o_ls, int64_t o_es,
-                                    int K, int koff, float* __restrict__ kpart) {
+                                    int K, int koff, float* __restrict__ kpart, int64_t g_cs, int64_t o_cs) {
   __shared__ float red[8][TB / 32];
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  g += blockIdx.y * g_cs;  // channel (gg shares g's layout)
+  gg += blockIdx.y * g_cs;
+  gout += blockIdx.y * o_cs;
+  kpart += (int64_t)blockIdx.y * gridDim.x * K;
   float dk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (idx < (int64_t)lines * n) {
     const int line = (int)(idx / n), s = (int)(idx - (int64_t)line * n);
@@ -337,19 +344,25 @@ struct TrainSynDims {
 };
 
 // 1x1 layers: u1 = A0 v + a0 (kept), h = A1 ReLU(u1) + a1 (pre kept), ReLU if R > 0
+template <int L, int CH>
 __global__ void tr_syn1x1_fwd_kernel(TrainSynDims d, const float* __restrict__ dense, float* __restrict__ u1,
                                      float* __restrict__ us0, float* __restrict__ hs0) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= d.P) return;
-  float v[16], o[3];
-  for (int i = 0; i < d.L; i++) v[i] = dense[(int64_t)i * d.P + p];
+  float v[L], o[3];
+#pragma unroll
+  for (int i = 0; i < L; i++) v[i] = dense[(int64_t)i * d.P + p];
+#pragma unroll
   for (int c = 0; c < 3; c++) o[c] = c_tw[d.oa1 + c];
-  for (int n = 0; n < d.CH; n++) {
+#pragma unroll 4
+  for (int n = 0; n < CH; n++) {
     float a = c_tw[d.oa0 + n];
-    for (int i = 0; i < d.L; i++) a = fmaf(c_tw[d.oA0 + n * d.L + i], v[i], a);
+#pragma unroll
+    for (int i = 0; i < L; i++) a = fmaf(c_tw[d.oA0 + n * L + i], v[i], a);
     u1[(int64_t)n * d.P + p] = a;
     const float r = fmaxf(a, 0.0f);
-    for (int c = 0; c < 3; c++) o[c] = fmaf(c_tw[d.oA1 + c * d.CH + n], r, o[c]);
+#pragma unroll
+    for (int c = 0; c < 3; c++) o[c] = fmaf(c_tw[d.oA1 + c * CH + n], r, o[c]);
   }
   for (int c = 0; c < 3; c++) {
     us0[c * d.P + p] = o[c];
@@ -463,12 +476,13 @@ __global__ void tr_conv_bwd_kernel(TrainSynDims d, int r, const float* __restric
 
 // adjoint of the 1x1 layers per pixel, dense gradient, per-CTA weight-gradient
 // partials (shared-memory outer products over the CTA's pixels)
+template <int L, int CH>
 __global__ void __launch_bounds__(TS_THREADS)
     tr_syn1x1_bwd_kernel(TrainSynDims d, const float* __restrict__ dense, const float* __restrict__ u1,
                          const float* __restrict__ us0, const float* __restrict__ gh, float* __restrict__ gdense,
                          float* __restrict__ wpart, int n_w) {
   extern __shared__ float ssm[];
-  const int VEC = 3 + 2 * d.CH + d.L;  // d2 (3), v1 (CH), d1 (CH), dense (L)
+  constexpr int VEC = 3 + 2 * CH + L;  // d2 (3), v1 (CH), d1 (CH), dense (L)
   float* vec = ssm + threadIdx.x * (VEC + 1);
   const int64_t p = blockIdx.x * (int64_t)TS_THREADS + threadIdx.x;
   if (p < d.P) {
@@ -479,19 +493,25 @@ __global__ void __launch_bounds__(TS_THREADS)
       d2[c] = g;
       vec[c] = g;
     }
-    for (int i = 0; i < d.L; i++) vec[3 + 2 * d.CH + i] = dense[(int64_t)i * d.P + p];
-    float gd[16];
-    for (int i = 0; i < d.L; i++) gd[i] = 0.0f;
-    for (int n = 0; n < d.CH; n++) {
+#pragma unroll
+    for (int i = 0; i < L; i++) vec[3 + 2 * CH + i] = dense[(int64_t)i * d.P + p];
+    float gd[L];
+#pragma unroll
+    for (int i = 0; i < L; i++) gd[i] = 0.0f;
+#pragma unroll 4
+    for (int n = 0; n < CH; n++) {
       const float a = u1[(int64_t)n * d.P + p];
       vec[3 + n] = fmaxf(a, 0.0f);
       float g = 0.0f;
-      for (int c = 0; c < 3; c++) g = fmaf(c_tw[d.oA1 + c * d.CH + n], d2[c], g);
+#pragma unroll
+      for (int c = 0; c < 3; c++) g = fmaf(c_tw[d.oA1 + c * CH + n], d2[c], g);
       g = a > 0.0f ? g : 0.0f;
-      vec[3 + d.CH + n] = g;
-      for (int i = 0; i < d.L; i++) gd[i] = fmaf(c_tw[d.oA0 + n * d.L + i], g, gd[i]);
+      vec[3 + CH + n] = g;
+#pragma unroll
+      for (int i = 0; i < L; i++) gd[i] = fmaf(c_tw[d.oA0 + n * L + i], g, gd[i]);
     }
-    for (int i = 0; i < d.L; i++) gdense[(int64_t)i * d.P + p] = gd[i];
+#pragma unroll
+    for (int i = 0; i < L; i++) gdense[(int64_t)i * d.P + p] = gd[i];
   } else {
     for (int v = 0; v < VEC; v++) vec[v] = 0.0f;
   }
@@ -499,17 +519,21 @@ __global__ void __launch_bounds__(TS_THREADS)
   // entries in the synthesis blob order: A0[n][i], a0[n], A1[c][n], a1[c]
   for (int e = threadIdx.x; e < n_w; e += TS_THREADS) {
     float acc = 0.0f;
-    if (e < d.CH * d.L) {
-      const int n = e / d.L, i = e - n * d.L;
-      for (int m = 0; m < TS_THREADS; m++) acc = fmaf(ssm[m * (VEC + 1) + 3 + d.CH + n], ssm[m * (VEC + 1) + 3 + 2 * d.CH + i], acc);
-    } else if (e < d.CH * d.L + d.CH) {
-      const int n = e - d.CH * d.L;
-      for (int m = 0; m < TS_THREADS; m++) acc += ssm[m * (VEC + 1) + 3 + d.CH + n];
-    } else if (e < d.CH * d.L + d.CH + 3 * d.CH) {
-      const int t = e - d.CH * d.L - d.CH, c = t / d.CH, n = t - c * d.CH;
+    if (e < CH * L) {
+      const int n = e / L, i = e - n * L;
+#pragma unroll 8
+      for (int m = 0; m < TS_THREADS; m++) acc = fmaf(ssm[m * (VEC + 1) + 3 + CH + n], ssm[m * (VEC + 1) + 3 + 2 * CH + i], acc);
+    } else if (e < CH * L + CH) {
+      const int n = e - CH * L;
+#pragma unroll 8
+      for (int m = 0; m < TS_THREADS; m++) acc += ssm[m * (VEC + 1) + 3 + CH + n];
+    } else if (e < CH * L + CH + 3 * CH) {
+      const int t = e - CH * L - CH, c = t / CH, n = t - c * CH;
+#pragma unroll 8
       for (int m = 0; m < TS_THREADS; m++) acc = fmaf(ssm[m * (VEC + 1) + c], ssm[m * (VEC + 1) + 3 + n], acc);
     } else {
-      const int c = e - d.CH * d.L - d.CH - 3 * d.CH;
+      const int c = e - CH * L - CH - 3 * CH;
+#pragma unroll 8
       for (int m = 0; m < TS_THREADS; m++) acc += ssm[m * (VEC + 1) + c];
     }
     wpart[(int64_t)blockIdx.x * n_w + e] = acc;
@@ -517,22 +541,27 @@ __global__ void __launch_bounds__(TS_THREADS)
 }
 
 // ------------------------------------------------------------ 6. reduction
-// grad[dst + e] (=|+=) sum over `blocks` partial rows of part[b * stride + e] (fp64)
-__global__ void tr_reduce_kernel(const float* __restrict__ part, int64_t blocks, int64_t stride, int n,
-                                 float* __restrict__ grad, int accumulate) {
-  __shared__ double red[TB];
-  for (int e = blockIdx.x; e < n; e += gridDim.x) {
-    double s = 0.0;
-    for (int64_t b = threadIdx.x; b < blocks; b += TB) s += (double)part[b * stride + e];
-    red[threadIdx.x] = s;
-    __syncthreads();
-    for (int o = TB / 2; o > 0; o >>= 1) {
-      if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) grad[e] = (float)(accumulate ? (double)grad[e] + red[0] : red[0]);
-    __syncthreads();
-  }
+// Two-stage fp64 reduction of partial rows part[b * stride + e], b < blocks,
+// e < n: stage 1 sums row chunks (blockIdx.y) with one thread per entry
+// (coalesced across the warp), stage 2 sums the chunks into grad[e].
+constexpr int TR_RCHUNK = 64;
+__global__ void tr_reduce1_kernel(const float* __restrict__ part, int64_t blocks, int64_t stride, int n,
+                                  double* __restrict__ tmp) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int64_t per = (blocks + gridDim.y - 1) / gridDim.y;
+  const int64_t b0 = blockIdx.y * per, b1 = b0 + per < blocks ? b0 + per : blocks;
+  double s = 0.0;
+#pragma unroll 4
+  for (int64_t b = b0; b < b1; b++) s += (double)part[b * stride + e];
+  tmp[(int64_t)blockIdx.y * n + e] = s;
+}
+__global__ void tr_reduce2_kernel(const double* __restrict__ tmp, int chunks, int n, float* __restrict__ grad) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double s = 0.0;
+  for (int c = 0; c < chunks; c++) s += tmp[(int64_t)c * n + e];
+  grad[e] = (float)s;
 }
 
 __global__ void tr_result_kernel(const double* __restrict__ rate_part, int64_t n_rate, const double* __restrict__ sse_part,
@@ -625,19 +654,22 @@ static void make_plan(const cc_model_desc& d, TrainPlan& pl) {
   pl.o_dctx = take(4 * lv.n_lat * d.n_ctx);
   pl.o_rate = take(8 * pl.arm_ctas * (TA_THREADS / 32));
   pl.o_wpart_arm = take(4 * pl.arm_ctas * pl.n_arm);
-  // upsampling chains: grid l (l >= 1) at level j, j = l-1 .. 0, and the x-pass intermediates
+  // upsampling stacks T_j = [y_hat_j, S_j] (L - j channels at level j; T_0 is
+  // the dense tensor) and the x-pass intermediates mid_j ((L-1-j) channels of
+  // h_{j+1} x w_j), offsets in floats; tap-gradient partial rows per adjoint
   pl.chain_off.assign(CC_MAX_LEVELS * CC_MAX_LEVELS, -1);
   pl.mid_off.assign(CC_MAX_LEVELS * CC_MAX_LEVELS, -1);
   int64_t c = 0, kp = 0;
-  for (int l = 1; l < d.L; l++)
-    for (int j = l - 1; j >= 0; j--) {
-      pl.mid_off[l * CC_MAX_LEVELS + j] = c;
-      c += (int64_t)lv.h[j + 1] * lv.w[j];
-      pl.chain_off[l * CC_MAX_LEVELS + j] = c;
-      c += (int64_t)lv.h[j] * lv.w[j];
-      // adjoint launches: y pass over h_{j+1} x w_j inputs, x pass over h_{j+1} x w_{j+1}
-      kp += ((int64_t)lv.h[j + 1] * lv.w[j] + TB - 1) / TB + ((int64_t)lv.h[j + 1] * lv.w[j + 1] + TB - 1) / TB;
-    }
+  for (int j = 1; j < d.L; j++) {  // T_0 lives in the dense buffer
+    pl.chain_off[j] = c;
+    c += (int64_t)(d.L - j) * lv.h[j] * lv.w[j];
+  }
+  for (int j = 0; j + 1 < d.L; j++) {
+    const int nch = d.L - 1 - j;
+    pl.mid_off[j] = c;
+    c += (int64_t)nch * lv.h[j + 1] * lv.w[j];
+    kp += (int64_t)nch * (((int64_t)lv.h[j + 1] * lv.w[j] + TB - 1) / TB + ((int64_t)lv.h[j + 1] * lv.w[j + 1] + TB - 1) / TB);
+  }
   pl.kpart_rows = kp > 0 ? kp : 1;
   pl.o_chain = take(4 * (c > 0 ? c : 1));
   pl.o_dense = take(4 * (size_t)d.L * P);
@@ -647,13 +679,13 @@ static void make_plan(const cc_model_desc& d, TrainPlan& pl) {
   pl.o_gh0 = take(4 * 3 * (size_t)P);
   pl.o_gh1 = take(4 * 3 * (size_t)P);
   pl.o_gdense = take(4 * (size_t)d.L * P);
-  pl.o_g0 = take(4 * (size_t)P);
-  pl.o_g1 = take(4 * (size_t)P);
+  pl.o_g0 = take(4 * (size_t)d.L * P);  // gradient stacks gT_j (ping)
+  pl.o_g1 = take(4 * (size_t)d.L * P);  // gmid / gT_j (pong)
   pl.o_kpart = take(4 * (size_t)pl.kpart_rows * d.up_taps);
   pl.o_cpart = take(4 * (size_t)(d.syn_n_res > 0 ? d.syn_n_res : 1) * pl.p_blocks * 84);
   pl.o_spart = take(4 * (size_t)pl.s_blocks * (d.L * CH + CH + 3 * CH + 3));
   pl.o_sse = take(8 * (size_t)((3 * P + TB - 1) / TB));
-  pl.o_grad_tmp = take(4 * (size_t)(pl.n_up + 84));
+  pl.o_grad_tmp = take(8 * (size_t)TR_RCHUNK * TR_MAX_W);  // stage-1 reduction chunks (fp64)
   pl.total = o;
 }
 
@@ -687,12 +719,55 @@ static const TrArmEntry kTrArm[] = {
     {16, 16, 2, tr_arm_launch<16, 16, 2>}, {24, 24, 2, tr_arm_launch<24, 24, 2>},
 };
 
+typedef void (*TrSynFwdFn)(int, int, cudaStream_t, const TrainSynDims&, const float*, float*, float*, float*);
+typedef void (*TrSynBwdFn)(int, int, size_t, cudaStream_t, const TrainSynDims&, const float*, const float*,
+                           const float*, const float*, float*, float*, int);
+template <int L, int CH>
+static void tr_syn_fwd_launch(int g, int t, cudaStream_t s, const TrainSynDims& d, const float* dense, float* u1,
+                              float* us0, float* hs0) {
+  tr_syn1x1_fwd_kernel<L, CH><<<g, t, 0, s>>>(d, dense, u1, us0, hs0);
+}
+template <int L, int CH>
+static void tr_syn_bwd_launch(int g, int t, size_t smem, cudaStream_t s, const TrainSynDims& d, const float* dense,
+                              const float* u1, const float* us0, const float* gh, float* gdense, float* wpart, int n_w) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tr_syn1x1_bwd_kernel<L, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr = true;
+  }
+  tr_syn1x1_bwd_kernel<L, CH><<<g, t, smem, s>>>(d, dense, u1, us0, gh, gdense, wpart, n_w);
+}
+struct TrSynEntry {
+  int L, CH;
+  TrSynFwdFn fwd;
+  TrSynBwdFn bwd;
+};
+static const TrSynEntry kTrSyn[] = {
+    {7, 40, tr_syn_fwd_launch<7, 40>, tr_syn_bwd_launch<7, 40>},
+    {7, 16, tr_syn_fwd_launch<7, 16>, tr_syn_bwd_launch<7, 16>},
+    {7, 8, tr_syn_fwd_launch<7, 8>, tr_syn_bwd_launch<7, 8>},
+    {4, 8, tr_syn_fwd_launch<4, 8>, tr_syn_bwd_launch<4, 8>},
+};
+static const TrSynEntry* find_tr_syn(const cc_model_desc& d) {
+  for (const auto& e : kTrSyn)
+    if (e.L == d.L && e.CH == d.syn_widths[1]) return &e;
+  return nullptr;
+}
+
 int train_supported(const cc_model_desc& d) {
-  if (d.up_2d) return 0;
-  if (d.syn_widths[1] > 64 || d.L > 16) return 0;
+  if (d.up_2d || !find_tr_syn(d)) return 0;
   for (const auto& e : kTrArm)
     if (e.C == d.n_ctx && e.NH == d.arm_widths[1] && e.NHL == d.arm_n_layers - 1) return 1;
   return 0;
+}
+
+// sum of partial rows into grad[0 .. n): fp64, two coalesced stages
+static int reduce_partials(const float* part, int64_t blocks, int64_t stride, int n, float* grad, double* tmp,
+                           cudaStream_t s) {
+  const int chunks = (int)(blocks < TR_RCHUNK ? (blocks > 0 ? blocks : 1) : TR_RCHUNK);
+  tr_reduce1_kernel<<<dim3((n + TB - 1) / TB, chunks), TB, 0, s>>>(part, blocks, stride, n, tmp);
+  tr_reduce2_kernel<<<(n + TB - 1) / TB, TB, 0, s>>>(tmp, chunks, n, grad);
+  return 2;
 }
 
 static int blocks_for(int64_t n) { return (int)((n + TB - 1) / TB); }
@@ -775,33 +850,36 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
     }
     tr_arm_gather_kernel<<<blocks_for(lv.n_lat), TB, 0, s>>>(lv, cx, F(pl.o_gown), F(pl.o_dctx), g_lat);
     launches++;
-    tr_reduce_kernel<<<(int)(pl.n_arm < 1024 ? pl.n_arm : 1024), TB, 0, s>>>(F(pl.o_wpart_arm), pl.arm_ctas, pl.n_arm,
-                                                                          (int)pl.n_arm, g_arm, 0);
-    launches++;
+    launches += reduce_partials(F(pl.o_wpart_arm), pl.arm_ctas, pl.n_arm, (int)pl.n_arm, g_arm,
+                                (double*)(W + pl.o_grad_tmp), s);
   }
-  // 3. upsampling forward: dense[0] = y_hat_0; grid l >= 1 through l steps
+  // 3. upsampling forward on stacks: T_{L-1} = [y_hat_{L-1}]; step j takes
+  //    T_{j+1} (L-1-j channels) through one x2 step into T_j[1..]; T_j[0] = y_hat_j
   float* dense = F(pl.o_dense);
   float* chain = F(pl.o_chain);
-  cudaMemcpyAsync(dense, F(pl.o_yq), sizeof(float) * (size_t)P, cudaMemcpyDeviceToDevice, s);
-  for (int l = 1; l < L; l++) {
-    const float* g = F(pl.o_yq) + lv.off[l];
-    for (int j = l - 1; j >= 0; j--) {
-      float* mid = chain + pl.mid_off[l * CC_MAX_LEVELS + j];
-      float* out = (j == 0) ? dense + (int64_t)l * P : chain + pl.chain_off[l * CC_MAX_LEVELS + j];
-      const int hs = lv.h[j + 1], ws2 = lv.w[j + 1], wd = lv.w[j], hd = lv.h[j];
-      // x pass: lines = rows (hs), n = ws2 -> m = wd
-      tr_tconv_fwd_kernel<<<blocks_for((int64_t)hs * wd), TB, 0, s>>>(g, mid, hs, ws2, wd, ws2, 1, wd, 1, K, koff);
-      // y pass: lines = columns (wd), n = hs -> m = hd
-      tr_tconv_fwd_kernel<<<blocks_for((int64_t)wd * hd), TB, 0, s>>>(mid, out, wd, hs, hd, 1, wd, 1, wd, K, koff);
-      launches += 2;
-      g = out;
-    }
+  auto Tj = [&](int j) { return j == 0 ? dense : chain + pl.chain_off[j]; };
+  for (int j = 0; j < L; j++)
+    cudaMemcpyAsync(Tj(j), F(pl.o_yq) + lv.off[j], sizeof(float) * (size_t)lv.h[j] * lv.w[j], cudaMemcpyDeviceToDevice,
+                    s);
+  for (int j = L - 2; j >= 0; j--) {
+    const int nch = L - 1 - j;
+    const int hs = lv.h[j + 1], ws2 = lv.w[j + 1], wd = lv.w[j], hd = lv.h[j];
+    float* mid = chain + pl.mid_off[j];
+    // x pass: per channel, lines = rows (hs), n = ws2 -> m = wd
+    tr_tconv_fwd_kernel<<<dim3(blocks_for((int64_t)hs * wd), nch), TB, 0, s>>>(
+        Tj(j + 1), mid, hs, ws2, wd, ws2, 1, wd, 1, K, koff, (int64_t)hs * ws2, (int64_t)hs * wd);
+    // y pass: per channel, lines = columns (wd), n = hs -> m = hd, into T_j channels 1..
+    tr_tconv_fwd_kernel<<<dim3(blocks_for((int64_t)wd * hd), nch), TB, 0, s>>>(
+        mid, Tj(j) + (int64_t)hd * wd, wd, hs, hd, 1, wd, 1, wd, K, koff, (int64_t)hs * wd, (int64_t)hd * wd);
+    launches += 2;
   }
   // 4. synthesis forward, distortion, synthesis adjoint
   float* u1 = F(pl.o_u1);
   float* us = F(pl.o_us);
   float* hsb = F(pl.o_hs);
-  tr_syn1x1_fwd_kernel<<<blocks_for(P), TB, 0, s>>>(sd, dense, u1, us, hsb);
+  const TrSynEntry* se = find_tr_syn(d);
+  if (!se) return -4;
+  se->fwd(blocks_for(P), TB, s, sd, dense, u1, us, hsb);
   launches++;
   for (int r = 0; r < R; r++) {
     tr_conv_fwd_kernel<<<blocks_for(P), TB, 0, s>>>(sd, r, hsb + (int64_t)r * 3 * P, us + (int64_t)(r + 1) * 3 * P,
@@ -818,8 +896,8 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
     tr_conv_bwd_kernel<<<(int)pl.p_blocks, TB, 0, s>>>(sd, r, hsb + (int64_t)r * 3 * P, us + (int64_t)(r + 1) * 3 * P,
                                                      gh, gh2, cpart);
     launches++;
-    tr_reduce_kernel<<<84, TB, 0, s>>>(cpart, pl.p_blocks, 84, 84, g_syn + (sd.oG - sd.oA0) + 84 * r, 0);
-    launches++;
+    launches += reduce_partials(cpart, pl.p_blocks, 84, 84, g_syn + (sd.oG - sd.oA0) + 84 * r,
+                                (double*)(W + pl.o_grad_tmp), s);
     float* t = gh;
     gh = gh2;
     gh2 = t;
@@ -828,56 +906,43 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
     const int n_w = L * CH + CH + 3 * CH + 3;
     const int vec = 3 + 2 * CH + L;
     const size_t smem = sizeof(float) * (size_t)TS_THREADS * (vec + 1);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(tr_syn1x1_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      attr = true;
-    }
-    tr_syn1x1_bwd_kernel<<<(int)pl.s_blocks, TS_THREADS, smem, s>>>(sd, dense, u1, us, gh, F(pl.o_gdense),
-                                                                    F(pl.o_spart), n_w);
+    se->bwd((int)pl.s_blocks, TS_THREADS, smem, s, sd, dense, u1, us, gh, F(pl.o_gdense), F(pl.o_spart), n_w);
     launches++;
-    tr_reduce_kernel<<<n_w < 1024 ? n_w : 1024, TB, 0, s>>>(F(pl.o_spart), pl.s_blocks, n_w, n_w, g_syn, 0);
-    launches++;
+    launches += reduce_partials(F(pl.o_spart), pl.s_blocks, n_w, n_w, g_syn, (double*)(W + pl.o_grad_tmp), s);
   }
-  // 5. upsampling adjoint: grad of y_hat_l (l >= 1) += T^T ... T^T gdense[l]; taps
+  // 5. upsampling adjoint on the stacks: gT_0 = gdense; gy_hat_j += gT_j[0];
+  //    gT_{j+1} = Up^T(gT_j[1..]) (y adjoint then x adjoint), tap partials
   float* gdense = F(pl.o_gdense);
-  // channel 0 goes straight to the level-0 latents
-  {
-    // g_lat[0 .. P) += gdense[0]: reuse the proxy kernel as an axpy-free add
-    // (y + u form: out = a + b)
-    tr_proxy_kernel<<<blocks_for(P), TB, 0, s>>>(g_lat, gdense, g_lat, P);
-    launches++;
-  }
   float* kpart = F(pl.o_kpart);
   int64_t krow = 0;
-  for (int l = 1; l < L; l++) {
-    const float* gcur = gdense + (int64_t)l * P;
-    for (int j = 0; j < l; j++) {
-      const int hs = lv.h[j + 1], ws2 = lv.w[j + 1], wd = lv.w[j], hd = lv.h[j];
-      const float* mid = chain + pl.mid_off[l * CC_MAX_LEVELS + j];
-      const float* gin = (j == l - 1) ? F(pl.o_yq) + lv.off[l] : chain + pl.chain_off[l * CC_MAX_LEVELS + (j + 1)];
-      float* gmid = F(pl.o_g1);   // gcur (gdense or o_g0) -> gmid -> gprev (o_g0: gcur is consumed)
-      float* gprev = F(pl.o_g0);
-      // the y pass's adjoint: lines = columns (wd), inputs mid (n = hs), outputs gcur (m = hd)
-      const int64_t b1 = blocks_for((int64_t)wd * hs);
-      tr_tconv_bwd_kernel<<<(int)b1, TB, 0, s>>>(mid, gcur, gmid, wd, hs, hd, 1, wd, 1, wd, K, koff,
-                                                 kpart + krow * K);
-      krow += b1;
-      // the x pass's adjoint: lines = rows (hs), inputs gin (n = ws2), outputs gmid (m = wd)
-      const int64_t b2 = blocks_for((int64_t)hs * ws2);
-      tr_tconv_bwd_kernel<<<(int)b2, TB, 0, s>>>(gin, gmid, gprev, hs, ws2, wd, ws2, 1, wd, 1, K, koff,
-                                                 kpart + krow * K);
-      krow += b2;
-      launches += 2;
-      gcur = gprev;
-    }
-    tr_proxy_kernel<<<blocks_for((int64_t)lv.h[l] * lv.w[l]), TB, 0, s>>>(g_lat + lv.off[l], gcur, g_lat + lv.off[l],
-                                                                        (int64_t)lv.h[l] * lv.w[l]);
+  const float* gT = gdense;
+  for (int j = 0; j < L; j++) {
+    tr_proxy_kernel<<<blocks_for((int64_t)lv.h[j] * lv.w[j]), TB, 0, s>>>(g_lat + lv.off[j], gT, g_lat + lv.off[j],
+                                                                        (int64_t)lv.h[j] * lv.w[j]);
     launches++;
+    if (j + 1 >= L) break;
+    const int nch = L - 1 - j;
+    const int hs = lv.h[j + 1], ws2 = lv.w[j + 1], wd = lv.w[j], hd = lv.h[j];
+    const float* mid = chain + pl.mid_off[j];
+    float* gmid = F(pl.o_g1);
+    float* gnext = (gT == F(pl.o_g0)) ? F(pl.o_g1) + (int64_t)nch * hs * wd : F(pl.o_g0);  // not aliasing gT / gmid
+    // y adjoint: inputs mid (per channel: lines = columns wd, n = hs), outputs gT_j[1..] (m = hd)
+    const int64_t b1 = blocks_for((int64_t)wd * hs);
+    tr_tconv_bwd_kernel<<<dim3((unsigned)b1, nch), TB, 0, s>>>(mid, gT + (int64_t)hd * wd, gmid, wd, hs, hd, 1, wd, 1,
+                                                               wd, K, koff, kpart + krow * K, (int64_t)hs * wd,
+                                                               (int64_t)hd * wd);
+    krow += b1 * nch;
+    // x adjoint: inputs T_{j+1} (lines = rows hs, n = ws2), outputs gmid (m = wd)
+    const int64_t b2 = blocks_for((int64_t)hs * ws2);
+    tr_tconv_bwd_kernel<<<dim3((unsigned)b2, nch), TB, 0, s>>>(Tj(j + 1), gmid, gnext, hs, ws2, wd, ws2, 1, wd, 1, K,
+                                                               koff, kpart + krow * K, (int64_t)hs * ws2,
+                                                               (int64_t)hs * wd);
+    krow += b2 * nch;
+    launches += 2;
+    gT = gnext;
   }
   if (krow > 0) {
-    tr_reduce_kernel<<<K, TB, 0, s>>>(kpart, krow, K, K, g_up, 0);
-    launches++;
+    launches += reduce_partials(kpart, krow, K, K, g_up, (double*)(W + pl.o_grad_tmp), s);
   } else {
     cudaMemsetAsync(g_up, 0, sizeof(float) * (size_t)K, s);
   }
