@@ -43,6 +43,8 @@ __constant__ float c_tw[TR_MAX_W];
 constexpr int TA_THREADS = 128;  // ARM: latents per CTA
 constexpr int TS_THREADS = 128;  // synthesis 1x1 backward: pixels per CTA
 constexpr int TB = 256;          // generic elementwise / stencil kernels
+constexpr int TR_GRID_CAP = 592; // grid-stride reductions: 4 CTAs per SM
+constexpr int TR_TCONV_CAP = 64; // transposed-conv adjoint: blocks per channel
 
 struct TrainLevels {
   int32_t L, H, W;
@@ -107,14 +109,35 @@ __device__ __forceinline__ float tr_bits(float y, float mu, float s, const Train
   return bits;
 }
 
+// Shared-memory record of one latent for the weight-gradient outer products:
+// per layer k the input [z_k, 1, 0 ...] (KIN[k] = round4(nin + 1) floats) and
+// the output gradient du_k (nout floats, even); 16-byte aligned.
+template <int C, int NH, int NHL>
+struct TrArmLayout {
+  static constexpr int NL = NHL + 1;
+  __host__ __device__ static constexpr int r4(int x) { return (x + 3) / 4 * 4; }
+  __host__ __device__ static constexpr int kin(int k) { return r4((k == 0 ? C : NH) + 1); }
+  __host__ __device__ static constexpr int nout(int k) { return k == NL - 1 ? 2 : NH; }
+  __host__ __device__ static constexpr int zoff(int k) { return k == 0 ? 0 : zoff(k - 1) + kin(k - 1); }
+  __host__ __device__ static constexpr int zend() { return zoff(NL - 1) + kin(NL - 1); }
+  __host__ __device__ static constexpr int doff(int k) { return k == 0 ? zend() : doff(k - 1) + r4(nout(k - 1)); }
+  __host__ __device__ static constexpr int woff(int k) {
+    return k == 0 ? 0 : woff(k - 1) + (k - 1 == 0 ? C : NH) * nout(k - 1) + nout(k - 1);
+  }
+  static constexpr int VEC_RAW = doff(NL - 1) + r4(2);
+  static constexpr int VEC = VEC_RAW + ((VEC_RAW / 4) % 2 == 0 ? 4 : 0);  // odd number of 16-byte words: bank spread
+  static_assert(NL <= 4, "up to 3 hidden layers");
+};
+
 template <int C, int NH, int NHL>
 __global__ void __launch_bounds__(TA_THREADS) tr_arm_kernel(const __grid_constant__ TrainArmParams p) {
   // per latent, in shared memory for the weight-gradient outer products:
   //   layer k input z_k (C or NH) and output gradient du_k (NH, or 2 for the last)
   constexpr int NL = NHL + 1;  // linear layers
-  constexpr int VEC = C + (NL - 1) * NH /* inputs of layers 1.. */ + (NL - 1) * NH /* du of hidden layers */ + 2;
-  extern __shared__ float tsm[];
-  float* vec = tsm + threadIdx.x * (VEC + 1);  // +1: bank spread
+  using LY = TrArmLayout<C, NH, NHL>;
+  constexpr int VEC = LY::VEC;
+  extern __shared__ __align__(16) float tsm[];
+  float* vec = tsm + threadIdx.x * VEC;
   const int64_t q = blockIdx.x * (int64_t)TA_THREADS + threadIdx.x;
   const bool valid = q < p.lv.n_lat;
   float bits = 0.0f;
@@ -163,19 +186,15 @@ __global__ void __launch_bounds__(TA_THREADS) tr_arm_kernel(const __grid_constan
     float du[NH > 2 ? NH : 2];
     du[0] = p.w_r * gmu;
     du[1] = p.w_r * gs;
-    // stash the layer inputs and output gradients
-    int vo = 0;
+    // stash the layer inputs [z_k, 1, 0 pad] and output gradients du_k
 #pragma unroll
-    for (int c = 0; c < C; c++) vec[vo + c] = z[0][c];
-    vo += C;
+    for (int k = 0; k < NL; k++) {
+      const int nin = (k == 0) ? C : NH;
 #pragma unroll
-    for (int k = 1; k < NL; k++)
-#pragma unroll
-      for (int n = 0; n < NH; n++) vec[vo + (k - 1) * NH + n] = z[k][n];
-    vo += (NL - 1) * NH;
-    const int du_base = vo;  // du of layer k (k < NL-1) at du_base + k*NH; last layer at du_base + (NL-1)*NH
-    vec[du_base + (NL - 1) * NH + 0] = du[0];
-    vec[du_base + (NL - 1) * NH + 1] = du[1];
+      for (int t2 = 0; t2 < LY::kin(k); t2++) vec[LY::zoff(k) + t2] = t2 < nin ? z[k][t2] : (t2 == nin ? 1.0f : 0.0f);
+    }
+    vec[LY::doff(NL - 1) + 0] = du[0];
+    vec[LY::doff(NL - 1) + 1] = du[1];
     int offk[NL];
     {
       int o2 = 0;
@@ -202,7 +221,7 @@ __global__ void __launch_bounds__(TA_THREADS) tr_arm_kernel(const __grid_constan
 #pragma unroll
         for (int n = 0; n < NH; n++) {
           du[n] = u[k - 1][n] > 0.0f ? dz[n] : 0.0f;
-          vec[du_base + (k - 1) * NH + n] = du[n];
+          vec[LY::doff(k - 1) + n] = du[n];
         }
       } else {
 #pragma unroll
@@ -217,34 +236,40 @@ __global__ void __launch_bounds__(TA_THREADS) tr_arm_kernel(const __grid_constan
   for (int o2 = 16; o2 > 0; o2 >>= 1) bits += __shfl_xor_sync(0xffffffffu, bits, o2);
   if ((threadIdx.x & 31) == 0) p.rate[blockIdx.x * (TA_THREADS / 32) + (threadIdx.x >> 5)] = (double)bits;
   __syncthreads();
-  // per-CTA weight gradients: entry e of layer k = sum over the CTA's latents of
-  // du_k[o] z_k[i] (weights) or du_k[o] (biases)
-  for (int e = threadIdx.x; e < p.n_arm; e += TA_THREADS) {
-    int k = 0, base = 0, rem = e;
-    int nin = C, nout = (NL == 1) ? 2 : NH;
-    while (true) {
-      nin = (k == 0) ? C : NH;
-      nout = (k == NL - 1) ? 2 : NH;
-      if (rem < nin * nout + nout) break;
-      rem -= nin * nout + nout;
-      base += nin * nout + nout;
-      k++;
-    }
-    (void)base;
-    const int zoff = (k == 0) ? 0 : C + (k - 1) * NH;
-    const int duoff = C + (NL - 1) * NH + k * NH;
-    float acc = 0.0f;
-    if (rem < nin * nout) {
-      const int o = rem / nin, i2 = rem - o * nin;
+  // per-CTA weight gradients, layer by layer, as register-blocked outer
+  // products over the CTA's latents: a thread owns a 2 (outputs) x 4 (inputs,
+  // the last input column being the constant 1 = the bias) tile, reading per
+  // latent one float2 of du and one float4 of z
+  int tile = threadIdx.x;
+#pragma unroll 1
+  for (int k = 0; k < NL; k++) {
+    const int nin = (k == 0) ? C : NH, nout = (k == NL - 1) ? 2 : NH;
+    const int tcols = LY::kin(k) / 4, trows = nout / 2, ntile = tcols * trows;
+    const int wbase = LY::woff(k);
+    for (; tile < ntile; tile += TA_THREADS) {
+      const int tr = tile / tcols, tc = tile - tr * tcols;
+      float acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+#pragma unroll 4
       for (int m = 0; m < TA_THREADS; m++) {
-        const float* v = tsm + m * (VEC + 1);
-        acc = fmaf(v[duoff + o], v[zoff + i2], acc);
+        const float* v = tsm + m * VEC;
+        const float2 dd = *reinterpret_cast<const float2*>(v + LY::doff(k) + 2 * tr);
+        const float4 zz = *reinterpret_cast<const float4*>(v + LY::zoff(k) + 4 * tc);
+        const float dv[2] = {dd.x, dd.y}, zv[4] = {zz.x, zz.y, zz.z, zz.w};
+#pragma unroll
+        for (int a = 0; a < 2; a++)
+#pragma unroll
+          for (int b = 0; b < 4; b++) acc[a][b] = fmaf(dv[a], zv[b], acc[a][b]);
       }
-    } else {
-      const int o = rem - nin * nout;
-      for (int m = 0; m < TA_THREADS; m++) acc += tsm[m * (VEC + 1) + duoff + o];
+#pragma unroll
+      for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+          const int o = 2 * tr + a, i2 = 4 * tc + b;
+          if (i2 < nin) p.wpart[(int64_t)blockIdx.x * p.n_arm + wbase + o * nin + i2] = acc[a][b];  // W[o][i]
+          else if (i2 == nin) p.wpart[(int64_t)blockIdx.x * p.n_arm + wbase + nin * nout + o] = acc[a][b];  // b[o]
+        }
     }
-    p.wpart[(int64_t)blockIdx.x * p.n_arm + e] = acc;
+    tile -= ntile;
   }
 }
 
@@ -283,7 +308,16 @@ __global__ void tr_tconv_fwd_kernel(const float* __restrict__ g, float* __restri
   if (idx >= (int64_t)lines * m) return;
   g += blockIdx.y * g_cs;  // channel
   out += blockIdx.y * o_cs;
-  const int line = (int)(idx / m), o = (int)(idx - (int64_t)line * m);
+  // consecutive threads on consecutive addresses: along the line when its
+  // elements are contiguous (x pass), across lines otherwise (y pass: columns)
+  int line, o;
+  if (g_es == 1) {
+    line = (int)(idx / m);
+    o = (int)(idx - (int64_t)line * m);
+  } else {
+    o = (int)(idx / lines);
+    line = (int)(idx - (int64_t)o * lines);
+  }
   const int q = o >> 1, r = o & 1;
   float acc = 0.0f;
   for (int t = 0; t < K / 2; t++)
@@ -298,14 +332,21 @@ __global__ void tr_tconv_bwd_kernel(const float* __restrict__ g, const float* __
                                     int lines, int n, int m, int64_t g_ls, int64_t g_es, int64_t o_ls, int64_t o_es,
                                     int K, int koff, float* __restrict__ kpart, int64_t g_cs, int64_t o_cs) {
   __shared__ float red[8][TB / 32];
-  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   g += blockIdx.y * g_cs;  // channel (gg shares g's layout)
   gg += blockIdx.y * g_cs;
   gout += blockIdx.y * o_cs;
   kpart += (int64_t)blockIdx.y * gridDim.x * K;
   float dk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (idx < (int64_t)lines * n) {
-    const int line = (int)(idx / n), s = (int)(idx - (int64_t)line * n);
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)lines * n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int line, s;  // coalesced mapping (see tr_tconv_fwd_kernel)
+    if (g_es == 1) {
+      line = (int)(idx / n);
+      s = (int)(idx - (int64_t)line * n);
+    } else {
+      s = (int)(idx / lines);
+      line = (int)(idx - (int64_t)s * lines);
+    }
     const int E = K / 4, P = K / 2 - 1 + 2 * E;
     const float xs = g[line * g_ls + (int64_t)s * g_es];
     const int i_lo = (s == 0) ? 0 : s + E, i_hi = (s == n - 1) ? n - 1 + 2 * E : s + E;  // extended positions
@@ -417,13 +458,12 @@ __global__ void tr_loss_kernel(TrainSynDims d, const float* __restrict__ xh, con
 __global__ void tr_conv_bwd_kernel(TrainSynDims d, int r, const float* __restrict__ hin, const float* __restrict__ us,
                                    const float* __restrict__ gh, float* __restrict__ gin, float* __restrict__ gpart) {
   __shared__ float red[84][TB / 32];
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int oG = d.oG + 84 * r;
   const bool relu = r < d.R - 1;
   float dG[84];
 #pragma unroll
   for (int e = 0; e < 84; e++) dG[e] = 0.0f;
-  if (p < d.P) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < d.P; p += (int64_t)gridDim.x * blockDim.x) {
     const int y = (int)(p / d.W), x = (int)(p - (int64_t)y * d.W);
     auto gpre = [&](int c, int64_t q) {
       const float v = gh[c * d.P + q];
@@ -432,13 +472,18 @@ __global__ void tr_conv_bwd_kernel(TrainSynDims d, int r, const float* __restric
     float gp[3];
     for (int co = 0; co < 3; co++) gp[co] = gpre(co, p);
     // weight / bias gradients from this output position
+#pragma unroll
     for (int co = 0; co < 3; co++) {
-      dG[81 + co] = gp[co];
+      dG[81 + co] += gp[co];
+#pragma unroll
       for (int ci = 0; ci < 3; ci++)
+#pragma unroll
         for (int ky = 0; ky < 3; ky++)
+#pragma unroll
           for (int kx = 0; kx < 3; kx++)
-            dG[((co * 3 + ci) * 3 + ky) * 3 + kx] =
-                gp[co] * hin[ci * d.P + (int64_t)clampi(y + ky - 1, 0, d.H - 1) * d.W + clampi(x + kx - 1, 0, d.W - 1)];
+            dG[((co * 3 + ci) * 3 + ky) * 3 + kx] = fmaf(
+                gp[co], hin[ci * d.P + (int64_t)clampi(y + ky - 1, 0, d.H - 1) * d.W + clampi(x + kx - 1, 0, d.W - 1)],
+                dG[((co * 3 + ci) * 3 + ky) * 3 + kx]);
     }
     // input gradient: every output q and tap whose clamped source is p
     const bool interior = y >= 1 && y <= d.H - 2 && x >= 1 && x <= d.W - 2;
@@ -460,6 +505,7 @@ __global__ void tr_conv_bwd_kernel(TrainSynDims d, int r, const float* __restric
       gin[ci * d.P + p] = a;
     }
   }
+#pragma unroll
   for (int e = 0; e < 84; e++) {
     float v = dG[e];
 #pragma unroll
@@ -641,7 +687,7 @@ static void make_plan(const cc_model_desc& d, TrainPlan& pl) {
   pl.n_par = lv.n_lat + pl.n_arm + pl.n_up + pl.n_syn;
   const int64_t P = (int64_t)d.H * d.W;
   pl.arm_ctas = (lv.n_lat + TA_THREADS - 1) / TA_THREADS;
-  pl.p_blocks = (P + TB - 1) / TB;
+  pl.p_blocks = (P + TB - 1) / TB < TR_GRID_CAP ? (P + TB - 1) / TB : TR_GRID_CAP;  // grid-stride conv adjoint
   pl.s_blocks = (P + TS_THREADS - 1) / TS_THREADS;
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -668,7 +714,8 @@ static void make_plan(const cc_model_desc& d, TrainPlan& pl) {
     const int nch = d.L - 1 - j;
     pl.mid_off[j] = c;
     c += (int64_t)nch * lv.h[j + 1] * lv.w[j];
-    kp += (int64_t)nch * (((int64_t)lv.h[j + 1] * lv.w[j] + TB - 1) / TB + ((int64_t)lv.h[j + 1] * lv.w[j + 1] + TB - 1) / TB);
+    auto capb = [](int64_t n) { const int64_t b = (n + TB - 1) / TB; return b < TR_TCONV_CAP ? b : (int64_t)TR_TCONV_CAP; };
+    kp += (int64_t)nch * (capb((int64_t)lv.h[j + 1] * lv.w[j]) + capb((int64_t)lv.h[j + 1] * lv.w[j + 1]));
   }
   pl.kpart_rows = kp > 0 ? kp : 1;
   pl.o_chain = take(4 * (c > 0 ? c : 1));
@@ -713,10 +760,11 @@ static void tr_arm_launch(dim3 g, int t, size_t smem, cudaStream_t s, const Trai
 struct TrArmEntry {
   int C, NH, NHL;
   TrArmFn fn;
+  int vec;  // floats per latent record in shared memory
 };
+#define TR_ARM(C, NH, NHL) {C, NH, NHL, tr_arm_launch<C, NH, NHL>, TrArmLayout<C, NH, NHL>::VEC}
 static const TrArmEntry kTrArm[] = {
-    {16, 24, 2, tr_arm_launch<16, 24, 2>}, {8, 8, 2, tr_arm_launch<8, 8, 2>}, {8, 8, 1, tr_arm_launch<8, 8, 1>},
-    {16, 16, 2, tr_arm_launch<16, 16, 2>}, {24, 24, 2, tr_arm_launch<24, 24, 2>},
+    TR_ARM(16, 24, 2), TR_ARM(8, 8, 2), TR_ARM(8, 8, 1), TR_ARM(16, 16, 2), TR_ARM(24, 24, 2),
 };
 
 typedef void (*TrSynFwdFn)(int, int, cudaStream_t, const TrainSynDims&, const float*, float*, float*, float*);
@@ -831,13 +879,11 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
     ap.wpart = F(pl.o_wpart_arm);
     ap.n_arm = (int)pl.n_arm;
     const int C = d.n_ctx, NH = d.arm_widths[1], NL = d.arm_n_layers;
-    const int vec = C + (NL - 1) * NH * 2 + 2;
-    const size_t smem = sizeof(float) * (size_t)TA_THREADS * (vec + 1);
-    TrArmFn fn = nullptr;
+    const TrArmEntry* ae = nullptr;
     for (const auto& e : kTrArm)
-      if (e.C == C && e.NH == NH && e.NHL == NL - 1) fn = e.fn;
-    if (!fn) return -3;
-    fn(dim3((unsigned)pl.arm_ctas), TA_THREADS, smem, s, ap);
+      if (e.C == C && e.NH == NH && e.NHL == NL - 1) ae = &e;
+    if (!ae) return -3;
+    ae->fn(dim3((unsigned)pl.arm_ctas), TA_THREADS, sizeof(float) * (size_t)TA_THREADS * ae->vec, s, ap);
     launches++;
   }
   {
@@ -927,13 +973,13 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
     float* gmid = F(pl.o_g1);
     float* gnext = (gT == F(pl.o_g0)) ? F(pl.o_g1) + (int64_t)nch * hs * wd : F(pl.o_g0);  // not aliasing gT / gmid
     // y adjoint: inputs mid (per channel: lines = columns wd, n = hs), outputs gT_j[1..] (m = hd)
-    const int64_t b1 = blocks_for((int64_t)wd * hs);
+    const int64_t b1 = blocks_for((int64_t)wd * hs) < TR_TCONV_CAP ? blocks_for((int64_t)wd * hs) : TR_TCONV_CAP;
     tr_tconv_bwd_kernel<<<dim3((unsigned)b1, nch), TB, 0, s>>>(mid, gT + (int64_t)hd * wd, gmid, wd, hs, hd, 1, wd, 1,
                                                                wd, K, koff, kpart + krow * K, (int64_t)hs * wd,
                                                                (int64_t)hd * wd);
     krow += b1 * nch;
     // x adjoint: inputs T_{j+1} (lines = rows hs, n = ws2), outputs gmid (m = wd)
-    const int64_t b2 = blocks_for((int64_t)hs * ws2);
+    const int64_t b2 = blocks_for((int64_t)hs * ws2) < TR_TCONV_CAP ? blocks_for((int64_t)hs * ws2) : TR_TCONV_CAP;
     tr_tconv_bwd_kernel<<<dim3((unsigned)b2, nch), TB, 0, s>>>(Tj(j + 1), gmid, gnext, hs, ws2, wd, ws2, 1, wd, 1, K,
                                                                koff, kpart + krow * K, (int64_t)hs * ws2,
                                                                (int64_t)hs * wd);
