@@ -456,8 +456,16 @@ static int side_stream(SideStream** out) {
   return CC_OK;
 }
 
-// whole path for images [0, n): pyramid (side stream) || ARM, then synthesis;
-// per-image workspace slices of `per` bytes
+// ARM || (pyramid -> synthesis) on two streams (default, measured +10 % on
+// the batched 2K workload); CCRD_SERIAL=1 runs everything on the caller's
+// stream (per-kernel timing; read at every call)
+static bool concurrent_streams() {
+  const char* e = getenv("CCRD_SERIAL");
+  return !(e && strcmp(e, "1") == 0);
+}
+
+// whole path for images [0, n): pyramid -> synthesis on a side stream || ARM
+// (or all serial); per-image workspace slices of `per` bytes
 static int forward_batch(const cc_model_desc& d, const cc_strip* win, const int16_t* const* lat,
                          const float* const* arm_w, const float* const* up_w, const float* const* syn_w,
                          const float* const* image, float* const* x_hat, char* slices, size_t per, int n,
@@ -500,19 +508,32 @@ static int forward_batch(const cc_model_desc& d, const cc_strip* win, const int1
   PyrImage imgs[MAX_JOBS_PER_LAUNCH];
   for (int i = 0; i < n; i++)
     imgs[i] = pyr_image(d, lat[i], up_w[i], slice_pyr(d, win, slices + per * (size_t)i));
-  SideStream* side = nullptr;
-  if (overlap && pg.L >= 3) {
+  if (overlap) {
+    // concurrent: the ARM kernels on `s`, the pyramid + synthesis kernels on a
+    // side stream (they do not depend on the ARM); an SM holds one ARM CTA
+    // (FMA-bound) next to one synthesis CTA (latency phases), so each fills
+    // the other's gaps.  Joined before the caller's next work on `s`.
+    SideStream* side = nullptr;
     if ((rc = side_stream(&side))) return rc;
     cudaEventRecord(side->fork, s);
     cudaStreamWaitEvent(side->s, side->fork, 0);
     if ((rc = pyr_many(d, win, imgs, n, side->s))) return rc;
+    for (int i = 0; i < n; i++) {
+      char* sl = slices + per * (size_t)i;
+      const float* s1 = slice_pyr(d, win, sl) + pg.s_off[1];
+      if ((rc = syn_one(d, win, lat[i], s1, up_w[i], syn_w[i], image[i], x_hat[i], nullptr, (double*)sl + n_arm,
+                        side->s)))
+        return rc;
+    }
     cudaEventRecord(side->join, side->s);
-  } else if ((rc = pyr_many(d, win, imgs, n, s))) {
-    return rc;
+    for (int i = 0; i < n; i++)
+      if ((rc = arm_one(d, win, lat[i], arm_w[i], (double*)(slices + per * (size_t)i), s))) return rc;
+    cudaStreamWaitEvent(s, side->join, 0);
+    return CC_OK;
   }
+  if ((rc = pyr_many(d, win, imgs, n, s))) return rc;
   for (int i = 0; i < n; i++)
     if ((rc = arm_one(d, win, lat[i], arm_w[i], (double*)(slices + per * (size_t)i), s))) return rc;
-  if (side) cudaStreamWaitEvent(s, side->join, 0);
   for (int i = 0; i < n; i++) {
     char* sl = slices + per * (size_t)i;
     const float* s1 = slice_pyr(d, win, sl) + pg.s_off[1];
@@ -613,7 +634,8 @@ int cc_rd_forward(const cc_model_desc* desc, const cc_image_io* io, int32_t n_im
       xh[i] = x.x_hat;
       jobs[i] = make_job(*desc, nullptr, (double*)(slices + per * (size_t)(b + i)));
     }
-    rc = forward_batch(*desc, nullptr, lat, aw, uw, sw, img, xh, slices + per * (size_t)b, per, m, s, false);
+    rc = forward_batch(*desc, nullptr, lat, aw, uw, sw, img, xh, slices + per * (size_t)b, per, m, s,
+                       concurrent_streams());
     if (rc) return rc;
     rc = launch_reduce(jobs, m, results + b, s);
     if (rc) return rc;
