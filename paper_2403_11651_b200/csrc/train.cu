@@ -237,39 +237,77 @@ __global__ void __launch_bounds__(TA_THREADS) tr_arm_kernel(const __grid_constan
   if ((threadIdx.x & 31) == 0) p.rate[blockIdx.x * (TA_THREADS / 32) + (threadIdx.x >> 5)] = (double)bits;
   __syncthreads();
   // per-CTA weight gradients, layer by layer, as register-blocked outer
-  // products over the CTA's latents: a thread owns a 2 (outputs) x 4 (inputs,
-  // the last input column being the constant 1 = the bias) tile, reading per
-  // latent one float2 of du and one float4 of z
+  // products over the CTA's latents: a thread owns a TH (outputs) x 4 (inputs,
+  // the last input column being the constant 1 = the bias) tile with two
+  // interleaved partial sums (2 x TH x 4 independent FMA chains), reading per
+  // latent one float4 (or float2) of du and one float4 of z
   int tile = threadIdx.x;
 #pragma unroll 1
   for (int k = 0; k < NL; k++) {
     const int nin = (k == 0) ? C : NH, nout = (k == NL - 1) ? 2 : NH;
-    const int tcols = LY::kin(k) / 4, trows = nout / 2, ntile = tcols * trows;
+    const int tcols = LY::kin(k) / 4;
     const int wbase = LY::woff(k);
-    for (; tile < ntile; tile += TA_THREADS) {
-      const int tr = tile / tcols, tc = tile - tr * tcols;
-      float acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
-#pragma unroll 4
-      for (int m = 0; m < TA_THREADS; m++) {
-        const float* v = tsm + m * VEC;
-        const float2 dd = *reinterpret_cast<const float2*>(v + LY::doff(k) + 2 * tr);
-        const float4 zz = *reinterpret_cast<const float4*>(v + LY::zoff(k) + 4 * tc);
-        const float dv[2] = {dd.x, dd.y}, zv[4] = {zz.x, zz.y, zz.z, zz.w};
+    if (nout % 4 == 0) {
+      const int trows = nout / 4, ntile = tcols * trows;
+      for (; tile < ntile; tile += TA_THREADS) {
+        const int tr = tile / tcols, tc = tile - tr * tcols;
+        float acc[2][4][4] = {};
+#pragma unroll 2
+        for (int m = 0; m < TA_THREADS; m += 2) {
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const float* v = tsm + (m + h) * VEC;
+            const float4 dd = *reinterpret_cast<const float4*>(v + LY::doff(k) + 4 * tr);
+            const float4 zz = *reinterpret_cast<const float4*>(v + LY::zoff(k) + 4 * tc);
+            const float dv[4] = {dd.x, dd.y, dd.z, dd.w}, zv[4] = {zz.x, zz.y, zz.z, zz.w};
+#pragma unroll
+            for (int a = 0; a < 4; a++)
+#pragma unroll
+              for (int b = 0; b < 4; b++) acc[h][a][b] = fmaf(dv[a], zv[b], acc[h][a][b]);
+          }
+        }
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+#pragma unroll
+          for (int b = 0; b < 4; b++) {
+            const int o = 4 * tr + a, i2 = 4 * tc + b;
+            const float v2 = acc[0][a][b] + acc[1][a][b];
+            if (i2 < nin) p.wpart[(int64_t)blockIdx.x * p.n_arm + wbase + o * nin + i2] = v2;  // W[o][i]
+            else if (i2 == nin) p.wpart[(int64_t)blockIdx.x * p.n_arm + wbase + nin * nout + o] = v2;  // b[o]
+          }
+      }
+      tile -= ntile;
+    } else {  // the 2-wide output layer
+      const int trows = nout / 2, ntile = tcols * trows;
+      for (; tile < ntile; tile += TA_THREADS) {
+        const int tr = tile / tcols, tc = tile - tr * tcols;
+        float acc[2][2][4] = {};
+#pragma unroll 2
+        for (int m = 0; m < TA_THREADS; m += 2) {
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const float* v = tsm + (m + h) * VEC;
+            const float2 dd = *reinterpret_cast<const float2*>(v + LY::doff(k) + 2 * tr);
+            const float4 zz = *reinterpret_cast<const float4*>(v + LY::zoff(k) + 4 * tc);
+            const float dv[2] = {dd.x, dd.y}, zv[4] = {zz.x, zz.y, zz.z, zz.w};
+#pragma unroll
+            for (int a = 0; a < 2; a++)
+#pragma unroll
+              for (int b = 0; b < 4; b++) acc[h][a][b] = fmaf(dv[a], zv[b], acc[h][a][b]);
+          }
+        }
 #pragma unroll
         for (int a = 0; a < 2; a++)
 #pragma unroll
-          for (int b = 0; b < 4; b++) acc[a][b] = fmaf(dv[a], zv[b], acc[a][b]);
+          for (int b = 0; b < 4; b++) {
+            const int o = 2 * tr + a, i2 = 4 * tc + b;
+            const float v2 = acc[0][a][b] + acc[1][a][b];
+            if (i2 < nin) p.wpart[(int64_t)blockIdx.x * p.n_arm + wbase + o * nin + i2] = v2;
+            else if (i2 == nin) p.wpart[(int64_t)blockIdx.x * p.n_arm + wbase + nin * nout + o] = v2;
+          }
       }
-#pragma unroll
-      for (int a = 0; a < 2; a++)
-#pragma unroll
-        for (int b = 0; b < 4; b++) {
-          const int o = 2 * tr + a, i2 = 4 * tc + b;
-          if (i2 < nin) p.wpart[(int64_t)blockIdx.x * p.n_arm + wbase + o * nin + i2] = acc[a][b];  // W[o][i]
-          else if (i2 == nin) p.wpart[(int64_t)blockIdx.x * p.n_arm + wbase + nin * nout + o] = acc[a][b];  // b[o]
-        }
+      tile -= ntile;
     }
-    tile -= ntile;
   }
 }
 
