@@ -194,29 +194,40 @@ struct ChainStep {
 // then the inputs in order (the oracle's summation order).
 template <int L, int CH, int R, int K>
 __device__ __forceinline__ void mlp_pair(const SynParams<L, CH, R, K>& p, const uint64_t (&v)[L], uint64_t (&out)[3]) {
+  // hidden layer in chunks of MC neurons: fewer live accumulators (each chunk
+  // adds its contribution to the three output pairs), same FMA count and the
+  // same per-output summation order as one pass (bias, then hidden 0 .. CH-1)
+  constexpr int MC = (CH % 20 == 0 && CH > 20) ? 20 : CH;
   const uint64_t one = f2pack(1.0f, 1.0f);
-  uint64_t acc[CH];
+  uint64_t o[3];
 #pragma unroll
-  for (int n = 0; n < CH; n++) acc[n] = ffma2(one, f2pack(p.w.a0[n], p.w.a0[n]), 0ull);
+  for (int c = 0; c < 3; c++) o[c] = ffma2(one, f2pack(p.w.a1[c], p.w.a1[c]), 0ull);
 #pragma unroll
-  for (int i = 0; i < L; i++)
+  for (int n0 = 0; n0 < CH; n0 += MC) {
+    uint64_t acc[MC];
 #pragma unroll
-    for (int n = 0; n < CH; n++) acc[n] = ffma2(v[i], f2pack(p.w.A0t[i][n], p.w.A0t[i][n]), acc[n]);
+    for (int n = 0; n < MC; n++) acc[n] = ffma2(one, f2pack(p.w.a0[n0 + n], p.w.a0[n0 + n]), 0ull);
 #pragma unroll
-  for (int n = 0; n < CH; n++) {
-    const float2 h = f2unpack(acc[n]);
-    acc[n] = f2pack(fmaxf(h.x, 0.0f), fmaxf(h.y, 0.0f));
+    for (int i = 0; i < L; i++)
+#pragma unroll
+      for (int n = 0; n < MC; n++) acc[n] = ffma2(v[i], f2pack(p.w.A0t[i][n0 + n], p.w.A0t[i][n0 + n]), acc[n]);
+#pragma unroll
+    for (int n = 0; n < MC; n++) {
+      const float2 h = f2unpack(acc[n]);
+      acc[n] = f2pack(fmaxf(h.x, 0.0f), fmaxf(h.y, 0.0f));
+    }
+#pragma unroll
+    for (int c = 0; c < 3; c++)
+#pragma unroll
+      for (int n = 0; n < MC; n++) o[c] = ffma2(acc[n], f2pack(p.w.A1[c][n0 + n], p.w.A1[c][n0 + n]), o[c]);
   }
 #pragma unroll
   for (int c = 0; c < 3; c++) {
-    uint64_t o = ffma2(one, f2pack(p.w.a1[c], p.w.a1[c]), 0ull);
-#pragma unroll
-    for (int n = 0; n < CH; n++) o = ffma2(acc[n], f2pack(p.w.A1[c][n], p.w.A1[c][n]), o);
     if (R > 0) {
-      const float2 h = f2unpack(o);
-      o = f2pack(fmaxf(h.x, 0.0f), fmaxf(h.y, 0.0f));
+      const float2 h = f2unpack(o[c]);
+      o[c] = f2pack(fmaxf(h.x, 0.0f), fmaxf(h.y, 0.0f));
     }
-    out[c] = o;
+    out[c] = o[c];
   }
 }
 
