@@ -817,7 +817,8 @@ int cc_rd_forward_strip(const cc_model_desc* desc, const cc_strip* strip, const 
   const int16_t* l1[1] = {io->latents};
   const float *a1[1] = {io->arm_w}, *u1[1] = {io->up_w}, *s1[1] = {io->syn_w}, *i1[1] = {io->image};
   float* x1[1] = {io->x_hat};
-  if ((rc = forward_batch(d, strip, l1, a1, u1, s1, i1, x1, (char*)workspace, per, 1, s, false))) return rc;
+  if ((rc = forward_batch(d, strip, l1, a1, u1, s1, i1, x1, (char*)workspace, per, 1, s, concurrent_streams())))
+    return rc;
   ReduceJob j = make_job(d, strip, (double*)workspace);
   return launch_reduce(&j, 1, result, s);
 }

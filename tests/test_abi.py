@@ -130,3 +130,60 @@ def test_reference_config_mac_per_pixel():
     assert P.cc_mac_per_pixel(P.desc_from_config(workload.CONFIGS["ref"])).total == pytest.approx(1951.25, abs=0.01)
     assert P.cc_mac_per_pixel(P.desc_from_config(workload.CONFIGS["batched2k"])).total == pytest.approx(1951.68,
                                                                                                       abs=0.01)
+
+
+def _has_gpu():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def test_up_2d_validation_and_table1_configs():
+    for name in ("t300", "t545", "t1079", "t2300"):
+        assert P.cc_validate(P.desc_from_config(workload.CONFIGS[name])) == 0, name
+    d = P.desc_from_config(workload.CONFIGS["t300"])
+    d.up_2d = 2
+    assert P.cc_validate(d) == ccrd.CC_EINVAL
+
+
+def test_training_entry_errors_without_gpu():
+    cfg = workload.CONFIGS["ref"].replace(H=24, W=40)
+    d = P.desc_from_config(cfg)
+    n = P.cc_train_param_count(d)
+    assert n == cfg.n_latents + cfg.n_arm_w + cfg.n_up_w + cfg.n_syn_w
+    ws = P.cc_train_workspace_bytes(d)
+    assert ws > 0
+    with pytest.raises(ccrd.CcError) as e:           # workspace too small
+        P.cc_train_step(d, 8, 8, 8, 8, 8, P.CcAdam(1e-3, 0.9, 0.999, 1e-8, 1), 8, 8, 8, 16)
+    assert e.value.code == ccrd.CC_EWORKSPACE
+    with pytest.raises(ccrd.CcError) as e:           # Adam step 0
+        P.cc_train_step(d, 8, 8, 8, 8, 8, P.CcAdam(1e-3, 0.9, 0.999, 1e-8, 0), 8, 8, 8, ws)
+    assert e.value.code == ccrd.CC_EINVAL
+    d2 = P.desc_from_config(workload.CONFIGS["t2300"])     # 2-D TConv: not compiled for training
+    assert P.cc_train_workspace_bytes(d2) == 0
+    with pytest.raises(ccrd.CcError) as e:
+        P.cc_train_step(d2, 8, 8, 8, 8, 8, None, 8, 8, 8, 1 << 30)
+    assert e.value.code == ccrd.CC_ENOTSUP
+    if not _has_gpu():
+        with pytest.raises(ccrd.CcError) as e:       # no device: loud failure
+            P.cc_train_step(d, 8, 8, 8, 8, 8, None, 8, 8, 8, ws)
+        assert e.value.code == ccrd.CC_ECUDA
+
+
+def test_strip_entry_errors_without_gpu():
+    cfg = workload.CONFIGS["ref"]
+    d = P.desc_from_config(cfg)
+    st = P.cc_strip_window(d, 100, 300)
+    ws = P.cc_workspace_bytes_strip(d, st)
+    assert ws > 0 and P.cc_strip_latent_count(d, st) > 0
+    im = workload.make_image(cfg, 0)
+    io = P.CcImageIO(1, im.arm_w.ctypes.data, im.up_w.ctypes.data, im.syn_w.ctypes.data, 0, 0)
+    with pytest.raises(ccrd.CcError) as e:
+        P.cc_rd_forward_strip(d, st, io, 8, 8, 16)
+    assert e.value.code == ccrd.CC_EWORKSPACE
+    if not _has_gpu():
+        with pytest.raises(ccrd.CcError) as e:
+            P.cc_rd_forward_strip(d, st, io, 8, 8, ws)
+        assert e.value.code == ccrd.CC_ECUDA
