@@ -492,55 +492,84 @@ __global__ void tr_loss_kernel(TrainSynDims d, const float* __restrict__ xh, con
 
 // adjoint of residual layer r: gpre = gh (x) ReLU'(us) (not on the last layer);
 // gin = gpre (residual) + G^T-gather over the clamped neighbourhood;
-// dG[co][ci][ky][kx] = sum gpre[co](p) hin[ci](clamp(p + tap)), dg[co] = sum gpre[co]
-__global__ void tr_conv_bwd_kernel(TrainSynDims d, int r, const float* __restrict__ hin, const float* __restrict__ us,
-                                   const float* __restrict__ gh, float* __restrict__ gin, float* __restrict__ gpart) {
-  __shared__ float red[84][TB / 32];
+// dG[co][ci][ky][kx] = sum gpre[co](p) hin[ci](clamp(p + tap)), dg[co] = sum gpre[co].
+// Tiles of CT_Y x CT_X pixels (one per thread) with a 1-pixel halo of gpre and
+// hin staged in shared memory; persistent CTAs accumulate dG in registers over
+// their tiles and reduce once.
+constexpr int CT_Y = 8, CT_X = 32;
+__global__ void __launch_bounds__(CT_Y * CT_X)
+    tr_conv_bwd_kernel(TrainSynDims d, int r, const float* __restrict__ hin, const float* __restrict__ us,
+                       const float* __restrict__ gh, float* __restrict__ gin, float* __restrict__ gpart) {
+  constexpr int SY = CT_Y + 2, SX = CT_X + 2;
+  __shared__ float sg[3][SY][SX], sh[3][SY][SX];
+  __shared__ float red[84][CT_Y * CT_X / 32];
   const int oG = d.oG + 84 * r;
   const bool relu = r < d.R - 1;
+  const int tiles_x = (d.W + CT_X - 1) / CT_X, n_tiles = tiles_x * ((d.H + CT_Y - 1) / CT_Y);
+  const int ty = threadIdx.x / CT_X, tx = threadIdx.x - ty * CT_X;
   float dG[84];
 #pragma unroll
   for (int e = 0; e < 84; e++) dG[e] = 0.0f;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < d.P; p += (int64_t)gridDim.x * blockDim.x) {
-    const int y = (int)(p / d.W), x = (int)(p - (int64_t)y * d.W);
-    auto gpre = [&](int c, int64_t q) {
-      const float v = gh[c * d.P + q];
-      return (!relu || us[c * d.P + q] > 0.0f) ? v : 0.0f;
-    };
-    float gp[3];
-    for (int co = 0; co < 3; co++) gp[co] = gpre(co, p);
-    // weight / bias gradients from this output position
-#pragma unroll
-    for (int co = 0; co < 3; co++) {
-      dG[81 + co] += gp[co];
-#pragma unroll
-      for (int ci = 0; ci < 3; ci++)
-#pragma unroll
-        for (int ky = 0; ky < 3; ky++)
-#pragma unroll
-          for (int kx = 0; kx < 3; kx++)
-            dG[((co * 3 + ci) * 3 + ky) * 3 + kx] = fmaf(
-                gp[co], hin[ci * d.P + (int64_t)clampi(y + ky - 1, 0, d.H - 1) * d.W + clampi(x + kx - 1, 0, d.W - 1)],
-                dG[((co * 3 + ci) * 3 + ky) * 3 + kx]);
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int Y0 = (tile / tiles_x) * CT_Y, X0 = (tile % tiles_x) * CT_X;
+    __syncthreads();  // previous tile's readers are done
+    for (int k = threadIdx.x; k < 3 * SY * SX; k += CT_Y * CT_X) {
+      const int c = k / (SY * SX), rem = k - c * (SY * SX), yy = rem / SX, xx = rem - yy * SX;
+      const int y = Y0 + yy - 1, x = X0 + xx - 1;
+      const bool in = y >= 0 && y < d.H && x >= 0 && x < d.W;
+      const int64_t q = (int64_t)clampi(y, 0, d.H - 1) * d.W + clampi(x, 0, d.W - 1);
+      float g = 0.0f;  // gpre exists only at in-image positions
+      if (in) {
+        g = gh[c * d.P + q];
+        if (relu && !(us[c * d.P + q] > 0.0f)) g = 0.0f;
+      }
+      sg[c][yy][xx] = g;
+      sh[c][yy][xx] = hin[c * d.P + q];  // replicate padding
     }
-    // input gradient: every output q and tap whose clamped source is p
-    const bool interior = y >= 1 && y <= d.H - 2 && x >= 1 && x <= d.W - 2;
-    for (int ci = 0; ci < 3; ci++) {
-      float a = gp[ci];  // residual
-      for (int ky = 0; ky < 3; ky++)
-        for (int kx = 0; kx < 3; kx++) {
-          if (interior) {
-            const int64_t q = (int64_t)(y - ky + 1) * d.W + (x - kx + 1);
-            for (int co = 0; co < 3; co++) a = fmaf(c_tw[oG + ((co * 3 + ci) * 3 + ky) * 3 + kx], gpre(co, q), a);
-          } else {
-            for (int qy = max(y - 1, 0); qy <= min(y + 1, d.H - 1); qy++)
-              for (int qx = max(x - 1, 0); qx <= min(x + 1, d.W - 1); qx++)
-                if (clampi(qy + ky - 1, 0, d.H - 1) == y && clampi(qx + kx - 1, 0, d.W - 1) == x)
-                  for (int co = 0; co < 3; co++)
-                    a = fmaf(c_tw[oG + ((co * 3 + ci) * 3 + ky) * 3 + kx], gpre(co, (int64_t)qy * d.W + qx), a);
-          }
+    __syncthreads();
+    const int y = Y0 + ty, x = X0 + tx;
+    if (y < d.H && x < d.W) {
+      float gp[3];
+#pragma unroll
+      for (int co = 0; co < 3; co++) gp[co] = sg[co][ty + 1][tx + 1];
+#pragma unroll
+      for (int co = 0; co < 3; co++) {
+        dG[81 + co] += gp[co];
+#pragma unroll
+        for (int ci = 0; ci < 3; ci++)
+#pragma unroll
+          for (int ky = 0; ky < 3; ky++)
+#pragma unroll
+            for (int kx = 0; kx < 3; kx++)
+              dG[((co * 3 + ci) * 3 + ky) * 3 + kx] =
+                  fmaf(gp[co], sh[ci][ty + ky][tx + kx], dG[((co * 3 + ci) * 3 + ky) * 3 + kx]);
+      }
+      const bool interior = y >= 1 && y <= d.H - 2 && x >= 1 && x <= d.W - 2;
+#pragma unroll
+      for (int ci = 0; ci < 3; ci++) {
+        float a = gp[ci];  // residual
+        if (interior) {
+#pragma unroll
+          for (int ky = 0; ky < 3; ky++)
+#pragma unroll
+            for (int kx = 0; kx < 3; kx++)
+#pragma unroll
+              for (int co = 0; co < 3; co++)
+                a = fmaf(c_tw[oG + ((co * 3 + ci) * 3 + ky) * 3 + kx], sg[co][ty + 2 - ky][tx + 2 - kx], a);
+        } else {  // every output q in the neighbourhood and tap whose clamped source is p
+          for (int dy = -1; dy <= 1; dy++)
+            for (int dx = -1; dx <= 1; dx++) {
+              const int qy = y + dy, qx = x + dx;
+              if (qy < 0 || qy >= d.H || qx < 0 || qx >= d.W) continue;
+              for (int ky = 0; ky < 3; ky++)
+                for (int kx = 0; kx < 3; kx++)
+                  if (clampi(qy + ky - 1, 0, d.H - 1) == y && clampi(qx + kx - 1, 0, d.W - 1) == x)
+                    for (int co = 0; co < 3; co++)
+                      a = fmaf(c_tw[oG + ((co * 3 + ci) * 3 + ky) * 3 + kx], sg[co][ty + 1 + dy][tx + 1 + dx], a);
+            }
         }
-      gin[ci * d.P + p] = a;
+        gin[ci * d.P + (int64_t)y * d.W + x] = a;
+      }
     }
   }
 #pragma unroll
@@ -551,76 +580,123 @@ __global__ void tr_conv_bwd_kernel(TrainSynDims d, int r, const float* __restric
     if ((threadIdx.x & 31) == 0) red[e][threadIdx.x >> 5] = v;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < 84; e += TB) {
+  for (int e = threadIdx.x; e < 84; e += CT_Y * CT_X) {
     float v = 0.0f;
-    for (int w2 = 0; w2 < TB / 32; w2++) v += red[e][w2];
+    for (int w2 = 0; w2 < CT_Y * CT_X / 32; w2++) v += red[e][w2];
     gpart[(int64_t)blockIdx.x * 84 + e] = v;
   }
 }
 
 // adjoint of the 1x1 layers per pixel, dense gradient, per-CTA weight-gradient
-// partials (shared-memory outer products over the CTA's pixels)
+// partials: register-tiled (4 x 4) outer products over the CTA's pixels, work
+// items = (tile, 32-pixel chunk), chunk partials summed in a fixed order
+template <int L, int CH>
+struct TrSyn1x1Layout {
+  __host__ __device__ static constexpr int r4(int x) { return (x + 3) / 4 * 4; }
+  static constexpr int D2 = 0;                   // [d2 (3), 0]
+  static constexpr int V1 = 4;                   // [relu(u1) (CH), 1, 0 ...]
+  static constexpr int D1 = V1 + r4(CH + 1);     // d1 (CH)
+  static constexpr int DN = D1 + r4(CH);         // [dense (L), 1, 0 ...]
+  static constexpr int RAW = DN + r4(L + 1);
+  static constexpr int VEC = RAW + ((RAW / 4) % 2 == 0 ? 4 : 0);  // odd count of 16-byte words
+  static constexpr int T0 = (CH / 4) * (r4(L + 1) / 4);          // dA0 | da0 tiles
+  static constexpr int T1 = r4(CH + 1) / 4;                      // dA1 | da1 tiles (rows: d2)
+  static constexpr int NW = L * CH + CH + 3 * CH + 3;
+  static_assert(CH % 4 == 0, "hidden width multiple of 4");
+};
+
 template <int L, int CH>
 __global__ void __launch_bounds__(TS_THREADS)
     tr_syn1x1_bwd_kernel(TrainSynDims d, const float* __restrict__ dense, const float* __restrict__ u1,
                          const float* __restrict__ us0, const float* __restrict__ gh, float* __restrict__ gdense,
                          float* __restrict__ wpart, int n_w) {
-  extern __shared__ float ssm[];
-  constexpr int VEC = 3 + 2 * CH + L;  // d2 (3), v1 (CH), d1 (CH), dense (L)
-  float* vec = ssm + threadIdx.x * (VEC + 1);
+  using LY = TrSyn1x1Layout<L, CH>;
+  constexpr int VEC = LY::VEC, NCHUNK = 4, MC = TS_THREADS / NCHUNK;
+  extern __shared__ __align__(16) float ssm[];
+  float* vec = ssm + threadIdx.x * VEC;
+  float* spart = ssm + TS_THREADS * VEC;  // [NCHUNK][NW]
   const int64_t p = blockIdx.x * (int64_t)TS_THREADS + threadIdx.x;
+  for (int v = 0; v < VEC; v++) vec[v] = 0.0f;
   if (p < d.P) {
     float d2[3];
+#pragma unroll
     for (int c = 0; c < 3; c++) {
       float g = gh[c * d.P + p];
       if (d.R > 0 && !(us0[c * d.P + p] > 0.0f)) g = 0.0f;
       d2[c] = g;
-      vec[c] = g;
+      vec[LY::D2 + c] = g;
     }
 #pragma unroll
-    for (int i = 0; i < L; i++) vec[3 + 2 * CH + i] = dense[(int64_t)i * d.P + p];
+    for (int i = 0; i < L; i++) vec[LY::DN + i] = dense[(int64_t)i * d.P + p];
+    vec[LY::DN + L] = 1.0f;
+    vec[LY::V1 + CH] = 1.0f;
     float gd[L];
 #pragma unroll
     for (int i = 0; i < L; i++) gd[i] = 0.0f;
 #pragma unroll 4
     for (int n = 0; n < CH; n++) {
       const float a = u1[(int64_t)n * d.P + p];
-      vec[3 + n] = fmaxf(a, 0.0f);
+      vec[LY::V1 + n] = fmaxf(a, 0.0f);
       float g = 0.0f;
 #pragma unroll
       for (int c = 0; c < 3; c++) g = fmaf(c_tw[d.oA1 + c * CH + n], d2[c], g);
       g = a > 0.0f ? g : 0.0f;
-      vec[3 + CH + n] = g;
+      vec[LY::D1 + n] = g;
 #pragma unroll
       for (int i = 0; i < L; i++) gd[i] = fmaf(c_tw[d.oA0 + n * L + i], g, gd[i]);
     }
 #pragma unroll
     for (int i = 0; i < L; i++) gdense[(int64_t)i * d.P + p] = gd[i];
-  } else {
-    for (int v = 0; v < VEC; v++) vec[v] = 0.0f;
   }
   __syncthreads();
-  // entries in the synthesis blob order: A0[n][i], a0[n], A1[c][n], a1[c]
-  for (int e = threadIdx.x; e < n_w; e += TS_THREADS) {
-    float acc = 0.0f;
-    if (e < CH * L) {
-      const int n = e / L, i = e - n * L;
-#pragma unroll 8
-      for (int m = 0; m < TS_THREADS; m++) acc = fmaf(ssm[m * (VEC + 1) + 3 + CH + n], ssm[m * (VEC + 1) + 3 + 2 * CH + i], acc);
-    } else if (e < CH * L + CH) {
-      const int n = e - CH * L;
-#pragma unroll 8
-      for (int m = 0; m < TS_THREADS; m++) acc += ssm[m * (VEC + 1) + 3 + CH + n];
-    } else if (e < CH * L + CH + 3 * CH) {
-      const int t = e - CH * L - CH, c = t / CH, n = t - c * CH;
-#pragma unroll 8
-      for (int m = 0; m < TS_THREADS; m++) acc = fmaf(ssm[m * (VEC + 1) + c], ssm[m * (VEC + 1) + 3 + n], acc);
-    } else {
-      const int c = e - CH * L - CH - 3 * CH;
-#pragma unroll 8
-      for (int m = 0; m < TS_THREADS; m++) acc += ssm[m * (VEC + 1) + c];
+  for (int item = threadIdx.x; item < (LY::T0 + LY::T1) * NCHUNK; item += TS_THREADS) {
+    const int tile = item / NCHUNK, ch = item - tile * NCHUNK;
+    const bool first = tile < LY::T0;
+    int roff, coff, tr, tc;
+    if (first) {  // rows d1[4 tr ..], cols [dense, 1][4 tc ..]
+      const int tcols = LY::r4(L + 1) / 4;
+      tr = tile / tcols;
+      tc = tile - tr * tcols;
+      roff = LY::D1 + 4 * tr;
+      coff = LY::DN + 4 * tc;
+    } else {      // rows d2[0..3], cols [relu(u1), 1][4 tc ..]
+      tr = 0;
+      tc = tile - LY::T0;
+      roff = LY::D2;
+      coff = LY::V1 + 4 * tc;
     }
-    wpart[(int64_t)blockIdx.x * n_w + e] = acc;
+    float acc[4][4] = {};
+#pragma unroll 4
+    for (int m = ch * MC; m < ch * MC + MC; m++) {
+      const float4 rr = *reinterpret_cast<const float4*>(ssm + m * VEC + roff);
+      const float4 cc = *reinterpret_cast<const float4*>(ssm + m * VEC + coff);
+      const float rv[4] = {rr.x, rr.y, rr.z, rr.w}, cv[4] = {cc.x, cc.y, cc.z, cc.w};
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) acc[a][b] = fmaf(rv[a], cv[b], acc[a][b]);
+    }
+    float* sp = spart + ch * LY::NW;
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+      for (int b = 0; b < 4; b++) {
+        const int row = 4 * tr + a, col = 4 * tc + b;
+        if (first) {
+          if (col < L) sp[row * L + col] = acc[a][b];           // A0[n][i]
+          else if (col == L) sp[CH * L + row] = acc[a][b];      // a0[n]
+        } else if (row < 3) {
+          if (col < CH) sp[CH * L + CH + row * CH + col] = acc[a][b];   // A1[c][n]
+          else if (col == CH) sp[CH * L + CH + 3 * CH + row] = acc[a][b];  // a1[c]
+        }
+      }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n_w; e += TS_THREADS) {
+    float v = 0.0f;
+#pragma unroll
+    for (int k = 0; k < NCHUNK; k++) v += spart[k * LY::NW + e];
+    wpart[(int64_t)blockIdx.x * n_w + e] = v;
   }
 }
 
@@ -827,13 +903,10 @@ struct TrSynEntry {
   int L, CH;
   TrSynFwdFn fwd;
   TrSynBwdFn bwd;
+  int vec;  // floats per pixel record of the 1x1 adjoint
 };
-static const TrSynEntry kTrSyn[] = {
-    {7, 40, tr_syn_fwd_launch<7, 40>, tr_syn_bwd_launch<7, 40>},
-    {7, 16, tr_syn_fwd_launch<7, 16>, tr_syn_bwd_launch<7, 16>},
-    {7, 8, tr_syn_fwd_launch<7, 8>, tr_syn_bwd_launch<7, 8>},
-    {4, 8, tr_syn_fwd_launch<4, 8>, tr_syn_bwd_launch<4, 8>},
-};
+#define TR_SYN(L, CH) {L, CH, tr_syn_fwd_launch<L, CH>, tr_syn_bwd_launch<L, CH>, TrSyn1x1Layout<L, CH>::VEC}
+static const TrSynEntry kTrSyn[] = {TR_SYN(7, 40), TR_SYN(7, 16), TR_SYN(7, 8), TR_SYN(4, 8)};
 static const TrSynEntry* find_tr_syn(const cc_model_desc& d) {
   for (const auto& e : kTrSyn)
     if (e.L == d.L && e.CH == d.syn_widths[1]) return &e;
@@ -977,8 +1050,8 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
   launches++;
   for (int r = R - 1; r >= 0; r--) {
     float* cpart = F(pl.o_cpart) + (int64_t)r * pl.p_blocks * 84;
-    tr_conv_bwd_kernel<<<(int)pl.p_blocks, TB, 0, s>>>(sd, r, hsb + (int64_t)r * 3 * P, us + (int64_t)(r + 1) * 3 * P,
-                                                     gh, gh2, cpart);
+    tr_conv_bwd_kernel<<<(int)pl.p_blocks, CT_Y * CT_X, 0, s>>>(sd, r, hsb + (int64_t)r * 3 * P,
+                                                              us + (int64_t)(r + 1) * 3 * P, gh, gh2, cpart);
     launches++;
     launches += reduce_partials(cpart, pl.p_blocks, 84, 84, g_syn + (sd.oG - sd.oA0) + 84 * r,
                                 (double*)(W + pl.o_grad_tmp), s);
@@ -988,8 +1061,7 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
   }
   {
     const int n_w = L * CH + CH + 3 * CH + 3;
-    const int vec = 3 + 2 * CH + L;
-    const size_t smem = sizeof(float) * (size_t)TS_THREADS * (vec + 1);
+    const size_t smem = sizeof(float) * ((size_t)TS_THREADS * se->vec + 4 * (size_t)n_w);
     se->bwd((int)pl.s_blocks, TS_THREADS, smem, s, sd, dense, u1, us, gh, F(pl.o_gdense), F(pl.o_spart), n_w);
     launches++;
     launches += reduce_partials(F(pl.o_spart), pl.s_blocks, n_w, n_w, g_syn, (double*)(W + pl.o_grad_tmp), s);
