@@ -39,6 +39,29 @@ namespace ccrd {
 
 constexpr int TR_MAX_W = 2048;  // arm + up + syn weights (floats)
 __constant__ float c_tw[TR_MAX_W];
+// the ARM weights again, packed for FFMA2 in the forward: per layer k, for
+// input i the pair (W[2n][i], W[2n+1][i]), then the bias pairs
+constexpr int TR_MAX_ARMP = 1536;  // float2
+__constant__ float2 c_tp[TR_MAX_ARMP];
+
+__global__ void tr_pack_arm_kernel(const float* __restrict__ w, float2* __restrict__ out, int nl, int C, int NH) {
+  // one thread per output pair; layer k: nin x (nout/2) weight pairs then nout/2 bias pairs
+  int src = 0, dst = 0;
+  for (int k = 0; k < nl; k++) {
+    const int nin = (k == 0) ? C : NH, nout = (k == nl - 1) ? 2 : NH, n2 = nout / 2;
+    for (int e = threadIdx.x; e < nin * n2 + n2; e += blockDim.x) {
+      if (e < nin * n2) {
+        const int i = e / n2, n = e - i * n2;
+        out[dst + e] = make_float2(w[src + (2 * n) * nin + i], w[src + (2 * n + 1) * nin + i]);
+      } else {
+        const int n = e - nin * n2;
+        out[dst + e] = make_float2(w[src + nin * nout + 2 * n], w[src + nin * nout + 2 * n + 1]);
+      }
+    }
+    src += nin * nout + nout;
+    dst += nin * n2 + n2;
+  }
+}
 
 constexpr int TA_THREADS = 128;  // ARM: latents per CTA
 constexpr int TS_THREADS = 128;  // synthesis 1x1 backward: pixels per CTA
@@ -155,29 +178,40 @@ __global__ void __launch_bounds__(TA_THREADS) tr_arm_kernel(const __grid_constan
       const int ii = i + p.dy[c], jj = j + p.dx[c];
       z[0][c] = (ii >= 0 && ii < h && jj >= 0 && jj < w) ? g[(int64_t)ii * w + jj] : 0.0f;
     }
-    // forward (weights: per layer W[out][in] then b[out], offset in c_tw)
-    int off = 0;
+    // forward, FFMA2: two output neurons per instruction (c_tp pairs)
+    int offp = 0;
     float mu = 0.0f, s = 0.0f;
 #pragma unroll
     for (int k = 0; k < NL; k++) {
-      const int nin = (k == 0) ? C : NH, nout = (k == NL - 1) ? 2 : NH;
+      const int nin = (k == 0) ? C : NH, nout = (k == NL - 1) ? 2 : NH, n2 = nout / 2;
       const bool res = (p.res_mask >> k) & 1u;
+      uint64_t acc[(NH > 2 ? NH : 2) / 2];
 #pragma unroll
-      for (int o = 0; o < nout; o++) {
-        float a = c_tw[off + nin * nout + o];
+      for (int n = 0; n < n2; n++) acc[n] = ldp2(c_tp[offp + nin * n2 + n]);
 #pragma unroll
-        for (int t2 = 0; t2 < nin; t2++) a = fmaf(c_tw[off + o * nin + t2], z[k][t2], a);
-        if (res) a += z[k][o];
+      for (int t2 = 0; t2 < nin; t2++) {
+        const uint64_t x = f2pack(z[k][t2], z[k][t2]);
+#pragma unroll
+        for (int n = 0; n < n2; n++) acc[n] = ffma2(x, ldp2(c_tp[offp + t2 * n2 + n]), acc[n]);
+      }
+#pragma unroll
+      for (int n = 0; n < n2; n++) {
+        float2 a = f2unpack(acc[n]);
+        if (res) {
+          a.x += z[k][2 * n];
+          a.y += z[k][2 * n + 1];
+        }
         if (k < NL - 1) {
-          u[k][o] = a;
-          z[k + 1][o] = fmaxf(a, 0.0f);
-        } else if (o == 0) {
-          mu = a;
+          u[k][2 * n] = a.x;
+          u[k][2 * n + 1] = a.y;
+          z[k + 1][2 * n] = fmaxf(a.x, 0.0f);
+          z[k + 1][2 * n + 1] = fmaxf(a.y, 0.0f);
         } else {
-          s = a;
+          mu = a.x;
+          s = a.y;
         }
       }
-      off += nin * nout + nout;
+      offp += nin * n2 + n2;
     }
     float gy, gmu, gs;
     bits = tr_bits(g[t], mu, s, p, gy, gmu, gs);
@@ -209,13 +243,23 @@ __global__ void __launch_bounds__(TA_THREADS) tr_arm_kernel(const __grid_constan
     for (int k = NL - 1; k >= 0; k--) {
       const int nin = (k == 0) ? C : NH, nout = (k == NL - 1) ? 2 : NH;
       const bool res = (p.res_mask >> k) & 1u;
+      // dz[2m, 2m+1] = sum_o du[o] (W[o][2m], W[o][2m+1]) (+ du if residual): FFMA2
       float dz[NH > C ? NH : C];
+      uint64_t dzp[(NH > C ? NH : C) / 2];
 #pragma unroll
-      for (int t2 = 0; t2 < nin; t2++) {
-        float a = res ? du[t2] : 0.0f;
+      for (int m = 0; m < nin / 2; m++) dzp[m] = res ? f2pack(du[2 * m], du[2 * m + 1]) : 0ull;
 #pragma unroll
-        for (int o = 0; o < nout; o++) a = fmaf(c_tw[offk[k] + o * nin + t2], du[o], a);
-        dz[t2] = a;
+      for (int o = 0; o < nout; o++) {
+        const uint64_t d2 = f2pack(du[o], du[o]);
+#pragma unroll
+        for (int m = 0; m < nin / 2; m++)
+          dzp[m] = ffma2(d2, ldp2(*reinterpret_cast<const float2*>(&c_tw[offk[k] + o * nin + 2 * m])), dzp[m]);
+      }
+#pragma unroll
+      for (int m = 0; m < nin / 2; m++) {
+        const float2 v = f2unpack(dzp[m]);
+        dz[2 * m] = v.x;
+        dz[2 * m + 1] = v.y;
       }
       if (k > 0) {
 #pragma unroll
@@ -947,6 +991,13 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
   const int64_t nw = pl.n_arm + pl.n_up + pl.n_syn;
   if (nw > TR_MAX_W) return -2;
   cudaMemcpyToSymbolAsync(c_tw, par + lv.n_lat, sizeof(float) * (size_t)nw, 0, cudaMemcpyDeviceToDevice, s);
+  {  // FFMA2-packed ARM weights (forward) through a workspace buffer
+    float2* packed = (float2*)(W + pl.o_grad_tmp);  // free until the first reduction
+    tr_pack_arm_kernel<<<1, 256, 0, s>>>(par + lv.n_lat, packed, d.arm_n_layers, d.n_ctx, d.arm_widths[1]);
+    cudaMemcpyToSymbolAsync(c_tp, packed, sizeof(float2) * (size_t)(pl.n_arm / 2 + 2), 0, cudaMemcpyDeviceToDevice,
+                            s);
+    launches++;
+  }
   const int koff = (int)pl.n_arm;  // taps in c_tw
   TrainSynDims sd;
   sd.H = d.H;
