@@ -89,6 +89,8 @@ def lib():
         L.orc_synthesis.argtypes = [P(OrcModel), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, P(OrcMacs)]
         L.orc_rd_forward.restype = C.c_int
         L.orc_rd_forward.argtypes = [P(OrcModel)] + [C.c_void_p] * 8 + [P(OrcMacs)]
+        L.orc_decode_u8.restype = None
+        L.orc_decode_u8.argtypes = [P(OrcModel), C.c_void_p, C.c_void_p]
         L.orc_train_param_count.restype = C.c_int64
         L.orc_train_param_count.argtypes = [P(OrcModel)]
         L.orc_train_grad.restype = C.c_int
@@ -286,3 +288,17 @@ def adam_step(params: np.ndarray, grad, mom1: np.ndarray, mom2: np.ndarray, lr, 
     g = _c(grad, np.float64)
     lib().orc_adam_step(params.size, _p(params), _p(g), _p(mom1), _p(mom2),
                         C.byref(OrcAdam(lr, beta1, beta2, eps, t)))
+
+
+def decode_u8(m: OrcModel, x_hat) -> np.ndarray:
+    """Decoder output (NEXT-3): interleaved 8-bit RGB [H][W][3] of clamp(x_hat)."""
+    xh = _c(x_hat, np.float64)
+    out = np.zeros((m.H, m.W, 3), np.uint8)
+    lib().orc_decode_u8(C.byref(m), _p(xh), _p(out))
+    return out
+
+
+def decode_image(cfg, im):
+    """Oracle decode of a workload image: RD forward's x_hat -> 8-bit RGB."""
+    r = rd_forward_image(cfg, im, want_xhat=True)
+    return decode_u8(model(cfg), r["x_hat"]), r["x_hat"]

@@ -383,3 +383,16 @@ int orc_rd_forward(const orc_model* m, const int16_t* latents, const float* arm_
   if (!x_hat) free(xh);
   return 0;
 }
+
+/* ---- decoder output (NEXT-3): clamp to [0,1], 8-bit = 255 x
+ *      rounded to nearest, ties to even (reading N3),
+ *      interleaved RGB. ------------------------------------------------------ */
+void orc_decode_u8(const orc_model* m, const double* x_hat, uint8_t* out) {
+  const int64_t P = (int64_t)m->H * m->W;
+  for (int64_t p = 0; p < P; p++)
+    for (int c = 0; c < 3; c++) {
+      double v = x_hat[(int64_t)c * P + p];
+      v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+      out[p * 3 + c] = (uint8_t)rint(255.0 * v);
+    }
+}

@@ -85,6 +85,11 @@ int orc_rd_forward(const orc_model* m, const int16_t* latents, const float* arm_
                    const float* up_w, const float* syn_w, const float* image,
                    double* out, double* x_hat, double* dense, orc_macs* macs);
 
+/* Decoder output (NEXT-3; "final output clamped to [0,1]";
+ * 8-bit RGB, pixel = 255 x): out[(y W + x) 3 + c] =
+ * rint(255 clamp(x_hat[c][y][x], 0, 1)) (round half to even; reading N3). */
+void orc_decode_u8(const orc_model* m, const double* x_hat, uint8_t* out);
+
 /* Rate and per-latent outputs for the latents of rows [r0, r1) of level l only
  * (bounded samples at full size; same arithmetic as orc_rate). */
 double orc_rate_rows(const orc_model* m, const int16_t* latents, const float* arm_w,

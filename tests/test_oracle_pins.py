@@ -521,3 +521,23 @@ def test_table1_configs_oracle_macs_match_table(name):
     assert r["macs"]["up"] == up
     tot = sum(r["macs"].values()) / (cfg.H * cfg.W)
     assert abs(tot - g["mac_per_pixel"]) / g["mac_per_pixel"] < 0.01
+
+
+# ---------------------------------------------------- decoder output (NEXT-3)
+def test_decode_u8_closed_forms():
+    """clamp to [0,1] then 255 x rounded half to even."""
+    cfg = workload.CONFIGS["tiny"].replace(H=1, W=8)
+    m = oracle.model(cfg)
+    xh = np.zeros((3, 1, 8))
+    xh[0, 0] = [-0.3, 0.0, 1 / 255, 128 / 255, 1.0, 1.7, 0.5 / 255, 1.5 / 255]
+    xh[1, 0] = np.linspace(0, 1, 8)
+    xh[2, 0] = 254.5 / 255
+    out = oracle.decode_u8(m, xh)
+    assert out.shape == (1, 8, 3)
+    assert list(out[0, :, 0]) == [0, 0, 1, 128, 255, 255, 0, 2]   # clamps; ties to even
+    assert list(out[0, :, 1]) == [int(np.rint(255 * v)) for v in np.linspace(0, 1, 8)]
+    assert np.all(out[0, :, 2] == 254)                            # 254.5 -> even
+    # monotone in x_hat
+    xs = np.sort(np.random.default_rng(0).uniform(-0.2, 1.2, 8 * 3)).reshape(3, 1, 8)
+    o = oracle.decode_u8(m, xs).transpose(2, 0, 1).ravel()
+    assert np.all(np.diff(o.astype(int)) >= 0)
