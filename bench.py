@@ -361,6 +361,69 @@ def run_strip(args, rk):
         print(json.dumps(out), flush=True)
 
 
+def run_decode(args, rk):
+    """NEXT-3: the decoder's data-parallel output stage (cc_decode: latents ->
+    upsampling -> synthesis -> clamp -> 8-bit RGB) over the batched 2K
+    workload, one cc_decode per image.  The sequential entropy decoding of the
+    latents is out of scope, so this is not a full decode time."""
+    import torch
+
+    import paper_2403_11651_b200 as P
+    from paper_2403_11651_b200 import dist
+
+    cfg = workload.CONFIGS[args.config]
+    n_img = args.images or cfg.n_img
+    dev = torch.device("cuda", rk.local_rank)
+    torch.cuda.set_device(dev)
+    P.load()
+    images = workload.make_batch(cfg, [workload.image_seed(args.seed, g) for g in dist.owned_images(rk.rank, n_img)],
+                                 threads=min(16, host_cores()))
+    desc = P.desc_from_config(cfg)
+    lats = [torch.from_numpy(im.latents).to(dev) for im in images]
+    outs = [torch.empty((cfg.H, cfg.W, 3), dtype=torch.uint8, device=dev) for _ in images]
+    ws_b = P.cc_workspace_bytes(desc, 1)
+    ws = torch.empty(ws_b, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        for i, im in enumerate(images):
+            P.cc_decode(desc, lats[i].data_ptr(), im.up_w, im.syn_w, outs[i].data_ptr(), ws.data_ptr(), ws_b,
+                        stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(rk.local_rank)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    sampler.stop()
+    ms = dist.max_over_ranks(ev0.elapsed_time(ev1), device=dev)
+    value = rk.world * n_img * cfg.H * cfg.W * args.steps / (ms / 1e3)
+    macs = P.cc_mac_per_pixel(desc)
+    flops = 2.0 * (macs.up + macs.syn) * value / rk.world
+    out = {
+        "metric": "decoder output stage (upsampling + synthesis + clamp + 8-bit) pixels/s", "value": value,
+        "unit": "pixels/s", "n_gpus": rk.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"decode_{cfg.name}: {n_img} x {cfg.H}x{cfg.W} per GPU, 8-bit RGB output",
+                   "H": cfg.H, "W": cfg.W, "mac_per_pixel_up_syn": round(macs.up + macs.syn, 3)},
+        "path_roofline": {"achieved_tflops_per_gpu": flops / 1e12, "frac": flops / 1e12 / FP32_PEAK_TFLOPS},
+        "context": "paper: ~100 ms per 512x768 decode on one CPU core incl. the sequential ARM (BASELINE.md)",
+        "e2e": None, "clocks": sampler.summary(),
+    }
+    if rk.rank == 0:
+        print(json.dumps(out), flush=True)
+
+
 def run_train(args, rk):
     """NEXT-2: the encoder training iteration (forward on the noise proxy,
     backward, Adam) of ONE image per GPU (BASELINE.json configs[2] by default:
@@ -532,6 +595,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--train", action="store_true", help="time the encoder training iteration (NEXT-2)")
+    ap.add_argument("--decode", action="store_true", help="time the decoder output stage (NEXT-3)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 breaks the timing rules", file=sys.stderr)
@@ -543,6 +607,8 @@ def main():
     rk = dist.init("nccl")
     if args.train:
         run_train(args, rk)
+    elif args.decode:
+        run_decode(args, rk)
     elif args.config == "8k":
         run_strip(args, rk)
     else:

@@ -219,6 +219,19 @@ int cc_train_step(const cc_model_desc* desc, float* params, const float* noise, 
                   float* adam_m, float* adam_v, const cc_adam* opt, cc_rd_result* result, float* grad,
                   void* workspace, size_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------------------ decode (NEXT-3)
+ * The decoder's data-parallel output stage ("upsample the
+ * latents to a dense representation and synthesize the decoded image";
+ * SPEC.md:309-312 "final output clamped to [0,1]"; SPEC.md:332, 624-625 8-bit
+ * output, pixel = 255 x): from the decoded latents (DEVICE, packed pyramid) to
+ * out_rgb8 (DEVICE, interleaved [H][W][3] uint8) = rint(255 clamp(x_hat, 0, 1))
+ * (ties to even, reading N3).  The autoregressive entropy decoding of the
+ * latents themselves is sequential and out of scope.  Same kernels as
+ * cc_rd_forward without the ARM and the distortion.  Workspace:
+ * cc_workspace_bytes(desc, 1). */
+int cc_decode(const cc_model_desc* desc, const int16_t* latents, const float* up_w, const float* syn_w,
+              uint8_t* out_rgb8, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Stage entry: ARM rate only (PAPER.md:120 R term).  rate: DEVICE double [1].
  * Optional DEVICE float arrays (packed like the latents, NULL to skip):
  * mu, scale (= b), bits (per latent -log2 P).  Workspace as cc_rd_forward(1). */

@@ -80,7 +80,7 @@ EXPORTS = ["cc_workspace_bytes", "cc_rd_forward", "cc_workspace_bytes_host", "cc
            "cc_strerror", "cc_last_error", "cc_version", "cc_last_launch_count",
            "cc_profile_begin", "cc_profile_end", "cc_strip_window", "cc_strip_latent_count",
            "cc_workspace_bytes_strip", "cc_rd_forward_strip", "cc_train_param_count",
-           "cc_train_workspace_bytes", "cc_train_step"]
+           "cc_train_workspace_bytes", "cc_train_step", "cc_decode"]
 
 _lib = None
 
@@ -144,6 +144,8 @@ def load(rebuild_if_stale: bool = True) -> C.CDLL:
     L.cc_train_param_count.argtypes = [D]
     L.cc_train_workspace_bytes.restype = S
     L.cc_train_workspace_bytes.argtypes = [D]
+    L.cc_decode.restype = C.c_int
+    L.cc_decode.argtypes = [D, V, V, V, V, V, S, V]
     L.cc_train_step.restype = C.c_int
     L.cc_train_step.argtypes = [D, V, V, V, V, V, P(CcAdam), V, V, V, S, V]
     _lib = L
@@ -271,6 +273,13 @@ def cc_rd_forward_strip(desc, strip: CcStrip, io: CcImageIO, result_ptr: int, ws
                         stream_ptr: int = 0) -> None:
     _check(load().cc_rd_forward_strip(C.byref(desc), C.byref(strip), C.byref(io), result_ptr, ws_ptr, ws_bytes,
                                       stream_ptr), "cc_rd_forward_strip")
+
+
+def cc_decode(desc, latents_ptr, up_w: np.ndarray, syn_w: np.ndarray, out_ptr, ws_ptr, ws_bytes, stream_ptr=0):
+    uw = np.ascontiguousarray(up_w, np.float32)
+    sw = np.ascontiguousarray(syn_w, np.float32)
+    _check(load().cc_decode(C.byref(desc), latents_ptr, uw.ctypes.data, sw.ctypes.data, out_ptr, ws_ptr, ws_bytes,
+                            stream_ptr), "cc_decode")
 
 
 def cc_train_param_count(desc) -> int:

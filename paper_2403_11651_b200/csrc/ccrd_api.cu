@@ -412,13 +412,13 @@ static int pyr_many(const cc_model_desc& d, const cc_strip* win, const PyrImage*
 // fused last upsampling step + synthesis + distortion of one image
 static int syn_one(const cc_model_desc& d, const cc_strip* win, const int16_t* lat, const float* s1,
                    const float* up_w, const float* syn_w, const float* image, float* x_hat, float* dense_out,
-                   double* syn_part, cudaStream_t s) {
+                   double* syn_part, cudaStream_t s, uint8_t* out_u8 = nullptr) {
   SynGeom sg;
   syn_geom(d, win, sg);
   {
     ProfScope ps(PK_SYN, s);
     find_syn_launcher(d.L, d.syn_widths[1], d.syn_n_res, d.up_taps)(sg, d, up_w, syn_w, lat, s1, nullptr, image,
-                                                                    x_hat, dense_out, nullptr, syn_part, s);
+                                                                    x_hat, dense_out, nullptr, syn_part, s, out_u8);
   }
   g_launches++;
   return cuda_check("synth_kernel");
@@ -498,7 +498,7 @@ static int forward_batch(const cc_model_desc& d, const cc_strip* win, const int1
         ProfScope ps(PK_SYN, s);
         find_syn_launcher(d.L, d.syn_widths[1], d.syn_n_res, d.up_taps)(
             sg, d, nullptr, syn_w[i], lat[i], nullptr, slice_dense(d, win, sl), image[i], x_hat[i], nullptr, nullptr,
-            (double*)sl + n_arm, s);
+            (double*)sl + n_arm, s, nullptr);
       }
       g_launches++;
       if ((rc = cuda_check("synth_kernel(dense_in)"))) return rc;
@@ -855,6 +855,42 @@ int cc_train_step(const cc_model_desc* desc, float* params, const float* noise, 
   return cuda_check("cc_train_step");
 }
 
+// ---------------------------------------------------------------- decode
+int cc_decode(const cc_model_desc* desc, const int16_t* latents, const float* up_w, const float* syn_w,
+              uint8_t* out_rgb8, void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  int rc = validate(desc);
+  if (rc) return rc;
+  if (!latents || !up_w || !syn_w || !out_rgb8) return fail(CC_EINVAL, "null latents / up_w / syn_w / out");
+  const cc_model_desc& d = *desc;
+  const size_t per = slice_bytes(d, nullptr);
+  if (!workspace || workspace_bytes < per) return fail(CC_EWORKSPACE, "need %zu workspace bytes", per);
+  if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
+  cudaStream_t s = (cudaStream_t)stream;
+  PyrGeom pg;
+  pyr_geom(d, nullptr, pg);
+  if (d.up_2d) {
+    Pyr2dImage im2;
+    im2.lat = latents;
+    im2.S = slice_pyr(d, nullptr, workspace);
+    im2.dense = slice_dense(d, nullptr, workspace);
+    for (int t = 0; t < 64; t++) im2.k2[t] = t < d.up_taps * d.up_taps ? up_w[t] : 0.0f;
+    launch_pyramid2d(pg, d.up_taps, &im2, 1, s);
+    g_launches += pyramid2d_launch_count(pg, 1);
+    SynGeom sg;
+    syn_geom(d, nullptr, sg);
+    find_syn_launcher(d.L, d.syn_widths[1], d.syn_n_res, d.up_taps)(sg, d, nullptr, syn_w, latents, nullptr, im2.dense,
+                                                                    nullptr, nullptr, nullptr, nullptr, nullptr, s,
+                                                                    out_rgb8);
+    g_launches++;
+    return cuda_check("cc_decode(2d)");
+  }
+  float* S = slice_pyr(d, nullptr, workspace);
+  PyrImage im = pyr_image(d, latents, up_w, S);
+  if ((rc = pyr_many(d, nullptr, &im, 1, s))) return rc;
+  return syn_one(d, nullptr, latents, S + pg.s_off[1], up_w, syn_w, nullptr, nullptr, nullptr, nullptr, s, out_rgb8);
+}
+
 // ---------------------------------------------------------------- stages
 int cc_arm_rate(const cc_model_desc* desc, const int16_t* latents, const float* arm_w, double* rate, float* mu,
                 float* scale, float* bits, void* workspace, size_t workspace_bytes, void* stream) {
@@ -939,7 +975,7 @@ int cc_synthesize(const cc_model_desc* desc, const float* dense, const float* sy
   cudaStream_t s = (cudaStream_t)stream;
   double* part = sse ? (double*)workspace : nullptr;
   find_syn_launcher(d.L, d.syn_widths[1], d.syn_n_res, d.up_taps)(sg, d, nullptr, syn_w, nullptr, nullptr, dense,
-                                                                   image, x_hat, nullptr, h_1x1, part, s);
+                                                                   image, x_hat, nullptr, h_1x1, part, s, nullptr);
   g_launches++;
   if ((rc = cuda_check("synth_kernel(dense_in)"))) return rc;
   if (sse) {

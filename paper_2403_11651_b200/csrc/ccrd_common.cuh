@@ -178,6 +178,7 @@ struct SynParams {
   float* dense_out;        // debug [L][H][W] or null
   float* h1_out;           // debug [3][H][W] or null
   double* partial;         // [n tiles] per-CTA SSE partial sums
+  uint8_t* out_u8;         // decode: interleaved 8-bit RGB [H][W][3] of clamp(x_hat) or null
   SynWeights<L, CH, R, K> w;
 };
 
@@ -243,7 +244,7 @@ typedef int (*ArmLaunchFn)(const ArmGeom& g, const cc_model_desc& d, const float
 typedef int (*SynLaunchFn)(const SynGeom& g, const cc_model_desc& d, const float* up_w,
                            const float* syn_w, const int16_t* lat, const float* s1, const float* dense_in,
                            const float* image, float* x_hat, float* dense_out, float* h1_out,
-                           double* partial, cudaStream_t s);
+                           double* partial, cudaStream_t s, uint8_t* out_u8);
 
 ArmLaunchFn find_arm_launcher(int C, int NH, int NHL);     // FFMA2 path (arm_rate.cu)
 ArmLaunchFn find_arm_tc_launcher(int C, int NH, int NHL);  // tensor-core path (arm_tc.cu)

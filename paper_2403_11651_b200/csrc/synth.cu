@@ -499,6 +499,11 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
             for (int c = 0; c < 3; c++) hout[c * HP + ctr] = fmaxf(o[c], 0.0f);
           } else {
             const int64_t gi = (int64_t)(y - Ys) * W + x;
+            if (p.out_u8 != nullptr) {  // decoder output: clamp to [0,1], 8-bit, ties to even (reading N3)
+#pragma unroll
+              for (int c = 0; c < 3; c++)
+                p.out_u8[gi * 3 + c] = (uint8_t)__float2uint_rn(255.0f * fminf(fmaxf(o[c], 0.0f), 1.0f));
+            }
 #pragma unroll
             for (int c = 0; c < 3; c++) {
               if (p.x_hat != nullptr) p.x_hat[c * Pimg + gi] = o[c];
@@ -557,6 +562,11 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
       if (y >= Ye || x >= W) continue;
       const int ctr = (y - RY) * RW0 + (x - RX);
       const int64_t gi = (int64_t)(y - Ys) * W + x;
+      if (p.out_u8 != nullptr) {
+#pragma unroll
+        for (int c = 0; c < 3; c++)
+          p.out_u8[gi * 3 + c] = (uint8_t)__float2uint_rn(255.0f * fminf(fmaxf(hin[c * HP + ctr], 0.0f), 1.0f));
+      }
 #pragma unroll
       for (int c = 0; c < 3; c++) {
         const float xh = hin[c * HP + ctr];
@@ -595,7 +605,7 @@ template <int L, int CH, int R, int K>
 static int launch_syn(const SynGeom& g, const cc_model_desc& d, const float* up_w,
                       const float* syn_w, const int16_t* lat, const float* s1, const float* dense_in,
                       const float* image, float* x_hat, float* dense_out, float* h1_out,
-                      double* partial, cudaStream_t stream) {
+                      double* partial, cudaStream_t stream, uint8_t* out_u8) {
   (void)d;
   SynParams<L, CH, R, K> p;
   p.g = g;
@@ -607,6 +617,7 @@ static int launch_syn(const SynGeom& g, const cc_model_desc& d, const float* up_
   p.dense_out = dense_out;
   p.h1_out = h1_out;
   p.partial = partial;
+  p.out_u8 = out_u8;
   for (int t = 0; t < K; t++) p.w.k[t] = up_w ? up_w[t] : 0.0f;
   // last vertical step: (a0, a1) += sv[u] (k[K-1-2u], k[K-2u]), zero where a
   // phase has no tap (u = K/2 for a0, u = 0 for a1)
