@@ -17,6 +17,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "ccoracle.c")
 _SRC_TRAIN = os.path.join(_HERE, "cctrain.c")  # NEXT-2: one training iteration
+_SRC_ANALYSIS = os.path.join(_HERE, "ccanalysis.c")  # NEXT-4: N-O analysis transform
 _LIB = os.path.join(_HERE, "libccoracle.so")
 
 MAX_LAYERS = 8
@@ -36,6 +37,10 @@ class OrcModel(C.Structure):
     ]
 
 
+class OrcAnalysis(C.Structure):
+    _fields_ = [("H", C.c_int32), ("W", C.c_int32), ("L", C.c_int32), ("C", C.c_int32), ("blocks", C.c_int32)]
+
+
 class OrcAdam(C.Structure):
     _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
                 ("t", C.c_int32)]
@@ -48,10 +53,11 @@ class OrcMacs(C.Structure):
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc (plain C99 + OpenMP)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
-            os.path.getmtime(_SRC), os.path.getmtime(_SRC_TRAIN), os.path.getmtime(os.path.join(_HERE, "ccoracle.h"))):
+            os.path.getmtime(_SRC), os.path.getmtime(_SRC_TRAIN), os.path.getmtime(_SRC_ANALYSIS),
+            os.path.getmtime(os.path.join(_HERE, "ccoracle.h"))):
         tmp = _LIB + f".{os.getpid()}.tmp"
         subprocess.check_call(["gcc", "-O2", "-std=c99", "-fopenmp", "-fPIC", "-shared",
-                               "-o", tmp, _SRC, _SRC_TRAIN, "-lm"])
+                               "-o", tmp, _SRC, _SRC_TRAIN, _SRC_ANALYSIS, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -89,6 +95,10 @@ def lib():
         L.orc_synthesis.argtypes = [P(OrcModel), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, P(OrcMacs)]
         L.orc_rd_forward.restype = C.c_int
         L.orc_rd_forward.argtypes = [P(OrcModel)] + [C.c_void_p] * 8 + [P(OrcMacs)]
+        L.orc_analysis_param_count.restype = C.c_int64
+        L.orc_analysis_param_count.argtypes = [P(OrcAnalysis)]
+        L.orc_analysis_forward.restype = C.c_int
+        L.orc_analysis_forward.argtypes = [P(OrcAnalysis), C.c_void_p, C.c_void_p, C.c_void_p, P(C.c_int64)]
         L.orc_decode_u8.restype = None
         L.orc_decode_u8.argtypes = [P(OrcModel), C.c_void_p, C.c_void_p]
         L.orc_train_param_count.restype = C.c_int64
@@ -302,3 +312,23 @@ def decode_image(cfg, im):
     """Oracle decode of a workload image: RD forward's x_hat -> 8-bit RGB."""
     r = rd_forward_image(cfg, im, want_xhat=True)
     return decode_u8(model(cfg), r["x_hat"]), r["x_hat"]
+
+
+# -------------------------------------------------- N-O analysis (NEXT-4)
+def analysis_model(acfg) -> OrcAnalysis:
+    return OrcAnalysis(acfg.H, acfg.W, acfg.L, acfg.C, acfg.blocks)
+
+
+def analysis_forward(acfg, image, weights):
+    """Continuous latents (fp64, packed level after level) and the MAC count."""
+    m = analysis_model(acfg)
+    n_lat = sum(-(-acfg.H // (1 << l)) * -(-acfg.W // (1 << l)) for l in range(acfg.L))
+    out = np.zeros(n_lat)
+    macs = C.c_int64(0)
+    img = _c(image, np.float32)
+    w = _c(weights, np.float32)
+    assert w.size == lib().orc_analysis_param_count(C.byref(m))
+    rc = lib().orc_analysis_forward(C.byref(m), _p(img), _p(w), _p(out), C.byref(macs))
+    if rc != 0:
+        raise ValueError(f"orc_analysis_forward rc={rc}")
+    return out, macs.value

@@ -264,3 +264,61 @@ def make_batch(cfg: Config, seeds: List[int], filter_kind: str = "random",
 def image_seed(base: int, index: int) -> int:
     """Per-image seed: SeedSequence(base + image_index)."""
     return base + index
+
+
+# ------------------------------------------------ N-O analysis (NEXT-4)
+@dataclasses.dataclass(frozen=True)
+class AnalysisConfig:
+    """N-O Cool-chic analysis transform (readings A1-A7 of
+    DESIGN.md): L grids, C features, `blocks` ConvNeXt-style blocks per level."""
+    name: str
+    H: int
+    W: int
+    L: int = 7
+    C: int = 64
+    blocks: int = 3
+
+    def replace(self, **kw):
+        return dataclasses.replace(self, **kw)
+
+    @property
+    def n_params(self):
+        C = self.C
+        blk = C * 49 + C + 4 * C * C + 4 * C + 4 * C * C + C
+        n = C * 3 + C
+        for l in range(self.L):
+            n += self.blocks * blk + (C * C + C if l > 0 else 0) + C + 1
+        return n
+
+
+ANALYSIS = {
+    "no_tiny": AnalysisConfig("no_tiny", 37, 53, L=4, C=8, blocks=2),
+    "no_kodak": AnalysisConfig("no_kodak", 512, 768),
+    "no_2k": AnalysisConfig("no_2k", 1365, 2048),
+}
+
+
+def gen_analysis_weights(rng: np.random.Generator, acfg: AnalysisConfig) -> np.ndarray:
+    """Seeded fp32 blob in the oracle's order, variance-preserving scales (the
+    paper's weights are trained; these only keep 3L residual blocks bounded):
+    dw ~ N(0, 1/7), W1 ~ N(0, 1/sqrt(C)), W2 ~ N(0, 0.3/sqrt(4C)), identity and
+    stem ~ N(0, 1/sqrt(fan_in)), merge ~ N(0, 1/sqrt(C)), biases ~ N(0, 0.02)."""
+    C = acfg.C
+    parts = [rng.normal(0, 1 / np.sqrt(3), C * 3), rng.normal(0, 0.02, C)]
+    for l in range(acfg.L):
+        for b in range(acfg.blocks):
+            parts += [rng.normal(0, 1 / 7, C * 49), rng.normal(0, 0.02, C),
+                      rng.normal(0, 1 / np.sqrt(C), 4 * C * C), rng.normal(0, 0.02, 4 * C),
+                      rng.normal(0, 0.3 / np.sqrt(4 * C), 4 * C * C), rng.normal(0, 0.02, C)]
+            if l > 0 and b == 0:
+                parts += [rng.normal(0, 1 / np.sqrt(C), C * C), rng.normal(0, 0.02, C)]
+        parts += [rng.normal(0, 1 / np.sqrt(C), C), rng.normal(0, 0.02, 1)]
+    w = np.concatenate(parts).astype(np.float32)
+    assert w.size == acfg.n_params
+    return w
+
+
+def make_analysis_input(acfg: AnalysisConfig, seed: int):
+    """(image [3][H][W] fp32 -- the sinusoid recipe of configs[0] --, weights)."""
+    r_img, _, r_w = _streams(seed)
+    return gen_image(r_img, acfg.H, acfg.W), gen_analysis_weights(r_w, acfg)
