@@ -424,6 +424,76 @@ def run_decode(args, rk):
         print(json.dumps(out), flush=True)
 
 
+def run_analysis(args, rk):
+    """NEXT-4: the N-O analysis transform forward (encoding = one forward pass,
+    PAPER.md:422-449, 483-484) on Kodak-sized images (no_kodak) by default;
+    --tf32 runs the point-wise GEMMs on TF32 tensor cores."""
+    import torch
+
+    import paper_2403_11651_b200 as P
+    from paper_2403_11651_b200 import dist
+
+    acfg = workload.ANALYSIS[args.analysis]
+    n_img = args.images or 8
+    dev = torch.device("cuda", rk.local_rank)
+    torch.cuda.set_device(dev)
+    P.load()
+    ad = P.analysis_desc(acfg, args.tf32)
+    ins = [workload.make_analysis_input(acfg, workload.image_seed(args.seed, g))
+           for g in dist.owned_images(rk.rank, n_img)]
+    imgs = [torch.from_numpy(i).to(dev) for i, _ in ins]
+    w = torch.from_numpy(ins[0][1]).to(dev)   # N-O: one shared network
+    n_lat = sum(-(-acfg.H // (1 << l)) * -(-acfg.W // (1 << l)) for l in range(acfg.L))
+    lats = [torch.empty(n_lat, device=dev) for _ in imgs]
+    ws_b = P.cc_analysis_workspace_bytes(ad)
+    ws = torch.empty(ws_b, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        for i in range(n_img):
+            P.cc_analysis_forward(ad, imgs[i].data_ptr(), w.data_ptr(), lats[i].data_ptr(), ws.data_ptr(), ws_b,
+                                  stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(rk.local_rank)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    sampler.stop()
+    ms = dist.max_over_ranks(ev0.elapsed_time(ev1), device=dev)
+    px = acfg.H * acfg.W
+    value = rk.world * n_img * px * args.steps / (ms / 1e3)
+    C = acfg.C
+    macs = 3 * C * px
+    for l in range(acfg.L):
+        hl, wl = -(-acfg.H // (1 << l)), -(-acfg.W // (1 << l))
+        macs += acfg.blocks * (C * 49 + 8 * C * C) * hl * wl + (C * C * hl * wl if l > 0 else 0) + C * hl * wl
+    tflops = 2.0 * macs / px * value / rk.world / 1e12
+    peak = FP32_PEAK_TFLOPS * (1 if not args.tf32 else 1)
+    out = {
+        "metric": "N-O analysis transform (encoding forward) pixels/s", "value": value, "unit": "pixels/s",
+        "n_gpus": rk.world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "tf32" if args.tf32 else "f32",
+        "data": "synthetic",
+        "config": {"workload": f"{acfg.name}: {n_img} x {acfg.H}x{acfg.W} per GPU, C={C}, L={acfg.L}, "
+                               f"{acfg.blocks} blocks/level", "kmac_per_pixel": round(macs / px / 1e3, 2)},
+        "achieved_tflops_per_gpu": tflops,
+        "context": "paper: N-O encoding < 1 s per image (one forward pass, ~160 kMAC/px), hardware not stated",
+        "e2e": None, "clocks": sampler.summary(),
+    }
+    if rk.rank == 0:
+        print(json.dumps(out), flush=True)
+
+
 def run_train(args, rk):
     """NEXT-2: the encoder training iteration (forward on the noise proxy,
     backward, Adam) of ONE image per GPU (BASELINE.json configs[2] by default:
@@ -596,6 +666,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--train", action="store_true", help="time the encoder training iteration (NEXT-2)")
     ap.add_argument("--decode", action="store_true", help="time the decoder output stage (NEXT-3)")
+    ap.add_argument("--analysis", default="", help="time the N-O analysis transform (NEXT-4): no_kodak | no_2k")
+    ap.add_argument("--tf32", action="store_true", help="analysis: TF32 tensor-core point-wise GEMMs")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 breaks the timing rules", file=sys.stderr)
@@ -609,6 +681,8 @@ def main():
         run_train(args, rk)
     elif args.decode:
         run_decode(args, rk)
+    elif args.analysis:
+        run_analysis(args, rk)
     elif args.config == "8k":
         run_strip(args, rk)
     else:

@@ -232,6 +232,28 @@ int cc_train_step(const cc_model_desc* desc, float* params, const float* noise, 
 int cc_decode(const cc_model_desc* desc, const int16_t* latents, const float* up_w, const float* syn_w,
               uint8_t* out_rgb8, void* workspace, size_t workspace_bytes, void* stream);
 
+/* --------------------------------------------- N-O analysis (NEXT-4)
+ * The non-overfitted Cool-chic analysis transform y_hat = f_alpha(x)
+ * (Eq. 3): C-channel ConvNeXt-style blocks (depth-wise 7x7,
+ * point-wise C -> 4C -> C with ReLU, residual), `blocks` per level, a stride-2
+ * downsampling block opening each level l >= 1 (identity branch: 2x2 average
+ * pooling + 1x1 conv), a 1x1 C -> 1 merge giving latent grid l after each
+ * level.  Fig. 4 is missing from the paper: every structural choice is a
+ * reading (A1-A7).  Weight blob: stem W[C][3], b[C]; per level, per
+ * block: dw k[C][7][7], dw b[C], W1[4C][C], b1[4C], W2[C][4C], b2[C], then
+ * (downsampling blocks only) Wid[C][C], bid[C]; per level: Wm[C], bm.
+ * image: DEVICE [3][H][W] fp32; weights: DEVICE blob; latents: DEVICE fp32,
+ * packed level after level (the decoder's ceil dims), continuous (rounding
+ * belongs to the coder).  tf32 = 1 runs the point-wise GEMMs on TF32 tensor
+ * cores (cuBLASLt), 0 in fp32. */
+typedef struct {
+  int32_t H, W, L, C, blocks, tf32;
+} cc_analysis_desc;
+int64_t cc_analysis_param_count(const cc_analysis_desc* a);     /* -1 on error */
+size_t cc_analysis_workspace_bytes(const cc_analysis_desc* a);  /* 0 on error  */
+int cc_analysis_forward(const cc_analysis_desc* a, const float* image, const float* weights, float* latents,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
 /* Stage entry: ARM rate only (PAPER.md:120 R term).  rate: DEVICE double [1].
  * Optional DEVICE float arrays (packed like the latents, NULL to skip):
  * mu, scale (= b), bits (per latent -log2 P).  Workspace as cc_rd_forward(1). */

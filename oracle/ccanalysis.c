@@ -57,6 +57,7 @@ int64_t orc_analysis_param_count(const orc_analysis* a) {
 /* depth-wise 7x7, stride s, zero padding 3: in [C][h][w] -> out [C][ho][wo] */
 static void dwconv(const double* in, int C, int h, int w, int s, const float* k, const float* kb, double* out, int ho,
                    int wo, int64_t* macs) {
+#pragma omp parallel for  /* independent channels */
   for (int c = 0; c < C; c++)
     for (int y = 0; y < ho; y++)
       for (int x = 0; x < wo; x++) {
@@ -74,6 +75,7 @@ static void dwconv(const double* in, int C, int h, int w, int s, const float* k,
 /* out[n][p] = b[n] + sum_k W[n][k] in[k][p] (+ relu) */
 static void pointwise(const double* in, int K, int64_t P, const float* Wt, const float* b, int N, int relu, double* out,
                       int64_t* macs) {
+#pragma omp parallel for  /* independent output channels */
   for (int n = 0; n < N; n++)
     for (int64_t p = 0; p < P; p++) {
       double a = (double)b[n];

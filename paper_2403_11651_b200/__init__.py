@@ -10,7 +10,8 @@ from .ccrd import (  # noqa: F401
     cc_rd_forward, cc_rd_forward_host, cc_rd_forward_strip, cc_strip_latent_count, cc_strip_window,
     cc_synthesize, cc_upsample, cc_validate, cc_workspace_bytes, cc_workspace_bytes_host,
     cc_workspace_bytes_strip, desc_from_config, load, cc_train_param_count, cc_train_workspace_bytes,
-    cc_train_step, CcAdam, DeviceTrainer, cc_decode,
+    cc_train_step, CcAdam, DeviceTrainer, cc_decode, CcAnalysisDesc, analysis_desc, cc_analysis_param_count,
+    cc_analysis_workspace_bytes, cc_analysis_forward,
 )
 
 __version__ = "0.1.0"

@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libccrd.so")
-SOURCES = ["arm_rate.cu", "arm_tc.cu", "pyramid.cu", "synth.cu", "train.cu", "ccrd_api.cu"]
+SOURCES = ["arm_rate.cu", "arm_tc.cu", "pyramid.cu", "synth.cu", "train.cu", "analysis.cu", "ccrd_api.cu"]
 HEADERS = ["ccrd_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -59,7 +59,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
     objs = [os.path.join(objdir, s.replace(".cu", ".o")) for s in SOURCES]
     if force or jobs or _stale(lib, objs):
         tmp = lib + f".{os.getpid()}.tmp"
-        subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart"])
+        subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart", "-lcublasLt"])
         os.replace(tmp, lib)
     return lib
 

@@ -68,6 +68,11 @@ class CcAdam(C.Structure):
                 ("t", C.c_int32)]
 
 
+class CcAnalysisDesc(C.Structure):
+    _fields_ = [("H", C.c_int32), ("W", C.c_int32), ("L", C.c_int32), ("C", C.c_int32), ("blocks", C.c_int32),
+                ("tf32", C.c_int32)]
+
+
 class CcProfileSummary(C.Structure):
     _fields_ = [("arm_ms", C.c_double), ("syn_ms", C.c_double), ("reduce_ms", C.c_double), ("pyr_ms", C.c_double),
                 ("arm_launches", C.c_int64), ("syn_launches", C.c_int64), ("reduce_launches", C.c_int64),
@@ -80,7 +85,8 @@ EXPORTS = ["cc_workspace_bytes", "cc_rd_forward", "cc_workspace_bytes_host", "cc
            "cc_strerror", "cc_last_error", "cc_version", "cc_last_launch_count",
            "cc_profile_begin", "cc_profile_end", "cc_strip_window", "cc_strip_latent_count",
            "cc_workspace_bytes_strip", "cc_rd_forward_strip", "cc_train_param_count",
-           "cc_train_workspace_bytes", "cc_train_step", "cc_decode"]
+           "cc_train_workspace_bytes", "cc_train_step", "cc_decode", "cc_analysis_param_count",
+           "cc_analysis_workspace_bytes", "cc_analysis_forward"]
 
 _lib = None
 
@@ -144,6 +150,13 @@ def load(rebuild_if_stale: bool = True) -> C.CDLL:
     L.cc_train_param_count.argtypes = [D]
     L.cc_train_workspace_bytes.restype = S
     L.cc_train_workspace_bytes.argtypes = [D]
+    A = P(CcAnalysisDesc)
+    L.cc_analysis_param_count.restype = C.c_int64
+    L.cc_analysis_param_count.argtypes = [A]
+    L.cc_analysis_workspace_bytes.restype = S
+    L.cc_analysis_workspace_bytes.argtypes = [A]
+    L.cc_analysis_forward.restype = C.c_int
+    L.cc_analysis_forward.argtypes = [A, V, V, V, V, S, V]
     L.cc_decode.restype = C.c_int
     L.cc_decode.argtypes = [D, V, V, V, V, V, S, V]
     L.cc_train_step.restype = C.c_int
@@ -280,6 +293,26 @@ def cc_decode(desc, latents_ptr, up_w: np.ndarray, syn_w: np.ndarray, out_ptr, w
     sw = np.ascontiguousarray(syn_w, np.float32)
     _check(load().cc_decode(C.byref(desc), latents_ptr, uw.ctypes.data, sw.ctypes.data, out_ptr, ws_ptr, ws_bytes,
                             stream_ptr), "cc_decode")
+
+
+def analysis_desc(acfg, tf32=False) -> CcAnalysisDesc:
+    return CcAnalysisDesc(acfg.H, acfg.W, acfg.L, acfg.C, acfg.blocks, int(bool(tf32)))
+
+
+def cc_analysis_param_count(ad: CcAnalysisDesc) -> int:
+    n = load().cc_analysis_param_count(C.byref(ad))
+    if n < 0:
+        raise CcError(CC_EINVAL, "cc_analysis_param_count")
+    return n
+
+
+def cc_analysis_workspace_bytes(ad: CcAnalysisDesc) -> int:
+    return load().cc_analysis_workspace_bytes(C.byref(ad))
+
+
+def cc_analysis_forward(ad: CcAnalysisDesc, image_ptr, weights_ptr, latents_ptr, ws_ptr, ws_bytes, stream_ptr=0):
+    _check(load().cc_analysis_forward(C.byref(ad), image_ptr, weights_ptr, latents_ptr, ws_ptr, ws_bytes, stream_ptr),
+           "cc_analysis_forward")
 
 
 def cc_train_param_count(desc) -> int:

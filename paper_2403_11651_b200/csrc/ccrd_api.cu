@@ -855,6 +855,41 @@ int cc_train_step(const cc_model_desc* desc, float* params, const float* noise, 
   return cuda_check("cc_train_step");
 }
 
+// ---------------------------------------------------------------- analysis
+static int validate_analysis(const cc_analysis_desc* a) {
+  if (!a) return fail(CC_EINVAL, "null analysis descriptor");
+  if (a->H < 1 || a->W < 1 || a->L < 1 || a->L > CC_MAX_LEVELS || a->C < 1 || a->C > 512 || a->blocks < 1)
+    return fail(CC_EINVAL, "bad analysis descriptor (H %d, W %d, L %d, C %d, blocks %d)", a->H, a->W, a->L, a->C,
+                a->blocks);
+  if (a->tf32 != 0 && a->tf32 != 1) return fail(CC_EINVAL, "tf32 must be 0 or 1");
+  return CC_OK;
+}
+
+int64_t cc_analysis_param_count(const cc_analysis_desc* a) {
+  if (validate_analysis(a)) return -1;
+  return analysis_param_count(*a);
+}
+
+size_t cc_analysis_workspace_bytes(const cc_analysis_desc* a) {
+  if (validate_analysis(a)) return 0;
+  return analysis_workspace_bytes(*a);
+}
+
+int cc_analysis_forward(const cc_analysis_desc* a, const float* image, const float* weights, float* latents,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  int rc = validate_analysis(a);
+  if (rc) return rc;
+  if (!image || !weights || !latents) return fail(CC_EINVAL, "null image / weights / latents");
+  const size_t need = analysis_workspace_bytes(*a);
+  if (!workspace || workspace_bytes < need) return fail(CC_EWORKSPACE, "need %zu workspace bytes", need);
+  if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
+  const int n = analysis_forward_impl(*a, image, weights, latents, workspace, (cudaStream_t)stream);
+  if (n < 0) return fail(CC_ECUDA, "cuBLASLt matmul failed (%d)", n);
+  g_launches = n;
+  return cuda_check("cc_analysis_forward");
+}
+
 // ---------------------------------------------------------------- decode
 int cc_decode(const cc_model_desc* desc, const int16_t* latents, const float* up_w, const float* syn_w,
               uint8_t* out_rgb8, void* workspace, size_t workspace_bytes, void* stream) {

@@ -250,6 +250,12 @@ ArmLaunchFn find_arm_launcher(int C, int NH, int NHL);     // FFMA2 path (arm_ra
 ArmLaunchFn find_arm_tc_launcher(int C, int NH, int NHL);  // tensor-core path (arm_tc.cu)
 int device_sm_count();  // current device's SMs (lazily cached; 148 without a device)
 
+// N-O analysis transform (analysis.cu, NEXT-4)
+int64_t analysis_param_count(const cc_analysis_desc& a);
+size_t analysis_workspace_bytes(const cc_analysis_desc& a);
+int analysis_forward_impl(const cc_analysis_desc& a, const float* image, const float* w, float* lat, void* ws,
+                          cudaStream_t s);
+
 // training iteration (train.cu, NEXT-2)
 int64_t train_param_count(const cc_model_desc& d);
 size_t train_workspace_bytes(const cc_model_desc& d);
