@@ -242,12 +242,19 @@ int cc_decode(const cc_model_desc* desc, const int16_t* latents, const float* up
  * reading (A1-A7).  Weight blob: stem W[C][3], b[C]; per level, per
  * block: dw k[C][7][7], dw b[C], W1[4C][C], b1[4C], W2[C][4C], b2[C], then
  * (downsampling blocks only) Wid[C][C], bid[C]; per level: Wm[C], bm.
- * image: DEVICE [3][H][W] fp32; weights: DEVICE blob; latents: DEVICE fp32,
- * packed level after level (the decoder's ceil dims), continuous (rounding
- * belongs to the coder).  tf32 = 1 runs the point-wise GEMMs on TF32 tensor
- * cores (cuBLASLt), 0 in fp32. */
+ * N images share the one network (N-O: the same f_alpha for every image,
+ * PAPER.md:426-429).  image: DEVICE [N][3][H][W] fp32; weights: DEVICE blob;
+ * latents: DEVICE fp32 [N][n_lat], each image's grids packed level after
+ * level (the decoder's ceil dims), continuous (rounding belongs to the coder).  tf32 selects the arithmetic of the point-wise
+ * layers: 0 = fp32 (cuBLASLt GEMMs, CUBLAS_COMPUTE_32F); 1 = TF32 on the
+ * tcgen05 tensor cores, each block ONE fused kernel when C == 64 (depth-wise
+ * conv, both point-wise layers with the hidden layer kept in TMEM, residual
+ * and merge; analysis_tc.cu), else cuBLASLt TF32; 2 = TF32 cuBLASLt GEMMs
+ * unfused (the library baseline).  C: a multiple of 4 in [4, 512].  Operands of TF32 products are rounded to
+ * TF32 (10-bit mantissa), accumulation is fp32. */
 typedef struct {
   int32_t H, W, L, C, blocks, tf32;
+  int32_t N; /* images per call, >= 1 */
 } cc_analysis_desc;
 int64_t cc_analysis_param_count(const cc_analysis_desc* a);     /* -1 on error */
 size_t cc_analysis_workspace_bytes(const cc_analysis_desc* a);  /* 0 on error  */

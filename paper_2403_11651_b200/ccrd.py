@@ -70,7 +70,7 @@ class CcAdam(C.Structure):
 
 class CcAnalysisDesc(C.Structure):
     _fields_ = [("H", C.c_int32), ("W", C.c_int32), ("L", C.c_int32), ("C", C.c_int32), ("blocks", C.c_int32),
-                ("tf32", C.c_int32)]
+                ("tf32", C.c_int32), ("N", C.c_int32)]
 
 
 class CcProfileSummary(C.Structure):
@@ -295,8 +295,10 @@ def cc_decode(desc, latents_ptr, up_w: np.ndarray, syn_w: np.ndarray, out_ptr, w
                             stream_ptr), "cc_decode")
 
 
-def analysis_desc(acfg, tf32=False) -> CcAnalysisDesc:
-    return CcAnalysisDesc(acfg.H, acfg.W, acfg.L, acfg.C, acfg.blocks, int(bool(tf32)))
+def analysis_desc(acfg, tf32=0, n=1) -> CcAnalysisDesc:
+    """tf32: 0 fp32 | 1 (or True) TF32, fused tensor-core blocks | 2 TF32 cuBLASLt unfused;
+    n: images per call (one shared network)."""
+    return CcAnalysisDesc(acfg.H, acfg.W, acfg.L, acfg.C, acfg.blocks, int(tf32), int(n))
 
 
 def cc_analysis_param_count(ad: CcAnalysisDesc) -> int:

@@ -20,16 +20,22 @@ namespace ccrd {
 
 constexpr int AN_TB = 256;
 
+// one pixel per threadIdx.y, 4 channels per threadIdx.x (blockDim.x = C / 4)
 __global__ void an_stem_kernel(const float* __restrict__ img, const float* __restrict__ w, float* __restrict__ x,
                                int64_t P, int C) {
-  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= P * C) return;
-  const int64_t p = idx / C;
-  const int c = (int)(idx - p * C);
-  float a = w[C * 3 + c];
+  const int64_t p = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
+  if (p >= P) return;
+  const int c = 4 * threadIdx.x;
+  const float i0 = __ldg(img + p), i1 = __ldg(img + P + p), i2 = __ldg(img + 2 * P + p);
+  float o[4];
 #pragma unroll
-  for (int i = 0; i < 3; i++) a = fmaf(w[c * 3 + i], img[i * P + p], a);
-  x[idx] = a;
+  for (int e = 0; e < 4; e++) {
+    float a = __ldg(w + C * 3 + c + e);
+    a = fmaf(__ldg(w + (c + e) * 3), i0, a);
+    a = fmaf(__ldg(w + (c + e) * 3 + 1), i1, a);
+    o[e] = fmaf(__ldg(w + (c + e) * 3 + 2), i2, a);
+  }
+  *reinterpret_cast<float4*>(x + p * C + c) = make_float4(o[0], o[1], o[2], o[3]);
 }
 
 // depth-wise 7x7, stride s, zero padding 3; NHWC, one output (pixel, channel)
@@ -133,15 +139,18 @@ static int lt_gemm(int m, int64_t n, int k, const float* A, const float* B, cons
 
 // ---------------------------------------------------------------- plan
 struct AnPlan {
-  int64_t P0, n_params, n_lat;
+  int64_t P0, n_params, n_lat;  // n_lat: latents per image
   size_t o_x, o_y, o_t, o_h, o_pool, o_lt, total;
   size_t lt_bytes;
 };
 
 static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// x, y: the N images' activations (ping-pong); t0, h1, pool, cuBLASLt
+// workspace: one image at a time (unfused modes)
 static void an_plan(const cc_analysis_desc& a, AnPlan& pl) {
   const int C = a.C;
+  const int N = a.N;
   pl.P0 = (int64_t)a.H * a.W;
   pl.n_params = (int64_t)C * 3 + C;
   pl.n_lat = 0;
@@ -153,18 +162,19 @@ static void an_plan(const cc_analysis_desc& a, AnPlan& pl) {
     pl.n_params += C + 1;
     pl.n_lat += (int64_t)((a.H + (1 << l) - 1) >> l) * ((a.W + (1 << l) - 1) >> l);
   }
-  pl.lt_bytes = 32u << 20;
+  const bool fused = a.tf32 == 1 && C == 64;
+  pl.lt_bytes = fused ? 0 : (32u << 20);
   size_t o = 0;
   auto take = [&](size_t b) {
     const size_t r = o;
     o += a256(b);
     return r;
   };
-  pl.o_x = take(4 * (size_t)pl.P0 * C);
-  pl.o_y = take(4 * (size_t)pl.P0 * C);
-  pl.o_t = take(4 * (size_t)pl.P0 * C);
-  pl.o_h = take(4 * (size_t)pl.P0 * 4 * C);
-  pl.o_pool = take(4 * (size_t)((pl.P0 + 3) / 4 + a.W + a.H + 1) * C);
+  pl.o_x = take(4 * (size_t)pl.P0 * C * N);
+  pl.o_y = take(4 * (size_t)pl.P0 * C * N);
+  pl.o_t = take(fused ? 0 : 4 * (size_t)pl.P0 * C);
+  pl.o_h = take(fused ? 0 : 4 * (size_t)pl.P0 * 4 * C);
+  pl.o_pool = take(fused ? 0 : 4 * (size_t)((pl.P0 + 3) / 4 + a.W + a.H + 1) * C);
   pl.o_lt = take(pl.lt_bytes);
   pl.total = o;
 }
@@ -182,27 +192,25 @@ size_t analysis_workspace_bytes(const cc_analysis_desc& a) {
 
 static int blocks_of(int64_t n) { return (int)((n + AN_TB - 1) / AN_TB); }
 
-// Returns launches (>= 0) or a negative code (< -100: cuBLASLt status).
-int analysis_forward_impl(const cc_analysis_desc& a, const float* image, const float* w, float* lat, void* ws,
-                          cudaStream_t s) {
-  AnPlan pl;
-  an_plan(a, pl);
-  char* W = (char*)ws;
-  float* x = (float*)(W + pl.o_x);
-  float* y = (float*)(W + pl.o_y);
+static void launch_stem(const float* image, const float* w, float* x, int64_t P, int C, cudaStream_t s) {
+  const dim3 tb(C / 4, AN_TB / (C / 4));  // C % 4 == 0 (validated), C / 4 <= AN_TB
+  an_stem_kernel<<<(unsigned)((P + tb.y - 1) / tb.y), tb, 0, s>>>(image, w, x, P, C);
+}
+
+// One image through the unfused path (dw kernels + cuBLASLt GEMMs); x holds
+// the stem output.  Returns launches or a negative code.
+static int unfused_one(const cc_analysis_desc& a, const AnPlan& pl, const float* w, float* lat, float* x, float* y,
+                       char* W, cudaStream_t s) {
   float* t0 = (float*)(W + pl.o_t);
   float* h1 = (float*)(W + pl.o_h);
   float* pool = (float*)(W + pl.o_pool);
   void* ltws = W + pl.o_lt;
   const int C = a.C;
-  const bool tf32 = a.tf32 != 0;
+  const bool tf32 = a.tf32 != 0;  // 1 (C != 64) or 2: TF32 cuBLASLt
   int launches = 0, rc;
   int h = a.H, wd = a.W;
   int64_t P = pl.P0;
-  const float* q = w;
-  an_stem_kernel<<<blocks_of(P * C), AN_TB, 0, s>>>(image, q, x, P, C);
-  launches++;
-  q += C * 3 + C;
+  const float* q = w + C * 3 + C;
   int64_t loff = 0;
   for (int l = 0; l < a.L; l++) {
     for (int b = 0; b < a.blocks; b++) {
@@ -246,6 +254,57 @@ int analysis_forward_impl(const cc_analysis_desc& a, const float* image, const f
     launches++;
     q += C + 1;
     loff += P;
+  }
+  return launches;
+}
+
+// Returns launches (>= 0) or a negative code (< -100: cuBLASLt status).
+int analysis_forward_impl(const cc_analysis_desc& a, const float* image, const float* w, float* lat, void* ws,
+                          cudaStream_t s) {
+  AnPlan pl;
+  an_plan(a, pl);
+  char* W = (char*)ws;
+  float* x = (float*)(W + pl.o_x);
+  float* y = (float*)(W + pl.o_y);
+  const int C = a.C, N = a.N;
+  const int64_t P0 = pl.P0;
+  int launches = 0;
+  if (!(a.tf32 == 1 && C == 64)) {
+    for (int n = 0; n < N; n++) {
+      launch_stem(image + n * 3 * P0, w, x, P0, C, s);
+      const int r = unfused_one(a, pl, w, lat + n * pl.n_lat, x, y, W, s);
+      if (r < 0) return r;
+      launches += 1 + r;
+    }
+    return launches;
+  }
+  // fused tensor-core blocks (analysis_tc.cu), all N images per launch; the
+  // merge rides on each level's last block
+  for (int n = 0; n < N; n++) launch_stem(image + n * 3 * P0, w, x + n * P0 * C, P0, C, s);
+  launches += N;
+  const int sms = device_sm_count();
+  const float* q = w + C * 3 + C;
+  int h = a.H, wd = a.W;
+  int64_t loff = 0;
+  for (int l = 0; l < a.L; l++) {
+    for (int b = 0; b < a.blocks; b++) {
+      const bool down = l > 0 && b == 0;
+      const int ho = down ? (h + 1) / 2 : h, wo = down ? (wd + 1) / 2 : wd;
+      const float* blk = q;
+      q += (int64_t)C * 49 + C + 8LL * C * C + 4 * C + C + (down ? (int64_t)C * C + C : 0);
+      const bool last = b == a.blocks - 1;
+      if (analysis_block_tc(down, x, y, blk, last ? q : nullptr, last ? lat + loff : nullptr, h, wd, ho, wo, N,
+                            pl.n_lat, sms, s))
+        return -1;
+      launches++;
+      float* tmp = x;
+      x = y;
+      y = tmp;
+      h = ho;
+      wd = wo;
+    }
+    q += C + 1;
+    loff += (int64_t)h * wd;
   }
   return launches;
 }

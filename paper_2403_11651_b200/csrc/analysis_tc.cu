@@ -1,0 +1,639 @@
+// analysis_tc.cu -- one N-O ConvNeXt block of the analysis transform as ONE
+// persistent tcgen05 kernel (NEXT-4, TF32 mode, C = 64; PAPER.md:432-447,
+// readings A2/A3/A5 of DESIGN.md).
+//
+//   stride-1 block:      y = x + W2 ReLU(W1 dw(x) + b1) + b2
+//   downsampling block:  y = W2 ReLU(W1 dw_s2(x) + b1) + b2 + Wid pool(x) + bid
+//   (last block of a level, optional) latent = Wm . y + bm
+//
+// The unfused form (analysis.cu) streams t0 = dw(x) [P x C], the expansion
+// h [P x 4C] and its read-back through HBM: ~3.3 KB per pixel per block.
+// Here one CTA per SM keeps W1, W2 (and Wid) resident in shared memory and,
+// per tile of 4 x 32 output pixels (M = 128, one TMEM lane per pixel):
+//   1. depth-wise 7x7 on the CUDA cores (packed FFMA2, 2 channels x 8 pixels per thread;
+//      for downsampling blocks also the 2x2 mean pool) -> A tile in shared
+//      memory, K-major SWIZZLE_128B, rounded to TF32;
+//   2. tcgen05.mma SS: D1[128 x 256] (TMEM) = A x W1^T;
+//   3. epilogue in place: D1 <- tf32(ReLU(D1 + b1)) (tcgen05.ld / .st);
+//   4. tcgen05.mma TS (A = the hidden layer straight from TMEM):
+//      D2[128 x 64] = hidden x W2^T  (+ pool x Wid^T, SS, downsampling);
+//   5. epilogue: y = D2 + b2 (+ bid) (+ x), stored NHWC, and the level's C -> 1
+//      merge when requested.
+// HBM traffic per block: read x (+ halo, mostly L2 hits) and write y, 0.5 KB
+// per output pixel (2 KB/px in + 0.25 KB/px out for downsampling blocks).
+#include <cstdlib>
+
+#include "ccrd_common.cuh"
+#include "tcgen05.cuh"
+
+namespace ccrd {
+
+constexpr int BT_THREADS = 512;  // 16 warps: latency hiding for the depth-wise loads
+constexpr int BT_C = 64, BT_HID = 256;  // C = 64, expansion 4C (A2)
+constexpr int BT_TY = 4, BT_TX = 32;    // output tile: 4 rows x 32 pixels = MMA M 128
+
+struct BlockTcParams {
+  const float* in;   // x, NHWC [h][w][64]
+  float* out;        // y, NHWC [ho][wo][64]
+  const float* blk;  // block parameters: dw k[64][49], kb[64], W1[256][64], b1, W2[64][256], b2, (Wid[64][64], bid)
+  const float* wm;   // merge Wm[64], bm (nullable)
+  float* lat;        // latent grid [ho][wo] (nullable)
+  int h, w, ho, wo, tiles_x, n_tiles;
+  int tpi;                           // tiles per image (n_tiles = tpi x images)
+  int64_t in_img, out_img, lat_img;  // per-image strides (elements) of in, out, lat
+};
+
+// byte offset of element (r, k) of a K-major SWIZZLE_128B operand with R rows:
+// K split in 32-float (128-byte) atom columns of R x 128 bytes each
+__host__ __device__ constexpr uint32_t sw128(int r, int k, int R) {
+  return (uint32_t)((k >> 5) * (R * 128) + (r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 2) & 7) ^ (r & 7)) << 4) +
+                    (k & 3) * 4);
+}
+
+constexpr int XS_LD = 68;  // padded row: quarter-warp float4 reads hit distinct banks
+
+template <bool DOWN>
+struct BtSmem {
+  static constexpr uint32_t W1 = 0;                              // [256 x 64]
+  static constexpr uint32_t W2 = W1 + BT_HID * BT_C * 4;         // [64 x 256]
+  static constexpr uint32_t A1 = W2 + BT_C * BT_HID * 4;         // [128 x 64] dw output
+  static constexpr uint32_t AP = A1 + 128 * BT_C * 4;            // [128 x 64] pool (downsampling)
+  static constexpr uint32_t WID = AP + (DOWN ? 128 * BT_C * 4 : 0);  // [64 x 64]
+  static constexpr uint32_t B1 = WID + (DOWN ? BT_C * BT_C * 4 : 0);
+  static constexpr uint32_t B2 = B1 + BT_HID * 4;
+  static constexpr uint32_t WM = B2 + BT_C * 4;
+  static constexpr uint32_t MP = WM + BT_C * 4;                  // merge partials [4][128]
+  static constexpr uint32_t WK = MP + 4 * 128 * 4;               // dw weights [49][32] channel pairs
+  static constexpr uint32_t XS = WK + 49 * 32 * 8;               // residual x tile [128][68] (stride 1)
+  static constexpr uint32_t BAR = XS + (DOWN ? 0 : 128 * XS_LD * 4);  // 2 mbarriers
+  static constexpr uint32_t SLOT = BAR + 16;
+  static constexpr uint32_t TOTAL = SLOT + 16 + 1024;            // + alignment slack
+};
+
+// instruction descriptor: D f32, A/B tf32, both K-major, M = 128
+__host__ __device__ constexpr uint32_t bt_idesc(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ uint64_t ldg_f2(const float* p) { return ldp2(__ldg(reinterpret_cast<const float2*>(p))); }
+
+template <bool DOWN>
+__global__ void __launch_bounds__(BT_THREADS, 1) an_block_tc_kernel(const __grid_constant__ BlockTcParams p) {
+  using S = BtSmem<DOWN>;
+  extern __shared__ uint8_t bt_raw[];
+  uint8_t* sm = bt_raw + ((1024u - (smem_u32(bt_raw) & 1023u)) & 1023u);
+  const uint32_t su = smem_u32(sm);
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  float* b1s = reinterpret_cast<float*>(sm + S::B1);
+  float* b2s = reinterpret_cast<float*>(sm + S::B2);
+  float* wms = reinterpret_cast<float*>(sm + S::WM);
+  float* mp = reinterpret_cast<float*>(sm + S::MP);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::BAR);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(sm + S::SLOT);
+
+  const float* dk = p.blk;
+  const float* dkb = dk + BT_C * 49;
+  const float* W1 = dkb + BT_C;
+  const float* b1 = W1 + BT_HID * BT_C;
+  const float* W2 = b1 + BT_HID;
+  const float* b2 = W2 + BT_C * BT_HID;
+  const float* Wid = b2 + BT_C;
+  const float* bid = Wid + BT_C * BT_C;
+
+  // ---- resident operands: weights -> shared memory (TF32, swizzled), biases.
+  // Unrolled loads, all of a thread's in flight at once; scalar because a
+  // block's parameters are only 4-byte aligned in the blob (65-float merges).
+  {
+    constexpr int N1 = BT_HID * BT_C / 4 / BT_THREADS;  // 8 groups of 4 per thread per matrix
+    float4 a[N1], b[N1];
+#pragma unroll
+    for (int u = 0; u < N1; u++) {
+      const float* pa = W1 + 4 * (t + u * BT_THREADS);
+      const float* pb = W2 + 4 * (t + u * BT_THREADS);
+      a[u] = make_float4(__ldg(pa), __ldg(pa + 1), __ldg(pa + 2), __ldg(pa + 3));
+      b[u] = make_float4(__ldg(pb), __ldg(pb + 1), __ldg(pb + 2), __ldg(pb + 3));
+    }
+#pragma unroll
+    for (int u = 0; u < N1; u++) {
+      const int i = 4 * (t + u * BT_THREADS);  // W1 [256][64], W2 [64][256]; k = i & .. is a multiple of 4
+      *reinterpret_cast<float4*>(sm + S::W1 + sw128(i >> 6, i & 63, BT_HID)) =
+          make_float4(tf32_rna(a[u].x), tf32_rna(a[u].y), tf32_rna(a[u].z), tf32_rna(a[u].w));
+      *reinterpret_cast<float4*>(sm + S::W2 + sw128(i >> 8, i & 255, BT_C)) =
+          make_float4(tf32_rna(b[u].x), tf32_rna(b[u].y), tf32_rna(b[u].z), tf32_rna(b[u].w));
+    }
+    if constexpr (DOWN) {
+#pragma unroll
+      for (int u = 0; u < BT_C * BT_C / 4 / BT_THREADS; u++) {
+        const int i = 4 * (t + u * BT_THREADS);
+        const float* pc = Wid + i;
+        const float4 c = make_float4(__ldg(pc), __ldg(pc + 1), __ldg(pc + 2), __ldg(pc + 3));
+        *reinterpret_cast<float4*>(sm + S::WID + sw128(i >> 6, i & 63, BT_C)) =
+            make_float4(tf32_rna(c.x), tf32_rna(c.y), tf32_rna(c.z), tf32_rna(c.w));
+      }
+    }
+  }
+  // depth-wise weights, channel-pair interleaved: wks[tap][cp] = (k[2cp][tap], k[2cp+1][tap])
+  float2* wks = reinterpret_cast<float2*>(sm + S::WK);
+  for (int i = t; i < 49 * 32; i += BT_THREADS) {
+    const int tap = i >> 5, c2 = i & 31;
+    wks[i] = make_float2(__ldg(dk + (2 * c2) * 49 + tap), __ldg(dk + (2 * c2 + 1) * 49 + tap));
+  }
+  if (t < BT_HID) b1s[t] = __ldg(b1 + t);
+  if (t < BT_C) {
+    b2s[t] = __ldg(b2 + t) + (DOWN ? __ldg(bid + t) : 0.0f);
+    wms[t] = p.wm ? __ldg(p.wm + t) : 0.0f;
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar + 1)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *slot;                                       // D1 / hidden: columns 0..255
+  const uint32_t tmem_d2 = tmem + BT_HID;                            // D2: columns 256..319
+  const uint32_t tlane = tmem + ((uint32_t)((warp & 3) * 32) << 16);  // this warp's lane quarter
+
+  // depth-wise mapping: channel pair cp = lane, output row ry, 8-pixel group xq
+  const int cp = lane, ry = warp & 3, xq = warp >> 2;
+  const uint64_t kb2 = f2pack(__ldg(dkb + 2 * cp), __ldg(dkb + 2 * cp + 1));
+  const float bm = p.wm ? __ldg(p.wm + BT_C) : 0.0f;
+  float* xs = reinterpret_cast<float*>(sm + S::XS);
+
+  constexpr int STR = DOWN ? 2 : 1;
+  constexpr int NX = STR * 7 + 7;  // input columns under 8 outputs (14 or 21)
+  uint32_t ph = 0;
+#pragma unroll 1
+  for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+    const int img = tile / p.tpi, tr = tile - img * p.tpi;
+    const int ty = tr / p.tiles_x, tx = tr - ty * p.tiles_x;
+    const int oy = ty * BT_TY + ry, ox0 = tx * BT_TX + xq * 8;
+    const float* pin = p.in + img * p.in_img;
+    float* pout = p.out + img * p.out_img;
+    float* plat = p.lat ? p.lat + img * p.lat_img : nullptr;
+
+    // ---- 1. depth-wise 7x7 (zero padding 3) of outputs (oy, ox0 .. ox0+7)
+    uint64_t acc[8], ps[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      acc[j] = kb2;
+      ps[j] = 0;
+    }
+    const int gx0 = STR * ox0 - 3;
+    const bool interior = gx0 >= 0 && gx0 + NX <= p.w;  // warp-uniform: no column checks
+#pragma unroll
+    for (int ky = 0; ky < 7; ky++) {
+      const int iy = STR * oy + ky - 3;
+      if (iy < 0 || iy >= p.h) continue;  // zero padding rows (warp-uniform)
+      const float* row = pin + ((int64_t)iy * p.w + gx0) * BT_C + 2 * cp;
+      uint64_t v[NX];
+      if (interior) {
+#pragma unroll
+        for (int ix = 0; ix < NX; ix++) v[ix] = ldg_f2(row + ix * BT_C);
+      } else {
+#pragma unroll
+        for (int ix = 0; ix < NX; ix++) {
+          v[ix] = 0ull;
+          if (gx0 + ix >= 0 && gx0 + ix < p.w) v[ix] = ldg_f2(row + ix * BT_C);
+        }
+      }
+      if constexpr (!DOWN) {
+        if (ky == 3) {  // the centre row: this tile's residual x
+#pragma unroll
+          for (int j = 0; j < 8; j++)
+            *reinterpret_cast<uint64_t*>(xs + (ry * 32 + xq * 8 + j) * XS_LD + 2 * cp) = v[j + 3];
+        }
+      } else {
+        if (ky == 3 || ky == 4) {
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            ps[j] = ffma2(v[2 * j + 3], f2pack(1.0f, 1.0f), ps[j]);
+            ps[j] = ffma2(v[2 * j + 4], f2pack(1.0f, 1.0f), ps[j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int kx = 0; kx < 7; kx++) {
+        const uint64_t wv = ldp2(wks[(ky * 7 + kx) * 32 + cp]);
+#pragma unroll
+        for (int j = 0; j < 8; j++) acc[j] = ffma2(v[STR * j + kx], wv, acc[j]);
+      }
+    }
+    if constexpr (!DOWN) {
+      if (oy < 0 || oy >= p.h) {  // rows below the image: residual 0 (never stored)
+#pragma unroll
+        for (int j = 0; j < 8; j++) *reinterpret_cast<uint64_t*>(xs + (ry * 32 + xq * 8 + j) * XS_LD + 2 * cp) = 0ull;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const int r = ry * 32 + xq * 8 + j;
+      const float2 a = f2unpack(acc[j]);
+      *reinterpret_cast<float2*>(sm + S::A1 + sw128(r, 2 * cp, 128)) = make_float2(tf32_rna(a.x), tf32_rna(a.y));
+      if constexpr (DOWN) {
+        // mean over the in-image samples of the 2x2 window (ceil mode, A3)
+        const int ox = ox0 + j;
+        const float inv = 1.0f / (float)(((2 * oy + 1 < p.h) ? 2 : 1) * ((2 * ox + 1 < p.w) ? 2 : 1));
+        const float2 q = f2unpack(ps[j]);
+        *reinterpret_cast<float2*>(sm + S::AP + sw128(r, 2 * cp, 128)) =
+            make_float2(tf32_rna(q.x * inv), tf32_rna(q.y * inv));
+      }
+    }
+
+    // ---- 2. D1 = A x W1^T   (M 128, N 256, K 64: 8 MMAs of K 8)
+    asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (t == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int s = 0; s < 8; s++)
+        mma_tf32(tmem, umma_desc_sw128(su + S::A1 + (s >> 2) * (128 * 128) + (s & 3) * 32),
+                 umma_desc_sw128(su + S::W1 + (s >> 2) * (BT_HID * 128) + (s & 3) * 32), bt_idesc(BT_HID), s > 0);
+      mma_commit(bar);
+    }
+    mbar_wait(bar, ph);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+
+    // ---- 3. hidden = tf32(ReLU(D1 + b1)), in place in TMEM
+#pragma unroll 1
+    for (int cc = 0; cc < 2; cc++) {
+      const int col = (warp >> 2) * 64 + cc * 32;
+      float v[32];
+      tmem_row<32>(tlane + col, v);
+#pragma unroll
+      for (int j = 0; j < 32; j++) v[j] = tf32_rna(fmaxf(v[j] + b1s[col + j], 0.0f));
+      tmem_st32(tlane + col, v);
+    }
+    tmem_wait_st();
+
+    // ---- 4. D2 = hidden x W2^T (TS, K 256) (+ pool x Wid^T, SS, K 64)
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (t == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int s = 0; s < 32; s++)
+        mma_tf32_ts(tmem_d2, tmem + 8 * s, umma_desc_sw128(su + S::W2 + (s >> 2) * (BT_C * 128) + (s & 3) * 32),
+                    bt_idesc(BT_C), s > 0);
+      if constexpr (DOWN) {
+#pragma unroll
+        for (int s = 0; s < 8; s++)
+          mma_tf32(tmem_d2, umma_desc_sw128(su + S::AP + (s >> 2) * (128 * 128) + (s & 3) * 32),
+                   umma_desc_sw128(su + S::WID + (s >> 2) * (BT_C * 128) + (s & 3) * 32), bt_idesc(BT_C), 1);
+      }
+      mma_commit(bar + 1);
+    }
+    mbar_wait(bar + 1, ph);
+    ph ^= 1;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+
+    // ---- 5. y = D2 + b2 (+ bid) (+ x); pixel = TMEM lane = (row warp&3, column lane),
+    //         16 channels per warp (quarter cq = warp >> 2)
+    {
+      const int cq = warp >> 2, r = (warp & 3) * 32 + lane;
+      float d[16];
+      tmem_row<16>(tlane + BT_HID + cq * 16, d);
+      const int oy2 = ty * BT_TY + (warp & 3), ox2 = tx * BT_TX + lane;
+      float part = 0.0f;
+      if (oy2 < p.ho && ox2 < p.wo) {
+        float4* o = reinterpret_cast<float4*>(pout + ((int64_t)oy2 * p.wo + ox2) * BT_C + cq * 16);
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const int c = cq * 16 + 4 * i;
+          float4 y = make_float4(d[4 * i] + b2s[c], d[4 * i + 1] + b2s[c + 1], d[4 * i + 2] + b2s[c + 2],
+                                 d[4 * i + 3] + b2s[c + 3]);
+          if constexpr (!DOWN) {
+            const float4 x = *reinterpret_cast<const float4*>(xs + r * XS_LD + c);
+            y.x += x.x;
+            y.y += x.y;
+            y.z += x.z;
+            y.w += x.w;
+          }
+          o[i] = y;
+          part = fmaf(wms[c], y.x, part);
+          part = fmaf(wms[c + 1], y.y, part);
+          part = fmaf(wms[c + 2], y.z, part);
+          part = fmaf(wms[c + 3], y.w, part);
+        }
+      }
+      if (plat) mp[cq * 128 + r] = part;
+    }
+    // TMEM D1/D2 and the A tiles are rewritten by the next tile
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (plat && t < 128) {
+      const int oy2 = ty * BT_TY + (t >> 5), ox2 = tx * BT_TX + (t & 31);
+      if (oy2 < p.ho && ox2 < p.wo) plat[(int64_t)oy2 * p.wo + ox2] = ((mp[t] + mp[128 + t]) + (mp[256 + t] + mp[384 + t])) + bm;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ---------------------------------------------------------------- warp-specialised stride-1 block
+// Same arithmetic as an_block_tc_kernel<false>, pipelined across tiles:
+//   warps 0-7  (depth-wise): dw of tile i -> A[i % 2] (double buffer) -> arrive A_full
+//   warps 8-15 (epilogue, one per TMEM lane quarter x column half); lane 0 of
+//              warp 8 issues the MMAs:
+//     MMA1(i) once A_full[i % 2] and MMA2(i-1) completed; commits D1_full and A_empty[i % 2]
+//     epi2(i-1) (overlaps MMA1(i)), epi1(i), then MMA2(i) -> D2_full
+// so the tensor cores and the epilogue run under the depth-wise work of the
+// next tiles.  The residual x is re-read from L2 in epi2.
+struct WsSmem {
+  static constexpr uint32_t W1 = 0;
+  static constexpr uint32_t W2 = W1 + BT_HID * BT_C * 4;
+  static constexpr uint32_t A = W2 + BT_C * BT_HID * 4;  // 2 x [128 x 64]
+  static constexpr uint32_t B1 = A + 2 * 128 * BT_C * 4;
+  static constexpr uint32_t B2 = B1 + BT_HID * 4;
+  static constexpr uint32_t WM = B2 + BT_C * 4;
+  static constexpr uint32_t MP = WM + BT_C * 4;          // merge partials [2][128]
+  static constexpr uint32_t WK = MP + 2 * 128 * 4;
+  static constexpr uint32_t BAR = WK + 49 * 32 * 8;      // A_full[2], A_empty[2], D1_full, D2_full
+  static constexpr uint32_t SLOT = BAR + 6 * 8;
+  static constexpr uint32_t TOTAL = SLOT + 16 + 1024;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+__global__ void __launch_bounds__(BT_THREADS, 1) an_block_ws_kernel(const __grid_constant__ BlockTcParams p) {
+  using S = WsSmem;
+  extern __shared__ uint8_t bt_raw[];
+  uint8_t* sm = bt_raw + ((1024u - (smem_u32(bt_raw) & 1023u)) & 1023u);
+  const uint32_t su = smem_u32(sm);
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  float* b1s = reinterpret_cast<float*>(sm + S::B1);
+  float* b2s = reinterpret_cast<float*>(sm + S::B2);
+  float* wms = reinterpret_cast<float*>(sm + S::WM);
+  float* mp = reinterpret_cast<float*>(sm + S::MP);
+  float2* wks = reinterpret_cast<float2*>(sm + S::WK);
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(sm + S::BAR);
+  uint64_t* a_empty = a_full + 2;
+  uint64_t* d1_full = a_full + 4;
+  uint64_t* d2_full = a_full + 5;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(sm + S::SLOT);
+
+  const float* dk = p.blk;
+  const float* dkb = dk + BT_C * 49;
+  const float* W1 = dkb + BT_C;
+  const float* b1 = W1 + BT_HID * BT_C;
+  const float* W2 = b1 + BT_HID;
+  const float* b2 = W2 + BT_C * BT_HID;
+  {
+    constexpr int N1 = BT_HID * BT_C / 4 / BT_THREADS;
+    float4 a[N1], b[N1];
+#pragma unroll
+    for (int u = 0; u < N1; u++) {
+      const float* pa = W1 + 4 * (t + u * BT_THREADS);
+      const float* pb = W2 + 4 * (t + u * BT_THREADS);
+      a[u] = make_float4(__ldg(pa), __ldg(pa + 1), __ldg(pa + 2), __ldg(pa + 3));
+      b[u] = make_float4(__ldg(pb), __ldg(pb + 1), __ldg(pb + 2), __ldg(pb + 3));
+    }
+#pragma unroll
+    for (int u = 0; u < N1; u++) {
+      const int i = 4 * (t + u * BT_THREADS);
+      *reinterpret_cast<float4*>(sm + S::W1 + sw128(i >> 6, i & 63, BT_HID)) =
+          make_float4(tf32_rna(a[u].x), tf32_rna(a[u].y), tf32_rna(a[u].z), tf32_rna(a[u].w));
+      *reinterpret_cast<float4*>(sm + S::W2 + sw128(i >> 8, i & 255, BT_C)) =
+          make_float4(tf32_rna(b[u].x), tf32_rna(b[u].y), tf32_rna(b[u].z), tf32_rna(b[u].w));
+    }
+  }
+  for (int i = t; i < 49 * 32; i += BT_THREADS) {
+    const int tap = i >> 5, c2 = i & 31;
+    wks[i] = make_float2(__ldg(dk + (2 * c2) * 49 + tap), __ldg(dk + (2 * c2 + 1) * 49 + tap));
+  }
+  if (t < BT_HID) b1s[t] = __ldg(b1 + t);
+  if (t < BT_C) {
+    b2s[t] = __ldg(b2 + t);
+    wms[t] = p.wm ? __ldg(p.wm + t) : 0.0f;
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (t == 0) {
+    for (int k = 0; k < 2; k++) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(smem_u32(a_full + k)));  // 8 dw warps
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(a_empty + k)));
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(d1_full)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(d2_full)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *slot;
+  const uint32_t tmem_d2 = tmem + BT_HID;
+  const uint32_t tlane = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+
+  if (warp < 8) {
+    // ================= depth-wise producers: channel pair lane, row warp&3, 16 pixels
+    const int cp = lane, ry = warp & 3, xh = warp >> 2;
+    const uint64_t kb2 = f2pack(__ldg(dkb + 2 * cp), __ldg(dkb + 2 * cp + 1));
+    int i = 0;
+#pragma unroll 1
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, i++) {
+      const int b = i & 1;
+      if (i >= 2) mbar_wait(a_empty + b, ((i >> 1) - 1) & 1);
+      const int img = tile / p.tpi, tr = tile - img * p.tpi;
+      const int ty = tr / p.tiles_x, tx = tr - ty * p.tiles_x;
+      const int oy = ty * BT_TY + ry, ox0 = tx * BT_TX + xh * 16;
+      const float* pin = p.in + img * p.in_img;
+      uint64_t acc[16];
+#pragma unroll
+      for (int j = 0; j < 16; j++) acc[j] = kb2;
+      const int gx0 = ox0 - 3;
+      const bool interior = gx0 >= 0 && gx0 + 22 <= p.w;
+#pragma unroll
+      for (int ky = 0; ky < 7; ky++) {
+        const int iy = oy + ky - 3;
+        if (iy < 0 || iy >= p.h) continue;
+        const float* row = pin + ((int64_t)iy * p.w + gx0) * BT_C + 2 * cp;
+        uint64_t v[22];
+        if (interior) {
+#pragma unroll
+          for (int ix = 0; ix < 22; ix++) v[ix] = ldg_f2(row + ix * BT_C);
+        } else {
+#pragma unroll
+          for (int ix = 0; ix < 22; ix++) {
+            v[ix] = 0ull;
+            if (gx0 + ix >= 0 && gx0 + ix < p.w) v[ix] = ldg_f2(row + ix * BT_C);
+          }
+        }
+#pragma unroll
+        for (int kx = 0; kx < 7; kx++) {
+          const uint64_t wv = ldp2(wks[(ky * 7 + kx) * 32 + cp]);
+#pragma unroll
+          for (int j = 0; j < 16; j++) acc[j] = ffma2(v[j + kx], wv, acc[j]);
+        }
+      }
+      uint8_t* A = sm + S::A + b * (128 * BT_C * 4);
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        const float2 a = f2unpack(acc[j]);
+        *reinterpret_cast<float2*>(A + sw128(ry * 32 + xh * 16 + j, 2 * cp, 128)) =
+            make_float2(tf32_rna(a.x), tf32_rna(a.y));
+      }
+      asm volatile("fence.proxy.async.shared::cta;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_full + b);
+    }
+  } else {
+    // ================= MMA issue + epilogues
+    const int e = warp - 8, hh = e >> 2, q = e & 3;
+    const bool leader = (e == 0 && lane == 0);
+    const float bm = p.wm ? __ldg(p.wm + BT_C) : 0.0f;
+    int i = 0, prev = -1;
+#pragma unroll 1
+    for (int tile = blockIdx.x;; tile += gridDim.x, i++) {
+      const bool has = tile < p.n_tiles;
+      if (leader && has) {
+        mbar_wait(a_full + (i & 1), (i >> 1) & 1);
+        if (i >= 1) mbar_wait(d2_full, (i - 1) & 1);  // MMA2(i-1) consumed the hidden layer in D1
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t a_u = su + S::A + (i & 1) * (128 * BT_C * 4);
+#pragma unroll
+        for (int s = 0; s < 8; s++)
+          mma_tf32(tmem, umma_desc_sw128(a_u + (s >> 2) * (128 * 128) + (s & 3) * 32),
+                   umma_desc_sw128(su + S::W1 + (s >> 2) * (BT_HID * 128) + (s & 3) * 32), bt_idesc(BT_HID), s > 0);
+        mma_commit(d1_full);
+        mma_commit(a_empty + (i & 1));
+      }
+      __syncwarp();
+      if (prev >= 0) {
+        // ---- epi2(prev): y = D2 + b2 + x
+        mbar_wait(d2_full, (i - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        float d[32];
+        tmem_row<32>(tlane + BT_HID + hh * 32, d);
+        const int pimg = prev / p.tpi, ptr = prev - pimg * p.tpi;
+        const int pty = ptr / p.tiles_x, ptx = ptr - pty * p.tiles_x;
+        const float* pin = p.in + pimg * p.in_img;
+        float* pout = p.out + pimg * p.out_img;
+        float* plat = p.lat ? p.lat + pimg * p.lat_img : nullptr;
+        const int oy2 = pty * BT_TY + q, ox2 = ptx * BT_TX + lane;
+        float part = 0.0f;
+        if (oy2 < p.ho && ox2 < p.wo) {
+          const int64_t po = ((int64_t)oy2 * p.wo + ox2) * BT_C + hh * 32;
+          const float4* xr = reinterpret_cast<const float4*>(pin + po);
+          float4* o = reinterpret_cast<float4*>(pout + po);
+          float4 xv[8];
+#pragma unroll
+          for (int u = 0; u < 8; u++) xv[u] = __ldg(xr + u);
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            const int c = hh * 32 + 4 * u;
+            const float4 y = make_float4(d[4 * u] + b2s[c] + xv[u].x, d[4 * u + 1] + b2s[c + 1] + xv[u].y,
+                                         d[4 * u + 2] + b2s[c + 2] + xv[u].z, d[4 * u + 3] + b2s[c + 3] + xv[u].w);
+            o[u] = y;
+            part = fmaf(wms[c], y.x, part);
+            part = fmaf(wms[c + 1], y.y, part);
+            part = fmaf(wms[c + 2], y.z, part);
+            part = fmaf(wms[c + 3], y.w, part);
+          }
+        }
+        if (plat) {
+          mp[hh * 128 + q * 32 + lane] = part;
+          epi_sync();
+          const int te = e * 32 + lane;
+          if (te < 128) {
+            const int oy3 = pty * BT_TY + (te >> 5), ox3 = ptx * BT_TX + (te & 31);
+            if (oy3 < p.ho && ox3 < p.wo) plat[(int64_t)oy3 * p.wo + ox3] = (mp[te] + mp[128 + te]) + bm;
+          }
+        }
+      }
+      if (!has) break;
+      // ---- epi1(i): hidden = tf32(ReLU(D1 + b1)) in place
+      mbar_wait(d1_full, i & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+      for (int cc = 0; cc < 4; cc++) {
+        const int col = hh * 128 + cc * 32;
+        float v[32];
+        tmem_row<32>(tlane + col, v);
+#pragma unroll
+        for (int j = 0; j < 32; j++) v[j] = tf32_rna(fmaxf(v[j] + b1s[col + j], 0.0f));
+        tmem_st32(tlane + col, v);
+      }
+      tmem_wait_st();
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      epi_sync();  // also: every epi2(prev) read of D2 and of mp is done
+      if (leader) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+        for (int s = 0; s < 32; s++)
+          mma_tf32_ts(tmem_d2, tmem + 8 * s, umma_desc_sw128(su + S::W2 + (s >> 2) * (BT_C * 128) + (s & 3) * 32),
+                      bt_idesc(BT_C), s > 0);
+        mma_commit(d2_full);
+      }
+      __syncwarp();
+      prev = tile;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ---------------------------------------------------------------- launcher
+template <bool DOWN>
+static int launch_block_tc(const BlockTcParams& p, int sm_count, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(an_block_tc_kernel<DOWN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)BtSmem<DOWN>::TOTAL) != cudaSuccess)
+      return -1;
+    attr = true;
+  }
+  const int grid = p.n_tiles < sm_count ? p.n_tiles : sm_count;
+  an_block_tc_kernel<DOWN><<<grid, BT_THREADS, BtSmem<DOWN>::TOTAL, s>>>(p);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
+int analysis_block_tc(bool down, const float* in, float* out, const float* blk, const float* wm, float* lat, int h,
+                      int w, int ho, int wo, int n_img, int64_t lat_img, int sm_count, cudaStream_t s) {
+  BlockTcParams p;
+  p.in = in;
+  p.out = out;
+  p.blk = blk;
+  p.wm = wm;
+  p.lat = lat;
+  p.h = h;
+  p.w = w;
+  p.ho = ho;
+  p.wo = wo;
+  p.tiles_x = (wo + BT_TX - 1) / BT_TX;
+  p.tpi = p.tiles_x * ((ho + BT_TY - 1) / BT_TY);
+  p.n_tiles = p.tpi * n_img;
+  p.in_img = (int64_t)h * w * BT_C;
+  p.out_img = (int64_t)ho * wo * BT_C;
+  p.lat_img = lat_img;
+  if (down) return launch_block_tc<true>(p, sm_count, s);
+  static const bool seq = getenv("CCRD_AN_SEQ") && getenv("CCRD_AN_SEQ")[0] == '1';  // A/B: sequential kernel
+  if (seq) return launch_block_tc<false>(p, sm_count, s);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(an_block_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WsSmem::TOTAL) !=
+        cudaSuccess)
+      return -1;
+    attr = true;
+  }
+  const int grid = p.n_tiles < sm_count ? p.n_tiles : sm_count;
+  an_block_ws_kernel<<<grid, BT_THREADS, WsSmem::TOTAL, s>>>(p);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace ccrd

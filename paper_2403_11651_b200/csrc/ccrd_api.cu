@@ -858,10 +858,12 @@ int cc_train_step(const cc_model_desc* desc, float* params, const float* noise, 
 // ---------------------------------------------------------------- analysis
 static int validate_analysis(const cc_analysis_desc* a) {
   if (!a) return fail(CC_EINVAL, "null analysis descriptor");
-  if (a->H < 1 || a->W < 1 || a->L < 1 || a->L > CC_MAX_LEVELS || a->C < 1 || a->C > 512 || a->blocks < 1)
+  if (a->H < 1 || a->W < 1 || a->L < 1 || a->L > CC_MAX_LEVELS || a->C < 4 || a->C > 512 || a->C % 4 || a->blocks < 1)
     return fail(CC_EINVAL, "bad analysis descriptor (H %d, W %d, L %d, C %d, blocks %d)", a->H, a->W, a->L, a->C,
                 a->blocks);
-  if (a->tf32 != 0 && a->tf32 != 1) return fail(CC_EINVAL, "tf32 must be 0 or 1");
+  if (a->tf32 < 0 || a->tf32 > 2) return fail(CC_EINVAL, "tf32 must be 0, 1 or 2");
+  if (a->N < 1 || (int64_t)a->N * a->H * a->W > ((int64_t)1 << 31) / 4)
+    return fail(CC_EINVAL, "bad analysis batch N %d (N H W must stay below 2^29)", a->N);
   return CC_OK;
 }
 

@@ -187,3 +187,28 @@ def test_strip_entry_errors_without_gpu():
         with pytest.raises(ccrd.CcError) as e:
             P.cc_rd_forward_strip(d, st, io, 8, 8, ws)
         assert e.value.code == ccrd.CC_ECUDA
+
+
+def test_analysis_entry_errors_without_gpu():
+    acfg = workload.ANALYSIS["no_kodak"]
+    ad = P.analysis_desc(acfg, 1, 4)
+    assert P.cc_analysis_param_count(ad) == acfg.n_params           # 787,719 (A1-A7)
+    ws4 = P.cc_analysis_workspace_bytes(ad)
+    ws1 = P.cc_analysis_workspace_bytes(P.analysis_desc(acfg, 1, 1))
+    assert ws4 >= 4 * 2 * acfg.H * acfg.W * acfg.C * 4 and ws1 < ws4   # x / y for the whole batch
+    # the unfused modes also hold one image's 4C expansion and the cuBLASLt workspace
+    assert P.cc_analysis_workspace_bytes(P.analysis_desc(acfg, 2, 1)) > ws1
+    for bad in (dict(N=0), dict(tf32=3), dict(C=6), dict(L=0), dict(blocks=0), dict(H=0)):
+        d = P.analysis_desc(acfg, 1, 1)
+        for k, v in bad.items():
+            setattr(d, k, v)
+        assert P.cc_analysis_workspace_bytes(d) == 0, bad
+        with pytest.raises(ccrd.CcError):
+            P.cc_analysis_param_count(d)
+    with pytest.raises(ccrd.CcError) as e:                             # workspace too small
+        P.cc_analysis_forward(ad, 8, 8, 8, 8, 16, 0)
+    assert e.value.code == ccrd.CC_EWORKSPACE
+    if not _has_gpu():
+        with pytest.raises(ccrd.CcError) as e:                         # no device: loud failure
+            P.cc_analysis_forward(ad, 8, 8, 8, 8, ws4, 0)
+        assert e.value.code == ccrd.CC_ECUDA
