@@ -493,8 +493,9 @@ def run_analysis(args, rk):
     out = {
         "metric": "N-O analysis transform (encoding forward) pixels/s", "value": value, "unit": "pixels/s",
         "n_gpus": rk.world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "tf32" if args.tf32 else "f32",
-        "mode": ["fp32 cuBLASLt", "TF32 fused tcgen05 block kernels", "TF32 cuBLASLt unfused"][args.tf32],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": ["f32", "tf32", "tf32", "f16-operand/f32-accumulate"][args.tf32],
+        "mode": ["fp32 cuBLASLt", "TF32 fused tcgen05 block kernels", "TF32 cuBLASLt unfused",
+                 "fused tcgen05 block kernels, FP16 operands, TMA-staged depth-wise"][args.tf32],
         "data": "synthetic",
         "config": {"workload": f"{acfg.name}: {n_img} x {acfg.H}x{acfg.W} per GPU in one call, C={C}, L={acfg.L}, "
                                f"{acfg.blocks} blocks/level", "kmac_per_pixel": round(macs / px / 1e3, 2),
@@ -504,7 +505,7 @@ def run_analysis(args, rk):
         "context": "paper: N-O encoding < 1 s per image (one forward pass, ~160 kMAC/px), hardware not stated",
         "e2e": {"value": rk.world * n_img * acfg.H * acfg.W * args.steps / (e2e_ms / 1e3), "unit": "pixels/s",
                 "h2d_bytes_per_step": h_img.numel() * 4, "d2h_bytes_per_step": h_lat.numel() * 4},
-        "gpu_launches": P.cc_last_launch_count() * args.steps,
+        "gpu_launches": P.ccrd.cc_last_launch_count() * args.steps,
         "clocks": sampler.summary(),
     }
     if rk.rank == 0:
@@ -684,8 +685,9 @@ def main():
     ap.add_argument("--train", action="store_true", help="time the encoder training iteration (NEXT-2)")
     ap.add_argument("--decode", action="store_true", help="time the decoder output stage (NEXT-3)")
     ap.add_argument("--analysis", default="", help="time the N-O analysis transform (NEXT-4): no_kodak | no_2k")
-    ap.add_argument("--tf32", type=int, default=1, choices=(0, 1, 2),
-                    help="analysis arithmetic: 0 fp32 cuBLASLt | 1 TF32 fused tcgen05 blocks | 2 TF32 cuBLASLt unfused")
+    ap.add_argument("--tf32", type=int, default=1, choices=(0, 1, 2, 3),
+                    help="analysis arithmetic: 0 fp32 cuBLASLt | 1 TF32 fused tcgen05 blocks | 2 TF32 cuBLASLt "
+                         "unfused | 3 fused, FP16 operands, TMA-staged depth-wise")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 breaks the timing rules", file=sys.stderr)

@@ -245,13 +245,17 @@ int cc_decode(const cc_model_desc* desc, const int16_t* latents, const float* up
  * N images share the one network (N-O: the same f_alpha for every image,
  * PAPER.md:426-429).  image: DEVICE [N][3][H][W] fp32; weights: DEVICE blob;
  * latents: DEVICE fp32 [N][n_lat], each image's grids packed level after
- * level (the decoder's ceil dims), continuous (rounding belongs to the coder).  tf32 selects the arithmetic of the point-wise
- * layers: 0 = fp32 (cuBLASLt GEMMs, CUBLAS_COMPUTE_32F); 1 = TF32 on the
- * tcgen05 tensor cores, each block ONE fused kernel when C == 64 (depth-wise
- * conv, both point-wise layers with the hidden layer kept in TMEM, residual
- * and merge; analysis_tc.cu), else cuBLASLt TF32; 2 = TF32 cuBLASLt GEMMs
- * unfused (the library baseline).  C: a multiple of 4 in [4, 512].  Operands of TF32 products are rounded to
- * TF32 (10-bit mantissa), accumulation is fp32. */
+ * level (the decoder's ceil dims), continuous (rounding belongs to the coder).
+ * C: a multiple of 4 in [4, 512].  tf32 selects the arithmetic of the
+ * point-wise layers: 0 = fp32 (cuBLASLt GEMMs, CUBLAS_COMPUTE_32F); 1 = TF32
+ * on the tcgen05 tensor cores, each block ONE fused kernel when C == 64
+ * (depth-wise conv, both point-wise layers with the hidden layer kept in TMEM,
+ * residual and merge; analysis_tc.cu), else cuBLASLt TF32; 2 = TF32 cuBLASLt
+ * GEMMs unfused (the library baseline); 3 = as 1 with FP16 tensor-core
+ * operands (the same 10-bit mantissa as TF32, 5-bit exponent: |values| <
+ * 65504) and a TMA-staged depth-wise stage in the stride-1 blocks
+ * (downsampling blocks stay TF32) -- the fast path.  Operands of the TF32 /
+ * FP16 products are rounded to 10-bit mantissas, accumulation is fp32. */
 typedef struct {
   int32_t H, W, L, C, blocks, tf32;
   int32_t N; /* images per call, >= 1 */

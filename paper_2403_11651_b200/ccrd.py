@@ -296,7 +296,8 @@ def cc_decode(desc, latents_ptr, up_w: np.ndarray, syn_w: np.ndarray, out_ptr, w
 
 
 def analysis_desc(acfg, tf32=0, n=1) -> CcAnalysisDesc:
-    """tf32: 0 fp32 | 1 (or True) TF32, fused tensor-core blocks | 2 TF32 cuBLASLt unfused;
+    """tf32: 0 fp32 | 1 (or True) TF32, fused tensor-core blocks | 2 TF32 cuBLASLt unfused |
+    3 fused with FP16 operands + TMA-staged depth-wise (stride-1 blocks);
     n: images per call (one shared network)."""
     return CcAnalysisDesc(acfg.H, acfg.W, acfg.L, acfg.C, acfg.blocks, int(tf32), int(n))
 

@@ -162,7 +162,7 @@ static void an_plan(const cc_analysis_desc& a, AnPlan& pl) {
     pl.n_params += C + 1;
     pl.n_lat += (int64_t)((a.H + (1 << l) - 1) >> l) * ((a.W + (1 << l) - 1) >> l);
   }
-  const bool fused = a.tf32 == 1 && C == 64;
+  const bool fused = (a.tf32 == 1 || a.tf32 == 3) && C == 64;
   pl.lt_bytes = fused ? 0 : (32u << 20);
   size_t o = 0;
   auto take = [&](size_t b) {
@@ -206,7 +206,7 @@ static int unfused_one(const cc_analysis_desc& a, const AnPlan& pl, const float*
   float* pool = (float*)(W + pl.o_pool);
   void* ltws = W + pl.o_lt;
   const int C = a.C;
-  const bool tf32 = a.tf32 != 0;  // 1 (C != 64) or 2: TF32 cuBLASLt
+  const bool tf32 = a.tf32 != 0;  // 1 / 3 (C != 64) or 2: TF32 cuBLASLt
   int launches = 0, rc;
   int h = a.H, wd = a.W;
   int64_t P = pl.P0;
@@ -269,7 +269,7 @@ int analysis_forward_impl(const cc_analysis_desc& a, const float* image, const f
   const int C = a.C, N = a.N;
   const int64_t P0 = pl.P0;
   int launches = 0;
-  if (!(a.tf32 == 1 && C == 64)) {
+  if (!((a.tf32 == 1 || a.tf32 == 3) && C == 64)) {
     for (int n = 0; n < N; n++) {
       launch_stem(image + n * 3 * P0, w, x, P0, C, s);
       const int r = unfused_one(a, pl, w, lat + n * pl.n_lat, x, y, W, s);
@@ -293,7 +293,7 @@ int analysis_forward_impl(const cc_analysis_desc& a, const float* image, const f
       const float* blk = q;
       q += (int64_t)C * 49 + C + 8LL * C * C + 4 * C + C + (down ? (int64_t)C * C + C : 0);
       const bool last = b == a.blocks - 1;
-      if (analysis_block_tc(down, x, y, blk, last ? q : nullptr, last ? lat + loff : nullptr, h, wd, ho, wo, N,
+      if (analysis_block_tc(a.tf32, down, x, y, blk, last ? q : nullptr, last ? lat + loff : nullptr, h, wd, ho, wo, N,
                             pl.n_lat, sms, s))
         return -1;
       launches++;

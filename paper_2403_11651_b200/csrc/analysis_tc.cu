@@ -21,6 +21,8 @@
 //      merge when requested.
 // HBM traffic per block: read x (+ halo, mostly L2 hits) and write y, 0.5 KB
 // per output pixel (2 KB/px in + 0.25 KB/px out for downsampling blocks).
+#include <cuda.h>
+
 #include <cstdlib>
 
 #include "ccrd_common.cuh"
@@ -588,6 +590,351 @@ __global__ void __launch_bounds__(BT_THREADS, 1) an_block_ws_kernel(const __grid
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// ---------------------------------------------------------------- FP16-operand, TMA-staged stride-1 block (mode 3)
+// The warp-specialised block with FP16 tensor-core operands (10-bit mantissa,
+// like TF32; fp32 accumulation): W1, W2 and the A tiles take half the shared
+// memory, which buys a double-buffered input stage.  One TMA per stage brings
+// [10 rows][38 px][32 channels] of x (the tile + the 3-pixel halo; the TMA
+// zero-fills out-of-image coordinates = the convolution's zero padding) into
+// shared memory; the depth-wise warps read it in register sliding windows
+// (8 pixels x 2 channels per thread, no bounds checks).  Two stages (channel
+// halves) per tile.
+constexpr int HS_ROWS = BT_TY + 6, HS_COLS = BT_TX + 6, HS_CH = 32;
+constexpr uint32_t HS_STAGE = HS_ROWS * HS_COLS * HS_CH * 4;  // 48,640 bytes
+
+struct H16Params {
+  CUtensorMap tin;  // x as [n][h][w][64] fp32, box {32, 38, 10, 1}
+  BlockTcParams p;
+};
+
+struct H16Smem {
+  static constexpr uint32_t W1 = 0;                          // [256 x 64] f16
+  static constexpr uint32_t W2 = W1 + BT_HID * BT_C * 2;     // [64 x 256] f16
+  static constexpr uint32_t A = W2 + BT_C * BT_HID * 2;      // 2 x [128 x 64] f16
+  static constexpr uint32_t ST = A + 2 * 128 * BT_C * 2;     // 2 input stages
+  static constexpr uint32_t B1 = ST + 2 * HS_STAGE;
+  static constexpr uint32_t B2 = B1 + BT_HID * 4;
+  static constexpr uint32_t WM = B2 + BT_C * 4;
+  static constexpr uint32_t MP = WM + BT_C * 4;
+  static constexpr uint32_t WK = MP + 2 * 128 * 4;
+  static constexpr uint32_t BAR = WK + 49 * 32 * 8;  // st_full[2], a_full[2], a_empty[2], d1_full, d2_full
+  static constexpr uint32_t SLOT = BAR + 8 * 8;
+  static constexpr uint32_t TOTAL = SLOT + 16 + 1024;
+};
+
+// K-major SWIZZLE_128B offset of 16-bit element (r, k): 64 elements per atom row
+__host__ __device__ constexpr uint32_t sw128h(int r, int k, int R) {
+  return (uint32_t)((k >> 6) * (R * 128) + (r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 3) & 7) ^ (r & 7)) << 4) +
+                    (k & 7) * 2);
+}
+// instruction descriptor kind::f16: D f32, A/B f16, K-major, M = 128
+__host__ __device__ constexpr uint32_t h16_idesc(int n) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                           uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+// {lo, hi} -> f16x2 (lo in the low half: the lower K index)
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void dw_sync() { asm volatile("bar.sync 2, 256;" ::: "memory"); }
+
+__global__ void __launch_bounds__(BT_THREADS, 1) an_block_h16_kernel(const __grid_constant__ H16Params hp) {
+  using S = H16Smem;
+  const BlockTcParams& p = hp.p;
+  extern __shared__ uint8_t bt_raw[];
+  uint8_t* sm = bt_raw + ((1024u - (smem_u32(bt_raw) & 1023u)) & 1023u);
+  const uint32_t su = smem_u32(sm);
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  float* b1s = reinterpret_cast<float*>(sm + S::B1);
+  float* b2s = reinterpret_cast<float*>(sm + S::B2);
+  float* wms = reinterpret_cast<float*>(sm + S::WM);
+  float* mp = reinterpret_cast<float*>(sm + S::MP);
+  float2* wks = reinterpret_cast<float2*>(sm + S::WK);
+  uint64_t* st_full = reinterpret_cast<uint64_t*>(sm + S::BAR);
+  uint64_t* a_full = st_full + 2;
+  uint64_t* a_empty = st_full + 4;
+  uint64_t* d1_full = st_full + 6;
+  uint64_t* d2_full = st_full + 7;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(sm + S::SLOT);
+
+  const float* dk = p.blk;
+  const float* dkb = dk + BT_C * 49;
+  const float* W1 = dkb + BT_C;
+  const float* b1 = W1 + BT_HID * BT_C;
+  const float* W2 = b1 + BT_HID;
+  const float* b2 = W2 + BT_C * BT_HID;
+  {
+    constexpr int N1 = BT_HID * BT_C / 4 / BT_THREADS;
+#pragma unroll
+    for (int u = 0; u < N1; u++) {
+      const int i = 4 * (t + u * BT_THREADS);
+      const float* pa = W1 + i;
+      const float* pb = W2 + i;
+      const float a0 = __ldg(pa), a1 = __ldg(pa + 1), a2 = __ldg(pa + 2), a3 = __ldg(pa + 3);
+      const float c0 = __ldg(pb), c1 = __ldg(pb + 1), c2 = __ldg(pb + 2), c3 = __ldg(pb + 3);
+      *reinterpret_cast<uint2*>(sm + S::W1 + sw128h(i >> 6, i & 63, BT_HID)) = make_uint2(pack_h2(a0, a1), pack_h2(a2, a3));
+      *reinterpret_cast<uint2*>(sm + S::W2 + sw128h(i >> 8, i & 255, BT_C)) = make_uint2(pack_h2(c0, c1), pack_h2(c2, c3));
+    }
+  }
+  for (int i = t; i < 49 * 32; i += BT_THREADS) {
+    const int tap = i >> 5, c2 = i & 31;
+    wks[i] = make_float2(__ldg(dk + (2 * c2) * 49 + tap), __ldg(dk + (2 * c2 + 1) * 49 + tap));
+  }
+  if (t < BT_HID) b1s[t] = __ldg(b1 + t);
+  if (t < BT_C) {
+    b2s[t] = __ldg(b2 + t);
+    wms[t] = p.wm ? __ldg(p.wm + t) : 0.0f;
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (t == 0) {
+    for (int k = 0; k < 2; k++) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(st_full + k)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(smem_u32(a_full + k)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(a_empty + k)));
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(d1_full)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(d2_full)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *slot;                 // D1: columns 0..255
+  const uint32_t tmem_h = tmem + BT_HID;       // hidden, f16x2: 256..383
+  const uint32_t tmem_d2 = tmem + BT_HID + 128;  // D2: 384..447
+  const uint32_t tlane = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+
+  if (warp < 8) {
+    // ================= depth-wise producers over the TMA stages
+    const int n_my = (p.n_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // tiles of this CTA
+    const int n_st = 2 * n_my;
+    auto issue = [&](int s) {  // stage s = (local tile s / 2, channel half s % 2) -> buffer s % 2
+      const int tile = blockIdx.x + (s >> 1) * gridDim.x;
+      const int img = tile / p.tpi, tr = tile - img * p.tpi;
+      const int ty = tr / p.tiles_x, tx = tr - ty * p.tiles_x;
+      mbar_expect_tx(st_full + (s & 1), HS_STAGE);
+      tma_load_4d(sm + S::ST + (s & 1) * HS_STAGE, &hp.tin, st_full + (s & 1), (s & 1) * HS_CH, tx * BT_TX - 3,
+                  ty * BT_TY - 3, img);
+    };
+    if (t == 0) {
+      issue(0);
+      if (n_st > 1) issue(1);
+    }
+    const int cp16 = lane & 15, ry = warp & 3, xg = ((warp >> 2) << 1) | (lane >> 4);
+#pragma unroll 1
+    for (int s = 0; s < n_st; s++) {
+      const int i = s >> 1, hf = s & 1;
+      const int cpair = hf * 16 + cp16;  // channel pair of this stage
+      mbar_wait(st_full + (s & 1), (s >> 1) & 1);
+      const float* stg = reinterpret_cast<const float*>(sm + S::ST + (s & 1) * HS_STAGE);
+      uint64_t acc[8];
+      {
+        const uint64_t kb2 = f2pack(__ldg(dkb + 2 * cpair), __ldg(dkb + 2 * cpair + 1));
+#pragma unroll
+        for (int j = 0; j < 8; j++) acc[j] = kb2;
+      }
+#pragma unroll
+      for (int ky = 0; ky < 7; ky++) {
+        const float* row = stg + ((ry + ky) * HS_COLS + xg * 8) * HS_CH + 2 * cp16;
+        uint64_t v[14];
+#pragma unroll
+        for (int ix = 0; ix < 14; ix++) v[ix] = *reinterpret_cast<const uint64_t*>(row + ix * HS_CH);
+#pragma unroll
+        for (int kx = 0; kx < 7; kx++) {
+          const uint64_t wv = ldp2(wks[(ky * 7 + kx) * 32 + cpair]);
+#pragma unroll
+          for (int j = 0; j < 8; j++) acc[j] = ffma2(v[j + kx], wv, acc[j]);
+        }
+      }
+      dw_sync();  // every depth-wise thread is done with this stage's buffer
+      if (t == 0 && s + 2 < n_st) issue(s + 2);
+      if (hf == 0 && i >= 2) mbar_wait(a_empty + (i & 1), ((i >> 1) - 1) & 1);
+      uint8_t* A = sm + S::A + (i & 1) * (128 * BT_C * 2);
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const float2 a = f2unpack(acc[j]);
+        *reinterpret_cast<uint32_t*>(A + sw128h(ry * 32 + xg * 8 + j, 2 * cpair, 128)) = pack_h2(a.x, a.y);
+      }
+      if (hf == 1) {
+        asm volatile("fence.proxy.async.shared::cta;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_full + (i & 1));
+      }
+    }
+  } else {
+    // ================= MMA issue + epilogues (as an_block_ws_kernel, f16 operands)
+    const int e = warp - 8, hh = e >> 2, q = e & 3;
+    const bool leader = (e == 0 && lane == 0);
+    const float bm = p.wm ? __ldg(p.wm + BT_C) : 0.0f;
+    int i = 0, prev = -1;
+#pragma unroll 1
+    for (int tile = blockIdx.x;; tile += gridDim.x, i++) {
+      const bool has = tile < p.n_tiles;
+      if (leader && has) {
+        mbar_wait(a_full + (i & 1), (i >> 1) & 1);
+        if (i >= 1) mbar_wait(d2_full, (i - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t a_u = su + S::A + (i & 1) * (128 * BT_C * 2);
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          mma_f16(tmem, umma_desc_sw128(a_u + k * 32), umma_desc_sw128(su + S::W1 + k * 32), h16_idesc(BT_HID), k > 0);
+        mma_commit(d1_full);
+        mma_commit(a_empty + (i & 1));
+      }
+      __syncwarp();
+      if (prev >= 0) {
+        mbar_wait(d2_full, (i - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        float d[32];
+        tmem_row<32>(tlane + BT_HID + 128 + hh * 32, d);
+        const int pimg = prev / p.tpi, ptr = prev - pimg * p.tpi;
+        const int pty = ptr / p.tiles_x, ptx = ptr - pty * p.tiles_x;
+        const float* pin = p.in + pimg * p.in_img;
+        float* pout = p.out + pimg * p.out_img;
+        float* plat = p.lat ? p.lat + pimg * p.lat_img : nullptr;
+        const int oy2 = pty * BT_TY + q, ox2 = ptx * BT_TX + lane;
+        float part = 0.0f;
+        if (oy2 < p.ho && ox2 < p.wo) {
+          const int64_t po = ((int64_t)oy2 * p.wo + ox2) * BT_C + hh * 32;
+          const float4* xr = reinterpret_cast<const float4*>(pin + po);
+          float4* o = reinterpret_cast<float4*>(pout + po);
+          float4 xv[8];
+#pragma unroll
+          for (int u = 0; u < 8; u++) xv[u] = __ldg(xr + u);
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            const int c = hh * 32 + 4 * u;
+            const float4 y = make_float4(d[4 * u] + b2s[c] + xv[u].x, d[4 * u + 1] + b2s[c + 1] + xv[u].y,
+                                         d[4 * u + 2] + b2s[c + 2] + xv[u].z, d[4 * u + 3] + b2s[c + 3] + xv[u].w);
+            o[u] = y;
+            part = fmaf(wms[c], y.x, part);
+            part = fmaf(wms[c + 1], y.y, part);
+            part = fmaf(wms[c + 2], y.z, part);
+            part = fmaf(wms[c + 3], y.w, part);
+          }
+        }
+        if (plat) {
+          mp[hh * 128 + q * 32 + lane] = part;
+          epi_sync();
+          const int te = e * 32 + lane;
+          if (te < 128) {
+            const int oy3 = pty * BT_TY + (te >> 5), ox3 = ptx * BT_TX + (te & 31);
+            if (oy3 < p.ho && ox3 < p.wo) plat[(int64_t)oy3 * p.wo + ox3] = (mp[te] + mp[128 + te]) + bm;
+          }
+        }
+      }
+      if (!has) break;
+      mbar_wait(d1_full, i & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+      for (int cc = 0; cc < 4; cc++) {
+        const int col = hh * 128 + cc * 32;
+        float v[32];
+        tmem_row<32>(tlane + col, v);
+        uint32_t hv[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+          hv[j] = pack_h2(fmaxf(v[2 * j] + b1s[col + 2 * j], 0.0f), fmaxf(v[2 * j + 1] + b1s[col + 2 * j + 1], 0.0f));
+        tmem_st16(tlane + BT_HID + (col >> 1), hv);
+      }
+      tmem_wait_st();
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      epi_sync();
+      if (leader) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+        for (int k = 0; k < 16; k++)
+          mma_f16_ts(tmem_d2, tmem_h + 8 * k, umma_desc_sw128(su + S::W2 + (k >> 2) * (BT_C * 128) + (k & 3) * 32),
+                     h16_idesc(BT_C), k > 0);
+        mma_commit(d2_full);
+      }
+      __syncwarp();
+      prev = tile;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+static int launch_block_h16(const BlockTcParams& p, int n_img, int sm_count, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(an_block_h16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H16Smem::TOTAL) !=
+        cudaSuccess)
+      return -1;
+    attr = true;
+  }
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return -1;
+  H16Params hp;
+  hp.p = p;
+  const cuuint64_t dims[4] = {(cuuint64_t)BT_C, (cuuint64_t)p.w, (cuuint64_t)p.h, (cuuint64_t)n_img};
+  const cuuint64_t strides[3] = {(cuuint64_t)BT_C * 4, (cuuint64_t)p.w * BT_C * 4, (cuuint64_t)p.h * p.w * BT_C * 4};
+  const cuuint32_t box[4] = {(cuuint32_t)HS_CH, (cuuint32_t)HS_COLS, (cuuint32_t)HS_ROWS, 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  if (enc(&hp.tin, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(p.in), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -1;
+  const int grid = p.n_tiles < sm_count ? p.n_tiles : sm_count;
+  an_block_h16_kernel<<<grid, BT_THREADS, H16Smem::TOTAL, s>>>(hp);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
 // ---------------------------------------------------------------- launcher
 template <bool DOWN>
 static int launch_block_tc(const BlockTcParams& p, int sm_count, cudaStream_t s) {
@@ -603,8 +950,8 @@ static int launch_block_tc(const BlockTcParams& p, int sm_count, cudaStream_t s)
   return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
 }
 
-int analysis_block_tc(bool down, const float* in, float* out, const float* blk, const float* wm, float* lat, int h,
-                      int w, int ho, int wo, int n_img, int64_t lat_img, int sm_count, cudaStream_t s) {
+int analysis_block_tc(int mode, bool down, const float* in, float* out, const float* blk, const float* wm, float* lat,
+                      int h, int w, int ho, int wo, int n_img, int64_t lat_img, int sm_count, cudaStream_t s) {
   BlockTcParams p;
   p.in = in;
   p.out = out;
@@ -622,6 +969,7 @@ int analysis_block_tc(bool down, const float* in, float* out, const float* blk, 
   p.out_img = (int64_t)ho * wo * BT_C;
   p.lat_img = lat_img;
   if (down) return launch_block_tc<true>(p, sm_count, s);
+  if (mode == 3) return launch_block_h16(p, n_img, sm_count, s);
   static const bool seq = getenv("CCRD_AN_SEQ") && getenv("CCRD_AN_SEQ")[0] == '1';  // A/B: sequential kernel
   if (seq) return launch_block_tc<false>(p, sm_count, s);
   static bool attr = false;

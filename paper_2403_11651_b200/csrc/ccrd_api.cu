@@ -861,7 +861,7 @@ static int validate_analysis(const cc_analysis_desc* a) {
   if (a->H < 1 || a->W < 1 || a->L < 1 || a->L > CC_MAX_LEVELS || a->C < 4 || a->C > 512 || a->C % 4 || a->blocks < 1)
     return fail(CC_EINVAL, "bad analysis descriptor (H %d, W %d, L %d, C %d, blocks %d)", a->H, a->W, a->L, a->C,
                 a->blocks);
-  if (a->tf32 < 0 || a->tf32 > 2) return fail(CC_EINVAL, "tf32 must be 0, 1 or 2");
+  if (a->tf32 < 0 || a->tf32 > 3) return fail(CC_EINVAL, "tf32 must be 0, 1, 2 or 3");
   if (a->N < 1 || (int64_t)a->N * a->H * a->W > ((int64_t)1 << 31) / 4)
     return fail(CC_EINVAL, "bad analysis batch N %d (N H W must stay below 2^29)", a->N);
   return CC_OK;

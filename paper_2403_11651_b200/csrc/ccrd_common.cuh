@@ -253,8 +253,8 @@ int device_sm_count();  // current device's SMs (lazily cached; 148 without a de
 // N-O analysis transform (analysis.cu, NEXT-4)
 int64_t analysis_param_count(const cc_analysis_desc& a);
 size_t analysis_workspace_bytes(const cc_analysis_desc& a);
-int analysis_block_tc(bool down, const float* in, float* out, const float* blk, const float* wm, float* lat, int h,
-                      int w, int ho, int wo, int n_img, int64_t lat_img, int sm_count, cudaStream_t s);
+int analysis_block_tc(int mode, bool down, const float* in, float* out, const float* blk, const float* wm, float* lat,
+                      int h, int w, int ho, int wo, int n_img, int64_t lat_img, int sm_count, cudaStream_t s);
 int analysis_forward_impl(const cc_analysis_desc& a, const float* image, const float* w, float* lat, void* ws,
                           cudaStream_t s);
 
