@@ -198,7 +198,7 @@ def test_analysis_entry_errors_without_gpu():
     assert ws4 >= 4 * 2 * acfg.H * acfg.W * acfg.C * 4 and ws1 < ws4   # x / y for the whole batch
     # the unfused modes also hold one image's 4C expansion and the cuBLASLt workspace
     assert P.cc_analysis_workspace_bytes(P.analysis_desc(acfg, 2, 1)) > ws1
-    for bad in (dict(N=0), dict(tf32=3), dict(C=6), dict(L=0), dict(blocks=0), dict(H=0)):
+    for bad in (dict(N=0), dict(tf32=4), dict(C=6), dict(L=0), dict(blocks=0), dict(H=0)):
         d = P.analysis_desc(acfg, 1, 1)
         for k, v in bad.items():
             setattr(d, k, v)
