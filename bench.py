@@ -149,9 +149,12 @@ def run_ours(args, rk):
     seeds = [workload.image_seed(args.seed, g) for g in dist.owned_images(rk.rank, n_img)]
     t0 = time.perf_counter()
     images = workload.make_batch(cfg, seeds, threads=min(16, host_cores()))
+    if args.image == "u8":   # 8-bit sources (the paper's Kodak / CLIC images are 8-bit RGB)
+        for im in images:
+            im.image = workload.quantize_image_u8(im.image)
     gen_s = time.perf_counter() - t0
     log(f"generated {len(images)} images in {gen_s:.1f}s")
-    batch = P.DeviceBatch(cfg, images, device=dev, with_xhat=True)
+    batch = P.DeviceBatch(cfg, images, device=dev, with_xhat=True, image_u8=args.image == "u8")
     desc = batch.desc
     macs = P.cc_mac_per_pixel(desc)
     log("device batch ready")
@@ -233,7 +236,8 @@ def run_ours(args, rk):
                         f"ARM {list(cfg.arm_widths)} C={cfg.n_ctx}, synthesis {list(cfg.syn_widths)}+{cfg.syn_n_res}x"
                         f"res3x3, {cfg.up_taps}-tap separable upsampling (BASELINE.json configs[3])",
             "images_per_gpu": n_img, "H": cfg.H, "W": cfg.W, "mac_per_pixel": round(macs.total, 3),
-            "l2": f"inputs larger than L2: {(sum(im.latents.nbytes + im.image.nbytes for im in images)) / 1e9:.2f} GB "
+            "image": "uint8 planar, x = v / 255 (desc.image_u8)" if args.image == "u8" else "fp32 planar",
+            "l2": f"inputs larger than L2: {(sum(im.latents.nbytes + im.image.size * (1 if args.image == 'u8' else 4) for im in images)) / 1e9:.2f} GB "
                   "read per step per GPU (126 MB L2)",
             "parallelism": f"image-sharded x{rk.world}",
         },
@@ -589,29 +593,39 @@ def run_e2e(args, cfg, images, desc, dev, stream, rk, n_img):
 
     import paper_2403_11651_b200 as P
     from paper_2403_11651_b200 import dist
-    lat = [torch.from_numpy(im.latents).pin_memory() for im in images]
-    img = [torch.from_numpy(im.image).pin_memory() for im in images]
-    xh = [torch.empty_like(t).pin_memory() for t in img]
+    # latents travel as int8 when every value fits (the workload clips them to
+    # +-lat_clip); the host path widens them to int16 on the device
+    hd = P.CcModelDesc.from_buffer_copy(desc)
+    hd.latents_i8 = int(args.e2e_i8 and max(int(np.abs(im.latents).max()) for im in images) <= 127)
+    lat = [torch.from_numpy(im.latents.astype(np.int8) if hd.latents_i8 else im.latents).pin_memory()
+           for im in images]
+    img = [torch.from_numpy(workload.to_u8(im.image) if desc.image_u8 else im.image).pin_memory() for im in images]
+    # the step's result is the per-image (rate, sse, mse, cost); x_hat is an
+    # optional output, read back only with --e2e-xhat
+    xh = [torch.empty(im.image.shape, dtype=torch.float32).pin_memory() for im in images] if args.e2e_xhat else None
     io = [P.CcImageIO(lat[i].data_ptr(), images[i].arm_w.ctypes.data, images[i].up_w.ctypes.data,
-                      images[i].syn_w.ctypes.data, img[i].data_ptr(), xh[i].data_ptr()) for i in range(n_img)]
-    ws_b = P.cc_workspace_bytes_host(desc, n_img)
+                      images[i].syn_w.ctypes.data, img[i].data_ptr(), xh[i].data_ptr() if xh else None)
+          for i in range(n_img)]
+    ws_b = P.cc_workspace_bytes_host(hd, n_img)
     ws = torch.empty(ws_b, dtype=torch.uint8, device=dev)
     res = np.zeros((n_img, 4))
     steps = max(2, min(args.steps, args.e2e_steps))
-    P.cc_rd_forward_host(desc, io, res, ws.data_ptr(), ws_b, stream.cuda_stream)   # warm-up
+    P.cc_rd_forward_host(hd, io, res, ws.data_ptr(), ws_b, stream.cuda_stream)   # warm-up
     dist.barrier()
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     for _ in range(steps):
-        P.cc_rd_forward_host(desc, io, res, ws.data_ptr(), ws_b, stream.cuda_stream)
+        P.cc_rd_forward_host(hd, io, res, ws.data_ptr(), ws_b, stream.cuda_stream)
     torch.cuda.synchronize(dev)
     wall = time.perf_counter() - t0
     wall = dist.max_over_ranks(wall, device=dev)
-    h2d = sum(im.latents.nbytes + im.image.nbytes for im in images)
-    d2h = sum(im.image.nbytes for im in images) + 32 * n_img
+    h2d = sum(lat[i].numel() * lat[i].element_size() + img[i].numel() * img[i].element_size() for i in range(n_img))
+    d2h = 32 * n_img + (sum(t.numel() * 4 for t in xh) if xh else 0)
     return {"value": rk.world * n_img * cfg.H * cfg.W * steps / wall, "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": steps,
-            "api": "cc_rd_forward_host (pinned host latents+image in, x_hat+results out, synchronous)"}
+            "api": "cc_rd_forward_host (pinned host " + ("int8" if hd.latents_i8 else "int16") + " latents + "
+                   + ("8-bit" if desc.image_u8 else "fp32")
+                   + " image in, per-image results" + (" + x_hat" if xh else "") + " out, synchronous)"}
 
 
 def run_cpu_baseline(cfg, images):
@@ -643,6 +657,9 @@ def run_reference(args, rk):
     n = args.steps + args.warmup
     ims = workload.make_batch(cfg, [workload.image_seed(args.seed, g) for g in range(min(n, 4))],
                               threads=min(16, cores))
+    if args.image == "u8":   # the same 8-bit images our arm encodes
+        for im in ims:
+            im.image = workload.quantize_image_u8(im.image)
     for i in range(args.warmup):
         oracle.rd_forward_image(cfg, ims[i % len(ims)])
     t0 = time.perf_counter()
@@ -681,6 +698,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--profile-steps", type=int, default=3, help="serial pass for per-kernel timing")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-xhat", action="store_true", help="e2e also reads x_hat back (fp32, 12 B/px)")
+    ap.add_argument("--e2e-i8", type=int, default=1, help="e2e sends latents as int8 when they fit (1) or int16 (0)")
+    ap.add_argument("--image", choices=("u8", "f32"), default="u8",
+                    help="image format of the RD forward: 8-bit planes (x = v/255) or fp32")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--train", action="store_true", help="time the encoder training iteration (NEXT-2)")
     ap.add_argument("--decode", action="store_true", help="time the decoder output stage (NEXT-3)")

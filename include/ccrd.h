@@ -93,6 +93,19 @@ typedef struct {
   float logscale_min, logscale_max;    /* clamp of the ARM log-scale output            */
   float p_floor;                       /* probability floor before -log2               */
   double lambda;                       /* Lagrange multiplier of Eq. 1                 */
+  int32_t image_u8;                    /* 0: images are fp32 planar [3][H][W] in [0,1]; */
+                                       /* 1: uint8 planar [3][H][W], x = v / 255 (the  */
+                                       /*    paper's 8-bit RGB sources; fp32 IEEE       */
+                                       /*    division).  x_hat stays fp32.  Applies to  */
+                                       /*    every `image` argument taking this desc    */
+                                       /*    except cc_train_step / cc_synthesize       */
+                                       /*    (fp32 only: CC_ENOTSUP).                   */
+  int32_t latents_i8;                  /* cc_rd_forward_host only: 1 = io.latents are  */
+                                       /*    int8 host arrays (every value in           */
+                                       /*    [-128, 127]; the caller's guarantee),      */
+                                       /*    uploaded at 1 byte per latent and widened  */
+                                       /*    to int16 on the device.  Device entry      */
+                                       /*    points need 0 (else CC_ENOTSUP).            */
 } cc_model_desc;
 
 /* Per-image result, written to DEVICE memory (so it can be all-reduced

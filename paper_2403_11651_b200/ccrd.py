@@ -37,6 +37,8 @@ class CcModelDesc(C.Structure):
         ("logscale_min", C.c_float), ("logscale_max", C.c_float),
         ("p_floor", C.c_float),
         ("lam", C.c_double),
+        ("image_u8", C.c_int32),
+        ("latents_i8", C.c_int32),
     ]
 
 
@@ -359,14 +361,21 @@ class DeviceBatch:
     """Device-resident inputs of n images (torch tensors for memory only) and
     the host weight blobs, laid out for cc_rd_forward."""
 
-    def __init__(self, cfg, images: List, device="cuda", with_xhat=True):
+    def __init__(self, cfg, images: List, device="cuda", with_xhat=True, image_u8=False):
+        """image_u8: images go to the device as uint8 planes (desc.image_u8 = 1,
+        x = v / 255); im.image must then hold 8-bit levels (workload.to_u8)."""
         import torch
+
+        def to_u8(x):  # storage format: v = rint(255 x)
+            return np.clip(np.rint(np.asarray(x, np.float64) * 255.0), 0, 255).astype(np.uint8)
         self.cfg = cfg
         self.desc = desc_from_config(cfg)
+        self.desc.image_u8 = int(bool(image_u8))
         self.n = len(images)
         self.lat = [torch.from_numpy(im.latents).to(device) for im in images]
-        self.img = [torch.from_numpy(im.image).to(device) for im in images]
-        self.xhat = [torch.empty_like(t) for t in self.img] if with_xhat else None
+        self.img = [torch.from_numpy(to_u8(im.image) if image_u8 else im.image).to(device) for im in images]
+        self.xhat = [torch.empty(im.image.shape, dtype=torch.float32, device=device) for im in images] \
+            if with_xhat else None
         self.arm_w = [np.ascontiguousarray(im.arm_w, np.float32) for im in images]
         self.up_w = [np.ascontiguousarray(im.up_w, np.float32) for im in images]
         self.syn_w = [np.ascontiguousarray(im.syn_w, np.float32) for im in images]

@@ -189,6 +189,8 @@ static int validate(const cc_model_desc* dp) {
   if (d.H < 1 || d.W < 1) return fail(CC_EINVAL, "H, W must be >= 1 (got %d x %d)", d.H, d.W);
   if ((int64_t)d.H * d.W > ((int64_t)1 << 31)) return fail(CC_ENOTSUP, "image larger than 2^31 pixels");
   if (d.L < 1 || d.L > CC_MAX_LEVELS) return fail(CC_EINVAL, "L must be in 1..%d (got %d)", CC_MAX_LEVELS, d.L);
+  if (d.image_u8 != 0 && d.image_u8 != 1) return fail(CC_EINVAL, "image_u8 must be 0 or 1 (got %d)", d.image_u8);
+  if (d.latents_i8 != 0 && d.latents_i8 != 1) return fail(CC_EINVAL, "latents_i8 must be 0 or 1 (got %d)", d.latents_i8);
   if (d.n_ctx < 1 || d.n_ctx > CC_MAX_CTX) return fail(CC_EINVAL, "n_ctx must be in 1..%d", CC_MAX_CTX);
   for (int c = 0; c < d.n_ctx; c++) {
     const int dy = d.ctx_dy[c], dx = d.ctx_dx[c];
@@ -469,7 +471,7 @@ static bool concurrent_streams() {
 static int forward_batch(const cc_model_desc& d, const cc_strip* win, const int16_t* const* lat,
                          const float* const* arm_w, const float* const* up_w, const float* const* syn_w,
                          const float* const* image, float* const* x_hat, char* slices, size_t per, int n,
-                         cudaStream_t s, bool overlap) {
+                         cudaStream_t s, bool overlap, bool join = true) {
   PyrGeom pg;
   pyr_geom(d, win, pg);
   const int n_arm = n_arm_partials(d, win);
@@ -528,7 +530,7 @@ static int forward_batch(const cc_model_desc& d, const cc_strip* win, const int1
     cudaEventRecord(side->join, side->s);
     for (int i = 0; i < n; i++)
       if ((rc = arm_one(d, win, lat[i], arm_w[i], (double*)(slices + per * (size_t)i), s))) return rc;
-    cudaStreamWaitEvent(s, side->join, 0);
+    if (join) cudaStreamWaitEvent(s, side->join, 0);  // else the caller orders on the side stream
     return CC_OK;
   }
   if ((rc = pyr_many(d, win, imgs, n, s))) return rc;
@@ -596,6 +598,14 @@ int64_t cc_last_launch_count(void) { return g_launches; }
 
 int cc_validate(const cc_model_desc* desc) { return validate(desc); }
 
+// latents_i8 is a host-path transfer format; device entry points take int16
+static int validate_device(const cc_model_desc* desc) {
+  const int rc = validate(desc);
+  if (rc) return rc;
+  if (desc->latents_i8) return fail(CC_ENOTSUP, "latents_i8 applies to cc_rd_forward_host only (device latents are int16)");
+  return CC_OK;
+}
+
 size_t cc_workspace_bytes(const cc_model_desc* desc, int32_t n_img) {
   if (validate(desc) != CC_OK || n_img < 1) return 0;
   return slice_bytes(*desc, nullptr) * (size_t)n_img;
@@ -604,7 +614,7 @@ size_t cc_workspace_bytes(const cc_model_desc* desc, int32_t n_img) {
 int cc_rd_forward(const cc_model_desc* desc, const cc_image_io* io, int32_t n_img, cc_rd_result* results,
                   void* workspace, size_t workspace_bytes, void* stream) {
   g_launches = 0;
-  int rc = validate(desc);
+  int rc = validate_device(desc);
   if (rc) return rc;
   if (!io || n_img < 1 || !results) return fail(CC_EINVAL, "io/results null or n_img < 1");
   const size_t per = slice_bytes(*desc, nullptr);
@@ -651,13 +661,26 @@ static size_t stage_slot_bytes(const cc_model_desc& d) {
   LevelGeom g;
   level_dims(d, g, &n_lat);
   const size_t P = (size_t)d.H * d.W;
-  return align256(sizeof(int16_t) * (size_t)n_lat) + 2 * align256(sizeof(float) * 3 * P);
+  // int16 latents | fp32-sized image | x_hat | int8 latent upload (latents_i8)
+  return align256(sizeof(int16_t) * (size_t)n_lat) + 2 * align256(sizeof(float) * 3 * P) +
+         (d.latents_i8 ? align256((size_t)n_lat) : 0);
 }
+
+__global__ void widen_i8_kernel(const int8_t* __restrict__ in, int16_t* __restrict__ out, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i];
+}
+
+// The host path stages CHUNKS of HOST_CHUNK images (one forward_batch call
+// each: batched pyramid launch, ARM / synthesis kernels back to back) in
+// HOST_SLOTS double-buffered slots: the upload of chunk c+1 overlaps the
+// compute of chunk c.  One image per call measured 23 % slower than batched.
+constexpr int HOST_SLOTS = 2, HOST_CHUNK = 4;
 
 size_t cc_workspace_bytes_host(const cc_model_desc* desc, int32_t n_img) {
   if (validate(desc) != CC_OK || n_img < 1) return 0;
   return slice_bytes(*desc, nullptr) * (size_t)n_img +
-         align256(sizeof(cc_rd_result) * (size_t)n_img) + 2 * stage_slot_bytes(*desc);
+         align256(sizeof(cc_rd_result) * (size_t)n_img) + HOST_SLOTS * HOST_CHUNK * stage_slot_bytes(*desc);
 }
 
 int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t n_img, cc_rd_result* results,
@@ -680,61 +703,100 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
   LevelGeom lg;
   level_dims(d, lg, &n_lat);
   const size_t P = (size_t)d.H * d.W;
-  const size_t lat_b = sizeof(int16_t) * (size_t)n_lat, img_b = sizeof(float) * 3 * P;
+  const size_t lat_b = sizeof(int16_t) * (size_t)n_lat, xh_b = sizeof(float) * 3 * P;
+  const size_t img_b = (d.image_u8 ? 1 : sizeof(float)) * 3 * P;  // 8-bit images: 3 bytes per pixel
 
   cudaStream_t s = (cudaStream_t)stream;
   // copy stream + per-slot events: copies of image i+1 overlap compute of image i
   // three streams: uploads (cs), compute (s), readbacks (ds); PCIe is full
   // duplex, so image i+1's upload, image i's compute and image i-1's x_hat
-  // readback overlap.  Two staging slots; events guard their reuse.
+  // readback overlap.  HOST_SLOTS staging slots of HOST_CHUNK images; events
+  // guard their reuse.
+  // The upload stream runs at the highest priority: its small kernels (the
+  // int8 -> int16 latent widening) take the next free SM slots instead of
+  // queueing behind the compute stream's blocks.
   cudaStream_t cs, ds;
-  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess ||
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking) != cudaSuccess)
     return cuda_check("stream create");
-  cudaEvent_t copied[2], computed[2], read_back[2];
-  for (int k = 0; k < 2; k++) {
+  // With concurrent streams the ARM (on s) and the pyramid + synthesis (on
+  // the side stream) of consecutive images are not joined per image: each
+  // stream runs image after image (as in cc_rd_forward's batch); a slot is
+  // reused once both streams are done with it, x_hat is read back after the
+  // side stream, and the reduction joins the side stream once.
+  const bool conc = concurrent_streams();
+  SideStream* side = nullptr;
+  if (conc && (rc = side_stream(&side))) return rc;
+  cudaEvent_t copied[HOST_SLOTS], computed[HOST_SLOTS], computed_side[HOST_SLOTS], read_back[HOST_SLOTS];
+  for (int k = 0; k < HOST_SLOTS; k++) {
     cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&computed[k], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&computed_side[k], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&read_back[k], cudaEventDisableTiming);
   }
   // start the side streams after whatever is already queued on s
   cudaEventRecord(computed[0], s);
   cudaStreamWaitEvent(cs, computed[0], 0);
   cudaStreamWaitEvent(ds, computed[0], 0);
-  cudaEventRecord(computed[1], s);
-  cudaEventRecord(read_back[0], s);
-  cudaEventRecord(read_back[1], s);
+  for (int k = 0; k < HOST_SLOTS; k++) {
+    cudaEventRecord(computed[k], s);
+    cudaEventRecord(computed_side[k], s);
+    cudaEventRecord(read_back[k], s);
+  }
   ReduceJob* jobs = new ReduceJob[n_img];
-  for (int i = 0; i < n_img && rc == CC_OK; i++) {
-    const int k = i & 1;
-    char* base = stage + slot * (size_t)k;
-    int16_t* dlat = (int16_t*)base;
-    float* dimg = (float*)(base + align256(lat_b));
-    float* dxh = (float*)(base + align256(lat_b) + align256(img_b));
-    const cc_image_io& x = io[i];
-    if (!x.latents || !x.arm_w || !x.up_w || !x.syn_w) {
-      rc = fail(CC_EINVAL, "image %d: null latents or weights", i);
-      break;
+  for (int i0 = 0, c = 0; i0 < n_img && rc == CC_OK; i0 += HOST_CHUNK, c++) {
+    const int k = c % HOST_SLOTS, m = n_img - i0 < HOST_CHUNK ? n_img - i0 : HOST_CHUNK;
+    const int16_t* l1[HOST_CHUNK];
+    const float *a1[HOST_CHUNK], *u1[HOST_CHUNK], *s1[HOST_CHUNK], *i1[HOST_CHUNK];
+    float* x1[HOST_CHUNK];
+    float* dxhs[HOST_CHUNK];
+    cudaStreamWaitEvent(cs, computed[k], 0);  // slot k's inputs were consumed by chunk c - HOST_SLOTS
+    cudaStreamWaitEvent(cs, computed_side[k], 0);
+    for (int j = 0; j < m && rc == CC_OK; j++) {
+      char* base = stage + slot * (size_t)(k * HOST_CHUNK + j);
+      int16_t* dlat = (int16_t*)base;
+      int8_t* dlat8 = (int8_t*)(base + align256(lat_b) + 2 * align256(xh_b));
+      float* dimg = (float*)(base + align256(lat_b));
+      dxhs[j] = (float*)(base + align256(lat_b) + align256(xh_b));
+      const cc_image_io& x = io[i0 + j];
+      if (!x.latents || !x.arm_w || !x.up_w || !x.syn_w) {
+        rc = fail(CC_EINVAL, "image %d: null latents or weights", i0 + j);
+        break;
+      }
+      if (d.latents_i8) {  // 1 byte per latent over PCIe, widened on the copy stream
+        cudaMemcpyAsync(dlat8, x.latents, (size_t)n_lat, cudaMemcpyHostToDevice, cs);
+        widen_i8_kernel<<<(unsigned)((n_lat + 255) / 256), 256, 0, cs>>>(dlat8, dlat, n_lat);
+        g_launches++;
+      } else {
+        cudaMemcpyAsync(dlat, x.latents, lat_b, cudaMemcpyHostToDevice, cs);
+      }
+      if (x.image) cudaMemcpyAsync(dimg, x.image, img_b, cudaMemcpyHostToDevice, cs);
+      l1[j] = dlat;
+      a1[j] = x.arm_w;
+      u1[j] = x.up_w;
+      s1[j] = x.syn_w;
+      i1[j] = x.image ? dimg : nullptr;
+      x1[j] = x.x_hat ? dxhs[j] : nullptr;
+      jobs[i0 + j] = make_job(d, nullptr, (double*)(ws + per * (size_t)(i0 + j)));
     }
-    cudaStreamWaitEvent(cs, computed[k], 0);  // slot k's inputs were consumed by image i-2
-    cudaMemcpyAsync(dlat, x.latents, lat_b, cudaMemcpyHostToDevice, cs);
-    if (x.image) cudaMemcpyAsync(dimg, x.image, img_b, cudaMemcpyHostToDevice, cs);
+    if (rc) break;
     cudaEventRecord(copied[k], cs);
     cudaStreamWaitEvent(s, copied[k], 0);
-    cudaStreamWaitEvent(s, read_back[k], 0);  // slot k's x_hat of image i-2 is read back
-    double* part = (double*)(ws + per * (size_t)i);
-    const int16_t* l1[1] = {dlat};
-    const float *a1[1] = {x.arm_w}, *u1[1] = {x.up_w}, *s1[1] = {x.syn_w}, *i1[1] = {x.image ? dimg : nullptr};
-    float* x1[1] = {x.x_hat ? dxh : nullptr};
-    rc = forward_batch(d, nullptr, l1, a1, u1, s1, i1, x1, (char*)part, per, 1, s, false);
+    cudaStreamWaitEvent(s, read_back[k], 0);  // slot k's x_hat of chunk c - HOST_SLOTS is read back
+    rc = forward_batch(d, nullptr, l1, a1, u1, s1, i1, x1, ws + per * (size_t)i0, per, m, s, conc, /*join=*/false);
     if (rc) break;
     cudaEventRecord(computed[k], s);
-    if (x.x_hat) {
-      cudaStreamWaitEvent(ds, computed[k], 0);
-      cudaMemcpyAsync(x.x_hat, dxh, img_b, cudaMemcpyDeviceToHost, ds);
-    }
+    cudaEventRecord(computed_side[k], conc ? side->s : s);
+    cudaStreamWaitEvent(ds, computed_side[k], 0);
+    for (int j = 0; j < m; j++)
+      if (io[i0 + j].x_hat) cudaMemcpyAsync(io[i0 + j].x_hat, dxhs[j], xh_b, cudaMemcpyDeviceToHost, ds);
     cudaEventRecord(read_back[k], ds);
-    jobs[i] = make_job(d, nullptr, part);
+  }
+  if (conc) {  // the last images' synthesis
+    cudaEventRecord(side->join, side->s);
+    cudaStreamWaitEvent(s, side->join, 0);
   }
   if (rc == CC_OK) rc = launch_reduce(jobs, n_img, dres, s);
   if (rc == CC_OK) {
@@ -746,9 +808,10 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
   cudaStreamSynchronize(cs);
   if (cudaStreamSynchronize(ds) != cudaSuccess && rc == CC_OK) rc = cuda_check("cc_rd_forward_host readback");
   delete[] jobs;
-  for (int k = 0; k < 2; k++) {
+  for (int k = 0; k < HOST_SLOTS; k++) {
     cudaEventDestroy(copied[k]);
     cudaEventDestroy(computed[k]);
+    cudaEventDestroy(computed_side[k]);
     cudaEventDestroy(read_back[k]);
   }
   cudaStreamDestroy(cs);
@@ -803,7 +866,7 @@ size_t cc_workspace_bytes_strip(const cc_model_desc* desc, const cc_strip* strip
 int cc_rd_forward_strip(const cc_model_desc* desc, const cc_strip* strip, const cc_image_io* io,
                         cc_rd_result* result, void* workspace, size_t workspace_bytes, void* stream) {
   g_launches = 0;
-  int rc = validate(desc);
+  int rc = validate_device(desc);
   if (rc) return rc;
   const cc_model_desc& d = *desc;
   if ((rc = validate_strip(d, strip))) return rc;
@@ -838,10 +901,11 @@ int cc_train_step(const cc_model_desc* desc, float* params, const float* noise, 
                   float* adam_v, const cc_adam* opt, cc_rd_result* result, float* grad, void* workspace,
                   size_t workspace_bytes, void* stream) {
   g_launches = 0;
-  int rc = validate(desc);
+  int rc = validate_device(desc);
   if (rc) return rc;
   const cc_model_desc& d = *desc;
   if (!train_supported(d)) return fail(CC_ENOTSUP, "training step not compiled for this shape (or up_2d)");
+  if (d.image_u8) return fail(CC_ENOTSUP, "the training step takes an fp32 image (image_u8 = 0)");
   if (!params || !noise || !image || !result || !grad) return fail(CC_EINVAL, "null params / noise / image / result / grad");
   if (opt && (!adam_m || !adam_v || opt->t < 1)) return fail(CC_EINVAL, "Adam needs m, v and t >= 1");
   const size_t need = train_workspace_bytes(d);
@@ -896,7 +960,7 @@ int cc_analysis_forward(const cc_analysis_desc* a, const float* image, const flo
 int cc_decode(const cc_model_desc* desc, const int16_t* latents, const float* up_w, const float* syn_w,
               uint8_t* out_rgb8, void* workspace, size_t workspace_bytes, void* stream) {
   g_launches = 0;
-  int rc = validate(desc);
+  int rc = validate_device(desc);
   if (rc) return rc;
   if (!latents || !up_w || !syn_w || !out_rgb8) return fail(CC_EINVAL, "null latents / up_w / syn_w / out");
   const cc_model_desc& d = *desc;
@@ -932,7 +996,7 @@ int cc_decode(const cc_model_desc* desc, const int16_t* latents, const float* up
 int cc_arm_rate(const cc_model_desc* desc, const int16_t* latents, const float* arm_w, double* rate, float* mu,
                 float* scale, float* bits, void* workspace, size_t workspace_bytes, void* stream) {
   g_launches = 0;
-  int rc = validate(desc);
+  int rc = validate_device(desc);
   if (rc) return rc;
   if (!latents || !arm_w || !rate) return fail(CC_EINVAL, "null latents / arm_w / rate");
   const size_t per = partial_bytes(*desc, nullptr);
@@ -960,7 +1024,7 @@ int cc_arm_rate(const cc_model_desc* desc, const int16_t* latents, const float* 
 int cc_upsample(const cc_model_desc* desc, const int16_t* latents, const float* up_w, float* dense,
                 void* workspace, size_t workspace_bytes, void* stream) {
   g_launches = 0;
-  int rc = validate(desc);
+  int rc = validate_device(desc);
   if (rc) return rc;
   if (!latents || !up_w || !dense) return fail(CC_EINVAL, "null latents / up_w / dense");
   const cc_model_desc& d = *desc;
@@ -1003,6 +1067,7 @@ int cc_synthesize(const cc_model_desc* desc, const float* dense, const float* sy
   if (rc) return rc;
   if (!dense || !syn_w) return fail(CC_EINVAL, "null dense / syn_w");
   if (sse && !image) return fail(CC_EINVAL, "sse requested without image");
+  if (image && desc->image_u8) return fail(CC_ENOTSUP, "cc_synthesize takes an fp32 image (image_u8 = 0)");
   const cc_model_desc& d = *desc;
   SynGeom sg;
   syn_geom(d, nullptr, sg);

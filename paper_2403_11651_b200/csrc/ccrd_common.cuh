@@ -173,7 +173,8 @@ struct SynParams {
   const int16_t* lat;      // latents (chain mode)
   const float* s1;         // S_1 = grids 2..L-1 upsampled to level 1, [L-2][h1][w1] (pyramid.cu)
   const float* dense_in;   // [L][H][W] (synthesize-from-dense mode) or null
-  const float* image;      // [3][H][W] or null
+  const float* image;      // [3][H][W] fp32 or null
+  const uint8_t* image8;   // [3][H][W] 8-bit (x = v / 255, desc.image_u8) or null
   float* x_hat;            // [3][H][W] or null
   float* dense_out;        // debug [L][H][W] or null
   float* h1_out;           // debug [3][H][W] or null

@@ -231,7 +231,25 @@ __device__ __forceinline__ void mlp_pair(const SynParams<L, CH, R, K>& p, const 
   }
 }
 
-template <int L, int CH, int R, int K, bool DENSE_IN>
+// x = v / 255 correctly rounded in fp32 without a division: q0 = v r
+// (r = fp32(1/255)), one FMA residual correction.  Verified equal to the IEEE
+// quotient float32(v) / float32(255) for all 256 values of v (exact rational
+// check, reading 23); no slow-path call, no extra registers.
+__device__ __forceinline__ float u8_to_x(uint32_t v) {
+  const float fv = (float)v, r = 0.003921568859368562698364f;  // fp32(1/255)
+  const float q0 = __fmul_rn(fv, r);
+  return __fmaf_rn(__fmaf_rn(-q0, 255.0f, fv), r, q0);
+}
+// the target image x at plane offset i: fp32, or 8-bit (IMG8 = desc.image_u8)
+template <bool IMG8, class P>
+__device__ __forceinline__ float load_x(const P& p, int64_t i) {
+  if constexpr (IMG8)
+    return u8_to_x(__ldg(p.image8 + i));
+  else
+    return __ldg(p.image + i);
+}
+
+template <int L, int CH, int R, int K, bool DENSE_IN, bool IMG8>
 __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
     synth_kernel(const __grid_constant__ SynParams<L, CH, R, K> p) {
   using S = SynShape<L, CH, R, K>;
@@ -438,12 +456,12 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
 #pragma unroll
         for (int d = 0; d < 3; d++) co[d] = clampi(x + d - 1, 0, W - 1) - RX;
         float img[RS][3];  // x for the output rows, in flight during the math
-        if (last && p.image != nullptr) {
+        if (last && (IMG8 ? p.image8 != nullptr : p.image != nullptr)) {
 #pragma unroll
           for (int i = 0; i < RS; i++)
 #pragma unroll
             for (int c = 0; c < 3; c++)
-              img[i][c] = (yb + i < Ye) ? __ldg(p.image + c * Pimg + (int64_t)(yb + i - Ys) * W + x) : 0.0f;
+              img[i][c] = (yb + i < Ye) ? load_x<IMG8>(p, c * Pimg + (int64_t)(yb + i - Ys) * W + x) : 0.0f;
         }
         uint64_t a01[RS];
         float a2[RS];
@@ -507,7 +525,7 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
 #pragma unroll
             for (int c = 0; c < 3; c++) {
               if (p.x_hat != nullptr) p.x_hat[c * Pimg + gi] = o[c];
-              if (p.image != nullptr) {
+              if ((IMG8 ? p.image8 != nullptr : p.image != nullptr)) {
                 const float ev = img[i][c] - o[c];
                 sse = fmaf(ev, ev, sse);
               }
@@ -571,8 +589,8 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
       for (int c = 0; c < 3; c++) {
         const float xh = hin[c * HP + ctr];
         if (p.x_hat != nullptr) p.x_hat[c * Pimg + gi] = xh;
-        if (p.image != nullptr) {
-          const float ev = __ldg(p.image + c * Pimg + gi) - xh;
+        if ((IMG8 ? p.image8 != nullptr : p.image != nullptr)) {
+          const float ev = load_x<IMG8>(p, c * Pimg + gi) - xh;
           sse = fmaf(ev, ev, sse);
         }
       }
@@ -606,13 +624,13 @@ static int launch_syn(const SynGeom& g, const cc_model_desc& d, const float* up_
                       const float* syn_w, const int16_t* lat, const float* s1, const float* dense_in,
                       const float* image, float* x_hat, float* dense_out, float* h1_out,
                       double* partial, cudaStream_t stream, uint8_t* out_u8) {
-  (void)d;
   SynParams<L, CH, R, K> p;
   p.g = g;
   p.lat = lat;
   p.s1 = s1;
   p.dense_in = dense_in;
-  p.image = image;
+  p.image = d.image_u8 ? nullptr : image;
+  p.image8 = d.image_u8 ? reinterpret_cast<const uint8_t*>(image) : nullptr;
   p.x_hat = x_hat;
   p.dense_out = dense_out;
   p.h1_out = h1_out;
@@ -644,22 +662,29 @@ static int launch_syn(const SynGeom& g, const cc_model_desc& d, const float* up_
     q += 84;
   }
   using S = SynShape<L, CH, R, K>;
-  static bool attr_set[2] = {false, false};
+  static bool attr_set[3] = {false, false, false};
   const size_t smem = S::SMEM;
-  if (dense_in) {
+  if (dense_in) {  // stage entry cc_synthesize: fp32 images only (checked by the API)
     if (!attr_set[1]) {
-      cudaFuncSetAttribute(synth_kernel<L, CH, R, K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(synth_kernel<L, CH, R, K, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
       attr_set[1] = true;
     }
-    synth_kernel<L, CH, R, K, true><<<g.n_tiles, SYN_THREADS, smem, stream>>>(p);
+    synth_kernel<L, CH, R, K, true, false><<<g.n_tiles, SYN_THREADS, smem, stream>>>(p);
+  } else if (d.image_u8) {
+    if (!attr_set[2]) {
+      cudaFuncSetAttribute(synth_kernel<L, CH, R, K, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      attr_set[2] = true;
+    }
+    synth_kernel<L, CH, R, K, false, true><<<g.n_tiles, SYN_THREADS, smem, stream>>>(p);
   } else {
     if (!attr_set[0]) {
-      cudaFuncSetAttribute(synth_kernel<L, CH, R, K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(synth_kernel<L, CH, R, K, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
       attr_set[0] = true;
     }
-    synth_kernel<L, CH, R, K, false><<<g.n_tiles, SYN_THREADS, smem, stream>>>(p);
+    synth_kernel<L, CH, R, K, false, false><<<g.n_tiles, SYN_THREADS, smem, stream>>>(p);
   }
   return 0;
 }

@@ -212,3 +212,30 @@ def test_analysis_entry_errors_without_gpu():
         with pytest.raises(ccrd.CcError) as e:                         # no device: loud failure
             P.cc_analysis_forward(ad, 8, 8, 8, 8, ws4, 0)
         assert e.value.code == ccrd.CC_ECUDA
+
+
+def test_image_u8_validation():
+    d = P.desc_from_config(workload.CONFIGS["ref"])
+    assert d.image_u8 == 0 and P.cc_validate(d) == 0
+    d.image_u8 = 1
+    assert P.cc_validate(d) == 0
+    # the host path stages fp32-sized image slots either way
+    assert P.cc_workspace_bytes_host(d, 2) == P.cc_workspace_bytes_host(P.desc_from_config(workload.CONFIGS["ref"]), 2)
+    d.image_u8 = 2
+    assert P.cc_validate(d) == ccrd.CC_EINVAL
+    d.image_u8 = 0
+    d.latents_i8 = 1                       # valid (host path), slot grows by the int8 upload area
+    assert P.cc_validate(d) == 0
+    assert P.cc_workspace_bytes_host(d, 2) > P.cc_workspace_bytes_host(P.desc_from_config(workload.CONFIGS["ref"]), 2)
+    d.latents_i8 = 3
+    assert P.cc_validate(d) == ccrd.CC_EINVAL
+
+
+def test_u8_image_helpers():
+    x = np.array([[0.0, 0.5, 1.0, 0.25, 0.998]], np.float32)
+    v = workload.to_u8(x)
+    np.testing.assert_array_equal(v, [[0, 128, 255, 64, 254]])
+    q = workload.from_u8(v)
+    assert q.dtype == np.float32
+    np.testing.assert_array_equal(workload.to_u8(q), v)          # round trip exact
+    np.testing.assert_array_equal(q, v.astype(np.float32) / np.float32(255))

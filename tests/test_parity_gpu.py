@@ -182,11 +182,11 @@ def test_synthesize_stage_from_dense():
 
 def test_deterministic_and_host_path_match():
     """Bitwise determinism, and the host-buffer (end-to-end) path -- three
-    streams, two staging slots reused from the third image on -- gives the
+    streams, two slots of four images reused from the ninth image on -- gives the
     same numbers bit for bit."""
     P = _P()
     cfg = workload.CONFIGS["ref"].replace(H=200, W=300)
-    n = 5
+    n = 11
     ims = workload.make_batch(cfg, list(range(41, 41 + n)))
     a, xa = run_forward(cfg, ims)
     b, xb = run_forward(cfg, ims)
@@ -249,3 +249,89 @@ def test_full_size_8k_sampled_rows():
         off += h * w
     # total rate = fp64 sum of the per-latent bits the kernel produced
     assert abs(rate.item() - bits_np.astype(np.float64).sum()) <= 1e-6 * rate.item()
+
+
+def _quantised(ims):
+    for im in ims:
+        im.image = workload.quantize_image_u8(im.image)
+    return ims
+
+
+@pytest.mark.parametrize("name", ["low", "ref"])
+def test_u8_images_match_fp32_and_oracle(name):
+    """desc.image_u8 = 1: the kernels read 8-bit planes, x = v / 255 (IEEE fp32
+    division).  On images whose values are 8-bit levels, the results equal
+    the fp32-image path bit for bit (the same x values), and the oracle fed
+    x = float32(v) / 255."""
+    P = _P()
+    cfg = workload.CONFIGS[name].replace(H=123, W=201)
+    ims = _quantised(workload.make_batch(cfg, [61, 62]))
+    a, xa = run_forward(cfg, ims)
+    b = P.DeviceBatch(cfg, ims, with_xhat=True, image_u8=True)
+    assert b.img[0].dtype == torch.uint8
+    res = b.forward()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(res.cpu().numpy(), a)
+    for u, v in zip(b.xhat, xa):
+        np.testing.assert_array_equal(u.cpu().numpy(), v)
+    for k, im in enumerate(ims):
+        check_image(cfg, im, res.cpu().numpy()[k], None)
+
+
+def test_u8_host_path_results_only():
+    """The end-to-end host path with 8-bit images and no x_hat read-back (what
+    bench.py's e2e times): same results as the device path, bit for bit."""
+    P = _P()
+    cfg = workload.CONFIGS["ref"].replace(H=200, W=300)
+    n = 11
+    ims = _quantised(workload.make_batch(cfg, list(range(71, 71 + n))))
+    a, _ = run_forward(cfg, ims, with_xhat=False)
+    d = P.desc_from_config(cfg)
+    d.image_u8 = 1
+    lat = [torch.from_numpy(im.latents).pin_memory() for im in ims]
+    img = [torch.from_numpy(workload.to_u8(im.image)).pin_memory() for im in ims]
+    io = [P.CcImageIO(lat[i].data_ptr(), ims[i].arm_w.ctypes.data, ims[i].up_w.ctypes.data,
+                      ims[i].syn_w.ctypes.data, img[i].data_ptr(), None) for i in range(n)]
+    ws_b = P.cc_workspace_bytes_host(d, n)
+    ws = torch.empty(ws_b, dtype=torch.uint8, device="cuda")
+    res = np.zeros((n, 4))
+    for _ in range(2):
+        P.cc_rd_forward_host(d, io, res, ws.data_ptr(), ws_b, torch.cuda.current_stream().cuda_stream)
+        np.testing.assert_array_equal(res, a)
+
+
+def test_i8_latents_host_path():
+    """latents_i8 (host path): int8 latent uploads widened on the device give
+    the device path's results bit for bit; device entry points refuse the flag."""
+    P = _P()
+    cfg = workload.CONFIGS["ref"].replace(H=150, W=222)
+    n = 3
+    ims = _quantised(workload.make_batch(cfg, list(range(81, 81 + n))))
+    assert max(np.abs(im.latents).max() for im in ims) <= 127
+    a, _ = run_forward(cfg, ims, with_xhat=False)
+    d = P.desc_from_config(cfg)
+    d.image_u8 = 1
+    d.latents_i8 = 1
+    lat = [torch.from_numpy(im.latents.astype(np.int8)).pin_memory() for im in ims]
+    img = [torch.from_numpy(workload.to_u8(im.image)).pin_memory() for im in ims]
+    io = [P.CcImageIO(lat[i].data_ptr(), ims[i].arm_w.ctypes.data, ims[i].up_w.ctypes.data,
+                      ims[i].syn_w.ctypes.data, img[i].data_ptr(), None) for i in range(n)]
+    ws_b = P.cc_workspace_bytes_host(d, n)
+    ws = torch.empty(ws_b, dtype=torch.uint8, device="cuda")
+    res = np.zeros((n, 4))
+    P.cc_rd_forward_host(d, io, res, ws.data_ptr(), ws_b, torch.cuda.current_stream().cuda_stream)
+    np.testing.assert_array_equal(res, a)
+    b = P.DeviceBatch(cfg, ims, with_xhat=False)
+    b.desc.latents_i8 = 1
+    with pytest.raises(P.CcError) as e:
+        b.forward()
+    assert e.value.code == P.ccrd.CC_ENOTSUP
+
+
+def test_u8_training_refused():
+    P = _P()
+    d = P.desc_from_config(workload.CONFIGS["ref"].replace(H=24, W=40))
+    d.image_u8 = 1
+    with pytest.raises(P.CcError) as e:
+        P.cc_train_step(d, 8, 8, 8, 8, 8, None, 8, 8, 8, 1 << 30)
+    assert e.value.code == P.ccrd.CC_ENOTSUP

@@ -190,6 +190,23 @@ def gen_image(rng: np.random.Generator, H: int, W: int) -> np.ndarray:
     return out
 
 
+def to_u8(img: np.ndarray) -> np.ndarray:
+    """8-bit planes of an image in [0, 1] (the paper's sources are 8-bit RGB):
+    v = rint(255 x), clipped.  A storage format, not method arithmetic."""
+    return np.clip(np.rint(np.asarray(img, np.float64) * 255.0), 0, 255).astype(np.uint8)
+
+
+def from_u8(v: np.ndarray) -> np.ndarray:
+    """x = v / 255 in fp32 (IEEE division) -- the value the kernels read for
+    desc.image_u8 = 1; the oracle is fed this image."""
+    return np.asarray(v, np.uint8).astype(np.float32) / np.float32(255.0)
+
+
+def quantize_image_u8(img: np.ndarray) -> np.ndarray:
+    """An fp32 image whose values are exactly representable as 8-bit levels."""
+    return from_u8(to_u8(img))
+
+
 def gen_latents(rng: np.random.Generator, cfg: Config) -> np.ndarray:
     """i.i.d. rounded Laplace(0, lat_scale) clipped to +-lat_clip, int16, packed
     level by level (BASELINE.json configs[0]/[1]; reading #20)."""
