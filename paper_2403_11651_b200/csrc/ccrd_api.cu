@@ -673,14 +673,24 @@ __global__ void widen_i8_kernel(const int8_t* __restrict__ in, int16_t* __restri
 
 // The host path stages CHUNKS of HOST_CHUNK images (one forward_batch call
 // each: batched pyramid launch, ARM / synthesis kernels back to back) in
-// HOST_SLOTS double-buffered slots: the upload of chunk c+1 overlaps the
-// compute of chunk c.  One image per call measured 23 % slower than batched.
-constexpr int HOST_SLOTS = 2, HOST_CHUNK = 4;
+// HOST_SLOTS rotating slots: uploads run ahead of the compute by up to
+// HOST_SLOTS - 1 chunks.  One image per call measured 23 % slower than batched.
+constexpr int HOST_SLOTS_MAX = 4, HOST_CHUNK_MAX = 8;
+// defaults 3 slots x 4 images (swept on B200, batched 2K: 2x1 9.42, 2x2 9.70,
+// 2x4 9.54, 3x4 10.07, 4x4 10.06, 2x8 9.62 Gpx/s e2e); CCRD_HOST_SLOTS /
+// CCRD_HOST_CHUNK (read per call) for experiments
+static int host_env(const char* name, int def, int lo, int hi) {
+  const char* v = getenv(name);
+  const int x = v ? atoi(v) : def;
+  return x < lo ? lo : (x > hi ? hi : x);
+}
 
 size_t cc_workspace_bytes_host(const cc_model_desc* desc, int32_t n_img) {
   if (validate(desc) != CC_OK || n_img < 1) return 0;
   return slice_bytes(*desc, nullptr) * (size_t)n_img +
-         align256(sizeof(cc_rd_result) * (size_t)n_img) + HOST_SLOTS * HOST_CHUNK * stage_slot_bytes(*desc);
+         align256(sizeof(cc_rd_result) * (size_t)n_img) +
+         (size_t)host_env("CCRD_HOST_SLOTS", 3, 2, HOST_SLOTS_MAX) * host_env("CCRD_HOST_CHUNK", 4, 1, HOST_CHUNK_MAX) *
+             stage_slot_bytes(*desc);
 }
 
 int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t n_img, cc_rd_result* results,
@@ -699,6 +709,8 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
   cc_rd_result* dres = (cc_rd_result*)(ws + per * (size_t)n_img);
   char* stage = ws + per * (size_t)n_img + align256(sizeof(cc_rd_result) * (size_t)n_img);
   const size_t slot = stage_slot_bytes(d);
+  const int HOST_SLOTS = host_env("CCRD_HOST_SLOTS", 3, 2, HOST_SLOTS_MAX);
+  const int HOST_CHUNK = host_env("CCRD_HOST_CHUNK", 4, 1, HOST_CHUNK_MAX);
   int64_t n_lat = 0;
   LevelGeom lg;
   level_dims(d, lg, &n_lat);
@@ -729,7 +741,8 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
   const bool conc = concurrent_streams();
   SideStream* side = nullptr;
   if (conc && (rc = side_stream(&side))) return rc;
-  cudaEvent_t copied[HOST_SLOTS], computed[HOST_SLOTS], computed_side[HOST_SLOTS], read_back[HOST_SLOTS];
+  cudaEvent_t copied[HOST_SLOTS_MAX], computed[HOST_SLOTS_MAX], computed_side[HOST_SLOTS_MAX],
+      read_back[HOST_SLOTS_MAX];
   for (int k = 0; k < HOST_SLOTS; k++) {
     cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&computed[k], cudaEventDisableTiming);
@@ -748,10 +761,10 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
   ReduceJob* jobs = new ReduceJob[n_img];
   for (int i0 = 0, c = 0; i0 < n_img && rc == CC_OK; i0 += HOST_CHUNK, c++) {
     const int k = c % HOST_SLOTS, m = n_img - i0 < HOST_CHUNK ? n_img - i0 : HOST_CHUNK;
-    const int16_t* l1[HOST_CHUNK];
-    const float *a1[HOST_CHUNK], *u1[HOST_CHUNK], *s1[HOST_CHUNK], *i1[HOST_CHUNK];
-    float* x1[HOST_CHUNK];
-    float* dxhs[HOST_CHUNK];
+    const int16_t* l1[HOST_CHUNK_MAX];
+    const float *a1[HOST_CHUNK_MAX], *u1[HOST_CHUNK_MAX], *s1[HOST_CHUNK_MAX], *i1[HOST_CHUNK_MAX];
+    float* x1[HOST_CHUNK_MAX];
+    float* dxhs[HOST_CHUNK_MAX];
     cudaStreamWaitEvent(cs, computed[k], 0);  // slot k's inputs were consumed by chunk c - HOST_SLOTS
     cudaStreamWaitEvent(cs, computed_side[k], 0);
     for (int j = 0; j < m && rc == CC_OK; j++) {

@@ -182,11 +182,11 @@ def test_synthesize_stage_from_dense():
 
 def test_deterministic_and_host_path_match():
     """Bitwise determinism, and the host-buffer (end-to-end) path -- three
-    streams, two slots of four images reused from the ninth image on -- gives the
+    streams, three slots of four images reused from the 13th image on -- gives the
     same numbers bit for bit."""
     P = _P()
     cfg = workload.CONFIGS["ref"].replace(H=200, W=300)
-    n = 11
+    n = 14
     ims = workload.make_batch(cfg, list(range(41, 41 + n)))
     a, xa = run_forward(cfg, ims)
     b, xb = run_forward(cfg, ims)
@@ -283,7 +283,7 @@ def test_u8_host_path_results_only():
     bench.py's e2e times): same results as the device path, bit for bit."""
     P = _P()
     cfg = workload.CONFIGS["ref"].replace(H=200, W=300)
-    n = 11
+    n = 14
     ims = _quantised(workload.make_batch(cfg, list(range(71, 71 + n))))
     a, _ = run_forward(cfg, ims, with_xhat=False)
     d = P.desc_from_config(cfg)
