@@ -79,6 +79,84 @@ __host__ __device__ constexpr uint32_t bt_idesc(int n) {
 
 __device__ __forceinline__ uint64_t ldg_f2(const float* p) { return ldp2(__ldg(reinterpret_cast<const float2*>(p))); }
 
+// 16 TMEM lanes x 8 NREP columns (16x256b, NREP repetitions): thread t gets
+// lane t/4 (regs 4m, 4m+1) and lane t/4 + 8 (regs 4m+2, 4m+3), columns
+// 8m + 2(t%4), +1 (CUTLASS SM100_TMEM_LOAD_16dp256b{2,4}x layouts)
+template <int NREP>
+__device__ __forceinline__ void tmem_ld16x256(uint32_t taddr, float (&v)[4 * NREP]);
+template <>
+__device__ __forceinline__ void tmem_ld16x256<4>(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int k = 0; k < 16; k++) v[k] = __uint_as_float(r[k]);
+}
+template <>
+__device__ __forceinline__ void tmem_ld16x256<2>(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int k = 0; k < 8; k++) v[k] = __uint_as_float(r[k]);
+}
+
+// Epilogue of one warp: its lane quarter (= tile row oy) x channels c0 ..
+// c0 + 8 NREP of D2 (TMEM address td2 = lane quarter + the column of c0):
+// y = D2 + b2 (+ x from `res`, RES) stored NHWC.  With the 16x256b loads every
+// global access of the warp covers 8 pixels x 32 contiguous bytes (the 32x32b
+// thread-per-pixel form puts lanes 256 B apart: 4x the L1 wavefronts).
+// partv[k] accumulates the merge partial (Wm . y over these channels) of
+// pixel column 8k + t/4.
+template <int NREP, bool RES>
+__device__ __forceinline__ void epi2_rows(uint32_t td2, int c0, const float* res, float* out, int oy, int ho, int ox0,
+                                          int wo, const float* b2s, const float* wms, float (&partv)[4], int lane) {
+  const int t0 = lane & 3, t1 = lane >> 2;
+#pragma unroll
+  for (int g = 0; g < 2; g++) {  // 16-lane halves of the quarter (all lanes: .sync.aligned)
+    float d[4 * NREP];
+    tmem_ld16x256<NREP>(td2 + ((uint32_t)(16 * g) << 16), d);
+#pragma unroll
+    for (int rr = 0; rr < 2; rr++) {
+      const int ox = ox0 + 16 * g + 8 * rr + t1;
+      if (oy < ho && ox < wo) {
+        const int64_t po = ((int64_t)oy * wo + ox) * BT_C + c0 + 2 * t0;
+        float2 xv[NREP];
+#pragma unroll
+        for (int m = 0; m < NREP; m++)
+          xv[m] = RES ? __ldg(reinterpret_cast<const float2*>(res + po + 8 * m)) : make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int m = 0; m < NREP; m++) {
+          const int c = c0 + 8 * m + 2 * t0;
+          const float2 y = make_float2(d[4 * m + 2 * rr] + b2s[c] + xv[m].x, d[4 * m + 2 * rr + 1] + b2s[c + 1] + xv[m].y);
+          *reinterpret_cast<float2*>(out + po + 8 * m) = y;
+          partv[2 * g + rr] = fmaf(wms[c], y.x, fmaf(wms[c + 1], y.y, partv[2 * g + rr]));
+        }
+      }
+    }
+  }
+}
+
+// Sum each pixel's partials over the 4 threads holding its channels and write
+// them to mp[slot][pixel] (pixel = quarter * 32 + column).
+__device__ __forceinline__ void epi2_partials(float (&partv)[4], float* mp, int slot, int quarter, int lane) {
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    partv[k] += __shfl_xor_sync(0xffffffffu, partv[k], 1);
+    partv[k] += __shfl_xor_sync(0xffffffffu, partv[k], 2);
+  }
+  if ((lane & 3) == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; k++) mp[slot * 128 + quarter * 32 + 8 * k + (lane >> 2)] = partv[k];
+  }
+}
+
 template <bool DOWN>
 __global__ void __launch_bounds__(BT_THREADS, 1) an_block_tc_kernel(const __grid_constant__ BlockTcParams p) {
   using S = BtSmem<DOWN>;
@@ -296,9 +374,14 @@ __global__ void __launch_bounds__(BT_THREADS, 1) an_block_tc_kernel(const __grid
     ph ^= 1;
     asm volatile("tcgen05.fence::after_thread_sync;");
 
-    // ---- 5. y = D2 + b2 (+ bid) (+ x); pixel = TMEM lane = (row warp&3, column lane),
-    //         16 channels per warp (quarter cq = warp >> 2)
-    {
+    // ---- 5. y = D2 + b2 (+ bid) (+ x); 16 channels per warp (quarter cq = warp >> 2)
+    if constexpr (DOWN) {
+      const int cq = warp >> 2;
+      float partv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      epi2_rows<2, false>(tlane + BT_HID + cq * 16, cq * 16, nullptr, pout, ty * BT_TY + (warp & 3), p.ho, tx * BT_TX,
+                          p.wo, b2s, wms, partv, lane);
+      if (plat) epi2_partials(partv, mp, cq, warp & 3, lane);
+    } else {
       const int cq = warp >> 2, r = (warp & 3) * 32 + lane;
       float d[16];
       tmem_row<16>(tlane + BT_HID + cq * 16, d);
@@ -518,36 +601,16 @@ __global__ void __launch_bounds__(BT_THREADS, 1) an_block_ws_kernel(const __grid
         // ---- epi2(prev): y = D2 + b2 + x
         mbar_wait(d2_full, (i - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        float d[32];
-        tmem_row<32>(tlane + BT_HID + hh * 32, d);
         const int pimg = prev / p.tpi, ptr = prev - pimg * p.tpi;
         const int pty = ptr / p.tiles_x, ptx = ptr - pty * p.tiles_x;
         const float* pin = p.in + pimg * p.in_img;
         float* pout = p.out + pimg * p.out_img;
         float* plat = p.lat ? p.lat + pimg * p.lat_img : nullptr;
-        const int oy2 = pty * BT_TY + q, ox2 = ptx * BT_TX + lane;
-        float part = 0.0f;
-        if (oy2 < p.ho && ox2 < p.wo) {
-          const int64_t po = ((int64_t)oy2 * p.wo + ox2) * BT_C + hh * 32;
-          const float4* xr = reinterpret_cast<const float4*>(pin + po);
-          float4* o = reinterpret_cast<float4*>(pout + po);
-          float4 xv[8];
-#pragma unroll
-          for (int u = 0; u < 8; u++) xv[u] = __ldg(xr + u);
-#pragma unroll
-          for (int u = 0; u < 8; u++) {
-            const int c = hh * 32 + 4 * u;
-            const float4 y = make_float4(d[4 * u] + b2s[c] + xv[u].x, d[4 * u + 1] + b2s[c + 1] + xv[u].y,
-                                         d[4 * u + 2] + b2s[c + 2] + xv[u].z, d[4 * u + 3] + b2s[c + 3] + xv[u].w);
-            o[u] = y;
-            part = fmaf(wms[c], y.x, part);
-            part = fmaf(wms[c + 1], y.y, part);
-            part = fmaf(wms[c + 2], y.z, part);
-            part = fmaf(wms[c + 3], y.w, part);
-          }
-        }
+        float partv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        epi2_rows<4, true>(tlane + BT_HID + hh * 32, hh * 32, pin, pout, pty * BT_TY + q, p.ho, ptx * BT_TX, p.wo, b2s,
+                           wms, partv, lane);
         if (plat) {
-          mp[hh * 128 + q * 32 + lane] = part;
+          epi2_partials(partv, mp, hh, q, lane);
           epi_sync();
           const int te = e * 32 + lane;
           if (te < 128) {
@@ -821,36 +884,16 @@ __global__ void __launch_bounds__(BT_THREADS, 1) an_block_h16_kernel(const __gri
       if (prev >= 0) {
         mbar_wait(d2_full, (i - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        float d[32];
-        tmem_row<32>(tlane + BT_HID + 128 + hh * 32, d);
         const int pimg = prev / p.tpi, ptr = prev - pimg * p.tpi;
         const int pty = ptr / p.tiles_x, ptx = ptr - pty * p.tiles_x;
         const float* pin = p.in + pimg * p.in_img;
         float* pout = p.out + pimg * p.out_img;
         float* plat = p.lat ? p.lat + pimg * p.lat_img : nullptr;
-        const int oy2 = pty * BT_TY + q, ox2 = ptx * BT_TX + lane;
-        float part = 0.0f;
-        if (oy2 < p.ho && ox2 < p.wo) {
-          const int64_t po = ((int64_t)oy2 * p.wo + ox2) * BT_C + hh * 32;
-          const float4* xr = reinterpret_cast<const float4*>(pin + po);
-          float4* o = reinterpret_cast<float4*>(pout + po);
-          float4 xv[8];
-#pragma unroll
-          for (int u = 0; u < 8; u++) xv[u] = __ldg(xr + u);
-#pragma unroll
-          for (int u = 0; u < 8; u++) {
-            const int c = hh * 32 + 4 * u;
-            const float4 y = make_float4(d[4 * u] + b2s[c] + xv[u].x, d[4 * u + 1] + b2s[c + 1] + xv[u].y,
-                                         d[4 * u + 2] + b2s[c + 2] + xv[u].z, d[4 * u + 3] + b2s[c + 3] + xv[u].w);
-            o[u] = y;
-            part = fmaf(wms[c], y.x, part);
-            part = fmaf(wms[c + 1], y.y, part);
-            part = fmaf(wms[c + 2], y.z, part);
-            part = fmaf(wms[c + 3], y.w, part);
-          }
-        }
+        float partv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        epi2_rows<4, true>(tlane + BT_HID + 128 + hh * 32, hh * 32, pin, pout, pty * BT_TY + q, p.ho, ptx * BT_TX, p.wo,
+                           b2s, wms, partv, lane);
         if (plat) {
-          mp[hh * 128 + q * 32 + lane] = part;
+          epi2_partials(partv, mp, hh, q, lane);
           epi_sync();
           const int te = e * 32 + lane;
           if (te < 128) {
