@@ -101,6 +101,9 @@ def lib():
         L.orc_analysis_forward.argtypes = [P(OrcAnalysis), C.c_void_p, C.c_void_p, C.c_void_p, P(C.c_int64)]
         L.orc_decode_u8.restype = None
         L.orc_decode_u8.argtypes = [P(OrcModel), C.c_void_p, C.c_void_p]
+        L.orc_arm_decode.restype = C.c_int
+        L.orc_arm_decode.argtypes = [P(OrcModel), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, P(C.c_double)]
         L.orc_train_param_count.restype = C.c_int64
         L.orc_train_param_count.argtypes = [P(OrcModel)]
         L.orc_train_grad.restype = C.c_int
@@ -306,6 +309,20 @@ def decode_u8(m: OrcModel, x_hat) -> np.ndarray:
     out = np.zeros((m.H, m.W, 3), np.uint8)
     lib().orc_decode_u8(C.byref(m), _p(xh), _p(out))
     return out
+
+
+def arm_decode(m: OrcModel, truth, arm_w):
+    """NEXT-3: raster-order autoregressive decode (the entropy decoder played by
+    `truth`).  Returns (status, decoded int16, mu, b, bits, rate); status -1 if
+    a context read an undecoded latent."""
+    t = _c(truth, np.int16)
+    aw = _c(arm_w, np.float32)
+    n = t.size
+    dec = np.full(n, -32768, np.int16)
+    mu, b, bits = (np.zeros(n) for _ in range(3))
+    rate = C.c_double(0.0)
+    st = lib().orc_arm_decode(C.byref(m), _p(t), _p(aw), _p(dec), _p(mu), _p(b), _p(bits), C.byref(rate))
+    return st, dec, mu, b, bits, rate.value
 
 
 def decode_image(cfg, im):

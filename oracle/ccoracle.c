@@ -162,6 +162,56 @@ double orc_rate_rows(const orc_model* m, const int16_t* latents, const float* ar
   return total;
 }
 
+/* ---- NEXT-3 (decoder: the decoder recovers
+ *      the latents one by one, the ARM conditioning each on already decoded
+ *      neighbours).  The autoregressive decode of every grid in raster order.
+ *      The entropy decoder (range coder) is out of scope: `truth` plays it --
+ *      once the ARM has produced (mu, b) for latent (i, j), the decoded value
+ *      truth[i][j] is revealed and written to `decoded`.  Contexts are read
+ *      from the DECODED grid only; a position not yet decoded is poison:
+ *      returns -1 if one is ever read (the template would not be causal), 0
+ *      otherwise.  Outputs (optional) per latent, packed like the latents:
+ *      mu, b, bits; *rate = their sum (rows in fixed order). -------------- */
+int orc_arm_decode(const orc_model* m, const int16_t* truth, const float* arm_w, int16_t* decoded,
+                   double* mu, double* b, double* bits, double* rate) {
+  int32_t h[ORC_MAX_LEVELS], w[ORC_MAX_LEVELS];
+  const int64_t n = orc_level_dims(m, h, w);
+  unsigned char* known = (unsigned char*)calloc((size_t)n, 1);
+  double total = 0.0, ctx[64];
+  int64_t off = 0;
+  int bad = 0;
+  for (int l = 0; l < m->L && !bad; l++) {
+    for (int i = 0; i < h[l] && !bad; i++)
+      for (int j = 0; j < w[l]; j++) {
+        for (int c = 0; c < m->n_ctx; c++) {
+          const int ii = i + m->ctx_dy[c], jj = j + m->ctx_dx[c];
+          if (ii >= 0 && ii < h[l] && jj >= 0 && jj < w[l]) {
+            const int64_t q = off + (int64_t)ii * w[l] + jj;
+            if (!known[q]) bad = 1;
+            ctx[c] = (double)decoded[q];
+          } else {
+            ctx[c] = 0.0;
+          }
+        }
+        if (bad) break;
+        double mu_, b_;
+        orc_arm_mlp(m, ctx, arm_w, &mu_, &b_, NULL);
+        const int64_t q = off + (int64_t)i * w[l] + j;
+        const double bt = orc_laplace_bits((double)truth[q], mu_, b_, m->p_floor);
+        if (mu) mu[q] = mu_;
+        if (b) b[q] = b_;
+        if (bits) bits[q] = bt;
+        total += bt;
+        decoded[q] = truth[q]; /* the entropy decoder's answer */
+        known[q] = 1;
+      }
+    off += (int64_t)h[l] * w[l];
+  }
+  free(known);
+  if (rate) *rate = total;
+  return bad ? -1 : 0;
+}
+
 /* ---- step 7: one stride-2 transposed convolution along one axis
  *      (Table 1 "1-1-TConv-K", caption "Transpose convolutions use a stride of
  *      2"; readings #11-#13).  Definition of a transposed convolution with

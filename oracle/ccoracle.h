@@ -88,6 +88,10 @@ int orc_rd_forward(const orc_model* m, const int16_t* latents, const float* arm_
 /* Decoder output (NEXT-3; "final output clamped to [0,1]";
  * 8-bit RGB, pixel = 255 x): out[(y W + x) 3 + c] =
  * rint(255 clamp(x_hat[c][y][x], 0, 1)) (round half to even; reading N3). */
+/* NEXT-3: autoregressive decode in raster order (entropy decoder played by
+ * `truth`); 0, or -1 if a context read an undecoded latent. */
+int orc_arm_decode(const orc_model* m, const int16_t* truth, const float* arm_w, int16_t* decoded,
+                   double* mu, double* b, double* bits, double* rate);
 void orc_decode_u8(const orc_model* m, const double* x_hat, uint8_t* out);
 
 /* Rate and per-latent outputs for the latents of rows [r0, r1) of level l only
