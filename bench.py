@@ -428,6 +428,81 @@ def run_decode(args, rk):
         print(json.dumps(out), flush=True)
 
 
+def run_arm_decode(args, rk):
+    """NEXT-3: the decoder's autoregressive ARM as an anti-diagonal wavefront
+    (cc_arm_decode) over the BASELINE.json configs[3] batch -- all images and
+    grids in one call; the entropy decoder is played by the true latents
+    (include/ccrd.h).  Also times one image alone (decode latency)."""
+    import torch
+
+    import paper_2403_11651_b200 as P
+    from paper_2403_11651_b200 import dist
+
+    cfg = workload.CONFIGS[args.config]
+    n_img = args.images or cfg.n_img
+    dev = torch.device("cuda", rk.local_rank)
+    torch.cuda.set_device(dev)
+    P.load()
+    ims = workload.make_batch(cfg, [workload.image_seed(args.seed, g) for g in dist.owned_images(rk.rank, n_img)],
+                              threads=min(16, host_cores()))
+    d = P.desc_from_config(cfg)
+    lat = [torch.from_numpy(im.latents).to(dev) for im in ims]
+    dec = [torch.empty_like(t) for t in lat]
+    rate = torch.zeros(n_img, dtype=torch.float64, device=dev)
+    io = [P.CcImageIO(lat[i].data_ptr(), ims[i].arm_w.ctypes.data, 0, 0, 0, 0) for i in range(n_img)]
+    wsb = P.cc_arm_decode_workspace_bytes(d, n_img)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    dptr = [t.data_ptr() for t in dec]
+
+    def step(k=n_img):
+        P.cc_arm_decode(d, io[:k], dptr[:k], rate.data_ptr(), None, None, None, 0, ws.data_ptr(), wsb,
+                        stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(rk.local_rank)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    sampler.stop()
+    ms = dist.max_over_ranks(ev0.elapsed_time(ev1), device=dev)
+    # one image alone: the decode latency
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(3):
+        step(1)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    lat1_ms = e0.elapsed_time(e1) / 3
+    assert all(torch.equal(a, b) for a, b in zip(dec, lat)), "decoded latents differ from the encoded ones"
+    value = rk.world * n_img * cfg.H * cfg.W * args.steps / (ms / 1e3)
+    macs = P.cc_mac_per_pixel(d)
+    arm_tflops = 2.0 * macs.arm_macs * n_img * args.steps / (ms / 1e3) / 1e12
+    out = {
+        "metric": "autoregressive latent decode (wavefront ARM) pixels/s", "value": value, "unit": "pixels/s",
+        "n_gpus": rk.world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"decode_{args.config}: {n_img} x {cfg.H}x{cfg.W} per GPU, all grids in one call; "
+                               "entropy decoder played by the true latents (include/ccrd.h)",
+                   "latents_per_image": int(ims[0].latents.size)},
+        "latency_one_image_ms": lat1_ms,
+        "arm_tflops": arm_tflops, "arm_frac_of_fp32_peak": arm_tflops / FP32_PEAK_TFLOPS,
+        "context": "paper: ~100 ms per 512x768 decode on one CPU core (ARM + upsampling + synthesis), BASELINE.md",
+        "e2e": None, "gpu_launches": P.ccrd.cc_last_launch_count() * args.steps, "clocks": sampler.summary(),
+    }
+    if rk.rank == 0:
+        print(json.dumps(out), flush=True)
+
+
 def run_analysis(args, rk):
     """NEXT-4: the N-O analysis transform forward (encoding = one forward pass,
     PAPER.md:422-449, 483-484) on Kodak-sized images (no_kodak) by default;
@@ -705,6 +780,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--train", action="store_true", help="time the encoder training iteration (NEXT-2)")
     ap.add_argument("--decode", action="store_true", help="time the decoder output stage (NEXT-3)")
+    ap.add_argument("--arm-decode", action="store_true", help="time the wavefront autoregressive ARM decode (NEXT-3)")
     ap.add_argument("--analysis", default="", help="time the N-O analysis transform (NEXT-4): no_kodak | no_2k")
     ap.add_argument("--tf32", type=int, default=1, choices=(0, 1, 2, 3),
                     help="analysis arithmetic: 0 fp32 cuBLASLt | 1 TF32 fused tcgen05 blocks | 2 TF32 cuBLASLt "
@@ -724,6 +800,8 @@ def main():
         run_decode(args, rk)
     elif args.analysis:
         run_analysis(args, rk)
+    elif args.arm_decode:
+        run_arm_decode(args, rk)
     elif args.config == "8k":
         run_strip(args, rk)
     else:

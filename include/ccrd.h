@@ -278,6 +278,29 @@ size_t cc_analysis_workspace_bytes(const cc_analysis_desc* a);  /* 0 on error  *
 int cc_analysis_forward(const cc_analysis_desc* a, const float* image, const float* weights, float* latents,
                         void* workspace, size_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------------ NEXT-3: ARM decode
+ * The decoder's autoregressive ARM (the latents
+ * are decoded one by one, the ARM conditioning each on already decoded
+ * neighbours) as a wavefront over the anti-diagonals t = a i + j of every
+ * grid, a = 1 + max over the template's dy < 0 of floor(dx / -dy) (so every
+ * context of (i, j) lies on an earlier t); all images and grids at once.  The
+ * entropy decoder (range coder) is out of scope: it is played by
+ * io[i].latents (DEVICE int16, packed like the latents) -- a latent's value
+ * is revealed only after its (mu, b) were computed from the latents decoded
+ * before it; contexts are read from the decoded values only, and a read of a
+ * not-yet-decoded latent is counted in *poison_reads.  io[i].arm_w: HOST
+ * blob; the other io fields are ignored.  Outputs: decoded[i] (DEVICE int16,
+ * packed), rate (DEVICE double [n_img], sum of -log2 P per image), optional
+ * per-latent mu / scale / bits (host arrays of DEVICE pointers, or NULL),
+ * poison_reads (DEVICE int32 [1] or NULL; accumulated, the caller zeroes it).
+ * Per-latent (mu, scale, bits) are bit-identical to cc_arm_rate's.  Latent
+ * values must not be -32768 (the undecoded marker).  Test hook: env
+ * CCRD_DEC_SKEW overrides a (a too small skew must produce poison reads). */
+size_t cc_arm_decode_workspace_bytes(const cc_model_desc* desc, int32_t n_img); /* 0 on error */
+int cc_arm_decode(const cc_model_desc* desc, const cc_image_io* io, int32_t n_img, int16_t* const* decoded,
+                  double* rate, float* const* mu, float* const* scale, float* const* bits, int32_t* poison_reads,
+                  void* workspace, size_t workspace_bytes, void* stream);
+
 /* Stage entry: ARM rate only (PAPER.md:120 R term).  rate: DEVICE double [1].
  * Optional DEVICE float arrays (packed like the latents, NULL to skip):
  * mu, scale (= b), bits (per latent -log2 P).  Workspace as cc_rd_forward(1). */

@@ -11,7 +11,7 @@ from .ccrd import (  # noqa: F401
     cc_synthesize, cc_upsample, cc_validate, cc_workspace_bytes, cc_workspace_bytes_host,
     cc_workspace_bytes_strip, desc_from_config, load, cc_train_param_count, cc_train_workspace_bytes,
     cc_train_step, CcAdam, DeviceTrainer, cc_decode, CcAnalysisDesc, analysis_desc, cc_analysis_param_count,
-    cc_analysis_workspace_bytes, cc_analysis_forward,
+    cc_analysis_workspace_bytes, cc_analysis_forward, cc_arm_decode, cc_arm_decode_workspace_bytes,
 )
 
 __version__ = "0.1.0"

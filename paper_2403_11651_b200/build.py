@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libccrd.so")
-SOURCES = ["arm_rate.cu", "arm_tc.cu", "pyramid.cu", "synth.cu", "train.cu", "analysis.cu", "analysis_tc.cu", "ccrd_api.cu"]
+SOURCES = ["arm_rate.cu", "arm_tc.cu", "arm_decode.cu", "pyramid.cu", "synth.cu", "train.cu", "analysis.cu", "analysis_tc.cu", "ccrd_api.cu"]
 HEADERS = ["ccrd_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

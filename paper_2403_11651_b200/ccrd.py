@@ -88,7 +88,7 @@ EXPORTS = ["cc_workspace_bytes", "cc_rd_forward", "cc_workspace_bytes_host", "cc
            "cc_profile_begin", "cc_profile_end", "cc_strip_window", "cc_strip_latent_count",
            "cc_workspace_bytes_strip", "cc_rd_forward_strip", "cc_train_param_count",
            "cc_train_workspace_bytes", "cc_train_step", "cc_decode", "cc_analysis_param_count",
-           "cc_analysis_workspace_bytes", "cc_analysis_forward"]
+           "cc_analysis_workspace_bytes", "cc_analysis_forward", "cc_arm_decode_workspace_bytes", "cc_arm_decode"]
 
 _lib = None
 
@@ -124,6 +124,10 @@ def load(rebuild_if_stale: bool = True) -> C.CDLL:
     L.cc_rd_forward_host.argtypes = [D, P(CcImageIO), C.c_int32, V, V, S, V]
     L.cc_arm_rate.restype = C.c_int
     L.cc_arm_rate.argtypes = [D, V, V, V, V, V, V, V, S, V]
+    L.cc_arm_decode_workspace_bytes.restype = S
+    L.cc_arm_decode_workspace_bytes.argtypes = [D, C.c_int32]
+    L.cc_arm_decode.restype = C.c_int
+    L.cc_arm_decode.argtypes = [D, V, C.c_int32, V, V, V, V, V, V, V, S, V]
     L.cc_upsample.restype = C.c_int
     L.cc_upsample.argtypes = [D, V, V, V, V, S, V]
     L.cc_synthesize.restype = C.c_int
@@ -252,6 +256,26 @@ def cc_arm_rate(desc, latents_ptr, arm_w: np.ndarray, rate_ptr, mu_ptr, scale_pt
     aw = np.ascontiguousarray(arm_w, np.float32)
     _check(load().cc_arm_rate(C.byref(desc), latents_ptr, aw.ctypes.data, rate_ptr, mu_ptr, scale_ptr, bits_ptr,
                               ws_ptr, ws_bytes, stream_ptr), "cc_arm_rate")
+
+
+def cc_arm_decode_workspace_bytes(desc, n_img: int) -> int:
+    return load().cc_arm_decode_workspace_bytes(C.byref(desc), n_img)
+
+
+def cc_arm_decode(desc, io: Sequence["CcImageIO"], decoded_ptrs, rate_ptr, mu_ptrs=None, scale_ptrs=None,
+                  bits_ptrs=None, poison_ptr=0, ws_ptr=0, ws_bytes=0, stream_ptr=0) -> None:
+    """NEXT-3 wavefront ARM decode of len(io) images (include/ccrd.h): io[i].latents
+    (device) play the entropy decoder, io[i].arm_w host blobs; *_ptrs: lists of
+    device pointers (or None)."""
+    n = len(io)
+    arr = (CcImageIO * n)(*io)
+    vp = C.c_void_p * n
+
+    def ptrs(lst):
+        return vp(*lst) if lst is not None else None
+    _check(load().cc_arm_decode(C.byref(desc), arr, n, ptrs(decoded_ptrs), rate_ptr, ptrs(mu_ptrs),
+                                ptrs(scale_ptrs), ptrs(bits_ptrs), poison_ptr or None, ws_ptr, ws_bytes, stream_ptr),
+           "cc_arm_decode")
 
 
 def cc_upsample(desc, latents_ptr, up_w: np.ndarray, dense_ptr, ws_ptr=0, ws_bytes=0, stream_ptr=0) -> None:

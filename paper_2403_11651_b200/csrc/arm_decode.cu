@@ -1,0 +1,267 @@
+// arm_decode.cu -- NEXT-3: the decoder's autoregressive ARM as a wavefront on
+// the GPU (the decoder recovers the latents one by
+// one, the ARM conditioning each on already decoded neighbours; SURVEY.md
+// 8(f) NEXT-3 "wavefront-parallel autoregressive ARM (anti-diagonal schedule
+// over the causal template) emitting per-latent (mu, b)").
+//
+// Dependency: latent (i, j) of a grid needs the decoded latents at
+// (i + dy, j + dx) for every context offset (dy < 0, or dy = 0 and dx < 0).
+// With the skew a = 1 + max over dy < 0 of floor(dx / -dy), every context of
+// (i, j) lies on an earlier step of t = a i + j, so the latents of one step
+// are independent: step t evaluates all of them at once (anti-diagonal
+// wavefront), T = a (h - 1) + w steps per grid instead of h w.
+//
+// One launch per image (its ARM weights in the parameter bank: uniform FFMA2
+// operands), one CTA per grid; thread k owns the rows r = k (mod threads).  The
+// decoded values of the last 32 columns of each live row sit in a shared-memory
+// ring (row r at ring row r mod RR, RR >= w/a + 5: no live row aliases a
+// context row; a row's newest column is at most 3a + 4 < 32 ahead of any
+// column read from it, so no slot is overwritten while still needed).  The
+// ring starts POISONED (INT16_MIN, never a valid latent here): a context read
+// of a latent not decoded yet is counted and corrupts (mu, b), so the parity
+// tests catch any schedule error.  The entropy decoder (range coder) is out of
+// scope: it is played by `truth` -- after (mu, b) of a latent exist, its value
+// is revealed and written to the ring and to `decoded`.
+//
+// Arithmetic: the encoder's own code (arm_math.cuh: FFMA2 dense layers, folded
+// residuals, Laplace -log2 P), one latent per thread: every latent's (mu,
+// log-scale, bits) is bit-identical to cc_arm_rate's.
+#include <cstring>
+#include <vector>
+
+#include "arm_math.cuh"
+#include "ccrd_common.cuh"
+
+namespace ccrd {
+
+constexpr int DEC_THREADS = 512;
+constexpr int DEC_STREAMS = 64;  // one launch per image, spread over a pool of streams (concurrent kernels)
+constexpr int DEC_RING = 32;  // columns kept per live row
+constexpr int16_t DEC_POISON = INT16_MIN;
+
+// One launch = one image: its ARM weights live in the kernel-parameter bank, so
+// every FFMA2 takes them as uniform operands (no shared-memory traffic), as in
+// the encoder's arm_rate_kernel.
+template <int C, int NH, int NHL>
+struct DecParams {
+  ArmGeom g;        // level dims, Laplace clamps / floor (laplace_bits)
+  int32_t a;        // wavefront skew
+  int32_t rr_mask;  // ring rows - 1 (power of two)
+  int8_t dy[CC_MAX_CTX], dx[CC_MAX_CTX];
+  const int16_t* truth;  // the entropy decoder's answers, packed like the latents
+  int16_t* decoded;
+  float* mu;             // optional per-latent outputs
+  float* scale;
+  float* bits;
+  double* partial;        // [L] per-grid rate of this image
+  int32_t* poison_reads;  // optional counter
+  ArmWeights<C, NH, NHL> w;
+};
+
+template <int C, int NH, int NHL>
+__global__ void __launch_bounds__(DEC_THREADS, 1)
+    arm_decode_kernel(const __grid_constant__ DecParams<C, NH, NHL> p) {
+  extern __shared__ int16_t ring[];  // [RR][DEC_RING]
+  __shared__ float wsum[DEC_THREADS / 32];
+  const int l = blockIdx.x;
+  const int nring = (p.rr_mask + 1) * DEC_RING;
+  for (int i = threadIdx.x; i < nring; i += DEC_THREADS) ring[i] = DEC_POISON;
+  __syncthreads();
+
+  const int h = p.g.lv.h[l], w = p.g.lv.w[l], a = p.a;
+  const int64_t off = p.g.lv.off[l];
+  const int16_t* __restrict__ truth = p.truth + off;
+  int16_t* decoded = p.decoded + off;
+  const int T = a * (h - 1) + w;
+  float bsum = 0.0f;
+  int poison = 0;
+#pragma unroll 1
+  for (int s = 0; s < T; s++) {
+    // rows on this step: 0 <= s - a r < w
+    const int r_lo = s - w + 1 <= 0 ? 0 : (s - w + a) / a;
+    const int r_hi = min(h - 1, s / a);
+    int r = r_lo + (((int)threadIdx.x - r_lo) % DEC_THREADS + DEC_THREADS) % DEC_THREADS;
+#pragma unroll 1
+    for (; r <= r_hi; r += DEC_THREADS) {
+      const int j = s - a * r;
+      const int64_t q = (int64_t)r * w + j;
+      // the entropy decoder's answer, loaded now (used only after (mu, b) exist)
+      // so its memory latency hides under the MLP
+      const int16_t yv = truth[q];
+      float z0[1][C];
+#pragma unroll
+      for (int c = 0; c < C; c++) {
+        const int rr = r + p.dy[c], jj = j + p.dx[c];
+        float v = 0.0f;
+        if (rr >= 0 && jj >= 0 && jj < w) {
+          const int16_t q = ring[(rr & p.rr_mask) * DEC_RING + (jj & (DEC_RING - 1))];
+          poison += (q == DEC_POISON);
+          v = (float)q;
+        }
+        z0[0][c] = v;
+      }
+      float z[1][NH];
+      dense_ffma2<1, C, NH / 2, true>(z0, z, p.w.w0, p.w.b0);
+#pragma unroll
+      for (int k = 0; k < NHL - 1; k++) {
+        float zn[1][NH];
+        dense_ffma2<1, NH, NH / 2, true>(z, zn, p.w.wh[k], p.w.bh[k]);
+#pragma unroll
+        for (int n = 0; n < NH; n++) z[0][n] = zn[0][n];
+      }
+      uint64_t o = ldp2(p.w.bo);
+#pragma unroll
+      for (int n = 0; n < NH; n++) o = ffma2(f2pack(z[0][n], z[0][n]), ldp2(p.w.wo[n]), o);
+      const float2 ms = f2unpack(o);
+      const float bt = laplace_bits((float)yv, ms.x, ms.y, p.g);
+      bsum += bt;
+      ring[(r & p.rr_mask) * DEC_RING + (j & (DEC_RING - 1))] = yv;
+      decoded[q] = yv;
+      if (p.bits) p.bits[off + q] = bt;
+      if (p.mu) p.mu[off + q] = ms.x;
+      if (p.scale) p.scale[off + q] = __expf(fminf(fmaxf(ms.y, p.g.lsmin), p.g.lsmax));
+    }
+    __syncthreads();  // step s's ring writes before step s + 1's reads
+  }
+  if (p.poison_reads && poison) atomicAdd(p.poison_reads, poison);
+  // CTA rate partial, fixed order
+#pragma unroll
+  for (int o2 = 16; o2 > 0; o2 >>= 1) bsum += __shfl_xor_sync(0xffffffffu, bsum, o2);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = bsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < DEC_THREADS / 32; k++) t += (double)wsum[k];
+    p.partial[l] = t;
+  }
+}
+
+// rate[i] = sum over the grids of image i, level order
+__global__ void dec_rate_kernel(const double* __restrict__ partial, int L, int n, double* __restrict__ rate) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double t = 0.0;
+  for (int l = 0; l < L; l++) t += partial[i * L + l];
+  rate[i] = t;
+}
+
+// ---------------------------------------------------------------- host side
+int dec_skew(const cc_model_desc& d) {
+  int a = 1;
+  for (int c = 0; c < d.n_ctx; c++)
+    if (d.ctx_dy[c] < 0) {
+      const int dy = -d.ctx_dy[c], dx = d.ctx_dx[c];
+      const int need = (dx >= 0 ? dx / dy : -((-dx + dy - 1) / dy)) + 1;  // floor(dx / dy) + 1
+      if (need > a) a = need;
+    }
+  return a;
+}
+
+static int ring_rows(const cc_model_desc& d, int a, int w0) {
+  int rr = 1;
+  while (rr < w0 / a + 6) rr <<= 1;
+  (void)d;
+  return rr;
+}
+
+size_t dec_workspace_bytes(const cc_model_desc& d, int n_img) {
+  return (size_t)n_img * d.L * sizeof(double) + 256;  // per-grid rate partials
+}
+
+// a pool of streams for the per-image launches (joined back to the caller's)
+struct DecStreams {
+  cudaStream_t s[DEC_STREAMS] = {};
+  cudaEvent_t ev[DEC_STREAMS + 1] = {};
+  int device = -1;
+};
+static thread_local DecStreams g_dec;
+
+static int dec_streams(DecStreams** out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (g_dec.device != dev) {
+    for (int k = 0; k < DEC_STREAMS; k++)
+      if (cudaStreamCreateWithFlags(&g_dec.s[k], cudaStreamNonBlocking) != cudaSuccess) return -1;
+    for (int k = 0; k <= DEC_STREAMS; k++)
+      if (cudaEventCreateWithFlags(&g_dec.ev[k], cudaEventDisableTiming) != cudaSuccess) return -1;
+    g_dec.device = dev;
+  }
+  *out = &g_dec;
+  return 0;
+}
+
+template <int C, int NH, int NHL>
+static int launch_dec(const cc_model_desc& d, const ArmGeom& g, int a_override, int n_img,
+                      const int16_t* const* truth, const float* const* arm_w, int16_t* const* decoded,
+                      float* const* mu, float* const* scale, float* const* bits, double* rate, int32_t* poison,
+                      void* ws, cudaStream_t s) {
+  DecParams<C, NH, NHL> p;
+  memset(&p, 0, sizeof(p));
+  p.g = g;
+  p.a = a_override > 0 ? a_override : dec_skew(d);
+  const int rr = ring_rows(d, p.a, g.lv.w[0]);
+  p.rr_mask = rr - 1;
+  for (int c = 0; c < d.n_ctx; c++) {
+    p.dy[c] = d.ctx_dy[c];
+    p.dx[c] = d.ctx_dx[c];
+  }
+  p.poison_reads = poison;
+  const size_t smem = (size_t)rr * DEC_RING * sizeof(int16_t);
+  if (smem > 200 * 1024) return -2;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(arm_decode_kernel<C, NH, NHL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  DecStreams* ps = nullptr;
+  if (dec_streams(&ps)) return -1;
+  double* part = reinterpret_cast<double*>(ws);
+  cudaEventRecord(ps->ev[DEC_STREAMS], s);  // fork after the caller's queued work
+  const int ns = n_img < DEC_STREAMS ? n_img : DEC_STREAMS;
+  for (int k = 0; k < ns; k++) cudaStreamWaitEvent(ps->s[k], ps->ev[DEC_STREAMS], 0);
+  for (int i = 0; i < n_img; i++) {
+    pack_arm_weights<C, NH, NHL>(d, arm_w[i], p.w);
+    p.truth = truth[i];
+    p.decoded = decoded[i];
+    p.mu = mu ? mu[i] : nullptr;
+    p.scale = scale ? scale[i] : nullptr;
+    p.bits = bits ? bits[i] : nullptr;
+    p.partial = part + (size_t)i * d.L;
+    arm_decode_kernel<C, NH, NHL><<<d.L, DEC_THREADS, smem, ps->s[i % ns]>>>(p);
+  }
+  for (int k = 0; k < ns; k++) {  // join
+    cudaEventRecord(ps->ev[k], ps->s[k]);
+    cudaStreamWaitEvent(s, ps->ev[k], 0);
+  }
+  dec_rate_kernel<<<(n_img + 127) / 128, 128, 0, s>>>(part, d.L, n_img, rate);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
+typedef int (*DecLaunchFn)(const cc_model_desc&, const ArmGeom&, int, int, const int16_t* const*, const float* const*,
+                           int16_t* const*, float* const*, float* const*, float* const*, double*, int32_t*, void*,
+                           cudaStream_t);
+struct DecEntry {
+  int C, NH, NHL;
+  DecLaunchFn fn;
+};
+static const DecEntry kDec[] = {
+    {8, 8, 1, launch_dec<8, 8, 1>},     {8, 8, 2, launch_dec<8, 8, 2>},
+    {16, 16, 2, launch_dec<16, 16, 2>}, {16, 24, 2, launch_dec<16, 24, 2>},
+    {24, 24, 2, launch_dec<24, 24, 2>},
+};
+
+// Returns launches (n_img + 1) or a negative code (-3: ARM shape not compiled,
+// -2: ring exceeds shared memory).
+int arm_decode_impl(const cc_model_desc& d, const ArmGeom& g, int a_override, int n_img, const int16_t* const* truth,
+                    const float* const* arm_w, int16_t* const* decoded, float* const* mu, float* const* scale,
+                    float* const* bits, double* rate, int32_t* poison, void* ws, cudaStream_t s) {
+  const int NH = d.arm_widths[1], NHL = d.arm_n_layers - 1;
+  for (const auto& e : kDec)
+    if (e.C == d.n_ctx && e.NH == NH && e.NHL == NHL) {
+      const int rc = e.fn(d, g, a_override, n_img, truth, arm_w, decoded, mu, scale, bits, rate, poison, ws, s);
+      return rc < 0 ? rc : n_img + 1;
+    }
+  return -3;
+}
+
+}  // namespace ccrd

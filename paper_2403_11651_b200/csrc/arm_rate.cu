@@ -13,65 +13,10 @@
 //     feeds both latents;
 //   * stable Laplace -log2 P in fp32; bits -> warp shuffle -> one fp64 partial
 //     per warp (fixed order; final sum in ccrd_api.cu).
+#include "arm_math.cuh"
 #include "ccrd_common.cuh"
 
 namespace ccrd {
-
-// -log2 of the Laplace(mu, b) mass of the bin [y - 1/2, y + 1/2], floored at
-// p_floor (readings #1-#3).  With a = |y - mu| and
-// ib = 1/b:
-//   a <  1/2 : P = 1 - (exp(-(1/2 - a) ib) + exp(-(1/2 + a) ib)) / 2
-//   a >= 1/2 : -log2 P = 1 + (a - 1/2) ib log2(e) - log2(1 - exp(-ib))
-// (the second form is log-domain, so far tails do not underflow).
-// All exponentials / logarithms are single MUFU ops (ex2 / lg2): the worst
-// case, 1 - exp(-ib) at b = 256, cancels to ~1e-4 bits per latent, inside the
-// 1e-3-bit per-latent parity tolerance.
-__device__ __forceinline__ float laplace_bits(float y, float mu, float s, const ArmGeom& g) {
-  constexpr float LOG2E = 1.4426950408889634f;
-  s = fminf(fmaxf(s, g.lsmin), g.lsmax);
-  const float ibl = exp2f_approx(-s * LOG2E) * LOG2E;  // log2(e) / b
-  const float a = fabsf(y - mu);
-  const float am = fminf(a, 0.5f);
-  const float e1 = exp2f_approx((am - 0.5f) * ibl);
-  const float e2 = exp2f_approx(-(am + 0.5f) * ibl);
-  const float p_in = 1.0f - 0.5f * (e1 + e2);
-  const float bits_in = -log2f_approx(fmaxf(p_in, g.p_floor));
-  const float bits_out = fmaf(a - 0.5f, ibl, 1.0f) - log2f_approx(1.0f - exp2f_approx(-ibl));
-  return fminf(a < 0.5f ? bits_in : bits_out, g.bits_cap);
-}
-
-// One dense layer NIN -> 2*NO2 for NLAT latents with FFMA2 (two output neurons
-// per instruction; each uniform weight pair feeds NLAT instructions).
-template <int NLAT, int NIN, int NO2, bool RELU>
-__device__ __forceinline__ void dense_ffma2(const float (&in)[NLAT][NIN], float (&out)[NLAT][2 * NO2],
-                                            const float2 (&W)[NIN][NO2], const float2 (&B)[NO2]) {
-  uint64_t acc[NLAT][NO2];
-#pragma unroll
-  for (int n = 0; n < NO2; n++) {
-    const uint64_t b = ldp2(B[n]);
-#pragma unroll
-    for (int m = 0; m < NLAT; m++) acc[m][n] = b;
-  }
-  // latent-major inner order: one activation feeds NO2 consecutive FFMA2
-  // (operand-reuse cache), the NO2 weight pairs stay in uniform registers
-#pragma unroll
-  for (int i = 0; i < NIN; i++) {
-#pragma unroll
-    for (int m = 0; m < NLAT; m++) {
-      const uint64_t x = f2pack(in[m][i], in[m][i]);
-#pragma unroll
-      for (int n = 0; n < NO2; n++) acc[m][n] = ffma2(x, ldp2(W[i][n]), acc[m][n]);
-    }
-  }
-#pragma unroll
-  for (int m = 0; m < NLAT; m++)
-#pragma unroll
-    for (int n = 0; n < NO2; n++) {
-      float2 v = f2unpack(acc[m][n]);
-      out[m][2 * n] = RELU ? fmaxf(v.x, 0.0f) : v.x;
-      out[m][2 * n + 1] = RELU ? fmaxf(v.y, 0.0f) : v.y;
-    }
-}
 
 template <int C, int NH, int NHL>
 __global__ void __launch_bounds__(ARM_THREADS, ARM_CTAS_PER_SM)
@@ -184,35 +129,7 @@ static int launch_arm(const ArmGeom& g, const cc_model_desc& d, const float* arm
   p.mu = mu;
   p.scale = scale;
   p.bits = bits;
-  // pack weights (blob: per layer W[out][in] then b[out]); fold residuals
-  const float* q = arm_w;
-  auto res = [&](int k) { return (d.arm_residual_mask >> k) & 1u; };
-  for (int i = 0; i < C; i++)
-    for (int n = 0; n < NH / 2; n++) {
-      float a = q[(2 * n) * C + i], b = q[(2 * n + 1) * C + i];
-      if (res(0)) {  // only legal when C == NH (validated)
-        a += (i == 2 * n) ? 1.0f : 0.0f;
-        b += (i == 2 * n + 1) ? 1.0f : 0.0f;
-      }
-      p.w.w0[i][n] = make_float2(a, b);
-    }
-  for (int n = 0; n < NH / 2; n++) p.w.b0[n] = make_float2(q[C * NH + 2 * n], q[C * NH + 2 * n + 1]);
-  q += C * NH + NH;
-  for (int k = 0; k < NHL - 1; k++) {
-    for (int i = 0; i < NH; i++)
-      for (int n = 0; n < NH / 2; n++) {
-        float a = q[(2 * n) * NH + i], b = q[(2 * n + 1) * NH + i];
-        if (res(k + 1)) {
-          a += (i == 2 * n) ? 1.0f : 0.0f;
-          b += (i == 2 * n + 1) ? 1.0f : 0.0f;
-        }
-        p.w.wh[k][i][n] = make_float2(a, b);
-      }
-    for (int n = 0; n < NH / 2; n++) p.w.bh[k][n] = make_float2(q[NH * NH + 2 * n], q[NH * NH + 2 * n + 1]);
-    q += NH * NH + NH;
-  }
-  for (int i = 0; i < NH; i++) p.w.wo[i] = make_float2(q[i], q[NH + i]);
-  p.w.bo = make_float2(q[2 * NH], q[2 * NH + 1]);
+  pack_arm_weights<C, NH, NHL>(d, arm_w, p.w);
 
   arm_rate_kernel<C, NH, NHL><<<g.tile_begin[g.L], ARM_THREADS, 0, stream>>>(p);
   return 0;

@@ -3,6 +3,7 @@
 // host-buffer (end-to-end) path and the MAC closed form.
 #include <cstdarg>
 #include <cstdlib>
+#include <vector>
 #include <cstdio>
 #include <cstring>
 
@@ -967,6 +968,41 @@ int cc_analysis_forward(const cc_analysis_desc* a, const float* image, const flo
   if (n < 0) return fail(CC_ECUDA, "cuBLASLt matmul failed (%d)", n);
   g_launches = n;
   return cuda_check("cc_analysis_forward");
+}
+
+// ---------------------------------------------------------------- ARM decode (NEXT-3)
+size_t cc_arm_decode_workspace_bytes(const cc_model_desc* desc, int32_t n_img) {
+  if (validate_device(desc) != CC_OK || n_img < 1) return 0;
+  return dec_workspace_bytes(*desc, n_img);
+}
+
+int cc_arm_decode(const cc_model_desc* desc, const cc_image_io* io, int32_t n_img, int16_t* const* decoded,
+                  double* rate, float* const* mu, float* const* scale, float* const* bits, int32_t* poison_reads,
+                  void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  int rc = validate_device(desc);
+  if (rc) return rc;
+  if (!io || n_img < 1 || !decoded || !rate) return fail(CC_EINVAL, "io / decoded / rate null or n_img < 1");
+  const size_t need = dec_workspace_bytes(*desc, n_img);
+  if (!workspace || workspace_bytes < need) return fail(CC_EWORKSPACE, "need %zu workspace bytes", need);
+  std::vector<const int16_t*> truth(n_img);
+  std::vector<const float*> aw(n_img);
+  for (int i = 0; i < n_img; i++) {
+    if (!io[i].latents || !io[i].arm_w || !decoded[i]) return fail(CC_EINVAL, "image %d: null latents / arm_w / decoded", i);
+    truth[i] = io[i].latents;
+    aw[i] = io[i].arm_w;
+  }
+  if (!have_device()) return fail(CC_ECUDA, "no CUDA device");
+  ArmGeom g;
+  arm_geom(*desc, nullptr, g);
+  const char* sk = getenv("CCRD_DEC_SKEW");
+  const int n = arm_decode_impl(*desc, g, sk ? atoi(sk) : 0, n_img, truth.data(), aw.data(), decoded, mu, scale, bits,
+                                rate, poison_reads, workspace, (cudaStream_t)stream);
+  if (n == -3) return fail(CC_ENOTSUP, "ARM shape not compiled for the decoder");
+  if (n == -2) return fail(CC_ENOTSUP, "decoder ring exceeds shared memory (grid too wide)");
+  if (n < 0) return cuda_check("cc_arm_decode launch");
+  g_launches = n;
+  return cuda_check("cc_arm_decode");
 }
 
 // ---------------------------------------------------------------- decode

@@ -254,6 +254,12 @@ int device_sm_count();  // current device's SMs (lazily cached; 148 without a de
 // N-O analysis transform (analysis.cu, NEXT-4)
 int64_t analysis_param_count(const cc_analysis_desc& a);
 size_t analysis_workspace_bytes(const cc_analysis_desc& a);
+// NEXT-3 wavefront ARM decode (arm_decode.cu)
+int dec_skew(const cc_model_desc& d);
+size_t dec_workspace_bytes(const cc_model_desc& d, int n_img);
+int arm_decode_impl(const cc_model_desc& d, const ArmGeom& g, int a_override, int n_img, const int16_t* const* truth,
+                    const float* const* arm_w, int16_t* const* decoded, float* const* mu, float* const* scale,
+                    float* const* bits, double* rate, int32_t* poison, void* ws, cudaStream_t s);
 int analysis_block_tc(int mode, bool down, const float* in, float* out, const float* blk, const float* wm, float* lat,
                       int h, int w, int ho, int wo, int n_img, int64_t lat_img, int sm_count, cudaStream_t s);
 int analysis_forward_impl(const cc_analysis_desc& a, const float* image, const float* w, float* lat, void* ws,

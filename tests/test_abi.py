@@ -239,3 +239,22 @@ def test_u8_image_helpers():
     assert q.dtype == np.float32
     np.testing.assert_array_equal(workload.to_u8(q), v)          # round trip exact
     np.testing.assert_array_equal(q, v.astype(np.float32) / np.float32(255))
+
+
+def test_arm_decode_entry_errors_without_gpu():
+    cfg = workload.CONFIGS["ref"].replace(H=24, W=40)
+    d = P.desc_from_config(cfg)
+    wsb = P.cc_arm_decode_workspace_bytes(d, 3)
+    assert wsb >= 3 * cfg.L * 8
+    d8 = P.desc_from_config(cfg)
+    d8.latents_i8 = 1                      # host-path transfer format: refused by device entries
+    assert P.cc_arm_decode_workspace_bytes(d8, 3) == 0
+    im = workload.make_image(cfg, 1)
+    io = [P.CcImageIO(8, im.arm_w.ctypes.data, 0, 0, 0, 0)]
+    with pytest.raises(ccrd.CcError) as e:          # workspace too small
+        P.cc_arm_decode(d, io, [8], 8, ws_ptr=8, ws_bytes=1)
+    assert e.value.code == ccrd.CC_EWORKSPACE
+    if not _has_gpu():
+        with pytest.raises(ccrd.CcError) as e:      # no device: loud failure
+            P.cc_arm_decode(d, io, [8], 8, ws_ptr=8, ws_bytes=wsb)
+        assert e.value.code == ccrd.CC_ECUDA
