@@ -20,22 +20,26 @@ namespace ccrd {
 
 constexpr int AN_TB = 256;
 
-// one pixel per threadIdx.y, 4 channels per threadIdx.x (blockDim.x = C / 4)
+// grid-stride over pixels: threadIdx.x = 4 channels (blockDim.x = C / 4),
+// threadIdx.y = pixel within the block's group; a thread's 4 weights rows stay
+// in registers across its pixels (the stem writes C floats per pixel: HBM-bound)
 __global__ void an_stem_kernel(const float* __restrict__ img, const float* __restrict__ w, float* __restrict__ x,
                                int64_t P, int C) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
-  if (p >= P) return;
   const int c = 4 * threadIdx.x;
-  const float i0 = __ldg(img + p), i1 = __ldg(img + P + p), i2 = __ldg(img + 2 * P + p);
-  float o[4];
+  float wr[4][3], bb[4];
 #pragma unroll
   for (int e = 0; e < 4; e++) {
-    float a = __ldg(w + C * 3 + c + e);
-    a = fmaf(__ldg(w + (c + e) * 3), i0, a);
-    a = fmaf(__ldg(w + (c + e) * 3 + 1), i1, a);
-    o[e] = fmaf(__ldg(w + (c + e) * 3 + 2), i2, a);
+    bb[e] = __ldg(w + C * 3 + c + e);
+#pragma unroll
+    for (int i = 0; i < 3; i++) wr[e][i] = __ldg(w + (c + e) * 3 + i);
   }
-  *reinterpret_cast<float4*>(x + p * C + c) = make_float4(o[0], o[1], o[2], o[3]);
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; p < P; p += (int64_t)gridDim.x * blockDim.y) {
+    const float i0 = __ldg(img + p), i1 = __ldg(img + P + p), i2 = __ldg(img + 2 * P + p);
+    float o[4];
+#pragma unroll
+    for (int e = 0; e < 4; e++) o[e] = fmaf(wr[e][2], i2, fmaf(wr[e][1], i1, fmaf(wr[e][0], i0, bb[e])));
+    *reinterpret_cast<float4*>(x + p * C + c) = make_float4(o[0], o[1], o[2], o[3]);
+  }
 }
 
 // depth-wise 7x7, stride s, zero padding 3; NHWC, one output (pixel, channel)
@@ -194,7 +198,9 @@ static int blocks_of(int64_t n) { return (int)((n + AN_TB - 1) / AN_TB); }
 
 static void launch_stem(const float* image, const float* w, float* x, int64_t P, int C, cudaStream_t s) {
   const dim3 tb(C / 4, AN_TB / (C / 4));  // C % 4 == 0 (validated), C / 4 <= AN_TB
-  an_stem_kernel<<<(unsigned)((P + tb.y - 1) / tb.y), tb, 0, s>>>(image, w, x, P, C);
+  const int64_t need = (P + tb.y - 1) / tb.y;
+  const int64_t cap = (int64_t)device_sm_count() * 8;
+  an_stem_kernel<<<(unsigned)(need < cap ? need : cap), tb, 0, s>>>(image, w, x, P, C);
 }
 
 // One image through the unfused path (dw kernels + cuBLASLt GEMMs); x holds
