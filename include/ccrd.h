@@ -266,8 +266,9 @@ int cc_decode(const cc_model_desc* desc, const int16_t* latents, const float* up
  * residual and merge; analysis_tc.cu), else cuBLASLt TF32; 2 = TF32 cuBLASLt
  * GEMMs unfused (the library baseline); 3 = as 1 with FP16 tensor-core
  * operands (the same 10-bit mantissa as TF32, 5-bit exponent: |values| <
- * 65504) and a TMA-staged depth-wise stage in the stride-1 blocks
- * (downsampling blocks stay TF32) -- the fast path.  Operands of the TF32 /
+ * 65504): stride-1 blocks with a TMA-staged depth-wise stage,
+ * downsampling blocks warp-specialised with the stride-2 depth-wise + pool
+ * read from global memory -- the fast path.  Operands of the TF32 /
  * FP16 products are rounded to 10-bit mantissas, accumulation is fp32. */
 typedef struct {
   int32_t H, W, L, C, blocks, tf32;

@@ -937,6 +937,257 @@ __global__ void __launch_bounds__(BT_THREADS, 1) an_block_h16_kernel(const __gri
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// ---------------------------------------------------------------- FP16 warp-specialised downsampling block
+// The downsampling block (A3) in the mode-3 design: FP16 operands, warps 0-7
+// compute the stride-2 depth-wise 7x7 AND the 2x2 mean pool straight from
+// global memory (a stride-2 stage would need 115 KB) into double-buffered A /
+// AP tiles; warps 8-15 run MMA1 (A x W1^T), the ReLU epilogue into TMEM, MMA2
+// (hidden x W2^T, TS) + (pool x Wid^T, SS) and the output epilogue.  A slot is
+// released after MMA2 (which still reads the pool tile).
+struct H16dSmem {
+  static constexpr uint32_t W1 = 0;                          // [256 x 64] f16
+  static constexpr uint32_t W2 = W1 + BT_HID * BT_C * 2;     // [64 x 256] f16
+  static constexpr uint32_t WID = W2 + BT_C * BT_HID * 2;    // [64 x 64] f16
+  static constexpr uint32_t A = WID + BT_C * BT_C * 2;       // 2 x [128 x 64] f16 (dw)
+  static constexpr uint32_t AP = A + 2 * 128 * BT_C * 2;     // 2 x [128 x 64] f16 (pool)
+  static constexpr uint32_t B1 = AP + 2 * 128 * BT_C * 2;
+  static constexpr uint32_t B2 = B1 + BT_HID * 4;
+  static constexpr uint32_t WM = B2 + BT_C * 4;
+  static constexpr uint32_t MP = WM + BT_C * 4;
+  static constexpr uint32_t WK = MP + 2 * 128 * 4;
+  static constexpr uint32_t BAR = WK + 49 * 32 * 8;  // a_full[2], a_empty[2], d1_full, d2_full
+  static constexpr uint32_t SLOT = BAR + 6 * 8;
+  static constexpr uint32_t TOTAL = SLOT + 16 + 1024;
+};
+
+__global__ void __launch_bounds__(BT_THREADS, 1) an_block_h16d_kernel(const __grid_constant__ BlockTcParams p) {
+  using S = H16dSmem;
+  extern __shared__ uint8_t bt_raw[];
+  uint8_t* sm = bt_raw + ((1024u - (smem_u32(bt_raw) & 1023u)) & 1023u);
+  const uint32_t su = smem_u32(sm);
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  float* b1s = reinterpret_cast<float*>(sm + S::B1);
+  float* b2s = reinterpret_cast<float*>(sm + S::B2);
+  float* wms = reinterpret_cast<float*>(sm + S::WM);
+  float* mp = reinterpret_cast<float*>(sm + S::MP);
+  float2* wks = reinterpret_cast<float2*>(sm + S::WK);
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(sm + S::BAR);
+  uint64_t* a_empty = a_full + 2;
+  uint64_t* d1_full = a_full + 4;
+  uint64_t* d2_full = a_full + 5;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(sm + S::SLOT);
+
+  const float* dk = p.blk;
+  const float* dkb = dk + BT_C * 49;
+  const float* W1 = dkb + BT_C;
+  const float* b1 = W1 + BT_HID * BT_C;
+  const float* W2 = b1 + BT_HID;
+  const float* b2 = W2 + BT_C * BT_HID;
+  const float* Wid = b2 + BT_C;
+  const float* bid = Wid + BT_C * BT_C;
+  {
+    constexpr int N1 = BT_HID * BT_C / 4 / BT_THREADS;
+#pragma unroll
+    for (int u = 0; u < N1; u++) {
+      const int i = 4 * (t + u * BT_THREADS);
+      const float* pa = W1 + i;
+      const float* pb = W2 + i;
+      const float a0 = __ldg(pa), a1 = __ldg(pa + 1), a2 = __ldg(pa + 2), a3 = __ldg(pa + 3);
+      const float c0 = __ldg(pb), c1 = __ldg(pb + 1), c2 = __ldg(pb + 2), c3 = __ldg(pb + 3);
+      *reinterpret_cast<uint2*>(sm + S::W1 + sw128h(i >> 6, i & 63, BT_HID)) = make_uint2(pack_h2(a0, a1), pack_h2(a2, a3));
+      *reinterpret_cast<uint2*>(sm + S::W2 + sw128h(i >> 8, i & 255, BT_C)) = make_uint2(pack_h2(c0, c1), pack_h2(c2, c3));
+    }
+#pragma unroll
+    for (int u = 0; u < BT_C * BT_C / 4 / BT_THREADS; u++) {
+      const int i = 4 * (t + u * BT_THREADS);
+      const float* pc = Wid + i;
+      *reinterpret_cast<uint2*>(sm + S::WID + sw128h(i >> 6, i & 63, BT_C)) =
+          make_uint2(pack_h2(__ldg(pc), __ldg(pc + 1)), pack_h2(__ldg(pc + 2), __ldg(pc + 3)));
+    }
+  }
+  for (int i = t; i < 49 * 32; i += BT_THREADS) {
+    const int tap = i >> 5, c2 = i & 31;
+    wks[i] = make_float2(__ldg(dk + (2 * c2) * 49 + tap), __ldg(dk + (2 * c2 + 1) * 49 + tap));
+  }
+  if (t < BT_HID) b1s[t] = __ldg(b1 + t);
+  if (t < BT_C) {
+    b2s[t] = __ldg(b2 + t) + __ldg(bid + t);
+    wms[t] = p.wm ? __ldg(p.wm + t) : 0.0f;
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (t == 0) {
+    for (int k = 0; k < 2; k++) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(smem_u32(a_full + k)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(a_empty + k)));
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(d1_full)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(d2_full)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *slot;                   // D1: columns 0..255
+  const uint32_t tmem_h = tmem + BT_HID;         // hidden, f16x2: 256..383
+  const uint32_t tmem_d2 = tmem + BT_HID + 128;  // D2: 384..447
+  const uint32_t tlane = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+
+  if (warp < 8) {
+    // ================= depth-wise (stride 2) + 2x2 pool producers
+    const int cp = lane, ry = warp & 3, xh = warp >> 2;
+    const uint64_t kb2 = f2pack(__ldg(dkb + 2 * cp), __ldg(dkb + 2 * cp + 1));
+    int i = 0;
+#pragma unroll 1
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, i++) {
+      const int b = i & 1;
+      if (i >= 2) mbar_wait(a_empty + b, ((i >> 1) - 1) & 1);
+      const int img = tile / p.tpi, tr = tile - img * p.tpi;
+      const int ty = tr / p.tiles_x, tx = tr - ty * p.tiles_x;
+      const float* pin = p.in + img * p.in_img;
+      const int oy = ty * BT_TY + ry;
+      uint8_t* A = sm + S::A + b * (128 * BT_C * 2);
+      uint8_t* AP = sm + S::AP + b * (128 * BT_C * 2);
+#pragma unroll 1
+      for (int half = 0; half < 2; half++) {  // 2 x 8 output pixels (register budget)
+        const int ox0 = tx * BT_TX + xh * 16 + half * 8;
+        uint64_t acc[8], ps[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          acc[j] = kb2;
+          ps[j] = 0ull;
+        }
+        const int gx0 = 2 * ox0 - 3;
+        constexpr int NX = 21;  // input columns under 8 stride-2 outputs
+        const bool interior = gx0 >= 0 && gx0 + NX <= p.w;
+#pragma unroll
+        for (int ky = 0; ky < 7; ky++) {
+          const int iy = 2 * oy + ky - 3;
+          if (iy < 0 || iy >= p.h) continue;
+          const float* row = pin + ((int64_t)iy * p.w + gx0) * BT_C + 2 * cp;
+          uint64_t v[NX];
+          if (interior) {
+#pragma unroll
+            for (int ix = 0; ix < NX; ix++) v[ix] = ldg_f2(row + ix * BT_C);
+          } else {
+#pragma unroll
+            for (int ix = 0; ix < NX; ix++) {
+              v[ix] = 0ull;
+              if (gx0 + ix >= 0 && gx0 + ix < p.w) v[ix] = ldg_f2(row + ix * BT_C);
+            }
+          }
+          if (ky == 3 || ky == 4) {
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+              ps[j] = ffma2(v[2 * j + 3], f2pack(1.0f, 1.0f), ps[j]);
+              ps[j] = ffma2(v[2 * j + 4], f2pack(1.0f, 1.0f), ps[j]);
+            }
+          }
+#pragma unroll
+          for (int kx = 0; kx < 7; kx++) {
+            const uint64_t wv = ldp2(wks[(ky * 7 + kx) * 32 + cp]);
+#pragma unroll
+            for (int j = 0; j < 8; j++) acc[j] = ffma2(v[2 * j + kx], wv, acc[j]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          const int r = ry * 32 + xh * 16 + half * 8 + j;
+          const float2 a = f2unpack(acc[j]);
+          *reinterpret_cast<uint32_t*>(A + sw128h(r, 2 * cp, 128)) = pack_h2(a.x, a.y);
+          const int ox = ox0 + j;
+          const float inv = 1.0f / (float)(((2 * oy + 1 < p.h) ? 2 : 1) * ((2 * ox + 1 < p.w) ? 2 : 1));
+          const float2 q = f2unpack(ps[j]);
+          *reinterpret_cast<uint32_t*>(AP + sw128h(r, 2 * cp, 128)) = pack_h2(q.x * inv, q.y * inv);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_full + b);
+    }
+  } else {
+    // ================= MMA issue + epilogues
+    const int e = warp - 8, hh = e >> 2, q = e & 3;
+    const bool leader = (e == 0 && lane == 0);
+    const float bm = p.wm ? __ldg(p.wm + BT_C) : 0.0f;
+    int i = 0, prev = -1;
+#pragma unroll 1
+    for (int tile = blockIdx.x;; tile += gridDim.x, i++) {
+      const bool has = tile < p.n_tiles;
+      if (leader && has) {
+        mbar_wait(a_full + (i & 1), (i >> 1) & 1);
+        if (i >= 1) mbar_wait(d2_full, (i - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t a_u = su + S::A + (i & 1) * (128 * BT_C * 2);
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          mma_f16(tmem, umma_desc_sw128(a_u + k * 32), umma_desc_sw128(su + S::W1 + k * 32), h16_idesc(BT_HID), k > 0);
+        mma_commit(d1_full);
+      }
+      __syncwarp();
+      if (prev >= 0) {
+        mbar_wait(d2_full, (i - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const int pimg = prev / p.tpi, ptr = prev - pimg * p.tpi;
+        const int pty = ptr / p.tiles_x, ptx = ptr - pty * p.tiles_x;
+        float* pout = p.out + pimg * p.out_img;
+        float* plat = p.lat ? p.lat + pimg * p.lat_img : nullptr;
+        float partv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        epi2_rows<4, false>(tlane + BT_HID + 128 + hh * 32, hh * 32, nullptr, pout, pty * BT_TY + q, p.ho, ptx * BT_TX,
+                            p.wo, b2s, wms, partv, lane);
+        if (plat) {
+          epi2_partials(partv, mp, hh, q, lane);
+          epi_sync();
+          const int te = e * 32 + lane;
+          if (te < 128) {
+            const int oy3 = pty * BT_TY + (te >> 5), ox3 = ptx * BT_TX + (te & 31);
+            if (oy3 < p.ho && ox3 < p.wo) plat[(int64_t)oy3 * p.wo + ox3] = (mp[te] + mp[128 + te]) + bm;
+          }
+        }
+      }
+      if (!has) break;
+      mbar_wait(d1_full, i & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+      for (int cc = 0; cc < 4; cc++) {
+        const int col = hh * 128 + cc * 32;
+        float v[32];
+        tmem_row<32>(tlane + col, v);
+        uint32_t hv[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+          hv[j] = pack_h2(fmaxf(v[2 * j] + b1s[col + 2 * j], 0.0f), fmaxf(v[2 * j + 1] + b1s[col + 2 * j + 1], 0.0f));
+        tmem_st16(tlane + BT_HID + (col >> 1), hv);
+      }
+      tmem_wait_st();
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      epi_sync();
+      if (leader) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+        for (int k = 0; k < 16; k++)
+          mma_f16_ts(tmem_d2, tmem_h + 8 * k, umma_desc_sw128(su + S::W2 + (k >> 2) * (BT_C * 128) + (k & 3) * 32),
+                     h16_idesc(BT_C), k > 0);
+        const uint32_t ap_u = su + S::AP + (i & 1) * (128 * BT_C * 2);
+#pragma unroll
+        for (int k = 0; k < 4; k++)  // identity branch: pool x Wid^T (K = 64)
+          mma_f16(tmem_d2, umma_desc_sw128(ap_u + k * 32), umma_desc_sw128(su + S::WID + k * 32), h16_idesc(BT_C), 1);
+        mma_commit(d2_full);
+        mma_commit(a_empty + (i & 1));  // A and AP of this tile are consumed
+      }
+      __syncwarp();
+      prev = tile;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1011,6 +1262,18 @@ int analysis_block_tc(int mode, bool down, const float* in, float* out, const fl
   p.in_img = (int64_t)h * w * BT_C;
   p.out_img = (int64_t)ho * wo * BT_C;
   p.lat_img = lat_img;
+  if (down && mode == 3) {
+    static bool attr_d = false;
+    if (!attr_d) {
+      if (cudaFuncSetAttribute(an_block_h16d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H16dSmem::TOTAL) !=
+          cudaSuccess)
+        return -1;
+      attr_d = true;
+    }
+    const int grid = p.n_tiles < sm_count ? p.n_tiles : sm_count;
+    an_block_h16d_kernel<<<grid, BT_THREADS, H16dSmem::TOTAL, s>>>(p);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+  }
   if (down) return launch_block_tc<true>(p, sm_count, s);
   if (mode == 3) return launch_block_h16(p, n_img, sm_count, s);
   static const bool seq = getenv("CCRD_AN_SEQ") && getenv("CCRD_AN_SEQ")[0] == '1';  // A/B: sequential kernel
