@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(TS_THREADS)
 // Two-stage fp64 reduction of partial rows part[b * stride + e], b < blocks,
 // e < n: stage 1 sums row chunks (blockIdx.y) with one thread per entry
 // (coalesced across the warp), stage 2 sums the chunks into grad[e].
-constexpr int TR_RCHUNK = 64;
+constexpr int TR_RCHUNK = 128;
 __global__ void tr_reduce1_kernel(const float* __restrict__ part, int64_t blocks, int64_t stride, int n,
                                   double* __restrict__ tmp) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -760,12 +760,39 @@ __global__ void tr_reduce1_kernel(const float* __restrict__ part, int64_t blocks
   for (int64_t b = b0; b < b1; b++) s += (double)part[b * stride + e];
   tmp[(int64_t)blockIdx.y * n + e] = s;
 }
+// Narrow partial rows (n <= 128): the block's threads are (row slot, element)
+// pairs striding over the chunk's rows (n_pad = next power of two >= n), then a
+// fixed-order tree over the row slots -- all threads busy instead of n of them
+// walking every row serially (deterministic: fixed assignment and order).
+__global__ void __launch_bounds__(256) tr_reduce1_narrow_kernel(const float* __restrict__ part, int64_t blocks,
+                                                                int64_t stride, int n, int n_pad,
+                                                                double* __restrict__ tmp) {
+  __shared__ double red[256];
+  const int e = threadIdx.x & (n_pad - 1), slot = threadIdx.x / n_pad, slots = 256 / n_pad;
+  const int64_t per = (blocks + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = blockIdx.x * per, b1 = b0 + per < blocks ? b0 + per : blocks;
+  double s = 0.0;
+  if (e < n) {
+#pragma unroll 4
+    for (int64_t b = b0 + slot; b < b1; b += slots) s += (double)part[b * stride + e];
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int half = slots / 2; half > 0; half >>= 1) {
+    if (slot < half) red[threadIdx.x] += red[threadIdx.x + half * n_pad];
+    __syncthreads();
+  }
+  if (slot == 0 && e < n) tmp[(int64_t)blockIdx.x * n + e] = red[threadIdx.x];
+}
+// one warp per element: lanes stride over the chunks, fixed-order shuffle tree
 __global__ void tr_reduce2_kernel(const double* __restrict__ tmp, int chunks, int n, float* __restrict__ grad) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (e >= n) return;
   double s = 0.0;
-  for (int c = 0; c < chunks; c++) s += tmp[(int64_t)c * n + e];
-  grad[e] = (float)s;
+  for (int c = lane; c < chunks; c += 32) s += tmp[(int64_t)c * n + e];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) grad[e] = (float)s;
 }
 
 __global__ void tr_result_kernel(const double* __restrict__ rate_part, int64_t n_rate, const double* __restrict__ sse_part,
@@ -968,8 +995,14 @@ int train_supported(const cc_model_desc& d) {
 static int reduce_partials(const float* part, int64_t blocks, int64_t stride, int n, float* grad, double* tmp,
                            cudaStream_t s) {
   const int chunks = (int)(blocks < TR_RCHUNK ? (blocks > 0 ? blocks : 1) : TR_RCHUNK);
-  tr_reduce1_kernel<<<dim3((n + TB - 1) / TB, chunks), TB, 0, s>>>(part, blocks, stride, n, tmp);
-  tr_reduce2_kernel<<<(n + TB - 1) / TB, TB, 0, s>>>(tmp, chunks, n, grad);
+  if (n <= 128) {
+    int n_pad = 1;
+    while (n_pad < n) n_pad <<= 1;
+    tr_reduce1_narrow_kernel<<<chunks, 256, 0, s>>>(part, blocks, stride, n, n_pad, tmp);
+  } else {
+    tr_reduce1_kernel<<<dim3((n + TB - 1) / TB, chunks), TB, 0, s>>>(part, blocks, stride, n, tmp);
+  }
+  tr_reduce2_kernel<<<(n + 7) / 8, 256, 0, s>>>(tmp, chunks, n, grad);
   return 2;
 }
 
