@@ -677,9 +677,14 @@ __global__ void __launch_bounds__(TS_THREADS)
     float gd[L];
 #pragma unroll
     for (int i = 0; i < L; i++) gd[i] = 0.0f;
-#pragma unroll 4
+    // all CH pre-activations in flight at once (a 4-deep unroll left ~10
+    // serial memory latencies per pixel)
+    float ua[CH];
+#pragma unroll
+    for (int n = 0; n < CH; n++) ua[n] = u1[(int64_t)n * d.P + p];
+#pragma unroll
     for (int n = 0; n < CH; n++) {
-      const float a = u1[(int64_t)n * d.P + p];
+      const float a = ua[n];
       vec[LY::V1 + n] = fmaxf(a, 0.0f);
       float g = 0.0f;
 #pragma unroll
