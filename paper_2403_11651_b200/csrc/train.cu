@@ -410,9 +410,13 @@ __global__ void tr_tconv_fwd_kernel(const float* __restrict__ g, float* __restri
 // Adjoint: gg[s] = sum over extended positions i with clamp(i - E) = s of
 // sum_j k[j] gout[2i + j - P]; tap gradient dk[j] = sum x_ext[i] gout[2i + j - P]
 // (per-block partials [blocks][K]).
+// KT > 0: the tap count as a compile-time constant (unrolled loops, the tap
+// gradients in registers; with a runtime K they lived in local memory)
+template <int KT>
 __global__ void tr_tconv_bwd_kernel(const float* __restrict__ g, const float* __restrict__ gout, float* __restrict__ gg,
                                     int lines, int n, int m, int64_t g_ls, int64_t g_es, int64_t o_ls, int64_t o_es,
-                                    int K, int koff, float* __restrict__ kpart, int64_t g_cs, int64_t o_cs) {
+                                    int K_, int koff, float* __restrict__ kpart, int64_t g_cs, int64_t o_cs) {
+  const int K = KT > 0 ? KT : K_;
   __shared__ float red[8][TB / 32];
   g += blockIdx.y * g_cs;  // channel (gg shares g's layout)
   gg += blockIdx.y * g_cs;
@@ -434,7 +438,9 @@ __global__ void tr_tconv_bwd_kernel(const float* __restrict__ g, const float* __
     const int i_lo = (s == 0) ? 0 : s + E, i_hi = (s == n - 1) ? n - 1 + 2 * E : s + E;  // extended positions
     float acc = 0.0f;
     for (int i = i_lo; i <= i_hi; i++)
-      for (int j = 0; j < K; j++) {
+#pragma unroll
+      for (int j = 0; j < (KT > 0 ? KT : 8); j++) {
+        if (KT == 0 && j >= K) break;
         const int o = 2 * i + j - P;
         if (o >= 0 && o < m) {
           const float go = gout[line * o_ls + (int64_t)o * o_es];
@@ -445,7 +451,9 @@ __global__ void tr_tconv_bwd_kernel(const float* __restrict__ g, const float* __
     gg[line * g_ls + (int64_t)s * g_es] = acc;
   }
   // block partial of the tap gradient
-  for (int j = 0; j < K; j++) {
+#pragma unroll
+  for (int j = 0; j < (KT > 0 ? KT : 8); j++) {
+    if (KT == 0 && j >= K) break;
     float v = dk[j];
 #pragma unroll
     for (int o2 = 16; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o2);
@@ -1013,6 +1021,8 @@ static int reduce_partials(const float* part, int64_t blocks, int64_t stride, in
 
 static int blocks_for(int64_t n) { return (int)((n + TB - 1) / TB); }
 
+#define TCONV_BWD(K) ((K) == 8 ? tr_tconv_bwd_kernel<8> : (K) == 4 ? tr_tconv_bwd_kernel<4> : tr_tconv_bwd_kernel<0>)
+
 // The iteration.  Returns the number of kernel launches (>= 0) or -1 if a
 // CUDA call failed (the caller checks cudaGetLastError).
 int train_step_impl(const cc_model_desc& d, float* par, const float* noise, const float* image, float* am, float* av,
@@ -1173,13 +1183,13 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
     float* gnext = (gT == F(pl.o_g0)) ? F(pl.o_g1) + (int64_t)nch * hs * wd : F(pl.o_g0);  // not aliasing gT / gmid
     // y adjoint: inputs mid (per channel: lines = columns wd, n = hs), outputs gT_j[1..] (m = hd)
     const int64_t b1 = blocks_for((int64_t)wd * hs) < TR_TCONV_CAP ? blocks_for((int64_t)wd * hs) : TR_TCONV_CAP;
-    tr_tconv_bwd_kernel<<<dim3((unsigned)b1, nch), TB, 0, s>>>(mid, gT + (int64_t)hd * wd, gmid, wd, hs, hd, 1, wd, 1,
+    TCONV_BWD(K)<<<dim3((unsigned)b1, nch), TB, 0, s>>>(mid, gT + (int64_t)hd * wd, gmid, wd, hs, hd, 1, wd, 1,
                                                                wd, K, koff, kpart + krow * K, (int64_t)hs * wd,
                                                                (int64_t)hd * wd);
     krow += b1 * nch;
     // x adjoint: inputs T_{j+1} (lines = rows hs, n = ws2), outputs gmid (m = wd)
     const int64_t b2 = blocks_for((int64_t)hs * ws2) < TR_TCONV_CAP ? blocks_for((int64_t)hs * ws2) : TR_TCONV_CAP;
-    tr_tconv_bwd_kernel<<<dim3((unsigned)b2, nch), TB, 0, s>>>(Tj(j + 1), gmid, gnext, hs, ws2, wd, ws2, 1, wd, 1, K,
+    TCONV_BWD(K)<<<dim3((unsigned)b2, nch), TB, 0, s>>>(Tj(j + 1), gmid, gnext, hs, ws2, wd, ws2, 1, wd, 1, K,
                                                                koff, kpart + krow * K, (int64_t)hs * ws2,
                                                                (int64_t)hs * wd);
     krow += b2 * nch;
