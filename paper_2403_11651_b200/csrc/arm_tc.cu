@@ -38,6 +38,8 @@
 // parity-tested, not the default.
 #include <cstring>
 
+#include <cstdlib>
+
 #include "ccrd_common.cuh"
 #include "tcgen05.cuh"
 
@@ -290,6 +292,274 @@ __global__ void __launch_bounds__(TC_THREADS, TC_CTAS_PER_SM)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
 }
 
+// ---------------------------------------------------------------- warp-specialised pipeline
+// The same arithmetic as arm_tc_kernel (exact context x [B_hi + B_lo], 3xTF32
+// hidden layer, FFMA2 output layer, the same Laplace bits), pipelined over
+// blocks of 128 latents with dedicated warps, two blocks in flight:
+//   warps 0-3 (front): stage the tile's causal window, gather the contexts of
+//             block b into A0[b % 2]; epilogue 0 of block b-1: TMEM D0 ->
+//             ReLU -> hi / lo split into A1[(b-1) % 2];
+//   warp 8:   allocates TMEM, issues MMA0(b) and MMA1(b-1) as their operands
+//             arrive (mbarriers), commits to the waiting warps;
+//   warps 4-7 (back): epilogue 1 of block b: TMEM D1 -> ReLU -> output layer
+//             -> Laplace bits (y re-read from the int16 latents) -> partials.
+// The serial version pays two MMA round trips per block on the same warps;
+// here the front, back and tensor work of neighbouring blocks overlap.
+constexpr int TW_THREADS = 288;  // 9 warps
+#ifndef CCRD_TW_A1_SLOTS
+#define CCRD_TW_A1_SLOTS 1
+#endif
+constexpr int TW_A1_SLOTS = CCRD_TW_A1_SLOTS;
+
+template <int C, int NH, int NHL>
+struct ArmTcwShape {
+  using S = ArmTcShape<C, NH, NHL>;
+  static constexpr int K0 = S::K0, K1 = S::K1, NP = S::NP;
+  static constexpr int A0F = TC_M * K0;        // floats per A0 slot
+  static constexpr int A1F = 2 * TC_M * K1;    // hi + lo per A1 slot
+  static constexpr int OFF_B = 0;
+  static constexpr int OFF_WIN = S::B_FLOATS;
+  static constexpr int OFF_A0 = OFF_WIN + ((ARM_SH * ARM_SW + 31) / 32) * 32;
+  static constexpr int A1S = TW_A1_SLOTS;  // A1 slots (1: smaller CTA, more CTAs per SM)
+  static constexpr int OFF_A1 = OFF_A0 + 2 * A0F;
+  static constexpr int FLOATS = OFF_A1 + A1S * A1F;
+  static constexpr size_t SMEM = sizeof(float) * (size_t)FLOATS + 16 * 8 + 64;
+  static_assert(S::NHID == 1, "one hidden NH -> NH layer");
+};
+
+__device__ __forceinline__ void tw_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void front_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+template <int C, int NH, int NHL>
+__global__ void __launch_bounds__(TW_THREADS, 1) arm_tcw_kernel(const __grid_constant__ ArmTcParams<C, NH, NHL> p) {
+  using S = ArmTcShape<C, NH, NHL>;
+  using W = ArmTcwShape<C, NH, NHL>;
+  constexpr int K0 = S::K0, NP = S::NP, K1 = S::K1;
+  extern __shared__ __align__(1024) float tsm[];
+  float* sB = tsm + W::OFF_B;
+  float* win = tsm + W::OFF_WIN;
+  float* sA0 = tsm + W::OFF_A0;
+  float* sA1 = tsm + W::OFF_A1;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tsm + W::FLOATS);
+  uint64_t* a0_full = bars;       // [2] front -> MMA
+  uint64_t* d0_full = bars + 2;   // [2] MMA0 commit
+  uint64_t* a1_full = bars + 4;   // [2] front epilogue 0 -> MMA
+  uint64_t* d1_full = bars + 6;   // [2] MMA1 commit
+  uint64_t* d1_empty = bars + 8;  // [2] back done with D1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  {
+    const float4* src0 = reinterpret_cast<const float4*>(&p.B0[0][0]);
+    float4* dst = reinterpret_cast<float4*>(sB);
+    for (int i = t; i < 2 * S::BW0 / 4; i += TW_THREADS) dst[i] = src0[i];
+    const float4* src1 = reinterpret_cast<const float4*>(&p.B1[0][0][0]);
+    for (int i = t; i < 2 * S::BW1 / 4; i += TW_THREADS) dst[2 * S::BW0 / 4 + i] = src1[i];
+  }
+  if (warp == 8) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (t == 0) {
+    for (int k = 0; k < 2; k++) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(smem_u32(a0_full + k)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(d0_full + k)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(smem_u32(a1_full + k)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(d1_full + k)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(smem_u32(d1_empty + k)));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;  // D0[0], D0[1], D1[0], D1[1]: NP columns each
+  constexpr uint32_t IDESC =
+      (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+
+  const int n_tiles = p.g.tile_begin[p.g.L];
+  const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int nb = 4 * my_tiles;  // blocks of 128 latents (a tile = 8 rows x 64 = 4 blocks)
+  auto tile_of = [&](int b) { return (int)blockIdx.x + (b >> 2) * (int)gridDim.x; };
+
+  if (warp < 4) {
+    // ======================= front: window, gather, epilogue 0
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+    int l = 0, i0 = 0, j0 = 0;
+#pragma unroll 1
+    for (int b = 0; b <= nb; b++) {
+      if (b < nb) {
+        const int tile = tile_of(b), q = b & 3, s = b & 1;
+        if (q == 0) {  // stage this tile's causal window (fp32, zero outside the grid)
+          l = 0;
+          while (l + 1 < p.g.L && tile >= p.g.tile_begin[l + 1]) l++;
+          const int tl = tile - p.g.tile_begin[l];
+          const int ty = tl / p.g.tiles_x[l];
+          i0 = p.g.own_lo[l] + ty * ARM_TY;
+          j0 = (tl - ty * p.g.tiles_x[l]) * ARM_TX;
+          const int w = p.g.lv.w[l], rlo = p.g.lv.lo[l], rhi = p.g.lv.hi[l];
+          const int16_t* __restrict__ grid = p.lat + p.g.lv.off[l];
+          constexpr int IT = (S::WIN + 127) / 128;
+          int16_t v[IT];
+#pragma unroll
+          for (int k = 0; k < IT; k++) {
+            const int e = t + k * 128;
+            const int r = e / ARM_SW, c = e - r * ARM_SW;
+            const int gi = i0 - ARM_HALO_TOP + r, gj = j0 - ARM_HALO_X + c;
+            v[k] = (e < S::WIN && gi >= rlo && gi < rhi && gj >= 0 && gj < w)
+                       ? __ldg(grid + (int64_t)(gi - rlo) * w + gj) : (int16_t)0;
+          }
+          front_sync();  // every front thread is done with the previous tile's window
+#pragma unroll
+          for (int k = 0; k < IT; k++) {
+            const int e = t + k * 128;
+            if (e < S::WIN) win[e] = (float)v[k];
+          }
+          front_sync();
+        }
+        // A0 row t: [context (C), 1 (bias), 0 ...]   (A0[s] is free: MMA0(b-2) completed,
+        // observed by this warp in epilogue 0 of block b-2)
+        const int ry = 2 * q + (t >> 6), cx = t & 63;
+        const float* center = win + (ry + ARM_HALO_TOP) * ARM_SW + cx + ARM_HALO_X;
+        float row[K0];
+#pragma unroll
+        for (int c = 0; c < C; c++) row[c] = center[p.g.ctx_off[c]];
+        row[C] = 1.0f;
+#pragma unroll
+        for (int c = C + 1; c < K0; c++) row[c] = 0.0f;
+        float* A0 = sA0 + s * W::A0F;
+#pragma unroll
+        for (int c4 = 0; c4 < K0 / 4; c4++)
+          *reinterpret_cast<float4*>(A0 + kmaj(t, 4 * c4, K0)) =
+              make_float4(row[4 * c4], row[4 * c4 + 1], row[4 * c4 + 2], row[4 * c4 + 3]);
+        asm volatile("fence.proxy.async.shared::cta;");
+        __syncwarp();
+        if (lane == 0) tw_arrive(a0_full + s);
+      }
+      if (b >= 1) {  // epilogue 0 of block b-1
+        const int bb = b - 1, s = bb & 1;
+        mbar_wait(d0_full + s, (bb >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        float z[NP];
+        tmem_row<NP>(taddr + s * NP, z);
+        // the A1 slot of block bb was last read by MMA1(bb - A1S)
+        if (W::A1S == 2 && bb >= 2) mbar_wait(d1_full + s, ((bb >> 1) - 1) & 1);
+        if (W::A1S == 1 && bb >= 1) mbar_wait(d1_full + ((bb - 1) & 1), ((bb - 1) >> 1) & 1);
+        float* aH = sA1 + (W::A1S == 2 ? s : 0) * W::A1F;
+        float* aL = aH + TC_M * K1;
+#pragma unroll
+        for (int c4 = 0; c4 < K1 / 4; c4++) {
+          float hi[4], lo[4];
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            const int c = 4 * c4 + e;
+            const float x = (c < NH) ? fmaxf(z[c], 0.0f) : (c == NH ? 1.0f : 0.0f);
+            hi[e] = tf32_rna(x);
+            lo[e] = x - hi[e];
+          }
+          *reinterpret_cast<float4*>(aH + kmaj(t, 4 * c4, K1)) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<float4*>(aL + kmaj(t, 4 * c4, K1)) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) tw_arrive(a1_full + s);
+      }
+    }
+  } else if (warp < 8) {
+    // ======================= back: epilogue 1, output layer, Laplace bits
+    const int tb = t - 128;
+    const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+#pragma unroll 1
+    for (int b = 0; b < nb; b++) {
+      const int tile = tile_of(b), q = b & 3, s = b & 1;
+      mbar_wait(d1_full + s, (b >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      float z[NP];
+      tmem_row<NP>(taddr + 2 * NP + s * NP, z);
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) tw_arrive(d1_empty + s);  // D1[s] may be overwritten
+      uint64_t o = ldp2(p.bo);
+#pragma unroll
+      for (int n = 0; n < NH; n++) {
+        const float zn = fmaxf(z[n], 0.0f);
+        o = ffma2(f2pack(zn, zn), ldp2(p.wo[n]), o);
+      }
+      int l = 0;
+      while (l + 1 < p.g.L && tile >= p.g.tile_begin[l + 1]) l++;
+      const int tl = tile - p.g.tile_begin[l];
+      const int ty = tl / p.g.tiles_x[l];
+      const int i = p.g.own_lo[l] + ty * ARM_TY + 2 * q + (tb >> 6);
+      const int j = (tl - ty * p.g.tiles_x[l]) * ARM_TX + (tb & 63);
+      const int w = p.g.lv.w[l], rlo = p.g.lv.lo[l];
+      float bits = 0.0f;
+      if (i < p.g.own_hi[l] && j < w) {
+        const int64_t qi = p.g.lv.off[l] + (int64_t)(i - rlo) * w + j;
+        const float y = (float)__ldg(p.lat + qi);
+        const float2 ms = f2unpack(o);
+        bits = laplace_bits_tc(y, ms.x, ms.y, p.g);
+        if (p.bits != nullptr) {
+          p.bits[qi] = bits;
+          if (p.mu) p.mu[qi] = ms.x;
+          if (p.scale) p.scale[qi] = __expf(fminf(fmaxf(ms.y, p.g.lsmin), p.g.lsmax));
+        }
+      }
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) bits += __shfl_xor_sync(0xffffffffu, bits, o2);
+      if (lane == 0) p.partial[(int64_t)tile * 16 + q * 4 + (warp & 3)] = (double)bits;
+    }
+  } else if (lane == 0) {
+    // ======================= MMA issue
+    const uint32_t sB_u = smem_u32(sB), sA0_u = smem_u32(sA0), sA1_u = smem_u32(sA1);
+    auto mma0 = [&](int b) {
+      const int s = b & 1;
+      mbar_wait(a0_full + s, (b >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t a_u = sA0_u + 4 * s * W::A0F, d = tmem + s * NP;
+#pragma unroll
+      for (int k = 0; k < K0 / 8; k++) {
+        const uint64_t da = umma_desc(a_u + k * 256, 128, (K0 / 4) * 128);
+        mma_tf32(d, da, umma_desc(sB_u + k * 256, 128, (K0 / 4) * 128), IDESC, k > 0);
+        mma_tf32(d, da, umma_desc(sB_u + S::BW0 * 4 + k * 256, 128, (K0 / 4) * 128), IDESC, 1);
+      }
+      mma_commit(d0_full + s);
+    };
+    auto mma1 = [&](int b) {
+      const int s = b & 1;
+      mbar_wait(a1_full + s, (b >> 1) & 1);
+      if (b >= 2) mbar_wait(d1_empty + s, ((b >> 1) - 1) & 1);  // back done with D1[s] of block b-2
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t ah = sA1_u + 4 * (W::A1S == 2 ? s : 0) * W::A1F, al = ah + 4 * TC_M * K1, d = tmem + 2 * NP + s * NP;
+      const uint32_t bh = sB_u + 4 * (2 * S::BW0), bl = bh + 4 * S::BW1;
+#pragma unroll
+      for (int k = 0; k < K1 / 8; k++) {
+        const uint64_t dah = umma_desc(ah + k * 256, 128, (K1 / 4) * 128);
+        const uint64_t dal = umma_desc(al + k * 256, 128, (K1 / 4) * 128);
+        const uint64_t dbh = umma_desc(bh + k * 256, 128, (K1 / 4) * 128);
+        const uint64_t dbl = umma_desc(bl + k * 256, 128, (K1 / 4) * 128);
+        mma_tf32(d, dah, dbh, IDESC, k > 0);
+        mma_tf32(d, dah, dbl, IDESC, 1);
+        mma_tf32(d, dal, dbh, IDESC, 1);
+      }
+      mma_commit(d1_full + s);
+    };
+#pragma unroll 1
+    for (int b = 0; b < nb; b++) {
+      mma0(b);
+      if (b >= 1) mma1(b - 1);
+    }
+    if (nb >= 1) mma1(nb - 1);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+}
+
 // ---------------------------------------------------------------- host launcher
 // tf32 round-to-nearest (ties away, like cvt.rna) of a finite float
 static float tf32_rna_host(float x) {
@@ -339,13 +609,28 @@ static int launch_arm_tc(const ArmGeom& g, const cc_model_desc& d, const float* 
   for (int i = 0; i < NH; i++) p.wo[i] = make_float2(q[i], q[NH + i]);
   p.bo = make_float2(q[2 * NH], q[2 * NH + 1]);
 
+  const int tiles = g.tile_begin[g.L];
+  if (tiles == 0) return 0;
+  static const bool ss = getenv("CCRD_ARM_TC_SS") && getenv("CCRD_ARM_TC_SS")[0] == '1';  // the serial version
+  if constexpr (NHL == 2) {
+    if (!ss) {
+      using W = ArmTcwShape<C, NH, NHL>;
+      static bool attr_w = false;
+      if (!attr_w) {
+        cudaFuncSetAttribute(arm_tcw_kernel<C, NH, NHL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W::SMEM);
+        attr_w = true;
+      }
+      const int per_sm = (int)((227u * 1024u) / W::SMEM) < 1 ? 1 : (int)((227u * 1024u) / W::SMEM);
+      const int cap = per_sm * device_sm_count();
+      arm_tcw_kernel<C, NH, NHL><<<tiles < cap ? tiles : cap, TW_THREADS, W::SMEM, stream>>>(p);
+      return 1;
+    }
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(arm_tc_kernel<C, NH, NHL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
     attr = true;
   }
-  const int tiles = g.tile_begin[g.L];
-  if (tiles == 0) return 0;
   const int cap = TC_CTAS_PER_SM * device_sm_count();
   arm_tc_kernel<C, NH, NHL><<<tiles < cap ? tiles : cap, TC_THREADS, S::SMEM, stream>>>(p);
   return 1;
