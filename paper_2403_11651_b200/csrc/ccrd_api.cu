@@ -686,6 +686,39 @@ static int host_env(const char* name, int def, int lo, int hi) {
   return x < lo ? lo : (x > hi ? hi : x);
 }
 
+// the host path's upload / read-back streams and slot events, per thread and device
+struct HostPool {
+  cudaStream_t cs = nullptr, ds = nullptr;
+  cudaEvent_t copied[HOST_SLOTS_MAX], computed[HOST_SLOTS_MAX], computed_side[HOST_SLOTS_MAX],
+      read_back[HOST_SLOTS_MAX];
+  int device = -1;
+};
+static thread_local HostPool g_host;
+
+static int host_pool(HostPool** out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cuda_check("cudaGetDevice");
+  if (g_host.device != dev) {
+    // the upload stream runs at the highest priority: its small kernels (the
+    // int8 -> int16 latent widening) take the next free SM slots instead of
+    // queueing behind the compute stream's blocks
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if (cudaStreamCreateWithPriority(&g_host.cs, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&g_host.ds, cudaStreamNonBlocking) != cudaSuccess)
+      return cuda_check("stream create");
+    for (int k = 0; k < HOST_SLOTS_MAX; k++)
+      if (cudaEventCreateWithFlags(&g_host.copied[k], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&g_host.computed[k], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&g_host.computed_side[k], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&g_host.read_back[k], cudaEventDisableTiming) != cudaSuccess)
+        return cuda_check("event create");
+    g_host.device = dev;
+  }
+  *out = &g_host;
+  return CC_OK;
+}
+
 size_t cc_workspace_bytes_host(const cc_model_desc* desc, int32_t n_img) {
   if (validate(desc) != CC_OK || n_img < 1) return 0;
   return slice_bytes(*desc, nullptr) * (size_t)n_img +
@@ -725,15 +758,11 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
   // duplex, so image i+1's upload, image i's compute and image i-1's x_hat
   // readback overlap.  HOST_SLOTS staging slots of HOST_CHUNK images; events
   // guard their reuse.
-  // The upload stream runs at the highest priority: its small kernels (the
-  // int8 -> int16 latent widening) take the next free SM slots instead of
-  // queueing behind the compute stream's blocks.
-  cudaStream_t cs, ds;
-  int prio_lo = 0, prio_hi = 0;
-  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-  if (cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking) != cudaSuccess)
-    return cuda_check("stream create");
+  // streams and events live in a per-thread pool (creating and destroying 2
+  // streams + 16 events per call cost more than a small batch's compute)
+  HostPool* hp = nullptr;
+  if ((rc = host_pool(&hp))) return rc;
+  cudaStream_t cs = hp->cs, ds = hp->ds;
   // With concurrent streams the ARM (on s) and the pyramid + synthesis (on
   // the side stream) of consecutive images are not joined per image: each
   // stream runs image after image (as in cc_rd_forward's batch); a slot is
@@ -742,14 +771,8 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
   const bool conc = concurrent_streams();
   SideStream* side = nullptr;
   if (conc && (rc = side_stream(&side))) return rc;
-  cudaEvent_t copied[HOST_SLOTS_MAX], computed[HOST_SLOTS_MAX], computed_side[HOST_SLOTS_MAX],
-      read_back[HOST_SLOTS_MAX];
-  for (int k = 0; k < HOST_SLOTS; k++) {
-    cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&computed[k], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&computed_side[k], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&read_back[k], cudaEventDisableTiming);
-  }
+  cudaEvent_t *copied = hp->copied, *computed = hp->computed, *computed_side = hp->computed_side,
+              *read_back = hp->read_back;
   // start the side streams after whatever is already queued on s
   cudaEventRecord(computed[0], s);
   cudaStreamWaitEvent(cs, computed[0], 0);
@@ -822,14 +845,6 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
   cudaStreamSynchronize(cs);
   if (cudaStreamSynchronize(ds) != cudaSuccess && rc == CC_OK) rc = cuda_check("cc_rd_forward_host readback");
   delete[] jobs;
-  for (int k = 0; k < HOST_SLOTS; k++) {
-    cudaEventDestroy(copied[k]);
-    cudaEventDestroy(computed[k]);
-    cudaEventDestroy(computed_side[k]);
-    cudaEventDestroy(read_back[k]);
-  }
-  cudaStreamDestroy(cs);
-  cudaStreamDestroy(ds);
   if (rc == CC_OK) rc = cuda_check("cc_rd_forward_host");
   return rc;
 }
