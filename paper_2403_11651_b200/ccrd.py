@@ -437,6 +437,7 @@ class DeviceStrip:
         self.img = None if image_rows is None else torch.as_tensor(image_rows).to(device).contiguous()
         if self.img is not None:
             assert tuple(self.img.shape) == (3, rows, cfg.W), self.img.shape
+            self.desc.image_u8 = int(self.img.dtype == torch.uint8)   # 8-bit rows: x = v / 255
         self.xhat = torch.empty((3, rows, cfg.W), dtype=torch.float32, device=device) if with_xhat else None
         self.arm_w = np.ascontiguousarray(arm_w, np.float32)
         self.up_w = np.ascontiguousarray(up_w, np.float32)

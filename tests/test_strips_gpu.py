@@ -104,3 +104,31 @@ def test_strip_window_too_small_is_rejected():
     st.lo[1] += 1
     with pytest.raises(P.CcError):
         P.cc_workspace_bytes_strip(d, st) or P.cc_rd_forward_strip(d, st, P.CcImageIO(), 0, 0, 0)
+
+
+def test_strips_u8_rows_bit_identical_to_full_u8():
+    """8-bit image rows (desc.image_u8) through the strip entry point: the
+    stitched x_hat and the summed shares equal the full 8-bit image's."""
+    import paper_2403_11651_b200 as P
+    from paper_2403_11651_b200 import dist as ccdist
+    cfg = workload.CONFIGS["ref"].replace(H=150, W=222)
+    im = workload.make_image(cfg, 33)
+    im.image = workload.quantize_image_u8(im.image)
+    b = P.DeviceBatch(cfg, [im], image_u8=True)
+    full = b.forward().cpu().numpy()[0]
+    xf = b.xhat[0].cpu().numpy()
+    u8 = workload.to_u8(im.image)
+    d = P.desc_from_config(cfg)
+    strips, lays = ccdist.strip_layouts(d, 3)
+    off = _full_off(cfg)
+    full_lat = torch.from_numpy(im.latents).cuda()
+    xh = np.zeros((3, cfg.H, cfg.W), np.float32)
+    tot = np.zeros(4)
+    for st, lay in zip(strips, lays):
+        ds = P.ccrd.DeviceStrip(cfg, st, im.arm_w, im.up_w, im.syn_w, image_rows=u8[:, st.r0:st.r1])
+        assert ds.desc.image_u8 == 1
+        ds.lat.copy_(ccdist.pack_window(full_lat, off, lay))
+        tot += ds.forward().cpu().numpy()
+        xh[:, st.r0:st.r1] = ds.xhat.cpu().numpy()
+    np.testing.assert_array_equal(xh, xf)
+    np.testing.assert_allclose(tot, full, rtol=1e-7)
