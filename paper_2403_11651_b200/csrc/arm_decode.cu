@@ -35,7 +35,7 @@
 namespace ccrd {
 
 constexpr int DEC_THREADS = 512;
-constexpr int DEC_STREAMS = 64;  // one launch per image, spread over a pool of streams (concurrent kernels)
+constexpr int DEC_STREAMS = 128;  // per image two launches (level 0 / the rest) on separate halves of a pool
 constexpr int DEC_RING = 32;  // columns kept per live row
 constexpr int16_t DEC_POISON = INT16_MIN;
 
@@ -54,6 +54,7 @@ struct DecParams {
   float* scale;
   float* bits;
   double* partial;        // [L] per-grid rate of this image
+  int32_t l0;             // first grid of this launch (CTA b runs grid l0 + b)
   int32_t* poison_reads;  // optional counter
   ArmWeights<C, NH, NHL> w;
 };
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
     arm_decode_kernel(const __grid_constant__ DecParams<C, NH, NHL> p) {
   extern __shared__ int16_t ring[];  // [RR][DEC_RING]
   __shared__ float wsum[DEC_THREADS / 32];
-  const int l = blockIdx.x;
+  const int l = p.l0 + (int)blockIdx.x;
   const int nring = (p.rr_mask + 1) * DEC_RING;
   for (int i = threadIdx.x; i < nring; i += DEC_THREADS) ring[i] = DEC_POISON;
   __syncthreads();
@@ -217,21 +218,35 @@ static int launch_dec(const cc_model_desc& d, const ArmGeom& g, int a_override, 
   if (dec_streams(&ps)) return -1;
   double* part = reinterpret_cast<double*>(ws);
   cudaEventRecord(ps->ev[DEC_STREAMS], s);  // fork after the caller's queued work
-  const int ns = n_img < DEC_STREAMS ? n_img : DEC_STREAMS;
-  for (int k = 0; k < ns; k++) cudaStreamWaitEvent(ps->s[k], ps->ev[DEC_STREAMS], 0);
-  for (int i = 0; i < n_img; i++) {
-    pack_arm_weights<C, NH, NHL>(d, arm_w[i], p.w);
-    p.truth = truth[i];
-    p.decoded = decoded[i];
-    p.mu = mu ? mu[i] : nullptr;
-    p.scale = scale ? scale[i] : nullptr;
-    p.bits = bits ? bits[i] : nullptr;
-    p.partial = part + (size_t)i * d.L;
-    arm_decode_kernel<C, NH, NHL><<<d.L, DEC_THREADS, smem, ps->s[i % ns]>>>(p);
+  const int half = DEC_STREAMS / 2;
+  const int ns = n_img < half ? n_img : half;  // streams per pass
+  for (int k = 0; k < ns; k++) {
+    cudaStreamWaitEvent(ps->s[k], ps->ev[DEC_STREAMS], 0);
+    cudaStreamWaitEvent(ps->s[half + k], ps->ev[DEC_STREAMS], 0);
   }
-  for (int k = 0; k < ns; k++) {  // join
+  // every image's level-0 grid first (the longest wavefront: T = a (h - 1) + w
+  // steps on one SM), then the smaller grids fill the remaining SMs -- with
+  // all of an image's grids in one launch the block scheduler interleaved them
+  // and most level-0 grids started late (64 x 2K: 50 -> see DESIGN 8.3.1)
+  for (int pass = 0; pass < 2; pass++) {
+    if (pass == 1 && d.L < 2) break;
+    for (int i = 0; i < n_img; i++) {
+      pack_arm_weights<C, NH, NHL>(d, arm_w[i], p.w);
+      p.truth = truth[i];
+      p.decoded = decoded[i];
+      p.mu = mu ? mu[i] : nullptr;
+      p.scale = scale ? scale[i] : nullptr;
+      p.bits = bits ? bits[i] : nullptr;
+      p.partial = part + (size_t)i * d.L;
+      p.l0 = pass == 0 ? 0 : 1;
+      arm_decode_kernel<C, NH, NHL><<<pass == 0 ? 1 : d.L - 1, DEC_THREADS, smem, ps->s[pass * half + i % ns]>>>(p);
+    }
+  }
+  for (int k = 0; k < ns; k++) {  // join both passes' streams
     cudaEventRecord(ps->ev[k], ps->s[k]);
     cudaStreamWaitEvent(s, ps->ev[k], 0);
+    cudaEventRecord(ps->ev[half + k], ps->s[half + k]);
+    cudaStreamWaitEvent(s, ps->ev[half + k], 0);
   }
   dec_rate_kernel<<<(n_img + 127) / 128, 128, 0, s>>>(part, d.L, n_img, rate);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
@@ -259,7 +274,7 @@ int arm_decode_impl(const cc_model_desc& d, const ArmGeom& g, int a_override, in
   for (const auto& e : kDec)
     if (e.C == d.n_ctx && e.NH == NH && e.NHL == NHL) {
       const int rc = e.fn(d, g, a_override, n_img, truth, arm_w, decoded, mu, scale, bits, rate, poison, ws, s);
-      return rc < 0 ? rc : n_img + 1;
+      return rc < 0 ? rc : (d.L > 1 ? 2 : 1) * n_img + 1;
     }
   return -3;
 }
