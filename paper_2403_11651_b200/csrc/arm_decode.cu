@@ -59,7 +59,8 @@ struct DecParams {
   ArmWeights<C, NH, NHL> w;
 };
 
-template <int C, int NH, int NHL>
+// CHECK: count context reads of not-yet-decoded latents (tests pass a counter)
+template <int C, int NH, int NHL, bool CHECK>
 __global__ void __launch_bounds__(DEC_THREADS, 1)
     arm_decode_kernel(const __grid_constant__ DecParams<C, NH, NHL> p) {
   extern __shared__ int16_t ring[];  // [RR][DEC_RING]
@@ -90,16 +91,26 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
       // so its memory latency hides under the MLP
       const int16_t yv = truth[q];
       float z0[1][C];
+      if (r >= ARM_HALO_TOP && j >= ARM_HALO_X && j + ARM_HALO_X < w) {
+        // interior (every context in the grid: no bounds checks)
 #pragma unroll
-      for (int c = 0; c < C; c++) {
-        const int rr = r + p.dy[c], jj = j + p.dx[c];
-        float v = 0.0f;
-        if (rr >= 0 && jj >= 0 && jj < w) {
-          const int16_t q = ring[(rr & p.rr_mask) * DEC_RING + (jj & (DEC_RING - 1))];
-          poison += (q == DEC_POISON);
-          v = (float)q;
+        for (int c = 0; c < C; c++) {
+          const int16_t q = ring[((r + p.dy[c]) & p.rr_mask) * DEC_RING + ((j + p.dx[c]) & (DEC_RING - 1))];
+          if constexpr (CHECK) poison += (q == DEC_POISON);
+          z0[0][c] = (float)q;
         }
-        z0[0][c] = v;
+      } else {
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+          const int rr = r + p.dy[c], jj = j + p.dx[c];
+          float v = 0.0f;
+          if (rr >= 0 && jj >= 0 && jj < w) {
+            const int16_t q = ring[(rr & p.rr_mask) * DEC_RING + (jj & (DEC_RING - 1))];
+            if constexpr (CHECK) poison += (q == DEC_POISON);
+            v = (float)q;
+          }
+          z0[0][c] = v;
+        }
       }
       float z[1][NH];
       dense_ffma2<1, C, NH / 2, true>(z0, z, p.w.w0, p.w.b0);
@@ -124,7 +135,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
     }
     __syncthreads();  // step s's ring writes before step s + 1's reads
   }
-  if (p.poison_reads && poison) atomicAdd(p.poison_reads, poison);
+  if (CHECK && p.poison_reads && poison) atomicAdd(p.poison_reads, poison);
   // CTA rate partial, fixed order
 #pragma unroll
   for (int o2 = 16; o2 > 0; o2 >>= 1) bsum += __shfl_xor_sync(0xffffffffu, bsum, o2);
@@ -211,7 +222,8 @@ static int launch_dec(const cc_model_desc& d, const ArmGeom& g, int a_override, 
   if (smem > 200 * 1024) return -2;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(arm_decode_kernel<C, NH, NHL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(arm_decode_kernel<C, NH, NHL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(arm_decode_kernel<C, NH, NHL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   DecStreams* ps = nullptr;
@@ -239,7 +251,8 @@ static int launch_dec(const cc_model_desc& d, const ArmGeom& g, int a_override, 
       p.bits = bits ? bits[i] : nullptr;
       p.partial = part + (size_t)i * d.L;
       p.l0 = pass == 0 ? 0 : 1;
-      arm_decode_kernel<C, NH, NHL><<<pass == 0 ? 1 : d.L - 1, DEC_THREADS, smem, ps->s[pass * half + i % ns]>>>(p);
+      auto kern = poison ? arm_decode_kernel<C, NH, NHL, true> : arm_decode_kernel<C, NH, NHL, false>;
+      kern<<<pass == 0 ? 1 : d.L - 1, DEC_THREADS, smem, ps->s[pass * half + i % ns]>>>(p);
     }
   }
   for (int k = 0; k < ns; k++) {  // join both passes' streams
