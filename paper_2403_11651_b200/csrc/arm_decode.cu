@@ -37,6 +37,10 @@ namespace ccrd {
 constexpr int DEC_THREADS = 512;
 constexpr int DEC_STREAMS = 128;  // per image two launches (level 0 / the rest) on separate halves of a pool
 constexpr int DEC_RING = 32;  // columns kept per live row
+constexpr int DEC_PAD = ARM_HALO_X;  // |dx| <= 4
+constexpr int DEC_RW = DEC_RING + 2 * DEC_PAD;  // ring row: physical column p holds logical column (p - 4) & 31
+                                                // (the 4 columns at either end duplicated), so a context read
+                                                // is (row constant + dx + 4) + (j & 31), never wrapping
 constexpr int16_t DEC_POISON = INT16_MIN;
 
 // One launch = one image: its ARM weights live in the kernel-parameter bank, so
@@ -63,10 +67,10 @@ struct DecParams {
 template <int C, int NH, int NHL, bool CHECK>
 __global__ void __launch_bounds__(DEC_THREADS, 1)
     arm_decode_kernel(const __grid_constant__ DecParams<C, NH, NHL> p) {
-  extern __shared__ int16_t ring[];  // [RR][DEC_RING]
+  extern __shared__ int16_t ring[];  // [RR][DEC_RW]
   __shared__ float wsum[DEC_THREADS / 32];
   const int l = p.l0 + (int)blockIdx.x;
-  const int nring = (p.rr_mask + 1) * DEC_RING;
+  const int nring = (p.rr_mask + 1) * DEC_RW;
   for (int i = threadIdx.x; i < nring; i += DEC_THREADS) ring[i] = DEC_POISON;
   __syncthreads();
 
@@ -77,6 +81,10 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
   const int T = a * (h - 1) + w;
   float bsum = 0.0f;
   int poison = 0;
+  // per context, for the thread's current row: ring offset of (r + dy, j + dx)
+  // minus (j & 31) -- recomputed only when the thread's row changes
+  int cached_r = -1;
+  int roff[C];
 #pragma unroll 1
   for (int s = 0; s < T; s++) {
     // rows on this step: 0 <= s - a r < w
@@ -93,9 +101,15 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
       float z0[1][C];
       if (r >= ARM_HALO_TOP && j >= ARM_HALO_X && j + ARM_HALO_X < w) {
         // interior (every context in the grid: no bounds checks)
+        if (r != cached_r) {
+#pragma unroll
+          for (int c = 0; c < C; c++) roff[c] = ((r + p.dy[c]) & p.rr_mask) * DEC_RW + DEC_PAD + p.dx[c];
+          cached_r = r;
+        }
+        const int16_t* rj = ring + (j & (DEC_RING - 1));
 #pragma unroll
         for (int c = 0; c < C; c++) {
-          const int16_t q = ring[((r + p.dy[c]) & p.rr_mask) * DEC_RING + ((j + p.dx[c]) & (DEC_RING - 1))];
+          const int16_t q = rj[roff[c]];
           if constexpr (CHECK) poison += (q == DEC_POISON);
           z0[0][c] = (float)q;
         }
@@ -105,7 +119,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
           const int rr = r + p.dy[c], jj = j + p.dx[c];
           float v = 0.0f;
           if (rr >= 0 && jj >= 0 && jj < w) {
-            const int16_t q = ring[(rr & p.rr_mask) * DEC_RING + (jj & (DEC_RING - 1))];
+            const int16_t q = ring[(rr & p.rr_mask) * DEC_RW + (jj & (DEC_RING - 1)) + DEC_PAD];
             if constexpr (CHECK) poison += (q == DEC_POISON);
             v = (float)q;
           }
@@ -127,7 +141,13 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
       const float2 ms = f2unpack(o);
       const float bt = laplace_bits((float)yv, ms.x, ms.y, p.g);
       bsum += bt;
-      ring[(r & p.rr_mask) * DEC_RING + (j & (DEC_RING - 1))] = yv;
+      {
+        const int lc = j & (DEC_RING - 1);
+        int16_t* rw = ring + (r & p.rr_mask) * DEC_RW + lc + DEC_PAD;
+        rw[0] = yv;
+        if (lc >= DEC_RING - DEC_PAD) rw[-DEC_RING] = yv;  // left pad
+        if (lc < DEC_PAD) rw[DEC_RING] = yv;               // right pad
+      }
       decoded[q] = yv;
       if (p.bits) p.bits[off + q] = bt;
       if (p.mu) p.mu[off + q] = ms.x;
@@ -218,7 +238,7 @@ static int launch_dec(const cc_model_desc& d, const ArmGeom& g, int a_override, 
     p.dx[c] = d.ctx_dx[c];
   }
   p.poison_reads = poison;
-  const size_t smem = (size_t)rr * DEC_RING * sizeof(int16_t);
+  const size_t smem = (size_t)rr * DEC_RW * sizeof(int16_t);
   if (smem > 200 * 1024) return -2;
   static bool attr = false;
   if (!attr) {
