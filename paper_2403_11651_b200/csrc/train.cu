@@ -31,6 +31,7 @@
 //   6. fp64 reduction of every partial into the gradient, Adam, cost.
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "ccrd_common.cuh"
@@ -38,11 +39,17 @@
 namespace ccrd {
 
 constexpr int TR_MAX_W = 2048;  // arm + up + syn weights (floats)
-__constant__ float c_tw[TR_MAX_W];
+// TR_BANKS copies of the constant banks: up to TR_BANKS images train
+// concurrently on different streams (a stream keeps a bank; a stream taking
+// over another stream's bank waits for that stream's last use of it).  Every
+// kernel addresses its bank through the offsets it is given (bank x size +
+// the layer offset): the loads stay uniform (LDCU c[0x3][UR + imm]).
+constexpr int TR_BANKS = 3;
+__constant__ float c_tw[TR_BANKS * TR_MAX_W];
 // the ARM weights again, packed for FFMA2 in the forward: per layer k, for
 // input i the pair (W[2n][i], W[2n+1][i]), then the bias pairs
 constexpr int TR_MAX_ARMP = 1536;  // float2
-__constant__ float2 c_tp[TR_MAX_ARMP];
+__constant__ float2 c_tp[TR_BANKS * TR_MAX_ARMP];
 
 __global__ void tr_pack_arm_kernel(const float* __restrict__ w, float2* __restrict__ out, int nl, int C, int NH) {
   // one thread per output pair; layer k: nin x (nout/2) weight pairs then nout/2 bias pairs
@@ -96,6 +103,7 @@ struct TrainArmParams {
   double* rate;    // [CTAs][4]    per-warp bits
   float* wpart;    // [CTAs][n_arm] partial weight gradients
   int32_t n_arm;
+  int32_t tw0, tp0;  // this step's constant-bank base offsets (c_tw, c_tp)
 };
 
 // bits and d bits / d (y, mu, s) -- fp32, IEEE exp / log (the hybrid stable
@@ -152,7 +160,10 @@ struct TrArmLayout {
   static_assert(NL <= 4, "up to 3 hidden layers");
 };
 
-template <int C, int NH, int NHL>
+// BANK: the constant bank this step's weights sit in, a template parameter so
+// the weight reads keep their immediate constant offsets (uniform LDCU; a
+// runtime bank base turns them into per-thread LDC, -9% per iteration)
+template <int C, int NH, int NHL, int BANK>
 __global__ void __launch_bounds__(TA_THREADS) tr_arm_kernel(const __grid_constant__ TrainArmParams p) {
   // per latent, in shared memory for the weight-gradient outer products:
   //   layer k input z_k (C or NH) and output gradient du_k (NH, or 2 for the last)
@@ -179,7 +190,7 @@ __global__ void __launch_bounds__(TA_THREADS) tr_arm_kernel(const __grid_constan
       z[0][c] = (ii >= 0 && ii < h && jj >= 0 && jj < w) ? g[(int64_t)ii * w + jj] : 0.0f;
     }
     // forward, FFMA2: two output neurons per instruction (c_tp pairs)
-    int offp = 0;
+    int offp = BANK * TR_MAX_ARMP;
     float mu = 0.0f, s = 0.0f;
 #pragma unroll
     for (int k = 0; k < NL; k++) {
@@ -231,7 +242,7 @@ __global__ void __launch_bounds__(TA_THREADS) tr_arm_kernel(const __grid_constan
     vec[LY::doff(NL - 1) + 1] = du[1];
     int offk[NL];
     {
-      int o2 = 0;
+      int o2 = BANK * TR_MAX_W;
 #pragma unroll
       for (int k = 0; k < NL; k++) {
         const int nin = (k == 0) ? C : NH, nout = (k == NL - 1) ? 2 : NH;
@@ -950,10 +961,17 @@ template <int C, int NH, int NHL>
 static void tr_arm_launch(dim3 g, int t, size_t smem, cudaStream_t s, const TrainArmParams& p) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tr_arm_kernel<C, NH, NHL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(tr_arm_kernel<C, NH, NHL, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(tr_arm_kernel<C, NH, NHL, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(tr_arm_kernel<C, NH, NHL, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     attr = true;
   }
-  tr_arm_kernel<C, NH, NHL><<<g, t, smem, s>>>(p);
+  static_assert(TR_BANKS == 3, "one instantiation per bank");
+  switch (p.tp0 / TR_MAX_ARMP) {
+    case 0: tr_arm_kernel<C, NH, NHL, 0><<<g, t, smem, s>>>(p); break;
+    case 1: tr_arm_kernel<C, NH, NHL, 1><<<g, t, smem, s>>>(p); break;
+    default: tr_arm_kernel<C, NH, NHL, 2><<<g, t, smem, s>>>(p); break;
+  }
 }
 struct TrArmEntry {
   int C, NH, NHL;
@@ -1023,6 +1041,49 @@ static int blocks_for(int64_t n) { return (int)((n + TB - 1) / TB); }
 
 #define TCONV_BWD(K) ((K) == 8 ? tr_tconv_bwd_kernel<8> : (K) == 4 ? tr_tconv_bwd_kernel<4> : tr_tconv_bwd_kernel<0>)
 
+// ---------------------------------------------------------------- constant-bank ownership
+struct TrBank {
+  cudaStream_t owner = nullptr;
+  bool used = false;
+  cudaEvent_t last_use = nullptr;  // recorded after the owner's last step
+  uint64_t tick = 0;
+};
+static TrBank g_banks[TR_BANKS];
+static std::mutex g_bank_mu;
+static uint64_t g_bank_tick = 0;
+static int g_bank_dev = -1;
+
+// the bank stream s trains with; waits (on s) for a previous owner's last use
+static int acquire_bank(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_bank_mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (g_bank_dev != dev) {
+    for (auto& b : g_banks) {
+      b = TrBank();
+      cudaEventCreateWithFlags(&b.last_use, cudaEventDisableTiming);
+    }
+    g_bank_dev = dev;
+  }
+  int k = -1;
+  for (int i = 0; i < TR_BANKS; i++)
+    if (g_banks[i].used && g_banks[i].owner == s) k = i;
+  if (k < 0) {  // least recently used bank
+    k = 0;
+    for (int i = 1; i < TR_BANKS; i++)
+      if (g_banks[i].tick < g_banks[k].tick) k = i;
+    if (g_banks[k].used) cudaStreamWaitEvent(s, g_banks[k].last_use, 0);
+    g_banks[k].owner = s;
+    g_banks[k].used = true;
+  }
+  g_banks[k].tick = ++g_bank_tick;
+  return k;
+}
+static void release_bank(int k, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_bank_mu);
+  cudaEventRecord(g_banks[k].last_use, s);
+}
+
 // The iteration.  Returns the number of kernel launches (>= 0) or -1 if a
 // CUDA call failed (the caller checks cudaGetLastError).
 int train_step_impl(const cc_model_desc& d, float* par, const float* noise, const float* image, float* am, float* av,
@@ -1038,15 +1099,18 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
   // weights -> constant bank (arm | up | syn), device to device
   const int64_t nw = pl.n_arm + pl.n_up + pl.n_syn;
   if (nw > TR_MAX_W) return -2;
-  cudaMemcpyToSymbolAsync(c_tw, par + lv.n_lat, sizeof(float) * (size_t)nw, 0, cudaMemcpyDeviceToDevice, s);
+  const int bank = acquire_bank(s);
+  const int tw0 = bank * TR_MAX_W, tp0 = bank * TR_MAX_ARMP;
+  cudaMemcpyToSymbolAsync(c_tw, par + lv.n_lat, sizeof(float) * (size_t)nw, sizeof(float) * (size_t)tw0,
+                          cudaMemcpyDeviceToDevice, s);
   {  // FFMA2-packed ARM weights (forward) through a workspace buffer
     float2* packed = (float2*)(W + pl.o_grad_tmp);  // free until the first reduction
     tr_pack_arm_kernel<<<1, 256, 0, s>>>(par + lv.n_lat, packed, d.arm_n_layers, d.n_ctx, d.arm_widths[1]);
-    cudaMemcpyToSymbolAsync(c_tp, packed, sizeof(float2) * (size_t)(pl.n_arm / 2 + 2), 0, cudaMemcpyDeviceToDevice,
-                            s);
+    cudaMemcpyToSymbolAsync(c_tp, packed, sizeof(float2) * (size_t)(pl.n_arm / 2 + 2), sizeof(float2) * (size_t)tp0,
+                            cudaMemcpyDeviceToDevice, s);
     launches++;
   }
-  const int koff = (int)pl.n_arm;  // taps in c_tw
+  const int koff = tw0 + (int)pl.n_arm;  // taps in c_tw
   TrainSynDims sd;
   sd.H = d.H;
   sd.W = d.W;
@@ -1054,7 +1118,7 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
   sd.CH = CH;
   sd.R = R;
   sd.P = P;
-  sd.oA0 = (int)(pl.n_arm + pl.n_up);
+  sd.oA0 = tw0 + (int)(pl.n_arm + pl.n_up);
   sd.oa0 = sd.oA0 + L * CH;
   sd.oA1 = sd.oa0 + CH;
   sd.oa1 = sd.oA1 + 3 * CH;
@@ -1088,6 +1152,8 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
     ap.rate = (double*)(W + pl.o_rate);
     ap.wpart = F(pl.o_wpart_arm);
     ap.n_arm = (int)pl.n_arm;
+    ap.tw0 = tw0;
+    ap.tp0 = tp0;
     const int C = d.n_ctx, NH = d.arm_widths[1], NL = d.arm_n_layers;
     const TrArmEntry* ae = nullptr;
     for (const auto& e : kTrArm)
@@ -1211,6 +1277,7 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
         par, grad, am, av, pl.n_par, opt->lr, opt->beta1, opt->beta2, opt->eps, c1, c2);
     launches++;
   }
+  release_bank(bank, s);  // this stream's last use of the bank
   return launches;
 }
 

@@ -111,3 +111,39 @@ def test_train_gradient_full_size_ref_vs_oracle():
 def test_train_refuses_2d():
     import paper_2403_11651_b200 as P
     assert P.cc_train_workspace_bytes(P.desc_from_config(workload.CONFIGS["t2300"])) == 0
+
+
+def test_train_concurrent_streams_bit_identical():
+    """Several trainers stepping concurrently on their own streams (the
+    multi-image training mode bench.py --train --images N times) give exactly
+    the parameters each reaches alone: the per-stream constant weight banks
+    (train.cu acquire_bank) keep one image's weights from leaking into
+    another's kernels -- including with more streams than banks."""
+    import paper_2403_11651_b200 as P
+    cfg = workload.CONFIGS["ref"].replace(H=96, W=128)
+    K, steps = 5, 4
+    states = [make_state(cfg, 40 + k) for k in range(K)]
+
+    def trainers():
+        out = []
+        for im, y, u in states:
+            tr = P.DeviceTrainer(cfg, y, im.arm_w, im.up_w, im.syn_w, im.image)
+            tr.noise.copy_(torch.as_tensor(u))
+            out.append(tr)
+        torch.cuda.synchronize()
+        return out
+
+    alone = trainers()
+    for tr in alone:
+        for _ in range(steps):
+            tr.step(lr=1e-3)
+    torch.cuda.synchronize()
+    conc = trainers()
+    streams = [torch.cuda.Stream() for _ in range(K)]
+    for _ in range(steps):
+        for tr, st in zip(conc, streams):
+            tr.step(lr=1e-3, stream_ptr=st.cuda_stream)
+    torch.cuda.synchronize()
+    for a, c in zip(alone, conc):
+        assert torch.equal(a.params, c.params)
+        assert torch.equal(a.result, c.result)
