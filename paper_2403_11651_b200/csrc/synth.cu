@@ -21,6 +21,10 @@
 // The dense L x H x W tensor is never materialised in HBM.
 #include "ccrd_common.cuh"
 
+#ifndef CCRD_SYN_MC
+#define CCRD_SYN_MC 20  // hidden neurons per MLP chunk (live accumulators)
+#endif
+
 namespace ccrd {
 
 #ifdef CCRD_SYN_TIMING
@@ -197,7 +201,7 @@ __device__ __forceinline__ void mlp_pair(const SynParams<L, CH, R, K>& p, const 
   // hidden layer in chunks of MC neurons: fewer live accumulators (each chunk
   // adds its contribution to the three output pairs), same FMA count and the
   // same per-output summation order as one pass (bias, then hidden 0 .. CH-1)
-  constexpr int MC = (CH % 20 == 0 && CH > 20) ? 20 : CH;
+  constexpr int MC = (CH % CCRD_SYN_MC == 0 && CH > CCRD_SYN_MC) ? CCRD_SYN_MC : CH;
   const uint64_t one = f2pack(1.0f, 1.0f);
   uint64_t o[3];
 #pragma unroll

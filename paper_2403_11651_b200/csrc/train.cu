@@ -32,6 +32,7 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "ccrd_common.cuh"
@@ -99,7 +100,7 @@ struct TrainArmParams {
   float lsmin, lsmax, bits_cap, w_r;  // w_r = lambda / (H W)
   const float* yq;
   float* gown;     // [N_lat]      w_r d bits / d y_hat (own position)
-  float* dctx;     // [N_lat][C]   d J / d context value c of this latent
+  float* dctx;     // [C][N_lat]   d J / d context value c of this latent (coalesced stores / gathers)
   double* rate;    // [CTAs][4]    per-warp bits
   float* wpart;    // [CTAs][n_arm] partial weight gradients
   int32_t n_arm;
@@ -155,10 +156,72 @@ struct TrArmLayout {
   __host__ __device__ static constexpr int woff(int k) {
     return k == 0 ? 0 : woff(k - 1) + (k - 1 == 0 ? C : NH) * nout(k - 1) + nout(k - 1);
   }
+  // weight-gradient tiles of layer k (4 or 2 outputs x 4 inputs) and the
+  // warps they take when each layer gets warps of its own
+  __host__ __device__ static constexpr int ntile(int k) { return (kin(k) / 4) * (nout(k) % 4 == 0 ? nout(k) / 4 : nout(k) / 2); }
+  __host__ __device__ static constexpr int nw(int k) { return (ntile(k) + 31) / 32; }
+  __host__ __device__ static constexpr int wstart(int k) { return k == 0 ? 0 : wstart(k - 1) + nw(k - 1); }
+  __host__ __device__ static constexpr int wsum() { return wstart(NL - 1) + nw(NL - 1); }
   static constexpr int VEC_RAW = doff(NL - 1) + r4(2);
   static constexpr int VEC = VEC_RAW + ((VEC_RAW / 4) % 2 == 0 ? 4 : 0);  // odd number of 16-byte words: bank spread
   static_assert(NL <= 4, "up to 3 hidden layers");
 };
+
+// Weight gradient of layer K over one CTA's latents, as a register-blocked
+// outer product: the thread owns a TR (outputs: 4, or 2 for the output layer)
+// x 4 (inputs; the input column nin is the constant 1 = the bias) tile with
+// two interleaved partial sums, reading per latent one float4 (float2) of du
+// and one float4 of z from the shared records; FFMA2 over input pairs (each
+// lane its own fma chain: the same sums as scalar FMA).
+template <int C, int NH, int NHL, int K>
+__device__ __forceinline__ void tr_wgrad_tile(const float* tsm, const int tile, float* __restrict__ wp) {
+  using LY = TrArmLayout<C, NH, NHL>;
+  constexpr int NL = NHL + 1, VEC = LY::VEC;
+  constexpr int nin = (K == 0) ? C : NH, nout = (K == NL - 1) ? 2 : NH;
+  constexpr int tcols = LY::kin(K) / 4, TR = (nout % 4 == 0) ? 4 : 2;
+  const int tr = tile / tcols, tc = tile - tr * tcols;
+  const float* dp = tsm + LY::doff(K) + TR * tr;
+  const float* zp = tsm + LY::zoff(K) + 4 * tc;
+  uint64_t acc[2][TR][2];
+#pragma unroll
+  for (int h = 0; h < 2; h++)
+#pragma unroll
+    for (int a = 0; a < TR; a++) acc[h][a][0] = acc[h][a][1] = 0ull;
+#pragma unroll 8
+  for (int m = 0; m < TA_THREADS; m += 2) {
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      float dv[TR];
+      if constexpr (TR == 4) {
+        const float4 dd = *reinterpret_cast<const float4*>(dp + (m + h) * VEC);
+        dv[0] = dd.x, dv[1] = dd.y, dv[2] = dd.z, dv[3] = dd.w;
+      } else {
+        const float2 dd = *reinterpret_cast<const float2*>(dp + (m + h) * VEC);
+        dv[0] = dd.x, dv[1] = dd.y;
+      }
+      const ulonglong2 zz = *reinterpret_cast<const ulonglong2*>(zp + (m + h) * VEC);
+#pragma unroll
+      for (int a = 0; a < TR; a++) {
+        const uint64_t d2 = f2pack(dv[a], dv[a]);
+        acc[h][a][0] = ffma2(d2, zz.x, acc[h][a][0]);
+        acc[h][a][1] = ffma2(d2, zz.y, acc[h][a][1]);
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < TR; a++)
+#pragma unroll
+    for (int bp = 0; bp < 2; bp++) {
+      const float2 x0 = f2unpack(acc[0][a][bp]), x1 = f2unpack(acc[1][a][bp]);
+      const float vv[2] = {x0.x + x1.x, x0.y + x1.y};
+#pragma unroll
+      for (int e = 0; e < 2; e++) {
+        const int o = TR * tr + a, i2 = 4 * tc + 2 * bp + e;
+        if (i2 < nin) wp[LY::woff(K) + o * nin + i2] = vv[e];                 // W[o][i]
+        else if (i2 == nin) wp[LY::woff(K) + nin * nout + o] = vv[e];         // b[o]
+      }
+    }
+}
 
 // BANK: the constant bank this step's weights sit in, a template parameter so
 // the weight reads keep their immediate constant offsets (uniform LDCU; a
@@ -280,7 +343,7 @@ __global__ void __launch_bounds__(TA_THREADS) tr_arm_kernel(const __grid_constan
         }
       } else {
 #pragma unroll
-        for (int c = 0; c < C; c++) p.dctx[q * C + c] = dz[c];
+        for (int c = 0; c < C; c++) p.dctx[c * p.lv.n_lat + q] = dz[c];
       }
     }
   } else {
@@ -291,78 +354,35 @@ __global__ void __launch_bounds__(TA_THREADS) tr_arm_kernel(const __grid_constan
   for (int o2 = 16; o2 > 0; o2 >>= 1) bits += __shfl_xor_sync(0xffffffffu, bits, o2);
   if ((threadIdx.x & 31) == 0) p.rate[blockIdx.x * (TA_THREADS / 32) + (threadIdx.x >> 5)] = (double)bits;
   __syncthreads();
-  // per-CTA weight gradients, layer by layer, as register-blocked outer
-  // products over the CTA's latents: a thread owns a TH (outputs) x 4 (inputs,
-  // the last input column being the constant 1 = the bias) tile with two
-  // interleaved partial sums (2 x TH x 4 independent FMA chains), reading per
-  // latent one float4 (or float2) of du and one float4 of z
-  int tile = threadIdx.x;
-#pragma unroll 1
-  for (int k = 0; k < NL; k++) {
-    const int nin = (k == 0) ? C : NH, nout = (k == NL - 1) ? 2 : NH;
-    const int tcols = LY::kin(k) / 4;
-    const int wbase = LY::woff(k);
-    if (nout % 4 == 0) {
-      const int trows = nout / 4, ntile = tcols * trows;
-      for (; tile < ntile; tile += TA_THREADS) {
-        const int tr = tile / tcols, tc = tile - tr * tcols;
-        float acc[2][4][4] = {};
-#pragma unroll 2
-        for (int m = 0; m < TA_THREADS; m += 2) {
-#pragma unroll
-          for (int h = 0; h < 2; h++) {
-            const float* v = tsm + (m + h) * VEC;
-            const float4 dd = *reinterpret_cast<const float4*>(v + LY::doff(k) + 4 * tr);
-            const float4 zz = *reinterpret_cast<const float4*>(v + LY::zoff(k) + 4 * tc);
-            const float dv[4] = {dd.x, dd.y, dd.z, dd.w}, zv[4] = {zz.x, zz.y, zz.z, zz.w};
-#pragma unroll
-            for (int a = 0; a < 4; a++)
-#pragma unroll
-              for (int b = 0; b < 4; b++) acc[h][a][b] = fmaf(dv[a], zv[b], acc[h][a][b]);
-          }
-        }
-#pragma unroll
-        for (int a = 0; a < 4; a++)
-#pragma unroll
-          for (int b = 0; b < 4; b++) {
-            const int o = 4 * tr + a, i2 = 4 * tc + b;
-            const float v2 = acc[0][a][b] + acc[1][a][b];
-            if (i2 < nin) p.wpart[(int64_t)blockIdx.x * p.n_arm + wbase + o * nin + i2] = v2;  // W[o][i]
-            else if (i2 == nin) p.wpart[(int64_t)blockIdx.x * p.n_arm + wbase + nin * nout + o] = v2;  // b[o]
-          }
+  // per-CTA weight gradients, layer by layer (tr_wgrad_tile)
+  if constexpr (LY::wsum() <= TA_THREADS / 32) {
+    // each layer's tiles on warps of their own (no divergence between layers
+    // inside a warp; every SM sub-partition busy)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* wp = p.wpart + (int64_t)blockIdx.x * p.n_arm;
+    auto run = [&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      if (warp >= LY::wstart(k) && warp < LY::wstart(k) + LY::nw(k)) {
+        const int tile = (warp - LY::wstart(k)) * 32 + lane;
+        if (tile < LY::ntile(k)) tr_wgrad_tile<C, NH, NHL, k>(tsm, tile, wp);
       }
-      tile -= ntile;
-    } else {  // the 2-wide output layer
-      const int trows = nout / 2, ntile = tcols * trows;
-      for (; tile < ntile; tile += TA_THREADS) {
-        const int tr = tile / tcols, tc = tile - tr * tcols;
-        float acc[2][2][4] = {};
-#pragma unroll 2
-        for (int m = 0; m < TA_THREADS; m += 2) {
-#pragma unroll
-          for (int h = 0; h < 2; h++) {
-            const float* v = tsm + (m + h) * VEC;
-            const float2 dd = *reinterpret_cast<const float2*>(v + LY::doff(k) + 2 * tr);
-            const float4 zz = *reinterpret_cast<const float4*>(v + LY::zoff(k) + 4 * tc);
-            const float dv[2] = {dd.x, dd.y}, zv[4] = {zz.x, zz.y, zz.z, zz.w};
-#pragma unroll
-            for (int a = 0; a < 2; a++)
-#pragma unroll
-              for (int b = 0; b < 4; b++) acc[h][a][b] = fmaf(dv[a], zv[b], acc[h][a][b]);
-          }
-        }
-#pragma unroll
-        for (int a = 0; a < 2; a++)
-#pragma unroll
-          for (int b = 0; b < 4; b++) {
-            const int o = 2 * tr + a, i2 = 4 * tc + b;
-            const float v2 = acc[0][a][b] + acc[1][a][b];
-            if (i2 < nin) p.wpart[(int64_t)blockIdx.x * p.n_arm + wbase + o * nin + i2] = v2;
-            else if (i2 == nin) p.wpart[(int64_t)blockIdx.x * p.n_arm + wbase + nin * nout + o] = v2;
-          }
-      }
-      tile -= ntile;
-    }
+    };
+    run(std::integral_constant<int, 0>{});
+    run(std::integral_constant<int, 1>{});
+    if constexpr (NL > 2) run(std::integral_constant<int, 2>{});
+    if constexpr (NL > 3) run(std::integral_constant<int, 3>{});
+  } else {
+    float* wp = p.wpart + (int64_t)blockIdx.x * p.n_arm;
+    int tile = threadIdx.x;
+    auto run = [&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      for (; tile < LY::ntile(k); tile += TA_THREADS) tr_wgrad_tile<C, NH, NHL, k>(tsm, tile, wp);
+      tile -= LY::ntile(k);
+    };
+    run(std::integral_constant<int, 0>{});
+    run(std::integral_constant<int, 1>{});
+    if constexpr (NL > 2) run(std::integral_constant<int, 2>{});
+    if constexpr (NL > 3) run(std::integral_constant<int, 3>{});
   }
 }
 
@@ -385,7 +405,7 @@ __global__ void tr_arm_gather_kernel(TrainLevels lv, const __grid_constant__ Tra
   float g = gown[q];
   for (int c = 0; c < C; c++) {
     const int pi = i - cx.dy[c], pj = j - cx.dx[c];  // latent whose context c is (i, j)
-    if (pi >= 0 && pi < h && pj >= 0 && pj < w) g += dctx[(lv.off[l] + (int64_t)pi * w + pj) * C + c];
+    if (pi >= 0 && pi < h && pj >= 0 && pj < w) g += dctx[c * lv.n_lat + lv.off[l] + (int64_t)pi * w + pj];
   }
   gy[q] = g;
 }
