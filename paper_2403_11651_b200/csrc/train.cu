@@ -75,7 +75,10 @@ constexpr int TA_THREADS = 128;  // ARM: latents per CTA
 constexpr int TS_THREADS = 128;  // synthesis 1x1 backward: pixels per CTA
 constexpr int TB = 256;          // generic elementwise / stencil kernels
 constexpr int TR_GRID_CAP = 592; // grid-stride reductions: 4 CTAs per SM
-constexpr int TR_TCONV_CAP = 64; // transposed-conv adjoint: blocks per channel
+#ifndef CCRD_TR_TCONV_CAP
+#define CCRD_TR_TCONV_CAP 256
+#endif
+constexpr int TR_TCONV_CAP = CCRD_TR_TCONV_CAP;  // transposed-conv adjoint: blocks per channel
 
 struct TrainLevels {
   int32_t L, H, W;
