@@ -842,16 +842,21 @@ __global__ void tr_reduce2_kernel(const double* __restrict__ tmp, int chunks, in
   if (lane == 0) grad[e] = (float)s;
 }
 
-__global__ void tr_result_kernel(const double* __restrict__ rate_part, int64_t n_rate, const double* __restrict__ sse_part,
-                                 int64_t n_sse, double inv_3p, double lambda_over_p, cc_rd_result* out) {
-  __shared__ double ra[TB], sa[TB];
+constexpr int TR_RES_THREADS = 1024;  // one CTA: short serial chains per thread
+__global__ void __launch_bounds__(TR_RES_THREADS) tr_result_kernel(const double* __restrict__ rate_part, int64_t n_rate,
+                                                                  const double* __restrict__ sse_part, int64_t n_sse,
+                                                                  double inv_3p, double lambda_over_p,
+                                                                  cc_rd_result* out) {
+  __shared__ double ra[TR_RES_THREADS], sa[TR_RES_THREADS];
   double r = 0.0, s = 0.0;
-  for (int64_t i = threadIdx.x; i < n_rate; i += TB) r += rate_part[i];
-  for (int64_t i = threadIdx.x; i < n_sse; i += TB) s += sse_part[i];
+#pragma unroll 4
+  for (int64_t i = threadIdx.x; i < n_rate; i += TR_RES_THREADS) r += rate_part[i];
+#pragma unroll 4
+  for (int64_t i = threadIdx.x; i < n_sse; i += TR_RES_THREADS) s += sse_part[i];
   ra[threadIdx.x] = r;
   sa[threadIdx.x] = s;
   __syncthreads();
-  for (int o = TB / 2; o > 0; o >>= 1) {
+  for (int o = TR_RES_THREADS / 2; o > 0; o >>= 1) {
     if (threadIdx.x < o) {
       ra[threadIdx.x] += ra[threadIdx.x + o];
       sa[threadIdx.x] += sa[threadIdx.x + o];
@@ -1291,7 +1296,7 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
     cudaMemsetAsync(g_up, 0, sizeof(float) * (size_t)K, s);
   }
   // 6. cost of this forward, then Adam on every parameter
-  tr_result_kernel<<<1, TB, 0, s>>>((double*)(W + pl.o_rate), pl.arm_ctas * (TA_THREADS / 32), (double*)(W + pl.o_sse),
+  tr_result_kernel<<<1, TR_RES_THREADS, 0, s>>>((double*)(W + pl.o_rate), pl.arm_ctas * (TA_THREADS / 32), (double*)(W + pl.o_sse),
                                     n_sse, 1.0 / (3.0 * (double)P), d.lambda / (double)P, result);
   launches++;
   if (opt) {
