@@ -697,10 +697,9 @@ __global__ void __launch_bounds__(TS_THREADS)
                          const float* __restrict__ us0, const float* __restrict__ gh, float* __restrict__ gdense,
                          float* __restrict__ wpart, int n_w) {
   using LY = TrSyn1x1Layout<L, CH>;
-  constexpr int VEC = LY::VEC, NCHUNK = 4, MC = TS_THREADS / NCHUNK;
+  constexpr int VEC = LY::VEC;
   extern __shared__ __align__(16) float ssm[];
   float* vec = ssm + threadIdx.x * VEC;
-  float* spart = ssm + TS_THREADS * VEC;  // [NCHUNK][NW]
   const int64_t p = blockIdx.x * (int64_t)TS_THREADS + threadIdx.x;
   for (int v = 0; v < VEC; v++) vec[v] = 0.0f;
   if (p < d.P) {
@@ -740,53 +739,119 @@ __global__ void __launch_bounds__(TS_THREADS)
     for (int i = 0; i < L; i++) gdense[(int64_t)i * d.P + p] = gd[i];
   }
   __syncthreads();
-  for (int item = threadIdx.x; item < (LY::T0 + LY::T1) * NCHUNK; item += TS_THREADS) {
-    const int tile = item / NCHUNK, ch = item - tile * NCHUNK;
-    const bool first = tile < LY::T0;
-    int roff, coff, tr, tc;
-    if (first) {  // rows d1[4 tr ..], cols [dense, 1][4 tc ..]
-      const int tcols = LY::r4(L + 1) / 4;
-      tr = tile / tcols;
-      tc = tile - tr * tcols;
-      roff = LY::D1 + 4 * tr;
-      coff = LY::DN + 4 * tc;
-    } else {      // rows d2[0..3], cols [relu(u1), 1][4 tc ..]
-      tr = 0;
-      tc = tile - LY::T0;
-      roff = LY::D2;
-      coff = LY::V1 + 4 * tc;
-    }
-    float acc[4][4] = {};
-#pragma unroll 4
-    for (int m = ch * MC; m < ch * MC + MC; m++) {
-      const float4 rr = *reinterpret_cast<const float4*>(ssm + m * VEC + roff);
-      const float4 cc = *reinterpret_cast<const float4*>(ssm + m * VEC + coff);
-      const float rv[4] = {rr.x, rr.y, rr.z, rr.w}, cv[4] = {cc.x, cc.y, cc.z, cc.w};
+  // Weight gradients over the CTA's pixels as two small split-K products,
+  // G0 = D1^T [CH x P] . [dense, 1] [P x NC0] (dA0 | da0) and
+  // G1 = D2^T [4 x P] . [relu(u1), 1] [P x 8 T1] (dA1 | da1): warps 0-1 take
+  // G0's 8 x NC0 tiles, warps 2-3 G1's 4 x 8 tiles, each over one K-chunk of
+  // pixels, FFMA2 over column pairs with the row value a register broadcast
+  // (16 floats read per 64 MACs: the 4 x 4 tiles read 8 per 16 and were
+  // shared-memory bound); chunk partials then go through shared memory (over
+  // the records) and are summed in a fixed order (deterministic).
+  constexpr int NC0 = LY::r4(L + 1);                        // G0 columns (dense + bias, padded)
+  constexpr int T0n = CH / 8, T1n = (LY::r4(CH + 1) + 7) / 8;  // tiles
+  constexpr int K0 = (64 / T0n) < 32 ? (64 / T0n) : 32, K1 = (64 / T1n) < 32 ? (64 / T1n) : 32;  // K-chunks
+  constexpr int PX0 = (TS_THREADS + K0 - 1) / K0, PX1 = (TS_THREADS + K1 - 1) / K1;  // pixels per chunk
+  constexpr int G0F = CH * NC0, G1W = 8 * T1n, G1F = 4 * G1W;   // floats per chunk partial
+  static_assert(CH % 8 == 0 && (NC0 == 4 || NC0 == 8), "tile shapes");
+  static_assert(K0 * G0F + K1 * G1F <= TS_THREADS * VEC, "partials fit over the records");
+  const int t = threadIdx.x;
+  uint64_t acc0[8][NC0 / 2];
+  uint64_t acc1[4][4];
+  int tile = -1, kc = 0;
+  if (t < 64) {
+    if (t < T0n * K0) {
+      tile = t / K0;
+      kc = t - tile * K0;
 #pragma unroll
-      for (int a = 0; a < 4; a++)
+      for (int r = 0; r < 8; r++)
 #pragma unroll
-        for (int b = 0; b < 4; b++) acc[a][b] = fmaf(rv[a], cv[b], acc[a][b]);
-    }
-    float* sp = spart + ch * LY::NW;
+        for (int c = 0; c < NC0 / 2; c++) acc0[r][c] = 0ull;
+      const int m1 = (kc + 1) * PX0 < TS_THREADS ? (kc + 1) * PX0 : TS_THREADS;
+      for (int m = kc * PX0; m < m1; m++) {
+        const float* v = ssm + m * VEC;
+        const float4 d0 = *reinterpret_cast<const float4*>(v + LY::D1 + 8 * tile);
+        const float4 d1 = *reinterpret_cast<const float4*>(v + LY::D1 + 8 * tile + 4);
+        const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+        uint64_t z[NC0 / 2];
 #pragma unroll
-    for (int a = 0; a < 4; a++)
+        for (int c4 = 0; c4 < NC0 / 4; c4++) {
+          const ulonglong2 zz = *reinterpret_cast<const ulonglong2*>(v + LY::DN + 4 * c4);
+          z[2 * c4] = zz.x;
+          z[2 * c4 + 1] = zz.y;
+        }
 #pragma unroll
-      for (int b = 0; b < 4; b++) {
-        const int row = 4 * tr + a, col = 4 * tc + b;
-        if (first) {
-          if (col < L) sp[row * L + col] = acc[a][b];           // A0[n][i]
-          else if (col == L) sp[CH * L + row] = acc[a][b];      // a0[n]
-        } else if (row < 3) {
-          if (col < CH) sp[CH * L + CH + row * CH + col] = acc[a][b];   // A1[c][n]
-          else if (col == CH) sp[CH * L + CH + 3 * CH + row] = acc[a][b];  // a1[c]
+        for (int r = 0; r < 8; r++) {
+          const uint64_t d2 = f2pack(dv[r], dv[r]);
+#pragma unroll
+          for (int c = 0; c < NC0 / 2; c++) acc0[r][c] = ffma2(d2, z[c], acc0[r][c]);
         }
       }
+    }
+  } else {
+    const int u = t - 64;
+    if (u < T1n * K1) {
+      tile = u / K1;
+      kc = u - tile * K1;
+#pragma unroll
+      for (int r = 0; r < 4; r++)
+#pragma unroll
+        for (int c = 0; c < 4; c++) acc1[r][c] = 0ull;
+      const int m1 = (kc + 1) * PX1 < TS_THREADS ? (kc + 1) * PX1 : TS_THREADS;
+      for (int m = kc * PX1; m < m1; m++) {
+        const float* v = ssm + m * VEC;
+        const float4 dd = *reinterpret_cast<const float4*>(v + LY::D2);
+        const float dv[4] = {dd.x, dd.y, dd.z, dd.w};
+        const ulonglong2 za = *reinterpret_cast<const ulonglong2*>(v + LY::V1 + 8 * tile);
+        const ulonglong2 zb = *reinterpret_cast<const ulonglong2*>(v + LY::V1 + 8 * tile + 4);
+        const uint64_t z[4] = {za.x, za.y, zb.x, zb.y};
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+          const uint64_t d2 = f2pack(dv[r], dv[r]);
+#pragma unroll
+          for (int c = 0; c < 4; c++) acc1[r][c] = ffma2(d2, z[c], acc1[r][c]);
+        }
+      }
+    }
+  }
+  __syncthreads();  // every record read: the partials go over them
+  float* P0 = ssm;              // [K0][CH][NC0]
+  float* P1 = ssm + K0 * G0F;   // [K1][4][G1W]
+  if (tile >= 0) {
+    if (t < 64) {
+#pragma unroll
+      for (int r = 0; r < 8; r++)
+#pragma unroll
+        for (int c = 0; c < NC0 / 2; c++) {
+          const float2 x = f2unpack(acc0[r][c]);
+          *reinterpret_cast<float2*>(P0 + kc * G0F + (8 * tile + r) * NC0 + 2 * c) = x;
+        }
+    } else {
+#pragma unroll
+      for (int r = 0; r < 4; r++)
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+          const float2 x = f2unpack(acc1[r][c]);
+          *reinterpret_cast<float2*>(P1 + kc * G1F + r * G1W + 8 * tile + 2 * c) = x;
+        }
+    }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < n_w; e += TS_THREADS) {
+  for (int e = t; e < n_w; e += TS_THREADS) {
+    const float* src;
+    int stride, nk;
+    if (e < CH * L) {  // A0[n][i]
+      const int n = e / L, i = e - n * L;
+      src = P0 + n * NC0 + i, stride = G0F, nk = K0;
+    } else if (e < CH * L + CH) {  // a0[n]: the bias column
+      src = P0 + (e - CH * L) * NC0 + L, stride = G0F, nk = K0;
+    } else if (e < CH * L + CH + 3 * CH) {  // A1[c][n]
+      const int q = e - CH * L - CH, c = q / CH, n = q - c * CH;
+      src = P1 + c * G1W + n, stride = G1F, nk = K1;
+    } else {  // a1[c]: the bias column
+      src = P1 + (e - CH * L - CH - 3 * CH) * G1W + CH, stride = G1F, nk = K1;
+    }
     float v = 0.0f;
-#pragma unroll
-    for (int k = 0; k < NCHUNK; k++) v += spart[k * LY::NW + e];
+    for (int k = 0; k < nk; k++) v += src[k * stride];
     wpart[(int64_t)blockIdx.x * n_w + e] = v;
   }
 }
@@ -1254,7 +1319,7 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
   }
   {
     const int n_w = L * CH + CH + 3 * CH + 3;
-    const size_t smem = sizeof(float) * ((size_t)TS_THREADS * se->vec + 4 * (size_t)n_w);
+    const size_t smem = sizeof(float) * (size_t)TS_THREADS * se->vec;  // records, then the chunk partials over them
     se->bwd((int)pl.s_blocks, TS_THREADS, smem, s, sd, dense, u1, us, gh, F(pl.o_gdense), F(pl.o_spart), n_w);
     launches++;
     launches += reduce_partials(F(pl.o_spart), pl.s_blocks, n_w, n_w, g_syn, (double*)(W + pl.o_grad_tmp), s);
