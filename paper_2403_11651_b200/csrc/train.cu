@@ -583,36 +583,56 @@ __global__ void tr_loss_kernel(TrainSynDims d, const float* __restrict__ xh, con
 // hin staged in shared memory; persistent CTAs accumulate dG in registers over
 // their tiles and reduce once.
 constexpr int CT_Y = 8, CT_X = 32;
+// 4-byte global -> shared copy; src_bytes = 0 writes a zero (no read)
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(src_bytes)
+               : "memory");
+}
 __global__ void __launch_bounds__(CT_Y * CT_X)
     tr_conv_bwd_kernel(TrainSynDims d, int r, const float* __restrict__ hin, const float* __restrict__ us,
                        const float* __restrict__ gh, float* __restrict__ gin, float* __restrict__ gpart) {
-  constexpr int SY = CT_Y + 2, SX = CT_X + 2;
-  __shared__ float sg[3][SY][SX], sh[3][SY][SX];
-  __shared__ float red[84][CT_Y * CT_X / 32];
+  constexpr int SY = CT_Y + 2, SX = CT_X + 2, SN = 3 * SY * SX, NT = CT_Y * CT_X;
+  // the persistent CTA's tiles are double-buffered: the raw gh / us / hin
+  // windows of tile n+1 stream in (cp.async) while tile n computes
+  __shared__ float rg[2][SN], ru[2][SN], rh[2][SN];
+  __shared__ float sg[3][SY][SX];
+  __shared__ float red[84][NT / 32];
   const int oG = d.oG + 84 * r;
   const bool relu = r < d.R - 1;
   const int tiles_x = (d.W + CT_X - 1) / CT_X, n_tiles = tiles_x * ((d.H + CT_Y - 1) / CT_Y);
   const int ty = threadIdx.x / CT_X, tx = threadIdx.x - ty * CT_X;
+  auto issue = [&](int tile, int buf) {
+    const int Y0 = (tile / tiles_x) * CT_Y, X0 = (tile % tiles_x) * CT_X;
+    for (int k = threadIdx.x; k < SN; k += NT) {
+      const int c = k / (SY * SX), rem = k - c * (SY * SX), yy = rem / SX, xx = rem - yy * SX;
+      const int y = Y0 + yy - 1, x = X0 + xx - 1;
+      const bool in = y >= 0 && y < d.H && x >= 0 && x < d.W;  // gpre exists only in the image
+      const int64_t q = c * d.P + (int64_t)clampi(y, 0, d.H - 1) * d.W + clampi(x, 0, d.W - 1);
+      cp_async4(&rg[buf][k], gh + q, in ? 4 : 0);
+      if (relu) cp_async4(&ru[buf][k], us + q, in ? 4 : 0);
+      cp_async4(&rh[buf][k], hin + q, 4);  // replicate padding
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
   float dG[84];
 #pragma unroll
   for (int e = 0; e < 84; e++) dG[e] = 0.0f;
-  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+  int buf = 0;
+  if ((int)blockIdx.x < n_tiles) issue(blockIdx.x, 0);
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, buf ^= 1) {
     const int Y0 = (tile / tiles_x) * CT_Y, X0 = (tile % tiles_x) * CT_X;
-    __syncthreads();  // previous tile's readers are done
-    for (int k = threadIdx.x; k < 3 * SY * SX; k += CT_Y * CT_X) {
-      const int c = k / (SY * SX), rem = k - c * (SY * SX), yy = rem / SX, xx = rem - yy * SX;
-      const int y = Y0 + yy - 1, x = X0 + xx - 1;
-      const bool in = y >= 0 && y < d.H && x >= 0 && x < d.W;
-      const int64_t q = (int64_t)clampi(y, 0, d.H - 1) * d.W + clampi(x, 0, d.W - 1);
-      float g = 0.0f;  // gpre exists only at in-image positions
-      if (in) {
-        g = gh[c * d.P + q];
-        if (relu && !(us[c * d.P + q] > 0.0f)) g = 0.0f;
-      }
-      sg[c][yy][xx] = g;
-      sh[c][yy][xx] = hin[c * d.P + q];  // replicate padding
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // this tile's window landed; the previous tile's readers are done
+    if (tile + (int)gridDim.x < n_tiles) issue(tile + gridDim.x, buf ^ 1);
+    for (int k = threadIdx.x; k < SN; k += NT) {
+      float g = rg[buf][k];
+      if (relu && !(ru[buf][k] > 0.0f)) g = 0.0f;
+      (&sg[0][0][0])[k] = g;
     }
     __syncthreads();
+    const float* sh = rh[buf];
+#define SH(ci, yy, xx) sh[((ci) * SY + (yy)) * SX + (xx)]
     const int y = Y0 + ty, x = X0 + tx;
     if (y < d.H && x < d.W) {
       float gp[3];
@@ -628,8 +648,9 @@ __global__ void __launch_bounds__(CT_Y * CT_X)
 #pragma unroll
             for (int kx = 0; kx < 3; kx++)
               dG[((co * 3 + ci) * 3 + ky) * 3 + kx] =
-                  fmaf(gp[co], sh[ci][ty + ky][tx + kx], dG[((co * 3 + ci) * 3 + ky) * 3 + kx]);
+                  fmaf(gp[co], SH(ci, ty + ky, tx + kx), dG[((co * 3 + ci) * 3 + ky) * 3 + kx]);
       }
+#undef SH
       const bool interior = y >= 1 && y <= d.H - 2 && x >= 1 && x <= d.W - 2;
 #pragma unroll
       for (int ci = 0; ci < 3; ci++) {
