@@ -82,11 +82,20 @@ struct LevelGeom {
 // ARM tiling: one CTA = 8 rows x 64 latents of one grid; warp w owns row w,
 // lane t the latents at columns t and t + 32 (two latents per thread, so every
 // uniform weight load feeds two FFMA2).
-constexpr int ARM_LPT = 2;                 // latents per thread
+#ifndef CCRD_ARM_LPT  // experiment knobs (tools/ variants); the defaults are the measured best
+#define CCRD_ARM_LPT 2
+#endif
+#ifndef CCRD_ARM_TY
+#define CCRD_ARM_TY 8
+#endif
+#ifndef CCRD_ARM_CPS
+#define CCRD_ARM_CPS 2
+#endif
+constexpr int ARM_LPT = CCRD_ARM_LPT;      // latents per thread
 constexpr int ARM_TX = 32 * ARM_LPT;
-constexpr int ARM_TY = 8;
+constexpr int ARM_TY = CCRD_ARM_TY;
 constexpr int ARM_THREADS = 32 * ARM_TY;
-constexpr int ARM_CTAS_PER_SM = 2;
+constexpr int ARM_CTAS_PER_SM = CCRD_ARM_CPS;
 constexpr int ARM_HALO_TOP = 3;  // dy >= -3
 constexpr int ARM_HALO_X = 4;    // |dx| <= 4
 constexpr int ARM_SW = ARM_TX + 2 * ARM_HALO_X;
