@@ -472,7 +472,8 @@ static bool concurrent_streams() {
 static int forward_batch(const cc_model_desc& d, const cc_strip* win, const int16_t* const* lat,
                          const float* const* arm_w, const float* const* up_w, const float* const* syn_w,
                          const float* const* image, float* const* x_hat, char* slices, size_t per, int n,
-                         cudaStream_t s, bool overlap, bool join = true) {
+                         cudaStream_t s, bool overlap, bool join = true, bool fork = true,
+                         const cudaEvent_t* arm_wait = nullptr) {
   PyrGeom pg;
   pyr_geom(d, win, pg);
   const int n_arm = n_arm_partials(d, win);
@@ -518,8 +519,10 @@ static int forward_batch(const cc_model_desc& d, const cc_strip* win, const int1
     // the other's gaps.  Joined before the caller's next work on `s`.
     SideStream* side = nullptr;
     if ((rc = side_stream(&side))) return rc;
-    cudaEventRecord(side->fork, s);
-    cudaStreamWaitEvent(side->s, side->fork, 0);
+    if (fork) {  // else the caller has ordered the side stream after this batch's inputs
+      cudaEventRecord(side->fork, s);
+      cudaStreamWaitEvent(side->s, side->fork, 0);
+    }
     if ((rc = pyr_many(d, win, imgs, n, side->s))) return rc;
     for (int i = 0; i < n; i++) {
       char* sl = slices + per * (size_t)i;
@@ -529,8 +532,10 @@ static int forward_batch(const cc_model_desc& d, const cc_strip* win, const int1
         return rc;
     }
     cudaEventRecord(side->join, side->s);
-    for (int i = 0; i < n; i++)
+    for (int i = 0; i < n; i++) {
+      if (arm_wait) cudaStreamWaitEvent(s, arm_wait[i], 0);
       if ((rc = arm_one(d, win, lat[i], arm_w[i], (double*)(slices + per * (size_t)i), s))) return rc;
+    }
     if (join) cudaStreamWaitEvent(s, side->join, 0);  // else the caller orders on the side stream
     return CC_OK;
   }
@@ -691,6 +696,7 @@ struct HostPool {
   cudaStream_t cs = nullptr, ds = nullptr;
   cudaEvent_t copied[HOST_SLOTS_MAX], computed[HOST_SLOTS_MAX], computed_side[HOST_SLOTS_MAX],
       read_back[HOST_SLOTS_MAX];
+  cudaEvent_t img_copied[HOST_SLOTS_MAX * HOST_CHUNK_MAX];  // per image: its ARM starts once its own inputs land
   int device = -1;
 };
 static thread_local HostPool g_host;
@@ -712,6 +718,9 @@ static int host_pool(HostPool** out) {
           cudaEventCreateWithFlags(&g_host.computed[k], cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreateWithFlags(&g_host.computed_side[k], cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreateWithFlags(&g_host.read_back[k], cudaEventDisableTiming) != cudaSuccess)
+        return cuda_check("event create");
+    for (int k = 0; k < HOST_SLOTS_MAX * HOST_CHUNK_MAX; k++)
+      if (cudaEventCreateWithFlags(&g_host.img_copied[k], cudaEventDisableTiming) != cudaSuccess)
         return cuda_check("event create");
     g_host.device = dev;
   }
@@ -777,6 +786,7 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
   cudaEventRecord(computed[0], s);
   cudaStreamWaitEvent(cs, computed[0], 0);
   cudaStreamWaitEvent(ds, computed[0], 0);
+  if (conc) cudaStreamWaitEvent(side->s, computed[0], 0);
   for (int k = 0; k < HOST_SLOTS; k++) {
     cudaEventRecord(computed[k], s);
     cudaEventRecord(computed_side[k], s);
@@ -810,6 +820,7 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
         cudaMemcpyAsync(dlat, x.latents, lat_b, cudaMemcpyHostToDevice, cs);
       }
       if (x.image) cudaMemcpyAsync(dimg, x.image, img_b, cudaMemcpyHostToDevice, cs);
+      cudaEventRecord(hp->img_copied[k * HOST_CHUNK_MAX + j], cs);
       l1[j] = dlat;
       a1[j] = x.arm_w;
       u1[j] = x.up_w;
@@ -820,9 +831,14 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
     }
     if (rc) break;
     cudaEventRecord(copied[k], cs);
-    cudaStreamWaitEvent(s, copied[k], 0);
+    if (!conc) cudaStreamWaitEvent(s, copied[k], 0);  // concurrent: the ARM waits per image (below)
     cudaStreamWaitEvent(s, read_back[k], 0);  // slot k's x_hat of chunk c - HOST_SLOTS is read back
-    rc = forward_batch(d, nullptr, l1, a1, u1, s1, i1, x1, ws + per * (size_t)i0, per, m, s, conc, /*join=*/false);
+    if (conc) {  // the side stream waits for this chunk's inputs only, not for the ARM of earlier chunks
+      cudaStreamWaitEvent(side->s, copied[k], 0);
+      cudaStreamWaitEvent(side->s, read_back[k], 0);
+    }
+    rc = forward_batch(d, nullptr, l1, a1, u1, s1, i1, x1, ws + per * (size_t)i0, per, m, s, conc, /*join=*/false,
+                       /*fork=*/!conc, conc ? hp->img_copied + k * HOST_CHUNK_MAX : nullptr);
     if (rc) break;
     cudaEventRecord(computed[k], s);
     cudaEventRecord(computed_side[k], conc ? side->s : s);
