@@ -728,12 +728,16 @@ static int host_pool(HostPool** out) {
   return CC_OK;
 }
 
+// staging slots x images per slot of the host pipeline (measured best 4 x 4;
+// CCRD_HOST_SLOTS / CCRD_HOST_CHUNK override for experiments)
+static int host_slots() { return host_env("CCRD_HOST_SLOTS", 4, 2, HOST_SLOTS_MAX); }
+static int host_chunk() { return host_env("CCRD_HOST_CHUNK", 4, 1, HOST_CHUNK_MAX); }
+
 size_t cc_workspace_bytes_host(const cc_model_desc* desc, int32_t n_img) {
   if (validate(desc) != CC_OK || n_img < 1) return 0;
   return slice_bytes(*desc, nullptr) * (size_t)n_img +
          align256(sizeof(cc_rd_result) * (size_t)n_img) +
-         (size_t)host_env("CCRD_HOST_SLOTS", 3, 2, HOST_SLOTS_MAX) * host_env("CCRD_HOST_CHUNK", 4, 1, HOST_CHUNK_MAX) *
-             stage_slot_bytes(*desc);
+         (size_t)host_slots() * host_chunk() * stage_slot_bytes(*desc);
 }
 
 int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t n_img, cc_rd_result* results,
@@ -752,8 +756,8 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
   cc_rd_result* dres = (cc_rd_result*)(ws + per * (size_t)n_img);
   char* stage = ws + per * (size_t)n_img + align256(sizeof(cc_rd_result) * (size_t)n_img);
   const size_t slot = stage_slot_bytes(d);
-  const int HOST_SLOTS = host_env("CCRD_HOST_SLOTS", 3, 2, HOST_SLOTS_MAX);
-  const int HOST_CHUNK = host_env("CCRD_HOST_CHUNK", 4, 1, HOST_CHUNK_MAX);
+  const int HOST_SLOTS = host_slots();
+  const int HOST_CHUNK = host_chunk();
   int64_t n_lat = 0;
   LevelGeom lg;
   level_dims(d, lg, &n_lat);
@@ -819,8 +823,10 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
       } else {
         cudaMemcpyAsync(dlat, x.latents, lat_b, cudaMemcpyHostToDevice, cs);
       }
-      if (x.image) cudaMemcpyAsync(dimg, x.image, img_b, cudaMemcpyHostToDevice, cs);
+      // the ARM needs only the latents: its event goes before the image (70 % of
+      // the bytes; uploading all of a chunk's latents first measured slower)
       cudaEventRecord(hp->img_copied[k * HOST_CHUNK_MAX + j], cs);
+      if (x.image) cudaMemcpyAsync(dimg, x.image, img_b, cudaMemcpyHostToDevice, cs);
       l1[j] = dlat;
       a1[j] = x.arm_w;
       u1[j] = x.up_w;
