@@ -473,7 +473,7 @@ static int forward_batch(const cc_model_desc& d, const cc_strip* win, const int1
                          const float* const* arm_w, const float* const* up_w, const float* const* syn_w,
                          const float* const* image, float* const* x_hat, char* slices, size_t per, int n,
                          cudaStream_t s, bool overlap, bool join = true, bool fork = true,
-                         const cudaEvent_t* arm_wait = nullptr) {
+                         const cudaEvent_t* arm_wait = nullptr, const cudaEvent_t* syn_wait = nullptr) {
   PyrGeom pg;
   pyr_geom(d, win, pg);
   const int n_arm = n_arm_partials(d, win);
@@ -523,10 +523,12 @@ static int forward_batch(const cc_model_desc& d, const cc_strip* win, const int1
       cudaEventRecord(side->fork, s);
       cudaStreamWaitEvent(side->s, side->fork, 0);
     }
+    if (arm_wait) cudaStreamWaitEvent(side->s, arm_wait[n - 1], 0);  // every latent of the batch landed
     if ((rc = pyr_many(d, win, imgs, n, side->s))) return rc;
     for (int i = 0; i < n; i++) {
       char* sl = slices + per * (size_t)i;
       const float* s1 = slice_pyr(d, win, sl) + pg.s_off[1];
+      if (syn_wait) cudaStreamWaitEvent(side->s, syn_wait[i], 0);  // image i landed
       if ((rc = syn_one(d, win, lat[i], s1, up_w[i], syn_w[i], image[i], x_hat[i], nullptr, (double*)sl + n_arm,
                         side->s)))
         return rc;
@@ -696,7 +698,8 @@ struct HostPool {
   cudaStream_t cs = nullptr, ds = nullptr;
   cudaEvent_t copied[HOST_SLOTS_MAX], computed[HOST_SLOTS_MAX], computed_side[HOST_SLOTS_MAX],
       read_back[HOST_SLOTS_MAX];
-  cudaEvent_t img_copied[HOST_SLOTS_MAX * HOST_CHUNK_MAX];  // per image: its ARM starts once its own inputs land
+  cudaEvent_t img_copied[HOST_SLOTS_MAX * HOST_CHUNK_MAX];  // per image: latents landed (its ARM may start)
+  cudaEvent_t img_done[HOST_SLOTS_MAX * HOST_CHUNK_MAX];    // per image: image landed (its synthesis may start)
   int device = -1;
 };
 static thread_local HostPool g_host;
@@ -720,7 +723,8 @@ static int host_pool(HostPool** out) {
           cudaEventCreateWithFlags(&g_host.read_back[k], cudaEventDisableTiming) != cudaSuccess)
         return cuda_check("event create");
     for (int k = 0; k < HOST_SLOTS_MAX * HOST_CHUNK_MAX; k++)
-      if (cudaEventCreateWithFlags(&g_host.img_copied[k], cudaEventDisableTiming) != cudaSuccess)
+      if (cudaEventCreateWithFlags(&g_host.img_copied[k], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&g_host.img_done[k], cudaEventDisableTiming) != cudaSuccess)
         return cuda_check("event create");
     g_host.device = dev;
   }
@@ -827,6 +831,7 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
       // the bytes; uploading all of a chunk's latents first measured slower)
       cudaEventRecord(hp->img_copied[k * HOST_CHUNK_MAX + j], cs);
       if (x.image) cudaMemcpyAsync(dimg, x.image, img_b, cudaMemcpyHostToDevice, cs);
+      cudaEventRecord(hp->img_done[k * HOST_CHUNK_MAX + j], cs);
       l1[j] = dlat;
       a1[j] = x.arm_w;
       u1[j] = x.up_w;
@@ -839,12 +844,11 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
     cudaEventRecord(copied[k], cs);
     if (!conc) cudaStreamWaitEvent(s, copied[k], 0);  // concurrent: the ARM waits per image (below)
     cudaStreamWaitEvent(s, read_back[k], 0);  // slot k's x_hat of chunk c - HOST_SLOTS is read back
-    if (conc) {  // the side stream waits for this chunk's inputs only, not for the ARM of earlier chunks
-      cudaStreamWaitEvent(side->s, copied[k], 0);
+    if (conc)  // the side stream waits for this chunk's own inputs (per image, below), not for the ARM stream
       cudaStreamWaitEvent(side->s, read_back[k], 0);
-    }
     rc = forward_batch(d, nullptr, l1, a1, u1, s1, i1, x1, ws + per * (size_t)i0, per, m, s, conc, /*join=*/false,
-                       /*fork=*/!conc, conc ? hp->img_copied + k * HOST_CHUNK_MAX : nullptr);
+                       /*fork=*/!conc, conc ? hp->img_copied + k * HOST_CHUNK_MAX : nullptr,
+                       conc ? hp->img_done + k * HOST_CHUNK_MAX : nullptr);
     if (rc) break;
     cudaEventRecord(computed[k], s);
     cudaEventRecord(computed_side[k], conc ? side->s : s);
