@@ -1155,6 +1155,114 @@ static int blocks_for(int64_t n) { return (int)((n + TB - 1) / TB); }
 
 #define TCONV_BWD(K) ((K) == 8 ? tr_tconv_bwd_kernel<8> : (K) == 4 ? tr_tconv_bwd_kernel<4> : tr_tconv_bwd_kernel<0>)
 
+// The small levels' steps of the upsampling chain (forward or adjoint) in ONE
+// single-CTA launch: each of them is a few thousand elements, so as separate
+// launches they cost launch latency, not work.  Passes run in order with a
+// CTA barrier between them (a pass reads the previous one's output).
+constexpr int TCH_THREADS = 1024;
+constexpr int TCH_MAX_PASSES = 4 * CC_MAX_LEVELS;
+struct TrChainPass {
+  int32_t kind;  // 0 tconv forward, 1 tconv adjoint (+ tap partial rows), 2 add dst = a + b, 3 copy dst = a
+  int32_t lines, n, m, nch;
+  int64_t g_ls, g_es, o_ls, o_es, g_cs, o_cs;
+  const float* a;  // kind 0/1: g (input), 2/3: a
+  const float* b;  // kind 1: gout; 2: b
+  float* dst;      // kind 0: out, 1: gg, 2/3: dst
+  float* kpart;    // kind 1: nch rows of K
+  int64_t count;   // kind 2/3: elements
+};
+struct TrChain {
+  int32_t np, K, koff;
+  TrChainPass p[TCH_MAX_PASSES];
+};
+template <int KT>
+__global__ void __launch_bounds__(TCH_THREADS) tr_chain_kernel(const __grid_constant__ TrChain c) {
+  __shared__ float red[8][TCH_THREADS / 32];
+  const int K = KT;
+  for (int pi = 0; pi < c.np; pi++) {
+    const TrChainPass& P = c.p[pi];
+    if (P.kind >= 2) {
+      for (int64_t e = threadIdx.x; e < P.count; e += TCH_THREADS)
+        P.dst[e] = P.kind == 2 ? P.a[e] + P.b[e] : P.a[e];
+    } else if (P.kind == 0) {
+      const int64_t per = (int64_t)P.lines * P.m;
+      for (int64_t e = threadIdx.x; e < per * P.nch; e += TCH_THREADS) {
+        const int ch = (int)(e / per);
+        const int64_t idx = e - ch * per;
+        const float* g = P.a + ch * P.g_cs;
+        int line, o;
+        if (P.g_es == 1) {
+          line = (int)(idx / P.m);
+          o = (int)(idx - (int64_t)line * P.m);
+        } else {
+          o = (int)(idx / P.lines);
+          line = (int)(idx - (int64_t)o * P.lines);
+        }
+        const int q = o >> 1, r = o & 1;
+        float acc = 0.0f;
+#pragma unroll
+        for (int t = 0; t < K / 2; t++)
+          acc = fmaf(c_tw[c.koff + 2 * t + 1 - r], g[line * P.g_ls + (int64_t)clampi(q + r + K / 4 - 1 - t, 0, P.n - 1) * P.g_es], acc);
+        P.dst[ch * P.o_cs + line * P.o_ls + (int64_t)o * P.o_es] = acc;
+      }
+    } else {  // adjoint, one channel at a time (one tap-partial row each)
+      for (int ch = 0; ch < P.nch; ch++) {
+        const float* g = P.a + ch * P.g_cs;
+        const float* gout = P.b + ch * P.o_cs;
+        float* gg = P.dst + ch * P.g_cs;
+        float dk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int64_t idx = threadIdx.x; idx < (int64_t)P.lines * P.n; idx += TCH_THREADS) {
+          int line, s2;
+          if (P.g_es == 1) {
+            line = (int)(idx / P.n);
+            s2 = (int)(idx - (int64_t)line * P.n);
+          } else {
+            s2 = (int)(idx / P.lines);
+            line = (int)(idx - (int64_t)s2 * P.lines);
+          }
+          const int E = K / 4, PP = K / 2 - 1 + 2 * E;
+          const float xs = g[line * P.g_ls + (int64_t)s2 * P.g_es];
+          const int i_lo = (s2 == 0) ? 0 : s2 + E, i_hi = (s2 == P.n - 1) ? P.n - 1 + 2 * E : s2 + E;
+          float acc = 0.0f;
+          for (int i = i_lo; i <= i_hi; i++)
+#pragma unroll
+            for (int j = 0; j < K; j++) {
+              const int o = 2 * i + j - PP;
+              if (o >= 0 && o < P.m) {
+                const float go = gout[line * P.o_ls + (int64_t)o * P.o_es];
+                acc = fmaf(c_tw[c.koff + j], go, acc);
+                dk[j] = fmaf(xs, go, dk[j]);
+              }
+            }
+          gg[line * P.g_ls + (int64_t)s2 * P.g_es] = acc;
+        }
+#pragma unroll
+        for (int j = 0; j < K; j++) {
+          float v = dk[j];
+#pragma unroll
+          for (int o2 = 16; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o2);
+          if ((threadIdx.x & 31) == 0) red[j][threadIdx.x >> 5] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < K) {
+          float v = 0.0f;
+          for (int w2 = 0; w2 < TCH_THREADS / 32; w2++) v += red[threadIdx.x][w2];
+          P.kpart[(int64_t)ch * K + threadIdx.x] = v;
+        }
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+  }
+}
+// a level step goes to the chain when its largest pass is this small
+constexpr int64_t TCH_SMALL = 8192;
+static void launch_chain(const TrChain& c, cudaStream_t s) {
+  if (c.np == 0) return;
+  if (c.K == 8) tr_chain_kernel<8><<<1, TCH_THREADS, 0, s>>>(c);
+  else tr_chain_kernel<4><<<1, TCH_THREADS, 0, s>>>(c);
+}
+
 // ---------------------------------------------------------------- constant-bank ownership
 struct TrBank {
   cudaStream_t owner = nullptr;
@@ -1294,13 +1402,41 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
   float* dense = F(pl.o_dense);
   float* chain = F(pl.o_chain);
   auto Tj = [&](int j) { return j == 0 ? dense : chain + pl.chain_off[j]; };
-  for (int j = 0; j < L; j++)
-    cudaMemcpyAsync(Tj(j), F(pl.o_yq) + lv.off[j], sizeof(float) * (size_t)lv.h[j] * lv.w[j], cudaMemcpyDeviceToDevice,
-                    s);
+  // small levels (the coarse end of the chain) go to one single-CTA launch
+  const bool chain_ok = (K == 8 || K == 4);
+  auto small = [&](int j) { return chain_ok && (int64_t)lv.h[j] * lv.w[j] * (L - 1 - j) <= TCH_SMALL; };
+  TrChain fc;
+  fc.np = 0, fc.K = K, fc.koff = koff;
+  for (int j = 0; j < L; j++) {
+    if (j >= 1 && small(j - 1)) {  // T_j[0] = y_hat_j feeds only small steps: copy inside the chain
+      TrChainPass& c = fc.p[fc.np++];
+      c = TrChainPass{};
+      c.kind = 3, c.a = F(pl.o_yq) + lv.off[j], c.dst = Tj(j), c.count = (int64_t)lv.h[j] * lv.w[j];
+    } else {
+      cudaMemcpyAsync(Tj(j), F(pl.o_yq) + lv.off[j], sizeof(float) * (size_t)lv.h[j] * lv.w[j],
+                      cudaMemcpyDeviceToDevice, s);
+    }
+  }
   for (int j = L - 2; j >= 0; j--) {
     const int nch = L - 1 - j;
     const int hs = lv.h[j + 1], ws2 = lv.w[j + 1], wd = lv.w[j], hd = lv.h[j];
     float* mid = chain + pl.mid_off[j];
+    if (small(j)) {
+      TrChainPass& x = fc.p[fc.np++];
+      x = TrChainPass{};
+      x.kind = 0, x.a = Tj(j + 1), x.dst = mid, x.lines = hs, x.n = ws2, x.m = wd, x.nch = nch;
+      x.g_ls = ws2, x.g_es = 1, x.o_ls = wd, x.o_es = 1, x.g_cs = (int64_t)hs * ws2, x.o_cs = (int64_t)hs * wd;
+      TrChainPass& y = fc.p[fc.np++];
+      y = TrChainPass{};
+      y.kind = 0, y.a = mid, y.dst = Tj(j) + (int64_t)hd * wd, y.lines = wd, y.n = hs, y.m = hd, y.nch = nch;
+      y.g_ls = 1, y.g_es = wd, y.o_ls = 1, y.o_es = wd, y.g_cs = (int64_t)hs * wd, y.o_cs = (int64_t)hd * wd;
+      if (j == 0 || !small(j - 1)) {
+        launch_chain(fc, s);
+        launches++;
+        fc.np = 0;
+      }
+      continue;
+    }
     // x pass: per channel, lines = rows (hs), n = ws2 -> m = wd
     tr_tconv_fwd_kernel<<<dim3(blocks_for((int64_t)hs * wd), nch), TB, 0, s>>>(
         Tj(j + 1), mid, hs, ws2, wd, ws2, 1, wd, 1, K, koff, (int64_t)hs * ws2, (int64_t)hs * wd);
@@ -1351,16 +1487,41 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
   float* kpart = F(pl.o_kpart);
   int64_t krow = 0;
   const float* gT = gdense;
+  TrChain bc;  // the small levels' adjoint steps (from the first small one to the coarsest level)
+  bc.np = 0, bc.K = K, bc.koff = koff;
   for (int j = 0; j < L; j++) {
-    tr_proxy_kernel<<<blocks_for((int64_t)lv.h[j] * lv.w[j]), TB, 0, s>>>(g_lat + lv.off[j], gT, g_lat + lv.off[j],
-                                                                        (int64_t)lv.h[j] * lv.w[j]);
-    launches++;
+    const bool sm = L >= 2 && small(j < L - 1 ? j : L - 2);
+    if (sm) {
+      TrChainPass& a = bc.p[bc.np++];
+      a = TrChainPass{};
+      a.kind = 2, a.a = g_lat + lv.off[j], a.b = gT, a.dst = g_lat + lv.off[j], a.count = (int64_t)lv.h[j] * lv.w[j];
+    } else {
+      tr_proxy_kernel<<<blocks_for((int64_t)lv.h[j] * lv.w[j]), TB, 0, s>>>(g_lat + lv.off[j], gT, g_lat + lv.off[j],
+                                                                          (int64_t)lv.h[j] * lv.w[j]);
+      launches++;
+    }
     if (j + 1 >= L) break;
     const int nch = L - 1 - j;
     const int hs = lv.h[j + 1], ws2 = lv.w[j + 1], wd = lv.w[j], hd = lv.h[j];
     const float* mid = chain + pl.mid_off[j];
     float* gmid = F(pl.o_g1);
     float* gnext = (gT == F(pl.o_g0)) ? F(pl.o_g1) + (int64_t)nch * hs * wd : F(pl.o_g0);  // not aliasing gT / gmid
+    if (sm) {
+      TrChainPass& y = bc.p[bc.np++];
+      y = TrChainPass{};
+      y.kind = 1, y.a = mid, y.b = gT + (int64_t)hd * wd, y.dst = gmid, y.lines = wd, y.n = hs, y.m = hd, y.nch = nch;
+      y.g_ls = 1, y.g_es = wd, y.o_ls = 1, y.o_es = wd, y.g_cs = (int64_t)hs * wd, y.o_cs = (int64_t)hd * wd;
+      y.kpart = kpart + krow * K;
+      krow += nch;
+      TrChainPass& x = bc.p[bc.np++];
+      x = TrChainPass{};
+      x.kind = 1, x.a = Tj(j + 1), x.b = gmid, x.dst = gnext, x.lines = hs, x.n = ws2, x.m = wd, x.nch = nch;
+      x.g_ls = ws2, x.g_es = 1, x.o_ls = wd, x.o_es = 1, x.g_cs = (int64_t)hs * ws2, x.o_cs = (int64_t)hs * wd;
+      x.kpart = kpart + krow * K;
+      krow += nch;
+      gT = gnext;
+      continue;
+    }
     // y adjoint: inputs mid (per channel: lines = columns wd, n = hs), outputs gT_j[1..] (m = hd)
     const int64_t b1 = blocks_for((int64_t)wd * hs) < TR_TCONV_CAP ? blocks_for((int64_t)wd * hs) : TR_TCONV_CAP;
     TCONV_BWD(K)<<<dim3((unsigned)b1, nch), TB, 0, s>>>(mid, gT + (int64_t)hd * wd, gmid, wd, hs, hd, 1, wd, 1,
@@ -1375,6 +1536,10 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
     krow += b2 * nch;
     launches += 2;
     gT = gnext;
+  }
+  if (bc.np > 0) {
+    launch_chain(bc, s);
+    launches++;
   }
   if (krow > 0) {
     launches += reduce_partials(kpart, krow, K, K, g_up, (double*)(W + pl.o_grad_tmp), s);
