@@ -524,7 +524,7 @@ __global__ void tr_syn1x1_fwd_kernel(TrainSynDims d, const float* __restrict__ d
     float a = c_tw[d.oa0 + n];
 #pragma unroll
     for (int i = 0; i < L; i++) a = fmaf(c_tw[d.oA0 + n * L + i], v[i], a);
-    u1[(int64_t)n * d.P + p] = a;
+    if (u1 != nullptr) u1[(int64_t)n * d.P + p] = a;  // (the adjoint recomputes it: 160 B/px not stored)
     const float r = fmaxf(a, 0.0f);
 #pragma unroll
     for (int c = 0; c < 3; c++) o[c] = fmaf(c_tw[d.oA1 + c * CH + n], r, o[c]);
@@ -739,11 +739,22 @@ __global__ void __launch_bounds__(TS_THREADS)
     float gd[L];
 #pragma unroll
     for (int i = 0; i < L; i++) gd[i] = 0.0f;
-    // all CH pre-activations in flight at once (a 4-deep unroll left ~10
-    // serial memory latencies per pixel)
+    // the CH pre-activations recomputed from the dense input in the forward's
+    // exact order (bias, then inputs 0 .. L-1): bit-identical, and 160 B/px of
+    // HBM traffic each way saved against storing them
     float ua[CH];
+    {
+      float v[L];
 #pragma unroll
-    for (int n = 0; n < CH; n++) ua[n] = u1[(int64_t)n * d.P + p];
+      for (int i = 0; i < L; i++) v[i] = dense[(int64_t)i * d.P + p];
+#pragma unroll
+      for (int n = 0; n < CH; n++) {
+        float a = c_tw[d.oa0 + n];
+#pragma unroll
+        for (int i = 0; i < L; i++) a = fmaf(c_tw[d.oA0 + n * L + i], v[i], a);
+        ua[n] = a;
+      }
+    }
 #pragma unroll
     for (int n = 0; n < CH; n++) {
       const float a = ua[n];
@@ -1043,7 +1054,7 @@ static void make_plan(const cc_model_desc& d, TrainPlan& pl) {
   pl.kpart_rows = kp > 0 ? kp : 1;
   pl.o_chain = take(4 * (c > 0 ? c : 1));
   pl.o_dense = take(4 * (size_t)d.L * P);
-  pl.o_u1 = take(4 * (size_t)CH * P);
+  pl.o_u1 = take(0);  // hidden pre-activations: recomputed by the 1x1 adjoint, not stored
   pl.o_us = take(4 * (size_t)(d.syn_n_res + 1) * 3 * P);
   pl.o_hs = take(4 * (size_t)(d.syn_n_res + 1) * 3 * P);
   pl.o_gh0 = take(4 * 3 * (size_t)P);
@@ -1446,12 +1457,11 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
     launches += 2;
   }
   // 4. synthesis forward, distortion, synthesis adjoint
-  float* u1 = F(pl.o_u1);
   float* us = F(pl.o_us);
   float* hsb = F(pl.o_hs);
   const TrSynEntry* se = find_tr_syn(d);
   if (!se) return -4;
-  se->fwd(blocks_for(P), TB, s, sd, dense, u1, us, hsb);
+  se->fwd(blocks_for(P), TB, s, sd, dense, nullptr, us, hsb);  // u1 is recomputed by the adjoint
   launches++;
   for (int r = 0; r < R; r++) {
     tr_conv_fwd_kernel<<<blocks_for(P), TB, 0, s>>>(sd, r, hsb + (int64_t)r * 3 * P, us + (int64_t)(r + 1) * 3 * P,
@@ -1477,7 +1487,7 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
   {
     const int n_w = L * CH + CH + 3 * CH + 3;
     const size_t smem = sizeof(float) * (size_t)TS_THREADS * se->vec;  // records, then the chunk partials over them
-    se->bwd((int)pl.s_blocks, TS_THREADS, smem, s, sd, dense, u1, us, gh, F(pl.o_gdense), F(pl.o_spart), n_w);
+    se->bwd((int)pl.s_blocks, TS_THREADS, smem, s, sd, dense, nullptr, us, gh, F(pl.o_gdense), F(pl.o_spart), n_w);
     launches++;
     launches += reduce_partials(F(pl.o_spart), pl.s_blocks, n_w, n_w, g_syn, (double*)(W + pl.o_grad_tmp), s);
   }
