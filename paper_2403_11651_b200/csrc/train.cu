@@ -246,7 +246,8 @@ __global__ void __launch_bounds__(TA_THREADS) tr_arm_kernel(const __grid_constan
     while (l + 1 < p.lv.L && q >= p.lv.off[l + 1]) l++;
     const int h = p.lv.h[l], w = p.lv.w[l];
     const int64_t t = q - p.lv.off[l];
-    const int i = (int)(t / w), j = (int)(t - (int64_t)i * w);
+    const int t32 = (int)t;  // a grid's plane is < 2^31: 32-bit division
+    const int i = t32 / w, j = t32 - i * w;
     const float* g = p.yq + p.lv.off[l];
     float z[NL][NH > C ? NH : C];  // z[k] = input of layer k
     float u[NL][NH];               // pre-activations of the hidden layers
@@ -404,7 +405,8 @@ __global__ void tr_arm_gather_kernel(TrainLevels lv, const __grid_constant__ Tra
   while (l + 1 < lv.L && q >= lv.off[l + 1]) l++;
   const int h = lv.h[l], w = lv.w[l];
   const int64_t t = q - lv.off[l];
-  const int i = (int)(t / w), j = (int)(t - (int64_t)i * w);
+  const int t32 = (int)t;  // 32-bit division
+  const int i = t32 / w, j = t32 - i * w;
   float g = gown[q];
   for (int c = 0; c < C; c++) {
     const int pi = i - cx.dy[c], pj = j - cx.dx[c];  // latent whose context c is (i, j)
@@ -426,13 +428,16 @@ __global__ void tr_tconv_fwd_kernel(const float* __restrict__ g, float* __restri
   out += blockIdx.y * o_cs;
   // consecutive threads on consecutive addresses: along the line when its
   // elements are contiguous (x pass), across lines otherwise (y pass: columns)
+  // 32-bit index math (a 64-bit division is a ~100-instruction call; the
+  // planes here are < 2^31 elements)
+  const int i32 = (int)idx;
   int line, o;
   if (g_es == 1) {
-    line = (int)(idx / m);
-    o = (int)(idx - (int64_t)line * m);
+    line = i32 / m;
+    o = i32 - line * m;
   } else {
-    o = (int)(idx / lines);
-    line = (int)(idx - (int64_t)o * lines);
+    o = i32 / lines;
+    line = i32 - o * lines;
   }
   const int q = o >> 1, r = o & 1;
   float acc = 0.0f;
@@ -459,13 +464,14 @@ __global__ void tr_tconv_bwd_kernel(const float* __restrict__ g, const float* __
   float dk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)lines * n;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    int line, s;  // coalesced mapping (see tr_tconv_fwd_kernel)
+    int line, s;  // coalesced mapping (see tr_tconv_fwd_kernel); 32-bit index math
+    const int i32 = (int)idx;
     if (g_es == 1) {
-      line = (int)(idx / n);
-      s = (int)(idx - (int64_t)line * n);
+      line = i32 / n;
+      s = i32 - line * n;
     } else {
-      s = (int)(idx / lines);
-      line = (int)(idx - (int64_t)s * lines);
+      s = i32 / lines;
+      line = i32 - s * lines;
     }
     const int E = K / 4, P = K / 2 - 1 + 2 * E;
     const float xs = g[line * g_ls + (int64_t)s * g_es];
@@ -540,7 +546,8 @@ __global__ void tr_conv_fwd_kernel(TrainSynDims d, int r, const float* __restric
                                    float* __restrict__ hout) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= d.P) return;
-  const int y = (int)(p / d.W), x = (int)(p - (int64_t)y * d.W);
+  const int p32 = (int)p;  // 32-bit division (P < 2^31)
+  const int y = p32 / d.W, x = p32 - y * d.W;
   const int oG = d.oG + 84 * r;
   for (int co = 0; co < 3; co++) {
     float a = hin[co * d.P + p] + c_tw[oG + 81 + co];
@@ -1198,16 +1205,16 @@ __global__ void __launch_bounds__(TCH_THREADS) tr_chain_kernel(const __grid_cons
     } else if (P.kind == 0) {
       const int64_t per = (int64_t)P.lines * P.m;
       for (int64_t e = threadIdx.x; e < per * P.nch; e += TCH_THREADS) {
-        const int ch = (int)(e / per);
-        const int64_t idx = e - ch * per;
+        const int ch = (int)e / (int)per;  // the small levels: 32-bit index math
+        const int idx = (int)e - ch * (int)per;
         const float* g = P.a + ch * P.g_cs;
         int line, o;
         if (P.g_es == 1) {
-          line = (int)(idx / P.m);
-          o = (int)(idx - (int64_t)line * P.m);
+          line = idx / P.m;
+          o = idx - line * P.m;
         } else {
-          o = (int)(idx / P.lines);
-          line = (int)(idx - (int64_t)o * P.lines);
+          o = idx / P.lines;
+          line = idx - o * P.lines;
         }
         const int q = o >> 1, r = o & 1;
         float acc = 0.0f;
@@ -1225,11 +1232,11 @@ __global__ void __launch_bounds__(TCH_THREADS) tr_chain_kernel(const __grid_cons
         for (int64_t idx = threadIdx.x; idx < (int64_t)P.lines * P.n; idx += TCH_THREADS) {
           int line, s2;
           if (P.g_es == 1) {
-            line = (int)(idx / P.n);
-            s2 = (int)(idx - (int64_t)line * P.n);
+            line = (int)idx / P.n;
+            s2 = (int)idx - line * P.n;
           } else {
-            s2 = (int)(idx / P.lines);
-            line = (int)(idx - (int64_t)s2 * P.lines);
+            s2 = (int)idx / P.lines;
+            line = (int)idx - s2 * P.lines;
           }
           const int E = K / 4, PP = K / 2 - 1 + 2 * E;
           const float xs = g[line * P.g_ls + (int64_t)s2 * P.g_es];
