@@ -45,11 +45,11 @@ constexpr int TR_MAX_W = 2048;  // arm + up + syn weights (floats)
 // over another stream's bank waits for that stream's last use of it).  Every
 // kernel addresses its bank through the offsets it is given (bank x size +
 // the layer offset): the loads stay uniform (LDCU c[0x3][UR + imm]).
-constexpr int TR_BANKS = 3;
+constexpr int TR_BANKS = 4;
 __constant__ float c_tw[TR_BANKS * TR_MAX_W];
 // the ARM weights again, packed for FFMA2 in the forward: per layer k, for
 // input i the pair (W[2n][i], W[2n+1][i]), then the bias pairs
-constexpr int TR_MAX_ARMP = 1536;  // float2
+constexpr int TR_MAX_ARMP = 768;  // float2 (A2300's ARM: 627 pairs)
 __constant__ float2 c_tp[TR_BANKS * TR_MAX_ARMP];
 
 __global__ void tr_pack_arm_kernel(const float* __restrict__ w, float2* __restrict__ out, int nl, int C, int NH) {
@@ -1096,13 +1096,15 @@ static void tr_arm_launch(dim3 g, int t, size_t smem, cudaStream_t s, const Trai
     cudaFuncSetAttribute(tr_arm_kernel<C, NH, NHL, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(tr_arm_kernel<C, NH, NHL, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(tr_arm_kernel<C, NH, NHL, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(tr_arm_kernel<C, NH, NHL, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     attr = true;
   }
-  static_assert(TR_BANKS == 3, "one instantiation per bank");
+  static_assert(TR_BANKS == 4, "one instantiation per bank");
   switch (p.tp0 / TR_MAX_ARMP) {
     case 0: tr_arm_kernel<C, NH, NHL, 0><<<g, t, smem, s>>>(p); break;
     case 1: tr_arm_kernel<C, NH, NHL, 1><<<g, t, smem, s>>>(p); break;
-    default: tr_arm_kernel<C, NH, NHL, 2><<<g, t, smem, s>>>(p); break;
+    case 2: tr_arm_kernel<C, NH, NHL, 2><<<g, t, smem, s>>>(p); break;
+    default: tr_arm_kernel<C, NH, NHL, 3><<<g, t, smem, s>>>(p); break;
   }
 }
 struct TrArmEntry {
@@ -1338,7 +1340,7 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
   int launches = 0;
   // weights -> constant bank (arm | up | syn), device to device
   const int64_t nw = pl.n_arm + pl.n_up + pl.n_syn;
-  if (nw > TR_MAX_W) return -2;
+  if (nw > TR_MAX_W || pl.n_arm / 2 + 2 > TR_MAX_ARMP) return -2;
   const int bank = acquire_bank(s);
   const int tw0 = bank * TR_MAX_W, tp0 = bank * TR_MAX_ARMP;
   cudaMemcpyToSymbolAsync(c_tw, par + lv.n_lat, sizeof(float) * (size_t)nw, sizeof(float) * (size_t)tw0,
