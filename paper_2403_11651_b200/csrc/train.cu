@@ -46,6 +46,10 @@ constexpr int TR_MAX_W = 2048;  // arm + up + syn weights (floats)
 // kernel addresses its bank through the offsets it is given (bank x size +
 // the layer offset): the loads stay uniform (LDCU c[0x3][UR + imm]).
 constexpr int TR_BANKS = 4;
+// bank layout: ARM weights at 0, upsampling taps at TR_UP_OFF, synthesis at
+// TR_SYN_OFF -- fixed offsets, so kernels templated on the bank read their
+// weights at compile-time constant addresses (uniform LDCU)
+constexpr int TR_UP_OFF = 1280, TR_SYN_OFF = 1344;
 __constant__ float c_tw[TR_BANKS * TR_MAX_W];
 // the ARM weights again, packed for FFMA2 in the forward: per layer k, for
 // input i the pair (W[2n][i], W[2n+1][i]), then the bias pairs
@@ -512,28 +516,30 @@ struct TrainSynDims {
   int32_t H, W, L, CH, R;
   int64_t P;
   int32_t oA0, oa0, oA1, oa1, oG;  // offsets of the synthesis blocks in c_tw
+  int32_t bank;                    // constant bank of this step
 };
 
 // 1x1 layers: u1 = A0 v + a0 (kept), h = A1 ReLU(u1) + a1 (pre kept), ReLU if R > 0
-template <int L, int CH>
+template <int L, int CH, int BANK>
 __global__ void tr_syn1x1_fwd_kernel(TrainSynDims d, const float* __restrict__ dense, float* __restrict__ u1,
                                      float* __restrict__ us0, float* __restrict__ hs0) {
+  constexpr int oA0 = BANK * TR_MAX_W + TR_SYN_OFF, oa0 = oA0 + L * CH, oA1 = oa0 + CH, oa1 = oA1 + 3 * CH;
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= d.P) return;
   float v[L], o[3];
 #pragma unroll
   for (int i = 0; i < L; i++) v[i] = dense[(int64_t)i * d.P + p];
 #pragma unroll
-  for (int c = 0; c < 3; c++) o[c] = c_tw[d.oa1 + c];
+  for (int c = 0; c < 3; c++) o[c] = c_tw[oa1 + c];
 #pragma unroll 4
   for (int n = 0; n < CH; n++) {
-    float a = c_tw[d.oa0 + n];
+    float a = c_tw[oa0 + n];
 #pragma unroll
-    for (int i = 0; i < L; i++) a = fmaf(c_tw[d.oA0 + n * L + i], v[i], a);
+    for (int i = 0; i < L; i++) a = fmaf(c_tw[oA0 + n * L + i], v[i], a);
     if (u1 != nullptr) u1[(int64_t)n * d.P + p] = a;  // (the adjoint recomputes it: 160 B/px not stored)
     const float r = fmaxf(a, 0.0f);
 #pragma unroll
-    for (int c = 0; c < 3; c++) o[c] = fmaf(c_tw[d.oA1 + c * CH + n], r, o[c]);
+    for (int c = 0; c < 3; c++) o[c] = fmaf(c_tw[oA1 + c * CH + n], r, o[c]);
   }
   for (int c = 0; c < 3; c++) {
     us0[c * d.P + p] = o[c];
@@ -719,11 +725,12 @@ struct TrSyn1x1Layout {
   static_assert(CH % 4 == 0, "hidden width multiple of 4");
 };
 
-template <int L, int CH>
+template <int L, int CH, int BANK>
 __global__ void __launch_bounds__(TS_THREADS)
     tr_syn1x1_bwd_kernel(TrainSynDims d, const float* __restrict__ dense, const float* __restrict__ u1,
                          const float* __restrict__ us0, const float* __restrict__ gh, float* __restrict__ gdense,
                          float* __restrict__ wpart, int n_w) {
+  constexpr int oA0 = BANK * TR_MAX_W + TR_SYN_OFF, oa0 = oA0 + L * CH, oA1 = oa0 + CH, oa1 = oA1 + 3 * CH;
   using LY = TrSyn1x1Layout<L, CH>;
   constexpr int VEC = LY::VEC;
   extern __shared__ __align__(16) float ssm[];
@@ -756,9 +763,9 @@ __global__ void __launch_bounds__(TS_THREADS)
       for (int i = 0; i < L; i++) v[i] = dense[(int64_t)i * d.P + p];
 #pragma unroll
       for (int n = 0; n < CH; n++) {
-        float a = c_tw[d.oa0 + n];
+        float a = c_tw[oa0 + n];
 #pragma unroll
-        for (int i = 0; i < L; i++) a = fmaf(c_tw[d.oA0 + n * L + i], v[i], a);
+        for (int i = 0; i < L; i++) a = fmaf(c_tw[oA0 + n * L + i], v[i], a);
         ua[n] = a;
       }
     }
@@ -768,11 +775,11 @@ __global__ void __launch_bounds__(TS_THREADS)
       vec[LY::V1 + n] = fmaxf(a, 0.0f);
       float g = 0.0f;
 #pragma unroll
-      for (int c = 0; c < 3; c++) g = fmaf(c_tw[d.oA1 + c * CH + n], d2[c], g);
+      for (int c = 0; c < 3; c++) g = fmaf(c_tw[oA1 + c * CH + n], d2[c], g);
       g = a > 0.0f ? g : 0.0f;
       vec[LY::D1 + n] = g;
 #pragma unroll
-      for (int i = 0; i < L; i++) gd[i] = fmaf(c_tw[d.oA0 + n * L + i], g, gd[i]);
+      for (int i = 0; i < L; i++) gd[i] = fmaf(c_tw[oA0 + n * L + i], g, gd[i]);
     }
 #pragma unroll
     for (int i = 0; i < L; i++) gdense[(int64_t)i * d.P + p] = gd[i];
@@ -1123,17 +1130,30 @@ typedef void (*TrSynBwdFn)(int, int, size_t, cudaStream_t, const TrainSynDims&, 
 template <int L, int CH>
 static void tr_syn_fwd_launch(int g, int t, cudaStream_t s, const TrainSynDims& d, const float* dense, float* u1,
                               float* us0, float* hs0) {
-  tr_syn1x1_fwd_kernel<L, CH><<<g, t, 0, s>>>(d, dense, u1, us0, hs0);
+  switch (d.bank) {  // one instantiation per constant bank (compile-time weight addresses)
+    case 0: tr_syn1x1_fwd_kernel<L, CH, 0><<<g, t, 0, s>>>(d, dense, u1, us0, hs0); break;
+    case 1: tr_syn1x1_fwd_kernel<L, CH, 1><<<g, t, 0, s>>>(d, dense, u1, us0, hs0); break;
+    case 2: tr_syn1x1_fwd_kernel<L, CH, 2><<<g, t, 0, s>>>(d, dense, u1, us0, hs0); break;
+    default: tr_syn1x1_fwd_kernel<L, CH, 3><<<g, t, 0, s>>>(d, dense, u1, us0, hs0); break;
+  }
 }
 template <int L, int CH>
 static void tr_syn_bwd_launch(int g, int t, size_t smem, cudaStream_t s, const TrainSynDims& d, const float* dense,
                               const float* u1, const float* us0, const float* gh, float* gdense, float* wpart, int n_w) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tr_syn1x1_bwd_kernel<L, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(tr_syn1x1_bwd_kernel<L, CH, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(tr_syn1x1_bwd_kernel<L, CH, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(tr_syn1x1_bwd_kernel<L, CH, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(tr_syn1x1_bwd_kernel<L, CH, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     attr = true;
   }
-  tr_syn1x1_bwd_kernel<L, CH><<<g, t, smem, s>>>(d, dense, u1, us0, gh, gdense, wpart, n_w);
+  switch (d.bank) {
+    case 0: tr_syn1x1_bwd_kernel<L, CH, 0><<<g, t, smem, s>>>(d, dense, u1, us0, gh, gdense, wpart, n_w); break;
+    case 1: tr_syn1x1_bwd_kernel<L, CH, 1><<<g, t, smem, s>>>(d, dense, u1, us0, gh, gdense, wpart, n_w); break;
+    case 2: tr_syn1x1_bwd_kernel<L, CH, 2><<<g, t, smem, s>>>(d, dense, u1, us0, gh, gdense, wpart, n_w); break;
+    default: tr_syn1x1_bwd_kernel<L, CH, 3><<<g, t, smem, s>>>(d, dense, u1, us0, gh, gdense, wpart, n_w); break;
+  }
 }
 struct TrSynEntry {
   int L, CH;
@@ -1340,11 +1360,19 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
   int launches = 0;
   // weights -> constant bank (arm | up | syn), device to device
   const int64_t nw = pl.n_arm + pl.n_up + pl.n_syn;
-  if (nw > TR_MAX_W || pl.n_arm / 2 + 2 > TR_MAX_ARMP) return -2;
+  (void)nw;
+  if (pl.n_arm > TR_UP_OFF || pl.n_up > TR_SYN_OFF - TR_UP_OFF || pl.n_syn > TR_MAX_W - TR_SYN_OFF ||
+      pl.n_arm / 2 + 2 > TR_MAX_ARMP)
+    return -2;
   const int bank = acquire_bank(s);
   const int tw0 = bank * TR_MAX_W, tp0 = bank * TR_MAX_ARMP;
-  cudaMemcpyToSymbolAsync(c_tw, par + lv.n_lat, sizeof(float) * (size_t)nw, sizeof(float) * (size_t)tw0,
+  const float* pw = par + lv.n_lat;  // [arm | up | syn] -> the bank's fixed slots
+  cudaMemcpyToSymbolAsync(c_tw, pw, sizeof(float) * (size_t)pl.n_arm, sizeof(float) * (size_t)tw0,
                           cudaMemcpyDeviceToDevice, s);
+  cudaMemcpyToSymbolAsync(c_tw, pw + pl.n_arm, sizeof(float) * (size_t)pl.n_up, sizeof(float) * (size_t)(tw0 + TR_UP_OFF),
+                          cudaMemcpyDeviceToDevice, s);
+  cudaMemcpyToSymbolAsync(c_tw, pw + pl.n_arm + pl.n_up, sizeof(float) * (size_t)pl.n_syn,
+                          sizeof(float) * (size_t)(tw0 + TR_SYN_OFF), cudaMemcpyDeviceToDevice, s);
   {  // FFMA2-packed ARM weights (forward) through a workspace buffer
     float2* packed = (float2*)(W + pl.o_grad_tmp);  // free until the first reduction
     tr_pack_arm_kernel<<<1, 256, 0, s>>>(par + lv.n_lat, packed, d.arm_n_layers, d.n_ctx, d.arm_widths[1]);
@@ -1352,7 +1380,7 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
                             cudaMemcpyDeviceToDevice, s);
     launches++;
   }
-  const int koff = tw0 + (int)pl.n_arm;  // taps in c_tw
+  const int koff = tw0 + TR_UP_OFF;  // taps in c_tw
   TrainSynDims sd;
   sd.H = d.H;
   sd.W = d.W;
@@ -1360,7 +1388,8 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
   sd.CH = CH;
   sd.R = R;
   sd.P = P;
-  sd.oA0 = tw0 + (int)(pl.n_arm + pl.n_up);
+  sd.oA0 = tw0 + TR_SYN_OFF;
+  sd.bank = bank;
   sd.oa0 = sd.oA0 + L * CH;
   sd.oA1 = sd.oa0 + CH;
   sd.oa1 = sd.oA1 + 3 * CH;
