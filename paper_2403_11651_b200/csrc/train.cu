@@ -423,9 +423,11 @@ __global__ void tr_arm_gather_kernel(TrainLevels lv, const __grid_constant__ Tra
 // Along one axis of `lines` lines: out[o] = sum_t k[2t+1-r] g[clamp(q+r+K/4-1-t)],
 // o = 2q + r < m (the gather form of the stride-2 transposed conv on the
 // replicate-extended input, reading #12).
+template <int KT>  // KT > 0: the tap count at compile time (unrolled)
 __global__ void tr_tconv_fwd_kernel(const float* __restrict__ g, float* __restrict__ out, int lines, int n, int m,
-                                    int64_t g_ls, int64_t g_es, int64_t o_ls, int64_t o_es, int K, int koff,
+                                    int64_t g_ls, int64_t g_es, int64_t o_ls, int64_t o_es, int K_, int koff,
                                     int64_t g_cs, int64_t o_cs) {
+  const int K = KT > 0 ? KT : K_;
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= (int64_t)lines * m) return;
   g += blockIdx.y * g_cs;  // channel
@@ -444,10 +446,15 @@ __global__ void tr_tconv_fwd_kernel(const float* __restrict__ g, float* __restri
     line = i32 - o * lines;
   }
   const int q = o >> 1, r = o & 1;
+  // 32-bit offsets within the channel plane (< 2^31 elements)
+  const int gl = line * (int)g_ls, ge = (int)g_es;
   float acc = 0.0f;
-  for (int t = 0; t < K / 2; t++)
-    acc = fmaf(c_tw[koff + 2 * t + 1 - r], g[line * g_ls + (int64_t)clampi(q + r + K / 4 - 1 - t, 0, n - 1) * g_es], acc);
-  out[line * o_ls + (int64_t)o * o_es] = acc;
+#pragma unroll
+  for (int t = 0; t < (KT > 0 ? KT / 2 : 4); t++) {
+    if (KT == 0 && t >= K / 2) break;
+    acc = fmaf(c_tw[koff + 2 * t + 1 - r], g[gl + clampi(q + r + K / 4 - 1 - t, 0, n - 1) * ge], acc);
+  }
+  out[line * (int)o_ls + o * (int)o_es] = acc;
 }
 
 // Adjoint: gg[s] = sum over extended positions i with clamp(i - E) = s of
@@ -478,7 +485,7 @@ __global__ void tr_tconv_bwd_kernel(const float* __restrict__ g, const float* __
       line = i32 - s * lines;
     }
     const int E = K / 4, P = K / 2 - 1 + 2 * E;
-    const float xs = g[line * g_ls + (int64_t)s * g_es];
+    const float xs = g[line * (int)g_ls + s * (int)g_es];  // 32-bit plane offsets
     const int i_lo = (s == 0) ? 0 : s + E, i_hi = (s == n - 1) ? n - 1 + 2 * E : s + E;  // extended positions
     float acc = 0.0f;
     for (int i = i_lo; i <= i_hi; i++)
@@ -487,12 +494,12 @@ __global__ void tr_tconv_bwd_kernel(const float* __restrict__ g, const float* __
         if (KT == 0 && j >= K) break;
         const int o = 2 * i + j - P;
         if (o >= 0 && o < m) {
-          const float go = gout[line * o_ls + (int64_t)o * o_es];
+          const float go = gout[line * (int)o_ls + o * (int)o_es];
           acc = fmaf(c_tw[koff + j], go, acc);
           dk[j] = fmaf(xs, go, dk[j]);
         }
       }
-    gg[line * g_ls + (int64_t)s * g_es] = acc;
+    gg[line * (int)g_ls + s * (int)g_es] = acc;
   }
   // block partial of the tap gradient
 #pragma unroll
@@ -1194,6 +1201,7 @@ static int reduce_partials(const float* part, int64_t blocks, int64_t stride, in
 static int blocks_for(int64_t n) { return (int)((n + TB - 1) / TB); }
 
 #define TCONV_BWD(K) ((K) == 8 ? tr_tconv_bwd_kernel<8> : (K) == 4 ? tr_tconv_bwd_kernel<4> : tr_tconv_bwd_kernel<0>)
+#define TCONV_FWD(K) ((K) == 8 ? tr_tconv_fwd_kernel<8> : (K) == 4 ? tr_tconv_fwd_kernel<4> : tr_tconv_fwd_kernel<0>)
 
 // The small levels' steps of the upsampling chain (forward or adjoint) in ONE
 // single-CTA launch: each of them is a few thousand elements, so as separate
@@ -1487,10 +1495,10 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
       continue;
     }
     // x pass: per channel, lines = rows (hs), n = ws2 -> m = wd
-    tr_tconv_fwd_kernel<<<dim3(blocks_for((int64_t)hs * wd), nch), TB, 0, s>>>(
+    TCONV_FWD(K)<<<dim3(blocks_for((int64_t)hs * wd), nch), TB, 0, s>>>(
         Tj(j + 1), mid, hs, ws2, wd, ws2, 1, wd, 1, K, koff, (int64_t)hs * ws2, (int64_t)hs * wd);
     // y pass: per channel, lines = columns (wd), n = hs -> m = hd, into T_j channels 1..
-    tr_tconv_fwd_kernel<<<dim3(blocks_for((int64_t)wd * hd), nch), TB, 0, s>>>(
+    TCONV_FWD(K)<<<dim3(blocks_for((int64_t)wd * hd), nch), TB, 0, s>>>(
         mid, Tj(j) + (int64_t)hd * wd, wd, hs, hd, 1, wd, 1, wd, K, koff, (int64_t)hs * wd, (int64_t)hd * wd);
     launches += 2;
   }
