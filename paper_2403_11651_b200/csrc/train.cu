@@ -412,9 +412,11 @@ __global__ void tr_arm_gather_kernel(TrainLevels lv, const __grid_constant__ Tra
   const int t32 = (int)t;  // 32-bit division
   const int i = t32 / w, j = t32 - i * w;
   float g = gown[q];
+  const float* dl = dctx + lv.off[l];
+  const int nl32 = (int)lv.n_lat;  // C x N_lat < 2^31
   for (int c = 0; c < C; c++) {
     const int pi = i - cx.dy[c], pj = j - cx.dx[c];  // latent whose context c is (i, j)
-    if (pi >= 0 && pi < h && pj >= 0 && pj < w) g += dctx[c * lv.n_lat + lv.off[l] + (int64_t)pi * w + pj];
+    if (pi >= 0 && pi < h && pj >= 0 && pj < w) g += dl[c * nl32 + pi * w + pj];  // 32-bit offsets
   }
   gy[q] = g;
 }
@@ -562,15 +564,32 @@ __global__ void tr_conv_fwd_kernel(TrainSynDims d, int r, const float* __restric
   const int p32 = (int)p;  // 32-bit division (P < 2^31)
   const int y = p32 / d.W, x = p32 - y * d.W;
   const int oG = d.oG + 84 * r;
+  // the 27 window values once (each feeds 3 outputs), 32-bit plane offsets
+  const int P32 = (int)d.P;
+  int ro[3], cx[3];
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    ro[k] = clampi(y + k - 1, 0, d.H - 1) * d.W;
+    cx[k] = clampi(x + k - 1, 0, d.W - 1);
+  }
+  float v[3][3][3];
+#pragma unroll
+  for (int ci = 0; ci < 3; ci++)
+#pragma unroll
+    for (int ky = 0; ky < 3; ky++)
+#pragma unroll
+      for (int kx = 0; kx < 3; kx++) v[ci][ky][kx] = hin[ci * P32 + ro[ky] + cx[kx]];
+#pragma unroll
   for (int co = 0; co < 3; co++) {
-    float a = hin[co * d.P + p] + c_tw[oG + 81 + co];
+    float a = v[co][1][1] + c_tw[oG + 81 + co];  // residual (the centre tap is the pixel itself)
+#pragma unroll
     for (int ci = 0; ci < 3; ci++)
+#pragma unroll
       for (int ky = 0; ky < 3; ky++)
-        for (int kx = 0; kx < 3; kx++)
-          a = fmaf(c_tw[oG + ((co * 3 + ci) * 3 + ky) * 3 + kx],
-                   hin[ci * d.P + (int64_t)clampi(y + ky - 1, 0, d.H - 1) * d.W + clampi(x + kx - 1, 0, d.W - 1)], a);
-    us[co * d.P + p] = a;
-    hout[co * d.P + p] = (r < d.R - 1) ? fmaxf(a, 0.0f) : a;
+#pragma unroll
+        for (int kx = 0; kx < 3; kx++) a = fmaf(c_tw[oG + ((co * 3 + ci) * 3 + ky) * 3 + kx], v[ci][ky][kx], a);
+    us[co * P32 + p32] = a;
+    hout[co * P32 + p32] = (r < d.R - 1) ? fmaxf(a, 0.0f) : a;
   }
 }
 
