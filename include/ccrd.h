@@ -220,8 +220,14 @@ int cc_rd_forward_strip(const cc_model_desc* desc, const cc_strip* strip, const 
  * grad: DEVICE fp32, same length: receives the gradient at the input point.
  * opt: HOST; NULL = gradient only (no update).  result: DEVICE, the cost of
  * this forward (rate_bits, sse, mse, cost).  image: DEVICE [3][H][W].
- * Weights are staged into a __constant__ bank per call: one training call in
- * flight per process (CUDA stream order). */
+ * Concurrency: weights are staged into one of 4 per-device __constant__ banks
+ * per call.  Calls may run concurrently on different streams AND from
+ * different host threads: a bank is held exclusively from the start of a call
+ * to the end of its enqueue, a stream taking over a bank waits (on the GPU)
+ * for the previous owner's last step, and a caller finding all 4 banks held
+ * blocks on the host until one is released.  Results are bit-identical to
+ * the same steps run one at a time.  Shapes with H W >= 2^31 are CC_ENOTSUP
+ * (32-bit offsets inside a plane). */
 typedef struct {
   float lr, beta1, beta2, eps;
   int32_t t;  /* Adam step number, >= 1 */

@@ -19,7 +19,10 @@
 // column read from it, so no slot is overwritten while still needed).  The
 // ring starts POISONED (INT16_MIN, never a valid latent here): a context read
 // of a latent not decoded yet is counted and corrupts (mu, b), so the parity
-// tests catch any schedule error.  The entropy decoder (range coder) is out of
+// tests catch any schedule error.  With a counter (CHECK), each row re-poisons
+// its ring row when it starts and keeps the 8 slots ahead of its newest column
+// poisoned, so this holds for every row and column, not only the first RR rows
+// and 32 columns.  The entropy decoder (range coder) is out of
 // scope: it is played by `truth` -- after (mu, b) of a latent exist, its value
 // is revealed and written to the ring and to `decoded`.
 //
@@ -142,11 +145,32 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
       const float bt = laplace_bits((float)yv, ms.x, ms.y, p.g);
       bsum += bt;
       {
+        int16_t* row = ring + (r & p.rr_mask) * DEC_RW;
+        if constexpr (CHECK) {
+          // keep the poison meaningful past the first RR rows and 32 columns:
+          // the ring row of row r last held row r - RR, dead once row r starts
+          // (RR >= w/a + 6), so row r's first latent re-poisons all of it ...
+          if (j == 0)
+            for (int k = 0; k < DEC_RW; k++) row[k] = DEC_POISON;
+        }
         const int lc = j & (DEC_RING - 1);
-        int16_t* rw = ring + (r & p.rr_mask) * DEC_RW + lc + DEC_PAD;
+        int16_t* rw = row + lc + DEC_PAD;
         rw[0] = yv;
         if (lc >= DEC_RING - DEC_PAD) rw[-DEC_RING] = yv;  // left pad
         if (lc < DEC_PAD) rw[DEC_RING] = yv;               // right pad
+        if constexpr (CHECK) {
+          // ... and every latent poisons the slot 8 columns ahead (it holds
+          // column j - 24; readers of this row are at columns >= j - 3a - 4 >
+          // j - 24 for a <= 6), so columns j+1 .. j+8 of the row are always
+          // poison until decoded: a premature read near the wavefront counts
+          if (p.a <= 6) {
+            const int pc = (j + 8) & (DEC_RING - 1);
+            int16_t* pw = row + pc + DEC_PAD;
+            pw[0] = DEC_POISON;
+            if (pc >= DEC_RING - DEC_PAD) pw[-DEC_RING] = DEC_POISON;
+            if (pc < DEC_PAD) pw[DEC_RING] = DEC_POISON;
+          }
+        }
       }
       decoded[q] = yv;
       if (p.bits) p.bits[off + q] = bt;

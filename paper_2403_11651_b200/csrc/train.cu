@@ -30,6 +30,7 @@
 //   5. upsampling adjoint, in gather form, tap-gradient partials
 //   6. fp64 reduction of every partial into the gradient, Adam, cost.
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
 #include <mutex>
 #include <type_traits>
@@ -413,10 +414,11 @@ __global__ void tr_arm_gather_kernel(TrainLevels lv, const __grid_constant__ Tra
   const int i = t32 / w, j = t32 - i * w;
   float g = gown[q];
   const float* dl = dctx + lv.off[l];
-  const int nl32 = (int)lv.n_lat;  // C x N_lat < 2^31
   for (int c = 0; c < C; c++) {
     const int pi = i - cx.dy[c], pj = j - cx.dx[c];  // latent whose context c is (i, j)
-    if (pi >= 0 && pi < h && pj >= 0 && pj < w) g += dl[c * nl32 + pi * w + pj];  // 32-bit offsets
+    // channel plane c at a 64-bit offset (C x N_lat may exceed 2^31); 32-bit
+    // offsets only inside one grid (< P < 2^31 elements)
+    if (pi >= 0 && pi < h && pj >= 0 && pj < w) g += (dl + (int64_t)c * lv.n_lat)[pi * w + pj];
   }
   gy[q] = g;
 }
@@ -564,8 +566,11 @@ __global__ void tr_conv_fwd_kernel(TrainSynDims d, int r, const float* __restric
   const int p32 = (int)p;  // 32-bit division (P < 2^31)
   const int y = p32 / d.W, x = p32 - y * d.W;
   const int oG = d.oG + 84 * r;
-  // the 27 window values once (each feeds 3 outputs), 32-bit plane offsets
-  const int P32 = (int)d.P;
+  // the 27 window values once (each feeds 3 outputs); channel planes at 64-bit
+  // offsets (3 P may exceed 2^31), 32-bit offsets inside a plane (P < 2^31)
+  const float* hc[3] = {hin, hin + d.P, hin + 2 * d.P};
+  float* uc[3] = {us, us + d.P, us + 2 * d.P};
+  float* oc[3] = {hout, hout + d.P, hout + 2 * d.P};
   int ro[3], cx[3];
 #pragma unroll
   for (int k = 0; k < 3; k++) {
@@ -578,7 +583,7 @@ __global__ void tr_conv_fwd_kernel(TrainSynDims d, int r, const float* __restric
 #pragma unroll
     for (int ky = 0; ky < 3; ky++)
 #pragma unroll
-      for (int kx = 0; kx < 3; kx++) v[ci][ky][kx] = hin[ci * P32 + ro[ky] + cx[kx]];
+      for (int kx = 0; kx < 3; kx++) v[ci][ky][kx] = hc[ci][ro[ky] + cx[kx]];
 #pragma unroll
   for (int co = 0; co < 3; co++) {
     float a = v[co][1][1] + c_tw[oG + 81 + co];  // residual (the centre tap is the pixel itself)
@@ -588,8 +593,8 @@ __global__ void tr_conv_fwd_kernel(TrainSynDims d, int r, const float* __restric
       for (int ky = 0; ky < 3; ky++)
 #pragma unroll
         for (int kx = 0; kx < 3; kx++) a = fmaf(c_tw[oG + ((co * 3 + ci) * 3 + ky) * 3 + kx], v[ci][ky][kx], a);
-    us[co * P32 + p32] = a;
-    hout[co * P32 + p32] = (r < d.R - 1) ? fmaxf(a, 0.0f) : a;
+    uc[co][p32] = a;
+    oc[co][p32] = (r < d.R - 1) ? fmaxf(a, 0.0f) : a;
   }
 }
 
@@ -1197,6 +1202,9 @@ static const TrSynEntry* find_tr_syn(const cc_model_desc& d) {
 
 int train_supported(const cc_model_desc& d) {
   if (d.up_2d || !find_tr_syn(d)) return 0;
+  // the kernels use 32-bit offsets inside one plane (a grid, a channel of the
+  // image): P must stay below 2^31 (cc_validate admits exactly 2^31)
+  if ((int64_t)d.H * d.W >= ((int64_t)1 << 31)) return 0;
   for (const auto& e : kTrArm)
     if (e.C == d.n_ctx && e.NH == d.arm_widths[1] && e.NHL == d.arm_n_layers - 1) return 1;
   return 0;
@@ -1331,47 +1339,82 @@ static void launch_chain(const TrChain& c, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- constant-bank ownership
+// A bank is BUSY from acquire_bank (before its weights are copied in) to
+// release_bank (after the step's last kernel is enqueued): a busy bank is never
+// handed to another caller, so no copy into c_tw / c_tp can be enqueued while
+// another host thread is still enqueuing kernels that read that bank.  A free
+// bank remembers its last owner stream and an event recorded by that owner at
+// release (while it still owned the bank), so a new owner's stream waits for
+// every kernel of the previous owner's last step before overwriting it.  When
+// every bank is busy the caller BLOCKS on the host until one is released.
+// State is per device (one bank table per device; __constant__ memory is
+// per-device), the events are created on their device and reused.
+constexpr int TR_MAX_DEVICES = 64;
 struct TrBank {
   cudaStream_t owner = nullptr;
-  bool used = false;
-  cudaEvent_t last_use = nullptr;  // recorded after the owner's last step
+  bool used = false;  // has had an owner (last_use recorded)
+  bool busy = false;  // held by a caller between acquire and release
+  cudaEvent_t last_use = nullptr;
   uint64_t tick = 0;
 };
-static TrBank g_banks[TR_BANKS];
+struct TrBankSet {
+  TrBank b[TR_BANKS];
+  bool init = false;
+};
+static TrBankSet g_banks[TR_MAX_DEVICES];
 static std::mutex g_bank_mu;
+static std::condition_variable g_bank_cv;
 static uint64_t g_bank_tick = 0;
-static int g_bank_dev = -1;
 
-// the bank stream s trains with; waits (on s) for a previous owner's last use
-static int acquire_bank(cudaStream_t s) {
-  std::lock_guard<std::mutex> lk(g_bank_mu);
+// the bank stream s trains with on the current device (blocks while all are
+// busy); -1 if the device index is out of range or an event cannot be created
+static int acquire_bank(cudaStream_t s, int* dev_out) {
   int dev = 0;
-  cudaGetDevice(&dev);
-  if (g_bank_dev != dev) {
-    for (auto& b : g_banks) {
-      b = TrBank();
-      cudaEventCreateWithFlags(&b.last_use, cudaEventDisableTiming);
-    }
-    g_bank_dev = dev;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= TR_MAX_DEVICES) return -1;
+  std::unique_lock<std::mutex> lk(g_bank_mu);
+  TrBankSet& set = g_banks[dev];
+  if (!set.init) {
+    for (auto& b : set.b)
+      if (cudaEventCreateWithFlags(&b.last_use, cudaEventDisableTiming) != cudaSuccess) return -1;
+    set.init = true;
   }
   int k = -1;
-  for (int i = 0; i < TR_BANKS; i++)
-    if (g_banks[i].used && g_banks[i].owner == s) k = i;
-  if (k < 0) {  // least recently used bank
-    k = 0;
-    for (int i = 1; i < TR_BANKS; i++)
-      if (g_banks[i].tick < g_banks[k].tick) k = i;
-    if (g_banks[k].used) cudaStreamWaitEvent(s, g_banks[k].last_use, 0);
-    g_banks[k].owner = s;
-    g_banks[k].used = true;
+  for (;;) {
+    // the bank this stream used last, if free; else the least recently used free bank
+    for (int i = 0; i < TR_BANKS; i++)
+      if (!set.b[i].busy && set.b[i].used && set.b[i].owner == s) k = i;
+    if (k < 0)
+      for (int i = 0; i < TR_BANKS; i++)
+        if (!set.b[i].busy && (k < 0 || set.b[i].tick < set.b[k].tick)) k = i;
+    if (k >= 0) break;
+    g_bank_cv.wait(lk);
   }
-  g_banks[k].tick = ++g_bank_tick;
+  TrBank& b = set.b[k];
+  if (b.used && b.owner != s) cudaStreamWaitEvent(s, b.last_use, 0);  // previous owner's last step
+  b.owner = s;
+  b.used = true;
+  b.busy = true;
+  b.tick = ++g_bank_tick;
+  *dev_out = dev;
   return k;
 }
-static void release_bank(int k, cudaStream_t s) {
-  std::lock_guard<std::mutex> lk(g_bank_mu);
-  cudaEventRecord(g_banks[k].last_use, s);
+static void release_bank(int dev, int k, cudaStream_t s) {
+  {
+    std::lock_guard<std::mutex> lk(g_bank_mu);
+    TrBank& b = g_banks[dev].b[k];
+    cudaEventRecord(b.last_use, s);  // still the owner: nobody else can hold a busy bank
+    b.busy = false;
+  }
+  g_bank_cv.notify_all();
 }
+// releases the bank on every exit path of train_step_impl
+struct TrBankGuard {
+  int dev, k;
+  cudaStream_t s;
+  ~TrBankGuard() {
+    if (k >= 0) release_bank(dev, k, s);
+  }
+};
 
 // The iteration.  Returns the number of kernel launches (>= 0) or -1 if a
 // CUDA call failed (the caller checks cudaGetLastError).
@@ -1391,7 +1434,10 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
   if (pl.n_arm > TR_UP_OFF || pl.n_up > TR_SYN_OFF - TR_UP_OFF || pl.n_syn > TR_MAX_W - TR_SYN_OFF ||
       pl.n_arm / 2 + 2 > TR_MAX_ARMP)
     return -2;
-  const int bank = acquire_bank(s);
+  int bank_dev = 0;
+  const int bank = acquire_bank(s, &bank_dev);
+  if (bank < 0) return -1;
+  TrBankGuard bank_guard{bank_dev, bank, s};  // released after the last enqueue, on every path
   const int tw0 = bank * TR_MAX_W, tp0 = bank * TR_MAX_ARMP;
   const float* pw = par + lv.n_lat;  // [arm | up | syn] -> the bank's fixed slots
   cudaMemcpyToSymbolAsync(c_tw, pw, sizeof(float) * (size_t)pl.n_arm, sizeof(float) * (size_t)tw0,
@@ -1631,8 +1677,7 @@ int train_step_impl(const cc_model_desc& d, float* par, const float* noise, cons
         par, grad, am, av, pl.n_par, opt->lr, opt->beta1, opt->beta2, opt->eps, c1, c2);
     launches++;
   }
-  release_bank(bank, s);  // this stream's last use of the bank
-  return launches;
+  return launches;  // bank_guard records this stream's last use of the bank
 }
 
 }  // namespace ccrd

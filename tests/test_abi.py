@@ -161,6 +161,11 @@ def test_training_entry_errors_without_gpu():
     with pytest.raises(ccrd.CcError) as e:           # Adam step 0
         P.cc_train_step(d, 8, 8, 8, 8, 8, P.CcAdam(1e-3, 0.9, 0.999, 1e-8, 0), 8, 8, 8, ws)
     assert e.value.code == ccrd.CC_EINVAL
+    big = P.desc_from_config(cfg.replace(H=32768, W=65536))  # H W = 2^31: 32-bit plane offsets
+    assert P.cc_validate(big) == 0 and P.cc_train_workspace_bytes(big) == 0
+    with pytest.raises(ccrd.CcError) as e:
+        P.cc_train_step(big, 8, 8, 8, 8, 8, None, 8, 8, 8, 1 << 30)
+    assert e.value.code == ccrd.CC_ENOTSUP
     d2 = P.desc_from_config(workload.CONFIGS["t2300"])     # 2-D TConv: not compiled for training
     assert P.cc_train_workspace_bytes(d2) == 0
     with pytest.raises(ccrd.CcError) as e:

@@ -106,6 +106,22 @@ def test_too_small_skew_is_detected():
     assert not np.array_equal(good[4][0], bad[4][0])
 
 
+def test_too_small_skew_is_detected_on_every_row_and_column():
+    """Ring rows are reused every RR rows and ring columns every 32 columns;
+    with the poison counter the kernel re-poisons a ring row when its row
+    starts and keeps the 8 slots ahead of the wavefront poisoned, so the
+    premature reads of a too-small skew are counted on rows past RR and
+    columns past 32 too: the count grows in proportion to the grid."""
+    def count(H, W):
+        cfg = workload.CONFIGS["ref"].replace(H=H, W=W)
+        im = workload.make_image(cfg, 213)
+        return run_decode(cfg, [im], skew=1)[5]
+    base = count(64, 48)            # a = 1: RR = 64 ring rows for w = 48
+    assert base > 0
+    assert count(256, 48) > 3 * base     # 4x the rows, 3/4 of them past RR
+    assert count(64, 192) > 3 * base     # 4x the columns, 7/8 of them past 32
+
+
 @pytest.mark.timeout(600)
 def test_decode_full_2k_image():
     """BASELINE.json configs[3] size (1365 x 2048): bit-identical to the encoder."""

@@ -147,3 +147,55 @@ def test_train_concurrent_streams_bit_identical():
     for a, c in zip(alone, conc):
         assert torch.equal(a.params, c.params)
         assert torch.equal(a.result, c.result)
+
+
+def test_train_concurrent_host_threads_bit_identical():
+    """Trainers stepping from SEVERAL HOST THREADS at once, each on its own
+    stream, more threads than constant banks (6 > 4): a bank is held from the
+    start of a call to the end of its enqueue (train.cu acquire_bank /
+    release_bank), so no thread's weight copy can land in a bank another
+    thread's kernels are still reading.  Every image ends bit-identical to
+    its own serial run."""
+    import threading
+    import paper_2403_11651_b200 as P
+    cfg = workload.CONFIGS["ref"].replace(H=64, W=96)
+    K, steps = 6, 6
+    states = [make_state(cfg, 70 + k) for k in range(K)]
+
+    def trainers():
+        out = []
+        for im, y, u in states:
+            tr = P.DeviceTrainer(cfg, y, im.arm_w, im.up_w, im.syn_w, im.image)
+            tr.noise.copy_(torch.as_tensor(u))
+            out.append(tr)
+        torch.cuda.synchronize()
+        return out
+
+    alone = trainers()
+    for tr in alone:
+        for _ in range(steps):
+            tr.step(lr=1e-3)
+    torch.cuda.synchronize()
+    conc = trainers()
+    streams = [torch.cuda.Stream() for _ in range(K)]
+    errors = []
+    start = threading.Barrier(K)
+
+    def run(tr, st):
+        try:
+            start.wait()
+            for _ in range(steps):
+                tr.step(lr=1e-3, stream_ptr=st.cuda_stream)
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=run, args=(tr, st)) for tr, st in zip(conc, streams)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    torch.cuda.synchronize()
+    for a, c in zip(alone, conc):
+        assert torch.equal(a.params, c.params)
+        assert torch.equal(a.result, c.result)
