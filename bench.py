@@ -35,6 +35,30 @@ UNIT = "pixels/s"
 # 1.965 GHz (B200_PROFILING.md SM count, clocks.max.sm).  The FFMA2 probe
 # (tools/microbench/ffma_probe.cu) measured 126.9 FMA/clk/SM = 99.2 % of it.
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
+def tf32_peak_tflops():
+    """Dense TF32 tensor peak: the measured cuBLAS bf16 GEMM peak
+    (MEASURED_PEAKS.json; burst figure, a kernel timed alone) x the nominal
+    TF32 / BF16 ratio of B200_PROFILING.md (1.1 / 2.25 PFLOP/s dense)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            bf16 = float(json.load(f)["bf16_tflops"])
+        src = "measured bf16 %.1f TF/s (MEASURED_PEAKS.json, burst) x 1.1/2.25" % bf16
+    except Exception:
+        bf16 = 1590.0
+        src = "fallback bf16 1590 TF/s (B200_PROFILING.md) x 1.1/2.25"
+    return bf16 * 1.1 / 2.25, src
+
+
+def arm_tc_mac_per_latent(cfg):
+    """tcgen05 multiply-accumulates the tensor-core ARM issues per latent
+    (arm_tc.cu arm_tcg_kernel): layer 0 = context (K0 = C + 8 columns incl. the
+    bias block) x (W_hi + W_lo); hidden layer = A_hi (K1 = NH + 8) x (W_hi +
+    W_lo) + A_lo (NH) x W_hi; N = NH.  The 2-wide output layer runs on the CUDA
+    cores."""
+    C, NH = cfg.n_ctx, cfg.arm_widths[1]
+    return 2 * (C + 8) * NH + 2 * (NH + 8) * NH + NH * NH
 REASONS = [(0x1, "gpu_idle"), (0x2, "applications_clocks_setting"), (0x4, "sw_power_cap"),
            (0x8, "hw_slowdown"), (0x10, "sync_boost"), (0x20, "sw_thermal_slowdown"),
            (0x40, "hw_thermal_slowdown"), (0x80, "hw_power_brake_slowdown")]
@@ -206,14 +230,53 @@ def run_ours(args, rk):
     px_total = rk.world * n_img * P_img * args.steps
     value = px_total / (ms_max / 1e3)
 
-    # roofline of the dominant kernel (arm_rate: ~69 % of the MACs)
+    # per-kernel rooflines; the headline `roofline` is the kernel with the
+    # largest share of the serial step
+    arm_tc = P.cc_arm_path_for(desc) == P.CC_ARM_TC
+    arm_name = "arm_tcg_kernel" if arm_tc else "arm_rate_kernel"
     arm_avg_s = prof.arm_ms / max(1, prof.arm_launches) / 1e3
     syn_avg_s = prof.syn_ms / max(1, prof.syn_launches) / 1e3
-    arm_tflops = 2.0 * macs.arm_macs / arm_avg_s / 1e12
+    arm_tflops = 2.0 * macs.arm_macs / arm_avg_s / 1e12            # fp32-accurate algorithmic FLOP
     syn_tflops = 2.0 * (macs.up_macs + macs.syn_macs) / syn_avg_s / 1e12
     path_tflops = 2.0 * macs.total * value / rk.world / 1e12
-    traffic = load_traffic("arm_rate_kernel")
     serial_ms = prof.arm_ms + prof.syn_ms + prof.pyr_ms + prof.reduce_ms
+    arm_mac_latent = sum(cfg.arm_widths[k] * cfg.arm_widths[k + 1] for k in range(len(cfg.arm_widths) - 1))
+    timing = (f"launch durations from CUDA events in a {args.profile_steps}-step serial pass "
+              "(the timed steps run ARM || synthesis on two streams)")
+    fp32_src = "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (B200_PROFILING.md); FFMA2 probe measured 99.2 % of it"
+    kern = {}
+    if arm_tc:
+        tf32_peak, tf32_src = tf32_peak_tflops()
+        tc_macs = arm_tc_mac_per_latent(cfg) * macs.n_latents
+        tc_tflops = 2.0 * tc_macs / arm_avg_s / 1e12
+        kern[arm_name] = {
+            "bound": "tensor", "achieved": tc_tflops, "peak": tf32_peak, "unit": "TFLOP/s", "frac": tc_tflops / tf32_peak,
+            "algorithmic": f"{tc_macs} TF32 tensor MAC (2 FLOP) per launch = 1 image's {macs.n_latents} latents x "
+                           f"{arm_tc_mac_per_latent(cfg)} MAC (3xTF32 split of the {arm_mac_latent}-MAC fp32 ARM)",
+            "peak_source": tf32_src, "fp32_equiv_tflops": arm_tflops,
+            "fp32_equiv_frac_of_fp32_peak": arm_tflops / FP32_PEAK_TFLOPS}
+    else:
+        kern[arm_name] = {
+            "bound": "alu", "achieved": arm_tflops, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": arm_tflops / FP32_PEAK_TFLOPS,
+            "algorithmic": f"{macs.arm_macs} FP32 FMA (2 FLOP) per launch = 1 image's latents x {arm_mac_latent} MAC",
+            "peak_source": fp32_src}
+    kern[arm_name].update({"avg_launch_ms": arm_avg_s * 1e3, "launches": prof.arm_launches,
+                           "share": prof.arm_ms / serial_ms, "traffic": load_traffic(arm_name)})
+    kern["synth_kernel"] = {
+        "bound": "alu", "achieved": syn_tflops, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+        "frac": syn_tflops / FP32_PEAK_TFLOPS,
+        "algorithmic": f"{macs.up_macs + macs.syn_macs} FP32 FMA (2 FLOP) per launch = 1 image's pixels x "
+                       f"{(macs.up_macs + macs.syn_macs) / (cfg.H * cfg.W):.2f} MAC (last upsampling step + synthesis)",
+        "peak_source": fp32_src, "avg_launch_ms": syn_avg_s * 1e3, "launches": prof.syn_launches,
+        "share": prof.syn_ms / serial_ms, "traffic": load_traffic("synth_kernel")}
+    dom = max(kern, key=lambda k: kern[k]["share"])
+    roofline = {"kernel": dom, "timing": timing}
+    roofline.update({k: kern[dom][k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic", "algorithmic",
+                                               "avg_launch_ms", "peak_source")})
+    kern["pyramid_kernel"] = {"ms_total": prof.pyr_ms, "launches": prof.pyr_launches, "share": prof.pyr_ms / serial_ms}
+    kern["reduce_batch_kernel"] = {"ms_total": prof.reduce_ms, "launches": prof.reduce_launches}
+    kern["serial_ms_per_step"] = serial_ms / args.profile_steps
 
     # end to end: host (pinned) buffers through cc_rd_forward_host
     e2e = None
@@ -241,30 +304,13 @@ def run_ours(args, rk):
                   "read per step per GPU (126 MB L2)",
             "parallelism": f"image-sharded x{rk.world}",
         },
-        "roofline": {
-            "bound": "alu", "kernel": "arm_rate_kernel", "achieved": arm_tflops, "peak": FP32_PEAK_TFLOPS,
-            "unit": "TFLOP/s", "frac": arm_tflops / FP32_PEAK_TFLOPS, "traffic": traffic,
-            "timing": f"launch durations from CUDA events in a {args.profile_steps}-step serial pass "
-                      "(the timed steps run ARM || synthesis on two streams)",
-            "algorithmic": f"{macs.arm_macs} FP32 FMA (2 FLOP) per launch = 1 image's latents x "
-                           f"{sum(cfg.arm_widths[k] * cfg.arm_widths[k + 1] for k in range(len(cfg.arm_widths) - 1))} MAC",
-            "avg_launch_ms": arm_avg_s * 1e3,
-            "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (B200_PROFILING.md); "
-                           "FFMA2 probe measured 99.2 % of it",
-        },
-        "kernels": {  # serial pass (see roofline.timing); share = of the serial step
-            "arm_rate_kernel": {"avg_ms": arm_avg_s * 1e3, "launches": prof.arm_launches, "tflops": arm_tflops,
-                                "frac": arm_tflops / FP32_PEAK_TFLOPS, "share": prof.arm_ms / serial_ms},
-            "synth_kernel": {"avg_ms": syn_avg_s * 1e3, "launches": prof.syn_launches, "tflops": syn_tflops,
-                             "frac": syn_tflops / FP32_PEAK_TFLOPS, "share": prof.syn_ms / serial_ms},
-            "pyramid_kernel": {"ms_total": prof.pyr_ms, "launches": prof.pyr_launches,
-                               "share": prof.pyr_ms / serial_ms},
-            "reduce_batch_kernel": {"ms_total": prof.reduce_ms, "launches": prof.reduce_launches},
-            "serial_ms_per_step": serial_ms / args.profile_steps,
-        },
+        "roofline": roofline,
+        "kernels": kern,  # serial pass (see roofline.timing); share = of the serial step
         "streams": "ARM kernels || (pyramid -> synthesis) kernels on two CUDA streams, joined per step",
         "path_roofline": {"achieved_tflops_per_gpu": path_tflops, "frac": path_tflops / FP32_PEAK_TFLOPS,
-                          "note": "whole step: pixels/s x closed-form MAC/px x 2 / FP32 peak"},
+                          "note": "whole step, fp32-equivalent: pixels/s x closed-form MAC/px x 2 / FP32 CUDA-core "
+                                  "peak (the ARM's MACs run on the tensor cores when arm_path = tc)"},
+        "arm_path": "tc" if arm_tc else "ffma2",
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clocks,
@@ -355,8 +401,9 @@ def run_strip(args, rk):
                    "strip_rows": [st.r0, st.r1], "halo_bytes_recv_per_step_rank0": halo_bytes[0],
                    "l2": "inputs larger than L2 (0.4 GB of image + latents per step)",
                    "parallelism": f"strips x{rk.world}, NCCL halo exchange + all-reduce"},
-        "roofline": {"bound": "alu", "kernel": "arm_rate_kernel", "achieved": arm_tflops, "peak": FP32_PEAK_TFLOPS,
-                     "unit": "TFLOP/s", "frac": arm_tflops / FP32_PEAK_TFLOPS, "traffic": None,
+        "roofline": {"bound": "alu", "kernel": "arm_rate_kernel" if P.cc_arm_path_for(desc) != P.CC_ARM_TC
+                     else "arm_tcg_kernel (fp32-equivalent FLOP vs the FP32 peak)", "achieved": arm_tflops,
+                     "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": arm_tflops / FP32_PEAK_TFLOPS, "traffic": None,
                      "avg_launch_ms": arm_avg_s * 1e3},
         "path_roofline": {"achieved_tflops_per_gpu": path_tflops, "frac": path_tflops / FP32_PEAK_TFLOPS},
         "e2e": None, "gpu_launches": launches, "clocks": sampler.summary(), "input_gen_s": round(gen_s, 2),

@@ -348,6 +348,27 @@ const char* cc_version(void);
  * thread launched (bench bookkeeping). */
 int64_t cc_last_launch_count(void);
 
+/* ARM rate path (process-wide; host only, no device needed).  The ARM MLP
+ * (Table 1 ARM column) is computed either by
+ *   CC_ARM_FFMA2: packed FP32 FMAs on the CUDA cores (arm_rate.cu), every
+ *                 compiled ARM shape; the decoder's wavefront ARM uses the
+ *                 same arithmetic, so per-latent outputs are bit-identical
+ *                 to cc_arm_decode's;
+ *   CC_ARM_TC:    tcgen05 kind::tf32 MMAs with a 3xTF32 split (fp32-accurate,
+ *                 DESIGN.md 7.2) for the shapes it is compiled for
+ *                 ([16,24,24,2], [16,16,16,2], [24,24,24,2]), FFMA2 otherwise;
+ *   CC_ARM_AUTO:  (default) = CC_ARM_TC.
+ * The initial value comes from the environment (CCRD_ARM_PATH = ffma2 | tc).
+ * Workspace sizes do not depend on the path.  cc_set_arm_path: CC_EINVAL for
+ * an unknown value.  cc_arm_path_for: the path a descriptor runs on now
+ * (CC_ARM_FFMA2 or CC_ARM_TC), -1 for an invalid descriptor. */
+#define CC_ARM_AUTO 0
+#define CC_ARM_FFMA2 1
+#define CC_ARM_TC 2
+int cc_set_arm_path(int32_t path);
+int32_t cc_get_arm_path(void);
+int32_t cc_arm_path_for(const cc_model_desc* desc);
+
 /* Per-kernel timing (bench.py roofline): between cc_profile_begin() and
  * cc_profile_end(), every kernel the calling thread launches through this
  * library is bracketed by CUDA events recorded on its own stream.

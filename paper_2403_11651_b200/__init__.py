@@ -12,6 +12,7 @@ from .ccrd import (  # noqa: F401
     cc_workspace_bytes_strip, desc_from_config, load, cc_train_param_count, cc_train_workspace_bytes,
     cc_train_step, CcAdam, DeviceTrainer, cc_decode, CcAnalysisDesc, analysis_desc, cc_analysis_param_count,
     cc_analysis_workspace_bytes, cc_analysis_forward, cc_arm_decode, cc_arm_decode_workspace_bytes,
+    cc_set_arm_path, cc_get_arm_path, cc_arm_path_for, arm_path, CC_ARM_AUTO, CC_ARM_FFMA2, CC_ARM_TC,
 )
 
 __version__ = "0.1.0"

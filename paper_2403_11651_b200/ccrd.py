@@ -88,7 +88,11 @@ EXPORTS = ["cc_workspace_bytes", "cc_rd_forward", "cc_workspace_bytes_host", "cc
            "cc_profile_begin", "cc_profile_end", "cc_strip_window", "cc_strip_latent_count",
            "cc_workspace_bytes_strip", "cc_rd_forward_strip", "cc_train_param_count",
            "cc_train_workspace_bytes", "cc_train_step", "cc_decode", "cc_analysis_param_count",
-           "cc_analysis_workspace_bytes", "cc_analysis_forward", "cc_arm_decode_workspace_bytes", "cc_arm_decode"]
+           "cc_analysis_workspace_bytes", "cc_analysis_forward", "cc_arm_decode_workspace_bytes", "cc_arm_decode",
+           "cc_set_arm_path", "cc_get_arm_path", "cc_arm_path_for"]
+
+# ARM rate paths (include/ccrd.h)
+CC_ARM_AUTO, CC_ARM_FFMA2, CC_ARM_TC = 0, 1, 2
 
 _lib = None
 
@@ -167,6 +171,11 @@ def load(rebuild_if_stale: bool = True) -> C.CDLL:
     L.cc_decode.argtypes = [D, V, V, V, V, V, S, V]
     L.cc_train_step.restype = C.c_int
     L.cc_train_step.argtypes = [D, V, V, V, V, V, P(CcAdam), V, V, V, S, V]
+    L.cc_set_arm_path.restype = C.c_int
+    L.cc_set_arm_path.argtypes = [C.c_int32]
+    L.cc_get_arm_path.restype = C.c_int32
+    L.cc_arm_path_for.restype = C.c_int32
+    L.cc_arm_path_for.argtypes = [D]
     _lib = L
     return L
 
@@ -364,6 +373,34 @@ def cc_train_step(desc, params_ptr, noise_ptr, image_ptr, m_ptr, v_ptr, opt: Opt
 
 def cc_last_launch_count() -> int:
     return load().cc_last_launch_count()
+
+
+def cc_set_arm_path(path: int) -> None:
+    _check(load().cc_set_arm_path(path), "cc_set_arm_path")
+
+
+def cc_get_arm_path() -> int:
+    return load().cc_get_arm_path()
+
+
+def cc_arm_path_for(desc) -> int:
+    return load().cc_arm_path_for(C.byref(desc))
+
+
+class arm_path:
+    """Context manager: run a block with a given ARM path, then restore."""
+
+    def __init__(self, path: int):
+        self.path, self.old = path, None
+
+    def __enter__(self):
+        self.old = cc_get_arm_path()
+        cc_set_arm_path(self.path)
+        return self
+
+    def __exit__(self, *exc):
+        cc_set_arm_path(self.old)
+        return False
 
 
 def cc_profile_begin() -> None:

@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <vector>
 #include <cstdio>
+#include <atomic>
 #include <cstring>
 
 #include "ccrd_common.cuh"
@@ -167,22 +168,31 @@ int device_sm_count() {
   return sms;
 }
 
-// ARM path: the FFMA2 kernel (arm_rate.cu) by default -- measured faster than
-// the tensor-core kernel (arm_tc.cu).  CCRD_ARM_PATH=tc selects
-// the tensor-core kernel for the shapes it is compiled for (read once).
-static bool arm_use_tc(const cc_model_desc& d) {
-  static int want_tc = -1;
-  if (want_tc < 0) {
+// ARM path (cc_set_arm_path; initial value from CCRD_ARM_PATH = ffma2 | tc):
+// AUTO = the tensor-core warpgroup kernel (arm_tc.cu) for the shapes it is
+// compiled for -- measured 79 vs 140 us per 2K image against the FFMA2 kernel
+// (arm_rate.cu), which serves every other shape; FFMA2 / TC force a path.
+static std::atomic<int> g_arm_path{-1};
+static int arm_path() {
+  int v = g_arm_path.load(std::memory_order_relaxed);
+  if (v < 0) {
     const char* e = getenv("CCRD_ARM_PATH");
-    want_tc = (e && strcmp(e, "tc") == 0) ? 1 : 0;
+    v = (e && strcmp(e, "ffma2") == 0) ? CC_ARM_FFMA2 : (e && strcmp(e, "tc") == 0) ? CC_ARM_TC : CC_ARM_AUTO;
+    int expect = -1;
+    g_arm_path.compare_exchange_strong(expect, v);
+    v = g_arm_path.load();
   }
-  return want_tc && find_arm_tc_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1) != nullptr;
+  return v;
+}
+static bool arm_use_tc(const cc_model_desc& d) {
+  return arm_path() != CC_ARM_FFMA2 && find_arm_tc_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1) != nullptr;
 }
 static ArmLaunchFn arm_launcher(const cc_model_desc& d) {
   return arm_use_tc(d) ? find_arm_tc_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1)
                        : find_arm_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1);
 }
-static int arm_partials_per_tile(const cc_model_desc& d) { return arm_use_tc(d) ? 16 : ARM_TY; }
+static int arm_partials_per_tile(const cc_model_desc& d) { return arm_use_tc(d) ? arm_tc_partials_per_tile() : ARM_TY; }
+constexpr int ARM_PARTIALS_CAP = 16;  // per tile, any path: the workspace layout does not depend on the path
 
 static int validate(const cc_model_desc* dp) {
   if (!dp) return fail(CC_EINVAL, "null descriptor");
@@ -272,10 +282,15 @@ static void syn_geom(const cc_model_desc& d, const cc_strip* win, SynGeom& g) {
   g.n_tiles = g.tiles_x * ((g.y1 - g.y0 + SYN_TH - 1) / SYN_TH);
 }
 
-static int n_arm_partials(const cc_model_desc& d, const cc_strip* win) {  // one per ARM warp
+static int n_arm_partials(const cc_model_desc& d, const cc_strip* win) {  // written by the current path
   ArmGeom g;
   arm_geom(d, win, g);
   return g.tile_begin[d.L] * arm_partials_per_tile(d);
+}
+static int n_arm_cap(const cc_model_desc& d, const cc_strip* win) {  // reserved (synthesis partials follow)
+  ArmGeom g;
+  arm_geom(d, win, g);
+  return g.tile_begin[d.L] * ARM_PARTIALS_CAP;
 }
 static int n_syn_ctas(const cc_model_desc& d, const cc_strip* win) {
   SynGeom g;
@@ -301,7 +316,7 @@ static void pyr_geom(const cc_model_desc& d, const cc_strip* win, PyrGeom& g) {
 // Workspace per image: ARM partials + synthesis partials (fp64) + a result
 // scratch slot used by the stage entries + the upsampling pyramid S_1..S_{L-2}
 static size_t partial_bytes(const cc_model_desc& d, const cc_strip* win) {
-  return align256(sizeof(double) * (size_t)(n_arm_partials(d, win) + n_syn_ctas(d, win))) +
+  return align256(sizeof(double) * (size_t)(n_arm_cap(d, win) + n_syn_ctas(d, win))) +
          align256(sizeof(cc_rd_result));
 }
 // 2-D TConv (up_2d): the dense [L][H][W] level-0 tensor after the pyramid
@@ -361,7 +376,7 @@ static ReduceJob make_job(const cc_model_desc& d, const cc_strip* win, double* p
   j.n_arm = n_arm_partials(d, win);
   j.n_syn = n_syn_ctas(d, win);
   j.arm_partial = part;
-  j.syn_partial = part + j.n_arm;
+  j.syn_partial = part + n_arm_cap(d, win);
   const double P = (double)d.H * (double)d.W;
   j.inv_3p = 1.0 / (3.0 * P);
   j.lambda_over_p = d.lambda / P;
@@ -476,7 +491,7 @@ static int forward_batch(const cc_model_desc& d, const cc_strip* win, const int1
                          const cudaEvent_t* arm_wait = nullptr, const cudaEvent_t* syn_wait = nullptr) {
   PyrGeom pg;
   pyr_geom(d, win, pg);
-  const int n_arm = n_arm_partials(d, win);
+  const int n_arm = n_arm_cap(d, win);  // synthesis partials start here
   int rc;
   if (d.up_2d) {  // Table 1 2-D TConv: full pyramid -> dense, then synthesis from it
     static thread_local Pyr2dImage im2[MAX_JOBS_PER_LAUNCH];
@@ -603,6 +618,18 @@ int cc_profile_end(cc_profile_summary* out) {
   return cuda_check("cc_profile_end");
 }
 int64_t cc_last_launch_count(void) { return g_launches; }
+
+int cc_set_arm_path(int32_t path) {
+  if (path != CC_ARM_AUTO && path != CC_ARM_FFMA2 && path != CC_ARM_TC)
+    return fail(CC_EINVAL, "arm path must be CC_ARM_AUTO, CC_ARM_FFMA2 or CC_ARM_TC (got %d)", path);
+  g_arm_path.store(path);
+  return CC_OK;
+}
+int32_t cc_get_arm_path(void) { return arm_path(); }
+int32_t cc_arm_path_for(const cc_model_desc* desc) {
+  if (validate(desc) != CC_OK) return -1;
+  return arm_use_tc(*desc) ? CC_ARM_TC : CC_ARM_FFMA2;
+}
 
 int cc_validate(const cc_model_desc* desc) { return validate(desc); }
 

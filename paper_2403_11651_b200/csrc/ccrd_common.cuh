@@ -25,6 +25,11 @@ __device__ __forceinline__ float2 f2unpack(uint64_t v) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
   return r;
 }
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
   uint64_t d;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
@@ -258,6 +263,7 @@ typedef int (*SynLaunchFn)(const SynGeom& g, const cc_model_desc& d, const float
 
 ArmLaunchFn find_arm_launcher(int C, int NH, int NHL);     // FFMA2 path (arm_rate.cu)
 ArmLaunchFn find_arm_tc_launcher(int C, int NH, int NHL);  // tensor-core path (arm_tc.cu)
+int arm_tc_partials_per_tile();                            // rate partials per tile of that path
 int device_sm_count();  // current device's SMs (lazily cached; 148 without a device)
 
 // N-O analysis transform (analysis.cu, NEXT-4)

@@ -15,8 +15,11 @@ import paper_2403_11651_b200 as P  # noqa: E402
 import workload  # noqa: E402
 
 assert os.environ.get("CCRD_ARM_PATH") == "tc"
+# (W = 512 / 1024: every grid's rows 16-byte strided -> the TMA window path of
+# arm_tcg_kernel; the other widths take its LDG staging path)
 cases = [("ref", 70, 101, None), ("ref", 64, 200, None), ("ref", 71, 133, workload.TABLE1[1079]["arm"]),
-         ("ref", 53, 61, workload.TABLE1[2300]["arm"])]
+         ("ref", 53, 61, workload.TABLE1[2300]["arm"]), ("ref", 77, 512, None),
+         ("ref", 45, 1024, workload.TABLE1[2300]["arm"]), ("ref", 37, 512, workload.TABLE1[1079]["arm"])]
 for name, H, W, arm in cases:
     cfg = workload.CONFIGS[name].replace(H=H, W=W)
     if arm is not None:

@@ -263,3 +263,29 @@ def test_arm_decode_entry_errors_without_gpu():
         with pytest.raises(ccrd.CcError) as e:      # no device: loud failure
             P.cc_arm_decode(d, io, [8], 8, ws_ptr=8, ws_bytes=wsb)
         assert e.value.code == ccrd.CC_ECUDA
+
+
+def test_arm_path_selection_without_gpu():
+    """cc_set_arm_path / cc_arm_path_for (include/ccrd.h): host-only; the
+    tensor-core path covers the [16,24,24,2], [16,16,16,2] and [24,24,24,2]
+    ARMs, every other shape runs FFMA2 whatever is asked."""
+    old = P.cc_get_arm_path()
+    try:
+        with pytest.raises(ccrd.CcError) as e:
+            P.cc_set_arm_path(7)
+        assert e.value.code == ccrd.CC_EINVAL
+        ref = P.desc_from_config(workload.CONFIGS["ref"])
+        low = P.desc_from_config(workload.CONFIGS["low"])
+        t2300 = P.desc_from_config(workload.CONFIGS["t2300"])
+        P.cc_set_arm_path(P.CC_ARM_AUTO)
+        assert P.cc_get_arm_path() == P.CC_ARM_AUTO
+        assert P.cc_arm_path_for(ref) == P.CC_ARM_TC and P.cc_arm_path_for(t2300) == P.CC_ARM_TC
+        assert P.cc_arm_path_for(low) == P.CC_ARM_FFMA2
+        P.cc_set_arm_path(P.CC_ARM_FFMA2)
+        assert P.cc_arm_path_for(ref) == P.CC_ARM_FFMA2
+        ws_ffma2 = P.cc_workspace_bytes(ref, 3)
+        P.cc_set_arm_path(P.CC_ARM_TC)
+        assert P.cc_arm_path_for(ref) == P.CC_ARM_TC and P.cc_arm_path_for(low) == P.CC_ARM_FFMA2
+        assert P.cc_workspace_bytes(ref, 3) == ws_ffma2      # the layout does not depend on the path
+    finally:
+        P.cc_set_arm_path(old)

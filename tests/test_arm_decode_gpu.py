@@ -64,8 +64,12 @@ def encoder_arm(cfg, im):
     rate = torch.zeros(1, dtype=torch.float64, device="cuda")
     wsb = P.cc_workspace_bytes(d, 1)
     ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
-    P.cc_arm_rate(d, lat.data_ptr(), im.arm_w, rate.data_ptr(), mu.data_ptr(), sc.data_ptr(), bits.data_ptr(),
-                  ws.data_ptr(), wsb, torch.cuda.current_stream().cuda_stream)
+    # the decoder shares the FFMA2 encoder's arithmetic (arm_math.cuh): compare
+    # against that path (the tensor-core path agrees within the tolerances of
+    # test_arm_tc_gpu.py, not bit for bit)
+    with P.arm_path(P.CC_ARM_FFMA2):
+        P.cc_arm_rate(d, lat.data_ptr(), im.arm_w, rate.data_ptr(), mu.data_ptr(), sc.data_ptr(), bits.data_ptr(),
+                      ws.data_ptr(), wsb, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     return mu.cpu().numpy(), sc.cpu().numpy(), bits.cpu().numpy(), float(rate.item())
 

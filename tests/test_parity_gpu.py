@@ -26,6 +26,16 @@ def _P():
     return P
 
 
+@pytest.fixture(autouse=True, params=["tc", "ffma2"])
+def arm_path(request):
+    """Every parity case runs on both ARM paths (include/ccrd.h
+    cc_set_arm_path): the tensor-core kernel (the default for the shapes it is
+    compiled for; the others fall back to FFMA2) and the FFMA2 kernel."""
+    P = _P()
+    with P.arm_path(P.CC_ARM_TC if request.param == "tc" else P.CC_ARM_FFMA2):
+        yield request.param
+
+
 def run_forward(cfg, images, with_xhat=True):
     P = _P()
     b = P.DeviceBatch(cfg, images, with_xhat=with_xhat)

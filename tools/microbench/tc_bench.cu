@@ -99,7 +99,7 @@ __global__ void mma_rate(int N, int ts, int n_mma, unsigned long long* cyc) {
   const int t = threadIdx.x, warp = t >> 5;
   for (int i = t; i < 128 * 8 + 64 * 8; i += blockDim.x) sm[i] = 0.0f;
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&tbase)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(su32(&tbase)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (t == 0) {
@@ -118,7 +118,7 @@ __global__ void mma_rate(int N, int ts, int n_mma, unsigned long long* cyc) {
     for (int k = 0; k < n_mma; k++) {
       if (ts)
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
-                     ::"r"(tm), "r"(tm + 128), "l"(db), "r"(idesc), "r"(1));
+                     ::"r"(tm), "r"(tm + 64), "l"(db), "r"(idesc), "r"(1));
       else
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
                      ::"r"(tm), "l"(da), "l"(db), "r"(idesc), "r"(1));
@@ -130,7 +130,131 @@ __global__ void mma_rate(int N, int ts, int n_mma, unsigned long long* cyc) {
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tm));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tm));
+}
+
+
+// NC independent accumulators (D_c at column c * 64), issued round robin: is
+// the ~96-cycle per-MMA cost a dependency on the accumulator or the issue?
+__global__ void mma_chains(int N, int ts, int n_mma, int NC, int acc_mode, unsigned long long* cyc) {
+  extern __shared__ __align__(1024) float sm[];
+  float* sA = sm;
+  float* sB = sm + 128 * 8;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int t = threadIdx.x, warp = t >> 5;
+  for (int i = t; i < 128 * 8 + 64 * 8; i += blockDim.x) sm[i] = 0.0f;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = tbase;
+  if (t == 0) {
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint64_t da = sdesc(su32(sA), 128, 256), db = sdesc(su32(sB), 128, 256);
+    const unsigned long long t0 = clock64();
+    for (int k = 0; k < n_mma; k += NC)
+      for (int c = 0; c < NC; c++) {
+        const uint32_t d = tm + c * 64;
+        const uint32_t acc = acc_mode;
+        if (ts)
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
+                       ::"r"(d), "r"(tm + 448), "l"(db), "r"(idesc), "r"(acc));
+        else
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+                       ::"r"(d), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+      }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)));
+    mbar_wait(su32(&bar), 0);
+    const unsigned long long t1 = clock64();
+    cyc[blockIdx.x] = t1 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+
+
+// warp-wide issue: the whole warp runs the loop, elect.sync picks the issuing
+// lane inside ONE asm block of 8 MMAs (no per-MMA branch / ELECT loop).
+// sep: 8 different accumulators (columns 32 c) or one
+__global__ void mma_burst(int N, int ts, int n_iter, int sep, unsigned long long* cyc, int small = 0) {
+  extern __shared__ __align__(1024) float sm[];
+  float* sA = sm;
+  float* sB = sm + 128 * 8;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int t = threadIdx.x, warp = t >> 5;
+  for (int i = t; i < 128 * 8 + 64 * 8; i += blockDim.x) sm[i] = 0.0f;
+  if (warp == 0) {
+    if (small) asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(su32(&tbase)));
+    else asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = tbase;
+  if (warp == 0) {
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint64_t db = sdesc(su32(sB), 128, 256);
+    const uint64_t da = sdesc(su32(sA), 128, 256);
+    const uint32_t st = sep ? (small ? 8 : 32) : 0;
+    const uint32_t a_t = small ? tm + 96 : tm + 320;
+    const unsigned long long t0 = clock64();
+    for (int it = 0; it < n_iter; it++) {
+      if (ts)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+            "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, 1;\n\t"
+            "@p tcgen05.mma.cta_group::1.kind::tf32 [%4], [%1], %2, %3, 1;\n\t"
+            "@p tcgen05.mma.cta_group::1.kind::tf32 [%5], [%1], %2, %3, 1;\n\t"
+            "@p tcgen05.mma.cta_group::1.kind::tf32 [%6], [%1], %2, %3, 1;\n\t"
+            "@p tcgen05.mma.cta_group::1.kind::tf32 [%7], [%1], %2, %3, 1;\n\t"
+            "@p tcgen05.mma.cta_group::1.kind::tf32 [%8], [%1], %2, %3, 1;\n\t"
+            "@p tcgen05.mma.cta_group::1.kind::tf32 [%9], [%1], %2, %3, 1;\n\t"
+            "@p tcgen05.mma.cta_group::1.kind::tf32 [%10], [%1], %2, %3, 1;\n\t}"
+            ::"r"(tm), "r"(a_t), "l"(db), "r"(idesc), "r"(tm + st), "r"(tm + 2 * st), "r"(tm + 3 * st), "r"(tm + 4 * st),
+            "r"(tm + 5 * st), "r"(tm + 6 * st), "r"(tm + 7 * st));
+      else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+            "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n\t"
+            "@p tcgen05.mma.cta_group::1.kind::tf32 [%4], %1, %2, %3, 1;\n\t"
+            "@p tcgen05.mma.cta_group::1.kind::tf32 [%5], %1, %2, %3, 1;\n\t"
+            "@p tcgen05.mma.cta_group::1.kind::tf32 [%6], %1, %2, %3, 1;\n\t"
+            "@p tcgen05.mma.cta_group::1.kind::tf32 [%7], %1, %2, %3, 1;\n\t"
+            "@p tcgen05.mma.cta_group::1.kind::tf32 [%8], %1, %2, %3, 1;\n\t"
+            "@p tcgen05.mma.cta_group::1.kind::tf32 [%9], %1, %2, %3, 1;\n\t"
+            "@p tcgen05.mma.cta_group::1.kind::tf32 [%10], %1, %2, %3, 1;\n\t}"
+            ::"r"(tm), "l"(da), "l"(db), "r"(idesc), "r"(tm + st), "r"(tm + 2 * st), "r"(tm + 3 * st), "r"(tm + 4 * st),
+            "r"(tm + 5 * st), "r"(tm + 6 * st), "r"(tm + 7 * st));
+    }
+    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+                 "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(&bar)));
+    mbar_wait(su32(&bar), 0);
+    const unsigned long long t1 = clock64();
+    if (t == 0) cyc[blockIdx.x] = t1 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) {
+    if (small) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tm));
+    else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+  }
 }
 
 // N = 24 correctness: D[128 x 24] = A[128 x 8] B[24 x 8]^T, integer operands
@@ -215,7 +339,7 @@ int main() {
     }
   cudaFuncSetAttribute(mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   for (int ts = 0; ts < 2; ts++)
-    for (int N : {16, 24, 32, 48, 64, 128}) {
+    for (int N : {16, 24, 32, 48, 64}) {
       const int n_mma = 2048;
       mma_rate<<<sms, 128, 64 * 1024>>>(N, ts, n_mma, cyc);
       cudaError_t e = cudaDeviceSynchronize();
@@ -229,6 +353,81 @@ int main() {
       m /= sms;
       printf("mma tf32 %s M128 N%-3d K8: %6.2f cyc/MMA (floor 128N/256 = %5.1f) -> %6.0f MAC/cyc/SM\n", ts ? "TS" : "SS", N,
              m / n_mma, 128.0 * N / 256, 128.0 * N * 8 / (m / n_mma));
+    }
+
+  cudaFuncSetAttribute(mma_chains, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  for (int ts = 0; ts < 2; ts++)
+    for (int acc_mode = 1; acc_mode < 1; acc_mode++)
+      for (int N : {24, 32, 64})
+        for (int NC : {1, 2, 4, 7}) {
+          const int n_mma = 2016;
+          mma_chains<<<sms, 128, 64 * 1024>>>(N, ts, n_mma, NC, acc_mode, cyc);
+          cudaError_t e = cudaDeviceSynchronize();
+          if (e != cudaSuccess) {
+            printf("chains error %s\n", cudaGetErrorString(e));
+            return 1;
+          }
+          cudaMemcpy(h, cyc, sizeof(unsigned long long) * sms, cudaMemcpyDeviceToHost);
+          double m = 0;
+          for (int i = 0; i < sms; i++) m += (double)h[i];
+          m /= sms;
+          printf("chains %s acc=%d N%-3d NC %d: %6.2f cyc/MMA (floor %5.1f)\n", ts ? "TS" : "SS", acc_mode, N, NC,
+                 m / n_mma, 128.0 * N / 256);
+        }
+  // several CTAs per SM, one chain each (independent issuers): 4 x 128 columns
+  for (int ctas : {2, 4})
+    for (int N : {24, 32}) {
+      const int n_mma = 2016;
+      cudaFuncSetAttribute(mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 / ctas);
+      mma_rate<<<sms * ctas, 128, 200 * 1024 / ctas>>>(N, 1, n_mma, cyc);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) {
+        printf("multi-cta error %s\n", cudaGetErrorString(e));
+        return 1;
+      }
+      cudaMemcpy(h, cyc, sizeof(unsigned long long) * sms * ctas, cudaMemcpyDeviceToHost);
+      double m = 0;
+      for (int i = 0; i < sms * ctas; i++) m += (double)h[i];
+      m /= sms * ctas;
+      printf("%d CTAs/SM, one TS chain each, N%d: %6.2f cyc per MMA per CTA -> %.2f cyc/MMA per SM\n", ctas, N, m / n_mma,
+             m / n_mma / ctas);
+    }
+
+  cudaFuncSetAttribute(mma_burst, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  for (int ts = 0; ts < 2; ts++)
+    for (int sep = 0; sep < 2; sep++)
+      for (int N : {24, 32, 64, 128}) {
+        const int n_iter = 256;
+        mma_burst<<<sms, 128, 64 * 1024>>>(N, ts, n_iter, sep, cyc);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+          printf("burst error %s\n", cudaGetErrorString(e));
+          return 1;
+        }
+        cudaMemcpy(h, cyc, sizeof(unsigned long long) * sms, cudaMemcpyDeviceToHost);
+        double m = 0;
+        for (int i = 0; i < sms; i++) m += (double)h[i];
+        m /= sms;
+        printf("burst %s sep=%d N%-3d: %6.2f cyc/MMA (floor %5.1f)\n", ts ? "TS" : "SS", sep, N, m / (8.0 * n_iter),
+               128.0 * N / 256);
+      }
+
+  for (int ctas : {2, 4})
+    for (int N : {24, 48}) {
+      const int n_iter = 256;
+      cudaFuncSetAttribute(mma_burst, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 / ctas);
+      mma_burst<<<sms * ctas, 128, 200 * 1024 / ctas>>>(N, 1, n_iter, 0, cyc, 1);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) {
+        printf("burst multi error %s\n", cudaGetErrorString(e));
+        return 1;
+      }
+      cudaMemcpy(h, cyc, sizeof(unsigned long long) * sms * ctas, cudaMemcpyDeviceToHost);
+      double m = 0;
+      for (int i = 0; i < sms * ctas; i++) m += (double)h[i];
+      m /= sms * ctas;
+      printf("burst TS %d CTAs/SM N%d: %6.2f cyc/MMA per CTA -> %.2f per SM\n", ctas, N, m / (8.0 * n_iter),
+             m / (8.0 * n_iter) / ctas);
     }
   // N = 24 correctness
   float *A, *B, *D;
