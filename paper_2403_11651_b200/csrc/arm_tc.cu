@@ -1,45 +1,44 @@
-// arm_tc.cu -- ARM rate on the 5th-generation tensor cores (tcgen05 + TMEM).
+// arm_tc.cu -- ARM rate on the 5th-generation tensor cores (tcgen05 + TMEM),
+// the default ARM path for the shapes compiled here (cc_set_arm_path).
 //
 // Same function as arm_rate.cu (PAPER.md:106-109 ARM f_psi, :120 R term of
 // Eq. 1; Table 1 ARM column; readings #1-#8): for every latent the
 // causal context c, the MLP z1 = ReLU(W0 c + b0), z_{k+1} = ReLU(W_k z_k + b_k
 // [+ z_k]), (mu, s) = W_out z + b_out, then -log2 of the Laplace bin mass.
 //
-// The hidden layers are dense contractions over all latents at once -- [128
-// latents x K] x [K x N] per MMA block -- so they run as tcgen05.mma kind::tf32
-// with fp32 accumulators in TMEM:
-//   * layer 0: A = the context rows, small integers (|y| <= 2^10), EXACT in
-//     tf32, so only the weights are split: W = W_hi + W_lo (tf32 each) and
-//     D = A.W_hi + A.W_lo.  The bias rides on a constant-1 input column.
-//   * hidden layer k >= 1: the activations are arbitrary fp32, split per
-//     element z = z_hi + z_lo (cvt.rna.tf32 + exact subtraction):
-//     D = z_hi.W_hi + z_hi.W_lo + z_lo.W_hi ("3xTF32"): every product is exact
-//     in fp32 and only the z_lo.W_lo term (~2^-22 relative) is dropped, so the
-//     result is fp32-accurate (well inside the 1e-3-bit per-latent and 1e-4
-//     total-rate tolerances).
+// The hidden layers are dense contractions over blocks of 128 latents --
+// [128 x K] x [K x NH] -- run as tcgen05.mma kind::tf32 (M = 128, N = NH) with
+// fp32 accumulators in TMEM, fp32-accurate through a split:
+//   * layer 0: the context is small integers, exact in tf32 (11 significant
+//     bits) when |c| <= 2048, so only the weights are split, W = W_hi + W_lo
+//     (tf32 each): D0 = A0 W_hi + A0 W_lo.  The bias rides on a constant-1
+//     input column.  A window holding a latent outside +-2048 (detected while
+//     staging it) splits the context too, c = c_hi + c_lo, and adds c_lo W;
+//   * the hidden layer: the activations are split per element z = z_hi + z_lo
+//     (z_hi = z truncated to tf32, z_lo = z - z_hi, exact) and
+//     D1 = z_hi W_hi + z_hi W_lo + z_lo W_hi ("3xTF32"): only the z_lo W_lo term
+//     (~2^-22 relative) is dropped;
 //   * the 2-wide output layer, the Laplace bits and the reduction stay on the
-//     CUDA cores (packed FFMA2, uniform weights), one latent per thread.
+//     CUDA cores (packed FFMA2 over input pairs, constant-bank weights).
 //
-// CTA = 128 threads = one MMA block of M = 128 latents at a time: thread t
-// owns latent t of the block, writes row t of the A operand and reads TMEM
-// lane t of the accumulator (warp w <-> lanes 32w .. 32w+31).  A tile of the
-// FFMA2 kernel's geometry (8 rows x 64 latents; same tile table, same window
-// staging) is 4 blocks of 2 rows.  Operands are K-major, no-swizzle canonical
-// layout in shared memory (8-row x 16-byte core matrices; LBO = 128 B between
-// K-adjacent core matrices, SBO = K/4 x 128 B between 8-row groups; the encoding
-// is validated by tools/microbench/tc_probe.cu).  Several CTAs per SM overlap
-// one CTA's MMA wait with the others' CUDA-core work.
-//
-// Status (measured on B200): 142 us per 2K image vs 140 us for
-// the FFMA2 kernel -- each 128-latent block pays two serialised MMA round trips
-// and 4 CTAs per SM do not hide them; a variant with the A operands in TMEM
-// (tcgen05.st, TS MMAs) measured 175 us.  Beating FFMA2 needs a warp-specialised
-// multi-stage pipeline, so this path is opt-in (CCRD_ARM_PATH=tc) and
-// parity-tested, not the default.
+// Every operand that changes per block lives in TMEM (TS MMAs: A from TMEM, B
+// = the weights, K-major no-swizzle canonical layout in shared memory); thread
+// t of a warpgroup owns latent t of a block = TMEM lane t through all stages.
+// Measured constraints that shape the kernels (tools/microbench/tc_bench.cu):
+// one issuing thread sustains one MMA per ~25 cycles, two or more issuers per
+// SM reach the tensor pipe's N-floor; a 6 / 11-MMA batch + commit + wait takes
+// 467 / 569 cycles alone; TMEM loads need several in flight.  Hence several
+// warpgroups per SM, each issuing its own MMA batches (one asm statement per
+// batch), and -- in arm_tcp_kernel, the default -- two blocks in flight per
+// warpgroup so one block's MMA latency overlaps the other's CUDA-core stage.
+// The causal window of each 8 x 64 tile arrives by TMA (zero fill = the zero
+// padding of reading #5) where every grid's rows are 16-byte strided, by
+// predicated LDG otherwise.  DESIGN.md 7.2 has the measurements.
 #include <cuda.h>
 
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "arm_math.cuh"
 #include "ccrd_common.cuh"
@@ -47,24 +46,19 @@
 
 namespace ccrd {
 
-constexpr int TC_THREADS = 128;
-constexpr int TC_M = 128;
-constexpr int TC_CTAS_PER_SM = 4;
+constexpr int TC_M = 128;  // latents per MMA block (TMEM lanes)
 
 __host__ __device__ constexpr int rup(int x, int m) { return (x + m - 1) / m * m; }
 
 template <int C, int NH, int NHL>
 struct ArmTcShape {
   static constexpr int K0 = rup(C + 1, 8);                  // context + bias column
-  static constexpr int NP = rup(NH, 16) < 16 ? 16 : rup(NH, 16);  // MMA N (M = 128 needs N % 16 == 0)
+  static constexpr int NP = rup(NH, 16) < 16 ? 16 : rup(NH, 16);  // weight rows stored (the MMAs use N = NH)
   static constexpr int K1 = rup(NH + 1, 8);                 // hidden + bias column
   static constexpr int NHID = NHL - 1;                      // NH -> NH layers on the tensor cores
   static constexpr int BW0 = NP * K0;                       // floats per weight matrix
   static constexpr int BW1 = NP * K1;
-  static constexpr int A_FLOATS = TC_M * (K0 > 2 * K1 ? K0 : 2 * K1);  // A0 | (A_hi, A_lo)
-  static constexpr int WIN = ARM_SH * ARM_SW;
   static constexpr int B_FLOATS = 2 * BW0 + 2 * NHID * BW1;
-  static constexpr size_t SMEM = sizeof(float) * (size_t)(A_FLOATS + B_FLOATS + WIN) + 64;
   static_assert(NP <= 32, "one 32-column TMEM accumulator");
   static_assert(K0 % 8 == 0 && K1 % 8 == 0, "tcgen05 shape");
 };
@@ -92,478 +86,6 @@ struct ArmTcParams {
   float2 wm[NH / 2], wsl[NH / 2];                         // output layer as input pairs: mu, log-scale
   CUtensorMap tmap[CC_MAX_LEVELS];  // int16 grid l ([rows present][w]) for TMA window loads (arm_tcg_kernel, TMA)
 };
-
-// -log2 Laplace bin mass (identical to arm_rate.cu's; see there)
-__device__ __forceinline__ float laplace_bits_tc(float y, float mu, float s, const ArmGeom& g) {
-  constexpr float LOG2E = 1.4426950408889634f;
-  s = fminf(fmaxf(s, g.lsmin), g.lsmax);
-  const float ibl = exp2f_approx(-s * LOG2E) * LOG2E;
-  const float a = fabsf(y - mu);
-  const float am = fminf(a, 0.5f);
-  const float e1 = exp2f_approx((am - 0.5f) * ibl);
-  const float e2 = exp2f_approx(-(am + 0.5f) * ibl);
-  const float p_in = 1.0f - 0.5f * (e1 + e2);
-  const float bits_in = -log2f_approx(fmaxf(p_in, g.p_floor));
-  const float bits_out = fmaf(a - 0.5f, ibl, 1.0f) - log2f_approx(1.0f - exp2f_approx(-ibl));
-  return fminf(a < 0.5f ? bits_in : bits_out, g.bits_cap);
-}
-
-template <int C, int NH, int NHL>
-__global__ void __launch_bounds__(TC_THREADS, TC_CTAS_PER_SM)
-    arm_tc_kernel(const __grid_constant__ ArmTcParams<C, NH, NHL> p) {
-  using S = ArmTcShape<C, NH, NHL>;
-  constexpr int K0 = S::K0, NP = S::NP, K1 = S::K1;
-  extern __shared__ __align__(1024) float tsm[];
-  float* sA = tsm;                              // A0 [128 x K0] | A_hi, A_lo [128 x K1] each
-  float* sB = tsm + S::A_FLOATS;                // B0 hi, lo, then B1 hi, lo per hidden layer
-  float* win = sB + S::B_FLOATS;                // causal window of the tile (fp32)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(win + S::WIN + (S::WIN & 1));
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
-
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  // weights -> shared memory (canonical layout prepared on the host)
-  {
-    const float4* src0 = reinterpret_cast<const float4*>(&p.B0[0][0]);
-    float4* dst = reinterpret_cast<float4*>(sB);
-    for (int i = t; i < 2 * S::BW0 / 4; i += TC_THREADS) dst[i] = src0[i];
-    if constexpr (S::NHID > 0) {
-      const float4* src1 = reinterpret_cast<const float4*>(&p.B1[0][0][0]);
-      for (int i = t; i < 2 * S::NHID * S::BW1 / 4; i += TC_THREADS) dst[2 * S::BW0 / 4 + i] = src1[i];
-    }
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (t == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
-    asm volatile("fence.mbarrier_init.release.cluster;");
-  }
-  asm volatile("fence.proxy.async.shared::cta;");
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
-  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
-  const uint32_t sA_u = smem_u32(sA), sB_u = smem_u32(sB);
-  uint32_t phase = 0;
-
-  const int n_tiles = p.g.tile_begin[p.g.L];
-#pragma unroll 1
-  for (int b = blockIdx.x; b < n_tiles; b += gridDim.x) {
-    // ---- (level, tile) and the causal window (zero outside the grid)
-    int l = 0;
-#pragma unroll 1
-    while (l + 1 < p.g.L && b >= p.g.tile_begin[l + 1]) l++;
-    const int tl = b - p.g.tile_begin[l];
-    const int ty = tl / p.g.tiles_x[l];
-    const int i0 = p.g.own_lo[l] + ty * ARM_TY, j0 = (tl - ty * p.g.tiles_x[l]) * ARM_TX;
-    const int w = p.g.lv.w[l], rlo = p.g.lv.lo[l], rhi = p.g.lv.hi[l];
-    const int16_t* __restrict__ grid = p.lat + p.g.lv.off[l];
-    {
-      constexpr int IT = (S::WIN + TC_THREADS - 1) / TC_THREADS;
-      int16_t v[IT];
-#pragma unroll
-      for (int k = 0; k < IT; k++) {
-        const int s = t + k * TC_THREADS;
-        const int r = s / ARM_SW, c = s - r * ARM_SW;
-        const int gi = i0 - ARM_HALO_TOP + r, gj = j0 - ARM_HALO_X + c;
-        v[k] = (s < S::WIN && gi >= rlo && gi < rhi && gj >= 0 && gj < w) ? __ldg(grid + (int64_t)(gi - rlo) * w + gj)
-                                                                        : (int16_t)0;
-      }
-      __syncthreads();  // the previous tile's readers of `win` are done
-#pragma unroll
-      for (int k = 0; k < IT; k++) {
-        const int s = t + k * TC_THREADS;
-        if (s < S::WIN) win[s] = (float)v[k];
-      }
-      __syncthreads();
-    }
-
-    // ---- four blocks of 2 rows x 64 latents
-#pragma unroll 1
-    for (int q = 0; q < ARM_TY / 2; q++) {
-      const int ry = 2 * q + (t >> 6), cx = t & 63;  // this thread's latent in the tile
-      const float* center = win + (ry + ARM_HALO_TOP) * ARM_SW + cx + ARM_HALO_X;
-      const float y = center[0];
-      // A0 row t: [context (C), 1 (bias), 0 ...]
-      {
-        float row[K0];
-#pragma unroll
-        for (int c = 0; c < C; c++) row[c] = center[p.g.ctx_off[c]];
-        row[C] = 1.0f;
-#pragma unroll
-        for (int c = C + 1; c < K0; c++) row[c] = 0.0f;
-#pragma unroll
-        for (int c4 = 0; c4 < K0 / 4; c4++)
-          *reinterpret_cast<float4*>(sA + kmaj(t, 4 * c4, K0)) =
-              make_float4(row[4 * c4], row[4 * c4 + 1], row[4 * c4 + 2], row[4 * c4 + 3]);
-      }
-      asm volatile("fence.proxy.async.shared::cta;");
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncthreads();
-      if (t == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll
-        for (int s = 0; s < K0 / 8; s++) {
-          const uint64_t da = umma_desc(sA_u + s * 256, 128, (K0 / 4) * 128);
-          mma_tf32(tmem, da, umma_desc(sB_u + s * 256, 128, (K0 / 4) * 128), IDESC, s > 0);
-          mma_tf32(tmem, da, umma_desc(sB_u + S::BW0 * 4 + s * 256, 128, (K0 / 4) * 128), IDESC, 1);
-        }
-        mma_commit(bar);
-      }
-      mbar_wait(bar, phase);
-      phase ^= 1;
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      float z[NP];
-      tmem_row<NP>(taddr, z);
-#pragma unroll
-      for (int n = 0; n < NH; n++) z[n] = fmaxf(z[n], 0.0f);
-
-      // ---- hidden layers NH -> NH (3xTF32)
-#pragma unroll 1
-      for (int k = 0; k < S::NHID; k++) {
-        float* aH = sA;
-        float* aL = sA + TC_M * K1;
-#pragma unroll
-        for (int c4 = 0; c4 < K1 / 4; c4++) {
-          float hi[4], lo[4];
-#pragma unroll
-          for (int e = 0; e < 4; e++) {
-            const int c = 4 * c4 + e;
-            const float x = (c < NH) ? z[c] : (c == NH ? 1.0f : 0.0f);
-            hi[e] = tf32_rna(x);
-            lo[e] = x - hi[e];
-          }
-          *reinterpret_cast<float4*>(aH + kmaj(t, 4 * c4, K1)) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-          *reinterpret_cast<float4*>(aL + kmaj(t, 4 * c4, K1)) = make_float4(lo[0], lo[1], lo[2], lo[3]);
-        }
-        asm volatile("fence.proxy.async.shared::cta;");
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncthreads();
-        if (t == 0) {
-          asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t bh = sB_u + 4 * (2 * S::BW0 + 2 * k * S::BW1), bl = bh + 4 * S::BW1;
-          const uint32_t ah = sA_u, al = sA_u + 4 * TC_M * K1;
-#pragma unroll
-          for (int s = 0; s < K1 / 8; s++) {
-            const uint64_t dah = umma_desc(ah + s * 256, 128, (K1 / 4) * 128);
-            const uint64_t dal = umma_desc(al + s * 256, 128, (K1 / 4) * 128);
-            const uint64_t dbh = umma_desc(bh + s * 256, 128, (K1 / 4) * 128);
-            const uint64_t dbl = umma_desc(bl + s * 256, 128, (K1 / 4) * 128);
-            mma_tf32(tmem, dah, dbh, IDESC, s > 0);
-            mma_tf32(tmem, dah, dbl, IDESC, 1);
-            mma_tf32(tmem, dal, dbh, IDESC, 1);
-          }
-          mma_commit(bar);
-        }
-        mbar_wait(bar, phase);
-        phase ^= 1;
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        tmem_row<NP>(taddr, z);
-#pragma unroll
-        for (int n = 0; n < NH; n++) z[n] = fmaxf(z[n], 0.0f);
-      }
-
-      // ---- output layer (mu, log-scale) on the CUDA cores, Laplace bits
-      uint64_t o = ldp2(p.bo);
-#pragma unroll
-      for (int n = 0; n < NH; n++) o = ffma2(f2pack(z[n], z[n]), ldp2(p.wo[n]), o);
-      const int i = i0 + ry, j = j0 + cx;
-      float bits = 0.0f;
-      if (i < p.g.own_hi[l] && j < w) {
-        const float2 ms = f2unpack(o);
-        bits = laplace_bits_tc(y, ms.x, ms.y, p.g);
-        if (p.bits != nullptr) {
-          const int64_t qi = p.g.lv.off[l] + (int64_t)(i - rlo) * w + j;
-          p.bits[qi] = bits;
-          if (p.mu) p.mu[qi] = ms.x;
-          if (p.scale) p.scale[qi] = __expf(fminf(fmaxf(ms.y, p.g.lsmin), p.g.lsmax));
-        }
-      }
-#pragma unroll
-      for (int o2 = 16; o2 > 0; o2 >>= 1) bits += __shfl_xor_sync(0xffffffffu, bits, o2);
-      if (lane == 0) p.partial[(int64_t)b * 16 + q * 4 + warp] = (double)bits;
-      // the next block rewrites A and the accumulator: every thread's TMEM load
-      // of this block is complete (wait::ld in tmem_row) before the barrier
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncthreads();
-      asm volatile("tcgen05.fence::after_thread_sync;");
-    }
-  }
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
-}
-
-// ---------------------------------------------------------------- warp-specialised pipeline
-// The same arithmetic as arm_tc_kernel (exact context x [B_hi + B_lo], 3xTF32
-// hidden layer, FFMA2 output layer, the same Laplace bits), pipelined over
-// blocks of 128 latents with dedicated warps, two blocks in flight:
-//   warps 0-3 (front): stage the tile's causal window, gather the contexts of
-//             block b into A0[b % 2]; epilogue 0 of block b-1: TMEM D0 ->
-//             ReLU -> hi / lo split into A1[(b-1) % 2];
-//   warp 8:   allocates TMEM, issues MMA0(b) and MMA1(b-1) as their operands
-//             arrive (mbarriers), commits to the waiting warps;
-//   warps 4-7 (back): epilogue 1 of block b: TMEM D1 -> ReLU -> output layer
-//             -> Laplace bits (y re-read from the int16 latents) -> partials.
-// The serial version pays two MMA round trips per block on the same warps;
-// here the front, back and tensor work of neighbouring blocks overlap.
-constexpr int TW_THREADS = 288;  // 9 warps
-#ifndef CCRD_TW_A1_SLOTS
-#define CCRD_TW_A1_SLOTS 1
-#endif
-constexpr int TW_A1_SLOTS = CCRD_TW_A1_SLOTS;
-
-template <int C, int NH, int NHL>
-struct ArmTcwShape {
-  using S = ArmTcShape<C, NH, NHL>;
-  static constexpr int K0 = S::K0, K1 = S::K1, NP = S::NP;
-  static constexpr int A0F = TC_M * K0;        // floats per A0 slot
-  static constexpr int A1F = 2 * TC_M * K1;    // hi + lo per A1 slot
-  static constexpr int OFF_B = 0;
-  static constexpr int OFF_WIN = S::B_FLOATS;
-  static constexpr int OFF_A0 = OFF_WIN + ((ARM_SH * ARM_SW + 31) / 32) * 32;
-  static constexpr int A1S = TW_A1_SLOTS;  // A1 slots (1: smaller CTA, more CTAs per SM)
-  static constexpr int OFF_A1 = OFF_A0 + 2 * A0F;
-  static constexpr int FLOATS = OFF_A1 + A1S * A1F;
-  static constexpr size_t SMEM = sizeof(float) * (size_t)FLOATS + 16 * 8 + 64;
-  static_assert(S::NHID == 1, "one hidden NH -> NH layer");
-};
-
-__device__ __forceinline__ void tw_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void front_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
-
-template <int C, int NH, int NHL>
-__global__ void __launch_bounds__(TW_THREADS, 1) arm_tcw_kernel(const __grid_constant__ ArmTcParams<C, NH, NHL> p) {
-  using S = ArmTcShape<C, NH, NHL>;
-  using W = ArmTcwShape<C, NH, NHL>;
-  constexpr int K0 = S::K0, NP = S::NP, K1 = S::K1;
-  extern __shared__ __align__(1024) float tsm[];
-  float* sB = tsm + W::OFF_B;
-  float* win = tsm + W::OFF_WIN;
-  float* sA0 = tsm + W::OFF_A0;
-  float* sA1 = tsm + W::OFF_A1;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(tsm + W::FLOATS);
-  uint64_t* a0_full = bars;       // [2] front -> MMA
-  uint64_t* d0_full = bars + 2;   // [2] MMA0 commit
-  uint64_t* a1_full = bars + 4;   // [2] front epilogue 0 -> MMA
-  uint64_t* d1_full = bars + 6;   // [2] MMA1 commit
-  uint64_t* d1_empty = bars + 8;  // [2] back done with D1
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
-
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  {
-    const float4* src0 = reinterpret_cast<const float4*>(&p.B0[0][0]);
-    float4* dst = reinterpret_cast<float4*>(sB);
-    for (int i = t; i < 2 * S::BW0 / 4; i += TW_THREADS) dst[i] = src0[i];
-    const float4* src1 = reinterpret_cast<const float4*>(&p.B1[0][0][0]);
-    for (int i = t; i < 2 * S::BW1 / 4; i += TW_THREADS) dst[2 * S::BW0 / 4 + i] = src1[i];
-  }
-  if (warp == 8) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (t == 0) {
-    for (int k = 0; k < 2; k++) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(smem_u32(a0_full + k)));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(d0_full + k)));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(smem_u32(a1_full + k)));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(d1_full + k)));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(smem_u32(d1_empty + k)));
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;");
-  }
-  asm volatile("fence.proxy.async.shared::cta;");
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = *tmem_slot;  // D0[0], D0[1], D1[0], D1[1]: NP columns each
-  constexpr uint32_t IDESC =
-      (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
-
-  const int n_tiles = p.g.tile_begin[p.g.L];
-  const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  const int nb = 4 * my_tiles;  // blocks of 128 latents (a tile = 8 rows x 64 = 4 blocks)
-  auto tile_of = [&](int b) { return (int)blockIdx.x + (b >> 2) * (int)gridDim.x; };
-
-  if (warp < 4) {
-    // ======================= front: window, gather, epilogue 0
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
-    int l = 0, i0 = 0, j0 = 0;
-#pragma unroll 1
-    for (int b = 0; b <= nb; b++) {
-      if (b < nb) {
-        const int tile = tile_of(b), q = b & 3, s = b & 1;
-        if (q == 0) {  // stage this tile's causal window (fp32, zero outside the grid)
-          l = 0;
-          while (l + 1 < p.g.L && tile >= p.g.tile_begin[l + 1]) l++;
-          const int tl = tile - p.g.tile_begin[l];
-          const int ty = tl / p.g.tiles_x[l];
-          i0 = p.g.own_lo[l] + ty * ARM_TY;
-          j0 = (tl - ty * p.g.tiles_x[l]) * ARM_TX;
-          const int w = p.g.lv.w[l], rlo = p.g.lv.lo[l], rhi = p.g.lv.hi[l];
-          const int16_t* __restrict__ grid = p.lat + p.g.lv.off[l];
-          constexpr int IT = (S::WIN + 127) / 128;
-          int16_t v[IT];
-#pragma unroll
-          for (int k = 0; k < IT; k++) {
-            const int e = t + k * 128;
-            const int r = e / ARM_SW, c = e - r * ARM_SW;
-            const int gi = i0 - ARM_HALO_TOP + r, gj = j0 - ARM_HALO_X + c;
-            v[k] = (e < S::WIN && gi >= rlo && gi < rhi && gj >= 0 && gj < w)
-                       ? __ldg(grid + (int64_t)(gi - rlo) * w + gj) : (int16_t)0;
-          }
-          front_sync();  // every front thread is done with the previous tile's window
-#pragma unroll
-          for (int k = 0; k < IT; k++) {
-            const int e = t + k * 128;
-            if (e < S::WIN) win[e] = (float)v[k];
-          }
-          front_sync();
-        }
-        // A0 row t: [context (C), 1 (bias), 0 ...]   (A0[s] is free: MMA0(b-2) completed,
-        // observed by this warp in epilogue 0 of block b-2)
-        const int ry = 2 * q + (t >> 6), cx = t & 63;
-        const float* center = win + (ry + ARM_HALO_TOP) * ARM_SW + cx + ARM_HALO_X;
-        float row[K0];
-#pragma unroll
-        for (int c = 0; c < C; c++) row[c] = center[p.g.ctx_off[c]];
-        row[C] = 1.0f;
-#pragma unroll
-        for (int c = C + 1; c < K0; c++) row[c] = 0.0f;
-        float* A0 = sA0 + s * W::A0F;
-#pragma unroll
-        for (int c4 = 0; c4 < K0 / 4; c4++)
-          *reinterpret_cast<float4*>(A0 + kmaj(t, 4 * c4, K0)) =
-              make_float4(row[4 * c4], row[4 * c4 + 1], row[4 * c4 + 2], row[4 * c4 + 3]);
-        asm volatile("fence.proxy.async.shared::cta;");
-        __syncwarp();
-        if (lane == 0) tw_arrive(a0_full + s);
-      }
-      if (b >= 1) {  // epilogue 0 of block b-1
-        const int bb = b - 1, s = bb & 1;
-        mbar_wait(d0_full + s, (bb >> 1) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        float z[NP];
-        tmem_row<NP>(taddr + s * NP, z);
-        // the A1 slot of block bb was last read by MMA1(bb - A1S)
-        if (W::A1S == 2 && bb >= 2) mbar_wait(d1_full + s, ((bb >> 1) - 1) & 1);
-        if (W::A1S == 1 && bb >= 1) mbar_wait(d1_full + ((bb - 1) & 1), ((bb - 1) >> 1) & 1);
-        float* aH = sA1 + (W::A1S == 2 ? s : 0) * W::A1F;
-        float* aL = aH + TC_M * K1;
-#pragma unroll
-        for (int c4 = 0; c4 < K1 / 4; c4++) {
-          float hi[4], lo[4];
-#pragma unroll
-          for (int e = 0; e < 4; e++) {
-            const int c = 4 * c4 + e;
-            const float x = (c < NH) ? fmaxf(z[c], 0.0f) : (c == NH ? 1.0f : 0.0f);
-            hi[e] = tf32_rna(x);
-            lo[e] = x - hi[e];
-          }
-          *reinterpret_cast<float4*>(aH + kmaj(t, 4 * c4, K1)) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-          *reinterpret_cast<float4*>(aL + kmaj(t, 4 * c4, K1)) = make_float4(lo[0], lo[1], lo[2], lo[3]);
-        }
-        asm volatile("fence.proxy.async.shared::cta;");
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncwarp();
-        if (lane == 0) tw_arrive(a1_full + s);
-      }
-    }
-  } else if (warp < 8) {
-    // ======================= back: epilogue 1, output layer, Laplace bits
-    const int tb = t - 128;
-    const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-#pragma unroll 1
-    for (int b = 0; b < nb; b++) {
-      const int tile = tile_of(b), q = b & 3, s = b & 1;
-      mbar_wait(d1_full + s, (b >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      float z[NP];
-      tmem_row<NP>(taddr + 2 * NP + s * NP, z);
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncwarp();
-      if (lane == 0) tw_arrive(d1_empty + s);  // D1[s] may be overwritten
-      uint64_t o = ldp2(p.bo);
-#pragma unroll
-      for (int n = 0; n < NH; n++) {
-        const float zn = fmaxf(z[n], 0.0f);
-        o = ffma2(f2pack(zn, zn), ldp2(p.wo[n]), o);
-      }
-      int l = 0;
-      while (l + 1 < p.g.L && tile >= p.g.tile_begin[l + 1]) l++;
-      const int tl = tile - p.g.tile_begin[l];
-      const int ty = tl / p.g.tiles_x[l];
-      const int i = p.g.own_lo[l] + ty * ARM_TY + 2 * q + (tb >> 6);
-      const int j = (tl - ty * p.g.tiles_x[l]) * ARM_TX + (tb & 63);
-      const int w = p.g.lv.w[l], rlo = p.g.lv.lo[l];
-      float bits = 0.0f;
-      if (i < p.g.own_hi[l] && j < w) {
-        const int64_t qi = p.g.lv.off[l] + (int64_t)(i - rlo) * w + j;
-        const float y = (float)__ldg(p.lat + qi);
-        const float2 ms = f2unpack(o);
-        bits = laplace_bits_tc(y, ms.x, ms.y, p.g);
-        if (p.bits != nullptr) {
-          p.bits[qi] = bits;
-          if (p.mu) p.mu[qi] = ms.x;
-          if (p.scale) p.scale[qi] = __expf(fminf(fmaxf(ms.y, p.g.lsmin), p.g.lsmax));
-        }
-      }
-#pragma unroll
-      for (int o2 = 16; o2 > 0; o2 >>= 1) bits += __shfl_xor_sync(0xffffffffu, bits, o2);
-      if (lane == 0) p.partial[(int64_t)tile * 16 + q * 4 + (warp & 3)] = (double)bits;
-    }
-  } else if (lane == 0) {
-    // ======================= MMA issue
-    const uint32_t sB_u = smem_u32(sB), sA0_u = smem_u32(sA0), sA1_u = smem_u32(sA1);
-    auto mma0 = [&](int b) {
-      const int s = b & 1;
-      mbar_wait(a0_full + s, (b >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t a_u = sA0_u + 4 * s * W::A0F, d = tmem + s * NP;
-#pragma unroll
-      for (int k = 0; k < K0 / 8; k++) {
-        const uint64_t da = umma_desc(a_u + k * 256, 128, (K0 / 4) * 128);
-        mma_tf32(d, da, umma_desc(sB_u + k * 256, 128, (K0 / 4) * 128), IDESC, k > 0);
-        mma_tf32(d, da, umma_desc(sB_u + S::BW0 * 4 + k * 256, 128, (K0 / 4) * 128), IDESC, 1);
-      }
-      mma_commit(d0_full + s);
-    };
-    auto mma1 = [&](int b) {
-      const int s = b & 1;
-      mbar_wait(a1_full + s, (b >> 1) & 1);
-      if (b >= 2) mbar_wait(d1_empty + s, ((b >> 1) - 1) & 1);  // back done with D1[s] of block b-2
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t ah = sA1_u + 4 * (W::A1S == 2 ? s : 0) * W::A1F, al = ah + 4 * TC_M * K1, d = tmem + 2 * NP + s * NP;
-      const uint32_t bh = sB_u + 4 * (2 * S::BW0), bl = bh + 4 * S::BW1;
-#pragma unroll
-      for (int k = 0; k < K1 / 8; k++) {
-        const uint64_t dah = umma_desc(ah + k * 256, 128, (K1 / 4) * 128);
-        const uint64_t dal = umma_desc(al + k * 256, 128, (K1 / 4) * 128);
-        const uint64_t dbh = umma_desc(bh + k * 256, 128, (K1 / 4) * 128);
-        const uint64_t dbl = umma_desc(bl + k * 256, 128, (K1 / 4) * 128);
-        mma_tf32(d, dah, dbh, IDESC, k > 0);
-        mma_tf32(d, dah, dbl, IDESC, 1);
-        mma_tf32(d, dal, dbh, IDESC, 1);
-      }
-      mma_commit(d1_full + s);
-    };
-#pragma unroll 1
-    for (int b = 0; b < nb; b++) {
-      mma0(b);
-      if (b >= 1) mma1(b - 1);
-    }
-    if (nb >= 1) mma1(nb - 1);
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
-}
-
 
 // ---------------------------------------------------------------- warpgroup pipelines (the default TC ARM)
 // Measured constraints (tools/microbench/tc_bench.cu, B200): one issuing thread
@@ -597,7 +119,10 @@ struct ArmTcgShape {
   static constexpr int XC = K0 > NH ? K0 : NH;
   static constexpr int YC = K1, DC = NH;
   static constexpr int SLOT = XC + YC + DC;  // TMEM columns per warpgroup
-  static constexpr int NWG = (512 / SLOT) < 6 ? (512 / SLOT) : 6;
+#ifndef CCRD_TCG_NWG
+#define CCRD_TCG_NWG 6  // warpgroups per SM (experiment knob; TMEM caps it at 512 / SLOT)
+#endif
+  static constexpr int NWG = (512 / SLOT) < CCRD_TCG_NWG ? (512 / SLOT) : CCRD_TCG_NWG;
   static constexpr int THREADS = NWG * 128;
   static constexpr int WIN = ARM_SH * ARM_SW;
   static constexpr int WINP = (WIN + 31) / 32 * 32;
@@ -625,7 +150,42 @@ __device__ __forceinline__ int16_t ldg_s16_pred(const int16_t* ptr, bool ok) {
   return v;
 }
 
+#ifndef CCRD_TCG_SPIN
+#define CCRD_TCG_SPIN 0  // 1: plain try_wait spin on the MMA barrier (experiment knob)
+#endif
+#if CCRD_TCG_SPIN
+#define TCG_WAIT(b, ph) mbar_wait(b, ph)
+#else
+#define TCG_WAIT(b, ph) mbar_wait_sleep(b, ph)
+#endif
+
+#ifdef CCRD_TCG_TIMING
+// experiment build: per-CTA sums of phase durations of warpgroup 0, warp 0
+// (clock64), read back by cc_debug_tcg_timing (tools/ only)
+__device__ unsigned long long g_tcg_timing[1024][12];
+#define TCG_T(k)                                                     \
+  if (tw == 0) {                                                     \
+    unsigned long long t_;                                           \
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_));               \
+    if (k > 0) tacc[k - 1] += t_ - tlast;                            \
+    tlast = t_;                                                      \
+  }
+#else
+#define TCG_T(k)
+#endif
+
 __device__ __forceinline__ void wg_sync(int g) { asm volatile("bar.sync %0, 128;" ::"r"(g + 1) : "memory"); }
+
+
+// named barrier of warpgroup g with an OR over its threads' predicates
+__device__ __forceinline__ bool wg_sync_or(int g, bool v) {
+  uint32_t r;
+  asm volatile("{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, %2, 0;\n\tbar.red.or.pred q, %1, 128, p;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+               : "=r"(r)
+               : "r"(g + 1), "r"((int)v)
+               : "memory");
+  return r != 0;
+}
 
 // The context template of reading #4 (SPEC.md:256's nearest-causal list) as
 // compile-time shared-memory offsets dy * ARM_SW + dx: the gather becomes
@@ -648,6 +208,60 @@ static bool is_std_ctx(const cc_model_desc& d) {
       return false;
   return true;
 }
+
+// Windows holding a latent outside +-2048: the context is split exactly,
+// c = c_hi + c_lo (c_hi = c truncated to tf32, c_lo = c - c_hi, both exact in
+// tf32), row <- c_hi and c_lo to TMEM at taddr; MMA0 then adds c_lo (B0_hi +
+// B0_lo) (mma_batch_4t: with |c| up to 2^15 the c_lo B0_lo term is as large
+// as fp32 rounding, so it is kept).
+template <int C>
+__device__ __forceinline__ void split_ctx(float (&row)[C], uint32_t taddr) {
+  float lo[C];
+#pragma unroll
+  for (int c = 0; c < C; c++) {
+    const float h = __uint_as_float(__float_as_uint(row[c]) & 0xFFFFE000u);
+    lo[c] = row[c] - h;
+    row[c] = h;
+  }
+  tmem_st_cols<C>(taddr, lo);
+}
+
+// LDG staging of a tile's fp32 window by the 128 threads of a warpgroup
+// (zero outside the grid); returns whether a latent outside +-2048 is in it
+template <int WIN>
+__device__ __forceinline__ bool stage_window_ldg(const int16_t* lat, const ArmGeom& g, int l, int i0, int j0, float* win,
+                                                 int tw) {
+  const int w = g.lv.w[l], rlo = g.lv.lo[l], rhi = g.lv.hi[l];
+  const int16_t* __restrict__ base = lat + g.lv.off[l] + (int64_t)(i0 - ARM_HALO_TOP - rlo) * w + (j0 - ARM_HALO_X);
+  const bool inner = i0 - ARM_HALO_TOP >= rlo && i0 + ARM_TY <= rhi && j0 - ARM_HALO_X >= 0 && j0 + ARM_TX + ARM_HALO_X <= w;
+  constexpr int IT = (WIN + 127) / 128;
+  int16_t v[IT];
+  int off[IT];
+  bool ok[IT];
+  int r = tw / ARM_SW, c = tw - (tw / ARM_SW) * ARM_SW;
+#pragma unroll
+  for (int k = 0; k < IT; k++) {  // offsets and predicates first (no branches) ...
+    const int gi = i0 - ARM_HALO_TOP + r, gj = j0 - ARM_HALO_X + c;
+    ok[k] = ((k < IT - 1) || (tw + 128 * k < WIN)) && (inner || (gi >= rlo && gi < rhi && gj >= 0 && gj < w));
+    off[k] = r * w + c;
+    c += 128 - ARM_SW;  // + 128 elements = + 1 row + 56 columns, at most one wrap
+    const bool wrap = c >= ARM_SW;
+    c -= wrap ? ARM_SW : 0;
+    r += wrap ? 2 : 1;
+  }
+#pragma unroll
+  for (int k = 0; k < IT; k++) v[k] = ldg_s16_pred(base + off[k], ok[k]);  // ... then every load in flight
+  bool big = false;
+#pragma unroll
+  for (int k = 0; k < IT; k++) {
+    const int e = tw + k * 128;
+    if ((k < IT - 1) || e < WIN) win[e] = (float)v[k];
+    big |= v[k] > 2048 || v[k] < -2048;
+  }
+  return big;
+}
+
+
 
 template <int C, int NH, int NHL, bool STD, bool TMA>
 __global__ void __launch_bounds__(ArmTcgShape<C, NH>::THREADS, 1)
@@ -695,6 +309,10 @@ __global__ void __launch_bounds__(ArmTcgShape<C, NH>::THREADS, 1)
   float* win = wins + g * G::WINP;
   uint64_t* bar = bars + g;
   uint32_t phase = 0;
+#ifdef CCRD_TCG_TIMING
+  unsigned long long tacc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, tlast = 0, tstart = 0, ttile = 0;
+  if (tw == 0) asm volatile("mov.u64 %0, %%clock64;" : "=l"(tstart));
+#endif
   constexpr uint32_t IDESC =
       (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NH >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
   const uint32_t sB_u = smem_u32(sB);
@@ -735,9 +353,13 @@ __global__ void __launch_bounds__(ArmTcgShape<C, NH>::THREADS, 1)
   int it = 0;
 #pragma unroll 1
   for (int tile = (int)blockIdx.x * NWG + g; tile < n_tiles; tile += stride, it++) {
+#ifdef CCRD_TCG_TIMING
+    if (tw == 0) asm volatile("mov.u64 %0, %%clock64;" : "=l"(ttile));
+#endif
     int l, i0, j0;
     locate(tile, l, i0, j0);
     const int w = p.g.lv.w[l], rlo = p.g.lv.lo[l], rhi = p.g.lv.hi[l];
+    bool big = false;
     if constexpr (TMA) {
       // prefetch the next tile's window into the other buffer (its previous
       // contents were converted before this warpgroup's last staging barrier)
@@ -755,64 +377,56 @@ __global__ void __launch_bounds__(ArmTcgShape<C, NH>::THREADS, 1)
         f.z = (float)(int16_t)(q.y & 0xFFFFu);
         f.w = (float)(int16_t)(q.y >> 16);
         *reinterpret_cast<float4*>(win + 4 * u) = f;
+        big |= fmaxf(fmaxf(fabsf(f.x), fabsf(f.y)), fmaxf(fabsf(f.z), fabsf(f.w))) > 2048.0f;
       }
-      wg_sync(g);
     } else
     {  // causal window of the tile (fp32, zero outside the grid); every
        // thread of this warpgroup passed the previous tile's last pre-MMA
-       // barrier, so the previous window has no reader left.  Element e =
-       // (r, c) of the 11 x 72 window, e = tw + 128 k: 32-bit offsets from
-       // the window origin, bounds checks only on edge tiles.
-      const int16_t* __restrict__ base = p.lat + p.g.lv.off[l] + (int64_t)(i0 - ARM_HALO_TOP - rlo) * w + (j0 - ARM_HALO_X);
-      const bool inner = i0 - ARM_HALO_TOP >= rlo && i0 + ARM_TY <= rhi && j0 - ARM_HALO_X >= 0 && j0 + ARM_TX + ARM_HALO_X <= w;
-      constexpr int IT = (G::WIN + 127) / 128;
-      int16_t v[IT];
-      int off[IT];
-      bool ok[IT];
-      int r = tw / ARM_SW, c = tw - (tw / ARM_SW) * ARM_SW;
-#pragma unroll
-      for (int k = 0; k < IT; k++) {  // offsets and predicates first (no branches) ...
-        const int gi = i0 - ARM_HALO_TOP + r, gj = j0 - ARM_HALO_X + c;
-        ok[k] = ((k < IT - 1) || (tw + 128 * k < G::WIN)) &&
-                (inner || (gi >= rlo && gi < rhi && gj >= 0 && gj < w));
-        off[k] = r * w + c;
-        c += 128 - ARM_SW;  // + 128 elements = + 1 row + 56 columns, at most one wrap
-        const bool wrap = c >= ARM_SW;
-        c -= wrap ? ARM_SW : 0;
-        r += wrap ? 2 : 1;
-      }
-#pragma unroll
-      for (int k = 0; k < IT; k++) v[k] = ldg_s16_pred(base + off[k], ok[k]);  // ... then every load in flight
-#pragma unroll
-      for (int k = 0; k < IT; k++) {
-        const int e = tw + k * 128;
-        if ((k < IT - 1) || e < G::WIN) win[e] = (float)v[k];
-      }
-      wg_sync(g);
+       // barrier, so the previous window has no reader left
+      big = stage_window_ldg<G::WIN>(p.lat, p.g, l, i0, j0, win, tw);
     }
+    // a latent outside +-2048 in the window is not exact in tf32 (11
+    // significant bits): this tile splits the context, c = c_hi + c_lo
+    const bool split0 = wg_sync_or(g, big);
+#ifdef CCRD_TCG_TIMING
+    if (tw == 0) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_));
+      tacc[8] += t_ - ttile;
+      tacc[10] += 1;
+    }
+#endif
     float tbits = 0.0f;  // this thread's bits over the tile's 4 blocks
 #pragma unroll 1
     for (int q = 0; q < ARM_TY / 2; q++) {
       const int ry = 2 * q + (tw >> 6), cx = tw & 63;
       const float* center = win + (ry + ARM_HALO_TOP) * ARM_SW + cx + ARM_HALO_X;
       const float y = center[0];
+      TCG_T(0);
       {  // A0 row: [context (C), 1, 0 x 7]
         float row[C], tail[8] = {1.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
         for (int c = 0; c < C; c++) row[c] = center[STD ? std_ctx_dy(c) * ARM_SW + std_ctx_dx(c) : p.g.ctx_off[c]];
+        if (split0) split_ctx<C>(row, tl + cD);  // c_lo -> the D1 columns (free until MMA1)
         tmem_st_cols<C>(tl + cX, row);
         tmem_st_cols<8>(tl + cX + C, tail);
         tmem_wait_st();
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
+      TCG_T(1);
       wg_sync(g);
+      TCG_T(2);
       if (qd == (q & 3)) {  // MMA0: D0 = A0 B0_hi + A0 B0_lo (one elected lane; the issuing warp rotates)
         asm volatile("tcgen05.fence::after_thread_sync;");
-        mma_batch_hilo<K0 / 8>(tmem + cY, tmem + cX, dB0, IDESC, bar, LO0);
+        if (split0)  // + c_lo (B0_hi + B0_lo)
+          mma_batch_4t<K0 / 8, C / 8>(tmem + cY, tmem + cX, tmem + cD, dB0, IDESC, bar, LO0);
+        else
+          mma_batch_hilo<K0 / 8>(tmem + cY, tmem + cX, dB0, IDESC, bar, LO0);
       }
-      mbar_wait_sleep(bar, phase);
+      TCG_WAIT(bar, phase);
       phase ^= 1;
       asm volatile("tcgen05.fence::after_thread_sync;");
+      TCG_T(3);
       {  // epilogue 0: ReLU, z = hi + lo (hi = z truncated to tf32: exact split)
         float z[NH], lo[NH];
         tmem_ld_cols<NH>(tl + cY, z);
@@ -830,14 +444,17 @@ __global__ void __launch_bounds__(ArmTcgShape<C, NH>::THREADS, 1)
         tmem_wait_st();
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
+      TCG_T(4);
       wg_sync(g);
+      TCG_T(5);
       if (qd == (q & 3)) {  // MMA1: D1 = A1_hi B1_hi + A1_hi B1_lo + A1_lo B1_hi
         asm volatile("tcgen05.fence::after_thread_sync;");
         mma_batch_3x<K1 / 8, NH / 8>(tmem + cD, tmem + cY, tmem + cX, dB1, IDESC, bar, LO1);
       }
-      mbar_wait_sleep(bar, phase);
+      TCG_WAIT(bar, phase);
       phase ^= 1;
       asm volatile("tcgen05.fence::after_thread_sync;");
+      TCG_T(6);
       // epilogue 1: ReLU, output layer (mu, log-scale), Laplace bits
       float z[NH];
       tmem_ld_cols<NH>(tl + cD, z);
@@ -865,11 +482,308 @@ __global__ void __launch_bounds__(ArmTcgShape<C, NH>::THREADS, 1)
       // D1 / X / Y are rewritten by the next block only after the next
       // pre-MMA barriers, which every thread reaches after its loads here
       asm volatile("tcgen05.fence::before_thread_sync;");
+      TCG_T(7);
+#ifdef CCRD_TCG_TIMING
+      tacc[7] += 1;  // blocks
+#endif
     }
     // one fp64 partial per warp and tile (fixed order: deterministic)
 #pragma unroll
     for (int o2 = 16; o2 > 0; o2 >>= 1) tbits += __shfl_xor_sync(0xffffffffu, tbits, o2);
     if (lane == 0) p.partial[(int64_t)tile * 4 + qd] = (double)tbits;
+  }
+#ifdef CCRD_TCG_TIMING
+  if (tw == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_));
+    tacc[9] = t_ - tstart;
+  }
+  if (t == 0 && blockIdx.x < 1024)
+    for (int k = 0; k < 12; k++) g_tcg_timing[blockIdx.x][k] = tacc[k];
+#endif
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+
+// ---------------------------------------------------------------- ping-pong warpgroups
+// arm_tcg_kernel's arithmetic with TWO blocks of 128 latents in flight per
+// warpgroup (TMEM slot pair, one mbarrier each): a warpgroup's MMA latency
+// (measured 467 / 569 cycles for the 6 / 11-MMA batches alone,
+// tools/microbench/tc_bench.cu) overlaps the other block's stage instead of
+// idling.  Per pair of blocks (A, B):
+//   wait MMA0(A); epi0(A); MMA1(A) | wait MMA0(B); epi0(B); MMA1(B) |
+//   wait MMA1(A); epi1(A); gather(A'); MMA0(A') | wait MMA1(B); epi1(B); gather(B'); MMA0(B')
+// The blocks of a warpgroup are its tiles' 4 blocks in order (A = q 0 / 2, B =
+// q 1 / 3), so a tile's window is staged before gather(q 0) and its last
+// reader is gather(q 3).
+template <int C, int NH>
+struct ArmTcpShape {
+  using G = ArmTcgShape<C, NH>;
+  static constexpr int SLOT = G::SLOT;                       // TMEM columns per block in flight
+#ifndef CCRD_TCP_NWG
+#define CCRD_TCP_NWG 3
+#endif
+  static constexpr int NWG = (512 / (2 * SLOT)) < CCRD_TCP_NWG ? (512 / (2 * SLOT)) : CCRD_TCP_NWG;
+  static constexpr int THREADS = NWG * 128;
+  static constexpr size_t smem_bytes(int b_floats, bool tma) {
+    return sizeof(float) * ((size_t)b_floats + (size_t)NWG * G::WINP) + (tma ? (size_t)NWG * 2 * G::RAWB : 0) +
+           8 * 4 * NWG + 16;
+  }
+};
+
+#ifndef CCRD_TCP_MAXREG
+#define CCRD_TCP_MAXREG 104  // 384 x 104 + a synthesis CTA (256 x 96) fit one SM's 64 K registers
+#endif
+template <int C, int NH, int NHL, bool STD, bool TMA>
+__global__ void __maxnreg__(CCRD_TCP_MAXREG)
+    arm_tcp_kernel(const __grid_constant__ ArmTcParams<C, NH, NHL> p) {
+  using S = ArmTcShape<C, NH, NHL>;
+  using G = ArmTcgShape<C, NH>;
+  using Q = ArmTcpShape<C, NH>;
+  constexpr int K0 = S::K0, K1 = S::K1, NWG = Q::NWG;
+  extern __shared__ __align__(1024) float tsm[];
+  float* sB = tsm;
+  float* wins = tsm + S::B_FLOATS;
+  int16_t* raws = reinterpret_cast<int16_t*>(wins + NWG * G::WINP);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(raws) + (TMA ? NWG * 2 * G::RAWB : 0));
+  uint64_t* tbars = bars + 2 * NWG;  // TMA: 2 per warpgroup
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tbars + 2 * NWG);
+
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int g = warp >> 2, qd = warp & 3, tw = t & 127;
+  {
+    const float4* src0 = reinterpret_cast<const float4*>(&p.B0[0][0]);
+    float4* dst = reinterpret_cast<float4*>(sB);
+    for (int i = t; i < 2 * S::BW0 / 4; i += Q::THREADS) dst[i] = src0[i];
+    const float4* src1 = reinterpret_cast<const float4*>(&p.B1[0][0][0]);
+    for (int i = t; i < 2 * S::BW1 / 4; i += Q::THREADS) dst[2 * S::BW0 / 4 + i] = src1[i];
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (t < 4 * NWG) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + t)));
+  __shared__ uint32_t s_big[4];  // per warpgroup: some window held a latent outside +-2048
+  if (t < 4) s_big[t] = 0;       // (before the CTA barrier below)
+  asm volatile("fence.mbarrier_init.release.cluster;");
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tl = tmem + ((uint32_t)(qd * 32) << 16);
+  uint32_t cX[2], cY[2], cD[2];
+#pragma unroll
+  for (int s = 0; s < 2; s++) {
+    cX[s] = (uint32_t)((2 * g + s) * G::SLOT);
+    cY[s] = cX[s] + G::XC;
+    cD[s] = cY[s] + G::YC;
+    float cst[8] = {1.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+    tmem_st_cols<8>(tl + cY[s] + NH, cst);  // the constant bias input of A1_hi
+  }
+  tmem_wait_st();
+  float* win = wins + g * G::WINP;
+  uint64_t* bar = bars + 2 * g;  // one per slot
+  uint32_t ph[2] = {0, 0};
+  constexpr uint32_t IDESC =
+      (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NH >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+  const uint32_t sB_u = smem_u32(sB);
+  const uint64_t dB0 = umma_desc(sB_u, 128, (K0 / 4) * 128);
+  const uint64_t dB1 = umma_desc(sB_u + 8 * S::BW0, 128, (K1 / 4) * 128);
+  constexpr uint32_t LO0 = (4 * S::BW0) >> 4, LO1 = (4 * S::BW1) >> 4;
+
+  const int n_tiles = p.g.tile_begin[p.g.L];
+  const int stride = (int)gridDim.x * NWG;
+  const int first = (int)blockIdx.x * NWG + g;
+  const int my_tiles = first < n_tiles ? (n_tiles - 1 - first) / stride + 1 : 0;
+  const int nb = 4 * my_tiles;
+  auto locate = [&](int tile, int& l, int& i0, int& j0) {
+    l = 0;
+#pragma unroll 1
+    while (l + 1 < p.g.L && tile >= p.g.tile_begin[l + 1]) l++;
+    const int tt = tile - p.g.tile_begin[l];
+    const int ty = tt / p.g.tiles_x[l];
+    i0 = p.g.own_lo[l] + ty * ARM_TY;
+    j0 = (tt - ty * p.g.tiles_x[l]) * ARM_TX;
+  };
+  int16_t* raw = raws + g * G::RAWB;
+  auto tma_window = [&](int tile, int b) {
+    int tl_, ti0, tj0;
+    locate(tile, tl_, ti0, tj0);
+    uint64_t* tb = tbars + 2 * g + b;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(tb)), "r"(2 * G::RAWW * ARM_SH)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(raw + b * (G::RAWB / 2))),
+        "l"(reinterpret_cast<uint64_t>(&p.tmap[tl_])), "r"(smem_u32(tb)), "r"(tj0 - ARM_HALO_X - 4),
+        "r"(ti0 - ARM_HALO_TOP - p.g.lv.lo[tl_])
+        : "memory");
+  };
+  // current tile (the one whose window is staged)
+  int c_l = 0, c_i0 = 0, c_j0 = 0, c_it = -1;
+  auto stage = [&](int it) {  // stage the window of this warpgroup's it-th tile
+    const int tile = first + it * stride;
+    locate(tile, c_l, c_i0, c_j0);
+    c_it = it;
+    const int w = p.g.lv.w[c_l], rlo = p.g.lv.lo[c_l], rhi = p.g.lv.hi[c_l];
+    bool big = false;
+    if constexpr (TMA) {
+      if (tw == 0 && it + 1 < my_tiles) tma_window(tile + stride, (it + 1) & 1);
+      mbar_wait(tbars + 2 * g + (it & 1), (it >> 1) & 1);
+      const int16_t* rb = raw + (it & 1) * (G::RAWB / 2);
+      for (int u = tw; u < G::WIN / 4; u += 128) {
+        const int rr = u / (ARM_SW / 4), kk = u - rr * (ARM_SW / 4);
+        const uint2 q = *reinterpret_cast<const uint2*>(rb + rr * G::RAWW + 4 + 4 * kk);
+        float4 f;
+        f.x = (float)(int16_t)(q.x & 0xFFFFu);
+        f.y = (float)(int16_t)(q.x >> 16);
+        f.z = (float)(int16_t)(q.y & 0xFFFFu);
+        f.w = (float)(int16_t)(q.y >> 16);
+        *reinterpret_cast<float4*>(win + 4 * u) = f;
+        big |= fmaxf(fmaxf(fabsf(f.x), fabsf(f.y)), fmaxf(fabsf(f.z), fabsf(f.w))) > 2048.0f;
+      }
+    } else {
+      big = stage_window_ldg<G::WIN>(p.lat, p.g, c_l, c_i0, c_j0, win, tw);
+    }
+    // a latent outside +-2048 in the window is not exact in tf32 (11
+    // significant bits): the tile is redone with a split context after the
+    // main loop (no branch in the hot loop)
+    if (big) s_big[g] = 1;
+    wg_sync(g);
+  };
+  if (TMA && tw == 0 && my_tiles > 0) tma_window(first, 0);
+
+  // per-slot state of the block in flight: centre value, validity, index
+  float ys[2];
+  bool valid[2];
+  int64_t qidx[2];
+  float tbits = 0.0f;
+  // block b (tile b / 4, q = b % 4) into slot s, then MMA0; SPLIT: the exact
+  // path with the context split c = c_hi + c_lo (window staged by the caller)
+  auto gather = [&](int b, int s, auto split_tag) {
+    constexpr bool SPLIT = decltype(split_tag)::value;
+    const int q = b & 3;
+    if (!SPLIT && q == 0) stage(b >> 2);
+    const int ry = 2 * q + (tw >> 6), cx = tw & 63;
+    const float* center = win + (ry + ARM_HALO_TOP) * ARM_SW + cx + ARM_HALO_X;
+    ys[s] = center[0];
+    {
+      float row[C], tail[8] = {1.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int c = 0; c < C; c++) row[c] = center[STD ? std_ctx_dy(c) * ARM_SW + std_ctx_dx(c) : p.g.ctx_off[c]];
+      if constexpr (SPLIT) split_ctx<C>(row, tl + cD[s]);  // c_lo -> the D1 columns (free until MMA1)
+      tmem_st_cols<C>(tl + cX[s], row);
+      tmem_st_cols<8>(tl + cX[s] + C, tail);
+    }
+    const int i = c_i0 + ry, j = c_j0 + cx, w = p.g.lv.w[c_l];
+    valid[s] = i < p.g.own_hi[c_l] && j < w;
+    qidx[s] = p.g.lv.off[c_l] + (int64_t)(i - p.g.lv.lo[c_l]) * w + j;
+    tmem_wait_st();
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    wg_sync(g);
+    if (qd == (b & 3)) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if constexpr (SPLIT)  // + c_lo (B0_hi + B0_lo)
+        mma_batch_4t<K0 / 8, C / 8>(tmem + cY[s], tmem + cX[s], tmem + cD[s], dB0, IDESC, bar + s, LO0);
+      else
+        mma_batch_hilo<K0 / 8>(tmem + cY[s], tmem + cX[s], dB0, IDESC, bar + s, LO0);
+    }
+  };
+  auto epi0 = [&](int b, int s) {
+    TCG_WAIT(bar + s, ph[s]);
+    ph[s] ^= 1;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    float z[NH], lo[NH];
+    tmem_ld_cols<NH>(tl + cY[s], z);
+#pragma unroll
+    for (int n = 0; n < NH; n += 2) {
+      const float r0 = fmaxf(z[n], 0.0f), r1 = fmaxf(z[n + 1], 0.0f);
+      z[n] = __uint_as_float(__float_as_uint(r0) & 0xFFFFE000u);
+      z[n + 1] = __uint_as_float(__float_as_uint(r1) & 0xFFFFE000u);
+      const float2 d = f2unpack(fsub2(f2pack(r0, r1), f2pack(z[n], z[n + 1])));
+      lo[n] = d.x;
+      lo[n + 1] = d.y;
+    }
+    tmem_st_cols<NH>(tl + cY[s], z);
+    tmem_st_cols<NH>(tl + cX[s], lo);
+    tmem_wait_st();
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    wg_sync(g);
+    if (qd == (b & 3)) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      mma_batch_3x<K1 / 8, NH / 8>(tmem + cD[s], tmem + cY[s], tmem + cX[s], dB1, IDESC, bar + s, LO1);
+    }
+  };
+  auto epi1 = [&](int b, int s) {
+    TCG_WAIT(bar + s, ph[s]);
+    ph[s] ^= 1;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    float z[NH];
+    tmem_ld_cols<NH>(tl + cD[s], z);
+    uint64_t am = f2pack(p.bo.x, 0.0f), as = f2pack(p.bo.y, 0.0f);
+#pragma unroll
+    for (int n = 0; n < NH; n += 2) {
+      const uint64_t r2 = f2pack(fmaxf(z[n], 0.0f), fmaxf(z[n + 1], 0.0f));
+      am = ffma2(r2, ldp2(p.wm[n / 2]), am);
+      as = ffma2(r2, ldp2(p.wsl[n / 2]), as);
+    }
+    const float2 m2 = f2unpack(am), s2 = f2unpack(as);
+    const float mu = m2.x + m2.y, ls = s2.x + s2.y;
+    if (valid[s]) {
+      const float bits = laplace_bits(ys[s], mu, ls, p.g);
+      tbits += bits;
+      if (p.bits != nullptr) {
+        p.bits[qidx[s]] = bits;
+        if (p.mu) p.mu[qidx[s]] = mu;
+        if (p.scale) p.scale[qidx[s]] = __expf(fminf(fmaxf(ls, p.g.lsmin), p.g.lsmax));
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    if ((b & 3) == 3) {  // the tile's last block: one fp64 partial per warp
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) tbits += __shfl_xor_sync(0xffffffffu, tbits, o2);
+      if (lane == 0) p.partial[(int64_t)(first + (b >> 2) * stride) * 4 + qd] = (double)tbits;
+      tbits = 0.0f;
+    }
+  };
+
+  if (nb > 0) {
+    const std::integral_constant<bool, false> fast;
+    gather(0, 0, fast);
+    gather(1, 1, fast);
+#pragma unroll 1
+    for (int b = 0; b < nb; b += 2) {
+      epi0(b, 0);
+      epi0(b + 1, 1);
+      epi1(b, 0);
+      if (b + 2 < nb) gather(b + 2, 0, fast);
+      epi1(b + 1, 1);
+      if (b + 3 < nb) gather(b + 3, 1, fast);
+    }
+  }
+  // exact pass: every tile of this warpgroup whose window holds a latent
+  // outside +-2048 again, context split, one block at a time in slot 0 (its
+  // partials and per-latent outputs overwrite the main loop's)
+  if (s_big[g]) {
+    const std::integral_constant<bool, true> split;
+#pragma unroll 1
+    for (int it = 0; it < my_tiles; it++) {
+      locate(first + it * stride, c_l, c_i0, c_j0);
+      const bool big = stage_window_ldg<G::WIN>(p.lat, p.g, c_l, c_i0, c_j0, win, tw);
+      if (wg_sync_or(g, big)) {
+#pragma unroll 1
+        for (int q = 0; q < 4; q++) {
+          gather(4 * it + q, 0, split);
+          epi0(4 * it + q, 0);
+          epi1(4 * it + q, 0);
+        }
+      }
+      wg_sync(g);  // the window's readers are done before the next tile overwrites it
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -977,48 +891,42 @@ static int launch_arm_tc(const ArmGeom& g, const cc_model_desc& d, const float* 
 
   const int tiles = g.tile_begin[g.L];
   if (tiles == 0) return 0;
-  static const bool ss = getenv("CCRD_ARM_TC_SS") && getenv("CCRD_ARM_TC_SS")[0] == '1';  // the serial version
-  static const bool ws = getenv("CCRD_ARM_TC_WS") && getenv("CCRD_ARM_TC_WS")[0] == '1';  // warp-specialised
-  if constexpr (NHL == 2) {
-    if (!ss && !ws) {  // default: warpgroup pipelines
-      using G = ArmTcgShape<C, NH>;
-      constexpr size_t smem_t = G::smem_bytes(S::B_FLOATS, true), smem_n = G::smem_bytes(S::B_FLOATS, false);
-      static bool attr_g = false;
-      if (!attr_g) {
-        cudaFuncSetAttribute(arm_tcg_kernel<C, NH, NHL, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t);
-        cudaFuncSetAttribute(arm_tcg_kernel<C, NH, NHL, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t);
-        cudaFuncSetAttribute(arm_tcg_kernel<C, NH, NHL, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_n);
-        cudaFuncSetAttribute(arm_tcg_kernel<C, NH, NHL, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_n);
-        attr_g = true;
-      }
-      const bool tma = arm_tma_maps(g, lat, p.tmap);
-      const int need = (tiles + G::NWG - 1) / G::NWG, cap = device_sm_count();
-      const bool sc = is_std_ctx(d);
-      auto kern = tma ? (sc ? arm_tcg_kernel<C, NH, NHL, true, true> : arm_tcg_kernel<C, NH, NHL, false, true>)
-                      : (sc ? arm_tcg_kernel<C, NH, NHL, true, false> : arm_tcg_kernel<C, NH, NHL, false, false>);
-      kern<<<need < cap ? need : cap, G::THREADS, tma ? smem_t : smem_n, stream>>>(p);
-      return 1;
+  const bool tma = arm_tma_maps(g, lat, p.tmap);
+  const bool sc = is_std_ctx(d);
+  // default: ping-pong warpgroups (two blocks in flight each, arm_tcp_kernel);
+  // CCRD_ARM_TC_PP=0 selects the one-block warpgroups (arm_tcg_kernel)
+  static const bool pp = !(getenv("CCRD_ARM_TC_PP") && getenv("CCRD_ARM_TC_PP")[0] == '0');
+  if (pp) {
+    using Q = ArmTcpShape<C, NH>;
+    constexpr size_t qs_t = Q::smem_bytes(S::B_FLOATS, true), qs_n = Q::smem_bytes(S::B_FLOATS, false);
+    static bool attr_p = false;
+    if (!attr_p) {
+      cudaFuncSetAttribute(arm_tcp_kernel<C, NH, NHL, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qs_t);
+      cudaFuncSetAttribute(arm_tcp_kernel<C, NH, NHL, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qs_t);
+      cudaFuncSetAttribute(arm_tcp_kernel<C, NH, NHL, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qs_n);
+      cudaFuncSetAttribute(arm_tcp_kernel<C, NH, NHL, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qs_n);
+      attr_p = true;
     }
-    if (!ss) {
-      using W = ArmTcwShape<C, NH, NHL>;
-      static bool attr_w = false;
-      if (!attr_w) {
-        cudaFuncSetAttribute(arm_tcw_kernel<C, NH, NHL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W::SMEM);
-        attr_w = true;
-      }
-      const int per_sm = (int)((227u * 1024u) / W::SMEM) < 1 ? 1 : (int)((227u * 1024u) / W::SMEM);
-      const int cap = per_sm * device_sm_count();
-      arm_tcw_kernel<C, NH, NHL><<<tiles < cap ? tiles : cap, TW_THREADS, W::SMEM, stream>>>(p);
-      return 1;
-    }
+    const int need = (tiles + Q::NWG - 1) / Q::NWG, cap = device_sm_count();
+    auto kp = tma ? (sc ? arm_tcp_kernel<C, NH, NHL, true, true> : arm_tcp_kernel<C, NH, NHL, false, true>)
+                  : (sc ? arm_tcp_kernel<C, NH, NHL, true, false> : arm_tcp_kernel<C, NH, NHL, false, false>);
+    kp<<<need < cap ? need : cap, Q::THREADS, tma ? qs_t : qs_n, stream>>>(p);
+    return 1;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(arm_tc_kernel<C, NH, NHL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
-    attr = true;
+  using G = ArmTcgShape<C, NH>;
+  constexpr size_t smem_t = G::smem_bytes(S::B_FLOATS, true), smem_n = G::smem_bytes(S::B_FLOATS, false);
+  static bool attr_g = false;
+  if (!attr_g) {
+    cudaFuncSetAttribute(arm_tcg_kernel<C, NH, NHL, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t);
+    cudaFuncSetAttribute(arm_tcg_kernel<C, NH, NHL, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t);
+    cudaFuncSetAttribute(arm_tcg_kernel<C, NH, NHL, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_n);
+    cudaFuncSetAttribute(arm_tcg_kernel<C, NH, NHL, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_n);
+    attr_g = true;
   }
-  const int cap = TC_CTAS_PER_SM * device_sm_count();
-  arm_tc_kernel<C, NH, NHL><<<tiles < cap ? tiles : cap, TC_THREADS, S::SMEM, stream>>>(p);
+  const int need = (tiles + G::NWG - 1) / G::NWG, cap = device_sm_count();
+  auto kern = tma ? (sc ? arm_tcg_kernel<C, NH, NHL, true, true> : arm_tcg_kernel<C, NH, NHL, false, true>)
+                  : (sc ? arm_tcg_kernel<C, NH, NHL, true, false> : arm_tcg_kernel<C, NH, NHL, false, false>);
+  kern<<<need < cap ? need : cap, G::THREADS, tma ? smem_t : smem_n, stream>>>(p);
   return 1;
 }
 
@@ -1035,12 +943,8 @@ static const ArmTcEntry kArmTc[] = {
     {24, 24, 2, launch_arm_tc<24, 24, 2>},
 };
 
-// rate partials per 8 x 64 tile written by the selected tensor-core kernel
-int arm_tc_partials_per_tile() {
-  static const bool ss = getenv("CCRD_ARM_TC_SS") && getenv("CCRD_ARM_TC_SS")[0] == '1';
-  static const bool ws = getenv("CCRD_ARM_TC_WS") && getenv("CCRD_ARM_TC_WS")[0] == '1';
-  return (ss || ws) ? 16 : 4;
-}
+// rate partials per 8 x 64 tile written by the tensor-core kernels (one per warp)
+int arm_tc_partials_per_tile() { return 4; }
 
 ArmLaunchFn find_arm_tc_launcher(int C, int NH, int NHL) {
   for (const auto& e : kArmTc)
@@ -1049,3 +953,9 @@ ArmLaunchFn find_arm_tc_launcher(int C, int NH, int NHL) {
 }
 
 }  // namespace ccrd
+
+#ifdef CCRD_TCG_TIMING
+extern "C" int cc_debug_tcg_timing(unsigned long long* host, int n_cta) {
+  return (int)cudaMemcpyFromSymbol(host, ccrd::g_tcg_timing, sizeof(unsigned long long) * 12 * (size_t)n_cta);
+}
+#endif

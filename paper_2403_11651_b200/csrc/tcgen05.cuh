@@ -265,4 +265,40 @@ __device__ __forceinline__ void mma_batch_3x<3, 2>(uint32_t d, uint32_t ah, uint
       ::"r"(d), "r"(ah), "r"(idesc), "l"(bh), "r"(smem_u32(bar)), "r"(al), "r"(lo_off16));
 }
 
+// exact-context layer 0: D = A_hi (B_hi + B_lo) [KS1 k-steps] + A_lo (B_hi + B_lo) [KSL k-steps]
+template <int KS1, int KSL>
+__device__ __forceinline__ void mma_batch_4t(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint32_t idesc,
+                                             uint64_t* bar, uint32_t lo_off16);
+#define CCRD_4T_LO_HEAD "mov.b64 bh, b0;\n\tcvt.u64.u32 bl, %6;\n\tadd.s64 bl, bh, bl;\n\tmov.b32 a, %5;\n\t"
+template <>
+__device__ __forceinline__ void mma_batch_4t<3, 2>(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint32_t idesc,
+                                                   uint64_t* bar, uint32_t lo_off16) {
+  asm volatile(
+      CCRD_3X_HEAD
+      CCRD_MMA_TS("%0", "a", "bh", "0") CCRD_MMA_TS("%0", "a", "bl", "1") CCRD_ADVANCE
+      CCRD_MMA_TS("%0", "a", "bh", "1") CCRD_MMA_TS("%0", "a", "bl", "1") CCRD_ADVANCE
+      CCRD_MMA_TS("%0", "a", "bh", "1") CCRD_MMA_TS("%0", "a", "bl", "1")
+      CCRD_4T_LO_HEAD
+      CCRD_MMA_TS("%0", "a", "bh", "1") CCRD_MMA_TS("%0", "a", "bl", "1") CCRD_ADVANCE
+      CCRD_MMA_TS("%0", "a", "bh", "1") CCRD_MMA_TS("%0", "a", "bl", "1")
+      "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n\t}"
+      ::"r"(d), "r"(ah), "r"(idesc), "l"(bh), "r"(smem_u32(bar)), "r"(al), "r"(lo_off16));
+}
+template <>
+__device__ __forceinline__ void mma_batch_4t<4, 3>(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint32_t idesc,
+                                                   uint64_t* bar, uint32_t lo_off16) {
+  asm volatile(
+      CCRD_3X_HEAD
+      CCRD_MMA_TS("%0", "a", "bh", "0") CCRD_MMA_TS("%0", "a", "bl", "1") CCRD_ADVANCE
+      CCRD_MMA_TS("%0", "a", "bh", "1") CCRD_MMA_TS("%0", "a", "bl", "1") CCRD_ADVANCE
+      CCRD_MMA_TS("%0", "a", "bh", "1") CCRD_MMA_TS("%0", "a", "bl", "1") CCRD_ADVANCE
+      CCRD_MMA_TS("%0", "a", "bh", "1") CCRD_MMA_TS("%0", "a", "bl", "1")
+      CCRD_4T_LO_HEAD
+      CCRD_MMA_TS("%0", "a", "bh", "1") CCRD_MMA_TS("%0", "a", "bl", "1") CCRD_ADVANCE
+      CCRD_MMA_TS("%0", "a", "bh", "1") CCRD_MMA_TS("%0", "a", "bl", "1") CCRD_ADVANCE
+      CCRD_MMA_TS("%0", "a", "bh", "1") CCRD_MMA_TS("%0", "a", "bl", "1")
+      "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n\t}"
+      ::"r"(d), "r"(ah), "r"(idesc), "l"(bh), "r"(smem_u32(bar)), "r"(al), "r"(lo_off16));
+}
+
 }  // namespace ccrd

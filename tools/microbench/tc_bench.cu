@@ -257,6 +257,51 @@ __global__ void mma_burst(int N, int ts, int n_iter, int sep, unsigned long long
   }
 }
 
+
+// latency of a batch of n dependent (same accumulator) TS MMAs + commit +
+// mbarrier wait, issued by one elected lane of warp 0, averaged over reps
+__global__ void mma_latency(int N, int n, int reps, unsigned long long* cyc) {
+  extern __shared__ __align__(1024) float sm[];
+  float* sB = sm;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int t = threadIdx.x, warp = t >> 5;
+  for (int i = t; i < 64 * 8; i += blockDim.x) sm[i] = 0.0f;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(su32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = tbase;
+  if (warp == 0) {
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint64_t db = sdesc(su32(sB), 128, 256);
+    unsigned long long tot = 0;
+    for (int r = 0; r < reps; r++) {
+      const unsigned long long t0 = clock64();
+      for (int k = 0; k < n; k++)
+        asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+                     "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, 1;\n\t}"
+                     ::"r"(tm), "r"(tm + 64), "l"(db), "r"(idesc));
+      asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+                   "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(&bar)));
+      mbar_wait(su32(&bar), r & 1);
+      tot += clock64() - t0;
+    }
+    if (t == 0) cyc[blockIdx.x] = tot / reps;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tm));
+}
+
 // N = 24 correctness: D[128 x 24] = A[128 x 8] B[24 x 8]^T, integer operands
 __global__ void n24(const float* A, const float* B, float* D, int N) {
   __shared__ __align__(1024) float sA[128 * 8];
@@ -310,7 +355,7 @@ __global__ void n24(const float* A, const float* B, float* D, int N) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tm));
 }
 
-int main() {
+int main(int argc, char** argv) {
   int sms = 0, clk = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
@@ -319,6 +364,20 @@ int main() {
   cudaMalloc(&cyc, sizeof(unsigned long long) * 1024);
   cudaMalloc(&sink, sizeof(float) * 1024 * 1024);
   unsigned long long h[1024];
+
+  if (argc > 1 && atoi(argv[1]) == 2) {
+    for (int n : {1, 2, 6, 11, 22})
+      for (int ctas : {1, 4}) {
+        mma_latency<<<sms * ctas, 128, 4096>>>(24, n, 64, cyc);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) { printf("lat error %s\n", cudaGetErrorString(e)); return 1; }
+        cudaMemcpy(h, cyc, sizeof(unsigned long long) * sms * ctas, cudaMemcpyDeviceToHost);
+        double m = 0;
+        for (int i = 0; i < sms * ctas; i++) m += (double)h[i];
+        printf("latency: %2d MMAs (N24) + commit + wait, %d CTA/SM: %6.0f cyc\n", n, ctas, m / (sms * ctas));
+      }
+    return 0;
+  }
   const char* names[] = {"ldtm x32 (wait each)", "sttm x32", "ldtm x32 (2 in flight)"};
   for (int mode = 0; mode < 3; mode++)
     for (int warps : {4, 8, 16}) {
