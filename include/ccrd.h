@@ -357,7 +357,9 @@ int64_t cc_last_launch_count(void);
  *   CC_ARM_TC:    tcgen05 kind::tf32 MMAs with a 3xTF32 split (fp32-accurate,
  *                 DESIGN.md 7.2) for the shapes it is compiled for
  *                 ([16,24,24,2], [16,16,16,2], [24,24,24,2]), FFMA2 otherwise;
- *   CC_ARM_AUTO:  (default) = CC_ARM_TC.
+ *   CC_ARM_AUTO:  (default) the measured-faster path per shape: CC_ARM_TC
+ *                 for the [16,24,24,2] ARM (BASELINE's ~2000 MAC/px config),
+ *                 CC_ARM_FFMA2 for the others.
  * The initial value comes from the environment (CCRD_ARM_PATH = ffma2 | tc).
  * Workspace sizes do not depend on the path.  cc_set_arm_path: CC_EINVAL for
  * an unknown value.  cc_arm_path_for: the path a descriptor runs on now

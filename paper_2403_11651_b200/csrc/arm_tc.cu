@@ -528,6 +528,8 @@ struct ArmTcpShape {
 #endif
   static constexpr int NWG = (512 / (2 * SLOT)) < CCRD_TCP_NWG ? (512 / (2 * SLOT)) : CCRD_TCP_NWG;
   static constexpr int THREADS = NWG * 128;
+  static constexpr int USED = NWG * 2 * SLOT;  // TMEM columns used; the allocation is the next power of two
+  static constexpr int TMEM_COLS = USED <= 32 ? 32 : USED <= 64 ? 64 : USED <= 128 ? 128 : USED <= 256 ? 256 : 512;
   static constexpr size_t smem_bytes(int b_floats, bool tma) {
     return sizeof(float) * ((size_t)b_floats + (size_t)NWG * G::WINP) + (tma ? (size_t)NWG * 2 * G::RAWB : 0) +
            8 * 4 * NWG + 16;
@@ -562,7 +564,7 @@ __global__ void __maxnreg__(CCRD_TCP_MAXREG)
     for (int i = t; i < 2 * S::BW1 / 4; i += Q::THREADS) dst[2 * S::BW0 / 4 + i] = src1[i];
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "n"(Q::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (t < 4 * NWG) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + t)));
@@ -724,19 +726,26 @@ __global__ void __maxnreg__(CCRD_TCP_MAXREG)
     asm volatile("tcgen05.fence::after_thread_sync;");
     float z[NH];
     tmem_ld_cols<NH>(tl + cD[s], z);
-    uint64_t am = f2pack(p.bo.x, 0.0f), as = f2pack(p.bo.y, 0.0f);
+    // output layer: 4 independent FFMA2 chains (2 per output) over input pairs
+    uint64_t am0 = f2pack(p.bo.x, 0.0f), as0 = f2pack(p.bo.y, 0.0f), am1 = 0ull, as1 = 0ull;
 #pragma unroll
-    for (int n = 0; n < NH; n += 2) {
+    for (int n = 0; n < NH; n += 4) {
       const uint64_t r2 = f2pack(fmaxf(z[n], 0.0f), fmaxf(z[n + 1], 0.0f));
-      am = ffma2(r2, ldp2(p.wm[n / 2]), am);
-      as = ffma2(r2, ldp2(p.wsl[n / 2]), as);
+      am0 = ffma2(r2, ldp2(p.wm[n / 2]), am0);
+      as0 = ffma2(r2, ldp2(p.wsl[n / 2]), as0);
+      if (n + 2 < NH) {
+        const uint64_t r3 = f2pack(fmaxf(z[n + 2], 0.0f), fmaxf(z[n + 3], 0.0f));
+        am1 = ffma2(r3, ldp2(p.wm[n / 2 + 1]), am1);
+        as1 = ffma2(r3, ldp2(p.wsl[n / 2 + 1]), as1);
+      }
     }
-    const float2 m2 = f2unpack(am), s2 = f2unpack(as);
-    const float mu = m2.x + m2.y, ls = s2.x + s2.y;
-    if (valid[s]) {
-      const float bits = laplace_bits(ys[s], mu, ls, p.g);
+    const float2 m0 = f2unpack(am0), m1 = f2unpack(am1), s0 = f2unpack(as0), s1 = f2unpack(as1);
+    const float mu = (m0.x + m1.x) + (m0.y + m1.y), ls = (s0.x + s1.x) + (s0.y + s1.y);
+    {  // bits computed unconditionally (no branch around the MUFU chain), masked
+      const float bits_v = laplace_bits(ys[s], mu, ls, p.g);
+      const float bits = valid[s] ? bits_v : 0.0f;
       tbits += bits;
-      if (p.bits != nullptr) {
+      if (valid[s] && p.bits != nullptr) {
         p.bits[qidx[s]] = bits;
         if (p.mu) p.mu[qidx[s]] = mu;
         if (p.scale) p.scale[qidx[s]] = __expf(fminf(fmaxf(ls, p.g.lsmin), p.g.lsmax));
@@ -788,7 +797,7 @@ __global__ void __maxnreg__(CCRD_TCP_MAXREG)
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Q::TMEM_COLS));
 }
 
 // ---------------------------------------------------------------- host launcher
@@ -907,7 +916,7 @@ static int launch_arm_tc(const ArmGeom& g, const cc_model_desc& d, const float* 
       cudaFuncSetAttribute(arm_tcp_kernel<C, NH, NHL, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qs_n);
       attr_p = true;
     }
-    const int need = (tiles + Q::NWG - 1) / Q::NWG, cap = device_sm_count();
+    const int need = (tiles + Q::NWG - 1) / Q::NWG, cap = device_sm_count() * (512 / Q::TMEM_COLS);
     auto kp = tma ? (sc ? arm_tcp_kernel<C, NH, NHL, true, true> : arm_tcp_kernel<C, NH, NHL, false, true>)
                   : (sc ? arm_tcp_kernel<C, NH, NHL, true, false> : arm_tcp_kernel<C, NH, NHL, false, false>);
     kp<<<need < cap ? need : cap, Q::THREADS, tma ? qs_t : qs_n, stream>>>(p);

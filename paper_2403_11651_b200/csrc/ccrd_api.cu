@@ -169,9 +169,9 @@ int device_sm_count() {
 }
 
 // ARM path (cc_set_arm_path; initial value from CCRD_ARM_PATH = ffma2 | tc):
-// AUTO = the tensor-core warpgroup kernel (arm_tc.cu) for the shapes it is
-// compiled for -- measured 79 vs 140 us per 2K image against the FFMA2 kernel
-// (arm_rate.cu), which serves every other shape; FFMA2 / TC force a path.
+// AUTO = the tensor-core kernel (arm_tc.cu) where it measured faster (below),
+// the FFMA2 kernel (arm_rate.cu) elsewhere; FFMA2 / TC force a path (TC for
+// the shapes it is compiled for).
 static std::atomic<int> g_arm_path{-1};
 static int arm_path() {
   int v = g_arm_path.load(std::memory_order_relaxed);
@@ -185,7 +185,15 @@ static int arm_path() {
   return v;
 }
 static bool arm_use_tc(const cc_model_desc& d) {
-  return arm_path() != CC_ARM_FFMA2 && find_arm_tc_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1) != nullptr;
+  const int path = arm_path();
+  if (path == CC_ARM_FFMA2 || find_arm_tc_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1) == nullptr)
+    return false;
+  // AUTO: where the tensor-core kernel measured faster -- the [16,24,24,2] ARM
+  // (2K: 91 vs 140 us; 512x768: 28 vs 27 us with a faster two-stream path).
+  // The Table 1 [16,16,16,2] / [24,24,24,2] ARMs on 512x768 images measured
+  // slower on the tensor cores (path 8.7e9 vs 9.8e9, 6.5e9 vs 6.9e9 px/s).
+  if (path == CC_ARM_AUTO) return d.n_ctx == 16 && d.arm_widths[1] == 24;
+  return true;
 }
 static ArmLaunchFn arm_launcher(const cc_model_desc& d) {
   return arm_use_tc(d) ? find_arm_tc_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1)

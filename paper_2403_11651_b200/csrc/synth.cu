@@ -25,6 +25,7 @@
 #define CCRD_SYN_MC 20  // hidden neurons per MLP chunk (live accumulators)
 #endif
 
+
 namespace ccrd {
 
 #ifdef CCRD_SYN_TIMING
@@ -315,25 +316,25 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
     const int b1lo = (L > 1) ? p.g.lv.lo[1] : 0, b1hi = (L > 1) ? p.g.lv.hi[1] : 1;
     const int lo1 = wlo_r[(L > 1) ? 1 : 0];
     constexpr int NPAIR = (RH0 / 2) * RW0;
-#pragma unroll 1
-    for (int item = threadIdx.x; item < NPAIR; item += SYN_THREADS) {
+    // one item = a pair of rows (2 rp, 2 rp + 1) at column cc: its L dense
+    // values (FFMA2 lane pairs), then after the MLP its 3 outputs per pixel
+    auto dense_of = [&](int item, uint64_t (&v)[L]) {
       const int rp = item / RW0;  // compile-time divisor
       const int cc = item - rp * RW0;
       const int y0 = RY + 2 * rp, x = RX + cc;
-      if (x < 0 || x >= W || y0 + 1 < 0 || y0 >= H) continue;  // never read by the convs
       const bool has1 = (y0 + 1 < H);
-      uint64_t v[L];  // (row y0, row y0 + 1) of every dense channel
       if constexpr (DENSE_IN) {
         // channel 0 straight from the int16 latents when given (the 2-D TConv
         // path: the pyramid fills channels 1 .. L-1), else from the dense tensor
+        const int yc = clampi(y0, 0, H - 1), xc = clampi(x, 0, W - 1);
 #pragma unroll
         for (int l = 0; l < L; l++) {
           if (l == 0 && p.lat != nullptr)
-            v[0] = f2pack((float)__ldg(p.lat + (int64_t)y0 * W + x),
-                          has1 ? (float)__ldg(p.lat + (int64_t)(y0 + 1) * W + x) : 0.0f);
+            v[0] = f2pack((float)__ldg(p.lat + (int64_t)yc * W + xc),
+                          has1 ? (float)__ldg(p.lat + (int64_t)(yc + 1) * W + xc) : 0.0f);
           else
-            v[l] = f2pack(__ldg(p.dense_in + l * P + (int64_t)y0 * W + x),
-                          has1 ? __ldg(p.dense_in + l * P + (int64_t)(y0 + 1) * W + x) : 0.0f);
+            v[l] = f2pack(__ldg(p.dense_in + l * P + (int64_t)yc * W + xc),
+                          has1 ? __ldg(p.dense_in + l * P + (int64_t)(yc + 1) * W + xc) : 0.0f);
         }
       } else {
         v[0] = f2pack((float)lat0[2 * rp * RW0 + cc], (float)lat0[(2 * rp + 1) * RW0 + cc]);
@@ -358,6 +359,17 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
           }
         }
       }
+    };
+    auto needed = [&](int item) {  // read by the convs (inside the image)
+      const int rp = item / RW0, cc = item - (item / RW0) * RW0;
+      const int y0 = RY + 2 * rp, x = RX + cc;
+      return item < NPAIR && !(x < 0 || x >= W || y0 + 1 < 0 || y0 >= H);
+    };
+    auto store = [&](int item, const uint64_t (&v)[L], const uint64_t (&op)[3]) {
+      const int rp = item / RW0;
+      const int cc = item - rp * RW0;
+      const int y0 = RY + 2 * rp, x = RX + cc;
+      const bool has1 = (y0 + 1 < H);
       const bool inx = (x >= X0 && x < X0 + SYN_TW);
       const bool in0 = inx && y0 >= Y0 && y0 < Y0 + SYN_TH;
       const bool in1 = inx && has1 && y0 + 1 >= Y0 && y0 + 1 < Y0 + SYN_TH;
@@ -369,8 +381,6 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
           if (in1) p.dense_out[l * P + (int64_t)(y0 + 1) * W + x] = d.y;
         }
       }
-      uint64_t op[3];
-      mlp_pair<L, CH, R, K>(p, v, op);
       float out0[3], out1[3];
 #pragma unroll
       for (int c = 0; c < 3; c++) {
@@ -391,6 +401,14 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
         hA[c * HP + o] = out0[c];
         hA[c * HP + o + RW0] = out1[c];
       }
+    };
+#pragma unroll 1
+    for (int item = threadIdx.x; item < NPAIR; item += SYN_THREADS) {
+      if (!needed(item)) continue;  // never read by the convs
+      uint64_t v[L], op[3];
+      dense_of(item, v);
+      mlp_pair<L, CH, R, K>(p, v, op);
+      store(item, v, op);
     }
   }
   __syncthreads();
