@@ -69,6 +69,14 @@ __host__ __device__ constexpr int kmaj(int r, int k, int K) {
   return (r >> 3) * (K / 4) * 32 + (k >> 2) * 32 + (r & 7) * 4 + (k & 3);
 }
 
+// host-side packing of the tensor-core ARM's B operands
+template <int C, int NH, int NHL>
+struct ArmTcB {
+  using S = ArmTcShape<C, NH, NHL>;
+  float B0[2][S::BW0];                               // [hi/lo] layer 0 (bias in column C)
+  float B1[(S::NHID > 0) ? S::NHID : 1][2][S::BW1];  // [layer][hi/lo] (residual folded, bias in column NH)
+};
+
 template <int C, int NH, int NHL>
 struct ArmTcParams {
   using S = ArmTcShape<C, NH, NHL>;
@@ -78,12 +86,11 @@ struct ArmTcParams {
   float* mu;        // optional per-latent debug outputs
   float* scale;
   float* bits;
-  // weights, pre-split on the host into tf32 (hi, lo) pairs, canonical layout
-  float B0[2][S::BW0];                                    // [hi/lo] layer 0 (bias in column C)
-  float B1[(S::NHID > 0) ? S::NHID : 1][2][S::BW1];       // [layer][hi/lo] (residual folded, bias in column NH)
   float2 wo[NH];                                          // output layer (mu, log-scale) per input
   float2 bo;
   float2 wm[NH / 2], wsl[NH / 2];                         // output layer as input pairs: mu, log-scale
+  const float* gB;  // the weights, pre-split on the host into tf32 (hi, lo) pairs in the canonical
+                    // K-major layout (ArmTcB), in global memory: bulk-loaded into shared memory
   CUtensorMap tmap[CC_MAX_LEVELS];  // int16 grid l ([rows present][w]) for TMA window loads (arm_tcg_kernel, TMA)
 };
 
@@ -280,23 +287,29 @@ __global__ void __launch_bounds__(ArmTcgShape<C, NH>::THREADS, 1)
 
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int g = warp >> 2, qd = warp & 3, tw = t & 127;  // warpgroup, lane quadrant, latent of the block
-  {
-    const float4* src0 = reinterpret_cast<const float4*>(&p.B0[0][0]);
-    float4* dst = reinterpret_cast<float4*>(sB);
-    for (int i = t; i < 2 * S::BW0 / 4; i += G::THREADS) dst[i] = src0[i];
-    const float4* src1 = reinterpret_cast<const float4*>(&p.B1[0][0][0]);
-    for (int i = t; i < 2 * S::BW1 / 4; i += G::THREADS) dst[2 * S::BW0 / 4 + i] = src1[i];
-  }
+  __shared__ __align__(8) uint64_t wbar;  // the weights' bulk copy
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (t < 3 * NWG) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + t)));
+  if (t == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&wbar)));
   asm volatile("fence.mbarrier_init.release.cluster;");
   asm volatile("fence.proxy.async.shared::cta;");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
+  // the split weights (B operands, ~14 KB) in one bulk copy from global memory
+  // (a per-thread copy from the kernel-parameter bank serialises in the
+  // constant cache: ~7 % of the kernel's stall samples)
+  if (t == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&wbar)), "r"(4 * S::B_FLOATS)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(sB)),
+                 "l"(p.gB), "r"(4 * S::B_FLOATS), "r"(smem_u32(&wbar))
+                 : "memory");
+  }
   const uint32_t tmem = *tmem_slot;
   const uint32_t tl = tmem + ((uint32_t)(qd * 32) << 16);  // this warp's lanes
   const uint32_t cX = (uint32_t)(g * G::SLOT), cY = cX + G::XC, cD = cY + G::YC;
@@ -350,6 +363,7 @@ __global__ void __launch_bounds__(ArmTcgShape<C, NH>::THREADS, 1)
         : "memory");
   };
   if (TMA && tw == 0 && (int)blockIdx.x * NWG + g < n_tiles) tma_window((int)blockIdx.x * NWG + g, 0);
+  mbar_wait(&wbar, 0);  // the weights are in shared memory
   int it = 0;
 #pragma unroll 1
   for (int tile = (int)blockIdx.x * NWG + g; tile < n_tiles; tile += stride, it++) {
@@ -556,18 +570,13 @@ __global__ void __maxnreg__(CCRD_TCP_MAXREG)
 
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int g = warp >> 2, qd = warp & 3, tw = t & 127;
-  {
-    const float4* src0 = reinterpret_cast<const float4*>(&p.B0[0][0]);
-    float4* dst = reinterpret_cast<float4*>(sB);
-    for (int i = t; i < 2 * S::BW0 / 4; i += Q::THREADS) dst[i] = src0[i];
-    const float4* src1 = reinterpret_cast<const float4*>(&p.B1[0][0][0]);
-    for (int i = t; i < 2 * S::BW1 / 4; i += Q::THREADS) dst[2 * S::BW0 / 4 + i] = src1[i];
-  }
+  __shared__ __align__(8) uint64_t wbar;  // the weights' bulk copy
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "n"(Q::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (t < 4 * NWG) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + t)));
+  if (t == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&wbar)));
   __shared__ uint32_t s_big[4];  // per warpgroup: some window held a latent outside +-2048
   if (t < 4) s_big[t] = 0;       // (before the CTA barrier below)
   asm volatile("fence.mbarrier_init.release.cluster;");
@@ -575,6 +584,17 @@ __global__ void __maxnreg__(CCRD_TCP_MAXREG)
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
+  // the split weights (B operands, ~14 KB) in one bulk copy from global memory
+  // (a per-thread copy from the kernel-parameter bank serialises in the
+  // constant cache: ~7 % of the kernel's stall samples)
+  if (t == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&wbar)), "r"(4 * S::B_FLOATS)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(sB)),
+                 "l"(p.gB), "r"(4 * S::B_FLOATS), "r"(smem_u32(&wbar))
+                 : "memory");
+  }
   const uint32_t tmem = *tmem_slot;
   const uint32_t tl = tmem + ((uint32_t)(qd * 32) << 16);
   uint32_t cX[2], cY[2], cD[2];
@@ -687,6 +707,7 @@ __global__ void __maxnreg__(CCRD_TCP_MAXREG)
     tmem_wait_st();
     asm volatile("tcgen05.fence::before_thread_sync;");
     wg_sync(g);
+    if (b < 2) mbar_wait(&wbar, 0);  // the first use of the weights in shared memory
     if (qd == (b & 3)) {
       asm volatile("tcgen05.fence::after_thread_sync;");
       if constexpr (SPLIT)  // + c_lo (B0_hi + B0_lo)
@@ -862,8 +883,10 @@ static int launch_arm_tc(const ArmGeom& g, const cc_model_desc& d, const float* 
   using S = ArmTcShape<C, NH, NHL>;
   using P = ArmTcParams<C, NH, NHL>;
   static_assert(sizeof(P) <= 32 * 1024 - 16, "kernel parameters exceed the 32 KB bank");
-  P p;  // ~15 KB, copied into the launch's parameter bank
+  P p;  // ~2.5 KB, copied into the launch's parameter bank
   memset(&p, 0, sizeof(p));
+  ArmTcB<C, NH, NHL> hb;  // the B operands, to global memory below
+  memset(&hb, 0, sizeof(hb));
   p.g = g;
   p.lat = lat;
   p.partial = partial;
@@ -879,15 +902,15 @@ static int launch_arm_tc(const ArmGeom& g, const cc_model_desc& d, const float* 
   // blob: per layer W[out][in] then b[out]
   const float* q = arm_w;
   for (int n = 0; n < NH; n++) {
-    for (int i = 0; i < C; i++) put(p.B0[0], p.B0[1], n, i, S::K0, q[n * C + i] + ((res(0) && i == n) ? 1.0f : 0.0f));
-    put(p.B0[0], p.B0[1], n, C, S::K0, q[C * NH + n]);
+    for (int i = 0; i < C; i++) put(hb.B0[0], hb.B0[1], n, i, S::K0, q[n * C + i] + ((res(0) && i == n) ? 1.0f : 0.0f));
+    put(hb.B0[0], hb.B0[1], n, C, S::K0, q[C * NH + n]);
   }
   q += C * NH + NH;
   for (int k = 0; k < NHL - 1; k++) {
     for (int n = 0; n < NH; n++) {
       for (int i = 0; i < NH; i++)
-        put(p.B1[k][0], p.B1[k][1], n, i, S::K1, q[n * NH + i] + ((res(k + 1) && i == n) ? 1.0f : 0.0f));
-      put(p.B1[k][0], p.B1[k][1], n, NH, S::K1, q[NH * NH + n]);
+        put(hb.B1[k][0], hb.B1[k][1], n, i, S::K1, q[n * NH + i] + ((res(k + 1) && i == n) ? 1.0f : 0.0f));
+      put(hb.B1[k][0], hb.B1[k][1], n, NH, S::K1, q[NH * NH + n]);
     }
     q += NH * NH + NH;
   }
@@ -900,6 +923,15 @@ static int launch_arm_tc(const ArmGeom& g, const cc_model_desc& d, const float* 
 
   const int tiles = g.tile_begin[g.L];
   if (tiles == 0) return 0;
+  // the B operands to global memory: the scratch after the 16 reserved partial
+  // slots per tile (ARM_W_SCRATCH in ccrd_api.cu); pageable source, so the call
+  // returns once the driver has staged it (p may go out of scope)
+  float* gB = reinterpret_cast<float*>(partial + (size_t)tiles * 16);
+  static_assert(4 * S::B_FLOATS <= 8 * ARM_W_SCRATCH_DOUBLES, "weight scratch");
+  static_assert(sizeof(hb) == sizeof(float) * S::B_FLOATS, "packed B layout");
+  if (cudaMemcpyAsync(gB, &hb, sizeof(hb), cudaMemcpyHostToDevice, stream) != cudaSuccess)
+    return -1;
+  p.gB = gB;
   const bool tma = arm_tma_maps(g, lat, p.tmap);
   const bool sc = is_std_ctx(d);
   // default: ping-pong warpgroups (two blocks in flight each, arm_tcp_kernel);

@@ -298,7 +298,7 @@ static int n_arm_partials(const cc_model_desc& d, const cc_strip* win) {  // wri
 static int n_arm_cap(const cc_model_desc& d, const cc_strip* win) {  // reserved (synthesis partials follow)
   ArmGeom g;
   arm_geom(d, win, g);
-  return g.tile_begin[d.L] * ARM_PARTIALS_CAP;
+  return g.tile_begin[d.L] * ARM_PARTIALS_CAP + ARM_W_SCRATCH_DOUBLES;  // + the tensor-core ARM's weight scratch
 }
 static int n_syn_ctas(const cc_model_desc& d, const cc_strip* win) {
   SynGeom g;

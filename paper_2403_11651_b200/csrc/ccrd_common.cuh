@@ -264,6 +264,9 @@ typedef int (*SynLaunchFn)(const SynGeom& g, const cc_model_desc& d, const float
 ArmLaunchFn find_arm_launcher(int C, int NH, int NHL);     // FFMA2 path (arm_rate.cu)
 ArmLaunchFn find_arm_tc_launcher(int C, int NH, int NHL);  // tensor-core path (arm_tc.cu)
 int arm_tc_partials_per_tile();                            // rate partials per tile of that path
+// per image, after the ARM's 16 partial slots per tile: the tensor-core ARM's
+// packed weights (global copy, bulk-loaded into shared memory by each CTA)
+constexpr int ARM_W_SCRATCH_DOUBLES = 2560;
 int device_sm_count();  // current device's SMs (lazily cached; 148 without a device)
 
 // N-O analysis transform (analysis.cu, NEXT-4)
