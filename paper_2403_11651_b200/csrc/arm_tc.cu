@@ -577,6 +577,10 @@ __global__ void __maxnreg__(CCRD_TCP_MAXREG)
   }
   if (t < 4 * NWG) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + t)));
   if (t == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&wbar)));
+  // operand-ready barriers [warpgroup][slot][A0 | A1]: each warp arrives after
+  // its TMEM stores, only the issuing warp waits (the others go on)
+  __shared__ __align__(8) uint64_t rbar[4][4];
+  if (t < 4 * NWG) asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(smem_u32(&rbar[t >> 2][t & 3])));
   __shared__ uint32_t s_big[4];  // per warpgroup: some window held a latent outside +-2048
   if (t < 4) s_big[t] = 0;       // (before the CTA barrier below)
   asm volatile("fence.mbarrier_init.release.cluster;");
@@ -610,6 +614,7 @@ __global__ void __maxnreg__(CCRD_TCP_MAXREG)
   float* win = wins + g * G::WINP;
   uint64_t* bar = bars + 2 * g;  // one per slot
   uint32_t ph[2] = {0, 0};
+  uint32_t rph = 0;  // phase bits of rbar[g][2 s + k]
   constexpr uint32_t IDESC =
       (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NH >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
   const uint32_t sB_u = smem_u32(sB);
@@ -706,15 +711,18 @@ __global__ void __maxnreg__(CCRD_TCP_MAXREG)
     qidx[s] = p.g.lv.off[c_l] + (int64_t)(i - p.g.lv.lo[c_l]) * w + j;
     tmem_wait_st();
     asm volatile("tcgen05.fence::before_thread_sync;");
-    wg_sync(g);
-    if (b < 2) mbar_wait(&wbar, 0);  // the first use of the weights in shared memory
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&rbar[g][2 * s])) : "memory");
     if (qd == (b & 3)) {
+      if (b < 2) mbar_wait(&wbar, 0);  // the first use of the weights in shared memory
+      mbar_wait(&rbar[g][2 * s], (rph >> (2 * s)) & 1u);  // every warp's A0 rows are in TMEM
       asm volatile("tcgen05.fence::after_thread_sync;");
       if constexpr (SPLIT)  // + c_lo (B0_hi + B0_lo)
         mma_batch_4t<K0 / 8, C / 8>(tmem + cY[s], tmem + cX[s], tmem + cD[s], dB0, IDESC, bar + s, LO0);
       else
         mma_batch_hilo<K0 / 8>(tmem + cY[s], tmem + cX[s], dB0, IDESC, bar + s, LO0);
     }
+    rph ^= 1u << (2 * s);
   };
   auto epi0 = [&](int b, int s) {
     TCG_WAIT(bar + s, ph[s]);
@@ -735,11 +743,15 @@ __global__ void __maxnreg__(CCRD_TCP_MAXREG)
     tmem_st_cols<NH>(tl + cX[s], lo);
     tmem_wait_st();
     asm volatile("tcgen05.fence::before_thread_sync;");
-    wg_sync(g);
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&rbar[g][2 * s + 1])) : "memory");
     if (qd == (b & 3)) {
+      mbar_wait(&rbar[g][2 * s + 1], (rph >> (2 * s + 1)) & 1u);  // every warp's A1 rows are in TMEM
       asm volatile("tcgen05.fence::after_thread_sync;");
       mma_batch_3x<K1 / 8, NH / 8>(tmem + cD[s], tmem + cY[s], tmem + cX[s], dB1, IDESC, bar + s, LO1);
     }
+    rph ^= 1u << (2 * s + 1);
   };
   auto epi1 = [&](int b, int s) {
     TCG_WAIT(bar + s, ph[s]);
