@@ -371,6 +371,24 @@ int cc_set_arm_path(int32_t path);
 int32_t cc_get_arm_path(void);
 int32_t cc_arm_path_for(const cc_model_desc* desc);
 
+/* Synthesis 1x1 path (process-wide; host only).  Layer 0 of the per-pixel
+ * 1x1 MLP (Table 1 synthesis column) is computed either by
+ *   CC_SYN_FFMA2: packed FP32 FMAs, one thread per vertical pixel pair;
+ *   CC_SYN_MMA:   warp MMAs (mma.sync m16n8k8 tf32, 3xTF32 split,
+ *                 fp32-accurate), layer 1 still on FFMA2;
+ *                 only where it applies (L <= 7, C_h a multiple of 8, the
+ *                 latent-chain entries without debug outputs), FFMA2 otherwise;
+ *   CC_SYN_AUTO:  (default) CC_SYN_FFMA2 -- the measured-faster path (the
+ *                 warp-MMA form is issue-bound: 127 vs 109 us per 2K image,
+ *                 DESIGN.md 7.3).
+ * The initial value comes from the environment (CCRD_SYN_PATH = ffma2 | mma).
+ * cc_set_synth_path: CC_EINVAL for an unknown value. */
+#define CC_SYN_AUTO 0
+#define CC_SYN_FFMA2 1
+#define CC_SYN_MMA 2
+int cc_set_synth_path(int32_t path);
+int32_t cc_get_synth_path(void);
+
 /* Per-kernel timing (bench.py roofline): between cc_profile_begin() and
  * cc_profile_end(), every kernel the calling thread launches through this
  * library is bracketed by CUDA events recorded on its own stream.

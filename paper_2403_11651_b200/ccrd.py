@@ -89,10 +89,11 @@ EXPORTS = ["cc_workspace_bytes", "cc_rd_forward", "cc_workspace_bytes_host", "cc
            "cc_workspace_bytes_strip", "cc_rd_forward_strip", "cc_train_param_count",
            "cc_train_workspace_bytes", "cc_train_step", "cc_decode", "cc_analysis_param_count",
            "cc_analysis_workspace_bytes", "cc_analysis_forward", "cc_arm_decode_workspace_bytes", "cc_arm_decode",
-           "cc_set_arm_path", "cc_get_arm_path", "cc_arm_path_for"]
+           "cc_set_arm_path", "cc_get_arm_path", "cc_arm_path_for", "cc_set_synth_path", "cc_get_synth_path"]
 
-# ARM rate paths (include/ccrd.h)
+# ARM rate paths and synthesis 1x1 paths (include/ccrd.h)
 CC_ARM_AUTO, CC_ARM_FFMA2, CC_ARM_TC = 0, 1, 2
+CC_SYN_AUTO, CC_SYN_FFMA2, CC_SYN_MMA = 0, 1, 2
 
 _lib = None
 
@@ -176,6 +177,9 @@ def load(rebuild_if_stale: bool = True) -> C.CDLL:
     L.cc_get_arm_path.restype = C.c_int32
     L.cc_arm_path_for.restype = C.c_int32
     L.cc_arm_path_for.argtypes = [D]
+    L.cc_set_synth_path.restype = C.c_int
+    L.cc_set_synth_path.argtypes = [C.c_int32]
+    L.cc_get_synth_path.restype = C.c_int32
     _lib = L
     return L
 
@@ -385,6 +389,30 @@ def cc_get_arm_path() -> int:
 
 def cc_arm_path_for(desc) -> int:
     return load().cc_arm_path_for(C.byref(desc))
+
+
+def cc_set_synth_path(path: int) -> None:
+    _check(load().cc_set_synth_path(path), "cc_set_synth_path")
+
+
+def cc_get_synth_path() -> int:
+    return load().cc_get_synth_path()
+
+
+class synth_path:
+    """Context manager: run a block with a given synthesis 1x1 path, then restore."""
+
+    def __init__(self, path: int):
+        self.path, self.old = path, None
+
+    def __enter__(self):
+        self.old = cc_get_synth_path()
+        cc_set_synth_path(self.path)
+        return self
+
+    def __exit__(self, *exc):
+        cc_set_synth_path(self.old)
+        return False
 
 
 class arm_path:

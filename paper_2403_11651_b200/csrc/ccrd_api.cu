@@ -195,6 +195,21 @@ static bool arm_use_tc(const cc_model_desc& d) {
   if (path == CC_ARM_AUTO) return d.n_ctx == 16 && d.arm_widths[1] == 24;
   return true;
 }
+// Synthesis 1x1 path (cc_set_synth_path; initial value from CCRD_SYN_PATH =
+// ffma2 | mma): AUTO = FFMA2 (the warp-MMA form measured slower, DESIGN.md
+// 7.3); MMA = layer 0 on warp MMAs wherever synth.cu has that form.
+static std::atomic<int> g_syn_path{-1};
+int synth_path() {
+  int v = g_syn_path.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = getenv("CCRD_SYN_PATH");
+    v = (e && strcmp(e, "ffma2") == 0) ? CC_SYN_FFMA2 : (e && strcmp(e, "mma") == 0) ? CC_SYN_MMA : CC_SYN_AUTO;
+    int expect = -1;
+    g_syn_path.compare_exchange_strong(expect, v);
+    v = g_syn_path.load();
+  }
+  return v;
+}
 static ArmLaunchFn arm_launcher(const cc_model_desc& d) {
   return arm_use_tc(d) ? find_arm_tc_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1)
                        : find_arm_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1);
@@ -638,6 +653,14 @@ int32_t cc_arm_path_for(const cc_model_desc* desc) {
   if (validate(desc) != CC_OK) return -1;
   return arm_use_tc(*desc) ? CC_ARM_TC : CC_ARM_FFMA2;
 }
+
+int cc_set_synth_path(int32_t path) {
+  if (path != CC_SYN_AUTO && path != CC_SYN_FFMA2 && path != CC_SYN_MMA)
+    return fail(CC_EINVAL, "synthesis path must be CC_SYN_AUTO, CC_SYN_FFMA2 or CC_SYN_MMA (got %d)", path);
+  g_syn_path.store(path);
+  return CC_OK;
+}
+int32_t cc_get_synth_path(void) { return synth_path(); }
 
 int cc_validate(const cc_model_desc* desc) { return validate(desc); }
 

@@ -290,5 +290,7 @@ int train_supported(const cc_model_desc& d);
 int train_step_impl(const cc_model_desc& d, float* par, const float* noise, const float* image, float* am, float* av,
                     const cc_adam* opt, cc_rd_result* result, float* grad, void* ws, cudaStream_t s);
 SynLaunchFn find_syn_launcher(int L, int CH, int R, int K);
+// synthesis 1x1 path (cc_set_synth_path; ccrd_api.cu): CC_SYN_AUTO / FFMA2 / MMA
+int synth_path();
 
 }  // namespace ccrd

@@ -72,6 +72,11 @@ struct SynShape {
   static constexpr int BUF_B = (TMPH > HBUF) ? TMPH : HBUF;    // tmph  | h (pong)
   static constexpr int LAT0 = ((RH0 * RW0 + 1) / 2);           // int16 level-0 region, in floats
   static constexpr size_t SMEM = sizeof(float) * (size_t)(BUF_A + BUF_B + LAT0);
+  // MLP = 1: the 1x1 weights (A0t, a0, A1: contiguous in SynWeights) copied
+  // once per CTA, so that each lane reads its MMA fragments without
+  // lane-divergent constant-bank loads
+  static constexpr int WRAW = L * CH + CH + 3 * CH;
+  static constexpr size_t SMEM_MMA = SMEM + sizeof(float) * (size_t)WRAW;
   static constexpr int NWARPS = SYN_THREADS / 32;
   static constexpr int SEGS = SYN_THREADS / SYN_TW;            // column segments per tile column
   static constexpr int RS = SYN_TH / SEGS;                      // rows per segment
@@ -254,7 +259,46 @@ __device__ __forceinline__ float load_x(const P& p, int64_t i) {
     return __ldg(p.image + i);
 }
 
-template <int L, int CH, int R, int K, bool DENSE_IN, bool IMG8>
+// ------------------------------------------- 1x1 layer 0 on the tensor cores
+// Legacy warp MMA (mma.sync m16n8k8 tf32; HMMA.1688 on sm_100a, 1024 MACs per
+// warp instruction, 512 MAC/clk/SM measured -- tools/microbench/hmma_probe.cu)
+// needs no TMEM, so it coexists with the tensor-core ARM CTA that holds all of
+// its SM's TMEM.  fp32 accuracy through the 3xTF32 split: x = hi + lo with hi
+// = x rounded to tf32 and lo = x - hi (exact in fp32), D = lo_a hi_b + hi_a
+// lo_b + hi_a hi_b (the dropped lo_a lo_b is < 2^-22 |a b|).
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ uint32_t syn_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// N shared loads a, a + S, a + 2S, ... (32-bit shared addresses: no generic
+// window arithmetic inside the loop)
+template <int N, int S, int U = 0>
+__device__ __forceinline__ void lds_col(uint32_t a, float (&v)[N]) {
+  if constexpr (U < N) {
+    asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v[U]) : "r"(a), "n"(U * S));
+    lds_col<N, S, U + 1>(a, v);
+  }
+}
+__device__ __forceinline__ int lds_s16(uint32_t a) {
+  short v;
+  asm volatile("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+// the same rounding (to nearest, ties away from zero) in two integer ops, for
+// finite x (the values here are finite fp32 sums)
+__device__ __forceinline__ uint32_t tf32_round(float x) { return (__float_as_uint(x) + 0x1000u) & 0xffffe000u; }
+__device__ __forceinline__ void mma_tf32_1688(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// MLP = 0: the 1x1 stack on packed FFMA2 (one thread per vertical pixel pair);
+// MLP = 1: layer 0 as warp MMAs over m-tiles of 16 pixels, layer 1 on FFMA2
+// (chain mode only, no debug outputs).
+template <int L, int CH, int R, int K, bool DENSE_IN, bool IMG8, int MLP>
 __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
     synth_kernel(const __grid_constant__ SynParams<L, CH, R, K> p) {
   using S = SynShape<L, CH, R, K>;
@@ -274,6 +318,11 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
   const int Y0 = Ys + ty * SYN_TH, X0 = tx * SYN_TW;
   const int RY = Y0 - RE, RX = X0 - RE;  // origin of the level-0 region (even)
 
+  float* wraw = smem + S::BUF_A + S::BUF_B + S::LAT0;  // MLP = 1 only: [WRAW]
+  if constexpr (MLP == 1) {
+    const float* wsrc = &p.w.A0t[0][0];
+    for (int i = threadIdx.x; i < S::WRAW; i += SYN_THREADS) wraw[i] = wsrc[i];
+  }
   if (threadIdx.x < 32) {
     int r = RY, cl = RX;
     for (int j = 0; j < L; j++) {
@@ -402,13 +451,153 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
         hA[c * HP + o + RW0] = out1[c];
       }
     };
+    if constexpr (MLP == 0) {
 #pragma unroll 1
-    for (int item = threadIdx.x; item < NPAIR; item += SYN_THREADS) {
-      if (!needed(item)) continue;  // never read by the convs
-      uint64_t v[L], op[3];
-      dense_of(item, v);
-      mlp_pair<L, CH, R, K>(p, v, op);
-      store(item, v, op);
+      for (int item = threadIdx.x; item < NPAIR; item += SYN_THREADS) {
+        if (!needed(item)) continue;  // never read by the convs
+        uint64_t v[L], op[3];
+        dense_of(item, v);
+        mlp_pair<L, CH, R, K>(p, v, op);
+        store(item, v, op);
+      }
+    } else {
+      // m-tile = 2 row pairs x 4 columns of the level-0 region: MMA row g
+      // (0..7) = pixel (row 2 rp, column cc) and row g + 8 = (row 2 rp + 1, cc)
+      // with rp = 2 rq + g / 4, cc = 4 cq + g % 4, so each thread's two rows
+      // are a vertical pair -- the last upsampling step's FFMA2 lane pair.
+      // K (= 8) positions: t -> channel t + 1 (t < 3) or 0 (t = 3); t + 4 ->
+      // channel t + 4 (t < 3) or the constant 1 that carries the bias.  Lane
+      // (g, t) computes exactly its fragment's dense values: t < 3 two
+      // upsampled channels, t = 3 the level-0 latents and the constant.
+      static_assert(!DENSE_IN && L <= 7 && CH % 8 == 0 && RW0 % 4 == 0 && (RH0 / 2) % 2 == 0, "mma MLP shape");
+      constexpr int NJ = CH / 8;
+      constexpr int CQ = RW0 / 4, NMT = (RH0 / 4) * CQ;
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      const int g = lane >> 2, t = lane & 3;
+      const int chA = (t < 3) ? t + 1 : 0, chB = (t < 3) ? t + 4 : -1;  // chB = -1: the bias
+      // B fragments (per lane, once per CTA, from the shared copy of the
+      // weights): b0 = B[t][8j + g], b1 = B[t + 4][8j + g]
+      const float* sA0t = wraw;             // [L][CH]
+      const float* sa0 = wraw + L * CH;     // [CH]
+      const float* sA1 = sa0 + CH;          // [3][CH]
+      uint32_t bh[NJ][2], bl[NJ][2];
+#pragma unroll
+      for (int j = 0; j < NJ; j++) {
+        const int n = 8 * j + g;
+        const float w0 = (chA < L) ? sA0t[chA * CH + n] : 0.0f;
+        const float w1 = (chB < 0) ? sa0[n] : (chB < L) ? sA0t[chB * CH + n] : 0.0f;
+        bh[j][0] = tf32_rna(w0);
+        bh[j][1] = tf32_rna(w1);
+        bl[j][0] = tf32_rna(w0 - __uint_as_float(bh[j][0]));
+        bl[j][1] = tf32_rna(w1 - __uint_as_float(bh[j][1]));
+      }
+      // layer-1 weight pairs of this lane's hidden units (8 j + 2 t, 8 j + 2 t + 1)
+      uint64_t w1p[3][NJ];
+#pragma unroll
+      for (int c = 0; c < 3; c++)
+#pragma unroll
+        for (int j = 0; j < NJ; j++)
+          w1p[c][j] = *reinterpret_cast<const uint64_t*>(sA1 + c * CH + 8 * j + 2 * t);
+      const float bias1 = p.w.a1[(t < 3) ? t : 2];
+      // tmph row of source u = 0 for this lane's row pair (the window rows past
+      // the image already hold the replicated edge rows: LoadLevel1 clamps)
+      const int dr = g >> 2, dc = g & 3;
+      const int srcT = (dr + (RY >> 1) - K / 4 - lo1) * RW0 + dc;
+      const int latT = 2 * dr * RW0 + dc;
+      // shared-window addresses, fixed per lane: t = 3 reads a valid slot too
+      // (its values are discarded by the selects below), so every lane runs
+      // the same branch-free instruction stream
+      const int slotA = (t < 3 && chA < L) ? chA - 1 : 0;
+      const int slotB = (t < 3 && chB < L) ? chB - 1 : 0;
+      const uint32_t aA0 = syn_smem_u32(bufB) + 4u * (uint32_t)(slotA * S::TSLOT + srcT);
+      const uint32_t aB0 = syn_smem_u32(bufB) + 4u * (uint32_t)(slotB * S::TSLOT + srcT);
+      const uint32_t aL0 = syn_smem_u32(lat0) + 2u * (uint32_t)latT;
+      const bool okA = (t == 3) || chA < L, okB = (t == 3) || chB < L;
+#pragma unroll 1
+      for (int mt = warp; mt < NMT; mt += S::NWARPS) {
+        const int rq = mt / CQ, cq = mt - rq * CQ;
+        const int moff = 4 * rq * RW0 + 4 * cq;  // m-tile origin in the level-0 region
+        const uint32_t so = 4u * (uint32_t)(2 * rq * RW0 + 4 * cq);
+        uint64_t va = 0ull, vb = 0ull;  // (row 2 rp, row 2 rp + 1) of channels chA, chB
+        if constexpr (L > 1) {
+          float sa[K / 2 + 1], sb[K / 2 + 1];
+          lds_col<K / 2 + 1, 4 * RW0>(aA0 + so, sa);
+          lds_col<K / 2 + 1, 4 * RW0>(aB0 + so, sb);
+#pragma unroll
+          for (int u = K / 2; u >= 0; u--) {
+            va = ffma2(f2pack(sa[u], sa[u]), ldp2(p.w.kv[u]), va);
+            vb = ffma2(f2pack(sb[u], sb[u]), ldp2(p.w.kv[u]), vb);
+          }
+        }
+        const uint32_t la = aL0 + 2u * (uint32_t)moff;
+        const float l0 = (float)lds_s16(la), l1 = (float)lds_s16(la + 2u * RW0);
+        va = (t == 3) ? f2pack(l0, l1) : va;
+        vb = (t == 3) ? f2pack(1.0f, 1.0f) : vb;
+        va = okA ? va : 0ull;
+        vb = okB ? vb : 0ull;
+        const float2 fa = f2unpack(va), fb = f2unpack(vb);
+        uint32_t ah[4], al[4];
+        ah[0] = tf32_round(fa.x);
+        ah[1] = tf32_round(fa.y);
+        ah[2] = tf32_round(fb.x);
+        ah[3] = tf32_round(fb.y);
+        {
+          const float2 la = f2unpack(fsub2(va, f2pack(__uint_as_float(ah[0]), __uint_as_float(ah[1]))));
+          const float2 lb = f2unpack(fsub2(vb, f2pack(__uint_as_float(ah[2]), __uint_as_float(ah[3]))));
+          al[0] = __float_as_uint(la.x);
+          al[1] = __float_as_uint(la.y);
+          al[2] = __float_as_uint(lb.x);
+          al[3] = __float_as_uint(lb.y);
+        }
+        uint64_t o0[3], o1[3];  // layer-1 partials: pixel g / g + 8, lanes = (even, odd) hidden
+#pragma unroll
+        for (int c = 0; c < 3; c++) o0[c] = o1[c] = 0ull;
+#pragma unroll
+        for (int j = 0; j < NJ; j++) {
+          float d[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+          mma_tf32_1688(d, al, bh[j][0], bh[j][1]);
+          mma_tf32_1688(d, ah, bl[j][0], bl[j][1]);
+          mma_tf32_1688(d, ah, bh[j][0], bh[j][1]);
+          const uint64_t h0 = f2pack(fmaxf(d[0], 0.0f), fmaxf(d[1], 0.0f));
+          const uint64_t h1 = f2pack(fmaxf(d[2], 0.0f), fmaxf(d[3], 0.0f));
+#pragma unroll
+          for (int c = 0; c < 3; c++) {
+            o0[c] = ffma2(h0, w1p[c][j], o0[c]);
+            o1[c] = ffma2(h1, w1p[c][j], o1[c]);
+          }
+        }
+        float s0[3], s1[3];
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+          const float2 a = f2unpack(o0[c]), b = f2unpack(o1[c]);
+          s0[c] = a.x + a.y;
+          s1[c] = b.x + b.y;
+        }
+#pragma unroll
+        for (int m = 1; m <= 2; m <<= 1)
+#pragma unroll
+          for (int c = 0; c < 3; c++) {
+            s0[c] += __shfl_xor_sync(0xffffffffu, s0[c], m);
+            s1[c] += __shfl_xor_sync(0xffffffffu, s1[c], m);
+          }
+        // lane t keeps output channel min(t, 2) (t = 3 stores the same value
+        // as t = 2 to the same address)
+        float x0 = s0[2], x1 = s1[2];
+        x0 = (t == 1) ? s0[1] : x0;
+        x1 = (t == 1) ? s1[1] : x1;
+        x0 = (t == 0) ? s0[0] : x0;
+        x1 = (t == 0) ? s1[0] : x1;
+        x0 += bias1;
+        x1 += bias1;
+        if (R > 0) {
+          x0 = fmaxf(x0, 0.0f);
+          x1 = fmaxf(x1, 0.0f);
+        }
+        const int o = latT + moff;
+        float* hc = hA + ((t < 3) ? t : 2) * HP + o;
+        hc[0] = x0;
+        hc[RW0] = x1;
+      }
     }
   }
   __syncthreads();
@@ -641,6 +830,15 @@ namespace ccrd {
 #endif
 
 // ---------------------------------------------------------------- host launcher
+// one kernel variant: opt in to its dynamic shared memory size once, launch
+template <int L, int CH, int R, int K, bool DENSE_IN, bool IMG8, int MLP>
+static void syn_go(const SynParams<L, CH, R, K>& p, int n_tiles, size_t smem, cudaStream_t stream) {
+  static const bool attr = (cudaFuncSetAttribute(synth_kernel<L, CH, R, K, DENSE_IN, IMG8, MLP>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                            true);
+  (void)attr;
+  synth_kernel<L, CH, R, K, DENSE_IN, IMG8, MLP><<<n_tiles, SYN_THREADS, smem, stream>>>(p);
+}
 template <int L, int CH, int R, int K>
 static int launch_syn(const SynGeom& g, const cc_model_desc& d, const float* up_w,
                       const float* syn_w, const int16_t* lat, const float* s1, const float* dense_in,
@@ -684,29 +882,22 @@ static int launch_syn(const SynGeom& g, const cc_model_desc& d, const float* up_
     q += 84;
   }
   using S = SynShape<L, CH, R, K>;
-  static bool attr_set[3] = {false, false, false};
-  const size_t smem = S::SMEM;
+  // 1x1 layer 0 on warp MMAs (chain mode, no debug outputs) when selected
+  // (cc_set_synth_path CC_SYN_MMA; measured slower)
+  constexpr bool kMmaShape = L <= 7 && CH % 8 == 0 && S::RW0 % 4 == 0 && (S::RH0 / 2) % 2 == 0;
+  const bool mma = kMmaShape && !dense_in && !dense_out && !h1_out && synth_path() == CC_SYN_MMA;
+  const size_t smem = mma ? S::SMEM_MMA : S::SMEM;
   if (dense_in) {  // stage entry cc_synthesize: fp32 images only (checked by the API)
-    if (!attr_set[1]) {
-      cudaFuncSetAttribute(synth_kernel<L, CH, R, K, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      attr_set[1] = true;
+    syn_go<L, CH, R, K, true, false, 0>(p, g.n_tiles, smem, stream);
+  } else if (mma) {
+    if constexpr (kMmaShape) {
+      if (d.image_u8) syn_go<L, CH, R, K, false, true, 1>(p, g.n_tiles, smem, stream);
+      else syn_go<L, CH, R, K, false, false, 1>(p, g.n_tiles, smem, stream);
     }
-    synth_kernel<L, CH, R, K, true, false><<<g.n_tiles, SYN_THREADS, smem, stream>>>(p);
   } else if (d.image_u8) {
-    if (!attr_set[2]) {
-      cudaFuncSetAttribute(synth_kernel<L, CH, R, K, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      attr_set[2] = true;
-    }
-    synth_kernel<L, CH, R, K, false, true><<<g.n_tiles, SYN_THREADS, smem, stream>>>(p);
+    syn_go<L, CH, R, K, false, true, 0>(p, g.n_tiles, smem, stream);
   } else {
-    if (!attr_set[0]) {
-      cudaFuncSetAttribute(synth_kernel<L, CH, R, K, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      attr_set[0] = true;
-    }
-    synth_kernel<L, CH, R, K, false, false><<<g.n_tiles, SYN_THREADS, smem, stream>>>(p);
+    syn_go<L, CH, R, K, false, false, 0>(p, g.n_tiles, smem, stream);
   }
   return 0;
 }

@@ -290,3 +290,22 @@ def test_arm_path_selection_without_gpu():
         assert P.cc_workspace_bytes(ref, 3) == ws_ffma2      # the layout does not depend on the path
     finally:
         P.cc_set_arm_path(old)
+
+
+def test_synth_path_selection_without_gpu():
+    """cc_set_synth_path / cc_get_synth_path (include/ccrd.h): host-only
+    switch, CC_EINVAL for unknown values, AUTO by default."""
+    old = P.cc_get_synth_path()
+    try:
+        with pytest.raises(ccrd.CcError) as e:
+            P.cc_set_synth_path(5)
+        assert e.value.code == ccrd.CC_EINVAL
+        for path in (P.CC_SYN_MMA, P.CC_SYN_FFMA2, P.CC_SYN_AUTO):
+            P.cc_set_synth_path(path)
+            assert P.cc_get_synth_path() == path
+        ref = P.desc_from_config(workload.CONFIGS["ref"])
+        ws = P.cc_workspace_bytes(ref, 3)
+        P.cc_set_synth_path(P.CC_SYN_MMA)
+        assert P.cc_workspace_bytes(ref, 3) == ws            # the layout does not depend on the path
+    finally:
+        P.cc_set_synth_path(old)

@@ -26,13 +26,17 @@ def _P():
     return P
 
 
-@pytest.fixture(autouse=True, params=["tc", "ffma2"])
+@pytest.fixture(autouse=True, params=["tc", "ffma2", "tc+synmma"])
 def arm_path(request):
     """Every parity case runs on both ARM paths (include/ccrd.h
     cc_set_arm_path): the tensor-core kernel (the default for the shapes it is
-    compiled for; the others fall back to FFMA2) and the FFMA2 kernel."""
+    compiled for; the others fall back to FFMA2) and the FFMA2 kernel; and
+    once more with the synthesis 1x1 layer 0 on warp MMAs (cc_set_synth_path
+    CC_SYN_MMA, opt-in; the shapes and entries it does not cover run FFMA2)."""
     P = _P()
-    with P.arm_path(P.CC_ARM_TC if request.param == "tc" else P.CC_ARM_FFMA2):
+    arm = P.CC_ARM_FFMA2 if request.param == "ffma2" else P.CC_ARM_TC
+    syn = P.CC_SYN_MMA if request.param.endswith("synmma") else P.CC_SYN_FFMA2
+    with P.arm_path(arm), P.synth_path(syn):
         yield request.param
 
 
