@@ -25,6 +25,7 @@ __global__ void __launch_bounds__(ARM_THREADS, ARM_CTAS_PER_SM)
   constexpr int N = ARM_SH * ARM_SW;
   constexpr int IT = (N + ARM_THREADS - 1) / ARM_THREADS;
   __shared__ float tile[N];
+  pdl_trigger();
 
   // (level, tile) of this CTA through the prefix table
   const int b = blockIdx.x;
@@ -115,6 +116,7 @@ __global__ void __launch_bounds__(ARM_THREADS, ARM_CTAS_PER_SM)
 #pragma unroll
   for (int o2 = 16; o2 > 0; o2 >>= 1) bits += __shfl_xor_sync(0xffffffffu, bits, o2);
   if (lane == 0) p.partial[b * (ARM_THREADS / 32) + ly] = (double)bits;
+  pdl_wait();  // complete only after the previous kernel of the stream
 }
 
 // ---------------------------------------------------------------- host launcher
@@ -129,9 +131,10 @@ static int launch_arm(const ArmGeom& g, const cc_model_desc& d, const float* arm
   p.mu = mu;
   p.scale = scale;
   p.bits = bits;
+  if (g_launch_ctl.arm_stage == ARM_STAGE_ONLY) return 0;  // weights travel in the parameters
   pack_arm_weights<C, NH, NHL>(d, arm_w, p.w);
 
-  arm_rate_kernel<C, NH, NHL><<<g.tile_begin[g.L], ARM_THREADS, 0, stream>>>(p);
+  launch_ctl(arm_rate_kernel<C, NH, NHL>, (unsigned)g.tile_begin[g.L], ARM_THREADS, 0, stream, p);
   return 0;
 }
 

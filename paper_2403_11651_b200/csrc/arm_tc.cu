@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(ArmTcgShape<C, NH>::THREADS, 1)
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int g = warp >> 2, qd = warp & 3, tw = t & 127;  // warpgroup, lane quadrant, latent of the block
   __shared__ __align__(8) uint64_t wbar;  // the weights' bulk copy
+  pdl_trigger();  // the next image's ARM may be scheduled as this grid drains
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -519,6 +520,7 @@ __global__ void __launch_bounds__(ArmTcgShape<C, NH>::THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  pdl_wait();  // complete only after the previous kernel of the stream (TMEM already released)
 }
 
 
@@ -571,6 +573,7 @@ __global__ void __maxnreg__(CCRD_TCP_MAXREG)
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int g = warp >> 2, qd = warp & 3, tw = t & 127;
   __shared__ __align__(8) uint64_t wbar;  // the weights' bulk copy
+  pdl_trigger();  // the next image's ARM may be scheduled as this grid drains
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "n"(Q::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -831,6 +834,7 @@ __global__ void __maxnreg__(CCRD_TCP_MAXREG)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Q::TMEM_COLS));
+  pdl_wait();  // complete only after the previous kernel of the stream (TMEM already released)
 }
 
 // ---------------------------------------------------------------- host launcher
@@ -941,8 +945,13 @@ static int launch_arm_tc(const ArmGeom& g, const cc_model_desc& d, const float* 
   float* gB = reinterpret_cast<float*>(partial + (size_t)tiles * 16);
   static_assert(4 * S::B_FLOATS <= 8 * ARM_W_SCRATCH_DOUBLES, "weight scratch");
   static_assert(sizeof(hb) == sizeof(float) * S::B_FLOATS, "packed B layout");
-  if (cudaMemcpyAsync(gB, &hb, sizeof(hb), cudaMemcpyHostToDevice, stream) != cudaSuccess)
+  // ARM_LAUNCH_ONLY: an earlier ARM_STAGE_ONLY call of this image staged gB
+  // (a batch stages every image's weights before its first ARM kernel, so no
+  // copy sits between two ARM kernels of the stream)
+  if (g_launch_ctl.arm_stage != ARM_LAUNCH_ONLY &&
+      cudaMemcpyAsync(gB, &hb, sizeof(hb), cudaMemcpyHostToDevice, stream) != cudaSuccess)
     return -1;
+  if (g_launch_ctl.arm_stage == ARM_STAGE_ONLY) return 0;
   p.gB = gB;
   const bool tma = arm_tma_maps(g, lat, p.tmap);
   const bool sc = is_std_ctx(d);
@@ -963,7 +972,7 @@ static int launch_arm_tc(const ArmGeom& g, const cc_model_desc& d, const float* 
     const int need = (tiles + Q::NWG - 1) / Q::NWG, cap = device_sm_count() * (512 / Q::TMEM_COLS);
     auto kp = tma ? (sc ? arm_tcp_kernel<C, NH, NHL, true, true> : arm_tcp_kernel<C, NH, NHL, false, true>)
                   : (sc ? arm_tcp_kernel<C, NH, NHL, true, false> : arm_tcp_kernel<C, NH, NHL, false, false>);
-    kp<<<need < cap ? need : cap, Q::THREADS, tma ? qs_t : qs_n, stream>>>(p);
+    launch_ctl(kp, (unsigned)(need < cap ? need : cap), Q::THREADS, tma ? qs_t : qs_n, stream, p);
     return 1;
   }
   using G = ArmTcgShape<C, NH>;
@@ -979,7 +988,7 @@ static int launch_arm_tc(const ArmGeom& g, const cc_model_desc& d, const float* 
   const int need = (tiles + G::NWG - 1) / G::NWG, cap = device_sm_count();
   auto kern = tma ? (sc ? arm_tcg_kernel<C, NH, NHL, true, true> : arm_tcg_kernel<C, NH, NHL, false, true>)
                   : (sc ? arm_tcg_kernel<C, NH, NHL, true, false> : arm_tcg_kernel<C, NH, NHL, false, false>);
-  kern<<<need < cap ? need : cap, G::THREADS, tma ? smem_t : smem_n, stream>>>(p);
+  launch_ctl(kern, (unsigned)(need < cap ? need : cap), G::THREADS, tma ? smem_t : smem_n, stream, p);
   return 1;
 }
 

@@ -210,6 +210,11 @@ int synth_path() {
   }
   return v;
 }
+thread_local LaunchCtl g_launch_ctl;
+bool pdl_enabled() {
+  static const bool on = !(getenv("CCRD_PDL") && getenv("CCRD_PDL")[0] == '0');
+  return on;
+}
 static ArmLaunchFn arm_launcher(const cc_model_desc& d) {
   return arm_use_tc(d) ? find_arm_tc_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1)
                        : find_arm_launcher(d.n_ctx, d.arm_widths[1], d.arm_n_layers - 1);
@@ -438,6 +443,21 @@ static int arm_one(const cc_model_desc& d, const cc_strip* win, const int16_t* l
   return cuda_check("arm_rate_kernel");
 }
 
+// every image's ARM weights to its scratch before the batch's first ARM kernel
+// (ARM_STAGE_ONLY), so the ARM kernels follow one another in the stream
+static int arm_stage_all(const cc_model_desc& d, const cc_strip* win, const int16_t* const* lat,
+                         const float* const* arm_w, char* slices, size_t per, int n, cudaStream_t s) {
+  ArmGeom ag;
+  arm_geom(d, win, ag);
+  if (ag.tile_begin[d.L] == 0) return CC_OK;
+  LaunchCtlScope lc(false, ARM_STAGE_ONLY);
+  const ArmLaunchFn fn = arm_launcher(d);
+  for (int i = 0; i < n; i++)
+    if (fn(ag, d, arm_w[i], lat[i], (double*)(slices + per * (size_t)i), nullptr, nullptr, nullptr, s) < 0)
+      return fail(CC_ECUDA, "ARM weight staging copy failed");
+  return cuda_check("ARM weight staging");
+}
+
 // coarse upsampling pyramid of n images (batched launches)
 static int pyr_many(const cc_model_desc& d, const cc_strip* win, const PyrImage* imgs, int n, cudaStream_t s) {
   PyrGeom pg;
@@ -515,6 +535,9 @@ static int forward_batch(const cc_model_desc& d, const cc_strip* win, const int1
   PyrGeom pg;
   pyr_geom(d, win, pg);
   const int n_arm = n_arm_cap(d, win);  // synthesis partials start here
+  // no programmatic launches while cc_profile_* brackets every launch with
+  // events (each kernel's own duration is what those events measure)
+  const bool pdl = pdl_enabled() && !g_prof.on;
   int rc;
   if (d.up_2d) {  // Table 1 2-D TConv: full pyramid -> dense, then synthesis from it
     static thread_local Pyr2dImage im2[MAX_JOBS_PER_LAUNCH];
@@ -567,24 +590,33 @@ static int forward_batch(const cc_model_desc& d, const cc_strip* win, const int1
       char* sl = slices + per * (size_t)i;
       const float* s1 = slice_pyr(d, win, sl) + pg.s_off[1];
       if (syn_wait) cudaStreamWaitEvent(side->s, syn_wait[i], 0);  // image i landed
+      // synthesis i > 0 directly follows synthesis i - 1 in the side stream
+      LaunchCtlScope lc(pdl && i > 0 && !syn_wait, 0);
       if ((rc = syn_one(d, win, lat[i], s1, up_w[i], syn_w[i], image[i], x_hat[i], nullptr, (double*)sl + n_arm,
                         side->s)))
         return rc;
     }
     cudaEventRecord(side->join, side->s);
+    if ((rc = arm_stage_all(d, win, lat, arm_w, slices, per, n, s))) return rc;
     for (int i = 0; i < n; i++) {
       if (arm_wait) cudaStreamWaitEvent(s, arm_wait[i], 0);
+      LaunchCtlScope lc(pdl && i > 0 && !arm_wait, ARM_LAUNCH_ONLY);
       if ((rc = arm_one(d, win, lat[i], arm_w[i], (double*)(slices + per * (size_t)i), s))) return rc;
     }
     if (join) cudaStreamWaitEvent(s, side->join, 0);  // else the caller orders on the side stream
     return CC_OK;
   }
+  if ((rc = arm_stage_all(d, win, lat, arm_w, slices, per, n, s))) return rc;
   if ((rc = pyr_many(d, win, imgs, n, s))) return rc;
-  for (int i = 0; i < n; i++)
+  for (int i = 0; i < n; i++) {
+    LaunchCtlScope lc(pdl && i > 0, ARM_LAUNCH_ONLY);
     if ((rc = arm_one(d, win, lat[i], arm_w[i], (double*)(slices + per * (size_t)i), s))) return rc;
+  }
   for (int i = 0; i < n; i++) {
     char* sl = slices + per * (size_t)i;
     const float* s1 = slice_pyr(d, win, sl) + pg.s_off[1];
+    // the first synthesis reads the pyramid's output: ordered normally after the ARMs
+    LaunchCtlScope lc(pdl && i > 0, 0);
     if ((rc = syn_one(d, win, lat[i], s1, up_w[i], syn_w[i], image[i], x_hat[i], nullptr, (double*)sl + n_arm, s)))
       return rc;
   }

@@ -252,6 +252,55 @@ struct ReduceJob {
   double inv_3p, lambda_over_p;
 };
 
+// ------------------------------------------------ programmatic dependent launch
+// Consecutive per-image ARM (or synthesis) kernels of one stream are
+// independent, but stream order would hold kernel i + 1 until kernel i's last
+// CTA exits, leaving SMs idle in every tail.  With programmatic stream
+// serialization (PDL) kernel i + 1 may start once every CTA of kernel i has
+// started (pdl_trigger at each CTA's start); every CTA then waits for kernel
+// i's completion at its END (pdl_wait), so kernel i + 1 still completes after
+// kernel i and anything ordered after the last kernel sees every image.  Both
+// are no-ops in a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Per-thread launch controls, set by the batched forward (ccrd_api.cu) around
+// one launcher call through LaunchCtlScope:
+//   pdl:       launch with programmatic stream serialization (the previous
+//              operation in the stream must be an independent kernel);
+//   arm_stage: ARM launchers only -- ARM_STAGE_ONLY copies the packed weights
+//              to the image's scratch and returns, ARM_LAUNCH_ONLY launches
+//              with weights staged by an earlier call, 0 does both.
+enum { ARM_STAGE_ONLY = 1, ARM_LAUNCH_ONLY = 2 };
+struct LaunchCtl {
+  bool pdl = false;
+  int arm_stage = 0;
+};
+extern thread_local LaunchCtl g_launch_ctl;
+struct LaunchCtlScope {
+  LaunchCtl saved;
+  LaunchCtlScope(bool pdl, int arm_stage) : saved(g_launch_ctl) { g_launch_ctl = LaunchCtl{pdl, arm_stage}; }
+  ~LaunchCtlScope() { g_launch_ctl = saved; }
+};
+bool pdl_enabled();  // CCRD_PDL=0 disables programmatic dependent launches (experiments)
+
+// launch `kern` on `s`, with programmatic stream serialization when g_launch_ctl.pdl
+template <typename P>
+static inline cudaError_t launch_ctl(void (*kern)(P), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                                     const P& p) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_launch_ctl.pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
 // Host-side launchers (defined in arm_rate.cu / synth.cu).
 typedef int (*ArmLaunchFn)(const ArmGeom& g, const cc_model_desc& d, const float* arm_w,
                            const int16_t* lat, double* partial, float* mu, float* scale,

@@ -21,6 +21,9 @@
 // The dense L x H x W tensor is never materialised in HBM.
 #include "ccrd_common.cuh"
 
+#ifndef CCRD_SYN_VSCALAR
+#define CCRD_SYN_VSCALAR 0  // last vertical step on scalar FMAs (experiment)
+#endif
 #ifndef CCRD_SYN_MC
 #define CCRD_SYN_MC 20  // hidden neurons per MLP chunk (live accumulators)
 #endif
@@ -314,6 +317,7 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
   int16_t* lat0 = reinterpret_cast<int16_t*>(smem + S::BUF_A + S::BUF_B);  // [RH0][RW0]
   __shared__ int wlo_r[CC_MAX_LEVELS], wlo_c[CC_MAX_LEVELS];
   __shared__ double warp_buf[SYN_THREADS / 32];
+  pdl_trigger();  // the next image's synthesis may be scheduled as this grid drains
 
   const int H = p.g.H, W = p.g.W;
   const int Ys = p.g.y0, Ye = p.g.y1;  // output rows (full image: 0 .. H); x_hat / image rows are Ys-relative
@@ -402,6 +406,19 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
 #pragma unroll
           for (int l = 1; l < L; l++) {
             const float* src = bufB + (l - 1) * S::TSLOT;
+#if CCRD_SYN_VSCALAR
+            // scalar FMAs: K FMA-pipe cycles per channel instead of K + 2 (the
+            // packed form multiplies the two phases' missing taps by zero)
+            float sv[K / 2 + 1];
+#pragma unroll
+            for (int u = 0; u <= K / 2; u++) sv[u] = src[ro[u]];
+            float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+            for (int u = K / 2 - 1; u >= 0; u--) a0 = fmaf(sv[u], p.w.kv[u].x, a0);
+#pragma unroll
+            for (int u = K / 2; u >= 1; u--) a1 = fmaf(sv[u], p.w.kv[u].y, a1);
+            v[l] = f2pack(a0, a1);
+#else
             uint64_t a = 0ull;
 #pragma unroll
             for (int u = K / 2; u >= 0; u--) {
@@ -409,6 +426,7 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
               a = ffma2(f2pack(sv, sv), ldp2(p.w.kv[u]), a);
             }
             v[l] = a;
+#endif
           }
         }
       }
@@ -823,6 +841,7 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
     g_syn_timing[blockIdx.x][6] = sm;
   }
 #endif
+  pdl_wait();  // complete only after the previous kernel of the stream
 }
 
 #ifdef CCRD_SYN_TIMING
@@ -841,7 +860,7 @@ static void syn_go(const SynParams<L, CH, R, K>& p, int n_tiles, size_t smem, cu
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                             true);
   (void)attr;
-  synth_kernel<L, CH, R, K, DENSE_IN, IMG8, MLP><<<n_tiles, SYN_THREADS, smem, stream>>>(p);
+  launch_ctl(synth_kernel<L, CH, R, K, DENSE_IN, IMG8, MLP>, (unsigned)n_tiles, SYN_THREADS, smem, stream, p);
 }
 template <int L, int CH, int R, int K>
 static int launch_syn(const SynGeom& g, const cc_model_desc& d, const float* up_w,
