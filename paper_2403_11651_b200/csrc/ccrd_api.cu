@@ -786,6 +786,8 @@ static int host_env(const char* name, int def, int lo, int hi) {
 // the host path's upload / read-back streams and slot events, per thread and device
 struct HostPool {
   cudaStream_t cs = nullptr, ds = nullptr;
+  cudaStream_t wsm = nullptr;  // int8 -> int16 latent widening (keeps the upload stream copies-only)
+  cudaEvent_t widened[HOST_SLOTS_MAX * HOST_CHUNK_MAX];  // per image: int16 latents ready
   cudaEvent_t copied[HOST_SLOTS_MAX], computed[HOST_SLOTS_MAX], computed_side[HOST_SLOTS_MAX],
       read_back[HOST_SLOTS_MAX];
   cudaEvent_t img_copied[HOST_SLOTS_MAX * HOST_CHUNK_MAX];  // per image: latents landed (its ARM may start)
@@ -804,6 +806,7 @@ static int host_pool(HostPool** out) {
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     if (cudaStreamCreateWithPriority(&g_host.cs, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&g_host.wsm, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithFlags(&g_host.ds, cudaStreamNonBlocking) != cudaSuccess)
       return cuda_check("stream create");
     for (int k = 0; k < HOST_SLOTS_MAX; k++)
@@ -814,6 +817,7 @@ static int host_pool(HostPool** out) {
         return cuda_check("event create");
     for (int k = 0; k < HOST_SLOTS_MAX * HOST_CHUNK_MAX; k++)
       if (cudaEventCreateWithFlags(&g_host.img_copied[k], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&g_host.widened[k], cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreateWithFlags(&g_host.img_done[k], cudaEventDisableTiming) != cudaSuccess)
         return cuda_check("event create");
     g_host.device = dev;
@@ -878,6 +882,7 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
   const bool conc = concurrent_streams();
   SideStream* side = nullptr;
   if (conc && (rc = side_stream(&side))) return rc;
+  static const bool widen_stream = !(getenv("CCRD_WIDEN_STREAM") && getenv("CCRD_WIDEN_STREAM")[0] == '0');
   cudaEvent_t *copied = hp->copied, *computed = hp->computed, *computed_side = hp->computed_side,
               *read_back = hp->read_back;
   // start the side streams after whatever is already queued on s
@@ -897,6 +902,8 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
     const float *a1[HOST_CHUNK_MAX], *u1[HOST_CHUNK_MAX], *s1[HOST_CHUNK_MAX], *i1[HOST_CHUNK_MAX];
     float* x1[HOST_CHUNK_MAX];
     float* dxhs[HOST_CHUNK_MAX];
+    cudaEvent_t lat_ev[HOST_CHUNK_MAX];  // per image: its int16 latents are on the device
+    cudaEvent_t last_widened = nullptr;
     cudaStreamWaitEvent(cs, computed[k], 0);  // slot k's inputs were consumed by chunk c - HOST_SLOTS
     cudaStreamWaitEvent(cs, computed_side[k], 0);
     for (int j = 0; j < m && rc == CC_OK; j++) {
@@ -910,16 +917,28 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
         rc = fail(CC_EINVAL, "image %d: null latents or weights", i0 + j);
         break;
       }
-      if (d.latents_i8) {  // 1 byte per latent over PCIe, widened on the copy stream
+      // the ARM needs only the latents: its event goes before the image (70 % of
+      // the bytes; uploading all of a chunk's latents first measured slower)
+      cudaEvent_t lat_ready = hp->img_copied[k * HOST_CHUNK_MAX + j];
+      if (d.latents_i8) {  // 1 byte per latent over PCIe, widened to int16 on the device
         cudaMemcpyAsync(dlat8, x.latents, (size_t)n_lat, cudaMemcpyHostToDevice, cs);
-        widen_i8_kernel<<<(unsigned)((n_lat + 255) / 256), 256, 0, cs>>>(dlat8, dlat, n_lat);
+        if (widen_stream) {  // on its own stream: the upload stream stays copies-only
+          cudaEventRecord(lat_ready, cs);
+          cudaStreamWaitEvent(hp->wsm, lat_ready, 0);
+          widen_i8_kernel<<<(unsigned)((n_lat + 255) / 256), 256, 0, hp->wsm>>>(dlat8, dlat, n_lat);
+          lat_ready = hp->widened[k * HOST_CHUNK_MAX + j];
+          cudaEventRecord(lat_ready, hp->wsm);
+          last_widened = lat_ready;
+        } else {
+          widen_i8_kernel<<<(unsigned)((n_lat + 255) / 256), 256, 0, cs>>>(dlat8, dlat, n_lat);
+          cudaEventRecord(lat_ready, cs);
+        }
         g_launches++;
       } else {
         cudaMemcpyAsync(dlat, x.latents, lat_b, cudaMemcpyHostToDevice, cs);
+        cudaEventRecord(lat_ready, cs);
       }
-      // the ARM needs only the latents: its event goes before the image (70 % of
-      // the bytes; uploading all of a chunk's latents first measured slower)
-      cudaEventRecord(hp->img_copied[k * HOST_CHUNK_MAX + j], cs);
+      lat_ev[j] = lat_ready;
       if (x.image) cudaMemcpyAsync(dimg, x.image, img_b, cudaMemcpyHostToDevice, cs);
       cudaEventRecord(hp->img_done[k * HOST_CHUNK_MAX + j], cs);
       l1[j] = dlat;
@@ -932,12 +951,15 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
     }
     if (rc) break;
     cudaEventRecord(copied[k], cs);
-    if (!conc) cudaStreamWaitEvent(s, copied[k], 0);  // concurrent: the ARM waits per image (below)
+    if (!conc) {  // concurrent: the ARM waits per image (below)
+      cudaStreamWaitEvent(s, copied[k], 0);
+      if (last_widened) cudaStreamWaitEvent(s, last_widened, 0);
+    }
     cudaStreamWaitEvent(s, read_back[k], 0);  // slot k's x_hat of chunk c - HOST_SLOTS is read back
     if (conc)  // the side stream waits for this chunk's own inputs (per image, below), not for the ARM stream
       cudaStreamWaitEvent(side->s, read_back[k], 0);
     rc = forward_batch(d, nullptr, l1, a1, u1, s1, i1, x1, ws + per * (size_t)i0, per, m, s, conc, /*join=*/false,
-                       /*fork=*/!conc, conc ? hp->img_copied + k * HOST_CHUNK_MAX : nullptr,
+                       /*fork=*/!conc, conc ? lat_ev : nullptr,
                        conc ? hp->img_done + k * HOST_CHUNK_MAX : nullptr);
     if (rc) break;
     cudaEventRecord(computed[k], s);
@@ -959,6 +981,7 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
     cudaStreamSynchronize(s);
   }
   cudaStreamSynchronize(cs);
+  cudaStreamSynchronize(hp->wsm);
   if (cudaStreamSynchronize(ds) != cudaSuccess && rc == CC_OK) rc = cuda_check("cc_rd_forward_host readback");
   delete[] jobs;
   if (rc == CC_OK) rc = cuda_check("cc_rd_forward_host");

@@ -688,13 +688,23 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
         int co[3];
 #pragma unroll
         for (int d = 0; d < 3; d++) co[d] = clampi(x + d - 1, 0, W - 1) - RX;
-        float img[RS][3];  // x for the output rows, in flight during the math
+        // x for the output rows, in flight during the math.  8-bit: the raw
+        // bytes stay integers until the distortion below -- converted at the
+        // load, every warp stalled on its loads before the math (the largest
+        // single stall of the kernel)
+        float img[RS][3];
+        uint32_t img8[RS][3];
         if (last && (IMG8 ? p.image8 != nullptr : p.image != nullptr)) {
 #pragma unroll
           for (int i = 0; i < RS; i++)
 #pragma unroll
-            for (int c = 0; c < 3; c++)
-              img[i][c] = (yb + i < Ye) ? load_x<IMG8>(p, c * Pimg + (int64_t)(yb + i - Ys) * W + x) : 0.0f;
+            for (int c = 0; c < 3; c++) {
+              const int64_t gi = c * Pimg + (int64_t)(yb + i - Ys) * W + x;
+              if constexpr (IMG8)
+                img8[i][c] = (yb + i < Ye) ? (uint32_t)__ldg(p.image8 + gi) : 0u;
+              else
+                img[i][c] = (yb + i < Ye) ? __ldg(p.image + gi) : 0.0f;
+            }
         }
         uint64_t a01[RS];
         float a2[RS];
@@ -755,11 +765,20 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
               for (int c = 0; c < 3; c++)
                 p.out_u8[gi * 3 + c] = (uint8_t)__float2uint_rn(255.0f * fminf(fmaxf(o[c], 0.0f), 1.0f));
             }
+            // 8-bit: min(v, late) == v (v <= 255 <= late) ties each byte's
+            // conversion to this row's result, so the scheduler cannot hoist
+            // it (with its load wait) above the convolution
+            const uint32_t late = __float_as_uint(o[0]) | 255u;
 #pragma unroll
             for (int c = 0; c < 3; c++) {
               if (p.x_hat != nullptr) p.x_hat[c * Pimg + gi] = o[c];
               if ((IMG8 ? p.image8 != nullptr : p.image != nullptr)) {
-                const float ev = img[i][c] - o[c];
+                float xv;
+                if constexpr (IMG8)
+                  xv = u8_to_x(min(img8[i][c], late));
+                else
+                  xv = img[i][c];
+                const float ev = xv - o[c];
                 sse = fmaf(ev, ev, sse);
               }
             }
