@@ -829,13 +829,18 @@ static int host_pool(HostPool** out) {
 // staging slots x images per slot of the host pipeline (measured best 4 x 4;
 // CCRD_HOST_SLOTS / CCRD_HOST_CHUNK override for experiments)
 static int host_slots() { return host_env("CCRD_HOST_SLOTS", 4, 2, HOST_SLOTS_MAX); }
-static int host_chunk() { return host_env("CCRD_HOST_CHUNK", 4, 1, HOST_CHUNK_MAX); }
+// images per staged chunk: 1 for megapixel images (the pipeline fills after one
+// image's upload; 64 x 2K e2e: chunk 1 1.194e10, 2 1.188e10, 4 1.176e10 px/s),
+// 4 for small ones, whose host path is enqueue-bound
+static int host_chunk(const cc_model_desc& d) {
+  return host_env("CCRD_HOST_CHUNK", (int64_t)d.H * d.W >= (1 << 20) ? 1 : 4, 1, HOST_CHUNK_MAX);
+}
 
 size_t cc_workspace_bytes_host(const cc_model_desc* desc, int32_t n_img) {
   if (validate(desc) != CC_OK || n_img < 1) return 0;
   return slice_bytes(*desc, nullptr) * (size_t)n_img +
          align256(sizeof(cc_rd_result) * (size_t)n_img) +
-         (size_t)host_slots() * host_chunk() * stage_slot_bytes(*desc);
+         (size_t)host_slots() * host_chunk(*desc) * stage_slot_bytes(*desc);
 }
 
 int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t n_img, cc_rd_result* results,
@@ -855,7 +860,7 @@ int cc_rd_forward_host(const cc_model_desc* desc, const cc_image_io* io, int32_t
   char* stage = ws + per * (size_t)n_img + align256(sizeof(cc_rd_result) * (size_t)n_img);
   const size_t slot = stage_slot_bytes(d);
   const int HOST_SLOTS = host_slots();
-  const int HOST_CHUNK = host_chunk();
+  const int HOST_CHUNK = host_chunk(d);
   int64_t n_lat = 0;
   LevelGeom lg;
   level_dims(d, lg, &n_lat);
