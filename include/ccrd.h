@@ -378,14 +378,20 @@ int32_t cc_arm_path_for(const cc_model_desc* desc);
  *                 fp32-accurate), layer 1 still on FFMA2;
  *                 only where it applies (L <= 7, C_h a multiple of 8, the
  *                 latent-chain entries without debug outputs), FFMA2 otherwise;
- *   CC_SYN_AUTO:  (default) CC_SYN_FFMA2 -- the measured-faster path (the
- *                 warp-MMA form is issue-bound: 127 vs 109 us per 2K image,
- *                 DESIGN.md 7.3).
- * The initial value comes from the environment (CCRD_SYN_PATH = ffma2 | mma).
- * cc_set_synth_path: CC_EINVAL for an unknown value. */
+ *   CC_SYN_TMA:   CC_SYN_FFMA2's arithmetic in persistent CTAs whose tiles
+ *                 are staged by TMA one tile ahead; where it
+ *                 applies (L >= 3, 8-tap chains, latent rows and S_1 rows
+ *                 16-byte strided / aligned, no debug outputs), CC_SYN_FFMA2
+ *                 otherwise.  Bit-identical to CC_SYN_FFMA2;
+ *   CC_SYN_AUTO:  (default) CC_SYN_TMA where it applies, else CC_SYN_FFMA2
+ *                 (the warp-MMA form is issue-bound: 127 vs 109 us per 2K
+ *                 image).
+ * The initial value comes from the environment (CCRD_SYN_PATH = ffma2 | mma
+ * | tma).  cc_set_synth_path: CC_EINVAL for an unknown value. */
 #define CC_SYN_AUTO 0
 #define CC_SYN_FFMA2 1
 #define CC_SYN_MMA 2
+#define CC_SYN_TMA 3
 int cc_set_synth_path(int32_t path);
 int32_t cc_get_synth_path(void);
 

@@ -13,7 +13,7 @@ from .ccrd import (  # noqa: F401
     cc_train_step, CcAdam, DeviceTrainer, cc_decode, CcAnalysisDesc, analysis_desc, cc_analysis_param_count,
     cc_analysis_workspace_bytes, cc_analysis_forward, cc_arm_decode, cc_arm_decode_workspace_bytes,
     cc_set_arm_path, cc_get_arm_path, cc_arm_path_for, arm_path, CC_ARM_AUTO, CC_ARM_FFMA2, CC_ARM_TC,
-    cc_set_synth_path, cc_get_synth_path, synth_path, CC_SYN_AUTO, CC_SYN_FFMA2, CC_SYN_MMA,
+    cc_set_synth_path, cc_get_synth_path, synth_path, CC_SYN_AUTO, CC_SYN_FFMA2, CC_SYN_MMA, CC_SYN_TMA,
 )
 
 __version__ = "0.1.0"

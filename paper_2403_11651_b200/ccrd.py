@@ -93,7 +93,7 @@ EXPORTS = ["cc_workspace_bytes", "cc_rd_forward", "cc_workspace_bytes_host", "cc
 
 # ARM rate paths and synthesis 1x1 paths (include/ccrd.h)
 CC_ARM_AUTO, CC_ARM_FFMA2, CC_ARM_TC = 0, 1, 2
-CC_SYN_AUTO, CC_SYN_FFMA2, CC_SYN_MMA = 0, 1, 2
+CC_SYN_AUTO, CC_SYN_FFMA2, CC_SYN_MMA, CC_SYN_TMA = 0, 1, 2, 3
 
 _lib = None
 

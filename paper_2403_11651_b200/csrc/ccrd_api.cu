@@ -195,15 +195,20 @@ static bool arm_use_tc(const cc_model_desc& d) {
   if (path == CC_ARM_AUTO) return d.n_ctx == 16 && d.arm_widths[1] == 24;
   return true;
 }
-// Synthesis 1x1 path (cc_set_synth_path; initial value from CCRD_SYN_PATH =
-// ffma2 | mma): AUTO = FFMA2 (the warp-MMA form measured slower, DESIGN.md
-// 7.3); MMA = layer 0 on warp MMAs wherever synth.cu has that form.
+// Synthesis path (cc_set_synth_path; initial value from CCRD_SYN_PATH =
+// ffma2 | mma | tma): AUTO = TMA where it applies, else FFMA2 (the warp-MMA
+// form measured slower); MMA = layer 0 on warp MMAs wherever
+// synth.cu has that form; TMA = FFMA2 arithmetic, persistent CTAs with
+// TMA-staged tiles.
 static std::atomic<int> g_syn_path{-1};
 int synth_path() {
   int v = g_syn_path.load(std::memory_order_relaxed);
   if (v < 0) {
     const char* e = getenv("CCRD_SYN_PATH");
-    v = (e && strcmp(e, "ffma2") == 0) ? CC_SYN_FFMA2 : (e && strcmp(e, "mma") == 0) ? CC_SYN_MMA : CC_SYN_AUTO;
+    v = (e && strcmp(e, "ffma2") == 0) ? CC_SYN_FFMA2
+        : (e && strcmp(e, "mma") == 0) ? CC_SYN_MMA
+        : (e && strcmp(e, "tma") == 0) ? CC_SYN_TMA
+                                        : CC_SYN_AUTO;
     int expect = -1;
     g_syn_path.compare_exchange_strong(expect, v);
     v = g_syn_path.load();
@@ -687,8 +692,9 @@ int32_t cc_arm_path_for(const cc_model_desc* desc) {
 }
 
 int cc_set_synth_path(int32_t path) {
-  if (path != CC_SYN_AUTO && path != CC_SYN_FFMA2 && path != CC_SYN_MMA)
-    return fail(CC_EINVAL, "synthesis path must be CC_SYN_AUTO, CC_SYN_FFMA2 or CC_SYN_MMA (got %d)", path);
+  if (path != CC_SYN_AUTO && path != CC_SYN_FFMA2 && path != CC_SYN_MMA && path != CC_SYN_TMA)
+    return fail(CC_EINVAL, "synthesis path must be CC_SYN_AUTO, CC_SYN_FFMA2, CC_SYN_MMA or CC_SYN_TMA (got %d)",
+                path);
   g_syn_path.store(path);
   return CC_OK;
 }

@@ -2,6 +2,7 @@
 // CUDA product path.  Nothing here is shared with oracle/ (independent code).
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (TMA descriptors in kernel parameters)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -195,6 +196,10 @@ struct SynParams {
   double* partial;         // [n tiles] per-CTA SSE partial sums
   uint8_t* out_u8;         // decode: interleaved 8-bit RGB [H][W][3] of clamp(x_hat) or null
   SynWeights<L, CH, R, K> w;
+  // TMA staging (synth_kernel<..., TMA = true> only): level-0 latents (int16,
+  // 2-D), grid 1 (int16, 2-D), S_1 (fp32, 3-D [L-2][rows][w_1]) over the
+  // buffer windows
+  CUtensorMap tm_lat0, tm_g1, tm_s1;
 };
 
 // Coarse upsampling pyramid (pyramid.cu): S_j = grids j+1 .. L-1 at level j.

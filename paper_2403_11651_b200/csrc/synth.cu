@@ -19,6 +19,8 @@
 //   4. the last layer's output goes straight from registers to x_hat
 //      (optional) and the (x - x_hat)^2 partial sum -> fp64 per CTA.
 // The dense L x H x W tensor is never materialised in HBM.
+#include <cstdlib>
+
 #include "ccrd_common.cuh"
 
 #ifndef CCRD_SYN_VSCALAR
@@ -73,8 +75,29 @@ struct SynShape {
   static constexpr int BUF_A = (STACK > HBUF) ? STACK : HBUF;  // stack | h (ping)
   static constexpr int TMPH = NS * TSLOT;
   static constexpr int BUF_B = (TMPH > HBUF) ? TMPH : HBUF;    // tmph  | h (pong)
-  static constexpr int LAT0 = ((RH0 * RW0 + 1) / 2);           // int16 level-0 region, in floats
+  // int16 level-0 region [RH0][LP]: region column c at LO + c, so that the
+  // TMA box origin RX - LO is 16-byte aligned (RX = X0 - RE, X0 a multiple of 8)
+  static constexpr int LO = (-RE) & 7;
+  static constexpr int LP = (LO + RW0 + 7) & ~7;
+  static constexpr int LAT0 = ((RH0 * LP + 1) / 2);            // int16 level-0 region, in floats
   static constexpr size_t SMEM = sizeof(float) * (size_t)(BUF_A + BUF_B + LAT0);
+  // ---- TMA-staged variant (synth_kernel<..., TMA = true>)
+  // level-1 window origin lc = X0 / 2 + A1 (X0 / 2 a multiple of 8); S_1 (fp32)
+  // boxes need lc 16-byte aligned, grid 1 (int16) is boxed from lc - G0
+  static constexpr int A1 = (-(RE / 2) - K / 4) & ~1;
+  static constexpr int G0 = A1 & 7;
+  static constexpr int GP = (G0 + NC1 + 7) & ~7;  // grid-1 raw pitch (int16)
+  static constexpr bool TMA_OK = (L >= 3) && (A1 & 3) == 0 && (NC1 % 4) == 0 && NC1 <= 256 && NR1 <= 256 &&
+                                 LP <= 256 && RH0 <= 256 && SYN_TW % 16 == 0 && NR1 * GP * 2 <= 4 * BUF_B;
+  static constexpr int al128(int b) { return (b + 127) & ~127; }
+  // byte offsets from a 128-aligned base: bufA (= the stack) placed so that
+  // stack slot 1 (the S_1 box) is 128-aligned, bufB (holds the grid-1 box until
+  // the conversion into slot 0), lat0
+  static constexpr int T_A = (128 - (SLOT * 4) % 128) % 128;
+  static constexpr int T_B = al128(T_A + BUF_A * 4);
+  static constexpr int T_L = al128(T_B + BUF_B * 4);
+  static constexpr size_t SMEM_TMA = (size_t)T_L + (size_t)RH0 * LP * 2 + 128;  // + alignment slack
+  static constexpr uint32_t TMA_BYTES = (uint32_t)((L - 2) * SLOT * 4 + NR1 * GP * 2 + RH0 * LP * 2);
   // MLP = 1: the 1x1 weights (A0t, a0, A1: contiguous in SynWeights) copied
   // once per CTA, so that each lane reads its MMA fragments without
   // lane-divergent constant-bank loads
@@ -147,7 +170,8 @@ struct LoadLat0 {
 #pragma unroll
     for (int k = 0; k < IT; k++) {
       const int it = threadIdx.x + k * SYN_THREADS;
-      if (it < N) lat0[it] = v[k];
+      const int rr = it / S::RW0, cc = it - rr * S::RW0;
+      if (it < N) lat0[rr * S::LP + S::LO + cc] = v[k];
     }
   }
 };
@@ -302,21 +326,73 @@ __device__ __forceinline__ void mma_tf32_1688(float (&d)[4], const uint32_t (&a)
                : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// ------------------------------------------------ TMA tile staging (TMA = true)
+// One mbarrier per CTA; thread 0 arms it with the byte count of a tile's three
+// boxes (S_1 slots, grid 1, level-0 region) and issues them; every thread waits
+// on the phase parity.
+__device__ __forceinline__ void syn_mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(syn_smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void syn_mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t b = syn_smem_u32(bar);
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(b), "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void syn_tma_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          syn_smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(syn_smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void syn_tma_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          syn_smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(syn_smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 // MLP = 0: the 1x1 stack on packed FFMA2 (one thread per vertical pixel pair);
 // MLP = 1: layer 0 as warp MMAs over m-tiles of 16 pixels, layer 1 on FFMA2
 // (chain mode only, no debug outputs).
-template <int L, int CH, int R, int K, bool DENSE_IN, bool IMG8, int MLP>
+// TMA = true (S::TMA_OK shapes, chain mode, MLP = 0): a tile whose windows
+// lie inside the latent buffers (no replicate clamping needed) is staged by
+// three TMA boxes (S_1 slots, grid 1, level-0 region) that thread 0 issues at
+// the CTA's start -- no per-element index math, clamps or register round trip;
+// border tiles use the clamped LDG staging.  Both stage the same values, so
+// the results are bit-identical.  (Persistent CTAs prefetching the next tile
+// measured slower: DESIGN.md 7.4.)
+template <int L, int CH, int R, int K, bool DENSE_IN, bool IMG8, int MLP, bool TMA>
 __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
     synth_kernel(const __grid_constant__ SynParams<L, CH, R, K> p) {
   using S = SynShape<L, CH, R, K>;
+  static_assert(!TMA || (S::TMA_OK && !DENSE_IN && MLP == 0), "TMA staging: chain mode, FFMA2 MLP");
   constexpr int RE = S::RE, RH0 = S::RH0, RW0 = S::RW0;
   constexpr int HP = RH0 * RW0;
+  constexpr int LP = S::LP, LO = S::LO;
   extern __shared__ float smem[];
-  float* bufA = smem;
-  float* bufB = smem + S::BUF_A;
-  int16_t* lat0 = reinterpret_cast<int16_t*>(smem + S::BUF_A + S::BUF_B);  // [RH0][RW0]
+  float *bufA, *bufB;
+  int16_t* lat0;
+  if constexpr (TMA) {  // 128-byte aligned TMA destinations (SynShape T_*)
+    char* b = reinterpret_cast<char*>(smem) + ((128u - (syn_smem_u32(smem) & 127u)) & 127u);
+    bufA = reinterpret_cast<float*>(b + S::T_A);
+    bufB = reinterpret_cast<float*>(b + S::T_B);
+    lat0 = reinterpret_cast<int16_t*>(b + S::T_L);
+  } else {
+    bufA = smem;
+    bufB = smem + S::BUF_A;
+    lat0 = reinterpret_cast<int16_t*>(smem + S::BUF_A + S::BUF_B);  // [RH0][LP]
+  }
   __shared__ int wlo_r[CC_MAX_LEVELS], wlo_c[CC_MAX_LEVELS];
   __shared__ double warp_buf[SYN_THREADS / 32];
+  __shared__ uint64_t tbar;
   pdl_trigger();  // the next image's synthesis may be scheduled as this grid drains
 
   const int H = p.g.H, W = p.g.W;
@@ -325,6 +401,25 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
   const int tx = blockIdx.x - ty * p.g.tiles_x;
   const int Y0 = Ys + ty * SYN_TH, X0 = tx * SYN_TW;
   const int RY = Y0 - RE, RX = X0 - RE;  // origin of the level-0 region (even)
+
+  bool staged = false;  // TMA: this tile's boxes are in flight
+  if constexpr (TMA) {
+    const int lr = ((RY >> 1) - K / 4) & ~1, lc = ((RX >> 1) - K / 4) & ~1;
+    const int blo0 = p.g.lv.lo[0], blo1 = p.g.lv.lo[1];
+    staged = RY >= blo0 && RY + RH0 <= p.g.lv.hi[0] && RX >= 0 && RX + RW0 <= W && lr >= blo1 &&
+             lr + S::NR1 <= p.g.lv.hi[1] && lc >= 0 && lc + S::NC1 <= p.g.lv.w[1];
+    if (threadIdx.x == 0) {
+      syn_mbar_init(&tbar);
+      if (staged) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(syn_smem_u32(&tbar)),
+                     "r"(S::TMA_BYTES)
+                     : "memory");
+        syn_tma_3d(bufA + S::SLOT, &p.tm_s1, &tbar, lc, lr - blo1, 0);      // stack slots 1 .. L-2
+        syn_tma_2d(bufB, &p.tm_g1, &tbar, lc - S::G0, lr - blo1);          // grid 1 (int16), in tmph's space
+        syn_tma_2d(lat0, &p.tm_lat0, &tbar, RX - LO, RY - blo0);
+      }
+    }
+  }
 
   float* wraw = smem + S::BUF_A + S::BUF_B + S::LAT0;  // MLP = 1 only: [WRAW]
   if constexpr (MLP == 1) {
@@ -346,19 +441,29 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
 
   // ---------------------------------------------------------------- 1. chain
   if constexpr (!DENSE_IN) {
-    // level 0's region (int16) and the level-1 stack (grid 1 + S_1), all
-    // loads in flight together (clamped reads = replicate padding)
+    // level 0's region (int16) and the level-1 stack (grid 1 + S_1): by TMA,
+    // else all LDG loads in flight together (clamped reads = replicate padding)
     SYN_MARK(0);
-    LoadLat0<L, CH, R, K>::run(p, lat0, RY, RX);
+    SynCtx c{bufA, bufB, wlo_r, wlo_c};
+    if (TMA && staged) {
+      syn_mbar_wait(&tbar, 0);
+      // grid 1: int16 box -> fp32 slot 0 of the stack
+      const int16_t* g1raw = reinterpret_cast<const int16_t*>(bufB);
+#pragma unroll
+      for (int k = 0; k < (S::NR1 * S::NC1 + SYN_THREADS - 1) / SYN_THREADS; k++) {
+        const int i = threadIdx.x + k * SYN_THREADS;
+        const int rr = i / S::NC1, cc = i - rr * S::NC1;
+        if (i < S::NR1 * S::NC1) bufA[i] = (float)g1raw[rr * S::GP + S::G0 + cc];
+      }
+    } else {
+      LoadLat0<L, CH, R, K>::run(p, lat0, RY, RX);
+      if constexpr (L > 1) LoadLevel1<L, CH, R, K>::run(p, c);
+    }
+    __syncthreads();
     if constexpr (L > 1) {
-      SynCtx c{bufA, bufB, wlo_r, wlo_c};
-      LoadLevel1<L, CH, R, K>::run(p, c);
-      __syncthreads();
       SYN_MARK(1);
       ChainStep<L, CH, R, K, 0>::run(p, c);  // last step's horizontal pass
       SYN_MARK(2);
-    } else {
-      __syncthreads();
     }
   }
 
@@ -394,7 +499,7 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
                           has1 ? __ldg(p.dense_in + l * P + (int64_t)(yc + 1) * W + xc) : 0.0f);
         }
       } else {
-        v[0] = f2pack((float)lat0[2 * rp * RW0 + cc], (float)lat0[(2 * rp + 1) * RW0 + cc]);
+        v[0] = f2pack((float)lat0[2 * rp * LP + LO + cc], (float)lat0[(2 * rp + 1) * LP + LO + cc]);
         if constexpr (L > 1) {
           // last vertical x2 step, both phases in one FFMA2 lane pair:
           // (out[2q], out[2q+1]) = sum_u sv[u] (k[K-1-2u], k[K-2u]) over the
@@ -525,7 +630,8 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
       // the image already hold the replicated edge rows: LoadLevel1 clamps)
       const int dr = g >> 2, dc = g & 3;
       const int srcT = (dr + (RY >> 1) - K / 4 - lo1) * RW0 + dc;
-      const int latT = 2 * dr * RW0 + dc;
+      const int latT = 2 * dr * RW0 + dc;            // in the level-0 region (hA)
+      const int latTl = 2 * dr * LP + LO + dc;       // in the lat0 buffer
       // shared-window addresses, fixed per lane: t = 3 reads a valid slot too
       // (its values are discarded by the selects below), so every lane runs
       // the same branch-free instruction stream
@@ -533,7 +639,7 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
       const int slotB = (t < 3 && chB < L) ? chB - 1 : 0;
       const uint32_t aA0 = syn_smem_u32(bufB) + 4u * (uint32_t)(slotA * S::TSLOT + srcT);
       const uint32_t aB0 = syn_smem_u32(bufB) + 4u * (uint32_t)(slotB * S::TSLOT + srcT);
-      const uint32_t aL0 = syn_smem_u32(lat0) + 2u * (uint32_t)latT;
+      const uint32_t aL0 = syn_smem_u32(lat0) + 2u * (uint32_t)latTl;
       const bool okA = (t == 3) || chA < L, okB = (t == 3) || chB < L;
 #pragma unroll 1
       for (int mt = warp; mt < NMT; mt += S::NWARPS) {
@@ -551,8 +657,8 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
             vb = ffma2(f2pack(sb[u], sb[u]), ldp2(p.w.kv[u]), vb);
           }
         }
-        const uint32_t la = aL0 + 2u * (uint32_t)moff;
-        const float l0 = (float)lds_s16(la), l1 = (float)lds_s16(la + 2u * RW0);
+        const uint32_t la = aL0 + 2u * (uint32_t)(4 * rq * LP + 4 * cq);
+        const float l0 = (float)lds_s16(la), l1 = (float)lds_s16(la + 2u * LP);
         va = (t == 3) ? f2pack(l0, l1) : va;
         vb = (t == 3) ? f2pack(1.0f, 1.0f) : vb;
         va = okA ? va : 0ull;
@@ -873,13 +979,79 @@ namespace ccrd {
 
 // ---------------------------------------------------------------- host launcher
 // one kernel variant: opt in to its dynamic shared memory size once, launch
-template <int L, int CH, int R, int K, bool DENSE_IN, bool IMG8, int MLP>
+template <int L, int CH, int R, int K, bool DENSE_IN, bool IMG8, int MLP, bool TMA = false>
 static void syn_go(const SynParams<L, CH, R, K>& p, int n_tiles, size_t smem, cudaStream_t stream) {
-  static const bool attr = (cudaFuncSetAttribute(synth_kernel<L, CH, R, K, DENSE_IN, IMG8, MLP>,
+  static const bool attr = (cudaFuncSetAttribute(synth_kernel<L, CH, R, K, DENSE_IN, IMG8, MLP, TMA>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                             true);
   (void)attr;
-  launch_ctl(synth_kernel<L, CH, R, K, DENSE_IN, IMG8, MLP>, (unsigned)n_tiles, SYN_THREADS, smem, stream, p);
+  launch_ctl(synth_kernel<L, CH, R, K, DENSE_IN, IMG8, MLP, TMA>, (unsigned)n_tiles, SYN_THREADS, smem, stream, p);
+}
+
+// ---- tensor maps of the TMA staging (driver entry point, no -lcuda)
+typedef CUresult (*SynEncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static SynEncodeTiledFn syn_encode_tiled() {
+  static const SynEncodeTiledFn fn = [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    SynEncodeTiledFn f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      f = reinterpret_cast<SynEncodeTiledFn>(ptr);
+    cudaGetLastError();
+    return f;
+  }();
+  return fn;
+}
+// The three boxes of a tile (SynShape: S_1 [L-2][NR1][NC1] fp32, grid 1
+// [NR1][GP] int16 from column lc - G0, level-0 region [RH0][LP] int16 from
+// column RX - LO).  False (LDG staging) when a buffer is not 16-byte aligned /
+// strided as TMA requires, or the encoder is unavailable.
+template <int L, int CH, int R, int K>
+static bool syn_tma_maps(SynParams<L, CH, R, K>& p) {
+  using S = SynShape<L, CH, R, K>;
+  if constexpr (!S::TMA_OK) {
+    return false;
+  } else {
+    SynEncodeTiledFn enc = syn_encode_tiled();
+    if (!enc || p.lat == nullptr || p.s1 == nullptr) return false;
+    const LevelGeom& lv = p.g.lv;
+    const int64_t W = p.g.W, w1 = lv.w[1], r0 = lv.hi[0] - lv.lo[0], r1 = lv.hi[1] - lv.lo[1];
+    const int16_t* g1 = p.lat + lv.off[1];
+    auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+    if (r0 < 1 || r1 < 1 || (W * 2) % 16 || (w1 * 2) % 16 || !al16(p.lat) || !al16(g1) || !al16(p.s1)) return false;
+    const cuuint32_t es[3] = {1, 1, 1};
+    {
+      const cuuint64_t dims[2] = {(cuuint64_t)W, (cuuint64_t)r0};
+      const cuuint64_t str[1] = {(cuuint64_t)W * 2};
+      const cuuint32_t box[2] = {(cuuint32_t)S::LP, (cuuint32_t)S::RH0};
+      if (enc(&p.tm_lat0, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, (void*)p.lat, dims, str, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    }
+    {
+      const cuuint64_t dims[2] = {(cuuint64_t)w1, (cuuint64_t)r1};
+      const cuuint64_t str[1] = {(cuuint64_t)w1 * 2};
+      const cuuint32_t box[2] = {(cuuint32_t)S::GP, (cuuint32_t)S::NR1};
+      if (enc(&p.tm_g1, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, (void*)g1, dims, str, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    }
+    {
+      const cuuint64_t dims[3] = {(cuuint64_t)w1, (cuuint64_t)r1, (cuuint64_t)(L - 2)};
+      const cuuint64_t str[2] = {(cuuint64_t)w1 * 4, (cuuint64_t)(w1 * r1 * 4)};
+      const cuuint32_t box[3] = {(cuuint32_t)S::NC1, (cuuint32_t)S::NR1, (cuuint32_t)(L - 2)};
+      if (enc(&p.tm_s1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)p.s1, dims, str, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    }
+    return true;
+  }
 }
 template <int L, int CH, int R, int K>
 static int launch_syn(const SynGeom& g, const cc_model_desc& d, const float* up_w,
@@ -929,7 +1101,16 @@ static int launch_syn(const SynGeom& g, const cc_model_desc& d, const float* up_
   constexpr bool kMmaShape = L <= 7 && CH % 8 == 0 && S::RW0 % 4 == 0 && (S::RH0 / 2) % 2 == 0;
   const bool mma = kMmaShape && !dense_in && !dense_out && !h1_out && synth_path() == CC_SYN_MMA;
   const size_t smem = mma ? S::SMEM_MMA : S::SMEM;
-  if (dense_in) {  // stage entry cc_synthesize: fp32 images only (checked by the API)
+  // TMA-staged tiles (cc_set_synth_path CC_SYN_TMA / AUTO)
+  const int sp = synth_path();
+  const bool tma = !dense_in && !dense_out && !h1_out && !mma && (sp == CC_SYN_TMA || sp == CC_SYN_AUTO) &&
+                   syn_tma_maps(p);
+  if (tma) {
+    if constexpr (S::TMA_OK) {
+      if (d.image_u8) syn_go<L, CH, R, K, false, true, 0, true>(p, g.n_tiles, S::SMEM_TMA, stream);
+      else syn_go<L, CH, R, K, false, false, 0, true>(p, g.n_tiles, S::SMEM_TMA, stream);
+    }
+  } else if (dense_in) {  // stage entry cc_synthesize: fp32 images only (checked by the API)
     syn_go<L, CH, R, K, true, false, 0>(p, g.n_tiles, smem, stream);
   } else if (mma) {
     if constexpr (kMmaShape) {

@@ -26,16 +26,19 @@ def _P():
     return P
 
 
-@pytest.fixture(autouse=True, params=["tc", "ffma2", "tc+synmma"])
+@pytest.fixture(autouse=True, params=["tc", "ffma2", "tc+synmma", "tc+syntma"])
 def arm_path(request):
     """Every parity case runs on both ARM paths (include/ccrd.h
     cc_set_arm_path): the tensor-core kernel (the default for the shapes it is
     compiled for; the others fall back to FFMA2) and the FFMA2 kernel; and
     once more with the synthesis 1x1 layer 0 on warp MMAs (cc_set_synth_path
-    CC_SYN_MMA, opt-in; the shapes and entries it does not cover run FFMA2)."""
+    CC_SYN_MMA, opt-in; the shapes and entries it does not cover run FFMA2),
+    and once with the TMA-staged persistent synthesis (CC_SYN_TMA; shapes and
+    buffers it does not cover run the per-tile FFMA2 kernel)."""
     P = _P()
     arm = P.CC_ARM_FFMA2 if request.param == "ffma2" else P.CC_ARM_TC
-    syn = P.CC_SYN_MMA if request.param.endswith("synmma") else P.CC_SYN_FFMA2
+    syn = (P.CC_SYN_MMA if request.param.endswith("synmma") else
+           P.CC_SYN_TMA if request.param.endswith("syntma") else P.CC_SYN_FFMA2)
     with P.arm_path(arm), P.synth_path(syn):
         yield request.param
 
@@ -349,3 +352,38 @@ def test_u8_training_refused():
     with pytest.raises(P.CcError) as e:
         P.cc_train_step(d, 8, 8, 8, 8, 8, None, 8, 8, 8, 1 << 30)
     assert e.value.code == P.ccrd.CC_ENOTSUP
+
+
+@pytest.mark.parametrize("name,H,W,u8", [
+    ("ref", 512, 768, False), ("ref", 333, 1024, True), ("low", 300, 512, False), ("ref", 1365, 2048, True),
+    ("ref", 200, 304, False), ("ref", 70, 128, False),
+])
+def test_synth_tma_bit_identical_to_ldg(arm_path, name, H, W, u8):
+    """CC_SYN_TMA (persistent CTAs, interior tiles staged by TMA one tile
+    ahead, border tiles by clamped LDG) stages exactly the values the per-tile
+    kernel's clamped loads read, so x_hat and every result are bit-identical
+    to CC_SYN_FFMA2 -- on shapes with many interior tiles, a ragged last tile
+    row, 8-bit targets, and W = 304 / 128 (narrow: few or no interior tiles)."""
+    if arm_path != "tc":
+        pytest.skip("one ARM path suffices: the comparison is between synthesis paths")
+    P = _P()
+    cfg = workload.CONFIGS[name].replace(H=H, W=W)
+    ims = workload.make_batch(cfg, [5, 6])
+    if u8:
+        ims = _quantised(ims)
+
+    def fwd():
+        bt = P.DeviceBatch(cfg, ims, with_xhat=True, image_u8=u8)
+        r = bt.forward()
+        torch.cuda.synchronize()
+        return r.cpu().numpy(), [t.cpu().numpy() for t in bt.xhat]
+
+    with P.synth_path(P.CC_SYN_FFMA2):
+        a, xa = fwd()
+    with P.synth_path(P.CC_SYN_TMA):
+        b, xb = fwd()
+    np.testing.assert_array_equal(a, b)
+    for u, v in zip(xa, xb):
+        np.testing.assert_array_equal(u, v)
+    if H * W <= 512 * 768:
+        check_image(cfg, ims[0], b[0], xb[0])
