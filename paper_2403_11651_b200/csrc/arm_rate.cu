@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(ARM_THREADS, ARM_CTAS_PER_SM)
   const int rlo = p.g.lv.lo[l], rhi = p.g.lv.hi[l];  // buffer window (full image: 0 .. h)
   const int own_hi = p.g.own_hi[l];
   const int t = b - p.g.tile_begin[l];
-  const int ty = t / p.g.tiles_x[l];
+  const int ty = tile_row(t, p.g.tiles_x[l], p.g.tx_mul[l]);
   const int i0 = p.g.own_lo[l] + ty * ARM_TY, j0 = (t - ty * p.g.tiles_x[l]) * ARM_TX;
   const int16_t* __restrict__ grid = p.lat + p.g.lv.off[l];
 

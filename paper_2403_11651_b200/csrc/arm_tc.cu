@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(ArmTcgShape<C, NH>::THREADS, 1)
 #pragma unroll 1
     while (l + 1 < p.g.L && tile >= p.g.tile_begin[l + 1]) l++;
     const int tt = tile - p.g.tile_begin[l];
-    const int ty = tt / p.g.tiles_x[l];
+    const int ty = tile_row(tt, p.g.tiles_x[l], p.g.tx_mul[l]);
     i0 = p.g.own_lo[l] + ty * ARM_TY;
     j0 = (tt - ty * p.g.tiles_x[l]) * ARM_TX;
   };
@@ -635,7 +635,7 @@ __global__ void __maxnreg__(CCRD_TCP_MAXREG)
 #pragma unroll 1
     while (l + 1 < p.g.L && tile >= p.g.tile_begin[l + 1]) l++;
     const int tt = tile - p.g.tile_begin[l];
-    const int ty = tt / p.g.tiles_x[l];
+    const int ty = tile_row(tt, p.g.tiles_x[l], p.g.tx_mul[l]);
     i0 = p.g.own_lo[l] + ty * ARM_TY;
     j0 = (tt - ty * p.g.tiles_x[l]) * ARM_TX;
   };
@@ -690,7 +690,7 @@ __global__ void __maxnreg__(CCRD_TCP_MAXREG)
   // per-slot state of the block in flight: centre value, validity, index
   float ys[2];
   bool valid[2];
-  int64_t qidx[2];
+  int64_t qidx[2] = {0, 0};
   float tbits = 0.0f;
   // block b (tile b / 4, q = b % 4) into slot s, then MMA0; SPLIT: the exact
   // path with the context split c = c_hi + c_lo (window staged by the caller)
@@ -711,7 +711,7 @@ __global__ void __maxnreg__(CCRD_TCP_MAXREG)
     }
     const int i = c_i0 + ry, j = c_j0 + cx, w = p.g.lv.w[c_l];
     valid[s] = i < p.g.own_hi[c_l] && j < w;
-    qidx[s] = p.g.lv.off[c_l] + (int64_t)(i - p.g.lv.lo[c_l]) * w + j;
+    if (p.bits != nullptr) qidx[s] = p.g.lv.off[c_l] + (int64_t)(i - p.g.lv.lo[c_l]) * w + j;  // debug outputs only
     tmem_wait_st();
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncwarp();

@@ -292,7 +292,12 @@ static void arm_geom(const cc_model_desc& d, const cc_strip* win, ArmGeom& g) {
       g.own_lo[l] = win ? win->own_lo[l] : 0;
       g.own_hi[l] = win ? win->own_hi[l] : g.lv.h[l];
       g.tiles_x[l] = (g.lv.w[l] + ARM_TX - 1) / ARM_TX;
-      acc += g.tiles_x[l] * ((g.own_hi[l] - g.own_lo[l] + ARM_TY - 1) / ARM_TY);
+      const int64_t nt = (int64_t)g.tiles_x[l] * ((g.own_hi[l] - g.own_lo[l] + ARM_TY - 1) / ARM_TY);
+      // m = ceil(2^32 / d), e = m d - 2^32 < d: floor(n m / 2^32) = floor(n / d)
+      // for n e < 2^32, which n < nt, nt d < 2^32 guarantees
+      const uint64_t dx = (uint64_t)(g.tiles_x[l] > 0 ? g.tiles_x[l] : 1);
+      g.tx_mul[l] = (dx > 1 && (uint64_t)nt * dx < (1ull << 32)) ? (uint32_t)(((1ull << 32) + dx - 1) / dx) : 0u;
+      acc += (int)nt;
     }
   }
   g.tile_begin[CC_MAX_LEVELS] = acc;

@@ -43,6 +43,11 @@ __device__ __forceinline__ uint64_t ldp2(const float2& v) {
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
 
+// tile row of tile tt in a level with `tx` tiles per row (ArmGeom::tx_mul)
+__device__ __forceinline__ int tile_row(int tt, int tx, uint32_t mul) {
+  return mul ? (int)__umulhi((uint32_t)tt, mul) : tt / tx;
+}
+
 // Single-MUFU base-2 exponential / logarithm (PTX ex2.approx / lg2.approx).
 __device__ __forceinline__ float exp2f_approx(float x) {
   float r;
@@ -111,6 +116,10 @@ struct ArmGeom {
   LevelGeom lv;
   int32_t L;
   int32_t tiles_x[CC_MAX_LEVELS];
+  // ceil(2^32 / tiles_x): tile row = umulhi(t, tx_mul) for every tile t of
+  // the level (exact while tiles x tiles_x < 2^32, checked on the host; 0 =
+  // use the division)
+  uint32_t tx_mul[CC_MAX_LEVELS];
   int32_t tile_begin[CC_MAX_LEVELS + 1];  // prefix over levels; [L] = total CTAs
   int32_t own_lo[CC_MAX_LEVELS];          // latent rows whose rate this launch counts
   int32_t own_hi[CC_MAX_LEVELS];          //   (full image: 0 .. h)
