@@ -53,7 +53,7 @@ def tf32_peak_tflops():
 
 def arm_tc_mac_per_latent(cfg):
     """tcgen05 multiply-accumulates the tensor-core ARM issues per latent
-    (arm_tc.cu arm_tcg_kernel): layer 0 = context (K0 = C + 8 columns incl. the
+    (arm_tc.cu arm_tcp_kernel / arm_tcg_kernel): layer 0 = context (K0 = C + 8 columns incl. the
     bias block) x (W_hi + W_lo); hidden layer = A_hi (K1 = NH + 8) x (W_hi +
     W_lo) + A_lo (NH) x W_hi; N = NH.  The 2-wide output layer runs on the CUDA
     cores."""
@@ -233,7 +233,10 @@ def run_ours(args, rk):
     # per-kernel rooflines; the headline `roofline` is the kernel with the
     # largest share of the serial step
     arm_tc = P.cc_arm_path_for(desc) == P.CC_ARM_TC
-    arm_name = "arm_tcg_kernel" if arm_tc else "arm_rate_kernel"
+    # the tensor-core ARM's default kernel is the ping-pong one (arm_tc.cu;
+    # CCRD_ARM_TC_PP=0 selects the one-block arm_tcg_kernel)
+    arm_name = (("arm_tcg_kernel" if os.environ.get("CCRD_ARM_TC_PP", "1") == "0" else "arm_tcp_kernel")
+                if arm_tc else "arm_rate_kernel")
     arm_avg_s = prof.arm_ms / max(1, prof.arm_launches) / 1e3
     syn_avg_s = prof.syn_ms / max(1, prof.syn_launches) / 1e3
     arm_tflops = 2.0 * macs.arm_macs / arm_avg_s / 1e12            # fp32-accurate algorithmic FLOP
@@ -390,6 +393,21 @@ def run_strip(args, rk):
     arm_pl = sum(cfg.arm_widths[k] * cfg.arm_widths[k + 1] for k in range(len(cfg.arm_widths) - 1))
     arm_tflops = 2.0 * own_lat * arm_pl / arm_avg_s / 1e12
     path_tflops = 2.0 * macs.total * value / rk.world / 1e12
+    if P.cc_arm_path_for(desc) == P.CC_ARM_TC:
+        # the tensor-core ARM against the TF32 tensor peak with the executed
+        # 3xTF32 MACs (as the headline's `kernels` entry), fp32-equivalent beside
+        tf32_peak, tf32_src = tf32_peak_tflops()
+        tc_tflops = 2.0 * own_lat * arm_tc_mac_per_latent(cfg) / arm_avg_s / 1e12
+        arm_roof = {"bound": "tensor", "kernel": "arm_tcp_kernel", "achieved": tc_tflops, "peak": tf32_peak,
+                    "unit": "TFLOP/s", "frac": tc_tflops / tf32_peak, "traffic": None,
+                    "algorithmic": f"{own_lat} latents x {arm_tc_mac_per_latent(cfg)} TF32 tensor MAC per launch "
+                                   f"(3xTF32 split of the {arm_pl}-MAC fp32 ARM)",
+                    "peak_source": tf32_src, "fp32_equiv_tflops": arm_tflops,
+                    "fp32_equiv_frac_of_fp32_peak": arm_tflops / FP32_PEAK_TFLOPS, "avg_launch_ms": arm_avg_s * 1e3}
+    else:
+        arm_roof = {"bound": "alu", "kernel": "arm_rate_kernel", "achieved": arm_tflops, "peak": FP32_PEAK_TFLOPS,
+                    "unit": "TFLOP/s", "frac": arm_tflops / FP32_PEAK_TFLOPS, "traffic": None,
+                    "avg_launch_ms": arm_avg_s * 1e3}
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": rk.world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -401,10 +419,7 @@ def run_strip(args, rk):
                    "strip_rows": [st.r0, st.r1], "halo_bytes_recv_per_step_rank0": halo_bytes[0],
                    "l2": "inputs larger than L2 (0.4 GB of image + latents per step)",
                    "parallelism": f"strips x{rk.world}, NCCL halo exchange + all-reduce"},
-        "roofline": {"bound": "alu", "kernel": "arm_rate_kernel" if P.cc_arm_path_for(desc) != P.CC_ARM_TC
-                     else "arm_tcg_kernel (fp32-equivalent FLOP vs the FP32 peak)", "achieved": arm_tflops,
-                     "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": arm_tflops / FP32_PEAK_TFLOPS, "traffic": None,
-                     "avg_launch_ms": arm_avg_s * 1e3},
+        "roofline": arm_roof,
         "path_roofline": {"achieved_tflops_per_gpu": path_tflops, "frac": path_tflops / FP32_PEAK_TFLOPS},
         "e2e": None, "gpu_launches": launches, "clocks": sampler.summary(), "input_gen_s": round(gen_s, 2),
     }

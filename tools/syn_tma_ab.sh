@@ -11,5 +11,5 @@ for v in $VARS; do
 import json,sys
 d=json.loads(sys.stdin.read().strip().splitlines()[-1])
 k=d['kernels']
-print('value %.4e  synth %.1f us  arm %.1f us  frac %.3f' % (d['value'], k['synth_kernel']['avg_launch_ms']*1e3, k['arm_tcg_kernel']['avg_launch_ms']*1e3, d['roofline']['frac']))"
+print('value %.4e  synth %.1f us  arm %.1f us  frac %.3f' % (d['value'], k['synth_kernel']['avg_launch_ms']*1e3, k.get('arm_tcp_kernel', k.get('arm_tcg_kernel'))['avg_launch_ms']*1e3, d['roofline']['frac']))"
 done
