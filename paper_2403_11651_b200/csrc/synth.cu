@@ -191,31 +191,46 @@ struct ChainStep {
 
   static __device__ __forceinline__ void run(const SynParams<L, CH, R, K>& p, const SynCtx& c) {
     const float* kk = p.w.k;
-    // ---- horizontal: (rows of window J+1) x (cols of window J), column pairs
+    // ---- horizontal: (rows of window J+1) x (cols of window J); each thread
+    // owns PPT adjacent column pairs of a row (PPT = 2: 6 loads feed 4
+    // outputs, one 16-byte store), the same FMA order per output
     {
       constexpr int NCP = NCd / 2;
-      constexpr int NRG = SYN_THREADS / NCP;
-      const int cp = threadIdx.x % NCP, rg = threadIdx.x / NCP;
+      constexpr int PPT = (NCP % 2 == 0 && NCd % 4 == 0 && S::TSLOT % 4 == 0 && S::BUF_A % 4 == 0) ? 2 : 1;
+      constexpr int NCQ = NCP / PPT;
+      constexpr int NRG = SYN_THREADS / NCQ;
+      constexpr int NSV = K / 2 + PPT;  // sources of PPT pairs
+      const int cq = threadIdx.x % NCQ, rg = threadIdx.x / NCQ;
       if (rg < NRG) {
-        const int q = (c.wlo_c[J] >> 1) + cp;  // (lo_c[J] + 2 cp) / 2; lo_c[J] even
+        const int q = (c.wlo_c[J] >> 1) + PPT * cq;  // (lo_c[J] + 2 PPT cq) / 2; lo_c[J] even
         const int ws = p.g.lv.w[J + 1], lo_s = c.wlo_c[J + 1];
-        int off[K / 2 + 1];
+        int off[NSV];
 #pragma unroll
-        for (int u = 0; u <= K / 2; u++) off[u] = clampi(q - K / 4 + u, 0, ws - 1) - lo_s;
+        for (int u = 0; u < NSV; u++) off[u] = clampi(q - K / 4 + u, 0, ws - 1) - lo_s;
 #pragma unroll 2
         for (int k = rg; k < NSL * NRs; k += NRG) {
           const int sl = k / NRs, row = k - sl * NRs;
           const float* src = c.stack + (J + sl) * S::SLOT + row * NCs;
-          float sv[K / 2 + 1];
+          float sv[NSV];
 #pragma unroll
-          for (int u = 0; u <= K / 2; u++) sv[u] = src[off[u]];
-          float a0 = 0.0f, a1 = 0.0f;
+          for (int u = 0; u < NSV; u++) sv[u] = src[off[u]];
+          float a[2 * PPT];
 #pragma unroll
-          for (int t = 0; t < K / 2; t++) {
-            a0 = fmaf(kk[2 * t + 1], sv[K / 2 - 1 - t], a0);
-            a1 = fmaf(kk[2 * t], sv[K / 2 - t], a1);
+          for (int pr = 0; pr < PPT; pr++) {
+            float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+            for (int t = 0; t < K / 2; t++) {
+              a0 = fmaf(kk[2 * t + 1], sv[pr + K / 2 - 1 - t], a0);
+              a1 = fmaf(kk[2 * t], sv[pr + K / 2 - t], a1);
+            }
+            a[2 * pr] = a0;
+            a[2 * pr + 1] = a1;
           }
-          *reinterpret_cast<float2*>(c.tmph + (J + sl) * S::TSLOT + row * NCd + 2 * cp) = make_float2(a0, a1);
+          float* dst = c.tmph + (J + sl) * S::TSLOT + row * NCd + 2 * PPT * cq;
+          if constexpr (PPT == 2)
+            *reinterpret_cast<float4*>(dst) = make_float4(a[0], a[1], a[2], a[3]);
+          else
+            *reinterpret_cast<float2*>(dst) = make_float2(a[0], a[1]);
         }
       }
     }
@@ -462,7 +477,9 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
     __syncthreads();
     if constexpr (L > 1) {
       SYN_MARK(1);
+#ifndef CCRD_SYN_EXP_NOCHAIN  // timing experiment only (wrong results): no horizontal pass
       ChainStep<L, CH, R, K, 0>::run(p, c);  // last step's horizontal pass
+#endif
       SYN_MARK(2);
     }
   }
@@ -539,6 +556,9 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
     auto needed = [&](int item) {  // read by the convs (inside the image)
       const int rp = item / RW0, cc = item - (item / RW0) * RW0;
       const int y0 = RY + 2 * rp, x = RX + cc;
+#ifdef CCRD_SYN_EXP_NOHALO  // timing experiment only (wrong results): no MLP on the halo rows
+      if (2 * rp < RE || 2 * rp >= RE + SYN_TH) return false;
+#endif
       return item < NPAIR && !(x < 0 || x >= W || y0 + 1 < 0 || y0 >= H);
     };
     auto store = [&](int item, const uint64_t (&v)[L], const uint64_t (&op)[3]) {
@@ -894,7 +914,11 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
     }
     // halo ring of width e around the tile (non-last layers only), enumerated
     // directly: top / bottom rows, then left / right columns
+#ifdef CCRD_SYN_EXP_NORING  // timing experiment only (wrong results): no conv halo ring
+    if (false) {
+#else
     if (e > 0) {
+#endif
       const int NWr = SYN_TW + 2 * e;
       const int n_top = e * NWr, n_side = e * SYN_TH;
 #pragma unroll 1
