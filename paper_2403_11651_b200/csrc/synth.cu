@@ -374,6 +374,11 @@ __device__ __forceinline__ void syn_tma_3d(void* dst, const CUtensorMap* m, uint
       : "memory");
 }
 
+// ---- thread-block cluster helpers (CLU: vertical tile pairs)
+__device__ __forceinline__ void syn_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // MLP = 0: the 1x1 stack on packed FFMA2 (one thread per vertical pixel pair);
 // MLP = 1: layer 0 as warp MMAs over m-tiles of 16 pixels, layer 1 on FFMA2
 // (chain mode only, no debug outputs).
@@ -384,11 +389,12 @@ __device__ __forceinline__ void syn_tma_3d(void* dst, const CUtensorMap* m, uint
 // border tiles use the clamped LDG staging.  Both stage the same values, so
 // the results are bit-identical.  (Persistent CTAs prefetching the next tile
 // measured slower: DESIGN.md 7.4.)
-template <int L, int CH, int R, int K, bool DENSE_IN, bool IMG8, int MLP, bool TMA>
+template <int L, int CH, int R, int K, bool DENSE_IN, bool IMG8, int MLP, bool TMA, bool CLU = false>
 __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
     synth_kernel(const __grid_constant__ SynParams<L, CH, R, K> p) {
   using S = SynShape<L, CH, R, K>;
   static_assert(!TMA || (S::TMA_OK && !DENSE_IN && MLP == 0), "TMA staging: chain mode, FFMA2 MLP");
+  static_assert(!CLU || (TMA && S::RE == 2 && (R == 1 || R == 2)), "vertical pairs: one halo pair-row, one ring row");
   constexpr int RE = S::RE, RH0 = S::RH0, RW0 = S::RW0;
   constexpr int HP = RH0 * RW0;
   constexpr int LP = S::LP, LO = S::LO;
@@ -412,10 +418,35 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
 
   const int H = p.g.H, W = p.g.W;
   const int Ys = p.g.y0, Ye = p.g.y1;  // output rows (full image: 0 .. H); x_hat / image rows are Ys-relative
-  const int ty = blockIdx.x / p.g.tiles_x;
-  const int tx = blockIdx.x - ty * p.g.tiles_x;
+  // CLU: a cluster of two CTAs = two vertically adjacent tiles (rank 0 on top);
+  // each computes the 1x1 stack and the first 3x3 layer for its own rows only
+  // and reads the partner's rows it needs as halo through distributed shared
+  // memory.  A rank-1 CTA past the last tile row (odd tile rows) only joins
+  // the cluster barriers.
+  int ty, tx, tile, rank = 0;
+  bool partner = false;
+  if constexpr (CLU) {
+    const int tiles_y = p.g.n_tiles / p.g.tiles_x;
+    rank = (int)(blockIdx.x & 1u);
+    const int pr = (int)(blockIdx.x >> 1), py = pr / p.g.tiles_x;
+    tx = pr - py * p.g.tiles_x;
+    ty = 2 * py + rank;
+    tile = ty * p.g.tiles_x + tx;
+    partner = rank ? true : (ty + 1 < tiles_y);
+    if (ty >= tiles_y) {  // ghost: the partner's cluster barriers (after the 1x1 stack, each non-last 3x3 layer, the end)
+#pragma unroll
+      for (int k = 0; k < R + 1; k++) syn_cluster_sync();
+      return;
+    }
+  } else {
+    ty = blockIdx.x / p.g.tiles_x;
+    tx = blockIdx.x - ty * p.g.tiles_x;
+    tile = blockIdx.x;
+  }
   const int Y0 = Ys + ty * SYN_TH, X0 = tx * SYN_TW;
   const int RY = Y0 - RE, RX = X0 - RE;  // origin of the level-0 region (even)
+  // CLU: the pair-row of the region the partner computes (-1: none)
+  const int shared_rp = (CLU && partner) ? (rank ? 0 : RH0 / 2 - 1) : -1;
 
   bool staged = false;  // TMA: this tile's boxes are in flight
   if constexpr (TMA) {
@@ -553,9 +584,10 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
         }
       }
     };
-    auto needed = [&](int item) {  // read by the convs (inside the image)
+    auto needed = [&](int item) {  // read by the convs (inside the image), not computed by the partner
       const int rp = item / RW0, cc = item - (item / RW0) * RW0;
       const int y0 = RY + 2 * rp, x = RX + cc;
+      if (CLU && rp == shared_rp) return false;
 #ifdef CCRD_SYN_EXP_NOHALO  // timing experiment only (wrong results): no MLP on the halo rows
       if (2 * rp < RE || 2 * rp >= RE + SYN_TH) return false;
 #endif
@@ -749,6 +781,22 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
     }
   }
   __syncthreads();
+  if constexpr (CLU) {  // the partner's 1x1 outputs of my shared pair-row
+    syn_cluster_sync();
+    if (partner) {
+      const int src = rank ? RH0 - 4 : 2, dst = rank ? 0 : RH0 - 2;  // region rows (partner / mine)
+      const uint32_t local = syn_smem_u32(bufA);
+      uint32_t remote;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank ^ 1));
+      for (int i = threadIdx.x; i < 3 * 2 * RW0; i += SYN_THREADS) {
+        const int c = i / (2 * RW0), rr = i - c * 2 * RW0;  // rr = row (0..1) x RW0 + column
+        float v;
+        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote + 4u * (uint32_t)(c * HP + src * RW0 + rr)) : "memory");
+        bufA[c * HP + dst * RW0 + rr] = v;
+      }
+    }
+    __syncthreads();
+  }
 
   SYN_MARK(3);
   // ------------------------------------------------- 3. residual 3x3 layers
@@ -937,6 +985,7 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
           x = (j0 < n_side) ? X0 - e + (j - rr * e) : X0 + SYN_TW + (j - rr * e);
         }
         if (y < 0 || y >= H || x < 0 || x >= W) continue;
+        if (CLU && partner && (rank ? y < Y0 : y >= Y0 + SYN_TH)) continue;  // the partner's interior row
         float o[3];
         conv_px(r, y, x, o);
         const int ctr = (y - RY) * RW0 + (x - RX);
@@ -946,6 +995,22 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
     }
     if (!last) {
       __syncthreads();
+      if constexpr (CLU) {  // the partner's first-layer outputs of my shared ring row (region columns 1 .. RW0-2)
+        syn_cluster_sync();
+        if (partner) {
+          const int src = rank ? RH0 - 3 : 2, dst = rank ? 1 : RH0 - 2;
+          const uint32_t local = syn_smem_u32(hout);
+          uint32_t remote;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank ^ 1));
+          for (int i = threadIdx.x; i < 3 * (RW0 - 2); i += SYN_THREADS) {
+            const int c = i / (RW0 - 2), cc = 1 + i - c * (RW0 - 2);
+            float v;
+            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote + 4u * (uint32_t)(c * HP + src * RW0 + cc)) : "memory");
+            hout[c * HP + dst * RW0 + cc] = v;
+          }
+        }
+        __syncthreads();
+      }
       SYN_MARK(4);
       float* t = hin;
       hin = hout;
@@ -981,7 +1046,8 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
 
   // ------------------------------------------------------ 4. distortion
   const double s = block_sum<SYN_THREADS>(sse, warp_buf);
-  if (threadIdx.x == 0 && p.partial != nullptr) p.partial[blockIdx.x] = s;
+  if (threadIdx.x == 0 && p.partial != nullptr) p.partial[tile] = s;
+  if constexpr (CLU) syn_cluster_sync();  // the partner has read my shared memory
   SYN_MARK(5);
 #ifdef CCRD_SYN_TIMING
   if (threadIdx.x == 0 && blockIdx.x < (1 << 16)) {
@@ -1010,6 +1076,39 @@ static void syn_go(const SynParams<L, CH, R, K>& p, int n_tiles, size_t smem, cu
                             true);
   (void)attr;
   launch_ctl(synth_kernel<L, CH, R, K, DENSE_IN, IMG8, MLP, TMA>, (unsigned)n_tiles, SYN_THREADS, smem, stream, p);
+}
+
+// CLU: clusters of two vertically adjacent tiles, grid = 2 x tiles_x x
+// ceil(tiles_y / 2) (a rank-1 CTA past the last tile row is a ghost)
+template <int L, int CH, int R, int K, bool IMG8>
+static void syn_go_pairs(const SynParams<L, CH, R, K>& p, size_t smem, cudaStream_t stream) {
+  auto kern = synth_kernel<L, CH, R, K, false, IMG8, 0, true, true>;
+  static const bool attr = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), true);
+  (void)attr;
+  const int tiles_y = p.g.n_tiles / p.g.tiles_x;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * p.g.tiles_x * ((tiles_y + 1) / 2)));
+  cfg.blockDim = dim3(SYN_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_launch_ctl.pdl ? 2 : 1;
+  cudaLaunchKernelEx(&cfg, kern, p);
+}
+// Opt-in (CCRD_SYN_CLU=1, read per launch: tests toggle it): measured slower
+// than one CTA per tile (108.0 vs 100.3 us per 2K image, path 1.742e10 vs
+// 1.839e10 px/s) -- the three cluster barriers hold both CTAs of a pair in
+// step and cost more than the 1x1 / 3x3 rows they save.
+static bool syn_pairs_enabled() {
+  const char* e = getenv("CCRD_SYN_CLU");
+  return e && e[0] == '1';
 }
 
 // ---- tensor maps of the TMA staging (driver entry point, no -lcuda)
@@ -1131,8 +1230,17 @@ static int launch_syn(const SynGeom& g, const cc_model_desc& d, const float* up_
                    syn_tma_maps(p);
   if (tma) {
     if constexpr (S::TMA_OK) {
-      if (d.image_u8) syn_go<L, CH, R, K, false, true, 0, true>(p, g.n_tiles, S::SMEM_TMA, stream);
-      else syn_go<L, CH, R, K, false, false, 0, true>(p, g.n_tiles, S::SMEM_TMA, stream);
+      constexpr bool kPairs = S::RE == 2 && (R == 1 || R == 2);
+      if (kPairs && syn_pairs_enabled() && g.n_tiles / g.tiles_x >= 2) {
+        if constexpr (kPairs) {
+          if (d.image_u8) syn_go_pairs<L, CH, R, K, true>(p, S::SMEM_TMA, stream);
+          else syn_go_pairs<L, CH, R, K, false>(p, S::SMEM_TMA, stream);
+        }
+      } else if (d.image_u8) {
+        syn_go<L, CH, R, K, false, true, 0, true>(p, g.n_tiles, S::SMEM_TMA, stream);
+      } else {
+        syn_go<L, CH, R, K, false, false, 0, true>(p, g.n_tiles, S::SMEM_TMA, stream);
+      }
     }
   } else if (dense_in) {  // stage entry cc_synthesize: fp32 images only (checked by the API)
     syn_go<L, CH, R, K, true, false, 0>(p, g.n_tiles, smem, stream);

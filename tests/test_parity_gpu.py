@@ -9,6 +9,7 @@ Tolerances (north_star; DESIGN.md "Tolerances"):
   * dense upsampled tensor: per level 1e-5 relative to the level's max |value|.
 """
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -356,14 +357,17 @@ def test_u8_training_refused():
 
 @pytest.mark.parametrize("name,H,W,u8", [
     ("ref", 512, 768, False), ("ref", 333, 1024, True), ("low", 300, 512, False), ("ref", 1365, 2048, True),
-    ("ref", 200, 304, False), ("ref", 70, 128, False),
+    ("ref", 200, 304, False), ("ref", 70, 128, False), ("tiny", 200, 256, False), ("tiny", 160, 512, True),
 ])
 def test_synth_tma_bit_identical_to_ldg(arm_path, name, H, W, u8):
-    """CC_SYN_TMA (persistent CTAs, interior tiles staged by TMA one tile
-    ahead, border tiles by clamped LDG) stages exactly the values the per-tile
-    kernel's clamped loads read, so x_hat and every result are bit-identical
-    to CC_SYN_FFMA2 -- on shapes with many interior tiles, a ragged last tile
-    row, 8-bit targets, and W = 304 / 128 (narrow: few or no interior tiles)."""
+    """CC_SYN_TMA (interior tiles staged by TMA, border tiles by clamped LDG;
+    one CTA per tile, or with CCRD_SYN_CLU=1 vertical tile pairs in 2-CTA
+    clusters that exchange their shared halo rows through distributed shared
+    memory) computes every pixel exactly as the per-tile LDG kernel
+    does, so x_hat and every result are bit-identical to CC_SYN_FFMA2 -- on
+    shapes with many interior tiles, odd and even tile-row counts (a ghost
+    CTA in the last pair), a ragged last tile row, 8-bit targets, and
+    W = 304 / 128 (narrow: few or no interior tiles)."""
     if arm_path != "tc":
         pytest.skip("one ARM path suffices: the comparison is between synthesis paths")
     P = _P()
@@ -381,9 +385,16 @@ def test_synth_tma_bit_identical_to_ldg(arm_path, name, H, W, u8):
     with P.synth_path(P.CC_SYN_FFMA2):
         a, xa = fwd()
     with P.synth_path(P.CC_SYN_TMA):
-        b, xb = fwd()
+        b, xb = fwd()  # one CTA per tile (the default)
+        os.environ["CCRD_SYN_CLU"] = "1"
+        try:
+            c, xc = fwd()  # vertical tile pairs in 2-CTA clusters (opt-in)
+        finally:
+            del os.environ["CCRD_SYN_CLU"]
     np.testing.assert_array_equal(a, b)
-    for u, v in zip(xa, xb):
+    np.testing.assert_array_equal(a, c)
+    for u, v, w in zip(xa, xb, xc):
         np.testing.assert_array_equal(u, v)
+        np.testing.assert_array_equal(u, w)
     if H * W <= 512 * 768:
         check_image(cfg, ims[0], b[0], xb[0])
