@@ -48,43 +48,55 @@ __global__ void __launch_bounds__(PYR_THREADS)
     sw[it] = (k == 0) ? (float)__ldg(lat + gi) : __ldg(Sn + (int64_t)(k - 1) * ns * ws + gi);
   }
   __syncthreads();
-  // horizontal: column pairs (2q, 2q+1) share sources q - K/4 .. q + K/4 ----
+  // horizontal: column pairs (2q, 2q+1) share sources q - K/4 .. q + K/4; a
+  // thread takes two adjacent pairs (6 loads feed 4 outputs, one 16-byte store)
 #pragma unroll 2
-  for (int it = threadIdx.x; it < nch * SR * (PYR_TW / 2); it += PYR_THREADS) {
-    const int row = it / (PYR_TW / 2), cp = it - row * (PYR_TW / 2);  // row = k * SR + rr
-    const float* src = sw + row * SC + cp;
-    float s[K / 2 + 1];
+  for (int it = threadIdx.x; it < nch * SR * (PYR_TW / 4); it += PYR_THREADS) {
+    const int row = it / (PYR_TW / 4), cq = it - row * (PYR_TW / 4);  // row = k * SR + rr
+    const float* src = sw + row * SC + 2 * cq;
+    float s[K / 2 + 2];
 #pragma unroll
-    for (int u = 0; u <= K / 2; u++) s[u] = src[u];
-    float a0 = 0.0f, a1 = 0.0f;
+    for (int u = 0; u < K / 2 + 2; u++) s[u] = src[u];
+    float a[4];
 #pragma unroll
-    for (int t = 0; t < K / 2; t++) {
-      a0 = fmaf(im.k[2 * t + 1], s[K / 2 - 1 - t], a0);
-      a1 = fmaf(im.k[2 * t], s[K / 2 - t], a1);
+    for (int pr = 0; pr < 2; pr++) {
+      float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+      for (int t = 0; t < K / 2; t++) {
+        a0 = fmaf(im.k[2 * t + 1], s[pr + K / 2 - 1 - t], a0);
+        a1 = fmaf(im.k[2 * t], s[pr + K / 2 - t], a1);
+      }
+      a[2 * pr] = a0;
+      a[2 * pr + 1] = a1;
     }
-    *reinterpret_cast<float2*>(tmp + row * PYR_TW + 2 * cp) = make_float2(a0, a1);
+    *reinterpret_cast<float4*>(tmp + row * PYR_TW + 4 * cq) = make_float4(a[0], a[1], a[2], a[3]);
   }
   __syncthreads();
-  // vertical: row pairs, stored (cropped) to S_j[k] ----------------------------
+  // vertical: row pairs, stored (cropped) to S_j[k]; a thread takes two
+  // adjacent row pairs of a column (6 loads feed 4 outputs) ------------------
 #pragma unroll 2
-  for (int it = threadIdx.x; it < nch * (PYR_TH / 2) * PYR_TW; it += PYR_THREADS) {
+  for (int it = threadIdx.x; it < nch * (PYR_TH / 4) * PYR_TW; it += PYR_THREADS) {
     const int kr = it / PYR_TW, cc = it - kr * PYR_TW;
-    const int k = kr / (PYR_TH / 2), rp = kr - k * (PYR_TH / 2);
-    const float* src = tmp + (k * SR + rp) * PYR_TW + cc;
-    float s[K / 2 + 1];
+    const int k = kr / (PYR_TH / 4), rq = kr - k * (PYR_TH / 4);
+    const float* src = tmp + (k * SR + 2 * rq) * PYR_TW + cc;
+    float s[K / 2 + 2];
 #pragma unroll
-    for (int u = 0; u <= K / 2; u++) s[u] = src[u * PYR_TW];
-    float a0 = 0.0f, a1 = 0.0f;
+    for (int u = 0; u < K / 2 + 2; u++) s[u] = src[u * PYR_TW];
+    const int x = X0 + cc;
+    float* dst = Sj + (int64_t)k * nj * wj + x;
 #pragma unroll
-    for (int t = 0; t < K / 2; t++) {
-      a0 = fmaf(im.k[2 * t + 1], s[K / 2 - 1 - t], a0);
-      a1 = fmaf(im.k[2 * t], s[K / 2 - t], a1);
-    }
-    const int y = Y0 + 2 * rp, x = X0 + cc;
-    if (x < wj) {
-      float* dst = Sj + (int64_t)k * nj * wj + (int64_t)(y - loj) * wj + x;
-      if (y >= loj && y < hij) dst[0] = a0;
-      if (y + 1 >= loj && y + 1 < hij) dst[wj] = a1;
+    for (int pr = 0; pr < 2; pr++) {
+      float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+      for (int t = 0; t < K / 2; t++) {
+        a0 = fmaf(im.k[2 * t + 1], s[pr + K / 2 - 1 - t], a0);
+        a1 = fmaf(im.k[2 * t], s[pr + K / 2 - t], a1);
+      }
+      const int y = Y0 + 4 * rq + 2 * pr;
+      if (x < wj) {
+        if (y >= loj && y < hij) dst[(int64_t)(y - loj) * wj] = a0;
+        if (y + 1 >= loj && y + 1 < hij) dst[(int64_t)(y + 1 - loj) * wj] = a1;
+      }
     }
   }
 }
