@@ -1,15 +1,18 @@
 #!/bin/bash
-# A/B of the synthesis staging paths on the headline workload (run under gpurun):
-# per-tile LDG kernel (ffma2) vs TMA-staged persistent CTAs (tma, 1 / 2 CTAs per SM).
+# A/B of the synthesis variants on the headline workload (run under gpurun):
+#   AB_VARIANTS="ffma2 tma tma:clu" bash tools/syn_tma_ab.sh
+# ffma2 = per-tile kernel with clamped LDG staging, tma = TMA-staged interior
+# tiles (the default), tma:clu = + vertical tile pairs in 2-CTA clusters.
 CMD="python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline"
-VARS=${AB_VARIANTS:-"ffma2:2 tma:2 tma:1 ffma2:2 tma:2"}
+VARS=${AB_VARIANTS:-"ffma2 tma ffma2 tma"}
 for v in $VARS; do
-  v=${v/:/ }
-  set -- $v
-  echo "== path=$1 pctas=$2"
-  CCRD_SYN_PATH=$1 CCRD_SYN_PCTAS=$2 $CMD 2>/dev/null | python -c "
+  path=${v%%:*}
+  clu=0; [ "$v" != "${v%:clu}" ] && clu=1
+  echo "== path=$path clusters=$clu"
+  CCRD_SYN_PATH=$path CCRD_SYN_CLU=$clu $CMD 2>/dev/null | python -c "
 import json,sys
 d=json.loads(sys.stdin.read().strip().splitlines()[-1])
 k=d['kernels']
-print('value %.4e  synth %.1f us  arm %.1f us  frac %.3f' % (d['value'], k['synth_kernel']['avg_launch_ms']*1e3, k.get('arm_tcp_kernel', k.get('arm_tcg_kernel'))['avg_launch_ms']*1e3, d['roofline']['frac']))"
+a=k.get('arm_tcp_kernel', k.get('arm_tcg_kernel'))
+print('value %.4e  synth %.1f us  arm %.1f us  frac %.3f' % (d['value'], k['synth_kernel']['avg_launch_ms']*1e3, a['avg_launch_ms']*1e3, d['roofline']['frac']))"
 done
