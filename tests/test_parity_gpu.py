@@ -78,6 +78,7 @@ def test_rd_forward_configs(name, filt):
 @pytest.mark.parametrize("H,W,L,res,taps", [
     (37, 53, 5, 1, 8), (37, 53, 5, 1, 4), (33, 97, 4, 1, 8), (65, 129, 4, 3, 8), (64, 64, 4, 0, 8),
     (1, 1, 1, 1, 8), (3, 300, 2, 1, 8), (300, 3, 2, 1, 8), (5, 5, 2, 1, 8), (31, 63, 3, 1, 8),
+    (100, 256, 3, 1, 8), (100, 256, 5, 1, 8),  # interior tiles: TMA staging with 1 and 3 S_1 planes
 ])
 def test_rd_forward_odd_shapes(H, W, L, res, taps):
     cfg = workload.CONFIGS["tiny"].replace(H=H, W=W, L=L, syn_widths=(L, 8, 3), syn_n_res=res, up_taps=taps)
