@@ -528,9 +528,7 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
     constexpr int NPAIR = (RH0 / 2) * RW0;
     // one item = a pair of rows (2 rp, 2 rp + 1) at column cc: its L dense
     // values (FFMA2 lane pairs), then after the MLP its 3 outputs per pixel
-    auto dense_of = [&](int item, uint64_t (&v)[L]) {
-      const int rp = item / RW0;  // compile-time divisor
-      const int cc = item - rp * RW0;
+    auto dense_of = [&](int rp, int cc, uint64_t (&v)[L]) {
       const int y0 = RY + 2 * rp, x = RX + cc;
       const bool has1 = (y0 + 1 < H);
       if constexpr (DENSE_IN) {
@@ -584,18 +582,15 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
         }
       }
     };
-    auto needed = [&](int item) {  // read by the convs (inside the image), not computed by the partner
-      const int rp = item / RW0, cc = item - (item / RW0) * RW0;
+    auto needed = [&](int rp, int cc) {  // read by the convs (inside the image), not computed by the partner
       const int y0 = RY + 2 * rp, x = RX + cc;
       if (CLU && rp == shared_rp) return false;
 #ifdef CCRD_SYN_EXP_NOHALO  // timing experiment only (wrong results): no MLP on the halo rows
       if (2 * rp < RE || 2 * rp >= RE + SYN_TH) return false;
 #endif
-      return item < NPAIR && !(x < 0 || x >= W || y0 + 1 < 0 || y0 >= H);
+      return !(x < 0 || x >= W || y0 + 1 < 0 || y0 >= H);
     };
-    auto store = [&](int item, const uint64_t (&v)[L], const uint64_t (&op)[3]) {
-      const int rp = item / RW0;
-      const int cc = item - rp * RW0;
+    auto store = [&](int rp, int cc, const uint64_t (&v)[L], const uint64_t (&op)[3]) {
       const int y0 = RY + 2 * rp, x = RX + cc;
       const bool has1 = (y0 + 1 < H);
       const bool inx = (x >= X0 && x < X0 + SYN_TW);
@@ -631,13 +626,22 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
       }
     };
     if constexpr (MLP == 0) {
+      // item = rp x RW0 + cc, advanced by SYN_THREADS without a division
+      int rp = (int)threadIdx.x / RW0, cc = (int)threadIdx.x - rp * RW0;
 #pragma unroll 1
       for (int item = threadIdx.x; item < NPAIR; item += SYN_THREADS) {
-        if (!needed(item)) continue;  // never read by the convs
-        uint64_t v[L], op[3];
-        dense_of(item, v);
-        mlp_pair<L, CH, R, K>(p, v, op);
-        store(item, v, op);
+        if (needed(rp, cc)) {  // else never read by the convs
+          uint64_t v[L], op[3];
+          dense_of(rp, cc, v);
+          mlp_pair<L, CH, R, K>(p, v, op);
+          store(rp, cc, v, op);
+        }
+        cc += SYN_THREADS % RW0;
+        rp += SYN_THREADS / RW0;
+        if (cc >= RW0) {
+          cc -= RW0;
+          rp++;
+        }
       }
     } else {
       // m-tile = 2 row pairs x 4 columns of the level-0 region: MMA row g
