@@ -937,11 +937,17 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
 #pragma unroll
             for (int c = 0; c < 3; c++) hout[c * HP + ctr] = fmaxf(o[c], 0.0f);
           } else {
-            const int64_t gi = (int64_t)(y - Ys) * W + x;
-            if (p.out_u8 != nullptr) {  // decoder output: clamp to [0,1], 8-bit, ties to even (reading N3)
+            if (p.out_u8 != nullptr || p.x_hat != nullptr) {  // optional outputs (uniform branch)
+              const int64_t gi = (int64_t)(y - Ys) * W + x;
+              if (p.out_u8 != nullptr) {  // decoder output: clamp to [0,1], 8-bit, ties to even (reading N3)
 #pragma unroll
-              for (int c = 0; c < 3; c++)
-                p.out_u8[gi * 3 + c] = (uint8_t)__float2uint_rn(255.0f * fminf(fmaxf(o[c], 0.0f), 1.0f));
+                for (int c = 0; c < 3; c++)
+                  p.out_u8[gi * 3 + c] = (uint8_t)__float2uint_rn(255.0f * fminf(fmaxf(o[c], 0.0f), 1.0f));
+              }
+              if (p.x_hat != nullptr) {
+#pragma unroll
+                for (int c = 0; c < 3; c++) p.x_hat[c * Pimg + gi] = o[c];
+              }
             }
             // 8-bit: min(v, late) == v (v <= 255 <= late) ties each byte's
             // conversion to this row's result, so the scheduler cannot hoist
@@ -949,7 +955,6 @@ __global__ void __launch_bounds__(SYN_THREADS, SYN_CTAS_PER_SM)
             const uint32_t late = __float_as_uint(o[0]) | 255u;
 #pragma unroll
             for (int c = 0; c < 3; c++) {
-              if (p.x_hat != nullptr) p.x_hat[c * Pimg + gi] = o[c];
               if ((IMG8 ? p.image8 != nullptr : p.image != nullptr)) {
                 float xv;
                 if constexpr (IMG8)
