@@ -655,10 +655,13 @@ __global__ void __maxnreg__(CCRD_TCP_MAXREG)
   };
   // current tile (the one whose window is staged)
   int c_l = 0, c_i0 = 0, c_j0 = 0, c_it = -1;
+  int c_w = 0, c_oh = 0;  // the tile's grid width and owned-row end (per tile, not per block)
   auto stage = [&](int it) {  // stage the window of this warpgroup's it-th tile
     const int tile = first + it * stride;
     locate(tile, c_l, c_i0, c_j0);
     c_it = it;
+    c_w = p.g.lv.w[c_l];
+    c_oh = p.g.own_hi[c_l];
     const int w = p.g.lv.w[c_l], rlo = p.g.lv.lo[c_l], rhi = p.g.lv.hi[c_l];
     bool big = false;
     if constexpr (TMA) {
@@ -709,9 +712,9 @@ __global__ void __maxnreg__(CCRD_TCP_MAXREG)
       tmem_st_cols<C>(tl + cX[s], row);
       tmem_st_cols<8>(tl + cX[s] + C, tail);
     }
-    const int i = c_i0 + ry, j = c_j0 + cx, w = p.g.lv.w[c_l];
-    valid[s] = i < p.g.own_hi[c_l] && j < w;
-    if (p.bits != nullptr) qidx[s] = p.g.lv.off[c_l] + (int64_t)(i - p.g.lv.lo[c_l]) * w + j;  // debug outputs only
+    const int i = c_i0 + ry, j = c_j0 + cx;
+    valid[s] = i < c_oh && j < c_w;
+    if (p.bits != nullptr) qidx[s] = p.g.lv.off[c_l] + (int64_t)(i - p.g.lv.lo[c_l]) * c_w + j;  // debug outputs only
     tmem_wait_st();
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncwarp();
@@ -818,6 +821,8 @@ __global__ void __maxnreg__(CCRD_TCP_MAXREG)
 #pragma unroll 1
     for (int it = 0; it < my_tiles; it++) {
       locate(first + it * stride, c_l, c_i0, c_j0);
+      c_w = p.g.lv.w[c_l];
+      c_oh = p.g.own_hi[c_l];
       const bool big = stage_window_ldg<G::WIN>(p.lat, p.g, c_l, c_i0, c_j0, win, tw);
       if (wg_sync_or(g, big)) {
 #pragma unroll 1
