@@ -8,26 +8,28 @@
 namespace ccrd {
 
 // -log2 of the Laplace(mu, b) mass of the bin [y - 1/2, y + 1/2], floored at
-// p_floor (readings #1-#3).  With a = |y - mu| and
-// ib = 1/b:
-//   a <  1/2 : P = 1 - (exp(-(1/2 - a) ib) + exp(-(1/2 + a) ib)) / 2
-//   a >= 1/2 : -log2 P = 1 + (a - 1/2) ib log2(e) - log2(1 - exp(-ib))
-// (the second form is log-domain, so far tails do not underflow).
-// All exponentials / logarithms are single MUFU ops (ex2 / lg2): the worst
-// case, 1 - exp(-ib) at b = 256, cancels to ~1e-4 bits per latent, inside the
-// 1e-3-bit per-latent parity tolerance.
+// p_floor (readings #1-#3).  With a = |y - mu|,
+// ib = 1/b, t1 = exp(-|a - 1/2| ib) and t2 = exp(-(min(a, 1/2) + 1/2) ib):
+//   a <  1/2 : P = 1 - (t1 + t2) / 2            (t1, t2 = the two tail masses x 2)
+//   a >= 1/2 : P = t1 (1 - t2) / 2              (t2 = exp(-ib): the bin's far edge)
+// -- three MUFU ex2 and one lg2.  The far tails need no log-domain form: a P
+// below p_floor is floored, and t1 flushes to zero only below 2^-126 (then P
+// is floored too; a subnormal p_floor -- validated only as (0, 1) -- is
+// reached there as bits_cap).
+// The worst case, 1 - exp(-ib) at b = 256, cancels to ~1e-4 bits per latent,
+// inside the 1e-3-bit per-latent parity tolerance.
 __device__ __forceinline__ float laplace_bits(float y, float mu, float s, const ArmGeom& g) {
   constexpr float LOG2E = 1.4426950408889634f;
   s = fminf(fmaxf(s, g.lsmin), g.lsmax);
   const float ibl = exp2f_approx(-s * LOG2E) * LOG2E;  // log2(e) / b
   const float a = fabsf(y - mu);
   const float am = fminf(a, 0.5f);
-  const float e1 = exp2f_approx((am - 0.5f) * ibl);
-  const float e2 = exp2f_approx(-(am + 0.5f) * ibl);
-  const float p_in = 1.0f - 0.5f * (e1 + e2);
-  const float bits_in = -log2f_approx(fmaxf(p_in, g.p_floor));
-  const float bits_out = fmaf(a - 0.5f, ibl, 1.0f) - log2f_approx(1.0f - exp2f_approx(-ibl));
-  return fminf(a < 0.5f ? bits_in : bits_out, g.bits_cap);
+  const float t1 = exp2f_approx(-fabsf(a - 0.5f) * ibl);
+  const float t2 = exp2f_approx(-(am + 0.5f) * ibl);
+  const float p_in = 1.0f - 0.5f * (t1 + t2);
+  const float p_out = 0.5f * t1 * (1.0f - t2);
+  const float pr = a < 0.5f ? p_in : p_out;
+  return fminf(-log2f_approx(fmaxf(pr, g.p_floor)), g.bits_cap);
 }
 
 // One dense layer NIN -> 2*NO2 for NLAT latents with FFMA2 (two output neurons
