@@ -857,7 +857,7 @@ def main():
     ap.add_argument("--config", default="batched2k", choices=list(workload.CONFIGS))
     ap.add_argument("--images", type=int, default=0, help="images per GPU (default: the config's)")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--profile-steps", type=int, default=3, help="serial pass for per-kernel timing")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-xhat", action="store_true", help="e2e also reads x_hat back (fp32, 12 B/px)")
