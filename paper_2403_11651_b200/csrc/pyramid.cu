@@ -39,13 +39,25 @@ __global__ void __launch_bounds__(PYR_THREADS)
   const float* Sn = im.S + p.s_off[j + 1];  // S_{j+1}, nch - 1 channels
   const int16_t* lat = im.lat + p.lv.off[j + 1];
 
-  // source windows of every channel, replicate-extended (clamped) ------------
+  // source windows of every channel, replicate-extended (clamped): a thread
+  // owns one window column (its clamped source column computed once) and
+  // walks rows; grid j+1 (int16) first, then the S_{j+1} channels (fp32) ----
+  {
+    constexpr int RPI = PYR_THREADS / SC;  // rows per pass
+    const int cc = threadIdx.x % SC, rsub = threadIdx.x / SC;
+    if (rsub < RPI) {
+      const int gc = clampi(c0 + cc, 0, ws - 1);
 #pragma unroll 4
-  for (int it = threadIdx.x; it < nch * SR * SC; it += PYR_THREADS) {
-    const int k = it / (SR * SC), rem = it - k * (SR * SC);
-    const int rr = rem / SC, cc = rem - rr * SC;
-    const int64_t gi = (int64_t)(clampi(r0 + rr, los, his - 1) - los) * ws + clampi(c0 + cc, 0, ws - 1);
-    sw[it] = (k == 0) ? (float)__ldg(lat + gi) : __ldg(Sn + (int64_t)(k - 1) * ns * ws + gi);
+      for (int rr = rsub; rr < SR; rr += RPI)
+        sw[rr * SC + cc] = (float)__ldg(lat + (int64_t)(clampi(r0 + rr, los, his - 1) - los) * ws + gc);
+      const int64_t plane = (int64_t)ns * ws;
+#pragma unroll 4
+      for (int row = rsub; row < (nch - 1) * SR; row += RPI) {  // row = (k - 1) * SR + rr
+        const int k1 = row / SR, rr = row - k1 * SR;
+        sw[(SR + row) * SC + cc] =
+            __ldg(Sn + k1 * plane + (int64_t)(clampi(r0 + rr, los, his - 1) - los) * ws + gc);
+      }
+    }
   }
   __syncthreads();
   // horizontal: column pairs (2q, 2q+1) share sources q - K/4 .. q + K/4; a
