@@ -95,7 +95,9 @@ __global__ void __launch_bounds__(PYR_THREADS)
 #pragma unroll
     for (int u = 0; u < K / 2 + 2; u++) s[u] = src[u * PYR_TW];
     const int x = X0 + cc;
-    float* dst = Sj + (int64_t)k * nj * wj + x;
+    const int yb = Y0 + 4 * rq - loj;  // buffer row of the first of the 4 outputs
+    float* dst = Sj + (int64_t)k * nj * wj + (int64_t)yb * wj + x;
+    float o[4];
 #pragma unroll
     for (int pr = 0; pr < 2; pr++) {
       float a0 = 0.0f, a1 = 0.0f;
@@ -104,11 +106,13 @@ __global__ void __launch_bounds__(PYR_THREADS)
         a0 = fmaf(im.k[2 * t + 1], s[pr + K / 2 - 1 - t], a0);
         a1 = fmaf(im.k[2 * t], s[pr + K / 2 - t], a1);
       }
-      const int y = Y0 + 4 * rq + 2 * pr;
-      if (x < wj) {
-        if (y >= loj && y < hij) dst[(int64_t)(y - loj) * wj] = a0;
-        if (y + 1 >= loj && y + 1 < hij) dst[(int64_t)(y + 1 - loj) * wj] = a1;
-      }
+      o[2 * pr] = a0;
+      o[2 * pr + 1] = a1;
+    }
+    if (x < wj) {
+#pragma unroll
+      for (int r = 0; r < 4; r++)
+        if ((unsigned)(yb + r) < (unsigned)nj) dst[r * wj] = o[r];  // rows [lo_j, hi_j) only
     }
   }
 }
