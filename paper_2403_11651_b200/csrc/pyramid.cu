@@ -84,35 +84,49 @@ __global__ void __launch_bounds__(PYR_THREADS)
     *reinterpret_cast<float4*>(tmp + row * PYR_TW + 4 * cq) = make_float4(a[0], a[1], a[2], a[3]);
   }
   __syncthreads();
-  // vertical: row pairs, stored (cropped) to S_j[k]; a thread takes two
-  // adjacent row pairs of a column (6 loads feed 4 outputs) ------------------
-#pragma unroll 2
-  for (int it = threadIdx.x; it < nch * (PYR_TH / 4) * PYR_TW; it += PYR_THREADS) {
-    const int kr = it / PYR_TW, cc = it - kr * PYR_TW;
-    const int k = kr / (PYR_TH / 4), rq = kr - k * (PYR_TH / 4);
-    const float* src = tmp + (k * SR + 2 * rq) * PYR_TW + cc;
-    float s[K / 2 + 2];
+  // vertical: row pairs, stored (cropped) to S_j[k]; a thread takes four
+  // adjacent columns of one row pair: 16-byte shared loads, FFMA2 over column
+  // pairs (each output keeps its FMA order), 16-byte stores where the level's
+  // rows are 16-byte aligned ---------------------------------------------------
+  const bool vec = (wj & 3) == 0 && (reinterpret_cast<uintptr_t>(Sj) & 15) == 0;
+#pragma unroll 1
+  for (int it = threadIdx.x; it < nch * (PYR_TH / 2) * (PYR_TW / 4); it += PYR_THREADS) {
+    const int kr = it / (PYR_TW / 4), cq = it - kr * (PYR_TW / 4);
+    const int k = kr / (PYR_TH / 2), rp = kr - k * (PYR_TH / 2);
+    const float* src = tmp + (k * SR + rp) * PYR_TW + 4 * cq;
+    uint64_t s01[K / 2 + 1], s23[K / 2 + 1];  // source row u, columns (0, 1) and (2, 3)
 #pragma unroll
-    for (int u = 0; u < K / 2 + 2; u++) s[u] = src[u * PYR_TW];
-    const int x = X0 + cc;
-    const int yb = Y0 + 4 * rq - loj;  // buffer row of the first of the 4 outputs
-    float* dst = Sj + (int64_t)k * nj * wj + (int64_t)yb * wj + x;
-    float o[4];
-#pragma unroll
-    for (int pr = 0; pr < 2; pr++) {
-      float a0 = 0.0f, a1 = 0.0f;
-#pragma unroll
-      for (int t = 0; t < K / 2; t++) {
-        a0 = fmaf(im.k[2 * t + 1], s[pr + K / 2 - 1 - t], a0);
-        a1 = fmaf(im.k[2 * t], s[pr + K / 2 - t], a1);
-      }
-      o[2 * pr] = a0;
-      o[2 * pr + 1] = a1;
+    for (int u = 0; u <= K / 2; u++) {
+      const float4 f = *reinterpret_cast<const float4*>(src + u * PYR_TW);
+      s01[u] = f2pack(f.x, f.y);
+      s23[u] = f2pack(f.z, f.w);
     }
-    if (x < wj) {
+    uint64_t e01 = 0ull, e23 = 0ull, d01 = 0ull, d23 = 0ull;  // even / odd output row
 #pragma unroll
-      for (int r = 0; r < 4; r++)
-        if ((unsigned)(yb + r) < (unsigned)nj) dst[r * wj] = o[r];  // rows [lo_j, hi_j) only
+    for (int t = 0; t < K / 2; t++) {
+      const uint64_t k1 = f2pack(im.k[2 * t + 1], im.k[2 * t + 1]), k0 = f2pack(im.k[2 * t], im.k[2 * t]);
+      e01 = ffma2(k1, s01[K / 2 - 1 - t], e01);
+      e23 = ffma2(k1, s23[K / 2 - 1 - t], e23);
+      d01 = ffma2(k0, s01[K / 2 - t], d01);
+      d23 = ffma2(k0, s23[K / 2 - t], d23);
+    }
+    const int x = X0 + 4 * cq;
+    const int yb = Y0 + 2 * rp - loj;  // buffer row of the even output
+    float* dst = Sj + (int64_t)k * nj * wj + (int64_t)yb * wj + x;
+    const float2 e0 = f2unpack(e01), e1 = f2unpack(e23), o0 = f2unpack(d01), o1 = f2unpack(d23);
+    const float ev[4] = {e0.x, e0.y, e1.x, e1.y}, od[4] = {o0.x, o0.y, o1.x, o1.y};
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+      if ((unsigned)(yb + r) >= (unsigned)nj) continue;  // rows [lo_j, hi_j) only
+      const float* v = r ? od : ev;
+      float* d = dst + r * wj;
+      if (vec && x + 3 < wj) {
+        *reinterpret_cast<float4*>(d) = make_float4(v[0], v[1], v[2], v[3]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; c++)
+          if (x + c < wj) d[c] = v[c];
+      }
     }
   }
 }
