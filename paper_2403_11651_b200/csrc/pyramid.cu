@@ -47,15 +47,29 @@ __global__ void __launch_bounds__(PYR_THREADS)
     const int cc = threadIdx.x % SC, rsub = threadIdx.x / SC;
     if (rsub < RPI) {
       const int gc = clampi(c0 + cc, 0, ws - 1);
-#pragma unroll 4
-      for (int rr = rsub; rr < SR; rr += RPI)
-        sw[rr * SC + cc] = (float)__ldg(lat + (int64_t)(clampi(r0 + rr, los, his - 1) - los) * ws + gc);
       const int64_t plane = (int64_t)ns * ws;
+      if (r0 >= los && r0 + SR <= his) {  // no row clamping: pointer walks
+        const int64_t step = (int64_t)RPI * ws, first = (int64_t)(r0 + rsub - los) * ws + gc;
+        const int16_t* lp = lat + first;
+#pragma unroll 3
+        for (int rr = rsub; rr < SR; rr += RPI, lp += step) sw[rr * SC + cc] = (float)__ldg(lp);
+#pragma unroll 1
+        for (int k1 = 0; k1 < nch - 1; k1++) {
+          const float* sp = Sn + k1 * plane + first;
+          float* d = sw + (SR + k1 * SR) * SC + cc;
+#pragma unroll 3
+          for (int rr = rsub; rr < SR; rr += RPI, sp += step) d[rr * SC] = __ldg(sp);
+        }
+      } else {
 #pragma unroll 4
-      for (int row = rsub; row < (nch - 1) * SR; row += RPI) {  // row = (k - 1) * SR + rr
-        const int k1 = row / SR, rr = row - k1 * SR;
-        sw[(SR + row) * SC + cc] =
-            __ldg(Sn + k1 * plane + (int64_t)(clampi(r0 + rr, los, his - 1) - los) * ws + gc);
+        for (int rr = rsub; rr < SR; rr += RPI)
+          sw[rr * SC + cc] = (float)__ldg(lat + (int64_t)(clampi(r0 + rr, los, his - 1) - los) * ws + gc);
+#pragma unroll 4
+        for (int row = rsub; row < (nch - 1) * SR; row += RPI) {  // row = (k - 1) * SR + rr
+          const int k1 = row / SR, rr = row - k1 * SR;
+          sw[(SR + row) * SC + cc] =
+              __ldg(Sn + k1 * plane + (int64_t)(clampi(r0 + rr, los, his - 1) - los) * ws + gc);
+        }
       }
     }
   }
