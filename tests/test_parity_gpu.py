@@ -399,3 +399,34 @@ def test_synth_tma_bit_identical_to_ldg(arm_path, name, H, W, u8):
         np.testing.assert_array_equal(u, w)
     if H * W <= 512 * 768:
         check_image(cfg, ims[0], b[0], xb[0])
+
+
+def test_synth_tma_bit_identical_random_shapes(arm_path):
+    """Seeded sweep of shapes for the TMA-staged synthesis: widths that are
+    multiples of 16 (the TMA path's alignment) and not, heights with every
+    residue of the 32-row tile, configs with 1 / 2 residual layers and L = 3..7;
+    x_hat and results bit-identical to the per-tile LDG kernel."""
+    if arm_path != "tc":
+        pytest.skip("one ARM path suffices: the comparison is between synthesis paths")
+    P = _P()
+    rng = np.random.default_rng(2403)
+    for trial in range(12):
+        name = ["ref", "low", "tiny"][trial % 3]
+        W = int(rng.integers(4, 40)) * 16 + (0 if trial % 4 else int(rng.integers(1, 15)))
+        H = int(rng.integers(70, 400))
+        L = {"ref": 7, "low": 7, "tiny": int(rng.integers(3, 5))}[name]
+        cfg = workload.CONFIGS[name].replace(H=H, W=W, L=L, syn_widths=(L,) + tuple(workload.CONFIGS[name].syn_widths[1:]))
+        ims = workload.make_batch(cfg, [trial])
+
+        def fwd():
+            bt = P.DeviceBatch(cfg, ims, with_xhat=True)
+            r = bt.forward()
+            torch.cuda.synchronize()
+            return r.cpu().numpy(), bt.xhat[0].cpu().numpy()
+
+        with P.synth_path(P.CC_SYN_FFMA2):
+            a, xa = fwd()
+        with P.synth_path(P.CC_SYN_TMA):
+            b, xb = fwd()
+        np.testing.assert_array_equal(a, b, err_msg=f"{name} {H}x{W} L={L}")
+        np.testing.assert_array_equal(xa, xb, err_msg=f"{name} {H}x{W} L={L}")
