@@ -632,24 +632,29 @@ static int forward_batch(const cc_model_desc& d, const cc_strip* win, const int1
       cudaStreamWaitEvent(side->s, side->fork, 0);
     }
     if (arm_wait) cudaStreamWaitEvent(side->s, arm_wait[n - 1], 0);  // every latent of the batch landed
-    if ((rc = pyr_many(d, win, imgs, n, side->s))) return rc;
-    for (int i = 0; i < n; i++) {
+    auto syn_i = [&](int i) -> int {
       char* sl = slices + per * (size_t)i;
       const float* s1 = slice_pyr(d, win, sl) + pg.s_off[1];
       if (syn_wait) cudaStreamWaitEvent(side->s, syn_wait[i], 0);  // image i landed
       // synthesis i > 0 directly follows synthesis i - 1 in the side stream
       LaunchCtlScope lc(pdl && i > 0 && !syn_wait, 0);
-      if ((rc = syn_one(d, win, lat[i], s1, up_w[i], syn_w[i], image[i], x_hat[i], nullptr, (double*)sl + n_arm,
-                        side->s)))
-        return rc;
-    }
-    cudaEventRecord(side->join, side->s);
-    if ((rc = arm_stage_all(d, win, lat, arm_w, slices, per, n, s))) return rc;
-    for (int i = 0; i < n; i++) {
+      return syn_one(d, win, lat[i], s1, up_w[i], syn_w[i], image[i], x_hat[i], nullptr, (double*)sl + n_arm,
+                     side->s);
+    };
+    auto arm_i = [&](int i) -> int {
       if (arm_wait) cudaStreamWaitEvent(s, arm_wait[i], 0);
       LaunchCtlScope lc(pdl && i > 0 && !arm_wait, ARM_LAUNCH_ONLY);
-      if ((rc = arm_one(d, win, lat[i], arm_w[i], (double*)(slices + per * (size_t)i), s))) return rc;
-    }
+      return arm_one(d, win, lat[i], arm_w[i], (double*)(slices + per * (size_t)i), s);
+    };
+    if ((rc = pyr_many(d, win, imgs, n, side->s))) return rc;
+    // both streams get work from the start: the ARM weights staged, then image
+    // i's ARM and synthesis launches enqueued together (enqueueing all the
+    // synthesis launches first left the ARM stream idle while the host
+    // enqueued them: 1.8634e10 vs 1.8668e10 px/s)
+    if ((rc = arm_stage_all(d, win, lat, arm_w, slices, per, n, s))) return rc;
+    for (int i = 0; i < n; i++)
+      if ((rc = arm_i(i)) || (rc = syn_i(i))) return rc;
+    cudaEventRecord(side->join, side->s);
     if (join) cudaStreamWaitEvent(s, side->join, 0);  // else the caller orders on the side stream
     return CC_OK;
   }
