@@ -273,6 +273,9 @@ def run_ours(args, rk):
                        f"{(macs.up_macs + macs.syn_macs) / (cfg.H * cfg.W):.2f} MAC (last upsampling step + synthesis)",
         "peak_source": fp32_src, "avg_launch_ms": syn_avg_s * 1e3, "launches": prof.syn_launches,
         "share": prof.syn_ms / serial_ms, "traffic": load_traffic("synth_kernel")}
+    for e in kern.values():  # DRAM bytes of the ncu capture / this run's launch duration (HBM is not binding)
+        if e.get("traffic"):
+            e["dram_gbs"] = e["traffic"] / (e["avg_launch_ms"] * 1e-3) / 1e9
     dom = max(kern, key=lambda k: kern[k]["share"])
     roofline = {"kernel": dom, "timing": timing}
     roofline.update({k: kern[dom][k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic", "algorithmic",
